@@ -1,0 +1,1071 @@
+// libotm host runtime: context, level hierarchy, batched mixed-precision MG-PCG,
+// OC multiplier search, design loop, and the C ABI declared in include/otm.h.
+//
+// Solve strategy: fp64 defect correction around an fp32
+// multigrid-preconditioned CG.  The outer loop evaluates r = f - K T with T, K
+// and f in fp64 (the reference's discrete system, solver.py:398-401) and stops on
+// the reference's criterion ||r|| / ||f|| <= tol; the inner loop solves K d = r in
+// fp32 with PCG whose preconditioner is one V-cycle (damped-Jacobi smoothing,
+// full-weighting restriction, trilinear prolongation, dense pinned coarse solve,
+// child-mean coarse factors as in solver.py:257-267).  One inner iteration is a
+// captured CUDA graph; the host reads 6 scalars per iteration.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/otm.h"
+#include "otm_internal.h"
+
+using namespace otm;
+
+#define OTM_VERSION "0.1.0-b200"
+
+namespace {
+
+struct LevelBuf {
+    Geo g;
+    double scale[3];
+    int cf[3];            // axes coarsened from the previous (finer) level
+    LevelTemplate lt;
+    float* kap = nullptr;
+    float* dinv = nullptr;
+    float* f = nullptr;   // level 0: aliases the inner residual r
+    float* z = nullptr;   // Jacobi-from-zero iterate
+    float* res = nullptr; // residual, then the level's final V-cycle output
+};
+
+enum ProfClass { kProfL0Stencil = 0, kProfVcycle = 1, kProfRes64 = 2, kProfTensor = 3, kProfFilter = 4, kProfOC = 5,
+                 kProfClasses = 6 };
+
+struct ProfSlot {
+    cudaEvent_t a = nullptr, b = nullptr;
+    int cls = 0;
+    double bytes = 0.0;
+};
+
+}  // namespace
+
+struct otm_ctx {
+    otm_params P;
+    Geo g0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::vector<LevelBuf> L;
+    FilterSetup fs{};
+    SimpParams sp{};
+    double* kap64 = nullptr;
+    double* T64 = nullptr;
+    double* rho_f = nullptr;   // last filtered density used by otm_build (for sensitivities)
+    double* sensf = nullptr;   // design-loop scratch: sensitivity wrt rho_f, then wrt rho
+    double* sens = nullptr;
+    float *r = nullptr, *p = nullptr, *q = nullptr, *d = nullptr;
+    float* G = nullptr;
+    double* gj = nullptr;
+    int nc = 0;
+    Red red{};
+    PcgScalars* sc = nullptr;
+    double* scal = nullptr;      // generic device scalars (128)
+    double* h = nullptr;         // pinned host mirror (256)
+    int* changed = nullptr;      // device flag
+    bool built = false;
+    bool warm = false;
+    bool have_T = false;
+    std::string err;
+    size_t bytes = 0;
+    long long launches = 0;
+    // inner-iteration graphs (plain, profiled)
+    cudaGraphExec_t gexec = nullptr;
+    cudaGraphExec_t gexec_prof = nullptr;
+    int launches_per_inner = 0;
+    // profiling
+    bool prof = false;
+    std::vector<ProfSlot> slots;          // event pairs recorded inside the profiled graph
+    double prof_ms[kProfClasses] = {0};
+    long long prof_n[kProfClasses] = {0};
+    double prof_bytes[kProfClasses] = {0};
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;   // ad-hoc single-kernel timing
+};
+
+namespace {
+
+int fail(otm_ctx* c, int code, const std::string& msg) {
+    if (c) c->err = msg;
+    return code;
+}
+
+#define CK(call)                                                                            \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return fail(ctx, OTM_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define CKL()                                                                               \
+    do {                                                                                    \
+        cudaError_t e_ = cudaGetLastError();                                                \
+        if (e_ != cudaSuccess) return fail(ctx, OTM_ECUDA, std::string("launch: ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <typename T>
+cudaError_t dalloc(otm_ctx* ctx, T** p, size_t count) {
+    ctx->bytes += count * sizeof(T);
+    return cudaMalloc((void**)p, count * sizeof(T) + 16);
+}
+
+// trilinear template of a level: K = sum_ax scale_ax * (stiffness (x) mass (x) mass)
+// (solver.py:43-54); depends only on the corner XOR pattern.
+void level_template(const double scale[3], LevelTemplate& lt) {
+    const double st[2] = {1.0, -1.0};
+    const double ms[2] = {1.0 / 3.0, 1.0 / 6.0};
+    for (int dlt = 0; dlt < 8; ++dlt) {
+        double v = 0.0;
+        for (int ax = 0; ax < 3; ++ax) {
+            double term = scale[ax];
+            for (int q = 0; q < 3; ++q) {
+                const int bit = (dlt >> q) & 1;
+                term *= (q == ax) ? st[bit] : ms[bit];
+            }
+            v += term;
+        }
+        lt.kt[dlt] = v;
+    }
+    lt.equal = (scale[0] == scale[1] && scale[1] == scale[2]) ? 1 : 0;
+    lt.s12 = scale[0] / 12.0;
+    for (int a = 0; a < 8; ++a)
+        for (int i = 0; i < 3; ++i) {
+            double s = 0.0;
+            for (int b = 0; b < 8; ++b) s += lt.kt[a ^ b] * (double)((b >> i) & 1);
+            lt.f0[a * 3 + i] = s;
+        }
+}
+
+// cone taps (field.py:60-93)
+int setup_filter(otm_ctx* ctx, double radius) {
+    if (!(radius >= 1.0)) return fail(ctx, OTM_EINVAL, "filter radius must be >= 1");
+    const int reach = (int)std::ceil(radius) - 1;
+    std::vector<int> offs;
+    std::vector<double> w;
+    double tot = 0.0;
+    for (int dx = -reach; dx <= reach; ++dx)
+        for (int dy = -reach; dy <= reach; ++dy)
+            for (int dz = -reach; dz <= reach; ++dz) {
+                const double wt = std::max(0.0, radius - std::sqrt((double)(dx * dx + dy * dy + dz * dz)));
+                if (wt > 0.0) {
+                    offs.push_back(dx); offs.push_back(dy); offs.push_back(dz);
+                    w.push_back(wt);
+                    tot += wt;
+                }
+            }
+    for (auto& x : w) x /= tot;
+    FilterSetup& fs = ctx->fs;
+    fs.ntaps = (int)w.size();
+    fs.window = reach <= 1 ? 1 : 0;
+    for (int i = 0; i < 27; ++i) fs.w27[i] = 0.0;
+    if (fs.window) {
+        for (int i = 0; i < fs.ntaps; ++i) {
+            const int slot = (offs[3 * i] + 1) * 9 + (offs[3 * i + 1] + 1) * 3 + (offs[3 * i + 2] + 1);
+            fs.w27[slot] = w[i];
+        }
+    } else {
+        CK(dalloc(ctx, &fs.offs_dev, offs.size()));
+        CK(dalloc(ctx, &fs.wts_dev, w.size()));
+        CK(cudaMemcpy(fs.offs_dev, offs.data(), offs.size() * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(fs.wts_dev, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    return OTM_OK;
+}
+
+size_t max_blocks(const otm_ctx* ctx) {
+    size_t mb = 4096;
+    for (const auto& l : ctx->L) {
+        int xb;
+        const int ch = stencil_chunks(l.g, &xb);
+        mb = std::max(mb, (size_t)((l.g.pl + 127) / 128) * (size_t)ch);
+    }
+    return mb;
+}
+
+void prof_record(otm_ctx* ctx, int cls, double bytes, bool begin, int& slot_idx) {
+    // event pairs recorded while capturing the profiled graph
+    if (begin) {
+        ProfSlot s;
+        cudaEventCreate(&s.a);
+        cudaEventCreate(&s.b);
+        s.cls = cls;
+        s.bytes = bytes;
+        cudaEventRecordWithFlags(s.a, ctx->stream, cudaEventRecordExternal);
+        ctx->slots.push_back(s);
+        slot_idx = (int)ctx->slots.size() - 1;
+    } else {
+        cudaEventRecordWithFlags(ctx->slots[slot_idx].b, ctx->stream, cudaEventRecordExternal);
+    }
+}
+
+// Stream work of one inner PCG iteration (captured into a graph).
+int enqueue_inner(otm_ctx* ctx, bool prof) {
+    cudaStream_t s = ctx->stream;
+    const int nl = (int)ctx->L.size();
+    const float om = (float)ctx->P.jacobi_omega;
+    const double n0 = (double)ctx->g0.n;
+    int sl_v = -1, sl = -1;
+    int launches = 0;
+    if (prof) prof_record(ctx, kProfVcycle, 0.0, true, sl_v);
+    double vbytes = 0.0;
+    for (int l = 0; l + 1 < nl; ++l) {
+        LevelBuf& A = ctx->L[l];
+        LevelBuf& B = ctx->L[l + 1];
+        const double bsm = 44.0 * (double)A.g.n;
+        if (prof && l == 0) prof_record(ctx, kProfL0Stencil, bsm, true, sl);
+        launch_smooth_res(s, A.g, A.lt, A.kap, A.f, A.dinv, om, A.z, A.res);
+        if (prof && l == 0) prof_record(ctx, kProfL0Stencil, 0, false, sl);
+        launch_restrict(s, A.g, B.g, B.cf, A.res, B.f);
+        vbytes += bsm + 12.0 * A.g.n + 12.0 * B.g.n;
+        launches += 2;
+    }
+    {
+        LevelBuf& C = ctx->L[nl - 1];
+        launch_coarse_solve(s, (int)C.g.n, ctx->G, C.f, C.res);
+        launches += 1;
+    }
+    for (int l = nl - 2; l >= 0; --l) {
+        LevelBuf& A = ctx->L[l];
+        LevelBuf& B = ctx->L[l + 1];
+        launch_prolong(s, A.g, B.g, B.cf, B.res, A.z);
+        const double bj = 44.0 * (double)A.g.n;
+        if (prof && l == 0) prof_record(ctx, kProfL0Stencil, bj, true, sl);
+        launch_jacobi(s, A.g, A.lt, A.kap, A.z, A.f, A.dinv, om, A.res, l == 0, ctx->red, ctx->sc);
+        if (prof && l == 0) prof_record(ctx, kProfL0Stencil, 0, false, sl);
+        vbytes += 12.0 * B.g.n + 24.0 * A.g.n + bj;
+        launches += 2;
+    }
+    if (nl == 1) {
+        // single-level hierarchy: the coarse solve is the whole preconditioner; still need r.z
+        LevelBuf& A = ctx->L[0];
+        launch_jacobi(s, A.g, A.lt, A.kap, A.res, A.f, A.dinv, 0.0f, A.z, true, ctx->red, ctx->sc);
+        launches += 1;
+    }
+    if (prof) {
+        prof_record(ctx, kProfVcycle, 0, false, sl_v);
+        ctx->slots[sl_v].bytes = vbytes;
+    }
+    float* z0 = nl == 1 ? ctx->L[0].z : ctx->L[0].res;
+    launch_pupd(s, ctx->g0.n, z0, ctx->p, ctx->sc);
+    if (prof) prof_record(ctx, kProfL0Stencil, 28.0 * n0, true, sl);
+    launch_spmv(s, ctx->g0, ctx->L[0].lt, ctx->L[0].kap, ctx->p, ctx->q, ctx->red, ctx->sc);
+    if (prof) prof_record(ctx, kProfL0Stencil, 0, false, sl);
+    launch_upd(s, ctx->g0.n, ctx->d, ctx->r, ctx->p, ctx->q, ctx->red, ctx->sc);
+    launches += 3;
+    cudaMemcpyAsync(ctx->h, ctx->sc->flags, 8 * sizeof(double), cudaMemcpyDeviceToHost, s);
+    ctx->launches_per_inner = launches;
+    return OTM_OK;
+}
+
+int capture_inner(otm_ctx* ctx, bool prof) {
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    enqueue_inner(ctx, prof);
+    CK(cudaStreamEndCapture(ctx->stream, &graph));
+    cudaGraphExec_t ex;
+    CK(cudaGraphInstantiate(&ex, graph, 0));
+    cudaGraphDestroy(graph);
+    if (prof) ctx->gexec_prof = ex; else ctx->gexec = ex;
+    return OTM_OK;
+}
+
+int sync_scalars(otm_ctx* ctx, const double* dev, int count) {
+    CK(cudaMemcpyAsync(ctx->h, dev, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return OTM_OK;
+}
+
+void prof_harvest(otm_ctx* ctx) {
+    for (auto& s : ctx->slots) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, s.a, s.b) == cudaSuccess) {
+            ctx->prof_ms[s.cls] += ms;
+            ctx->prof_n[s.cls] += 1;
+            ctx->prof_bytes[s.cls] += s.bytes;
+        }
+    }
+}
+
+// time one eagerly launched region on the context stream (profiling mode)
+struct ProfScope {
+    otm_ctx* ctx;
+    int cls;
+    double bytes;
+    ProfScope(otm_ctx* c, int k, double b) : ctx(c), cls(k), bytes(b) {
+        if (ctx->prof) cudaEventRecord(ctx->ev_a, ctx->stream);
+    }
+    ~ProfScope() {
+        if (!ctx->prof) return;
+        cudaEventRecord(ctx->ev_b, ctx->stream);
+        cudaEventSynchronize(ctx->ev_b);
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, ctx->ev_a, ctx->ev_b) == cudaSuccess) {
+            ctx->prof_ms[cls] += ms;
+            ctx->prof_n[cls] += 1;
+            ctx->prof_bytes[cls] += bytes;
+        }
+    }
+};
+
+int build_levels(otm_ctx* ctx) {
+    cudaStream_t s = ctx->stream;
+    const int nl = (int)ctx->L.size();
+    for (int l = 1; l < nl; ++l) {
+        launch_coarsen(s, ctx->L[l - 1].g, ctx->L[l].g, ctx->L[l].cf, ctx->L[l - 1].kap, ctx->L[l].kap);
+        ctx->launches++;
+    }
+    for (int l = 0; l < nl; ++l) {
+        launch_dinv(s, ctx->L[l].g, ctx->L[l].kap, (float)ctx->L[l].lt.kt[0], ctx->L[l].dinv);
+        ctx->launches++;
+    }
+    CoarseTemplate ct;
+    for (int i = 0; i < 8; ++i) ct.kt[i] = ctx->L[nl - 1].lt.kt[i];
+    launch_coarse_setup(s, ctx->L[nl - 1].g, ctx->L[nl - 1].kap, ct, ctx->gj, ctx->G);
+    ctx->launches++;
+    CKL();
+    ctx->built = true;
+    return OTM_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* otm_version(void) { return OTM_VERSION; }
+
+void otm_default_params(otm_params* p) {
+    p->kappa0 = 1.0;
+    p->kappa_min = 1e-4;
+    p->penalty = 3.0;
+    p->filter_radius = 1.5;
+    p->coarse_target = 64;
+    p->direct_limit = 40000;
+    p->jacobi_omega = 0.8;
+    p->inner_reduction = 1e-4;
+    p->max_inner = 100;
+    p->device = 0;
+}
+
+void otm_default_oc_params(otm_oc_params* p) {
+    p->min_density = 0.001;
+    p->step_limit = 0.02;
+    p->damp = 0.5;
+    p->bisection_tol = 1e-5;
+}
+
+void otm_default_governor(otm_governor* g) {
+    g->vstar = 1.0;
+    g->df = 1.0;
+    g->gap = 0.0;
+    g->count = 0;
+    g->bound = 1e-4;
+    g->iter = 0;
+    g->g_prev = 1.0;
+    g->reduced = 0;
+}
+
+void otm_default_run_config(otm_run_config* c) {
+    for (int i = 0; i < 6; ++i) c->target[i] = NAN;
+    c->objective = 0;
+    c->model = 0;
+    c->volume_bound = NAN;
+    otm_default_oc_params(&c->oc);
+    c->max_iter = 500;
+    c->conv_threshold = 1e-4;
+    c->symmetry = 0;
+    c->solver_tol = 1e-6;
+    c->max_vcycles = 200;
+    c->governor_bound = 1e-4;
+}
+
+int otm_create(otm_ctx** out, int nx, int ny, int nz, const otm_params* pin) {
+    if (!out) return OTM_EINVAL;
+    *out = nullptr;
+    otm_ctx* ctx = new otm_ctx();
+    if (pin) ctx->P = *pin; else otm_default_params(&ctx->P);
+    const otm_params& P = ctx->P;
+    if (nx < 1 || ny < 1 || nz < 1) {
+        int rc = fail(ctx, OTM_EINVAL, "dims must be three positive integers");
+        *out = ctx;
+        return rc;
+    }
+    if (!(P.kappa0 > P.kappa_min && P.kappa_min > 0.0) || P.penalty < 1.0) {
+        *out = ctx;
+        return fail(ctx, OTM_EINVAL, "need kappa0 > kappa_min > 0 and penalty >= 1");
+    }
+    *out = ctx;
+    CK(cudaSetDevice(P.device));
+    ctx->sp = SimpParams{P.kappa0, P.kappa_min, P.penalty};
+    // level chain (solver.py:217-245)
+    std::vector<std::array<int, 3>> chain;
+    chain.push_back({nx, ny, nz});
+    while (true) {
+        auto cur = chain.back();
+        const long long prod = (long long)cur[0] * cur[1] * cur[2];
+        if (prod <= P.coarse_target) break;
+        bool odd = false;
+        for (int a = 0; a < 3; ++a)
+            if (cur[a] > 1 && cur[a] % 2) odd = true;
+        if (odd) break;
+        chain.push_back({cur[0] > 1 ? cur[0] / 2 : 1, cur[1] > 1 ? cur[1] / 2 : 1, cur[2] > 1 ? cur[2] / 2 : 1});
+    }
+    {
+        auto c = chain.back();
+        const long long prod = (long long)c[0] * c[1] * c[2];
+        if (prod > P.direct_limit) {
+            char buf[256];
+            snprintf(buf, sizeof buf, "dims (%d, %d, %d) cannot be coarsened below %d vertices (reached (%d, %d, %d))",
+                     nx, ny, nz, P.direct_limit, c[0], c[1], c[2]);
+            return fail(ctx, OTM_EINVAL, buf);
+        }
+        if (prod > 2048)
+            return fail(ctx, OTM_EINVAL, "coarsest level exceeds the on-device dense direct solve (2048 vertices)");
+    }
+    ctx->g0 = make_geo(nx, ny, nz);
+    double h[3] = {1, 1, 1}, norm = 1.0;
+    for (size_t li = 0; li < chain.size(); ++li) {
+        LevelBuf lb;
+        lb.g = make_geo(chain[li][0], chain[li][1], chain[li][2]);
+        const double vol = h[0] * h[1] * h[2];
+        for (int a = 0; a < 3; ++a) lb.scale[a] = norm * vol / (h[a] * h[a]);
+        for (int a = 0; a < 3; ++a) lb.cf[a] = li > 0 && chain[li][a] < chain[li - 1][a];
+        level_template(lb.scale, lb.lt);
+        ctx->L.push_back(lb);
+        if (li + 1 < chain.size())
+            for (int a = 0; a < 3; ++a)
+                if (chain[li + 1][a] < chain[li][a]) {
+                    h[a] *= 2.0;
+                    norm *= 0.5;
+                }
+    }
+    int rc = setup_filter(ctx, P.filter_radius);
+    if (rc) return rc;
+    const long long n = ctx->g0.n;
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+    CK(dalloc(ctx, &ctx->kap64, n));
+    CK(dalloc(ctx, &ctx->T64, 3 * n));
+    CK(dalloc(ctx, &ctx->rho_f, n));
+    CK(dalloc(ctx, &ctx->sensf, n));
+    CK(dalloc(ctx, &ctx->sens, n));
+    CK(dalloc(ctx, &ctx->r, 3 * n));
+    CK(dalloc(ctx, &ctx->p, 3 * n));
+    CK(dalloc(ctx, &ctx->q, 3 * n));
+    CK(dalloc(ctx, &ctx->d, 3 * n));
+    for (size_t l = 0; l < ctx->L.size(); ++l) {
+        LevelBuf& lb = ctx->L[l];
+        CK(dalloc(ctx, &lb.kap, lb.g.n));
+        CK(dalloc(ctx, &lb.dinv, lb.g.n));
+        if (l == 0) lb.f = ctx->r; else CK(dalloc(ctx, &lb.f, 3 * lb.g.n));
+        CK(dalloc(ctx, &lb.z, 3 * lb.g.n));
+        CK(dalloc(ctx, &lb.res, 3 * lb.g.n));
+    }
+    ctx->nc = (int)ctx->L.back().g.n;
+    CK(dalloc(ctx, &ctx->G, (size_t)ctx->nc * ctx->nc));
+    CK(dalloc(ctx, &ctx->gj, 2 * (size_t)ctx->nc * ctx->nc + 2));
+    const size_t mb = max_blocks(ctx);
+    CK(dalloc(ctx, &ctx->red.partials, mb * 32));
+    CK(dalloc(ctx, &ctx->red.counter, 4));
+    CK(cudaMemset(ctx->red.counter, 0, 4 * sizeof(unsigned)));
+    CK(dalloc(ctx, &ctx->sc, 1));
+    CK(cudaMemset(ctx->sc, 0, sizeof(PcgScalars)));
+    CK(dalloc(ctx, &ctx->scal, 128));
+    CK(cudaMemset(ctx->scal, 0, 128 * sizeof(double)));
+    CK(dalloc(ctx, &ctx->changed, 4));
+    CK(cudaMallocHost((void**)&ctx->h, 256 * sizeof(double)));
+    CK(cudaMemset(ctx->T64, 0, 3 * n * sizeof(double)));
+    CK(cudaMemset(ctx->p, 0, 3 * n * sizeof(float)));
+    CK(cudaEventCreate(&ctx->ev_a));
+    CK(cudaEventCreate(&ctx->ev_b));
+    CK(cudaDeviceSynchronize());
+    return OTM_OK;
+}
+
+int otm_destroy(otm_ctx* ctx) {
+    if (!ctx) return OTM_OK;
+    if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    if (ctx->gexec_prof) cudaGraphExecDestroy(ctx->gexec_prof);
+    for (auto& s : ctx->slots) { cudaEventDestroy(s.a); cudaEventDestroy(s.b); }
+    auto F = [](void* p) { if (p) cudaFree(p); };
+    F(ctx->kap64); F(ctx->T64); F(ctx->rho_f); F(ctx->sensf); F(ctx->sens); F(ctx->r); F(ctx->p); F(ctx->q); F(ctx->d);
+    for (size_t l = 0; l < ctx->L.size(); ++l) {
+        F(ctx->L[l].kap); F(ctx->L[l].dinv); F(ctx->L[l].z); F(ctx->L[l].res);
+        if (l > 0) F(ctx->L[l].f);
+    }
+    F(ctx->G); F(ctx->gj); F(ctx->red.partials); F(ctx->red.counter); F(ctx->sc); F(ctx->scal);
+    F(ctx->changed); F(ctx->fs.offs_dev); F(ctx->fs.wts_dev);
+    if (ctx->h) cudaFreeHost(ctx->h);
+    if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
+    if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return OTM_OK;
+}
+
+int otm_set_stream(otm_ctx* ctx, void* stream) {
+    if (!ctx) return OTM_EINVAL;
+    if (ctx->own_stream && ctx->stream) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaStreamDestroy(ctx->stream);
+    }
+    ctx->own_stream = false;
+    ctx->stream = (cudaStream_t)stream;
+    return OTM_OK;
+}
+
+const char* otm_last_error(const otm_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+int otm_num_levels(const otm_ctx* ctx) { return ctx ? (int)ctx->L.size() : 0; }
+size_t otm_device_bytes(const otm_ctx* ctx) { return ctx ? ctx->bytes : 0; }
+long long otm_launch_count(const otm_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int otm_level_info(const otm_ctx* ctx, int level, int dims[3], double axis_scale[3]) {
+    if (!ctx || level < 0 || level >= (int)ctx->L.size()) return OTM_EINVAL;
+    const LevelBuf& l = ctx->L[level];
+    dims[0] = l.g.nx; dims[1] = l.g.ny; dims[2] = l.g.nz;
+    for (int a = 0; a < 3; ++a) axis_scale[a] = l.scale[a];
+    return OTM_OK;
+}
+
+int otm_set_material(otm_ctx* ctx, double k0, double kmin, double p) {
+    if (!ctx) return OTM_EINVAL;
+    if (!(k0 > kmin && kmin > 0.0) || p < 1.0)
+        return fail(ctx, OTM_EINVAL, "need kappa0 > kappa_min > 0 and penalty >= 1");
+    ctx->sp = SimpParams{k0, kmin, p};
+    ctx->P.kappa0 = k0;
+    ctx->P.kappa_min = kmin;
+    ctx->P.penalty = p;
+    return OTM_OK;
+}
+
+int otm_filter(otm_ctx* ctx, const double* in, double* out, int adjoint) {
+    if (!ctx || !in || !out) return OTM_EINVAL;
+    ProfScope ps(ctx, kProfFilter, 16.0 * ctx->g0.n);
+    launch_filter(ctx->stream, ctx->g0, ctx->fs, adjoint, in, out, ctx->red);
+    ctx->launches++;
+    CKL();
+    return OTM_OK;
+}
+
+int otm_symmetrize(otm_ctx* ctx, double* a) {
+    if (!ctx || !a) return OTM_EINVAL;
+    launch_symmetrize(ctx->stream, ctx->g0, a);
+    ctx->launches++;
+    CKL();
+    return OTM_OK;
+}
+
+int otm_build(otm_ctx* ctx, const double* rho_f) {
+    if (!ctx || !rho_f) return OTM_EINVAL;
+    if (rho_f != ctx->rho_f)
+        CK(cudaMemcpyAsync(ctx->rho_f, rho_f, ctx->g0.n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    launch_simp(ctx->stream, ctx->g0.n, ctx->rho_f, ctx->kap64, ctx->L[0].kap, ctx->sp);
+    ctx->launches++;
+    return build_levels(ctx);
+}
+
+int otm_build_kappa(otm_ctx* ctx, const double* kap) {
+    if (!ctx || !kap) return OTM_EINVAL;
+    launch_set_kappa(ctx->stream, ctx->g0.n, kap, ctx->kap64, ctx->L[0].kap);
+    ctx->launches++;
+    return build_levels(ctx);
+}
+
+int otm_apply_K(otm_ctx* ctx, const double* T, double* out) {
+    if (!ctx || !T || !out) return OTM_EINVAL;
+    if (!ctx->built) return fail(ctx, OTM_ESTATE, "hierarchy not built; call build() first");
+    launch_apply64(ctx->stream, ctx->g0, ctx->L[0].lt, ctx->kap64, T, out, -1);
+    ctx->launches++;
+    CKL();
+    return OTM_OK;
+}
+
+int otm_macro_load(otm_ctx* ctx, int which, double* f) {
+    if (!ctx || !f) return OTM_EINVAL;
+    if (which < 0 || which > 2) return fail(ctx, OTM_EINVAL, "load case must be 0, 1 or 2");
+    if (!ctx->built) return fail(ctx, OTM_ESTATE, "hierarchy not built; call build() first");
+    launch_apply64(ctx->stream, ctx->g0, ctx->L[0].lt, ctx->kap64, nullptr, f, which);
+    ctx->launches++;
+    CKL();
+    return OTM_OK;
+}
+
+int otm_set_warm(otm_ctx* ctx, const double* T) {
+    if (!ctx) return OTM_EINVAL;
+    if (T) {
+        if (T != ctx->T64)
+            CK(cudaMemcpyAsync(ctx->T64, T, 3 * ctx->g0.n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        ctx->warm = true;
+        ctx->have_T = true;
+    } else {
+        ctx->warm = false;
+    }
+    return OTM_OK;
+}
+
+int otm_solve(otm_ctx* ctx, const double* fext, double tol, int max_cycles, int* cycles_out, double resid_out[3]) {
+    if (!ctx) return OTM_EINVAL;
+    if (!ctx->built) return fail(ctx, OTM_ESTATE, "hierarchy not built; call build() first");
+    if (max_cycles < 1) return fail(ctx, OTM_EINVAL, "max_vcycles must be >= 1");
+    cudaStream_t s = ctx->stream;
+    const long long n = ctx->g0.n;
+    if (!ctx->gexec) { int rc = capture_inner(ctx, false); if (rc) return rc; }
+    if (ctx->prof && !ctx->gexec_prof) { int rc = capture_inner(ctx, true); if (rc) return rc; }
+    double* fmean = ctx->scal + 16;
+    if (fext) { launch_sum3(s, n, fext, ctx->red, fmean); ctx->launches++; }
+    if (!ctx->warm) CK(cudaMemsetAsync(ctx->T64, 0, 3 * n * sizeof(double), s));
+    int cycles = 0;
+    double rel[3], fnorm[3], rnorm[3];
+    bool done[3];
+    auto residual = [&]() -> int {
+        {
+            ProfScope ps(ctx, kProfRes64, (24.0 + 8.0 + 12.0 + (fext ? 24.0 : 0.0)) * n);
+            launch_res64(s, ctx->g0, ctx->L[0].lt, ctx->kap64, ctx->T64, fext, fmean, ctx->r, ctx->red, ctx->scal);
+        }
+        ctx->launches++;
+        CKL();
+        int rc = sync_scalars(ctx, ctx->scal, 9);
+        if (rc) return rc;
+        for (int c = 0; c < 3; ++c) {
+            fnorm[c] = std::sqrt(ctx->h[3 + c]);
+            rnorm[c] = std::sqrt(ctx->h[c]);
+            rel[c] = fnorm[c] > 0.0 ? rnorm[c] / fnorm[c] : 0.0;
+            done[c] = fnorm[c] == 0.0 || rel[c] <= tol;
+        }
+        return OTM_OK;
+    };
+    int rc = residual();
+    if (rc) return rc;
+    bool zero_load[3];
+    for (int c = 0; c < 3; ++c) zero_load[c] = fnorm[c] == 0.0;
+    int status = OTM_OK;
+    while (!(done[0] && done[1] && done[2])) {
+        if (cycles >= max_cycles) { status = OTM_ENOCONV; break; }
+        // inner fp32 MG-PCG on K d = r
+        PcgScalars init;
+        std::memset(&init, 0, sizeof init);
+        for (int c = 0; c < 3; ++c) {
+            const double tgt = std::max(ctx->P.inner_reduction * rnorm[c], 0.5 * tol * fnorm[c]);
+            init.target2[c] = tgt * tgt;
+            init.active[c] = done[c] ? 0.0 : 1.0;
+        }
+        init.first = 1;
+        std::memcpy(ctx->h + 64, &init, sizeof init);
+        CK(cudaMemcpyAsync(ctx->sc, ctx->h + 64, sizeof init, cudaMemcpyHostToDevice, s));
+        CK(cudaMemsetAsync(ctx->d, 0, 3 * n * sizeof(float), s));
+        CK(cudaMemsetAsync(ctx->p, 0, 3 * n * sizeof(float), s));
+        int active_n = (int)!done[0] + (int)!done[1] + (int)!done[2];
+        for (int it = 0; it < ctx->P.max_inner; ++it) {
+            CK(cudaGraphLaunch(ctx->prof ? ctx->gexec_prof : ctx->gexec, s));
+            ctx->launches += ctx->launches_per_inner;
+            CK(cudaStreamSynchronize(s));
+            if (ctx->prof) prof_harvest(ctx);
+            cycles += active_n;
+            active_n = (int)(ctx->h[0] != 0.0) + (int)(ctx->h[1] != 0.0) + (int)(ctx->h[2] != 0.0);
+            if (active_n == 0 || cycles >= max_cycles) break;
+        }
+        launch_Tupd(s, 3 * n, ctx->T64, ctx->d);
+        ctx->launches++;
+        rc = residual();
+        if (rc) return rc;
+    }
+    // mean-free T (solver.py:398); zero loads short-circuit to T = 0 (solver.py:382-385)
+    launch_submean(s, n, ctx->T64, ctx->scal + 6);
+    ctx->launches++;
+    for (int c = 0; c < 3; ++c)
+        if (zero_load[c]) CK(cudaMemsetAsync(ctx->T64 + (size_t)c * n, 0, n * sizeof(double), s));
+    CKL();
+    ctx->have_T = true;
+    ctx->warm = true;
+    if (cycles_out) *cycles_out = cycles;
+    double worst = 0.0;
+    for (int c = 0; c < 3; ++c) {
+        if (resid_out) resid_out[c] = rel[c];
+        worst = std::max(worst, rel[c]);
+    }
+    if (status == OTM_ENOCONV) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "no convergence after %d V-cycles (residual %.3e)", cycles, worst);
+        return fail(ctx, OTM_ENOCONV, buf);
+    }
+    return OTM_OK;
+}
+
+int otm_get_T(otm_ctx* ctx, double* T) {
+    if (!ctx || !T) return OTM_EINVAL;
+    if (T != ctx->T64)
+        CK(cudaMemcpyAsync(T, ctx->T64, 3 * ctx->g0.n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    return OTM_OK;
+}
+
+int otm_tensor(otm_ctx* ctx, double kappa_out[6]) {
+    if (!ctx || !kappa_out) return OTM_EINVAL;
+    if (!ctx->have_T) return fail(ctx, OTM_ESTATE, "no solved fields; run solve first");
+    {
+        ProfScope ps(ctx, kProfTensor, 32.0 * ctx->g0.n);
+        launch_tensor(ctx->stream, ctx->g0, ctx->T64, ctx->kap64, ctx->red, ctx->scal + 32);
+    }
+    ctx->launches++;
+    CKL();
+    int rc = sync_scalars(ctx, ctx->scal + 32, 6);
+    if (rc) return rc;
+    for (int c = 0; c < 6; ++c) kappa_out[c] = ctx->h[c];
+    return OTM_OK;
+}
+
+int otm_pair_energy(otm_ctx* ctx, double* E) {
+    if (!ctx || !E) return OTM_EINVAL;
+    if (!ctx->have_T) return fail(ctx, OTM_ESTATE, "no solved fields; run solve first");
+    launch_pair_energy(ctx->stream, ctx->g0, ctx->T64, E);
+    ctx->launches++;
+    CKL();
+    return OTM_OK;
+}
+
+int otm_sensitivity(otm_ctx* ctx, const double dG[6], double* sens) {
+    if (!ctx || !dG || !sens) return OTM_EINVAL;
+    if (!ctx->have_T) return fail(ctx, OTM_ESTATE, "homogenization caches missing; run effective_tensor first");
+    Dg d;
+    for (int c = 0; c < 6; ++c) d.v[c] = dG[c];
+    {
+        ProfScope ps(ctx, kProfTensor, 40.0 * ctx->g0.n);
+        launch_sens(ctx->stream, ctx->g0, ctx->T64, ctx->rho_f, ctx->sp, d, sens);
+    }
+    ctx->launches++;
+    CKL();
+    return OTM_OK;
+}
+
+// objective.py:48-72
+int otm_objective(int kind, const double t[6], const double k[6], double* g_out, double dG[6]) {
+    double g = 0.0;
+    int any = 0;
+    for (int c = 0; c < 6; ++c) {
+        if (!std::isfinite(k[c])) return OTM_EINVAL;
+        if (!std::isnan(t[c])) any = 1;
+    }
+    if (!any) return OTM_EINVAL;
+    for (int c = 0; c < 6; ++c) {
+        const bool m = !std::isnan(t[c]);
+        if (kind == 0) {
+            const double d = m ? k[c] - t[c] : 0.0;
+            g += d * d;
+            dG[c] = 2.0 * d;
+        } else if (kind == 1) {
+            const double tt = m ? t[c] : 1.0;
+            const double d = m ? k[c] / tt - 1.0 : 0.0;
+            g += d * d;
+            dG[c] = m ? 2.0 * d / tt : 0.0;
+        } else {
+            const double d = m ? k[c] - t[c] : 0.0;
+            g += std::fabs(d);
+            dG[c] = (d > 0) - (d < 0);
+        }
+    }
+    *g_out = g;
+    return OTM_OK;
+}
+
+int otm_means(otm_ctx* ctx, const double* rho, double p, double out[2]) {
+    if (!ctx || !rho || !out) return OTM_EINVAL;
+    launch_means(ctx->stream, ctx->g0.n, rho, p, ctx->red, ctx->scal + 40);
+    ctx->launches++;
+    CKL();
+    int rc = sync_scalars(ctx, ctx->scal + 40, 2);
+    if (rc) return rc;
+    out[0] = ctx->h[0] / (double)ctx->g0.n;
+    out[1] = ctx->h[1] / (double)ctx->g0.n;
+    return OTM_OK;
+}
+
+// oc_update (optimize.py:114-160).  The reference's sequential multiplier search
+// (bracket l2 *= 4, then bisection of [1e-30, l2] with its two stopping rules) is
+// replayed exactly on the host; the device evaluates the candidate means of up to
+// 32 multipliers per pass: the next 31 bracket values, or the complete depth-5
+// subtree of bisection midpoints below the current interval.
+int otm_oc_update(otm_ctx* ctx, const double* rho, const double* sens, double V, const otm_oc_params* pp,
+                  double* rho_out, double* lam_out, int* active_out, int* changed_out) {
+    if (!ctx || !rho || !sens || !rho_out || !pp) return OTM_EINVAL;
+    if (!(pp->min_density >= 0.0 && pp->min_density < 1.0) || !(pp->step_limit > 0.0 && pp->step_limit <= 1.0) ||
+        !(pp->damp > 0.0 && pp->damp <= 1.0))
+        return fail(ctx, OTM_EINVAL, "invalid OC parameters");
+    cudaStream_t s = ctx->stream;
+    const long long n = ctx->g0.n;
+    OcArgs a;
+    a.step = pp->step_limit;
+    a.rmin = pp->min_density;
+    a.damp = pp->damp;
+    a.floor_ratio = std::pow(1e-10, pp->damp);
+    a.sqrt_damp = pp->damp == 0.5;
+    double* means = ctx->scal + 48;
+    ProfScope ps(ctx, kProfOC, 0.0);
+    auto lam_pow = [&](double lam) { return a.sqrt_damp ? 1.0 / std::sqrt(lam) : std::pow(lam, -a.damp); };
+    auto eval = [&](const std::vector<double>& lams) -> int {
+        LamSet ls;
+        for (int k = 0; k < kOcLam; ++k) ls.v[k] = k < (int)lams.size() ? (lams[k] == 0.0 ? 0.0 : lam_pow(lams[k])) : 0.0;
+        launch_oc_eval(s, n, rho, sens, a, (int)lams.size(), ls, ctx->red, means);
+        ctx->launches++;
+        if (ctx->prof) ctx->prof_bytes[kProfOC] += 16.0 * n;
+        CKL();
+        return sync_scalars(ctx, means, (int)lams.size());
+    };
+    double lam = 0.0;
+    bool active = true;
+    // pass 0: free step + first 31 bracket values
+    std::vector<double> lams;
+    lams.push_back(0.0);
+    double l2 = 1.0;
+    for (int i = 0; i < kOcLam - 1; ++i) { lams.push_back(l2); l2 *= 4.0; }
+    int rc = eval(lams);
+    if (rc) return rc;
+    if (ctx->h[0] <= V) {
+        active = false;
+        lam = 0.0;
+    } else {
+        // bracket (optimize.py:146-150)
+        std::vector<double> bm(ctx->h + 1, ctx->h + kOcLam);
+        std::vector<double> bl(lams.begin() + 1, lams.end());
+        l2 = 1.0;
+        int it = 0;
+        size_t pos = 0;
+        while (it < 200) {
+            if (pos == bl.size()) {
+                bl.clear();
+                double v = l2;
+                for (int i = 0; i < kOcLam && it + i < 200; ++i) { bl.push_back(v); v *= 4.0; }
+                rc = eval(bl);
+                if (rc) return rc;
+                bm.assign(ctx->h, ctx->h + bl.size());
+                pos = 0;
+            }
+            if (bm[pos] <= V) break;
+            l2 *= 4.0;
+            ++pos;
+            ++it;
+        }
+        // bisection (optimize.py:151-158) replayed over depth-5 subtrees
+        double l1 = 1e-30;
+        bool done = false;
+        while (!done) {
+            // BFS subtree of midpoints: node i covers (lo[i], hi[i]); child 2i+1 = (lo, mid), 2i+2 = (mid, hi)
+            const int nodes = kOcLam - 1;
+            std::vector<double> lo(nodes), hi(nodes), mid(nodes);
+            lo[0] = l1; hi[0] = l2;
+            for (int i = 0; i < nodes; ++i) {
+                mid[i] = 0.5 * (lo[i] + hi[i]);
+                if (2 * i + 2 < nodes) {
+                    lo[2 * i + 1] = lo[i]; hi[2 * i + 1] = mid[i];
+                    lo[2 * i + 2] = mid[i]; hi[2 * i + 2] = hi[i];
+                }
+            }
+            rc = eval(mid);
+            if (rc) return rc;
+            int node = 0;
+            while (true) {
+                if (!((l2 - l1) / (l1 + l2) > 1e-13)) { done = true; break; }
+                if (node >= nodes) break;   // next pass from (l1, l2)
+                const double m = 0.5 * (l1 + l2);
+                const double cur = ctx->h[node];
+                if (cur > V) { l1 = m; node = 2 * node + 2; }
+                else { l2 = m; node = 2 * node + 1; }
+                if (std::fabs(cur - V) <= pp->bisection_tol) { done = true; break; }
+            }
+        }
+        lam = 0.5 * (l1 + l2);
+    }
+    CK(cudaMemsetAsync(ctx->changed, 0, sizeof(int), s));
+    launch_oc_apply(s, n, rho, sens, a, lam, rho_out, ctx->changed);
+    ctx->launches++;
+    if (ctx->prof) ctx->prof_bytes[kProfOC] += 24.0 * n;
+    CKL();
+    int hchanged = 0;
+    CK(cudaMemcpyAsync(ctx->h + 128, ctx->changed, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::memcpy(&hchanged, ctx->h + 128, sizeof(int));
+    if (lam_out) *lam_out = lam;
+    if (active_out) *active_out = active ? 1 : 0;
+    if (changed_out) *changed_out = hchanged;
+    return OTM_OK;
+}
+
+// governor_update (optimize.py:57-86)
+double otm_governor_update(otm_governor* st, double g, double mean_rho, double mean_rho_p) {
+    if (g <= st->bound) {
+        st->gap = st->vstar - mean_rho_p;
+        st->vstar = st->vstar - st->gap * st->df;
+        st->df = 0.8 * st->df;
+        st->reduced = 1;
+    }
+    const bool little = std::fabs(st->g_prev - g) < std::max(0.1 * g, 1e-7);
+    const bool too_big = g > st->bound;
+    const bool near = mean_rho > st->vstar - 0.01;
+    if (little && too_big && near) st->count += 1;
+    else st->count = 0;
+    if (st->count >= 5) {
+        st->vstar = st->vstar + 0.3 * st->gap * st->df;
+        st->count = 0;
+    }
+    st->g_prev = g;
+    st->iter += 1;
+    return st->vstar;
+}
+
+void otm_run_init(otm_run_state* st, const otm_run_config* cfg) {
+    std::memset(st, 0, sizeof *st);
+    otm_default_governor(&st->gov);
+    st->gov.bound = cfg->governor_bound;
+}
+
+// One iteration of run_optimization (optimize.py:288-379), models "oc" and "fixed".
+int otm_run_step(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, double* rho, double* rho_f_out,
+                 double* sens_out, otm_iter_record* rec) {
+    if (!ctx || !cfg || !st || !rho || !rec) return OTM_EINVAL;
+    if (st->finished) return fail(ctx, OTM_ESTATE, "run already finished");
+    cudaStream_t s = ctx->stream;
+    const long long n = ctx->g0.n;
+    const auto t0 = std::chrono::steady_clock::now();
+    const int it = st->iter + 1;
+    // filter + SIMP + level-0 factors + sums of rho, rho^p, rho_f in one sweep
+    {
+        ProfScope ps(ctx, kProfFilter, 28.0 * n);
+        launch_filter_simp(s, ctx->g0, ctx->fs, ctx->sp, rho, ctx->rho_f, ctx->kap64, ctx->L[0].kap, ctx->red,
+                           ctx->scal + 56);
+    }
+    ctx->launches++;
+    CKL();
+    int rc = build_levels(ctx);
+    if (rc) return rc;
+    ctx->warm = st->warm != 0;
+    int cycles = 0;
+    double resid[3];
+    rc = otm_solve(ctx, nullptr, cfg->solver_tol, cfg->max_vcycles, &cycles, resid);
+    if (rc == OTM_ENOCONV) {
+        char buf[256];
+        snprintf(buf, sizeof buf, "solver failed at iteration %d: %s", it, ctx->err.c_str());
+        ctx->err = buf;
+        st->finished = 1;
+        return OTM_ENOCONV;
+    }
+    if (rc) return rc;
+    st->warm = 1;
+    double kap[6];
+    rc = otm_tensor(ctx, kap);
+    if (rc) return rc;
+    // the filter sums were synchronised with the tensor readback
+    CK(cudaMemcpyAsync(ctx->h, ctx->scal + 56, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const double mean_rho = ctx->h[0] / (double)n, mean_rho_p = ctx->h[1] / (double)n,
+                 mean_rf = ctx->h[2] / (double)n;
+    double g, dG[6];
+    if (otm_objective(cfg->objective, cfg->target, kap, &g, dG)) return fail(ctx, OTM_EINVAL, "objective failed");
+    rc = otm_sensitivity(ctx, dG, ctx->sensf);
+    if (rc) return rc;
+    rc = otm_filter(ctx, ctx->sensf, ctx->sens, 1);
+    if (rc) return rc;
+    if (rho_f_out) CK(cudaMemcpyAsync(rho_f_out, ctx->rho_f, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (cfg->symmetry == 1) {
+        launch_symmetrize(s, ctx->g0, ctx->sens);
+        ctx->launches++;
+    }
+    if (sens_out) CK(cudaMemcpyAsync(sens_out, ctx->sens, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    rec->iter = it;
+    rec->g = g;
+    rec->volfrac = mean_rho;
+    rec->volfrac_filtered = mean_rf;
+    rec->vstar = cfg->model == 0 ? st->gov.vstar : (cfg->model == 2 ? cfg->volume_bound : NAN);
+    rec->vcycles = cycles;
+    rec->ms = ms;
+    for (int c = 0; c < 6; ++c) rec->kappa[c] = kap[c];
+    for (int c = 0; c < 3; ++c) rec->solve_residual[c] = resid[c];
+    st->iter = it;
+    // convergence (optimize.py:327-345)
+    if (st->have_g_last && std::fabs(g - st->g_last) < cfg->conv_threshold) st->plateau += 1;
+    else st->plateau = 0;
+    st->g_last = g;
+    st->have_g_last = 1;
+    bool converged = false;
+    if (g <= 1e-12) converged = true;
+    else if (st->plateau >= 3) {
+        if (cfg->model == 0) {
+            const double cd = st->gov.reduced ? st->gov.gap * st->gov.df : INFINITY;
+            converged = cd < 1e-4 && g <= st->gov.bound;
+        } else {
+            converged = true;
+        }
+    }
+    st->converged = converged ? 1 : 0;
+    st->g = g;
+    st->mean_rho = mean_rho;
+    st->mean_rho_p = mean_rho_p;
+    if (converged || it == cfg->max_iter) st->finished = 1;
+    return OTM_OK;
+}
+
+int otm_run_update(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, double* rho) {
+    if (!ctx || !cfg || !st || !rho) return OTM_EINVAL;
+    if (st->finished) return fail(ctx, OTM_ESTATE, "run already finished");
+    double lam;
+    int active, changed;
+    int rc;
+    const double mean_rho = st->mean_rho;
+    if (cfg->model == 0) {
+        double vb = otm_governor_update(&st->gov, st->g, mean_rho, st->mean_rho_p);
+        vb = std::min(vb, mean_rho + 0.5 * cfg->oc.step_limit);
+        rc = otm_oc_update(ctx, rho, ctx->sens, vb, &cfg->oc, rho, &lam, &active, &changed);
+        if (rc) return rc;
+        if (!changed) {
+            rc = otm_oc_update(ctx, rho, ctx->sens, mean_rho - 0.25 * cfg->oc.step_limit, &cfg->oc, rho, &lam,
+                               &active, &changed);
+            if (rc) return rc;
+        }
+    } else {
+        rc = otm_oc_update(ctx, rho, ctx->sens, cfg->volume_bound, &cfg->oc, rho, &lam, &active, &changed);
+        if (rc) return rc;
+    }
+    if (cfg->symmetry == 1) {
+        launch_symmetrize(ctx->stream, ctx->g0, rho);
+        ctx->launches++;
+    }
+    CKL();
+    return OTM_OK;
+}
+
+int otm_profile_enable(otm_ctx* ctx, int on) {
+    if (!ctx) return OTM_EINVAL;
+    ctx->prof = on != 0;
+    return OTM_OK;
+}
+
+int otm_profile_reset(otm_ctx* ctx) {
+    if (!ctx) return OTM_EINVAL;
+    for (int i = 0; i < kProfClasses; ++i) {
+        ctx->prof_ms[i] = 0.0;
+        ctx->prof_n[i] = 0;
+        ctx->prof_bytes[i] = 0.0;
+    }
+    return OTM_OK;
+}
+
+int otm_profile_read(otm_ctx* ctx, int cls, double* ms_total, long long* launches, double* bytes) {
+    if (!ctx || cls < 0 || cls >= kProfClasses) return OTM_EINVAL;
+    if (ms_total) *ms_total = ctx->prof_ms[cls];
+    if (launches) *launches = ctx->prof_n[cls];
+    if (bytes) *bytes = ctx->prof_bytes[cls];
+    return OTM_OK;
+}
+
+}  // extern "C"

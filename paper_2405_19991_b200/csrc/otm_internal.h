@@ -1,0 +1,110 @@
+// Internal declarations shared by the kernel and host translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "otm_common.cuh"
+
+namespace otm {
+
+constexpr int kOcLam = 32;   // multipliers evaluated per OC bisection pass
+
+struct SimpParams {          // element.py:42-56, 91-100
+    double k0, kmin, p;
+};
+
+// Level template: K[a][b] = kt[a ^ b]; equal axis scales use the compact form
+// with s12 = scale / 12.  f0[a*3+i] = (K @ corners)[a][i] (element.py:86).
+struct LevelTemplate {
+    int equal;
+    double s12;
+    double kt[8];
+    double f0[24];
+};
+
+struct CoarseTemplate {
+    double kt[8];
+};
+
+struct Dg {
+    double v[6];
+};
+
+struct LamSet {
+    double v[kOcLam];    // lam^-damp per candidate multiplier; 0 encodes the free step
+};
+
+struct OcArgs {
+    double step, rmin, damp, floor_ratio;   // floor_ratio = (1e-10)^damp
+    int sqrt_damp;
+};
+
+// Device-resident scalars of the batched PCG (3 load cases).
+struct PcgScalars {
+    double red[16];
+    double rz[3], beta[3], pq[3], alpha[3], rr[3], target2[3], active[3];
+    double sumT[3];
+    double flags[8];     // copied to the host after every inner iteration
+    int first;
+    int pad;
+};
+
+// Deterministic two-stage reduction workspace.
+struct Red {
+    double* partials;    // >= max blocks * 32 doubles
+    unsigned* counter;   // zero-initialised
+};
+
+struct FilterSetup {
+    int window;          // 1: reach <= 1, register-window kernel
+    int ntaps;
+    double w27[27];
+    int* offs_dev;       // generic path
+    double* wts_dev;
+};
+
+int stencil_chunks(const Geo& g, int* xb);
+
+void launch_filter(cudaStream_t s, const Geo& g, const FilterSetup& fs, int adjoint, const double* in,
+                   double* out, Red& red);
+void launch_filter_simp(cudaStream_t s, const Geo& g, const FilterSetup& fs, const SimpParams& sp,
+                        const double* rho, double* rho_f, double* k64, float* k32, Red& red, double* out4);
+void launch_simp(cudaStream_t s, long long n, const double* rf, double* k64, float* k32, const SimpParams& sp);
+void launch_set_kappa(cudaStream_t s, long long n, const double* kin, double* k64, float* k32);
+void launch_means(cudaStream_t s, long long n, const double* rho, double p, Red& red, double* out2);
+void launch_symmetrize(cudaStream_t s, const Geo& g, double* a);
+void launch_coarsen(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* kf, float* kc);
+void launch_dinv(cudaStream_t s, const Geo& g, const float* k, float kdiag, float* dinv);
+void launch_coarse_setup(cudaStream_t s, const Geo& g, const float* k, const CoarseTemplate& ct, double* work,
+                         float* G);
+void launch_coarse_solve(cudaStream_t s, int n, const float* G, const float* f, float* z);
+void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
+                  const double* fext, const double* fmean, float* r32, Red& red, double* out9);
+void launch_apply64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
+                    double* out, int load_case);
+void launch_sum3(cudaStream_t s, long long n, const double* f, Red& red, double* out3);
+void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* f,
+                       const float* dinv, float omega, float* z, float* res);
+void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* z,
+                   const float* f, const float* dinv, float omega, float* zout, bool dot, Red& red,
+                   PcgScalars* sc);
+void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* p,
+                 float* q, Red& red, PcgScalars* sc);
+void launch_pupd(cudaStream_t s, long long n, const float* z, float* p, const PcgScalars* sc);
+void launch_upd(cudaStream_t s, long long n, float* d, float* r, const float* p, const float* q, Red& red,
+                PcgScalars* sc);
+void launch_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* res, float* fc);
+void launch_prolong(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* zc, float* zf);
+void launch_Tupd(cudaStream_t s, long long n3, double* T, const float* d);
+void launch_submean(cudaStream_t s, long long n, double* T, const double* sumT);
+void launch_tensor(cudaStream_t s, const Geo& g, const double* T, const double* kap, Red& red, double* out6);
+void launch_pair_energy(cudaStream_t s, const Geo& g, const double* T, double* E);
+void launch_sens(cudaStream_t s, const Geo& g, const double* T, const double* rf, const SimpParams& sp,
+                 const Dg& dG, double* sens);
+void launch_oc_eval(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a, int nlam,
+                    const LamSet& lam_pow, Red& red, double* out);
+void launch_oc_apply(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a,
+                     double lam, double* rho_out, int* changed);
+
+}  // namespace otm

@@ -1,0 +1,321 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the CPU oracle.  Tolerances:
+  * filter / symmetry / OC update / macro loads: bit-exact (same fp64 op order)
+  * operator K T: 1e-12 relative (summation order differs)
+  * homogenized tensor: 1e-5 relative to ||kappa|| (gate); observed ~1e-9
+  * sensitivities: 1e-4 relative to max|sens| (gate)
+  * C1 trajectory over 80 iterations: g rel 1e-3, |dV| 1e-4
+"""
+
+import numpy as np
+import pytest
+
+from otm_testutil import cuda_available, golden
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not cuda_available(), reason="needs a CUDA device")]
+
+
+@pytest.fixture(scope="module")
+def otm():
+    import paper_2405_19991_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def O():
+    from oracle import otm_oracle
+    return otm_oracle
+
+
+# ---------------------------------------------------------------- field
+@pytest.mark.parametrize("radius,tag", [(1.5, "1p5"), (2.0, "2p0")])
+def test_filter_bitexact(otm, radius, tag):
+    g = golden("filter.npz")
+    spec = otm.FilterSpec(radius)
+    fld = otm.DensityField(g["rho"].shape, g["rho"], np.zeros(g["rho"].shape))
+    assert np.array_equal(otm.filter_forward(fld, spec), g[f"fwd_{tag}"])
+    assert np.array_equal(otm.filter_backward(fld, spec, g["g"]), g[f"bwd_{tag}"])
+
+
+def test_filter_generic_reach(otm, O):
+    rng = np.random.default_rng(5)
+    rho = rng.uniform(0, 1, (8, 9, 10))
+    fld = otm.DensityField(rho.shape, rho, np.zeros(rho.shape))
+    spec = otm.FilterSpec(2.6)
+    assert np.abs(otm.filter_forward(fld, spec) - O.filter_fwd(rho, 2.6)).max() < 1e-15
+    assert np.abs(otm.filter_backward(fld, spec, rho) - O.filter_adj(rho, 2.6)).max() < 1e-15
+
+
+def test_filter_adjoint_identity(otm):
+    rng = np.random.default_rng(6)
+    a, b = rng.standard_normal((2, 12, 10, 14))
+    spec = otm.FilterSpec(1.5)
+    fld = otm.DensityField(a.shape, a, np.zeros(a.shape))
+    lhs = float((otm.filter_forward(fld, spec) * b).sum())
+    rhs = float((a * otm.filter_backward(fld, spec, b)).sum())
+    assert lhs == pytest.approx(rhs, rel=1e-13)
+
+
+def test_symmetry_projection(otm):
+    g = golden("filter.npz")
+    fld = otm.DensityField(g["sym_in"].shape, g["sym_in"].copy(), np.zeros(g["sym_in"].shape))
+    otm.project_central_symmetry(fld)
+    assert np.array_equal(fld.rho, g["sym_out"])
+
+
+def test_device_tensors_roundtrip(otm):
+    import torch
+    g = golden("filter.npz")
+    t = torch.from_numpy(g["rho"]).cuda()
+    fld = otm.DensityField(tuple(t.shape), t, torch.zeros_like(t))
+    out = otm.filter_forward(fld, otm.FilterSpec(1.5))
+    assert isinstance(out, torch.Tensor) and out.is_cuda
+    assert np.array_equal(out.cpu().numpy(), g["fwd_1p5"])
+
+
+# ---------------------------------------------------------------- operator
+@pytest.mark.parametrize("tag", ["a", "b", "c", "d"])
+def test_apply_K_and_macro_load(otm, tag):
+    g = golden("operator.npz")
+    kap = g[f"kappa_{tag}"]
+    h = otm.GridHierarchy(kap.shape)
+    h.build(kap)
+    KT = otm.apply_K(h.levels[0], g[f"T_{tag}"])
+    ref = g[f"KT_{tag}"]
+    assert np.abs(KT - ref).max() <= 1e-12 * np.abs(ref).max()
+    for i in range(3):
+        assert np.array_equal(otm.assemble_macro_load(h, i), g[f"f_{tag}"][i])
+
+
+def test_operator_matches_oracle_random_grids(otm, O):
+    rng = np.random.default_rng(1)
+    for _ in range(8):
+        dims = tuple(int(d) for d in rng.choice([4, 5, 6, 8], size=3))
+        kap = rng.uniform(1e-4, 1.0, dims)
+        T = rng.standard_normal(dims)
+        h = otm.GridHierarchy(dims)
+        h.build(kap)
+        ho = O.Hierarchy(dims)
+        ho.build(kap)
+        want = ho.levels[0].apply(T)
+        got = otm.apply_K(h.levels[0], T)
+        assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+
+
+def test_nullspace_and_symmetry(otm):
+    rng = np.random.default_rng(3)
+    h = otm.GridHierarchy((4, 6, 4))
+    h.build(rng.uniform(0.1, 1, (4, 6, 4)))
+    assert np.abs(otm.apply_K(h.levels[0], np.full((4, 6, 4), 3.7))).max() < 1e-12
+    a, b = rng.standard_normal((2, 4, 6, 4))
+    lhs = float((otm.apply_K(h.levels[0], a) * b).sum())
+    rhs = float((a * otm.apply_K(h.levels[0], b)).sum())
+    assert lhs == pytest.approx(rhs, rel=1e-11)
+
+
+def test_level_chain(otm):
+    g = golden("operator.npz")
+    for i, k in enumerate(g["chain_dims_keys"]):
+        dims = tuple(int(x) for x in str(k).strip("()").split(","))
+        h = otm.GridHierarchy(dims)
+        assert np.array_equal(np.array([l.dims for l in h.levels]), g[f"chain_dims_{i}"])
+    with pytest.raises(ValueError):
+        otm.GridHierarchy((63, 63, 63))
+    with pytest.raises(ValueError):
+        otm.GridHierarchy((0, 4, 4))
+
+
+# ---------------------------------------------------------------- solve
+def test_solve_equation_matches_reference(otm):
+    g = golden("solve.npz")
+    h = otm.GridHierarchy((8, 8, 8))
+    h.build(g["kappa"])
+    T, cyc = otm.solve_equation(h, g["f"], tol=1e-10)
+    assert np.abs(T - g["T"]).max() <= 1e-8 * np.abs(g["T"]).max()
+    assert abs(T.mean()) < 1e-12
+    r = g["f"] - otm.apply_K(h.levels[0], T)
+    assert np.linalg.norm(r) <= 1.01e-10 * np.linalg.norm(g["f"])
+    T2, _ = otm.solve_equation(h, g["f"], tol=1e-10, x0=g["x0"])
+    assert np.abs(T2 - g["T_warm"]).max() <= 1e-8 * np.abs(g["T"]).max()
+
+
+def test_solve_zero_load_and_failure(otm):
+    from paper_2405_19991_b200.solver import ConvergenceError
+    h = otm.GridHierarchy((8, 8, 8))
+    rng = np.random.default_rng(16)
+    h.build(rng.uniform(0.05, 1, (8, 8, 8)))
+    T, cycles = otm.solve_equation(h, np.zeros((8, 8, 8)))
+    assert cycles == 0 and np.abs(T).max() == 0
+    f = rng.standard_normal((8, 8, 8))
+    f -= f.mean()
+    with pytest.raises(ConvergenceError) as err:
+        otm.solve_equation(h, f, tol=1e-14, max_vcycles=1)
+    assert err.value.residual > 0
+
+
+def test_solve_deterministic_and_translation(otm):
+    rng = np.random.default_rng(14)
+    kap = rng.uniform(0.05, 1, (16, 16, 16))
+    f = rng.standard_normal((16, 16, 16))
+    f -= f.mean()
+    runs = []
+    for _ in range(2):
+        h = otm.GridHierarchy((16, 16, 16))
+        h.build(kap)
+        runs.append(otm.solve_equation(h, f, tol=1e-8)[0])
+    assert np.array_equal(runs[0], runs[1])
+    shift = (3, 1, 2)
+    h2 = otm.GridHierarchy((16, 16, 16))
+    h2.build(np.roll(kap, shift, (0, 1, 2)))
+    T2, _ = otm.solve_equation(h2, np.roll(f, shift, (0, 1, 2)), tol=1e-10)
+    h1 = otm.GridHierarchy((16, 16, 16))
+    h1.build(kap)
+    T1, _ = otm.solve_equation(h1, f, tol=1e-10)
+    assert np.allclose(np.roll(T1, shift, (0, 1, 2)), T2, atol=1e-8)
+
+
+# ---------------------------------------------------------------- homogenization
+@pytest.mark.parametrize("name", ["homog_rand8.npz", "homog_iwp16.npz", "homog_rand_6x8x10.npz"])
+def test_homogenize_and_sensitivity_vs_reference(otm, name):
+    g = golden(name)
+    mp = otm.MaterialParams()
+    spec = otm.FilterSpec(1.5)
+    rho = g["rho"]
+    fld = otm.DensityField(rho.shape, rho, np.zeros(rho.shape))
+    rho_f = otm.filter_forward(fld, spec)
+    assert np.array_equal(rho_f, g["rho_f"])
+    h = otm.GridHierarchy(rho.shape)
+    res = otm.homogenize(h, rho_f, mp, tol=1e-10)
+    kh = g["kappa_h"]
+    assert np.abs(res.tensor.vec - kh).max() <= 1e-9 * np.linalg.norm(kh)
+    gg, dG = otm.eval_objective(otm.ObjectiveSpec("mse", otm.ConductivityTensor(g["target"])), res.tensor)
+    sens_f = otm.tensor_sensitivity(res, dG)
+    assert np.abs(sens_f - g["sens_f"]).max() <= 1e-6 * np.abs(g["sens_f"]).max()
+    sens = otm.filter_backward(fld, spec, sens_f)
+    assert np.abs(sens - g["sens"]).max() <= 1e-6 * np.abs(g["sens"]).max()
+    assert np.abs(res.pair_energy - g["pair_energy"]).max() <= 1e-6 * np.abs(g["pair_energy"]).max()
+
+
+def test_closed_forms(otm):
+    mp = otm.MaterialParams()
+    h = otm.GridHierarchy((16, 16, 16))
+    res = otm.homogenize(h, np.ones((16, 16, 16)), mp, tol=1e-10)
+    assert np.abs(res.tensor.vec - [1, 1, 1, 0, 0, 0]).max() < 1e-5
+    res = otm.homogenize(h, np.zeros((16, 16, 16)), mp, tol=1e-10)
+    assert np.abs(res.tensor.vec - [1e-4, 1e-4, 1e-4, 0, 0, 0]).max() < 1e-8
+    k = float(otm.simp_conductivity(0.5, mp))
+    res = otm.homogenize(otm.GridHierarchy((8, 8, 8)), np.full((8, 8, 8), 0.5), mp, tol=1e-10)
+    assert np.abs(res.tensor.vec[:3] - k).max() < 1e-9 and np.abs(res.tensor.vec[3:]).max() < 1e-12
+    # laminate: arithmetic / harmonic means (test_homogenize.py:39-51)
+    n = 32
+    rho = np.zeros((n, n, n))
+    rho[:, :, : n // 2] = 1.0
+    mp1 = otm.MaterialParams(penalty=1.0)
+    v = otm.homogenize(otm.GridHierarchy((n, n, n)), rho, mp1, tol=1e-9).tensor.vec
+    arith = 0.5 * (1.0 + 1e-4)
+    harm = 2.0 * 1e-4 / (1.0 + 1e-4)
+    assert abs(v[0] - arith) / arith < 5e-3 and abs(v[1] - arith) / arith < 5e-3
+    assert abs(v[2] - harm) / harm < 5e-3 and np.abs(v[3:]).max() < 1e-6
+
+
+@pytest.mark.parametrize("tag", ["c2", "c3"])
+def test_first_iteration_full_size(otm, tag):
+    """BASELINE configs 2 and 3 at full size: tensor 1e-5, sensitivities 1e-4."""
+    g = golden(f"first_{tag}.npz")
+    dims = tuple(int(d) for d in g["dims"])
+    rho = otm.init_density(dims, otm.InitPattern("iwp", float(g["vf"]), seed=0)).rho
+    spec = otm.FilterSpec(1.5)
+    fld = otm.DensityField(dims, rho, np.zeros(dims))
+    rho_f = otm.filter_forward(fld, spec)
+    h = otm.GridHierarchy(dims)
+    res = otm.homogenize(h, rho_f, otm.MaterialParams(), tol=1e-6)
+    kh = g["kappa_h"]
+    kerr = np.abs(res.tensor.vec - kh).max() / np.linalg.norm(kh)
+    assert kerr <= 1e-5, kerr
+    sens = otm.filter_backward(fld, spec, otm.tensor_sensitivity(res, g["dG"]))
+    serr = np.abs(sens.ravel()[g["sens_idx"]] - g["sens_sample"]).max() / float(g["sens_absmax"])
+    assert serr <= 1e-4, serr
+    assert abs(np.abs(sens).max() - float(g["sens_absmax"])) <= 1e-4 * float(g["sens_absmax"])
+
+
+# ---------------------------------------------------------------- optimizer
+def test_oc_update_bitexact(otm):
+    g = golden("oc.npz")
+    for k in range(int(g["ncases"])):
+        p = otm.OCParams(step_limit=float(g[f"step_{k}"]))
+        new, info = otm.oc_update(g[f"rho_{k}"], g[f"sens_{k}"], float(g[f"bound_{k}"]), p)
+        assert info["active"] == bool(g[f"active_{k}"])
+        assert info["lam"] == pytest.approx(float(g[f"lam_{k}"]), rel=1e-12)
+        assert np.array_equal(new, g[f"new_{k}"]), k
+
+
+def test_oc_update_vs_oracle_random(otm, O):
+    rng = np.random.default_rng(11)
+    for trial in range(20):
+        dims = (10, 12, 14)
+        rho = rng.uniform(0.001, 1.0, dims)
+        sens = rng.standard_normal(dims) * 10.0 ** rng.uniform(-8, 0)
+        bound = float(rho.mean()) + rng.uniform(-0.02, 0.02)
+        p = otm.OCParams(step_limit=float(rng.choice([0.02, 0.05, 0.2])))
+        new, info = otm.oc_update(rho, sens, bound, p)
+        want, winfo = O.oc_step(rho, sens, bound, O.OC(step_limit=p.step_limit))
+        assert info["lam"] == pytest.approx(winfo["lam"], rel=1e-12)
+        assert np.array_equal(new, want)
+
+
+def test_governor_trace(otm):
+    g = golden("oc.npz")
+    st = otm.GovernorState()
+    for gval, row in zip(g["gov_g"], g["gov_trace"]):
+        v = otm.governor_update(st, float(gval), g["gov_rho"], 3.0)
+        got = [v, st.df, st.gap, st.count, float(st.reduced), st.current_decrease]
+        assert np.allclose(got, row, rtol=1e-12, atol=0)
+
+
+def test_trajectory_c1_80_iterations(otm):
+    """Config 1 (32^3 IWP vf 0.3, isotropic 0.1 target), first 80 OC iterations."""
+    g = golden("traj_c1.npz")
+    n = len(g["g"])
+    cfg = otm.RunConfig(dims=(32, 32, 32),
+                        target=otm.ObjectiveSpec("mse", otm.ConductivityTensor(g["target"])),
+                        init=otm.InitPattern("iwp", float(g["vf"]), seed=0), max_iter=n)
+    res = otm.run_optimization(cfg)
+    gs = np.array([r.g for r in res.log])
+    vs = np.array([r.volfrac for r in res.log])
+    assert len(gs) == n
+    relg = np.abs(gs - g["g"]) / np.abs(g["g"])
+    assert relg.max() <= 1e-3, (relg.argmax(), relg.max())
+    assert np.abs(vs - g["volfrac"]).max() <= 1e-4
+    assert np.allclose([r.vstar for r in res.log], g["vstar"], atol=1e-4)
+    assert np.abs(res.kappa.vec - g["kappa_final"]).max() <= 1e-3 * np.linalg.norm(g["kappa_final"])
+
+
+def test_run_deterministic(otm):
+    target = otm.ObjectiveSpec("mse", otm.ConductivityTensor([0.15, 0.15, 0.15, 0, 0, 0]))
+    out = []
+    for _ in range(2):
+        cfg = otm.RunConfig(dims=(16, 16, 16), target=target, init=otm.InitPattern("iwp", 0.5, seed=3),
+                            max_iter=6)
+        out.append(otm.run_optimization(cfg))
+    assert np.array_equal(out[0].field.rho, out[1].field.rho)
+    assert out[0].log[-1].g == out[1].log[-1].g
+
+
+def test_central_symmetry_every_iteration(otm):
+    target = otm.ObjectiveSpec("mse", otm.ConductivityTensor([0.2, 0.2, 0.2, 0, 0, 0]))
+    seen = []
+    cfg = otm.RunConfig(dims=(8, 8, 8), target=target, symmetry="central",
+                        init=otm.InitPattern("random", 0.5, seed=1), max_iter=6)
+    otm.run_optimization(cfg, callback=lambda it, fld, r, g: seen.append(fld.rho.cpu().numpy().copy()))
+    assert len(seen) >= 4
+    for rho in seen:
+        assert np.array_equal(rho, rho[::-1, ::-1, ::-1])
+
+
+def test_already_optimal(otm):
+    mp = otm.MaterialParams()
+    k = float(otm.simp_conductivity(0.5, mp))
+    cfg = otm.RunConfig(dims=(8, 8, 8), target=otm.ObjectiveSpec("mse", otm.ConductivityTensor([k, k, k, 0, 0, 0])),
+                        material=mp, init_field=np.full((8, 8, 8), 0.5), max_iter=5)
+    assert otm.run_optimization(cfg).log[0].g < 1e-9
