@@ -1,0 +1,308 @@
+#!/usr/bin/env python
+"""Benchmark: seconds per 128^3 anisotropic structure (BASELINE config 3) on B200.
+
+A "step" is one complete structure: 500 OC iterations of the adaptive-volume
+loop (``conv_threshold=0`` keeps the count fixed, as BASELINE.md asks for "a
+fixed 500 iterations") on the 128^3 IWP seed (vf 0.5), target
+[0.3,0.2,0.1,0.1,0.05,0.05] (reference packing k11,k22,k33,k12,k23,k13).
+
+  value  device-timed seconds/structure, density already resident in HBM
+  e2e    the same through the public API (run_optimization on a numpy seed,
+         H2D of the seed and D2H of the final field inside the timed region)
+  roofline  dominant kernel class (level-0 MG-PCG stencils) from CUDA events on
+         the library stream during the timed region, vs MEASURED_PEAKS.json
+  cpu_baseline  the CPU oracle (numpy port of the reference) on one OC
+         iteration of the same workload, extrapolated x500
+
+``--impl reference`` times that CPU port alone (rank 0) on the same metric.
+Multi-GPU (torchrun): every rank designs its own structure (replicas; the slab
+-decomposed solver is future work), value = max-over-ranks time /
+(ranks x steps).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+TARGET_C3 = [0.3, 0.2, 0.1, 0.1, 0.05, 0.05]
+CONFIGS = {
+    "c1": dict(dims=(32, 32, 32), target=[0.1, 0.1, 0.1, 0, 0, 0], vf=0.3),
+    "c2": dict(dims=(64, 64, 64), target=[0.3, 0.2, 0.1, 0, 0, 0], vf=0.5),
+    "c3": dict(dims=(128, 128, 128), target=TARGET_C3, vf=0.5),
+    "c4": dict(dims=(256, 256, 256), target=TARGET_C3, vf=0.5),
+}
+METRIC = "seconds/structure at 128³; MG-PCG stencil GB/s vs B200 HBM peak"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.path = f"/tmp/otm_clocks_{os.getpid()}.csv"
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_config(otm, name, max_iter, conv_threshold, init_field=None):
+    c = CONFIGS[name]
+    return otm.RunConfig(dims=c["dims"], target=otm.ObjectiveSpec("mse", otm.ConductivityTensor(c["target"])),
+                         init=otm.InitPattern("iwp", c["vf"], seed=0), init_field=init_field,
+                         max_iter=max_iter, conv_threshold=conv_threshold)
+
+
+# --------------------------------------------------------------------------- CPU legs
+def cpu_iteration_seconds(name, iters=1):
+    """Time `iters` OC iterations of the CPU oracle on the workload (bounded sample)."""
+    from oracle import otm_oracle as O
+    c = CONFIGS[name]
+    cfg = O.Run(dims=c["dims"], target=c["target"], init=("iwp", c["vf"], 0), max_iter=iters + 1,
+                conv_threshold=0.0)
+    t0 = time.perf_counter()
+    # iterations + 1 evaluations with `iters` updates: the final evaluation closes the last update
+    rho, kh, log, conv = O.optimize(cfg)
+    wall = time.perf_counter() - t0
+    return wall / (iters + 1), log
+
+
+def run_reference(args):
+    world, rank, _ = dist_init()
+    if rank != 0:
+        return
+    per_step = []
+    for s in range(args.warmup + args.steps):
+        t, _ = cpu_iteration_seconds(args.config, iters=0)
+        if s >= args.warmup:
+            per_step.append(t)
+    s_iter = statistics.median(per_step)
+    value = s_iter * args.iters
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "s/structure",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": s_iter * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (IWP seed, reference init_density)",
+            "config": {"workload": f"{args.config} {CONFIGS[args.config]['dims']} target "
+                                   f"{CONFIGS[args.config]['target']} vf {CONFIGS[args.config]['vf']}, "
+                                   f"{args.iters} OC iterations per structure (extrapolated from per-iteration time)",
+                       "step": "one OC iteration of the CPU oracle (filter, 3 GS-V-cycle solves, tensor, "
+                               "sensitivities, adjoint filter)"},
+            "cpu_baseline": {"value": value, "unit": "s/structure", "cores": 1, "kind": "port",
+                             "sample": f"{args.steps} single-iteration samples (cold solve from the seed)"},
+            "e2e": {"value": value, "unit": "s/structure", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU leg
+def run_gpu(args):
+    import numpy as np
+    import torch
+
+    world, rank, local = dist_init()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2405_19991_b200 as otm
+    from paper_2405_19991_b200 import _dev, _lib
+    from paper_2405_19991_b200.optimize import DesignRun
+
+    name = args.config
+    dims = CONFIGS[name]["dims"]
+    n = int(np.prod(dims))
+    seed = otm.init_density(dims, otm.InitPattern("iwp", CONFIGS[name]["vf"], seed=0)).rho
+    seed_dev = torch.from_numpy(seed).cuda()
+    lib = _lib.load()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # > 126 MB L2
+
+    hier = otm.GridHierarchy(dims)
+    ctx = hier.ctx
+
+    def one_structure():
+        cfg = make_config(otm, name, args.iters, 0.0, init_field=seed_dev)
+        run = DesignRun(cfg, hier=hier)
+        while not run.finished:
+            rc, _ = run.step()
+            if rc != _lib.OTM_OK:
+                ctx.check(rc)
+        return run
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        one_structure()
+    barrier()
+    # ---- timed region (device events on the library stream) ----
+    lib.otm_profile_reset(ctx.h)
+    lib.otm_profile_enable(ctx.h, 0 if args.no_prof else 1)
+    launches0 = lib.otm_launch_count(ctx.h)
+    clocks = Clocks(local)
+    clocks.start()
+    step_ms = []
+    iters_done = []
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    total_ms = 0.0
+    for _ in range(args.steps):
+        flush.fill_(1.0)                 # evict L2 between steps
+        barrier()
+        ev[0].record(ctx.stream)
+        run = one_structure()
+        ev[1].record(ctx.stream)
+        ev[1].synchronize()
+        ms = ev[0].elapsed_time(ev[1])
+        step_ms.append(ms)
+        total_ms += ms
+        iters_done.append(len(run.log))
+    barrier()
+    clk = clocks.stop()
+    lib.otm_profile_enable(ctx.h, 0)
+    launches = lib.otm_launch_count(ctx.h) - launches0
+    # max over ranks
+    t_max = total_ms
+    if world > 1:
+        tt = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_max = float(tt.item())
+    value = (t_max / 1e3) / (args.steps * world)
+    # roofline: level-0 stencil class measured inside the timed region
+    import ctypes as C
+    prof = {}
+    for cls, nm in ((0, "l0_stencil"), (1, "vcycle"), (2, "res64"), (3, "tensor_sens"), (4, "filter"), (5, "oc")):
+        ms_t, cnt, byt = C.c_double(), C.c_longlong(), C.c_double()
+        lib.otm_profile_read(ctx.h, cls, C.byref(ms_t), C.byref(cnt), C.byref(byt))
+        prof[nm] = {"ms": ms_t.value, "launches": cnt.value, "bytes": byt.value,
+                    "gbs": (byt.value / (ms_t.value * 1e-3) / 1e9) if ms_t.value > 0 else None}
+    peak, peak_kind = peaks()
+    l0 = prof["l0_stencil"]
+    achieved = l0["gbs"]
+    # ---- e2e through the public API with host buffers ----
+    e2e_ms = []
+    for s in range(max(1, min(args.steps, 2))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cfg = make_config(otm, name, args.iters, 0.0, init_field=seed)     # numpy seed: H2D inside
+        res = otm.run_optimization(cfg)                                     # numpy field back: D2H inside
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        assert isinstance(res.field.rho, np.ndarray)
+    e2e = statistics.median(e2e_ms) / 1e3
+    if world > 1:
+        tt = torch.tensor([e2e], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e = float(tt.item()) / world
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": "s/structure", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32",
+        "data": "synthetic (IWP seed from init_density, vf 0.5)",
+        "config": {"workload": f"{name} {dims} target {CONFIGS[name]['target']} (k11,k22,k33,k12,k23,k13), "
+                               f"vf {CONFIGS[name]['vf']}, {args.iters} OC iterations per structure",
+                   "iterations_per_step": iters_done, "parallelism": f"replicas x{world}",
+                   "l2": "flushed (256 MB write) before every timed step",
+                   "solver": "fp64 defect correction + fp32 MG-PCG (damped Jacobi V-cycle), tol 1e-6"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": None,
+                     "kernel": "level-0 stencils (smooth_res + jacobi + spmv), 3 load cases fp32",
+                     "bytes_per_vertex": "44 (smooth_res, jacobi) / 28 (spmv)", "peak_kind": peak_kind},
+        "kernels": prof,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "e2e": {"value": e2e, "unit": "s/structure", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
+    }
+    if not args.no_cpu and world == 1:
+        s_iter, _ = cpu_iteration_seconds(name, iters=0)
+        line["cpu_baseline"] = {"value": s_iter * args.iters, "unit": "s/structure", "cores": 1, "kind": "port",
+                                "sample": f"one OC iteration of the CPU oracle on {name} ({s_iter:.1f} s, cold "
+                                          f"solve from the seed), x{args.iters}"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--iters", type=int, default=500, help="OC iterations per structure")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-prof", action="store_true", help="no in-region kernel events")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -163,7 +163,26 @@ int setup_filter(otm_ctx* ctx, double radius) {
                     tot += wt;
                 }
             }
-    for (auto& x : w) x /= tot;
+    // w / w.sum() with numpy's summation order (pairwise_sum, n <= 128: eight
+    // strided accumulators, combined as a tree, then the tail) so the weights
+    // are bit-identical to field.py:93
+    (void)tot;
+    {
+        const size_t m = w.size();
+        double sum = 0.0;
+        if (m < 8) {
+            for (size_t i = 0; i < m; ++i) sum += w[i];
+        } else {
+            double r[8];
+            for (int j = 0; j < 8; ++j) r[j] = w[j];
+            size_t i = 8;
+            for (; i + 8 <= m; i += 8)
+                for (int j = 0; j < 8; ++j) r[j] += w[i + j];
+            sum = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+            for (; i < m; ++i) sum += w[i];
+        }
+        for (auto& x : w) x /= sum;
+    }
     FilterSetup& fs = ctx->fs;
     fs.ntaps = (int)w.size();
     fs.window = reach <= 1 ? 1 : 0;
@@ -624,7 +643,9 @@ int otm_solve(otm_ctx* ctx, const double* fext, double tol, int max_cycles, int*
     if (!ctx->gexec) { int rc = capture_inner(ctx, false); if (rc) return rc; }
     if (ctx->prof && !ctx->gexec_prof) { int rc = capture_inner(ctx, true); if (rc) return rc; }
     double* fmean = ctx->scal + 16;
-    if (fext) { launch_sum3(s, n, fext, ctx->red, fmean); ctx->launches++; }
+    if (fext) launch_sum3(s, n, fext, ctx->red, fmean);
+    else launch_load_means(s, ctx->g0, ctx->L[0].lt, ctx->kap64, ctx->red, fmean);
+    ctx->launches++;
     if (!ctx->warm) CK(cudaMemsetAsync(ctx->T64, 0, 3 * n * sizeof(double), s));
     int cycles = 0;
     double rel[3], fnorm[3], rnorm[3];

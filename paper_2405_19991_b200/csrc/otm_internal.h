@@ -83,6 +83,8 @@ void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const d
                   const double* fext, const double* fmean, float* r32, Red& red, double* out9);
 void launch_apply64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
                     double* out, int load_case);
+void launch_load_means(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, Red& red,
+                       double* out3);
 void launch_sum3(cudaStream_t s, long long n, const double* f, Red& red, double* out3);
 void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* f,
                        const float* dinv, float omega, float* z, float* res);

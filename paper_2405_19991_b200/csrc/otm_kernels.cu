@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(128) k_res64(Geo g, int xb, LevelTemplate lt, 
                 const long long v = (long long)x * g.pl + t;
                 double f;
                 if (EXPLICIT_F) {
-                    f = fext[(size_t)c * g.n + v] - fmean[c];
+                    f = fext[(size_t)c * g.n + v];
                 } else {
                     // reference order: sum over corners a = 0..7 of f0[a,c] * kappa[v - c_a]
                     f = 0.0;
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(128) k_res64(Geo g, int xb, LevelTemplate lt, 
                         f = __dadd_rn(f, __dmul_rn(lt.f0[a * 3 + c], k[q][jj * 2 + kk]));
                     }
                 }
-                const double r = f - kt;
+                const double r = (f - fmean[c]) - kt;   // ||f|| before projection (solver.py:381)
                 r32[(size_t)c * g.n + v] = (float)r;
                 acc[c] += r * r;
                 acc[3 + c] += f * f;
@@ -393,6 +393,35 @@ __global__ void __launch_bounds__(128) k_apply64(Geo g, int xb, LevelTemplate lt
         }
         for (int i = 0; i < 9; ++i) { w[0][i] = w[1][i]; w[1][i] = w[2][i]; }
         for (int i = 0; i < 4; ++i) k[0][i] = k[1][i];
+    }
+}
+
+// Means of the three macro loads (solver.py:386-387 projects them out; they are
+// round-off, but for a uniform medium round-off is all the load there is).
+__global__ void k_load_means(Geo g, LevelTemplate lt, const double* __restrict__ kap, double* partials,
+                             unsigned* counter, double* out) {
+    double v3[3] = {0.0, 0.0, 0.0};
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < g.n;
+         v += (long long)gridDim.x * blockDim.x) {
+        const int x = (int)(v / g.pl), rem = (int)(v - (long long)x * g.pl);
+        const int y = rem / g.nz, z = rem - y * g.nz;
+        const int xs[2] = {wrap_m(x, g.nx), x}, ys[2] = {wrap_m(y, g.ny), y}, zs[2] = {wrap_m(z, g.nz), z};
+        double k[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {   // element v - c_a
+            const int q = 1 - (a & 1), jj = 1 - ((a >> 1) & 1), kk = 1 - ((a >> 2) & 1);
+            k[a] = kap[((long long)xs[q] * g.ny + ys[jj]) * g.nz + zs[kk]];
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            double f = 0.0;
+#pragma unroll
+            for (int a = 0; a < 8; ++a) f = __dadd_rn(f, __dmul_rn(lt.f0[a * 3 + c], k[a]));
+            v3[c] += f;
+        }
+    }
+    if (reduce_finalize<3>(v3, partials, counter, out)) {
+        for (int c = 0; c < 3; ++c) out[c] /= (double)g.n;
     }
 }
 
@@ -907,7 +936,7 @@ void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const d
     if (fext)
         k_res64<true><<<grid, 128, 0, s>>>(g, xb, lt, kap, T, fext, fmean, r32, red.partials, red.counter, out9);
     else
-        k_res64<false><<<grid, 128, 0, s>>>(g, xb, lt, kap, T, nullptr, nullptr, r32, red.partials, red.counter,
+        k_res64<false><<<grid, 128, 0, s>>>(g, xb, lt, kap, T, nullptr, fmean, r32, red.partials, red.counter,
                                             out9);
 }
 void launch_apply64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
@@ -915,6 +944,12 @@ void launch_apply64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const
     int xb;
     const dim3 grid = stencil_grid(g, &xb);
     k_apply64<<<grid, 128, 0, s>>>(g, xb, lt, kap, T, out, load_case);
+}
+void launch_load_means(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, Red& red,
+                       double* out3) {
+    long long want = (g.n + 255) / 256;
+    unsigned blocks = (unsigned)(want < 1184 ? want : 1184);
+    k_load_means<<<blocks, 256, 0, s>>>(g, lt, kap, red.partials, red.counter, out3);
 }
 void launch_sum3(cudaStream_t s, long long n, const double* f, Red& red, double* out3) {
     k_sum3<<<592, 256, 0, s>>>(n, f, red.partials, red.counter, out3);
