@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -202,7 +203,7 @@ int setup_filter(otm_ctx* ctx, double radius) {
 }
 
 size_t max_blocks(const otm_ctx* ctx) {
-    size_t mb = 4096;
+    size_t mb = 4096 + (size_t)(ctx->g0.n / 1024) + 16;   // k_upd: n/4 threads in blocks of 256
     for (const auto& l : ctx->L) {
         int xb;
         const int ch = stencil_chunks(l.g, &xb);
@@ -669,6 +670,8 @@ int otm_solve(otm_ctx* ctx, const double* fext, double tol, int max_cycles, int*
     };
     int rc = residual();
     if (rc) return rc;
+    static const bool debug = getenv("OTM_DEBUG") != nullptr;
+    if (debug) fprintf(stderr, "[otm] solve start rel %.3e %.3e %.3e\n", rel[0], rel[1], rel[2]);
     bool zero_load[3];
     for (int c = 0; c < 3; ++c) zero_load[c] = fnorm[c] == 0.0;
     int status = OTM_OK;
@@ -699,8 +702,13 @@ int otm_solve(otm_ctx* ctx, const double* fext, double tol, int max_cycles, int*
         }
         launch_Tupd(s, 3 * n, ctx->T64, ctx->d);
         ctx->launches++;
+        const double inner_rr[3] = {ctx->h[3], ctx->h[4], ctx->h[5]};
         rc = residual();
         if (rc) return rc;
+        if (debug)
+            fprintf(stderr, "[otm]   outer: cycles %d  inner-est %.3e %.3e %.3e  true rel %.3e %.3e %.3e\n", cycles,
+                    std::sqrt(inner_rr[0]) / fnorm[0], std::sqrt(inner_rr[1]) / fnorm[1],
+                    std::sqrt(inner_rr[2]) / fnorm[2], rel[0], rel[1], rel[2]);
     }
     // mean-free T (solver.py:398); zero loads short-circuit to T = 0 (solver.py:382-385)
     launch_submean(s, n, ctx->T64, ctx->scal + 6);

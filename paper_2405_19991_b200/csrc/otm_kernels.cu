@@ -3,8 +3,11 @@
 // (paths relative to /root/reference/pkg/src/opentm/).
 #include "otm_common.cuh"
 #include "otm_internal.h"
+#include "otm_stencil2.cuh"
 
 #include <math.h>
+
+#include <algorithm>
 
 namespace otm {
 
@@ -181,39 +184,41 @@ __global__ void k_dinv(Geo g, const float* __restrict__ k, float kdiag, float* _
 // Coarsest level: assemble the dense periodic matrix (solver.py:278-296), invert
 // the vertex-0-pinned block (solver.py:298-305), and fold the mean projections of
 // coarse_solve (solver.py:307-324) into one symmetric matrix G = P Z P so the
-// per-cycle coarse solve is a dense mat-vec.  One block; A, Z in `work` (2 n^2).
-__global__ void k_coarse_setup(Geo g, const float* __restrict__ k, CoarseTemplate ct,
-                               double* __restrict__ work, float* __restrict__ G) {
+// per-cycle coarse solve is a dense mat-vec.  One block; A and Z live in shared
+// memory when they fit (n <= 64, the default chain) and in `work` otherwise.
+__global__ void __launch_bounds__(1024) k_coarse_setup(Geo g, const float* __restrict__ k, CoarseTemplate ct,
+                                                       double* __restrict__ work, float* __restrict__ G,
+                                                       int use_smem) {
+    extern __shared__ double sm[];
     const int n = (int)g.n;
-    double* A = work;
-    double* Z = work + (size_t)n * n;
-    for (int i = threadIdx.x; i < n * n; i += blockDim.x) A[i] = 0.0;
+    double* A = use_smem ? sm : work;
+    double* Z = A + (size_t)n * n;
+    for (int i = threadIdx.x; i < 2 * n * n; i += blockDim.x) A[i] = 0.0;
     __syncthreads();
-    // element loop: element e couples its 8 corners with kt[a^b] * k_e
-    if (threadIdx.x == 0) {
-        for (int e = 0; e < n; ++e) {
-            const int x = e / g.pl, rem = e - x * g.pl, y = rem / g.nz, z = rem - y * g.nz;
-            int vid[8];
-            for (int a = 0; a < 8; ++a) {
-                const int xx = (x + (a & 1)) % g.nx, yy = (y + ((a >> 1) & 1)) % g.ny,
-                          zz = (z + ((a >> 2) & 1)) % g.nz;
-                vid[a] = (xx * g.ny + yy) * g.nz + zz;
+    // row-wise assembly: row r couples through its 8 incident elements (no races)
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+        const int x = r / g.pl, rem = r - x * g.pl, y = rem / g.nz, z = rem - y * g.nz;
+        for (int a = 0; a < 8; ++a) {
+            const int ex = (x - (a & 1) + g.nx) % g.nx, ey = (y - ((a >> 1) & 1) + g.ny) % g.ny,
+                      ez = (z - ((a >> 2) & 1) + g.nz) % g.nz;
+            const double ke = (double)k[(ex * g.ny + ey) * g.nz + ez];
+            for (int b = 0; b < 8; ++b) {
+                const int cx = (ex + (b & 1)) % g.nx, cy = (ey + ((b >> 1) & 1)) % g.ny,
+                          cz = (ez + ((b >> 2) & 1)) % g.nz;
+                A[(size_t)r * n + (cx * g.ny + cy) * g.nz + cz] += ke * ct.kt[a ^ b];
             }
-            const double ke = (double)k[e];
-            for (int a = 0; a < 8; ++a)
-                for (int b = 0; b < 8; ++b) A[(size_t)vid[a] * n + vid[b]] += ke * ct.kt[a ^ b];
         }
     }
-    __syncthreads();
-    // Gauss-Jordan on the SPD block A[1:,1:] (no pivoting needed), result in Z[1:,1:]
-    const int m = n - 1;
     for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
         const int r = i / n, c = i - (i / n) * n;
         Z[i] = (r == c && r > 0) ? 1.0 : 0.0;
     }
     __syncthreads();
+    // Gauss-Jordan on the SPD block A[1:,1:] (no pivoting needed)
+    const int m = n - 1;
+    __shared__ double piv;
     for (int p = 1; p <= m; ++p) {
-        const double piv = A[(size_t)p * n + p];
+        if (threadIdx.x == 0) piv = A[(size_t)p * n + p];
         __syncthreads();
         for (int c = 1 + threadIdx.x; c < n; c += blockDim.x) {
             A[(size_t)p * n + c] /= piv;
@@ -232,8 +237,8 @@ __global__ void k_coarse_setup(Geo g, const float* __restrict__ k, CoarseTemplat
             if (r != p) A[(size_t)r * n + p] = 0.0;
         __syncthreads();
     }
-    // G = P Z P with P = I - 11^T/n: row means, column means, grand mean of Z
-    double* rmean = A;              // reuse A's storage (n doubles each)
+    // G = P Z P with P = I - 11^T/n
+    double* rmean = A;
     double* cmean = A + n;
     __shared__ double gmean;
     for (int r = threadIdx.x; r < n; r += blockDim.x) {
@@ -598,28 +603,56 @@ __global__ void __launch_bounds__(128) k_spmv(Geo g, int xb, LevelTemplate lt, c
     }
 }
 
-// p = z + beta p
+// p = z + beta p   (float4: n is a multiple of 4 on every level >= 4^3; scalar tail otherwise)
 __global__ void k_pupd(long long n, const float* __restrict__ z, float* __restrict__ p, const PcgScalars* sc) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 3 * n) return;
-    const int c = (int)(i / n);
-    p[i] = z[i] + (float)sc->beta[c] * p[i];
+    const long long n4 = n >> 2;
+    const float b[3] = {(float)sc->beta[0], (float)sc->beta[1], (float)sc->beta[2]};
+    if (i < n4) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const float4 zv = __ldg(reinterpret_cast<const float4*>(z + c * n) + i);
+            float4* pp = reinterpret_cast<float4*>(p + c * n) + i;
+            const float4 pv = *pp;
+            *pp = make_float4(zv.x + b[c] * pv.x, zv.y + b[c] * pv.y, zv.z + b[c] * pv.z, zv.w + b[c] * pv.w);
+        }
+    }
+    const long long t = (n4 << 2) + i;     // scalar tail
+    if (i < (n & 3)) {
+        for (int c = 0; c < 3; ++c) p[c * n + t] = z[c * n + t] + b[c] * p[c * n + t];
+    }
 }
 
 // d += alpha p ; r -= alpha q ; r.r partial sums -> convergence flags
-__global__ void k_upd(long long n, float* __restrict__ d, float* __restrict__ r, const float* __restrict__ p,
-                      const float* __restrict__ q, double* partials, unsigned* counter, PcgScalars* sc) {
+__global__ void __launch_bounds__(256) k_upd(long long n, float* __restrict__ d, float* __restrict__ r,
+                                             const float* __restrict__ p, const float* __restrict__ q,
+                                             double* partials, unsigned* counter, PcgScalars* sc) {
     double acc[3] = {0.0, 0.0, 0.0};
     const float al[3] = {(float)sc->alpha[0], (float)sc->alpha[1], (float)sc->alpha[2]};
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long n4 = n >> 2;
+    if (i < n4) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const long long j = c * n + i;
-            d[j] += al[c] * p[j];
-            const float rn = r[j] - al[c] * q[j];
-            r[j] = rn;
-            acc[c] += (double)rn * (double)rn;
+            const float4 pv = __ldg(reinterpret_cast<const float4*>(p + c * n) + i);
+            const float4 qv = __ldg(reinterpret_cast<const float4*>(q + c * n) + i);
+            float4* dp = reinterpret_cast<float4*>(d + c * n) + i;
+            float4* rp = reinterpret_cast<float4*>(r + c * n) + i;
+            float4 dv = *dp, rv = *rp;
+            dv.x += al[c] * pv.x; dv.y += al[c] * pv.y; dv.z += al[c] * pv.z; dv.w += al[c] * pv.w;
+            rv.x -= al[c] * qv.x; rv.y -= al[c] * qv.y; rv.z -= al[c] * qv.z; rv.w -= al[c] * qv.w;
+            *dp = dv;
+            *rp = rv;
+            acc[c] += ((double)rv.x * rv.x + (double)rv.y * rv.y) + ((double)rv.z * rv.z + (double)rv.w * rv.w);
+        }
+    }
+    if (i < (n & 3)) {
+        const long long t = (n4 << 2) + i;
+        for (int c = 0; c < 3; ++c) {
+            d[c * n + t] += al[c] * p[c * n + t];
+            const float rn = r[c * n + t] - al[c] * q[c * n + t];
+            r[c * n + t] = rn;
+            acc[c] += (double)rn * rn;
         }
     }
     if (reduce_finalize<3>(acc, partials, counter, sc->red + 6)) {
@@ -849,6 +882,173 @@ __global__ void k_oc_apply(long long n, const double* __restrict__ rho, const do
 }
 
 // ===========================================================================
+// Fast-path level stencils (otm_stencil2.cuh): one case x two z per thread
+// ===========================================================================
+struct OpF {           // plain fp32 operand a[c*n+v], factors kap[v]
+    const float* a; const float* kap; long long n;
+    __device__ __forceinline__ float t1(int c, long long v) const { return __ldg(a + c * n + v); }
+    __device__ __forceinline__ float2 t2(int c, long long v) const {
+        return __ldg(reinterpret_cast<const float2*>(a + c * n + v));
+    }
+    __device__ __forceinline__ float k1(long long v) const { return __ldg(kap + v); }
+    __device__ __forceinline__ float2 k2(long long v) const { return __ldg(reinterpret_cast<const float2*>(kap + v)); }
+};
+
+struct OpSmoothRes2 : OpF {   // operand = omega * dinv * f (Jacobi sweep from zero)
+    const float* dinv; float omega; float* z; float* res;
+    __device__ __forceinline__ float t1(int c, long long v) const {
+        return omega * __ldg(dinv + v) * __ldg(a + c * n + v);
+    }
+    __device__ __forceinline__ float2 t2(int c, long long v) const {
+        const float2 f = __ldg(reinterpret_cast<const float2*>(a + c * n + v));
+        const float2 d = __ldg(reinterpret_cast<const float2*>(dinv + v));
+        return make_float2(omega * d.x * f.x, omega * d.y * f.y);
+    }
+    __device__ __forceinline__ void sink(int c, long long v, const float (&kz)[2], const float (&zc)[2],
+                                         const float (&)[2][2][4]) {
+        const float2 f = __ldg(reinterpret_cast<const float2*>(a + c * n + v));
+        *reinterpret_cast<float2*>(z + c * n + v) = make_float2(zc[0], zc[1]);
+        *reinterpret_cast<float2*>(res + c * n + v) = make_float2(f.x - kz[0], f.y - kz[1]);
+    }
+};
+
+template <bool DOT>
+struct OpJacobi2 : OpF {      // operand = z ; zout = z + omega dinv (f - K z)
+    const float* f; const float* dinv; float omega; float* zout; double acc;
+    __device__ __forceinline__ void sink(int c, long long v, const float (&kz)[2], const float (&zc)[2],
+                                         const float (&)[2][2][4]) {
+        const float2 fv = __ldg(reinterpret_cast<const float2*>(f + c * n + v));
+        const float2 d = __ldg(reinterpret_cast<const float2*>(dinv + v));
+        const float z0 = zc[0] + omega * d.x * (fv.x - kz[0]);
+        const float z1 = zc[1] + omega * d.y * (fv.y - kz[1]);
+        *reinterpret_cast<float2*>(zout + c * n + v) = make_float2(z0, z1);
+        if (DOT) acc += (double)fv.x * (double)z0 + (double)fv.y * (double)z1;
+    }
+};
+
+struct OpSpmv2 : OpF {        // q = K p ; acc = p.q
+    float* q; double acc;
+    __device__ __forceinline__ void sink(int c, long long v, const float (&kp)[2], const float (&pc)[2],
+                                         const float (&)[2][2][4]) {
+        *reinterpret_cast<float2*>(q + c * n + v) = make_float2(kp[0], kp[1]);
+        acc += (double)pc[0] * (double)kp[0] + (double)pc[1] * (double)kp[1];
+    }
+};
+
+struct OpRes64 {              // fp64 defect r = (f(kappa) - fmean) - K T
+    const double* T; const double* kap; const double* fext; const double* fmean; float* r32; long long n;
+    const double* f0; double acc[3];
+    __device__ __forceinline__ double t1(int c, long long v) const { return __ldg(T + c * n + v); }
+    __device__ __forceinline__ double2 t2(int c, long long v) const {
+        return __ldg(reinterpret_cast<const double2*>(T + c * n + v));
+    }
+    __device__ __forceinline__ double k1(long long v) const { return __ldg(kap + v); }
+    __device__ __forceinline__ double2 k2(long long v) const { return __ldg(reinterpret_cast<const double2*>(kap + v)); }
+    __device__ __forceinline__ void sink(int c, long long v, const double (&kt)[2], const double (&tc)[2],
+                                         const double (&ks)[2][2][4]) {
+        double fv[2];
+        if (fext) {
+            const double2 e = __ldg(reinterpret_cast<const double2*>(fext + c * n + v));
+            fv[0] = e.x; fv[1] = e.y;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                double f = 0.0;
+#pragma unroll
+                for (int a = 0; a < 8; ++a) {
+                    const int q = 1 - (a & 1), jj = 1 - ((a >> 1) & 1), kk = 1 - ((a >> 2) & 1);
+                    f = __dadd_rn(f, __dmul_rn(f0[a * 3 + c], ks[i][q][jj * 2 + kk]));
+                }
+                fv[i] = f;
+            }
+        }
+        const double fm = fmean[c];
+        const double r0 = (fv[0] - fm) - kt[0], r1 = (fv[1] - fm) - kt[1];
+        *reinterpret_cast<float2*>(r32 + c * n + v) = make_float2((float)r0, (float)r1);
+        acc[0] += r0 * r0 + r1 * r1;
+        acc[1] += fv[0] * fv[0] + fv[1] * fv[1];
+        acc[2] += tc[0] + tc[1];
+    }
+};
+
+__global__ void __launch_bounds__(256, 3) k2_smooth_res(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
+                                                        const float* f, const float* dinv, float omega, float* z,
+                                                        float* res) {
+    OpSmoothRes2 op;
+    op.a = f; op.kap = kap; op.n = g.n; op.dinv = dinv; op.omega = omega; op.z = z; op.res = res;
+    march2<float>(g, xb, nch, lt, op);
+}
+
+template <bool DOT>
+__global__ void __launch_bounds__(256, 3) k2_jacobi(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
+                                                    const float* z, const float* f, const float* dinv, float omega,
+                                                    float* zout, double* partials, unsigned* counter,
+                                                    PcgScalars* sc) {
+    OpJacobi2<DOT> op;
+    op.a = z; op.kap = kap; op.n = g.n; op.f = f; op.dinv = dinv; op.omega = omega; op.zout = zout; op.acc = 0.0;
+    march2<float>(g, xb, nch, lt, op);
+    if (DOT) {
+        double v3[3] = {0.0, 0.0, 0.0};
+        const int c = blockIdx.z / nch;
+        v3[c] = op.acc;
+        if (reduce_finalize<3>(v3, partials, counter, sc->red)) {
+            for (int cc = 0; cc < 3; ++cc) {
+                const double rz = sc->red[cc];
+                sc->beta[cc] = (sc->first || sc->rz[cc] == 0.0) ? 0.0 : rz / sc->rz[cc];
+                sc->rz[cc] = rz;
+            }
+            sc->first = 0;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256, 3) k2_spmv(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
+                                                  const float* p, float* q, double* partials, unsigned* counter,
+                                                  PcgScalars* sc) {
+    OpSpmv2 op;
+    op.a = p; op.kap = kap; op.n = g.n; op.q = q; op.acc = 0.0;
+    march2<float>(g, xb, nch, lt, op);
+    double v3[3] = {0.0, 0.0, 0.0};
+    v3[blockIdx.z / nch] = op.acc;
+    if (reduce_finalize<3>(v3, partials, counter, sc->red + 3)) {
+        for (int c = 0; c < 3; ++c) {
+            const double pq = sc->red[3 + c];
+            sc->pq[c] = pq;
+            sc->alpha[c] = (sc->active[c] != 0.0 && pq > 0.0) ? sc->rz[c] / pq : 0.0;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256, 2) k2_res64(Geo g, int xb, int nch, LevelTemplate lt, const double* kap,
+                                                   const double* T, const double* fext, const double* fmean,
+                                                   float* r32, double* partials, unsigned* counter, double* out9) {
+    OpRes64 op;
+    op.T = T; op.kap = kap; op.fext = fext; op.fmean = fmean; op.r32 = r32; op.n = g.n; op.f0 = lt.f0;
+    op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
+    march2<double>(g, xb, nch, lt, op);
+    double v9[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) v9[i] = 0.0;
+    const int c = blockIdx.z / nch;
+    v9[c] = op.acc[0];
+    v9[3 + c] = op.acc[1];
+    v9[6 + c] = op.acc[2];
+    reduce_finalize<9>(v9, partials, counter, out9);
+}
+
+static inline dim3 fast_grid(const Geo& g, int xb, int* nch) {
+    *nch = (g.nx + xb - 1) / xb;
+    return dim3((unsigned)(g.nz / kTileZ), (unsigned)(g.ny / kTileY), (unsigned)(3 * *nch));
+}
+static inline int fast_xb(const Geo& g) {
+    // about 3.5 waves of 3 x 148 resident blocks, but never fewer than 4 planes per chunk
+    const long long per_chunk = 3LL * (g.nz / kTileZ) * (g.ny / kTileY);
+    long long chunks = (4LL * 3 * 148 + per_chunk - 1) / per_chunk;
+    int xb = (int)((g.nx + chunks - 1) / chunks);
+    return xb < 4 ? (g.nx < 4 ? g.nx : 4) : xb;
+}
+
+// ===========================================================================
 // Host launchers
 // ===========================================================================
 
@@ -924,13 +1124,26 @@ void launch_dinv(cudaStream_t s, const Geo& g, const float* k, float kdiag, floa
 }
 void launch_coarse_setup(cudaStream_t s, const Geo& g, const float* k, const CoarseTemplate& ct, double* work,
                          float* G) {
-    k_coarse_setup<<<1, 1024, 0, s>>>(g, k, ct, work, G);
+    const size_t bytes = 2 * (size_t)g.n * g.n * sizeof(double);
+    const int use_smem = bytes <= 96 * 1024;
+    if (use_smem) {
+        cudaFuncSetAttribute(k_coarse_setup, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    }
+    k_coarse_setup<<<1, 1024, use_smem ? bytes : 0, s>>>(g, k, ct, work, G, use_smem);
 }
 void launch_coarse_solve(cudaStream_t s, int n, const float* G, const float* f, float* z) {
     k_coarse_solve<<<1, 256, 0, s>>>(n, G, f, z);
 }
 void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
                   const double* fext, const double* fmean, float* r32, Red& red, double* out9) {
+    if (fast_tiling(g)) {
+        int nch;
+        const int xb = fast_xb(g);
+        const dim3 grid = fast_grid(g, xb, &nch);
+        k2_res64<<<grid, dim3(32, kTileY), 0, s>>>(g, xb, nch, lt, kap, T, fext, fmean, r32, red.partials,
+                                                   red.counter, out9);
+        return;
+    }
     int xb;
     const dim3 grid = stencil_grid(g, &xb);
     if (fext)
@@ -956,6 +1169,13 @@ void launch_sum3(cudaStream_t s, long long n, const double* f, Red& red, double*
 }
 void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* f,
                        const float* dinv, float omega, float* z, float* res) {
+    if (fast_tiling(g)) {
+        int nch;
+        const int xb = fast_xb(g);
+        const dim3 grid = fast_grid(g, xb, &nch);
+        k2_smooth_res<<<grid, dim3(32, kTileY), 0, s>>>(g, xb, nch, lt, kap, f, dinv, omega, z, res);
+        return;
+    }
     int xb;
     const dim3 grid = stencil_grid(g, &xb);
     k_smooth_res<<<grid, 128, 0, s>>>(g, xb, lt, kap, f, dinv, omega, z, res);
@@ -963,6 +1183,18 @@ void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, co
 void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* z,
                    const float* f, const float* dinv, float omega, float* zout, bool dot, Red& red,
                    PcgScalars* sc) {
+    if (fast_tiling(g)) {
+        int nch;
+        const int xb = fast_xb(g);
+        const dim3 grid = fast_grid(g, xb, &nch);
+        if (dot)
+            k2_jacobi<true><<<grid, dim3(32, kTileY), 0, s>>>(g, xb, nch, lt, kap, z, f, dinv, omega, zout,
+                                                              red.partials, red.counter, sc);
+        else
+            k2_jacobi<false><<<grid, dim3(32, kTileY), 0, s>>>(g, xb, nch, lt, kap, z, f, dinv, omega, zout,
+                                                               nullptr, nullptr, sc);
+        return;
+    }
     int xb;
     const dim3 grid = stencil_grid(g, &xb);
     if (dot)
@@ -972,18 +1204,25 @@ void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const 
 }
 void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* p,
                  float* q, Red& red, PcgScalars* sc) {
+    if (fast_tiling(g)) {
+        int nch;
+        const int xb = fast_xb(g);
+        const dim3 grid = fast_grid(g, xb, &nch);
+        k2_spmv<<<grid, dim3(32, kTileY), 0, s>>>(g, xb, nch, lt, kap, p, q, red.partials, red.counter, sc);
+        return;
+    }
     int xb;
     const dim3 grid = stencil_grid(g, &xb);
     k_spmv<<<grid, 128, 0, s>>>(g, xb, lt, kap, p, q, red.partials, red.counter, sc);
 }
 void launch_pupd(cudaStream_t s, long long n, const float* z, float* p, const PcgScalars* sc) {
-    k_pupd<<<nblk(3 * n, 256), 256, 0, s>>>(n, z, p, sc);
+    const long long th = std::max<long long>(n >> 2, n & 3);
+    k_pupd<<<nblk(th, 256), 256, 0, s>>>(n, z, p, sc);
 }
 void launch_upd(cudaStream_t s, long long n, float* d, float* r, const float* p, const float* q, Red& red,
                 PcgScalars* sc) {
-    long long want = (n + 255) / 256;
-    unsigned blocks = (unsigned)(want < 1184 ? want : 1184);
-    k_upd<<<blocks, 256, 0, s>>>(n, d, r, p, q, red.partials, red.counter, sc);
+    const long long th = std::max<long long>(n >> 2, n & 3);
+    k_upd<<<nblk(th, 256), 256, 0, s>>>(n, d, r, p, q, red.partials, red.counter, sc);
 }
 void launch_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* res, float* fc) {
     k_restrict<<<nblk(c.n, 256), 256, 0, s>>>(f, c, cf[0], cf[1], cf[2], res, fc);

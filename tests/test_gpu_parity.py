@@ -319,3 +319,20 @@ def test_already_optimal(otm):
     cfg = otm.RunConfig(dims=(8, 8, 8), target=otm.ObjectiveSpec("mse", otm.ConductivityTensor([k, k, k, 0, 0, 0])),
                         material=mp, init_field=np.full((8, 8, 8), 0.5), max_iter=5)
     assert otm.run_optimization(cfg).log[0].g < 1e-9
+
+
+@pytest.mark.parametrize("dims", [(8, 8, 64), (12, 16, 128), (64, 64, 64)])
+def test_fast_path_solve_vs_oracle(otm, O, dims):
+    """Grids whose z/y extents take the vectorised stencil path (nz % 64 == 0, ny % 8 == 0)."""
+    rng = np.random.default_rng(sum(dims))
+    rho = rng.uniform(0.05, 1.0, dims)
+    mp = otm.MaterialParams()
+    h = otm.GridHierarchy(dims)
+    T, cyc = otm.solve_cases(h, rho, mp, tol=1e-9)
+    ho = O.Hierarchy(dims)
+    To, _ = O.solve_three(ho, rho, O.Material(), tol=1e-11)
+    for i in range(3):
+        assert np.abs(T[i] - To[i]).max() <= 1e-6 * np.abs(To[i]).max()
+    res = otm.effective_tensor(h, T, rho, mp)
+    kh = O.tensor_from_energies(O.pair_energies(To), rho, O.Material())
+    assert np.abs(res.tensor.vec - kh).max() <= 1e-10 * np.linalg.norm(kh)
