@@ -43,11 +43,19 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// Block-wide sums of NQ values; result valid in thread 0.  smem: >= 32*NQ doubles.
+// Block-wide sums of NQ values; result valid in (linear) thread 0.  smem: >= 32*NQ doubles.
+__device__ __forceinline__ int block_tid() {
+    return threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+}
+__device__ __forceinline__ int block_threads() { return blockDim.x * blockDim.y * blockDim.z; }
+
+// (works for 1-, 2- and 3-D blocks: threads are linearised x-fastest, so warps
+// are consecutive linear indices)
 template <int NQ>
 __device__ __forceinline__ void block_sum(double (&v)[NQ], double* smem) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int nw = (blockDim.x + 31) >> 5;
+    const int tid = block_tid();
+    const int lane = tid & 31, wid = tid >> 5;
+    const int nw = (block_threads() + 31) >> 5;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
         double s = warp_sum(v[q]);
@@ -74,8 +82,9 @@ __device__ bool reduce_finalize(double (&v)[NQ], double* partials, unsigned* cou
     __shared__ bool is_last;
     const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
     const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const int tid = block_tid();
     block_sum<NQ>(v, smem);
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
 #pragma unroll
         for (int q = 0; q < NQ; ++q) partials[(size_t)bid * NQ + q] = v[q];
         __threadfence();
@@ -87,12 +96,12 @@ __device__ bool reduce_finalize(double (&v)[NQ], double* partials, unsigned* cou
     double acc[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
-    for (unsigned b = threadIdx.x; b < nb; b += blockDim.x) {
+    for (unsigned b = tid; b < nb; b += block_threads()) {
 #pragma unroll
         for (int q = 0; q < NQ; ++q) acc[q] += __ldcg(partials + (size_t)b * NQ + q);
     }
     block_sum<NQ>(acc, smem);
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
 #pragma unroll
         for (int q = 0; q < NQ; ++q) out[q] = acc[q];
         *counter = 0u;
