@@ -12,7 +12,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libotm.so")
+LIB_PATH = os.environ.get("OTM_LIB", os.path.join(_HERE, "libotm.so"))
 
 OTM_OK, OTM_EINVAL, OTM_ENOCONV, OTM_ECUDA, OTM_ESTATE = 0, 1, 2, 3, 4
 

@@ -374,8 +374,8 @@ void otm_default_params(otm_params* p) {
     p->coarse_target = 64;
     p->direct_limit = 40000;
     p->jacobi_omega = 0.8;
-    p->inner_reduction = 1e-4;
-    p->max_inner = 100;
+    p->inner_reduction = 1e-7;
+    p->max_inner = 60;
     p->device = 0;
 }
 

@@ -5,6 +5,10 @@
 #include "otm_internal.h"
 #include "otm_stencil2.cuh"
 
+#ifndef OTM_MINB
+#define OTM_MINB 2   // min resident blocks of the fp32 fast-path stencils (register cap 128)
+#endif
+
 #include <math.h>
 
 #include <algorithm>
@@ -905,7 +909,7 @@ struct OpSmoothRes2 : OpF {   // operand = omega * dinv * f (Jacobi sweep from z
         return make_float2(omega * d.x * f.x, omega * d.y * f.y);
     }
     __device__ __forceinline__ void sink(int c, long long v, const float (&kz)[2], const float (&zc)[2],
-                                         const float (&)[2][2][4]) {
+                                         const float (&)[2][3], const float (&)[2][3]) {
         const float2 f = __ldg(reinterpret_cast<const float2*>(a + c * n + v));
         *reinterpret_cast<float2*>(z + c * n + v) = make_float2(zc[0], zc[1]);
         *reinterpret_cast<float2*>(res + c * n + v) = make_float2(f.x - kz[0], f.y - kz[1]);
@@ -916,7 +920,7 @@ template <bool DOT>
 struct OpJacobi2 : OpF {      // operand = z ; zout = z + omega dinv (f - K z)
     const float* f; const float* dinv; float omega; float* zout; double acc;
     __device__ __forceinline__ void sink(int c, long long v, const float (&kz)[2], const float (&zc)[2],
-                                         const float (&)[2][2][4]) {
+                                         const float (&)[2][3], const float (&)[2][3]) {
         const float2 fv = __ldg(reinterpret_cast<const float2*>(f + c * n + v));
         const float2 d = __ldg(reinterpret_cast<const float2*>(dinv + v));
         const float z0 = zc[0] + omega * d.x * (fv.x - kz[0]);
@@ -929,7 +933,7 @@ struct OpJacobi2 : OpF {      // operand = z ; zout = z + omega dinv (f - K z)
 struct OpSpmv2 : OpF {        // q = K p ; acc = p.q
     float* q; double acc;
     __device__ __forceinline__ void sink(int c, long long v, const float (&kp)[2], const float (&pc)[2],
-                                         const float (&)[2][2][4]) {
+                                         const float (&)[2][3], const float (&)[2][3]) {
         *reinterpret_cast<float2*>(q + c * n + v) = make_float2(kp[0], kp[1]);
         acc += (double)pc[0] * (double)kp[0] + (double)pc[1] * (double)kp[1];
     }
@@ -945,7 +949,7 @@ struct OpRes64 {              // fp64 defect r = (f(kappa) - fmean) - K T
     __device__ __forceinline__ double k1(long long v) const { return __ldg(kap + v); }
     __device__ __forceinline__ double2 k2(long long v) const { return __ldg(reinterpret_cast<const double2*>(kap + v)); }
     __device__ __forceinline__ void sink(int c, long long v, const double (&kt)[2], const double (&tc)[2],
-                                         const double (&ks)[2][2][4]) {
+                                         const double (&K0)[2][3], const double (&K1)[2][3]) {
         double fv[2];
         if (fext) {
             const double2 e = __ldg(reinterpret_cast<const double2*>(fext + c * n + v));
@@ -957,7 +961,8 @@ struct OpRes64 {              // fp64 defect r = (f(kappa) - fmean) - K T
 #pragma unroll
                 for (int a = 0; a < 8; ++a) {
                     const int q = 1 - (a & 1), jj = 1 - ((a >> 1) & 1), kk = 1 - ((a >> 2) & 1);
-                    f = __dadd_rn(f, __dmul_rn(f0[a * 3 + c], ks[i][q][jj * 2 + kk]));
+                    const double ke = q == 0 ? K0[jj][i + kk] : K1[jj][i + kk];
+                    f = __dadd_rn(f, __dmul_rn(f0[a * 3 + c], ke));
                 }
                 fv[i] = f;
             }
@@ -971,7 +976,7 @@ struct OpRes64 {              // fp64 defect r = (f(kappa) - fmean) - K T
     }
 };
 
-__global__ void __launch_bounds__(256, 3) k2_smooth_res(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
+__global__ void __launch_bounds__(256, OTM_MINB) k2_smooth_res(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
                                                         const float* f, const float* dinv, float omega, float* z,
                                                         float* res) {
     OpSmoothRes2 op;
@@ -980,7 +985,7 @@ __global__ void __launch_bounds__(256, 3) k2_smooth_res(Geo g, int xb, int nch, 
 }
 
 template <bool DOT>
-__global__ void __launch_bounds__(256, 3) k2_jacobi(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
+__global__ void __launch_bounds__(256, OTM_MINB) k2_jacobi(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
                                                     const float* z, const float* f, const float* dinv, float omega,
                                                     float* zout, double* partials, unsigned* counter,
                                                     PcgScalars* sc) {
@@ -1002,7 +1007,7 @@ __global__ void __launch_bounds__(256, 3) k2_jacobi(Geo g, int xb, int nch, Leve
     }
 }
 
-__global__ void __launch_bounds__(256, 3) k2_spmv(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
+__global__ void __launch_bounds__(256, OTM_MINB) k2_spmv(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
                                                   const float* p, float* q, double* partials, unsigned* counter,
                                                   PcgScalars* sc) {
     OpSpmv2 op;
@@ -1136,7 +1141,7 @@ void launch_coarse_solve(cudaStream_t s, int n, const float* G, const float* f, 
 }
 void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
                   const double* fext, const double* fmean, float* r32, Red& red, double* out9) {
-    if (fast_tiling(g)) {
+    if (fast_tiling(g, lt)) {
         int nch;
         const int xb = fast_xb(g);
         const dim3 grid = fast_grid(g, xb, &nch);
@@ -1169,7 +1174,7 @@ void launch_sum3(cudaStream_t s, long long n, const double* f, Red& red, double*
 }
 void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* f,
                        const float* dinv, float omega, float* z, float* res) {
-    if (fast_tiling(g)) {
+    if (fast_tiling(g, lt)) {
         int nch;
         const int xb = fast_xb(g);
         const dim3 grid = fast_grid(g, xb, &nch);
@@ -1183,7 +1188,7 @@ void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, co
 void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* z,
                    const float* f, const float* dinv, float omega, float* zout, bool dot, Red& red,
                    PcgScalars* sc) {
-    if (fast_tiling(g)) {
+    if (fast_tiling(g, lt)) {
         int nch;
         const int xb = fast_xb(g);
         const dim3 grid = fast_grid(g, xb, &nch);
@@ -1204,7 +1209,7 @@ void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const 
 }
 void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* p,
                  float* q, Red& red, PcgScalars* sc) {
-    if (fast_tiling(g)) {
+    if (fast_tiling(g, lt)) {
         int nch;
         const int xb = fast_xb(g);
         const dim3 grid = fast_grid(g, xb, &nch);
