@@ -76,6 +76,7 @@ struct otm_ctx {
     double* h = nullptr;         // pinned host mirror (256)
     int* changed = nullptr;      // device flag
     bool built = false;
+    bool no_loop_graph = false;
     bool warm = false;
     bool have_T = false;
     std::string err;
@@ -84,6 +85,7 @@ struct otm_ctx {
     // inner-iteration graphs (plain, profiled)
     cudaGraphExec_t gexec = nullptr;
     cudaGraphExec_t gexec_prof = nullptr;
+    cudaGraphExec_t gexec_loop = nullptr;     // whole inner loop: conditional WHILE node
     int launches_per_inner = 0;
     // profiling
     bool prof = false;
@@ -229,7 +231,7 @@ void prof_record(otm_ctx* ctx, int cls, double bytes, bool begin, int& slot_idx)
 }
 
 // Stream work of one inner PCG iteration (captured into a graph).
-int enqueue_inner(otm_ctx* ctx, bool prof) {
+int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false) {
     cudaStream_t s = ctx->stream;
     const int nl = (int)ctx->L.size();
     const float om = (float)ctx->P.jacobi_omega;
@@ -282,8 +284,8 @@ int enqueue_inner(otm_ctx* ctx, bool prof) {
     if (prof) prof_record(ctx, kProfL0Stencil, 0, false, sl);
     launch_upd(s, ctx->g0.n, ctx->d, ctx->r, ctx->p, ctx->q, ctx->red, ctx->sc);
     launches += 3;
-    cudaMemcpyAsync(ctx->h, ctx->sc->flags, 8 * sizeof(double), cudaMemcpyDeviceToHost, s);
-    ctx->launches_per_inner = launches;
+    if (!in_loop) cudaMemcpyAsync(ctx->h, ctx->sc->flags, 8 * sizeof(double), cudaMemcpyDeviceToHost, s);
+    ctx->launches_per_inner = launches + (in_loop ? 1 : 0);
     return OTM_OK;
 }
 
@@ -296,6 +298,32 @@ int capture_inner(otm_ctx* ctx, bool prof) {
     CK(cudaGraphInstantiate(&ex, graph, 0));
     cudaGraphDestroy(graph);
     if (prof) ctx->gexec_prof = ex; else ctx->gexec = ex;
+    return OTM_OK;
+}
+
+// The whole inner PCG loop as one graph: a conditional WHILE node whose body is
+// one iteration followed by k_loop_ctl, which decides on the device whether to
+// run again (no host round trip per iteration).
+int capture_loop(otm_ctx* ctx) {
+    cudaGraph_t g;
+    CK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    enqueue_inner(ctx, false, true);
+    launch_loop_ctl(ctx->stream, ctx->sc, (unsigned long long)h);
+    cudaGraph_t captured;
+    CK(cudaStreamEndCapture(ctx->stream, &captured));
+    CK(cudaGraphInstantiate(&ctx->gexec_loop, g, 0));
+    cudaGraphDestroy(g);
     return OTM_OK;
 }
 
@@ -374,8 +402,8 @@ void otm_default_params(otm_params* p) {
     p->coarse_target = 64;
     p->direct_limit = 40000;
     p->jacobi_omega = 0.8;
-    p->inner_reduction = 1e-7;
-    p->max_inner = 60;
+    p->inner_reduction = 1e-4;
+    p->max_inner = 40;
     p->device = 0;
 }
 
@@ -505,7 +533,7 @@ int otm_create(otm_ctx** out, int nx, int ny, int nz, const otm_params* pin) {
     CK(dalloc(ctx, &ctx->scal, 128));
     CK(cudaMemset(ctx->scal, 0, 128 * sizeof(double)));
     CK(dalloc(ctx, &ctx->changed, 4));
-    CK(cudaMallocHost((void**)&ctx->h, 256 * sizeof(double)));
+    CK(cudaMallocHost((void**)&ctx->h, 512 * sizeof(double)));
     CK(cudaMemset(ctx->T64, 0, 3 * n * sizeof(double)));
     CK(cudaMemset(ctx->p, 0, 3 * n * sizeof(float)));
     CK(cudaEventCreate(&ctx->ev_a));
@@ -518,6 +546,7 @@ int otm_destroy(otm_ctx* ctx) {
     if (!ctx) return OTM_OK;
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
     if (ctx->gexec_prof) cudaGraphExecDestroy(ctx->gexec_prof);
+    if (ctx->gexec_loop) cudaGraphExecDestroy(ctx->gexec_loop);
     for (auto& s : ctx->slots) { cudaEventDestroy(s.a); cudaEventDestroy(s.b); }
     auto F = [](void* p) { if (p) cudaFree(p); };
     F(ctx->kap64); F(ctx->T64); F(ctx->rho_f); F(ctx->sensf); F(ctx->sens); F(ctx->r); F(ctx->p); F(ctx->q); F(ctx->d);
@@ -642,6 +671,10 @@ int otm_solve(otm_ctx* ctx, const double* fext, double tol, int max_cycles, int*
     cudaStream_t s = ctx->stream;
     const long long n = ctx->g0.n;
     if (!ctx->gexec) { int rc = capture_inner(ctx, false); if (rc) return rc; }
+    if (!ctx->gexec_loop && !ctx->no_loop_graph) {
+        int rc = capture_loop(ctx);
+        if (rc) { ctx->no_loop_graph = true; cudaGetLastError(); }
+    }
     if (ctx->prof && !ctx->gexec_prof) { int rc = capture_inner(ctx, true); if (rc) return rc; }
     double* fmean = ctx->scal + 16;
     if (fext) launch_sum3(s, n, fext, ctx->red, fmean);
@@ -686,11 +719,26 @@ int otm_solve(otm_ctx* ctx, const double* fext, double tol, int max_cycles, int*
             init.active[c] = done[c] ? 0.0 : 1.0;
         }
         init.first = 1;
+        init.it = 0;
+        init.max_it = ctx->P.max_inner;
+        init.cycles = cycles;
+        init.max_cycles = max_cycles;
+        init.nact = (int)!done[0] + (int)!done[1] + (int)!done[2];
         std::memcpy(ctx->h + 64, &init, sizeof init);
         CK(cudaMemcpyAsync(ctx->sc, ctx->h + 64, sizeof init, cudaMemcpyHostToDevice, s));
         CK(cudaMemsetAsync(ctx->d, 0, 3 * n * sizeof(float), s));
         CK(cudaMemsetAsync(ctx->p, 0, 3 * n * sizeof(float), s));
         int active_n = (int)!done[0] + (int)!done[1] + (int)!done[2];
+        if (ctx->gexec_loop && !ctx->prof) {
+            CK(cudaGraphLaunch(ctx->gexec_loop, s));
+            CK(cudaMemcpyAsync(ctx->h + 160, ctx->sc, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            PcgScalars fin;
+            std::memcpy(&fin, ctx->h + 160, sizeof fin);
+            ctx->launches += (long long)fin.it * ctx->launches_per_inner;
+            cycles = fin.cycles;
+            for (int k = 0; k < 6; ++k) ctx->h[k] = fin.flags[k];
+        } else
         for (int it = 0; it < ctx->P.max_inner; ++it) {
             CK(cudaGraphLaunch(ctx->prof ? ctx->gexec_prof : ctx->gexec, s));
             ctx->launches += ctx->launches_per_inner;

@@ -45,9 +45,13 @@ struct PcgScalars {
     double red[16];
     double rz[3], beta[3], pq[3], alpha[3], rr[3], target2[3], active[3];
     double sumT[3];
-    double flags[8];     // copied to the host after every inner iteration
+    double flags[8];     // active[3], rr[3]: copied to the host after the inner loop
     int first;
-    int pad;
+    int it;              // device-side inner loop control (conditional graph node)
+    int max_it;
+    int cycles;          // preconditioner applications summed over active cases
+    int max_cycles;
+    int nact;            // cases active at the start of the current iteration
 };
 
 // Deterministic two-stage reduction workspace.
@@ -98,6 +102,7 @@ void launch_upd(cudaStream_t s, long long n, float* d, float* r, const float* p,
                 PcgScalars* sc);
 void launch_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* res, float* fc);
 void launch_prolong(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* zc, float* zf);
+void launch_loop_ctl(cudaStream_t s, PcgScalars* sc, unsigned long long handle);
 void launch_Tupd(cudaStream_t s, long long n3, double* T, const float* d);
 void launch_submean(cudaStream_t s, long long n, double* T, const double* sumT);
 void launch_tensor(cudaStream_t s, const Geo& g, const double* T, const double* kap, Red& red, double* out6);

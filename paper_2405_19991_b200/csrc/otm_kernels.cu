@@ -12,6 +12,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace otm {
 
@@ -731,6 +732,18 @@ __global__ void k_prolong(Geo f, Geo c, int cx, int cy, int cz, const float* __r
     }
 }
 
+// Inner-loop control, last node of the WHILE body: count the V-cycles spent, and
+// keep looping while a case is active and the budgets allow.
+__global__ void k_loop_ctl(PcgScalars* sc, cudaGraphConditionalHandle h) {
+    sc->cycles += sc->nact;
+    int nact = 0;
+    for (int c = 0; c < 3; ++c) nact += sc->active[c] != 0.0;
+    sc->nact = nact;
+    sc->it += 1;
+    const bool more = nact > 0 && sc->it < sc->max_it && sc->cycles < sc->max_cycles;
+    cudaGraphSetConditional(h, more ? 1u : 0u);
+}
+
 // T += d (fp64 accumulation of the fp32 correction)
 __global__ void k_Tupd(long long n3, double* __restrict__ T, const float* __restrict__ d) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1046,6 +1059,8 @@ static inline dim3 fast_grid(const Geo& g, int xb, int* nch) {
     return dim3((unsigned)(g.nz / kTileZ), (unsigned)(g.ny / kTileY), (unsigned)(3 * *nch));
 }
 static inline int fast_xb(const Geo& g) {
+    static const int env_xb = getenv("OTM_XB") ? atoi(getenv("OTM_XB")) : 0;   // tuning experiments
+    if (env_xb > 0) return env_xb < g.nx ? env_xb : g.nx;
     // about 3.5 waves of 3 x 148 resident blocks, but never fewer than 4 planes per chunk
     const long long per_chunk = 3LL * (g.nz / kTileZ) * (g.ny / kTileY);
     long long chunks = (4LL * 3 * 148 + per_chunk - 1) / per_chunk;
@@ -1234,6 +1249,9 @@ void launch_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3]
 }
 void launch_prolong(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* zc, float* zf) {
     k_prolong<<<nblk(f.n, 256), 256, 0, s>>>(f, c, cf[0], cf[1], cf[2], zc, zf);
+}
+void launch_loop_ctl(cudaStream_t s, PcgScalars* sc, unsigned long long handle) {
+    k_loop_ctl<<<1, 1, 0, s>>>(sc, (cudaGraphConditionalHandle)handle);
 }
 void launch_Tupd(cudaStream_t s, long long n3, double* T, const float* d) {
     k_Tupd<<<nblk(n3, 256), 256, 0, s>>>(n3, T, d);
