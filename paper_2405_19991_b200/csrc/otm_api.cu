@@ -77,6 +77,7 @@ struct otm_ctx {
     int* changed = nullptr;      // device flag
     bool built = false;
     bool no_loop_graph = false;
+    bool no_tail = getenv("OTM_NO_TAIL") != nullptr;
     bool warm = false;
     bool have_T = false;
     std::string err;
@@ -240,7 +241,12 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false) {
     int launches = 0;
     if (prof) prof_record(ctx, kProfVcycle, 0.0, true, sl_v);
     double vbytes = 0.0;
-    for (int l = 0; l + 1 < nl; ++l) {
+    // first level handled by the single-CTA tail (all coarser levels are tail too)
+    int tl = nl - 1;
+    while (tl > 0 && ctx->L[tl - 1].g.n <= kTailMaxVerts && nl - (tl - 1) <= kTailMaxLevels) --tl;
+    const bool use_tail = tl < nl - 1 && !ctx->no_tail;
+    const int top = use_tail ? tl : nl - 1;     // levels [0, top) are launched per level
+    for (int l = 0; l < top; ++l) {
         LevelBuf& A = ctx->L[l];
         LevelBuf& B = ctx->L[l + 1];
         const double bsm = 44.0 * (double)A.g.n;
@@ -251,12 +257,27 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false) {
         vbytes += bsm + 12.0 * A.g.n + 12.0 * B.g.n;
         launches += 2;
     }
-    {
+    if (use_tail) {
+        TailArgs ta;
+        ta.nlev = nl - tl;
+        ta.omega = om;
+        ta.G = ctx->G;
+        for (int k = 0; k < ta.nlev; ++k) {
+            const LevelBuf& B = ctx->L[tl + k];
+            TailLevel& T = ta.L[k];
+            T.g = B.g;
+            for (int a = 0; a < 3; ++a) T.cf[a] = B.cf[a];
+            T.lt = B.lt;
+            T.kap = B.kap; T.dinv = B.dinv; T.f = B.f; T.z = B.z; T.res = B.res;
+        }
+        launch_vtail(s, ta);
+        launches += 1;
+    } else {
         LevelBuf& C = ctx->L[nl - 1];
         launch_coarse_solve(s, (int)C.g.n, ctx->G, C.f, C.res);
         launches += 1;
     }
-    for (int l = nl - 2; l >= 0; --l) {
+    for (int l = top - 1; l >= 0; --l) {
         LevelBuf& A = ctx->L[l];
         LevelBuf& B = ctx->L[l + 1];
         launch_prolong(s, A.g, B.g, B.cf, B.res, A.z);
@@ -266,6 +287,12 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false) {
         if (prof && l == 0) prof_record(ctx, kProfL0Stencil, 0, false, sl);
         vbytes += 12.0 * B.g.n + 24.0 * A.g.n + bj;
         launches += 2;
+    }
+    if (use_tail && tl == 0) {
+        // the whole hierarchy fits the tail: r.z and beta still come from a level-0 pass
+        LevelBuf& A = ctx->L[0];
+        launch_jacobi(s, A.g, A.lt, A.kap, A.res, A.f, A.dinv, 0.0f, A.z, true, ctx->red, ctx->sc);
+        launches += 1;
     }
     if (nl == 1) {
         // single-level hierarchy: the coarse solve is the whole preconditioner; still need r.z
@@ -277,7 +304,7 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false) {
         prof_record(ctx, kProfVcycle, 0, false, sl_v);
         ctx->slots[sl_v].bytes = vbytes;
     }
-    float* z0 = nl == 1 ? ctx->L[0].z : ctx->L[0].res;
+    float* z0 = (nl == 1 || (use_tail && tl == 0)) ? ctx->L[0].z : ctx->L[0].res;
     launch_pupd(s, ctx->g0.n, z0, ctx->p, ctx->sc);
     if (prof) prof_record(ctx, kProfL0Stencil, 28.0 * n0, true, sl);
     launch_spmv(s, ctx->g0, ctx->L[0].lt, ctx->L[0].kap, ctx->p, ctx->q, ctx->red, ctx->sc);

@@ -68,7 +68,28 @@ struct FilterSetup {
     double* wts_dev;
 };
 
+// Tail of the V-cycle (all levels with few vertices) run by one CTA.
+constexpr int kTailMaxLevels = 6;
+constexpr int kTailMaxVerts = 4096;
+struct TailLevel {
+    Geo g;
+    int cf[3];            // axes coarsened from the finer level
+    LevelTemplate lt;
+    float* kap;
+    float* dinv;
+    float* f;
+    float* z;
+    float* res;
+};
+struct TailArgs {
+    int nlev;             // levels in the tail; the last one is the coarsest (direct solve)
+    float omega;
+    const float* G;
+    TailLevel L[kTailMaxLevels];
+};
+
 int stencil_chunks(const Geo& g, int* xb);
+void launch_vtail(cudaStream_t s, const TailArgs& a);
 
 void launch_filter(cudaStream_t s, const Geo& g, const FilterSetup& fs, int adjoint, const double* in,
                    double* out, Red& red);

@@ -4,6 +4,7 @@
 #include "otm_common.cuh"
 #include "otm_internal.h"
 #include "otm_stencil2.cuh"
+#include "otm_stencil3.cuh"
 
 #ifndef OTM_MINB
 #define OTM_MINB 2   // min resident blocks of the fp32 fast-path stencils (register cap 128)
@@ -1054,6 +1055,120 @@ __global__ void __launch_bounds__(256, 2) k2_res64(Geo g, int xb, int nch, Level
     reduce_finalize<9>(v9, partials, counter, out9);
 }
 
+// ---- shared-memory-ring versions (otm_stencil3.cuh) ----
+__device__ __forceinline__ const float* s3_at(const float* slot, int a, int r, int col) {
+    return slot + a * kS3Tile + r * kS3Pitch + col;
+}
+
+struct Op3SmoothRes {     // arrays: 0 = f (halo), 1 = D^-1 (halo); operand = w D^-1 f
+    float omega; float* z; float* res; long long n;
+    __device__ __forceinline__ float operand(const float* slot, int r, int col) const {
+        return omega * *s3_at(slot, 1, r, col) * *s3_at(slot, 0, r, col);
+    }
+    __device__ __forceinline__ void sink(const float* slot, int c, long long v, int r, int col, const float (&kz)[2],
+                                         const float (&zc)[2]) {
+        const float2 f = *reinterpret_cast<const float2*>(s3_at(slot, 0, r, col));
+        *reinterpret_cast<float2*>(z + c * n + v) = make_float2(zc[0], zc[1]);
+        *reinterpret_cast<float2*>(res + c * n + v) = make_float2(f.x - kz[0], f.y - kz[1]);
+    }
+};
+
+template <bool DOT>
+struct Op3Jacobi {        // arrays: 0 = z (halo), 1 = f (center), 2 = D^-1 (center)
+    float omega; float* zout; long long n; double acc;
+    __device__ __forceinline__ float operand(const float* slot, int r, int col) const { return *s3_at(slot, 0, r, col); }
+    __device__ __forceinline__ void sink(const float* slot, int c, long long v, int r, int col, const float (&kz)[2],
+                                         const float (&zc)[2]) {
+        const float2 fv = *reinterpret_cast<const float2*>(s3_at(slot, 1, r, col));
+        const float2 d = *reinterpret_cast<const float2*>(s3_at(slot, 2, r, col));
+        const float z0 = zc[0] + omega * d.x * (fv.x - kz[0]);
+        const float z1 = zc[1] + omega * d.y * (fv.y - kz[1]);
+        *reinterpret_cast<float2*>(zout + c * n + v) = make_float2(z0, z1);
+        if (DOT) acc += (double)fv.x * (double)z0 + (double)fv.y * (double)z1;
+    }
+};
+
+struct Op3Spmv {          // arrays: 0 = p (halo)
+    float* q; long long n; double acc;
+    __device__ __forceinline__ float operand(const float* slot, int r, int col) const { return *s3_at(slot, 0, r, col); }
+    __device__ __forceinline__ void sink(const float*, int c, long long v, int, int, const float (&kp)[2],
+                                         const float (&pc)[2]) {
+        *reinterpret_cast<float2*>(q + c * n + v) = make_float2(kp[0], kp[1]);
+        acc += (double)pc[0] * (double)kp[0] + (double)pc[1] * (double)kp[1];
+    }
+};
+
+__global__ void __launch_bounds__(256, 3) k3_smooth_res(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
+                                                        const float* f, const float* dinv, float omega, float* z,
+                                                        float* res) {
+    S3Setup<2> su;
+    su.arr[0] = S3Array{f, 1, S3Halo};
+    su.arr[1] = S3Array{dinv, 0, S3Halo};
+    su.kap = kap;
+    Op3SmoothRes op{omega, z, res, g.n};
+    march3<2>(g, xb, nch, lt, su, op);
+}
+
+template <bool DOT>
+__global__ void __launch_bounds__(256, 3) k3_jacobi(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
+                                                    const float* z, const float* f, const float* dinv, float omega,
+                                                    float* zout, double* partials, unsigned* counter,
+                                                    PcgScalars* sc) {
+    S3Setup<3> su;
+    su.arr[0] = S3Array{z, 1, S3Halo};
+    su.arr[1] = S3Array{f, 1, S3Center};
+    su.arr[2] = S3Array{dinv, 0, S3Center};
+    su.kap = kap;
+    Op3Jacobi<DOT> op{omega, zout, g.n, 0.0};
+    march3<3>(g, xb, nch, lt, su, op);
+    if (DOT) {
+        double v3[3] = {0.0, 0.0, 0.0};
+        v3[blockIdx.z / nch] = op.acc;
+        if (reduce_finalize<3>(v3, partials, counter, sc->red)) {
+            for (int cc = 0; cc < 3; ++cc) {
+                const double rz = sc->red[cc];
+                sc->beta[cc] = (sc->first || sc->rz[cc] == 0.0) ? 0.0 : rz / sc->rz[cc];
+                sc->rz[cc] = rz;
+            }
+            sc->first = 0;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256, 3) k3_spmv(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
+                                                  const float* p, float* q, double* partials, unsigned* counter,
+                                                  PcgScalars* sc) {
+    S3Setup<1> su;
+    su.arr[0] = S3Array{p, 1, S3Halo};
+    su.kap = kap;
+    Op3Spmv op{q, g.n, 0.0};
+    march3<1>(g, xb, nch, lt, su, op);
+    double v3[3] = {0.0, 0.0, 0.0};
+    v3[blockIdx.z / nch] = op.acc;
+    if (reduce_finalize<3>(v3, partials, counter, sc->red + 3)) {
+        for (int cc = 0; cc < 3; ++cc) {
+            const double pq = sc->red[3 + cc];
+            sc->pq[cc] = pq;
+            sc->alpha[cc] = (sc->active[cc] != 0.0 && pq > 0.0) ? sc->rz[cc] / pq : 0.0;
+        }
+    }
+}
+
+static inline int s3_xb(const Geo& g) {
+    static const int env_xb = getenv("OTM_XB3") ? atoi(getenv("OTM_XB3")) : 0;
+    int xb = env_xb > 0 ? env_xb : 16;
+    if (xb > g.nx) xb = g.nx;
+    return xb;
+}
+static bool s3_enabled() {
+    static const bool off = getenv("OTM_NO_S3") != nullptr;
+    return !off;
+}
+template <class K>
+static void s3_attr(K kernel, size_t bytes) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
 static inline dim3 fast_grid(const Geo& g, int xb, int* nch) {
     *nch = (g.nx + xb - 1) / xb;
     return dim3((unsigned)(g.nz / kTileZ), (unsigned)(g.ny / kTileY), (unsigned)(3 * *nch));
@@ -1066,6 +1181,127 @@ static inline int fast_xb(const Geo& g) {
     long long chunks = (4LL * 3 * 148 + per_chunk - 1) / per_chunk;
     int xb = (int)((g.nx + chunks - 1) / chunks);
     return xb < 4 ? (g.nx < 4 ? g.nx : 4) : xb;
+}
+
+// ===========================================================================
+// V-cycle tail in one CTA: every level with <= kTailMaxVerts vertices, from the
+// smoothing of the first tail level down to the coarse solve and back up.  The
+// phases are separated by block barriers (global writes of the block are visible
+// to the block after __syncthreads); plain loads, no read-only cache path.
+// ===========================================================================
+__device__ float tail_apply(const TailLevel& L, const float* src, int c, int v) {
+    const Geo& g = L.g;
+    const int x = v / g.pl, rem = v - x * g.pl, y = rem / g.nz, z = rem - y * g.nz;
+    const int xs[3] = {wrap_m(x, g.nx), x, wrap_p(x, g.nx)};
+    const int ys[3] = {wrap_m(y, g.ny), y, wrap_p(y, g.ny)};
+    const int zs[3] = {wrap_m(z, g.nz), z, wrap_p(z, g.nz)};
+    const float* a = src + (size_t)c * g.n;
+    float t[3][3][3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            for (int k = 0; k < 3; ++k) t[i][j][k] = a[(xs[i] * g.ny + ys[j]) * g.nz + zs[k]];
+    float acc = 0.f;
+    // elements (q, jj, kk) at (x-1+q, y-1+jj, z-1+kk); vertex is corner a = (1-q)|(1-jj)<<1|(1-kk)<<2
+    for (int q = 0; q < 2; ++q)
+        for (int jj = 0; jj < 2; ++jj)
+            for (int kk = 0; kk < 2; ++kk) {
+                const float ke = L.kap[(xs[q] * g.ny + ys[jj]) * g.nz + zs[kk]];
+                const int av = (1 - q) | ((1 - jj) << 1) | ((1 - kk) << 2);
+                float e = 0.f;
+                for (int b = 0; b < 8; ++b)
+                    e += (float)L.lt.kt[av ^ b] * t[q + (b & 1)][jj + ((b >> 1) & 1)][kk + ((b >> 2) & 1)];
+                acc += ke * e;
+            }
+    return acc;
+}
+
+__global__ void __launch_bounds__(1024) k_vtail(TailArgs A) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const float om = A.omega;
+    // down: z0 = w D^-1 f, res = f - K z0, restrict
+    for (int l = 0; l + 1 < A.nlev; ++l) {
+        const TailLevel& L = A.L[l];
+        const int n = (int)L.g.n;
+        for (int i = tid; i < 3 * n; i += nt) L.z[i] = om * L.dinv[i % n] * L.f[i];
+        __syncthreads();
+        for (int i = tid; i < 3 * n; i += nt) {
+            const int c = i / n, v = i - c * n;
+            L.res[i] = L.f[i] - tail_apply(L, L.z, c, v);
+        }
+        __syncthreads();
+        const TailLevel& C = A.L[l + 1];
+        const int nc = (int)C.g.n;
+        for (int i = tid; i < 3 * nc; i += nt) {
+            const int c = i / nc, v = i - c * nc;
+            const int X = v / C.g.pl, rem = v - X * C.g.pl, Y = rem / C.g.nz, Z = rem - Y * C.g.nz;
+            float sum = 0.f;
+            for (int dx = -1; dx <= 1; ++dx) {
+                if (!C.cf[0] && dx) continue;
+                const float wx = C.cf[0] ? (dx ? 0.25f : 0.5f) : 1.f;
+                const int x = C.cf[0] ? (2 * X + dx + L.g.nx) % L.g.nx : X;
+                for (int dy = -1; dy <= 1; ++dy) {
+                    if (!C.cf[1] && dy) continue;
+                    const float wy = C.cf[1] ? (dy ? 0.25f : 0.5f) : 1.f;
+                    const int y = C.cf[1] ? (2 * Y + dy + L.g.ny) % L.g.ny : Y;
+                    for (int dz = -1; dz <= 1; ++dz) {
+                        if (!C.cf[2] && dz) continue;
+                        const float wz = C.cf[2] ? (dz ? 0.25f : 0.5f) : 1.f;
+                        const int z = C.cf[2] ? (2 * Z + dz + L.g.nz) % L.g.nz : Z;
+                        sum += wx * wy * wz * L.res[(size_t)c * L.g.n + (x * L.g.ny + y) * L.g.nz + z];
+                    }
+                }
+            }
+            C.f[i] = sum;
+        }
+        __syncthreads();
+    }
+    // coarse solve: res_L = G f_L
+    {
+        const TailLevel& C = A.L[A.nlev - 1];
+        const int n = (int)C.g.n;
+        for (int i = tid; i < 3 * n; i += nt) {
+            const int c = i / n, r = i - c * n;
+            const float* fr = C.f + (size_t)c * n;
+            float sum = 0.f;
+            for (int j = 0; j < n; ++j) sum += A.G[(size_t)r * n + j] * fr[j];
+            C.res[i] = sum;
+        }
+        __syncthreads();
+    }
+    // up: z += P res_{l+1}; res = z + w D^-1 (f - K z)
+    for (int l = A.nlev - 2; l >= 0; --l) {
+        const TailLevel& L = A.L[l];
+        const TailLevel& C = A.L[l + 1];
+        const int n = (int)L.g.n;
+        for (int i = tid; i < 3 * n; i += nt) {
+            const int c = i / n, v = i - c * n;
+            const int x = v / L.g.pl, rem = v - x * L.g.pl, y = rem / L.g.nz, z = rem - y * L.g.nz;
+            int xi[2], yi[2], zi[2];
+            float wx[2], wy[2], wz[2];
+            int nx_ = 1, ny_ = 1, nz_ = 1;
+            auto ax = [](int i0, int coars, int ncrs, int* idx, float* w, int& cnt) {
+                if (!coars) { idx[0] = i0; w[0] = 1.f; cnt = 1; return; }
+                const int J = i0 >> 1;
+                if (i0 & 1) { idx[0] = J; idx[1] = J + 1 == ncrs ? 0 : J + 1; w[0] = w[1] = .5f; cnt = 2; }
+                else { idx[0] = J; w[0] = 1.f; cnt = 1; }
+            };
+            ax(x, C.cf[0], C.g.nx, xi, wx, nx_);
+            ax(y, C.cf[1], C.g.ny, yi, wy, ny_);
+            ax(z, C.cf[2], C.g.nz, zi, wz, nz_);
+            float sum = 0.f;
+            for (int a = 0; a < nx_; ++a)
+                for (int b = 0; b < ny_; ++b)
+                    for (int d = 0; d < nz_; ++d)
+                        sum += wx[a] * wy[b] * wz[d] * C.res[(size_t)c * C.g.n + (xi[a] * C.g.ny + yi[b]) * C.g.nz + zi[d]];
+            L.z[i] += sum;
+        }
+        __syncthreads();
+        for (int i = tid; i < 3 * n; i += nt) {
+            const int c = i / n, v = i - c * n;
+            L.res[i] = L.z[i] + om * L.dinv[v] * (L.f[i] - tail_apply(L, L.z, c, v));
+        }
+        __syncthreads();
+    }
 }
 
 // ===========================================================================
@@ -1189,6 +1425,15 @@ void launch_sum3(cudaStream_t s, long long n, const double* f, Red& red, double*
 }
 void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* f,
                        const float* dinv, float omega, float* z, float* res) {
+    if (fast_tiling(g, lt) && s3_enabled()) {
+        int nch;
+        const int xb = s3_xb(g);
+        const dim3 grid = fast_grid(g, xb, &nch);
+        const size_t sm = s3_smem_bytes<2>();
+        s3_attr(k3_smooth_res, sm);
+        k3_smooth_res<<<grid, dim3(32, kTileY), sm, s>>>(g, xb, nch, lt, kap, f, dinv, omega, z, res);
+        return;
+    }
     if (fast_tiling(g, lt)) {
         int nch;
         const int xb = fast_xb(g);
@@ -1203,6 +1448,22 @@ void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, co
 void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* z,
                    const float* f, const float* dinv, float omega, float* zout, bool dot, Red& red,
                    PcgScalars* sc) {
+    if (fast_tiling(g, lt) && s3_enabled()) {
+        int nch;
+        const int xb = s3_xb(g);
+        const dim3 grid = fast_grid(g, xb, &nch);
+        const size_t sm = s3_smem_bytes<3>();
+        if (dot) {
+            s3_attr(k3_jacobi<true>, sm);
+            k3_jacobi<true><<<grid, dim3(32, kTileY), sm, s>>>(g, xb, nch, lt, kap, z, f, dinv, omega, zout,
+                                                               red.partials, red.counter, sc);
+        } else {
+            s3_attr(k3_jacobi<false>, sm);
+            k3_jacobi<false><<<grid, dim3(32, kTileY), sm, s>>>(g, xb, nch, lt, kap, z, f, dinv, omega, zout,
+                                                                nullptr, nullptr, sc);
+        }
+        return;
+    }
     if (fast_tiling(g, lt)) {
         int nch;
         const int xb = fast_xb(g);
@@ -1224,6 +1485,15 @@ void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const 
 }
 void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* p,
                  float* q, Red& red, PcgScalars* sc) {
+    if (fast_tiling(g, lt) && s3_enabled()) {
+        int nch;
+        const int xb = s3_xb(g);
+        const dim3 grid = fast_grid(g, xb, &nch);
+        const size_t sm = s3_smem_bytes<1>();
+        s3_attr(k3_spmv, sm);
+        k3_spmv<<<grid, dim3(32, kTileY), sm, s>>>(g, xb, nch, lt, kap, p, q, red.partials, red.counter, sc);
+        return;
+    }
     if (fast_tiling(g, lt)) {
         int nch;
         const int xb = fast_xb(g);
@@ -1253,6 +1523,7 @@ void launch_prolong(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3],
 void launch_loop_ctl(cudaStream_t s, PcgScalars* sc, unsigned long long handle) {
     k_loop_ctl<<<1, 1, 0, s>>>(sc, (cudaGraphConditionalHandle)handle);
 }
+void launch_vtail(cudaStream_t s, const TailArgs& a) { k_vtail<<<1, 1024, 0, s>>>(a); }
 void launch_Tupd(cudaStream_t s, long long n3, double* T, const float* d) {
     k_Tupd<<<nblk(n3, 256), 256, 0, s>>>(n3, T, d);
 }

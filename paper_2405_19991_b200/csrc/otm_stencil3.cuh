@@ -1,0 +1,241 @@
+// Shared-memory-ring stencil engine for the fp32 level stencils (fast path).
+//
+// Block = 256 threads = 32 (z pairs) x 8 (rows) -> a 64 x 8 (z, y) output tile of
+// ONE load case; the block walks an x chunk.  Every x-plane of every staged array
+// is copied global -> shared with cp.async (16-byte chunks for the 64-wide tile
+// rows, 4-byte copies for the periodic halo columns) into a ring of kStages
+// slots, kAhead planes before the arithmetic needs it, so many planes of loads
+// are in flight per SM without spending registers on them.  The copy work of a
+// plane is a fixed list of <= kMaxTasks descriptors per thread computed once.
+//
+// Arithmetic: the separable form of otm_stencil2.cuh (equal axis scales), fed
+// from shared memory; only the newly arrived plane is read each step.
+#pragma once
+
+#include <cuda_pipeline_primitives.h>
+
+#include "otm_common.cuh"
+#include "otm_internal.h"
+#include "otm_stencil2.cuh"
+
+namespace otm {
+
+constexpr int kS3Rows = 10;       // tile rows y0-1 .. y0+8
+constexpr int kS3Pitch = 72;      // floats per smem row: [3] = z0-1, [4..67] = z0..z0+63, [68] = z0+64
+constexpr int kS3Tile = kS3Rows * kS3Pitch;
+constexpr int kStages = 5;        // ring slots (kAhead + 2: the plane in use and its predecessor)
+constexpr int kAhead = 3;         // planes in flight ahead of the plane being consumed
+constexpr int kMaxTasks = 3;
+
+// staged array kinds
+enum S3Kind { S3Halo = 0, S3Center = 1 };
+
+struct S3Array {
+    const float* p;   // base pointer (case offset applied in-kernel when per_case)
+    int per_case;     // 1: field[c*n + v]; 0: shared by all cases (D^-1)
+    int kind;         // S3Halo (rows y0-1..y0+8, cols z0-1..z0+64) or S3Center (rows y0..y0+7, cols z0..z0+63)
+};
+
+template <int NARR>
+struct S3Setup {
+    S3Array arr[NARR];
+    const float* kap;
+};
+
+// smem layout per slot: NARR tiles then the factor tile (rows y0-1..y0+7 in tile rows 0..8)
+template <int NARR>
+__host__ __device__ constexpr int s3_slot_floats() { return (NARR + 1) * kS3Tile; }
+
+template <int NARR>
+__host__ __device__ constexpr size_t s3_smem_bytes() { return (size_t)kStages * s3_slot_floats<NARR>() * 4; }
+
+struct S3Task {
+    const float* g;   // source at plane 0 (case offset and in-plane offset applied); null = none
+    int soff;         // float offset inside the slot
+    int bytes;        // 16 or 4
+};
+
+__device__ __forceinline__ void cp_async16(float* s, const float* g) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g));
+}
+__device__ __forceinline__ void cp_async4(float* s, const float* g) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(g));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Enumerate the copy tasks of one plane and keep this thread's share.
+template <int NARR>
+__device__ int s3_tasks(const Geo& g, const S3Setup<NARR>& su, int c, int y0, int z0, S3Task (&mine)[kMaxTasks]) {
+    const int tid = threadIdx.x + 32 * threadIdx.y;
+    int count = 0, t = 0;
+    for (int a = 0; a < kMaxTasks; ++a) mine[a].g = nullptr;
+    auto add = [&](int src, int soff, int goff, int bytes) {
+        if ((t & 255) == tid && count < kMaxTasks) {
+            const float* base = src == NARR ? su.kap
+                                            : su.arr[src].p + (su.arr[src].per_case ? (long long)c * g.n : 0LL);
+            mine[count].g = base + goff;
+            mine[count].soff = soff;
+            mine[count].bytes = bytes;
+            ++count;
+        }
+        ++t;
+    };
+    const int zl = z0 == 0 ? g.nz - 1 : z0 - 1;
+    const int zr = z0 + 64 == g.nz ? 0 : z0 + 64;
+    for (int a = 0; a < NARR; ++a) {
+        const bool halo = su.arr[a].kind == S3Halo;
+        const int r0 = halo ? 0 : 1, r1 = halo ? kS3Rows : kS3Rows - 1;
+        for (int r = r0; r < r1; ++r) {
+            const int y = (y0 - 1 + r + g.ny) % g.ny;
+            const int tile = a * kS3Tile + r * kS3Pitch;
+            for (int ch = 0; ch < 16; ++ch) add(a, tile + 4 + 4 * ch, y * g.nz + z0 + 4 * ch, 16);
+            if (halo) {
+                add(a, tile + 3, y * g.nz + zl, 4);
+                add(a, tile + 68, y * g.nz + zr, 4);
+            }
+        }
+    }
+    for (int r = 0; r < kS3Rows - 1; ++r) {     // factors: rows y0-1..y0+7, cols z0-1..z0+63
+        const int y = (y0 - 1 + r + g.ny) % g.ny;
+        const int tile = NARR * kS3Tile + r * kS3Pitch;
+        for (int ch = 0; ch < 16; ++ch) add(NARR, tile + 4 + 4 * ch, y * g.nz + z0 + 4 * ch, 16);
+        add(NARR, tile + 3, y * g.nz + zl, 4);
+    }
+    return count;
+}
+
+template <int NARR>
+__device__ __forceinline__ void s3_issue(const Geo& g, const S3Setup<NARR>& su, int c, int x, float* slot,
+                                         const S3Task (&mine)[kMaxTasks]) {
+    const int xx = x < 0 ? x + g.nx : (x >= g.nx ? x - g.nx : x);
+    const long long po = (long long)xx * g.pl;
+#pragma unroll
+    for (int k = 0; k < kMaxTasks; ++k) {
+        const S3Task& tk = mine[k];
+        if (tk.g == nullptr) continue;
+        if (tk.bytes == 16) cp_async16(slot + tk.soff, tk.g + po);
+        else cp_async4(slot + tk.soff, tk.g + po);
+    }
+}
+
+// Op contract (fp32):
+//   float operand(const float* slot, int r, int col) const  -> operand at tile row r, smem column col
+//   void sink(const float* slot, int c, long long v, int r, int col, const float (&kt)[2], const float (&ctr)[2])
+//     slot = ring slot of the output plane x (for center-only arrays), r = tile row of the thread (1..8),
+//     col = smem column of vertex z (z+1 is col+1)
+template <int NARR, class Op>
+__device__ __forceinline__ void march3(const Geo& g, int xb, int nch, const LevelTemplate& lt,
+                                       const S3Setup<NARR>& su, Op& op) {
+    extern __shared__ float4 s3_smem4[];
+    float* smem = reinterpret_cast<float*>(s3_smem4);
+    constexpr int SLOT = s3_slot_floats<NARR>();
+    const int c = blockIdx.z / nch;
+    const int ch = blockIdx.z - c * nch;
+    const int z0 = blockIdx.x * kTileZ, y0 = blockIdx.y * kTileY;
+    const int x0 = ch * xb, x1 = min(g.nx, x0 + xb);
+    if (x0 >= x1) return;   // uniform per block
+    S3Task mine[kMaxTasks];
+    s3_tasks<NARR>(g, su, c, y0, z0, mine);
+    const int nplanes = (x1 - x0) + 2;          // operand planes x0-1 .. x1 (factors x0-1 .. x1-1 suffice)
+    // prologue: planes 0 .. kAhead-1
+#pragma unroll
+    for (int s = 0; s < kAhead; ++s) {
+        if (s < nplanes) s3_issue<NARR>(g, su, c, x0 - 1 + s, smem + s * SLOT, mine);
+        cp_commit();
+    }
+    const int tr = threadIdx.y + 1;             // tile row of this thread's output row
+    const int col = 4 + 2 * threadIdx.x;        // smem column of vertex z
+    const float s12 = (float)lt.s12;
+    float P1[3][4], P2[3][4], K0[2][3], K1[2][3], Qlo[2][3], Exlo[2], P0c[2];
+    auto readT = [&](const float* slot, float (&P)[3][4]) {
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) P[j][m] = op.operand(slot, tr - 1 + j, col - 1 + m);
+    };
+    auto readK = [&](const float* slot, float (&K)[2][3]) {
+        const float* kt = slot + NARR * kS3Tile;
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+            for (int m = 0; m < 3; ++m) K[jj][m] = kt[(tr - 1 + jj) * kS3Pitch + col - 1 + m];
+    };
+    // stage s holds operand plane x0-1+s and factor plane x0-1+s
+    for (int s = 0; s < nplanes; ++s) {
+        // plane s has landed once at most kAhead-1 newer groups are pending; the barrier
+        // publishes every thread's copies and retires all reads of iteration s-1
+        cp_wait<kAhead - 1>();
+        __syncthreads();
+        // keep kAhead planes in flight: plane s + kAhead goes to the slot of plane s - 2
+        // (kStages = kAhead + 2), whose last reader was iteration s - 1
+        if (s + kAhead < nplanes)
+            s3_issue<NARR>(g, su, c, x0 - 1 + s + kAhead, smem + ((s + kAhead) % kStages) * SLOT, mine);
+        cp_commit();
+        const float* slot = smem + (s % kStages) * SLOT;
+        if (s == 0) {
+            float P0[3][4];
+            readT(slot, P0);
+            readK(slot, K0);
+            P0c[0] = P0[1][1];
+            P0c[1] = P0[1][2];
+            // the element plane x0-1 needs operand plane x0 as well: finished at s == 1
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+#pragma unroll
+                for (int m = 0; m < 4; ++m) P2[j][m] = P0[j][m];   // park P0 in P2
+        } else if (s == 1) {
+            readT(slot, P1);
+            element_plane<float>(P2, P1, K0, Qlo, Exlo);
+        } else {
+            // operand plane x+1 (x = x0 + s - 2) and factor plane x arrive; emit output plane x
+            readT(slot, P2);
+            const float* xslot = smem + ((s - 1) % kStages) * SLOT;   // plane x: factors + pointwise arrays
+            readK(xslot, K1);
+            float Qhi[2][3], Exhi[2];
+            element_plane<float>(P1, P2, K1, Qhi, Exhi);
+            float KX[2][3];
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+                for (int m = 0; m < 3; ++m) KX[jj][m] = K0[jj][m] + K1[jj][m];
+            float kt[2], ctr[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const float qx = ((Qlo[0][i] + Qhi[0][i]) + (Qlo[0][i + 1] + Qhi[0][i + 1])) +
+                                 ((Qlo[1][i] + Qhi[1][i]) + (Qlo[1][i + 1] + Qhi[1][i + 1]));
+                const float eym = KX[0][i] + KX[0][i + 1], eyp = KX[1][i] + KX[1][i + 1];
+                const float ezm = KX[0][i] + KX[1][i], ezp = KX[0][i + 1] + KX[1][i + 1];
+                const float kv = Exlo[i] + Exhi[i];
+                float acc = 5.f * kv * P1[1][1 + i];
+                acc += Exhi[i] * P2[1][1 + i] + Exlo[i] * P0c[i];
+                acc += eyp * P1[2][1 + i] + eym * P1[0][1 + i];
+                acc += ezp * P1[1][2 + i] + ezm * P1[1][i];
+                kt[i] = s12 * (acc - qx);
+                ctr[i] = P1[1][1 + i];
+            }
+            const int x = x0 + s - 2;
+            op.sink(xslot, c, (long long)x * g.pl + (long long)(y0 + threadIdx.y) * g.nz + z0 + 2 * threadIdx.x, tr,
+                    col, kt, ctr);
+            // rotate
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+                for (int m = 0; m < 3; ++m) { Qlo[jj][m] = Qhi[jj][m]; K0[jj][m] = K1[jj][m]; }
+            Exlo[0] = Exhi[0];
+            Exlo[1] = Exhi[1];
+            P0c[0] = P1[1][1];
+            P0c[1] = P1[1][2];
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+#pragma unroll
+                for (int m = 0; m < 4; ++m) P1[j][m] = P2[j][m];
+        }
+    }
+    cp_wait<0>();
+}
+
+}  // namespace otm
