@@ -77,7 +77,7 @@ struct otm_ctx {
     int* changed = nullptr;      // device flag
     bool built = false;
     bool no_loop_graph = false;
-    bool no_tail = getenv("OTM_NO_TAIL") != nullptr;
+    bool no_tail = getenv("OTM_TAIL") == nullptr;   // single-CTA tail: opt-in, slower so far
     bool warm = false;
     bool have_T = false;
     std::string err;

@@ -110,6 +110,58 @@ __device__ bool reduce_finalize(double (&v)[NQ], double* partials, unsigned* cou
     return false;
 }
 
+// Wide variant for 32 quantities: a butterfly reduce-scatter leaves the warp sum
+// of quantity `lane` in lane `lane` (31 shuffles per lane instead of 160), then
+// warps and blocks are summed in index order as above.
+__device__ __forceinline__ double warp_reduce_scatter32(double (&v)[32]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < o; ++i) {
+            const double keep = up ? v[i + o] : v[i];
+            const double send = up ? v[i] : v[i + o];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    return v[0];
+}
+
+// 1-D blocks only.  Returns true in thread 0 of the last block, out[0..31] written.
+__device__ inline bool reduce_finalize32(double (&v)[32], double* partials, unsigned* counter, double* out) {
+    __shared__ double sm[32][33];
+    __shared__ bool is_last;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const unsigned nb = gridDim.x;
+    const double mine = warp_reduce_scatter32(v);
+    sm[wid][lane] = mine;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double s = 0.0;
+        for (int w = 0; w < nw; ++w) s += sm[w][threadIdx.x];
+        partials[(size_t)blockIdx.x * 32 + threadIdx.x] = s;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = atomicAdd(counter, 1u) == nb - 1;
+    __syncthreads();
+    if (!is_last) return false;
+    // last block: thread t sums quantity (t & 31) over blocks b = (t >> 5), (t >> 5) + nw, ...
+    double s = 0.0;
+    for (unsigned b = wid; b < nb; b += nw) s += __ldcg(partials + (size_t)b * 32 + lane);
+    sm[wid][lane] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double t = 0.0;
+        for (int w = 0; w < nw; ++w) t += sm[w][threadIdx.x];
+        out[threadIdx.x] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *counter = 0u;
+    return threadIdx.x == 0;
+}
+
 // ---------------------------------------------------------------------------
 // Register-window stencil core.
 //

@@ -845,32 +845,31 @@ __global__ void k_sens(Geo g, const double* __restrict__ T, const double* __rest
 // a few ulps from the reference's expression, which only matters for the means the
 // host compares against the bound; the final density is written by k_oc_apply with
 // the reference's exact expression.  lams[k] == 0 encodes the lam -> 0 "free" step.
-__global__ void __launch_bounds__(256) k_oc_eval(long long n, const double* __restrict__ rho,
-                                                 const double* __restrict__ sens, const OcArgs a, int nlam,
-                                                 const LamSet lam_pow, double* partials,
-                                                 unsigned* counter, double* out) {
+__global__ void __launch_bounds__(256, 2) k_oc_eval(long long n, const double* __restrict__ rho,
+                                                    const double* __restrict__ sens, const OcArgs a, int nlam,
+                                                    const LamSet lam_pow, double* partials, unsigned* counter,
+                                                    double* out) {
+    static_assert(kOcLam == 32, "reduce_finalize32 assumes 32 multipliers per pass");
     double acc[kOcLam];
 #pragma unroll
     for (int k = 0; k < kOcLam; ++k) acc[k] = 0.0;
     const double M = (double)n;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
-        const double r = rho[i];
-        const double desc = M * (-sens[i]);
+        const double r = __ldg(rho + i);
+        const double desc = M * (-__ldg(sens + i));
         const double lo = fmax(r - a.step, a.rmin), hi = fmin(r + a.step, 1.0);
+        const double lof = fmax(lo, r * a.floor_ratio);      // clip(max(x, floor), lo, hi) = min(max(x, lof), hi)
         const double ce = desc > 0.0 ? r * (a.sqrt_damp ? sqrt(desc) : pow(desc, a.damp)) : 0.0;
-        const double floor_v = r * a.floor_ratio;
         const double freev = desc > 0.0 ? hi : (desc < 0.0 ? lo : r);
 #pragma unroll
         for (int k = 0; k < kOcLam; ++k) {
-            if (k < nlam) {
-                const double lp = lam_pow.v[k];   // lam^-damp, or 0 for the free step
-                const double cand = lp == 0.0 ? freev : fmin(fmax(fmax(ce * lp, floor_v), lo), hi);
-                acc[k] += cand;
-            }
+            const double lp = lam_pow.v[k];   // lam^-damp, or 0 for the free step
+            const double cand = lp == 0.0 ? freev : fmin(fmax(ce * lp, lof), hi);
+            acc[k] += k < nlam ? cand : 0.0;
         }
     }
-    if (reduce_finalize<kOcLam>(acc, partials, counter, out)) {
+    if (reduce_finalize32(acc, partials, counter, out)) {
         for (int k = 0; k < kOcLam; ++k) out[k] /= M;
     }
 }
@@ -1160,9 +1159,9 @@ static inline int s3_xb(const Geo& g) {
     if (xb > g.nx) xb = g.nx;
     return xb;
 }
-static bool s3_enabled() {
-    static const bool off = getenv("OTM_NO_S3") != nullptr;
-    return !off;
+static bool s3_enabled() {     // opt-in (OTM_S3=1): slower than the k2 register window so far
+    static const bool on = getenv("OTM_S3") != nullptr;
+    return on;
 }
 template <class K>
 static void s3_attr(K kernel, size_t bytes) {
