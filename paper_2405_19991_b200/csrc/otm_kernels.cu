@@ -673,6 +673,132 @@ __global__ void __launch_bounds__(256) k_upd(long long n, float* __restrict__ d,
     }
 }
 
+// ---- small levels: one thread per (case, vertex), every load issued up front ----
+template <int OP, bool DOT>
+__global__ void __launch_bounds__(256) k_small(Geo g, LevelTemplate lt, const float* __restrict__ kap,
+                                               const float* __restrict__ a, const float* __restrict__ f,
+                                               const float* __restrict__ dinv, float omega, float* __restrict__ o1,
+                                               float* __restrict__ o2, double* partials, unsigned* counter,
+                                               PcgScalars* sc) {
+    // OP 0: smooth_res  (operand w D^-1 f; o1 = z0, o2 = f - K z0)
+    // OP 1: jacobi      (operand a = z;    o1 = z + w D^-1 (f - K z); DOT: r.z -> beta)
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double dot3[3] = {0.0, 0.0, 0.0};
+    if (i < 3 * g.n) {
+        const int c = (int)(i / g.n);
+        const int v = (int)(i - (long long)c * g.n);
+        const int x = v / g.pl, rem = v - x * g.pl, y = rem / g.nz, z = rem - y * g.nz;
+        const int xs[3] = {wrap_m(x, g.nx), x, wrap_p(x, g.nx)};
+        const int ys[3] = {wrap_m(y, g.ny) * g.nz, y * g.nz, wrap_p(y, g.ny) * g.nz};
+        const int zs[3] = {wrap_m(z, g.nz), z, wrap_p(z, g.nz)};
+        const float* src = (OP == 0 ? f : a) + (size_t)c * g.n;
+        float t[3][9], k[2][4];
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const int idx = xs[p] * g.pl + ys[j] + zs[q];
+                    float val = __ldg(src + idx);
+                    if (OP == 0) val *= omega * __ldg(dinv + idx);
+                    t[p][j * 3 + q] = val;
+                }
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int q = 0; q < 2; ++q) k[p][j * 2 + q] = __ldg(kap + xs[p] * g.pl + ys[j] + zs[q]);
+        float kt;
+        if (lt.equal) {
+            const KSum<float> s = ksum<float>(k);
+            kt = apply_compact<float>(t, k, s, (float)lt.s12);
+        } else {
+            float ktab[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) ktab[q] = (float)lt.kt[q];
+            kt = apply_generic<float>(t, k, ktab);
+        }
+        const float fv = __ldg(f + (size_t)c * g.n + v);
+        if (OP == 0) {
+            o1[(size_t)c * g.n + v] = t[1][4];
+            o2[(size_t)c * g.n + v] = fv - kt;
+        } else {
+            const float zn = t[1][4] + omega * __ldg(dinv + v) * (fv - kt);
+            o1[(size_t)c * g.n + v] = zn;
+            if (DOT) dot3[c] = (double)fv * (double)zn;
+        }
+    }
+    if (DOT) {
+        if (reduce_finalize<3>(dot3, partials, counter, sc->red)) {
+            for (int cc = 0; cc < 3; ++cc) {
+                const double rz = sc->red[cc];
+                sc->beta[cc] = (sc->first || sc->rz[cc] == 0.0) ? 0.0 : rz / sc->rz[cc];
+                sc->rz[cc] = rz;
+            }
+            sc->first = 0;
+        }
+    }
+}
+
+// restriction with every axis coarsened (3-D levels): unrolled 27-point gather
+__global__ void __launch_bounds__(256) k_restrict3(Geo f, Geo c, const float* __restrict__ res,
+                                                   float* __restrict__ fc) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 3 * c.n) return;
+    const int cc = (int)(i / c.n);
+    const int v = (int)(i - (long long)cc * c.n);
+    const int X = v / c.pl, rem = v - X * c.pl, Y = rem / c.nz, Z = rem - Y * c.nz;
+    const int xs[3] = {wrap_m(2 * X, f.nx), 2 * X, wrap_p(2 * X, f.nx)};
+    const int ys[3] = {wrap_m(2 * Y, f.ny) * f.nz, 2 * Y * f.nz, wrap_p(2 * Y, f.ny) * f.nz};
+    const int zs[3] = {wrap_m(2 * Z, f.nz), 2 * Z, wrap_p(2 * Z, f.nz)};
+    const float w[3] = {0.25f, 0.5f, 0.25f};
+    const float* r = res + (size_t)cc * f.n;
+    float vals[27];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) vals[(a * 3 + b) * 3 + d] = __ldg(r + (long long)xs[a] * f.pl + ys[b] + zs[d]);
+    float s = 0.f;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        float sb = 0.f;
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            const float sz = w[0] * vals[(a * 3 + b) * 3] + w[1] * vals[(a * 3 + b) * 3 + 1] + w[2] * vals[(a * 3 + b) * 3 + 2];
+            sb += w[b] * sz;
+        }
+        s += w[a] * sb;
+    }
+    fc[i] = s;
+}
+
+// trilinear prolongation + correction, every axis coarsened: 8 coarse loads, weights 0/0.5/1
+__global__ void __launch_bounds__(256) k_prolong3(Geo f, Geo c, const float* __restrict__ zc,
+                                                  float* __restrict__ zf) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 3 * f.n) return;
+    const int cc = (int)(i / f.n);
+    const int v = (int)(i - (long long)cc * f.n);
+    const int x = v / f.pl, rem = v - x * f.pl, y = rem / f.nz, z = rem - y * f.nz;
+    const int X0 = x >> 1, Y0 = y >> 1, Z0 = z >> 1;
+    const int X1 = X0 + 1 == c.nx ? 0 : X0 + 1, Y1 = Y0 + 1 == c.ny ? 0 : Y0 + 1, Z1 = Z0 + 1 == c.nz ? 0 : Z0 + 1;
+    const float wx1 = (x & 1) ? 0.5f : 0.f, wy1 = (y & 1) ? 0.5f : 0.f, wz1 = (z & 1) ? 0.5f : 0.f;
+    const float wx0 = 1.f - wx1, wy0 = 1.f - wy1, wz0 = 1.f - wz1;
+    const float* a = zc + (size_t)cc * c.n;
+    const long long r00 = (long long)X0 * c.pl + Y0 * c.nz, r01 = (long long)X0 * c.pl + Y1 * c.nz;
+    const long long r10 = (long long)X1 * c.pl + Y0 * c.nz, r11 = (long long)X1 * c.pl + Y1 * c.nz;
+    const float v000 = __ldg(a + r00 + Z0), v001 = __ldg(a + r00 + Z1), v010 = __ldg(a + r01 + Z0),
+                v011 = __ldg(a + r01 + Z1), v100 = __ldg(a + r10 + Z0), v101 = __ldg(a + r10 + Z1),
+                v110 = __ldg(a + r11 + Z0), v111 = __ldg(a + r11 + Z1);
+    const float s = wx0 * (wy0 * (wz0 * v000 + wz1 * v001) + wy1 * (wz0 * v010 + wz1 * v011)) +
+                    wx1 * (wy0 * (wz0 * v100 + wz1 * v101) + wy1 * (wz0 * v110 + wz1 * v111));
+    zf[i] += s;
+}
+
 // full-weighting restriction (solver.py:167-177): coarse J <- sum_d w(d) res[2J+d]
 __global__ void k_restrict(Geo f, Geo c, int cx, int cy, int cz, const float* __restrict__ res,
                            float* __restrict__ fc) {
@@ -1422,8 +1548,15 @@ void launch_load_means(cudaStream_t s, const Geo& g, const LevelTemplate& lt, co
 void launch_sum3(cudaStream_t s, long long n, const double* f, Red& red, double* out3) {
     k_sum3<<<592, 256, 0, s>>>(n, f, red.partials, red.counter, out3);
 }
+static inline bool small_level(const Geo& g) { return g.n <= 65536; }
+
 void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* f,
                        const float* dinv, float omega, float* z, float* res) {
+    if (!fast_tiling(g, lt) && small_level(g)) {
+        k_small<0, false><<<nblk(3 * g.n, 256), 256, 0, s>>>(g, lt, kap, nullptr, f, dinv, omega, z, res, nullptr,
+                                                             nullptr, nullptr);
+        return;
+    }
     if (fast_tiling(g, lt) && s3_enabled()) {
         int nch;
         const int xb = s3_xb(g);
@@ -1447,6 +1580,15 @@ void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, co
 void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* z,
                    const float* f, const float* dinv, float omega, float* zout, bool dot, Red& red,
                    PcgScalars* sc) {
+    if (!fast_tiling(g, lt) && small_level(g)) {
+        if (dot)
+            k_small<1, true><<<nblk(3 * g.n, 256), 256, 0, s>>>(g, lt, kap, z, f, dinv, omega, zout, nullptr,
+                                                                red.partials, red.counter, sc);
+        else
+            k_small<1, false><<<nblk(3 * g.n, 256), 256, 0, s>>>(g, lt, kap, z, f, dinv, omega, zout, nullptr,
+                                                                 nullptr, nullptr, sc);
+        return;
+    }
     if (fast_tiling(g, lt) && s3_enabled()) {
         int nch;
         const int xb = s3_xb(g);
@@ -1514,9 +1656,17 @@ void launch_upd(cudaStream_t s, long long n, float* d, float* r, const float* p,
     k_upd<<<nblk(th, 256), 256, 0, s>>>(n, d, r, p, q, red.partials, red.counter, sc);
 }
 void launch_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* res, float* fc) {
+    if (cf[0] && cf[1] && cf[2]) {
+        k_restrict3<<<nblk(3 * c.n, 256), 256, 0, s>>>(f, c, res, fc);
+        return;
+    }
     k_restrict<<<nblk(c.n, 256), 256, 0, s>>>(f, c, cf[0], cf[1], cf[2], res, fc);
 }
 void launch_prolong(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* zc, float* zf) {
+    if (cf[0] && cf[1] && cf[2]) {
+        k_prolong3<<<nblk(3 * f.n, 256), 256, 0, s>>>(f, c, zc, zf);
+        return;
+    }
     k_prolong<<<nblk(f.n, 256), 256, 0, s>>>(f, c, cf[0], cf[1], cf[2], zc, zf);
 }
 void launch_loop_ctl(cudaStream_t s, PcgScalars* sc, unsigned long long handle) {

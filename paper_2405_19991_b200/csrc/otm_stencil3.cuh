@@ -67,45 +67,51 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// Enumerate the copy tasks of one plane and keep this thread's share.
+// This thread's copy tasks of one plane: task ids tid, tid+256, tid+512 of the
+// plane's task list [array 0 tasks | array 1 tasks | ... | factor tasks], decoded
+// arithmetically (halo array row: 16 chunks + left + right halo; centre array
+// row: 16 chunks; factor row: 16 chunks + left halo).
 template <int NARR>
-__device__ int s3_tasks(const Geo& g, const S3Setup<NARR>& su, int c, int y0, int z0, S3Task (&mine)[kMaxTasks]) {
+__device__ __forceinline__ void s3_tasks(const Geo& g, const S3Setup<NARR>& su, int c, int y0, int z0,
+                                         S3Task (&mine)[kMaxTasks]) {
     const int tid = threadIdx.x + 32 * threadIdx.y;
-    int count = 0, t = 0;
-    for (int a = 0; a < kMaxTasks; ++a) mine[a].g = nullptr;
-    auto add = [&](int src, int soff, int goff, int bytes) {
-        if ((t & 255) == tid && count < kMaxTasks) {
-            const float* base = src == NARR ? su.kap
-                                            : su.arr[src].p + (su.arr[src].per_case ? (long long)c * g.n : 0LL);
-            mine[count].g = base + goff;
-            mine[count].soff = soff;
-            mine[count].bytes = bytes;
-            ++count;
-        }
-        ++t;
-    };
     const int zl = z0 == 0 ? g.nz - 1 : z0 - 1;
     const int zr = z0 + 64 == g.nz ? 0 : z0 + 64;
-    for (int a = 0; a < NARR; ++a) {
-        const bool halo = su.arr[a].kind == S3Halo;
-        const int r0 = halo ? 0 : 1, r1 = halo ? kS3Rows : kS3Rows - 1;
-        for (int r = r0; r < r1; ++r) {
-            const int y = (y0 - 1 + r + g.ny) % g.ny;
-            const int tile = a * kS3Tile + r * kS3Pitch;
-            for (int ch = 0; ch < 16; ++ch) add(a, tile + 4 + 4 * ch, y * g.nz + z0 + 4 * ch, 16);
-            if (halo) {
-                add(a, tile + 3, y * g.nz + zl, 4);
-                add(a, tile + 68, y * g.nz + zr, 4);
+#pragma unroll
+    for (int k = 0; k < kMaxTasks; ++k) {
+        int t = tid + 256 * k;
+        mine[k].g = nullptr;
+        mine[k].soff = 0;
+        mine[k].bytes = 16;
+        bool done = false;
+#pragma unroll
+        for (int a = 0; a < NARR; ++a) {
+            if (done) break;
+            const bool halo = su.arr[a].kind == S3Halo;
+            const int per_row = halo ? 18 : 16, nrows = halo ? kS3Rows : kS3Rows - 2;
+            const int cnt = per_row * nrows;
+            if (t < cnt) {
+                const int r = t / per_row + (halo ? 0 : 1), j = t - (t / per_row) * per_row;
+                const int y = (y0 - 1 + r + g.ny) % g.ny;
+                const float* base = su.arr[a].p + (su.arr[a].per_case ? (long long)c * g.n : 0LL) + (long long)y * g.nz;
+                const int srow = a * kS3Tile + r * kS3Pitch;
+                if (j < 16) { mine[k].g = base + z0 + 4 * j; mine[k].soff = srow + 4 + 4 * j; }
+                else if (j == 16) { mine[k].g = base + zl; mine[k].soff = srow + 3; mine[k].bytes = 4; }
+                else { mine[k].g = base + zr; mine[k].soff = srow + 68; mine[k].bytes = 4; }
+                done = true;
+            } else {
+                t -= cnt;
             }
         }
+        if (!done && t < 17 * (kS3Rows - 1)) {
+            const int r = t / 17, j = t - (t / 17) * 17;
+            const int y = (y0 - 1 + r + g.ny) % g.ny;
+            const float* base = su.kap + (long long)y * g.nz;
+            const int srow = NARR * kS3Tile + r * kS3Pitch;
+            if (j < 16) { mine[k].g = base + z0 + 4 * j; mine[k].soff = srow + 4 + 4 * j; }
+            else { mine[k].g = base + zl; mine[k].soff = srow + 3; mine[k].bytes = 4; }
+        }
     }
-    for (int r = 0; r < kS3Rows - 1; ++r) {     // factors: rows y0-1..y0+7, cols z0-1..z0+63
-        const int y = (y0 - 1 + r + g.ny) % g.ny;
-        const int tile = NARR * kS3Tile + r * kS3Pitch;
-        for (int ch = 0; ch < 16; ++ch) add(NARR, tile + 4 + 4 * ch, y * g.nz + z0 + 4 * ch, 16);
-        add(NARR, tile + 3, y * g.nz + zl, 4);
-    }
-    return count;
 }
 
 template <int NARR>
@@ -148,6 +154,7 @@ __device__ __forceinline__ void march3(const Geo& g, int xb, int nch, const Leve
         cp_commit();
     }
     const int tr = threadIdx.y + 1;             // tile row of this thread's output row
+    const long long vrow = (long long)(y0 + threadIdx.y) * g.nz + z0 + 2 * threadIdx.x;
     const int col = 4 + 2 * threadIdx.x;        // smem column of vertex z
     const float s12 = (float)lt.s12;
     float P1[3][4], P2[3][4], K0[2][3], K1[2][3], Qlo[2][3], Exlo[2], P0c[2];
@@ -164,76 +171,72 @@ __device__ __forceinline__ void march3(const Geo& g, int xb, int nch, const Leve
 #pragma unroll
             for (int m = 0; m < 3; ++m) K[jj][m] = kt[(tr - 1 + jj) * kS3Pitch + col - 1 + m];
     };
-    // stage s holds operand plane x0-1+s and factor plane x0-1+s
-    for (int s = 0; s < nplanes; ++s) {
+    // stage s holds operand plane x0-1+s and factor plane x0-1+s; stage s -> slot s % kStages
+    auto advance = [&](int s) {
         // plane s has landed once at most kAhead-1 newer groups are pending; the barrier
         // publishes every thread's copies and retires all reads of iteration s-1
         cp_wait<kAhead - 1>();
         __syncthreads();
-        // keep kAhead planes in flight: plane s + kAhead goes to the slot of plane s - 2
-        // (kStages = kAhead + 2), whose last reader was iteration s - 1
+        // plane s + kAhead goes to the slot of plane s - 2 (kStages = kAhead + 2),
+        // whose last reader was iteration s - 1
         if (s + kAhead < nplanes)
             s3_issue<NARR>(g, su, c, x0 - 1 + s + kAhead, smem + ((s + kAhead) % kStages) * SLOT, mine);
         cp_commit();
+    };
+    {
+        advance(0);
+        float P0[3][4];
+        readT(smem, P0);
+        readK(smem, K0);
+        P0c[0] = P0[1][1];
+        P0c[1] = P0[1][2];
+        advance(1);
+        readT(smem + SLOT, P1);
+        element_plane<float>(P0, P1, K0, Qlo, Exlo);
+    }
+    for (int s = 2; s < nplanes; ++s) {
+        advance(s);
+        // operand plane x+1 (x = x0 + s - 2) and factor plane x arrive; emit output plane x
         const float* slot = smem + (s % kStages) * SLOT;
-        if (s == 0) {
-            float P0[3][4];
-            readT(slot, P0);
-            readK(slot, K0);
-            P0c[0] = P0[1][1];
-            P0c[1] = P0[1][2];
-            // the element plane x0-1 needs operand plane x0 as well: finished at s == 1
+        const float* xslot = smem + ((s - 1) % kStages) * SLOT;   // plane x: factors + pointwise arrays
+        readT(slot, P2);
+        readK(xslot, K1);
+        float Qhi[2][3], Exhi[2];
+        element_plane<float>(P1, P2, K1, Qhi, Exhi);
+        float KX[2][3];
 #pragma unroll
-            for (int j = 0; j < 3; ++j)
+        for (int jj = 0; jj < 2; ++jj)
 #pragma unroll
-                for (int m = 0; m < 4; ++m) P2[j][m] = P0[j][m];   // park P0 in P2
-        } else if (s == 1) {
-            readT(slot, P1);
-            element_plane<float>(P2, P1, K0, Qlo, Exlo);
-        } else {
-            // operand plane x+1 (x = x0 + s - 2) and factor plane x arrive; emit output plane x
-            readT(slot, P2);
-            const float* xslot = smem + ((s - 1) % kStages) * SLOT;   // plane x: factors + pointwise arrays
-            readK(xslot, K1);
-            float Qhi[2][3], Exhi[2];
-            element_plane<float>(P1, P2, K1, Qhi, Exhi);
-            float KX[2][3];
+            for (int m = 0; m < 3; ++m) KX[jj][m] = K0[jj][m] + K1[jj][m];
+        float kt[2], ctr[2];
 #pragma unroll
-            for (int jj = 0; jj < 2; ++jj)
-#pragma unroll
-                for (int m = 0; m < 3; ++m) KX[jj][m] = K0[jj][m] + K1[jj][m];
-            float kt[2], ctr[2];
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const float qx = ((Qlo[0][i] + Qhi[0][i]) + (Qlo[0][i + 1] + Qhi[0][i + 1])) +
-                                 ((Qlo[1][i] + Qhi[1][i]) + (Qlo[1][i + 1] + Qhi[1][i + 1]));
-                const float eym = KX[0][i] + KX[0][i + 1], eyp = KX[1][i] + KX[1][i + 1];
-                const float ezm = KX[0][i] + KX[1][i], ezp = KX[0][i + 1] + KX[1][i + 1];
-                const float kv = Exlo[i] + Exhi[i];
-                float acc = 5.f * kv * P1[1][1 + i];
-                acc += Exhi[i] * P2[1][1 + i] + Exlo[i] * P0c[i];
-                acc += eyp * P1[2][1 + i] + eym * P1[0][1 + i];
-                acc += ezp * P1[1][2 + i] + ezm * P1[1][i];
-                kt[i] = s12 * (acc - qx);
-                ctr[i] = P1[1][1 + i];
-            }
-            const int x = x0 + s - 2;
-            op.sink(xslot, c, (long long)x * g.pl + (long long)(y0 + threadIdx.y) * g.nz + z0 + 2 * threadIdx.x, tr,
-                    col, kt, ctr);
-            // rotate
-#pragma unroll
-            for (int jj = 0; jj < 2; ++jj)
-#pragma unroll
-                for (int m = 0; m < 3; ++m) { Qlo[jj][m] = Qhi[jj][m]; K0[jj][m] = K1[jj][m]; }
-            Exlo[0] = Exhi[0];
-            Exlo[1] = Exhi[1];
-            P0c[0] = P1[1][1];
-            P0c[1] = P1[1][2];
-#pragma unroll
-            for (int j = 0; j < 3; ++j)
-#pragma unroll
-                for (int m = 0; m < 4; ++m) P1[j][m] = P2[j][m];
+        for (int i = 0; i < 2; ++i) {
+            const float qx = ((Qlo[0][i] + Qhi[0][i]) + (Qlo[0][i + 1] + Qhi[0][i + 1])) +
+                             ((Qlo[1][i] + Qhi[1][i]) + (Qlo[1][i + 1] + Qhi[1][i + 1]));
+            const float eym = KX[0][i] + KX[0][i + 1], eyp = KX[1][i] + KX[1][i + 1];
+            const float ezm = KX[0][i] + KX[1][i], ezp = KX[0][i + 1] + KX[1][i + 1];
+            const float kv = Exlo[i] + Exhi[i];
+            float acc = 5.f * kv * P1[1][1 + i];
+            acc += Exhi[i] * P2[1][1 + i] + Exlo[i] * P0c[i];
+            acc += eyp * P1[2][1 + i] + eym * P1[0][1 + i];
+            acc += ezp * P1[1][2 + i] + ezm * P1[1][i];
+            kt[i] = s12 * (acc - qx);
+            ctr[i] = P1[1][1 + i];
         }
+        const int x = x0 + s - 2;
+        op.sink(xslot, c, vrow + (long long)x * g.pl, tr, col, kt, ctr);
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+            for (int m = 0; m < 3; ++m) { Qlo[jj][m] = Qhi[jj][m]; K0[jj][m] = K1[jj][m]; }
+        Exlo[0] = Exhi[0];
+        Exlo[1] = Exhi[1];
+        P0c[0] = P1[1][1];
+        P0c[1] = P1[1][2];
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) P1[j][m] = P2[j][m];
     }
     cp_wait<0>();
 }
