@@ -1187,6 +1187,7 @@ __device__ __forceinline__ const float* s3_at(const float* slot, int a, int r, i
 
 struct Op3SmoothRes {     // arrays: 0 = f (halo), 1 = D^-1 (halo); operand = w D^-1 f
     float omega; float* z; float* res; long long n;
+    __device__ __forceinline__ void begin_case(int, int) {}
     __device__ __forceinline__ float operand(const float* slot, int r, int col) const {
         return omega * *s3_at(slot, 1, r, col) * *s3_at(slot, 0, r, col);
     }
@@ -1200,7 +1201,11 @@ struct Op3SmoothRes {     // arrays: 0 = f (halo), 1 = D^-1 (halo); operand = w 
 
 template <bool DOT>
 struct Op3Jacobi {        // arrays: 0 = z (halo), 1 = f (center), 2 = D^-1 (center)
-    float omega; float* zout; long long n; double acc;
+    float omega; float* zout; long long n; double acc; double acc3[3];
+    __device__ __forceinline__ void begin_case(int c, int last) {
+        if (last >= 0) acc3[last] += acc;
+        acc = 0.0;
+    }
     __device__ __forceinline__ float operand(const float* slot, int r, int col) const { return *s3_at(slot, 0, r, col); }
     __device__ __forceinline__ void sink(const float* slot, int c, long long v, int r, int col, const float (&kz)[2],
                                          const float (&zc)[2]) {
@@ -1214,7 +1219,11 @@ struct Op3Jacobi {        // arrays: 0 = z (halo), 1 = f (center), 2 = D^-1 (cen
 };
 
 struct Op3Spmv {          // arrays: 0 = p (halo)
-    float* q; long long n; double acc;
+    float* q; long long n; double acc; double acc3[3];
+    __device__ __forceinline__ void begin_case(int c, int last) {
+        if (last >= 0) acc3[last] += acc;
+        acc = 0.0;
+    }
     __device__ __forceinline__ float operand(const float* slot, int r, int col) const { return *s3_at(slot, 0, r, col); }
     __device__ __forceinline__ void sink(const float*, int c, long long v, int, int, const float (&kp)[2],
                                          const float (&pc)[2]) {
@@ -1231,7 +1240,8 @@ __global__ void __launch_bounds__(256, 3) k3_smooth_res(Geo g, int xb, int nch, 
     su.arr[1] = S3Array{dinv, 0, S3Halo};
     su.kap = kap;
     Op3SmoothRes op{omega, z, res, g.n};
-    march3<2>(g, xb, nch, lt, su, op);
+    int last;
+    march3<2>(g, lt, su, op, last);
 }
 
 template <bool DOT>
@@ -1244,11 +1254,12 @@ __global__ void __launch_bounds__(256, 3) k3_jacobi(Geo g, int xb, int nch, Leve
     su.arr[1] = S3Array{f, 1, S3Center};
     su.arr[2] = S3Array{dinv, 0, S3Center};
     su.kap = kap;
-    Op3Jacobi<DOT> op{omega, zout, g.n, 0.0};
-    march3<3>(g, xb, nch, lt, su, op);
+    Op3Jacobi<DOT> op{omega, zout, g.n, 0.0, {0.0, 0.0, 0.0}};
+    int last;
+    march3<3>(g, lt, su, op, last);
     if (DOT) {
-        double v3[3] = {0.0, 0.0, 0.0};
-        v3[blockIdx.z / nch] = op.acc;
+        if (last >= 0) op.acc3[last] += op.acc;
+        double v3[3] = {op.acc3[0], op.acc3[1], op.acc3[2]};
         if (reduce_finalize<3>(v3, partials, counter, sc->red)) {
             for (int cc = 0; cc < 3; ++cc) {
                 const double rz = sc->red[cc];
@@ -1266,10 +1277,11 @@ __global__ void __launch_bounds__(256, 3) k3_spmv(Geo g, int xb, int nch, LevelT
     S3Setup<1> su;
     su.arr[0] = S3Array{p, 1, S3Halo};
     su.kap = kap;
-    Op3Spmv op{q, g.n, 0.0};
-    march3<1>(g, xb, nch, lt, su, op);
-    double v3[3] = {0.0, 0.0, 0.0};
-    v3[blockIdx.z / nch] = op.acc;
+    Op3Spmv op{q, g.n, 0.0, {0.0, 0.0, 0.0}};
+    int last;
+    march3<1>(g, lt, su, op, last);
+    if (last >= 0) op.acc3[last] += op.acc;
+    double v3[3] = {op.acc3[0], op.acc3[1], op.acc3[2]};
     if (reduce_finalize<3>(v3, partials, counter, sc->red + 3)) {
         for (int cc = 0; cc < 3; ++cc) {
             const double pq = sc->red[3 + cc];
@@ -1279,15 +1291,22 @@ __global__ void __launch_bounds__(256, 3) k3_spmv(Geo g, int xb, int nch, LevelT
     }
 }
 
-static inline int s3_xb(const Geo& g) {
-    static const int env_xb = getenv("OTM_XB3") ? atoi(getenv("OTM_XB3")) : 0;
-    int xb = env_xb > 0 ? env_xb : 16;
-    if (xb > g.nx) xb = g.nx;
-    return xb;
+static bool s3_enabled() {     // OTM_NO_S3=1 falls back to the k2 register-window kernels
+    static const bool off = getenv("OTM_NO_S3") != nullptr;
+    return !off;
 }
-static bool s3_enabled() {     // opt-in (OTM_S3=1): slower than the k2 register window so far
-    static const bool on = getenv("OTM_S3") != nullptr;
-    return on;
+// persistent grid: resident blocks of the kernel x SMs (capped by the work units)
+template <class K>
+static dim3 s3_grid(K kernel, size_t smem, const Geo& g) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem);
+    if (per_sm < 1) per_sm = 1;
+    const long long units = 3LL * (g.nz / kTileZ) * (g.ny / kTileY) * g.nx;
+    long long b = (long long)per_sm * sms;
+    if (b > units) b = units;
+    return dim3((unsigned)b, 1, 1);
 }
 template <class K>
 static void s3_attr(K kernel, size_t bytes) {
@@ -1558,12 +1577,10 @@ void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, co
         return;
     }
     if (fast_tiling(g, lt) && s3_enabled()) {
-        int nch;
-        const int xb = s3_xb(g);
-        const dim3 grid = fast_grid(g, xb, &nch);
         const size_t sm = s3_smem_bytes<2>();
         s3_attr(k3_smooth_res, sm);
-        k3_smooth_res<<<grid, dim3(32, kTileY), sm, s>>>(g, xb, nch, lt, kap, f, dinv, omega, z, res);
+        k3_smooth_res<<<s3_grid(k3_smooth_res, sm, g), dim3(32, kTileY), sm, s>>>(g, 0, 0, lt, kap, f, dinv, omega,
+                                                                                 z, res);
         return;
     }
     if (fast_tiling(g, lt)) {
@@ -1590,18 +1607,15 @@ void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const 
         return;
     }
     if (fast_tiling(g, lt) && s3_enabled()) {
-        int nch;
-        const int xb = s3_xb(g);
-        const dim3 grid = fast_grid(g, xb, &nch);
         const size_t sm = s3_smem_bytes<3>();
         if (dot) {
             s3_attr(k3_jacobi<true>, sm);
-            k3_jacobi<true><<<grid, dim3(32, kTileY), sm, s>>>(g, xb, nch, lt, kap, z, f, dinv, omega, zout,
-                                                               red.partials, red.counter, sc);
+            k3_jacobi<true><<<s3_grid(k3_jacobi<true>, sm, g), dim3(32, kTileY), sm, s>>>(
+                g, 0, 0, lt, kap, z, f, dinv, omega, zout, red.partials, red.counter, sc);
         } else {
             s3_attr(k3_jacobi<false>, sm);
-            k3_jacobi<false><<<grid, dim3(32, kTileY), sm, s>>>(g, xb, nch, lt, kap, z, f, dinv, omega, zout,
-                                                                nullptr, nullptr, sc);
+            k3_jacobi<false><<<s3_grid(k3_jacobi<false>, sm, g), dim3(32, kTileY), sm, s>>>(
+                g, 0, 0, lt, kap, z, f, dinv, omega, zout, nullptr, nullptr, sc);
         }
         return;
     }
@@ -1627,12 +1641,10 @@ void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const 
 void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* p,
                  float* q, Red& red, PcgScalars* sc) {
     if (fast_tiling(g, lt) && s3_enabled()) {
-        int nch;
-        const int xb = s3_xb(g);
-        const dim3 grid = fast_grid(g, xb, &nch);
         const size_t sm = s3_smem_bytes<1>();
         s3_attr(k3_spmv, sm);
-        k3_spmv<<<grid, dim3(32, kTileY), sm, s>>>(g, xb, nch, lt, kap, p, q, red.partials, red.counter, sc);
+        k3_spmv<<<s3_grid(k3_spmv, sm, g), dim3(32, kTileY), sm, s>>>(g, 0, 0, lt, kap, p, q, red.partials,
+                                                                      red.counter, sc);
         return;
     }
     if (fast_tiling(g, lt)) {

@@ -134,16 +134,11 @@ __device__ __forceinline__ void s3_issue(const Geo& g, const S3Setup<NARR>& su, 
 //     slot = ring slot of the output plane x (for center-only arrays), r = tile row of the thread (1..8),
 //     col = smem column of vertex z (z+1 is col+1)
 template <int NARR, class Op>
-__device__ __forceinline__ void march3(const Geo& g, int xb, int nch, const LevelTemplate& lt,
-                                       const S3Setup<NARR>& su, Op& op) {
+__device__ __forceinline__ void march3_segment(const Geo& g, const LevelTemplate& lt, const S3Setup<NARR>& su,
+                                               Op& op, int c, int y0, int z0, int x0, int x1) {
     extern __shared__ float4 s3_smem4[];
     float* smem = reinterpret_cast<float*>(s3_smem4);
     constexpr int SLOT = s3_slot_floats<NARR>();
-    const int c = blockIdx.z / nch;
-    const int ch = blockIdx.z - c * nch;
-    const int z0 = blockIdx.x * kTileZ, y0 = blockIdx.y * kTileY;
-    const int x0 = ch * xb, x1 = min(g.nx, x0 + xb);
-    if (x0 >= x1) return;   // uniform per block
     S3Task mine[kMaxTasks];
     s3_tasks<NARR>(g, su, c, y0, z0, mine);
     const int nplanes = (x1 - x0) + 2;          // operand planes x0-1 .. x1 (factors x0-1 .. x1-1 suffice)
@@ -239,6 +234,35 @@ __device__ __forceinline__ void march3(const Geo& g, int xb, int nch, const Leve
             for (int m = 0; m < 4; ++m) P1[j][m] = P2[j][m];
     }
     cp_wait<0>();
+    __syncthreads();   // the next segment reuses the ring
+}
+
+// Persistent schedule: the work is the list of (case, tile column, x plane) units,
+// column-major in x; block b takes the contiguous range [b W / B, (b+1) W / B) and
+// walks it as one segment per tile column it touches.  B = resident blocks, so every
+// SM gets the same number of planes whatever the grid shape.
+template <int NARR, class Op>
+__device__ __forceinline__ void march3(const Geo& g, const LevelTemplate& lt, const S3Setup<NARR>& su, Op& op,
+                                       int& last_case) {
+    const int tz = g.nz / kTileZ, ty = g.ny / kTileY;
+    const long long cols = 3LL * tz * ty;
+    const long long W = cols * g.nx;
+    const long long B = gridDim.x;
+    long long u = W * blockIdx.x / B;
+    const long long u1 = W * (blockIdx.x + 1) / B;
+    last_case = -1;
+    while (u < u1) {
+        const long long col = u / g.nx;
+        const int x0 = (int)(u - col * g.nx);
+        const int x1 = (int)min((long long)g.nx, x0 + (u1 - u));
+        const int c = (int)(col / ((long long)tz * ty));
+        const int rest = (int)(col - (long long)c * tz * ty);
+        const int y0 = (rest / tz) * kTileY, z0 = (rest - (rest / tz) * tz) * kTileZ;
+        op.begin_case(c, last_case);
+        march3_segment<NARR>(g, lt, su, op, c, y0, z0, x0, x1);
+        last_case = c;
+        u += x1 - x0;
+    }
 }
 
 }  // namespace otm
