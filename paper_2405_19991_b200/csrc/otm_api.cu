@@ -75,6 +75,8 @@ struct otm_ctx {
     double* scal = nullptr;      // generic device scalars (128)
     double* h = nullptr;         // pinned host mirror (256)
     int* changed = nullptr;      // device flag
+    OcCtl* ocl = nullptr;        // cooperative OC search state
+    bool no_coop = getenv("OTM_NO_COOP_OC") != nullptr;
     bool built = false;
     bool no_loop_graph = false;
     bool no_tail = getenv("OTM_TAIL") == nullptr;   // single-CTA tail: opt-in, slower so far
@@ -560,7 +562,8 @@ int otm_create(otm_ctx** out, int nx, int ny, int nz, const otm_params* pin) {
     CK(dalloc(ctx, &ctx->scal, 128));
     CK(cudaMemset(ctx->scal, 0, 128 * sizeof(double)));
     CK(dalloc(ctx, &ctx->changed, 4));
-    CK(cudaMallocHost((void**)&ctx->h, 512 * sizeof(double)));
+    CK(dalloc(ctx, &ctx->ocl, 1));
+    CK(cudaMallocHost((void**)&ctx->h, 1024 * sizeof(double)));
     CK(cudaMemset(ctx->T64, 0, 3 * n * sizeof(double)));
     CK(cudaMemset(ctx->p, 0, 3 * n * sizeof(float)));
     CK(cudaEventCreate(&ctx->ev_a));
@@ -582,7 +585,7 @@ int otm_destroy(otm_ctx* ctx) {
         if (l > 0) F(ctx->L[l].f);
     }
     F(ctx->G); F(ctx->gj); F(ctx->red.partials); F(ctx->red.counter); F(ctx->sc); F(ctx->scal);
-    F(ctx->changed); F(ctx->fs.offs_dev); F(ctx->fs.wts_dev);
+    F(ctx->changed); F(ctx->ocl); F(ctx->fs.offs_dev); F(ctx->fs.wts_dev);
     if (ctx->h) cudaFreeHost(ctx->h);
     if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
     if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
@@ -894,6 +897,48 @@ int otm_means(otm_ctx* ctx, const double* rho, double p, double out[2]) {
     return OTM_OK;
 }
 
+// Cooperative single-launch search (k_oc_coop); V_retry = NaN disables the
+// frozen-state retry.  Returns OTM_ECUDA if the cooperative launch is unavailable.
+static int oc_search_coop(otm_ctx* ctx, const double* rho, const double* sens, double V, double V_retry,
+                          const otm_oc_params* pp, double* rho_out, double* lam_out, int* active_out,
+                          int* changed_out, int* retried_out) {
+    cudaStream_t s = ctx->stream;
+    OcArgs a;
+    a.step = pp->step_limit;
+    a.rmin = pp->min_density;
+    a.damp = pp->damp;
+    a.floor_ratio = std::pow(1e-10, pp->damp);
+    a.sqrt_damp = pp->damp == 0.5;
+    OcCtl init;
+    std::memset(&init, 0, sizeof init);
+    init.V = V;
+    init.V_retry = V_retry;
+    init.bis_tol = pp->bisection_tol;
+    std::memcpy(ctx->h + 256, &init, sizeof init);
+    CK(cudaMemcpyAsync(ctx->ocl, ctx->h + 256, sizeof init, cudaMemcpyHostToDevice, s));
+    {
+        ProfScope ps(ctx, kProfOC, 0.0);
+        if (launch_oc_coop(s, ctx->g0.n, rho, sens, a, rho_out, ctx->ocl, ctx->red.partials)) {
+            cudaGetLastError();
+            return OTM_ECUDA;
+        }
+    }
+    ctx->launches++;
+    CK(cudaMemcpyAsync(ctx->h + 256, ctx->ocl, sizeof init, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    OcCtl fin;
+    std::memcpy(&fin, ctx->h + 256, sizeof fin);
+    if (ctx->prof) ctx->prof_bytes[kProfOC] += (16.0 * fin.passes + 24.0 * (1 + fin.retried)) * ctx->g0.n;
+    if (lam_out) *lam_out = fin.lam;
+    if (active_out) *active_out = fin.active;
+    if (changed_out) *changed_out = fin.changed;
+    if (retried_out) *retried_out = fin.retried;
+    static const bool debug = getenv("OTM_DEBUG") != nullptr;
+    if (debug) fprintf(stderr, "[otm] oc: passes %d retried %d lam %.6e active %d\n", fin.passes, fin.retried,
+                       fin.lam, fin.active);
+    return OTM_OK;
+}
+
 // oc_update (optimize.py:114-160).  The reference's sequential multiplier search
 // (bracket l2 *= 4, then bisection of [1e-30, l2] with its two stopping rules) is
 // replayed exactly on the host; the device evaluates the candidate means of up to
@@ -905,6 +950,11 @@ int otm_oc_update(otm_ctx* ctx, const double* rho, const double* sens, double V,
     if (!(pp->min_density >= 0.0 && pp->min_density < 1.0) || !(pp->step_limit > 0.0 && pp->step_limit <= 1.0) ||
         !(pp->damp > 0.0 && pp->damp <= 1.0))
         return fail(ctx, OTM_EINVAL, "invalid OC parameters");
+    if (!ctx->no_coop) {
+        const int rc = oc_search_coop(ctx, rho, sens, V, NAN, pp, rho_out, lam_out, active_out, changed_out, nullptr);
+        if (rc == OTM_OK) return OTM_OK;
+        ctx->no_coop = true;   // fall back to host-driven passes for this context
+    }
     cudaStream_t s = ctx->stream;
     const long long n = ctx->g0.n;
     OcArgs a;
@@ -1126,7 +1176,30 @@ int otm_run_update(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, d
     int active, changed;
     int rc;
     const double mean_rho = st->mean_rho;
-    if (cfg->model == 0) {
+    if (cfg->model == 0 && !ctx->no_coop) {
+        // governor + OC step + frozen-state retry in one cooperative launch
+        double vb = otm_governor_update(&st->gov, st->g, mean_rho, st->mean_rho_p);
+        vb = std::min(vb, mean_rho + 0.5 * cfg->oc.step_limit);
+        rc = oc_search_coop(ctx, rho, ctx->sens, vb, mean_rho - 0.25 * cfg->oc.step_limit, &cfg->oc, rho, &lam,
+                            &active, &changed, nullptr);
+        if (rc == OTM_OK) {
+            if (cfg->symmetry == 1) {
+                launch_symmetrize(ctx->stream, ctx->g0, rho);
+                ctx->launches++;
+            }
+            CKL();
+            return OTM_OK;
+        }
+        ctx->no_coop = true;
+        // the governor already advanced: fall through to the host-driven passes with the same bound
+        rc = otm_oc_update(ctx, rho, ctx->sens, vb, &cfg->oc, rho, &lam, &active, &changed);
+        if (rc) return rc;
+        if (!changed) {
+            rc = otm_oc_update(ctx, rho, ctx->sens, mean_rho - 0.25 * cfg->oc.step_limit, &cfg->oc, rho, &lam,
+                               &active, &changed);
+            if (rc) return rc;
+        }
+    } else if (cfg->model == 0) {
         double vb = otm_governor_update(&st->gov, st->g, mean_rho, st->mean_rho_p);
         vb = std::min(vb, mean_rho + 0.5 * cfg->oc.step_limit);
         rc = otm_oc_update(ctx, rho, ctx->sens, vb, &cfg->oc, rho, &lam, &active, &changed);

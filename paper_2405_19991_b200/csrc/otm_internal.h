@@ -40,6 +40,25 @@ struct OcArgs {
     int sqrt_damp;
 };
 
+// Device-resident state of the cooperative OC search (k_oc_coop).
+struct OcCtl {
+    double V;            // volume bound of the current search
+    double V_retry;      // bound of the frozen-state retry (NaN: none)
+    double bis_tol;
+    double l1, l2;
+    int phase;           // 0 first pass, 1 bracket, 2 bisection tree, 3 apply
+    int bracket_it;
+    int nlam;
+    int active;
+    int changed;
+    int retried;
+    int passes;
+    double lam;
+    double lams[kOcLam];
+    double lam_pow[kOcLam];
+    double means[kOcLam];
+};
+
 // Device-resident scalars of the batched PCG (3 load cases).
 struct PcgScalars {
     double red[16];
@@ -132,6 +151,8 @@ void launch_sens(cudaStream_t s, const Geo& g, const double* T, const double* rf
                  const Dg& dG, double* sens);
 void launch_oc_eval(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a, int nlam,
                     const LamSet& lam_pow, Red& red, double* out);
+int launch_oc_coop(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a,
+                   double* rho_out, OcCtl* ctl, double* partials);
 void launch_oc_apply(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a,
                      double lam, double* rho_out, int* changed);
 

@@ -5,12 +5,15 @@
 #include "otm_internal.h"
 #include "otm_stencil2.cuh"
 #include "otm_stencil3.cuh"
+#include "otm_stencil4.cuh"
 
 #ifndef OTM_MINB
 #define OTM_MINB 2   // min resident blocks of the fp32 fast-path stencils (register cap 128)
 #endif
 
 #include <math.h>
+
+#include <cooperative_groups.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -1000,6 +1003,207 @@ __global__ void __launch_bounds__(256, 2) k_oc_eval(long long n, const double* _
     }
 }
 
+// The whole oc_update (optimize.py:114-160) in one cooperative launch.  Every
+// pass evaluates the candidate means of up to 32 multipliers (as k_oc_eval);
+// between passes, thread 0 of block 0 replays the reference's sequential search
+// (free step, bracket l2 *= 4, bisection of [1e-30, l2] with its two stopping
+// rules) over the evaluated means, exactly as the host version did, and picks the
+// next multipliers.  Then the density is written with the exact expression and,
+// if nothing changed and a retry bound is set (optimize.py:355-362), the search
+// reruns once with that bound.
+__device__ double oc_lam_pow(const OcArgs& a, double lam) {
+    return a.sqrt_damp ? 1.0 / sqrt(lam) : pow(lam, -a.damp);
+}
+
+__device__ void oc_plan_first(OcCtl* C, const OcArgs& a) {
+    C->phase = 0;
+    C->lams[0] = 0.0;
+    double l2 = 1.0;
+    for (int k = 1; k < kOcLam; ++k) { C->lams[k] = l2; l2 *= 4.0; }
+    C->nlam = kOcLam;
+}
+
+__device__ void oc_plan_tree(OcCtl* C) {
+    // BFS subtree of midpoints below (l1, l2): node i covers (lo, hi); children (lo, mid), (mid, hi)
+    const int nodes = kOcLam - 1;
+    double lo[kOcLam], hi[kOcLam];
+    lo[0] = C->l1;
+    hi[0] = C->l2;
+    for (int i = 0; i < nodes; ++i) {
+        const double mid = 0.5 * (lo[i] + hi[i]);
+        C->lams[i] = mid;
+        if (2 * i + 2 < nodes) {
+            lo[2 * i + 1] = lo[i]; hi[2 * i + 1] = mid;
+            lo[2 * i + 2] = mid;  hi[2 * i + 2] = hi[i];
+        }
+    }
+    C->nlam = nodes;
+    C->phase = 2;
+}
+
+// consume C->means of the pass just evaluated; plan the next pass or finish
+__device__ void oc_walk(OcCtl* C) {
+    const double V = C->V;
+    C->passes += 1;
+    if (C->phase == 0) {
+        if (C->means[0] <= V) { C->lam = 0.0; C->active = 0; C->phase = 3; return; }
+        C->l2 = 1.0;
+        C->bracket_it = 0;
+        for (int k = 1; k < kOcLam; ++k) {
+            if (C->means[k] <= V) { C->l1 = 1e-30; oc_plan_tree(C); return; }
+            C->l2 *= 4.0;
+            if (++C->bracket_it >= 200) { C->l1 = 1e-30; oc_plan_tree(C); return; }
+        }
+        // bracket continues from l2
+        double v = C->l2;
+        int k = 0;
+        for (; k < kOcLam && C->bracket_it + k < 200; ++k) { C->lams[k] = v; v *= 4.0; }
+        C->nlam = k;
+        C->phase = 1;
+        return;
+    }
+    if (C->phase == 1) {
+        for (int k = 0; k < C->nlam; ++k) {
+            if (C->means[k] <= V) { C->l1 = 1e-30; oc_plan_tree(C); return; }
+            C->l2 *= 4.0;
+            if (++C->bracket_it >= 200) { C->l1 = 1e-30; oc_plan_tree(C); return; }
+        }
+        double v = C->l2;
+        int k = 0;
+        for (; k < kOcLam && C->bracket_it + k < 200; ++k) { C->lams[k] = v; v *= 4.0; }
+        C->nlam = k;
+        return;
+    }
+    // phase 2: walk the evaluated subtree
+    int node = 0;
+    const int nodes = kOcLam - 1;
+    double l1 = C->l1, l2 = C->l2;
+    while (true) {
+        if (!((l2 - l1) / (l1 + l2) > 1e-13)) { C->lam = 0.5 * (l1 + l2); C->active = 1; C->phase = 3; return; }
+        if (node >= nodes) break;
+        const double m = 0.5 * (l1 + l2);
+        const double cur = C->means[node];
+        if (cur > V) { l1 = m; node = 2 * node + 2; }
+        else { l2 = m; node = 2 * node + 1; }
+        if (fabs(cur - V) <= C->bis_tol) { C->lam = 0.5 * (l1 + l2); C->active = 1; C->phase = 3; return; }
+    }
+    C->l1 = l1;
+    C->l2 = l2;
+    oc_plan_tree(C);
+}
+
+__global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* __restrict__ rho,
+                                                    const double* __restrict__ sens, const OcArgs a,
+                                                    double* rho_out, OcCtl* C, double* partials) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sm[32][33];
+    __shared__ double s_lp[kOcLam];
+    __shared__ int s_nlam, s_phase;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const double M = (double)n;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        C->passes = 0;
+        C->retried = 0;
+        oc_plan_first(C, a);
+        for (int k = 0; k < kOcLam; ++k) C->lam_pow[k] = k < C->nlam && C->lams[k] != 0.0 ? oc_lam_pow(a, C->lams[k]) : 0.0;
+    }
+    while (true) {
+        grid.sync();
+        if (threadIdx.x == 0) { s_phase = *(volatile int*)&C->phase; s_nlam = *(volatile int*)&C->nlam; }
+        if (threadIdx.x < kOcLam) s_lp[threadIdx.x] = ((volatile double*)C->lam_pow)[threadIdx.x];
+        __syncthreads();
+        if (s_phase == 3) {
+            // exact candidate of the chosen multiplier (reference expression)
+            const double lam = *(volatile double*)&C->lam;
+            int ch = 0;
+            for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+                 i += (long long)gridDim.x * blockDim.x) {
+                const double r = rho[i];
+                const double desc = M * (-sens[i]);
+                const double lo = fmax(r - a.step, a.rmin), hi = fmin(r + a.step, 1.0);
+                double out;
+                if (lam == 0.0) {
+                    out = desc > 0.0 ? hi : (desc < 0.0 ? lo : r);
+                } else {
+                    const double q = fmax(desc / lam, 1e-10);
+                    const double ratio = a.sqrt_damp ? sqrt(q) : pow(q, a.damp);
+                    out = fmin(fmax(r * ratio, lo), hi);
+                }
+                ch |= out != r;
+                rho_out[i] = out;
+            }
+            ch = __syncthreads_or(ch);
+            if (threadIdx.x == 0) partials[blockIdx.x] = ch ? 1.0 : 0.0;
+            grid.sync();
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                int any = 0;
+                for (unsigned b = 0; b < gridDim.x; ++b) any |= __ldcg(partials + b) != 0.0;
+                C->changed = any;
+                if (!any && !C->retried && !isnan(C->V_retry)) {
+                    C->retried = 1;
+                    C->V = C->V_retry;
+                    oc_plan_first(C, a);
+                    for (int k = 0; k < kOcLam; ++k)
+                        C->lam_pow[k] = k < C->nlam && C->lams[k] != 0.0 ? oc_lam_pow(a, C->lams[k]) : 0.0;
+                } else {
+                    C->phase = 4;
+                }
+            }
+            grid.sync();
+            if (*(volatile int*)&C->phase == 4) break;
+            continue;
+        }
+        // ---- one evaluation pass ----
+        double acc[kOcLam];
+#pragma unroll
+        for (int k = 0; k < kOcLam; ++k) acc[k] = 0.0;
+        const int nlam = s_nlam;
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+             i += (long long)gridDim.x * blockDim.x) {
+            const double r = __ldg(rho + i);
+            const double desc = M * (-__ldg(sens + i));
+            const double lo = fmax(r - a.step, a.rmin), hi = fmin(r + a.step, 1.0);
+            const double lof = fmax(lo, r * a.floor_ratio);
+            const double ce = desc > 0.0 ? r * (a.sqrt_damp ? sqrt(desc) : pow(desc, a.damp)) : 0.0;
+            const double freev = desc > 0.0 ? hi : (desc < 0.0 ? lo : r);
+#pragma unroll
+            for (int k = 0; k < kOcLam; ++k) {
+                const double lp = s_lp[k];
+                const double cand = lp == 0.0 ? freev : fmin(fmax(ce * lp, lof), hi);
+                acc[k] += k < nlam ? cand : 0.0;
+            }
+        }
+        const double mine = warp_reduce_scatter32(acc);
+        sm[wid][lane] = mine;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            double t = 0.0;
+            for (int w = 0; w < nw; ++w) t += sm[w][threadIdx.x];
+            partials[(size_t)blockIdx.x * 32 + threadIdx.x] = t;
+        }
+        grid.sync();
+        if (blockIdx.x == 0) {
+            double t = 0.0;
+            for (unsigned b = wid; b < gridDim.x; b += nw) t += __ldcg(partials + (size_t)b * 32 + lane);
+            sm[wid][lane] = t;
+            __syncthreads();
+            if (threadIdx.x < 32) {
+                double u = 0.0;
+                for (int w = 0; w < nw; ++w) u += sm[w][threadIdx.x];
+                C->means[threadIdx.x] = u / M;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                oc_walk(C);
+                for (int k = 0; k < kOcLam; ++k)
+                    C->lam_pow[k] = k < C->nlam && C->lams[k] != 0.0 ? oc_lam_pow(a, C->lams[k]) : 0.0;
+            }
+        }
+    }
+}
+
 // Exact candidate for the chosen multiplier (lam == 0: free step), written to
 // rho_out; flags[0] |= any(rho_out != rho).
 __global__ void k_oc_apply(long long n, const double* __restrict__ rho, const double* __restrict__ sens,
@@ -1291,9 +1495,9 @@ __global__ void __launch_bounds__(256, 3) k3_spmv(Geo g, int xb, int nch, LevelT
     }
 }
 
-static bool s3_enabled() {     // OTM_NO_S3=1 falls back to the k2 register-window kernels
-    static const bool off = getenv("OTM_NO_S3") != nullptr;
-    return !off;
+static bool s3_enabled() {     // OTM_K=3
+    static const bool on = getenv("OTM_K") && atoi(getenv("OTM_K")) == 3;
+    return on;
 }
 // persistent grid: resident blocks of the kernel x SMs (capped by the work units)
 template <class K>
@@ -1311,6 +1515,135 @@ static dim3 s3_grid(K kernel, size_t smem, const Geo& g) {
 template <class K>
 static void s3_attr(K kernel, size_t bytes) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+// ---- k4: three cases per thread, 21 weights, FFMA2 (otm_stencil4.cuh) ----
+struct Op4SmoothRes {     // tiles: f case 0..2 (halo), D^-1 (halo); operand = w D^-1 f
+    static constexpr int NT = 4;
+    float omega; float* z; float* res; long long n;
+    __device__ __forceinline__ float op1(const float* S, int c, int r, int col) const {
+        return omega * *s3_at(S, 3, r, col) * *s3_at(S, c, r, col);
+    }
+    __device__ __forceinline__ float2 op2(const float* S, int c, int r, int col) const {
+        const float2 d = *reinterpret_cast<const float2*>(s3_at(S, 3, r, col));
+        const float2 f = *reinterpret_cast<const float2*>(s3_at(S, c, r, col));
+        return make_float2(omega * d.x * f.x, omega * d.y * f.y);
+    }
+    __device__ __forceinline__ void prefetch(int, long long) {}
+    __device__ __forceinline__ void sink(const float* S0, int c, long long v, int r, int col, float2 kz, float2 zc) {
+        const float2 f = *reinterpret_cast<const float2*>(s3_at(S0, c, r, col));
+        *reinterpret_cast<float2*>(z + c * n + v) = zc;
+        *reinterpret_cast<float2*>(res + c * n + v) = make_float2(f.x - kz.x, f.y - kz.y);
+    }
+};
+
+template <bool DOT>
+struct Op4Jacobi {        // tiles: z case 0..2 (halo); f and D^-1 prefetched into registers
+    static constexpr int NT = 3;
+    const float* f; const float* dinv; float omega; float* zout; long long n;
+    float2 fp[3], dp;
+    double acc[3];
+    __device__ __forceinline__ float op1(const float* S, int c, int r, int col) const { return *s3_at(S, c, r, col); }
+    __device__ __forceinline__ float2 op2(const float* S, int c, int r, int col) const {
+        return *reinterpret_cast<const float2*>(s3_at(S, c, r, col));
+    }
+    long long pl;
+    __device__ __forceinline__ void prefetch(int x, long long vrow) {
+        const long long v = vrow + (long long)x * pl;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) fp[c] = __ldg(reinterpret_cast<const float2*>(f + c * n + v));
+        dp = __ldg(reinterpret_cast<const float2*>(dinv + v));
+    }
+    __device__ __forceinline__ void sink(const float*, int c, long long v, int, int, float2 kz, float2 zc) {
+        const float z0 = zc.x + omega * dp.x * (fp[c].x - kz.x);
+        const float z1 = zc.y + omega * dp.y * (fp[c].y - kz.y);
+        *reinterpret_cast<float2*>(zout + c * n + v) = make_float2(z0, z1);
+        if (DOT) acc[c] += (double)fp[c].x * (double)z0 + (double)fp[c].y * (double)z1;
+    }
+};
+
+struct Op4Spmv {          // tiles: p case 0..2 (halo)
+    static constexpr int NT = 3;
+    float* q; long long n; double acc[3];
+    __device__ __forceinline__ float op1(const float* S, int c, int r, int col) const { return *s3_at(S, c, r, col); }
+    __device__ __forceinline__ float2 op2(const float* S, int c, int r, int col) const {
+        return *reinterpret_cast<const float2*>(s3_at(S, c, r, col));
+    }
+    __device__ __forceinline__ void prefetch(int, long long) {}
+    __device__ __forceinline__ void sink(const float*, int c, long long v, int, int, float2 kp, float2 pc) {
+        *reinterpret_cast<float2*>(q + c * n + v) = kp;
+        acc[c] += (double)pc.x * (double)kp.x + (double)pc.y * (double)kp.y;
+    }
+};
+
+__global__ void __launch_bounds__(256, 2) k4_smooth_res(Geo g, LevelTemplate lt, const float* kap, const float* f,
+                                                        const float* dinv, float omega, float* z, float* res) {
+    S4Setup su;
+    su.arr[0] = f; su.arr[1] = f + g.n; su.arr[2] = f + 2 * g.n; su.arr[3] = dinv;
+    su.narr = 4;
+    su.kap = kap;
+    Op4SmoothRes op{omega, z, res, g.n};
+    march4(g, lt, su, op);
+}
+
+template <bool DOT>
+__global__ void __launch_bounds__(256, 2) k4_jacobi(Geo g, LevelTemplate lt, const float* kap, const float* z,
+                                                    const float* f, const float* dinv, float omega, float* zout,
+                                                    double* partials, unsigned* counter, PcgScalars* sc) {
+    S4Setup su;
+    su.arr[0] = z; su.arr[1] = z + g.n; su.arr[2] = z + 2 * g.n; su.arr[3] = nullptr;
+    su.narr = 3;
+    su.kap = kap;
+    Op4Jacobi<DOT> op;
+    op.f = f; op.dinv = dinv; op.omega = omega; op.zout = zout; op.n = g.n; op.pl = g.pl;
+    op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
+    march4(g, lt, su, op);
+    if (DOT) {
+        double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
+        if (reduce_finalize<3>(v3, partials, counter, sc->red)) {
+            for (int cc = 0; cc < 3; ++cc) {
+                const double rz = sc->red[cc];
+                sc->beta[cc] = (sc->first || sc->rz[cc] == 0.0) ? 0.0 : rz / sc->rz[cc];
+                sc->rz[cc] = rz;
+            }
+            sc->first = 0;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256, 2) k4_spmv(Geo g, LevelTemplate lt, const float* kap, const float* p,
+                                                  float* q, double* partials, unsigned* counter, PcgScalars* sc) {
+    S4Setup su;
+    su.arr[0] = p; su.arr[1] = p + g.n; su.arr[2] = p + 2 * g.n; su.arr[3] = nullptr;
+    su.narr = 3;
+    su.kap = kap;
+    Op4Spmv op{q, g.n, {0.0, 0.0, 0.0}};
+    march4(g, lt, su, op);
+    double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
+    if (reduce_finalize<3>(v3, partials, counter, sc->red + 3)) {
+        for (int cc = 0; cc < 3; ++cc) {
+            const double pq = sc->red[3 + cc];
+            sc->pq[cc] = pq;
+            sc->alpha[cc] = (sc->active[cc] != 0.0 && pq > 0.0) ? sc->rz[cc] / pq : 0.0;
+        }
+    }
+}
+
+static int kernel_gen() {     // OTM_K=2|3|4 selects the fast-path stencil generation (default 4)
+    static const int k = getenv("OTM_K") ? atoi(getenv("OTM_K")) : 4;
+    return k;
+}
+template <class K>
+static dim3 s4_grid(K kernel, size_t smem, const Geo& g) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem);
+    if (per_sm < 1) per_sm = 1;
+    const long long units = (long long)(g.nz / kTileZ) * (g.ny / kTileY) * g.nx;
+    long long b = (long long)per_sm * sms;
+    if (b > units) b = units;
+    return dim3((unsigned)b, 1, 1);
 }
 
 static inline dim3 fast_grid(const Geo& g, int xb, int* nch) {
@@ -1571,6 +1904,12 @@ static inline bool small_level(const Geo& g) { return g.n <= 65536; }
 
 void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* f,
                        const float* dinv, float omega, float* z, float* res) {
+    if (fast_tiling(g, lt) && kernel_gen() == 4) {
+        const size_t sm = s4_smem_bytes<4>();
+        s3_attr(k4_smooth_res, sm);
+        k4_smooth_res<<<s4_grid(k4_smooth_res, sm, g), dim3(32, kTileY), sm, s>>>(g, lt, kap, f, dinv, omega, z, res);
+        return;
+    }
     if (!fast_tiling(g, lt) && small_level(g)) {
         k_small<0, false><<<nblk(3 * g.n, 256), 256, 0, s>>>(g, lt, kap, nullptr, f, dinv, omega, z, res, nullptr,
                                                              nullptr, nullptr);
@@ -1597,6 +1936,19 @@ void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, co
 void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* z,
                    const float* f, const float* dinv, float omega, float* zout, bool dot, Red& red,
                    PcgScalars* sc) {
+    if (fast_tiling(g, lt) && kernel_gen() == 4) {
+        const size_t sm = s4_smem_bytes<3>();
+        if (dot) {
+            s3_attr(k4_jacobi<true>, sm);
+            k4_jacobi<true><<<s4_grid(k4_jacobi<true>, sm, g), dim3(32, kTileY), sm, s>>>(
+                g, lt, kap, z, f, dinv, omega, zout, red.partials, red.counter, sc);
+        } else {
+            s3_attr(k4_jacobi<false>, sm);
+            k4_jacobi<false><<<s4_grid(k4_jacobi<false>, sm, g), dim3(32, kTileY), sm, s>>>(
+                g, lt, kap, z, f, dinv, omega, zout, nullptr, nullptr, sc);
+        }
+        return;
+    }
     if (!fast_tiling(g, lt) && small_level(g)) {
         if (dot)
             k_small<1, true><<<nblk(3 * g.n, 256), 256, 0, s>>>(g, lt, kap, z, f, dinv, omega, zout, nullptr,
@@ -1640,6 +1992,13 @@ void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const 
 }
 void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* p,
                  float* q, Red& red, PcgScalars* sc) {
+    if (fast_tiling(g, lt) && kernel_gen() == 4) {
+        const size_t sm = s4_smem_bytes<3>();
+        s3_attr(k4_spmv, sm);
+        k4_spmv<<<s4_grid(k4_spmv, sm, g), dim3(32, kTileY), sm, s>>>(g, lt, kap, p, q, red.partials, red.counter,
+                                                                      sc);
+        return;
+    }
     if (fast_tiling(g, lt) && s3_enabled()) {
         const size_t sm = s3_smem_bytes<1>();
         s3_attr(k3_spmv, sm);
@@ -1708,6 +2067,21 @@ void launch_oc_eval(cudaStream_t s, long long n, const double* rho, const double
     long long want = (n + 255) / 256;
     unsigned blocks = (unsigned)(want < 592 ? want : 592);
     k_oc_eval<<<blocks, 256, 0, s>>>(n, rho, sens, a, nlam, lam_pow, red.partials, red.counter, out);
+}
+int launch_oc_coop(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a,
+                   double* rho_out, OcCtl* ctl, double* partials) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_oc_coop, 256, 0);
+    if (per_sm < 1) return 1;
+    long long want = (n + 255) / 256;
+    long long blocks = (long long)per_sm * sms;
+    if (blocks > want) blocks = want;
+    if (blocks < 1) blocks = 1;
+    void* args[] = {(void*)&n, (void*)&rho, (void*)&sens, (void*)&a, (void*)&rho_out, (void*)&ctl, (void*)&partials};
+    return cudaLaunchCooperativeKernel((void*)k_oc_coop, dim3((unsigned)blocks), dim3(256), args, 0, s) == cudaSuccess
+               ? 0 : 1;
 }
 void launch_oc_apply(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a,
                      double lam, double* rho_out, int* changed) {
