@@ -78,7 +78,7 @@ struct otm_ctx {
     OcCtl* ocl = nullptr;        // cooperative OC search state
     bool no_coop = getenv("OTM_NO_COOP_OC") != nullptr;
     bool built = false;
-    bool no_loop_graph = false;
+    bool no_loop_graph = getenv("OTM_NO_LOOP_GRAPH") != nullptr;   // ncu cannot profile conditional graphs
     bool no_tail = getenv("OTM_TAIL") == nullptr;   // single-CTA tail: opt-in, slower so far
     bool warm = false;
     bool have_T = false;

@@ -676,6 +676,58 @@ __global__ void __launch_bounds__(256) k_upd(long long n, float* __restrict__ d,
     }
 }
 
+// Prolongation, every axis coarsened, one thread per coarse vertex (X,Y,Z) and case:
+// it owns the fine block (2X..2X+1, 2Y..2Y+1, 2Z..2Z+1), whose trilinear values
+// only involve the coarse corners X..X+1 x Y..Y+1 x Z..Z+1 (8 loads per 8 fine
+// vertices), and updates it with 4 float2 read-modify-writes.
+__global__ void __launch_bounds__(256) k_prolong3b(Geo f, Geo c, const float* __restrict__ zc,
+                                                   float* __restrict__ zf) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 3 * c.n) return;
+    const int cc = (int)(i / c.n);
+    const int v = (int)(i - (long long)cc * c.n);
+    const int X = v / c.pl, rem = v - X * c.pl, Y = rem / c.nz, Z = rem - Y * c.nz;
+    const int X1 = X + 1 == c.nx ? 0 : X + 1, Y1 = Y + 1 == c.ny ? 0 : Y + 1, Z1 = Z + 1 == c.nz ? 0 : Z + 1;
+    const float* a = zc + (size_t)cc * c.n;
+    float q[2][2][2];
+    const int xs[2] = {X, X1}, ys[2] = {Y, Y1}, zs[2] = {Z, Z1};
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) q[p][j][k] = __ldg(a + (long long)xs[p] * c.pl + ys[j] * c.nz + zs[k]);
+    // interpolate along z: even fine z -> q0, odd -> (q0 + q1)/2
+    float qz[2][2][2];
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) { qz[p][j][0] = q[p][j][0]; qz[p][j][1] = 0.5f * (q[p][j][0] + q[p][j][1]); }
+    float* out = zf + (size_t)cc * f.n;
+#pragma unroll
+    for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+        for (int b2 = 0; b2 < 2; ++b2) {
+            float2 add;
+            // along y then x
+            float vz0, vz1;
+            {
+                const float y00 = b2 ? 0.5f * (qz[0][0][0] + qz[0][1][0]) : qz[0][0][0];
+                const float y01 = b2 ? 0.5f * (qz[0][0][1] + qz[0][1][1]) : qz[0][0][1];
+                const float y10 = b2 ? 0.5f * (qz[1][0][0] + qz[1][1][0]) : qz[1][0][0];
+                const float y11 = b2 ? 0.5f * (qz[1][0][1] + qz[1][1][1]) : qz[1][0][1];
+                vz0 = a2 ? 0.5f * (y00 + y10) : y00;
+                vz1 = a2 ? 0.5f * (y01 + y11) : y01;
+            }
+            add = make_float2(vz0, vz1);
+            float2* dst = reinterpret_cast<float2*>(out + (long long)(2 * X + a2) * f.pl + (2 * Y + b2) * f.nz + 2 * Z);
+            float2 cur = *dst;
+            cur.x += add.x;
+            cur.y += add.y;
+            *dst = cur;
+        }
+}
+
 // ---- small levels: one thread per (case, vertex), every load issued up front ----
 template <int OP, bool DOT>
 __global__ void __launch_bounds__(256) k_small(Geo g, LevelTemplate lt, const float* __restrict__ kap,
@@ -2035,7 +2087,7 @@ void launch_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3]
 }
 void launch_prolong(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* zc, float* zf) {
     if (cf[0] && cf[1] && cf[2]) {
-        k_prolong3<<<nblk(3 * f.n, 256), 256, 0, s>>>(f, c, zc, zf);
+        k_prolong3b<<<nblk(3 * c.n, 256), 256, 0, s>>>(f, c, zc, zf);
         return;
     }
     k_prolong<<<nblk(f.n, 256), 256, 0, s>>>(f, c, cf[0], cf[1], cf[2], zc, zf);

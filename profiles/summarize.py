@@ -31,12 +31,15 @@ def launches(path):
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h = rows[hi]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    gi = h.index("Grid Size") if "Grid Size" in h else None
     agg = collections.defaultdict(lambda: [0, 0.0])
     tot = 0.0
     for r in rows[hi + 1:]:
         if len(r) <= vi:
             continue
         name = r[ki].split("(")[0].replace("void ", "").replace("otm::", "")
+        if gi is not None and len(sys.argv) > 3 and sys.argv[3] == "grid":
+            name += " " + r[gi]
         try:
             v = float(r[vi].replace(",", ""))
         except ValueError:
