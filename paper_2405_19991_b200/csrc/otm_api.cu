@@ -208,7 +208,7 @@ int setup_filter(otm_ctx* ctx, double radius) {
 }
 
 size_t max_blocks(const otm_ctx* ctx) {
-    size_t mb = 4096 + (size_t)(ctx->g0.n / 1024) + 16;   // k_upd: n/4 threads in blocks of 256
+    size_t mb = 4096 + (size_t)(3 * ctx->g0.n / 512) + 16;   // k_res64b: 3n/2 threads in blocks of 256
     for (const auto& l : ctx->L) {
         int xb;
         const int ch = stencil_chunks(l.g, &xb);

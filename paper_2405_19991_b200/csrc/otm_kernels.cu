@@ -361,6 +361,92 @@ __global__ void __launch_bounds__(128) k_res64(Geo g, int xb, LevelTemplate lt, 
     reduce_finalize<9>(acc, partials, counter, red_out);
 }
 
+// fp64 defect, high-parallelism form: one thread per (case, x, y, z pair), every
+// operand / factor load issued up front (double2 where aligned), no x-march.
+// Requires nz even.  Same outputs and sums as k_res64.
+__global__ void __launch_bounds__(256) k_res64b(Geo g, LevelTemplate lt, const double* __restrict__ kap,
+                                                const double* __restrict__ T, const double* __restrict__ fext,
+                                                const double* __restrict__ fmean, float* __restrict__ r32,
+                                                double* partials, unsigned* counter, double* red_out) {
+    const long long npair = g.n >> 1;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double acc[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc[q] = 0.0;
+    if (i < 3 * npair) {
+        const int c = (int)(i / npair);
+        const long long vp = (i - (long long)c * npair) * 2;     // even vertex index
+        const int x = (int)(vp / g.pl), rem = (int)(vp - (long long)x * g.pl);
+        const int y = rem / g.nz, z = rem - y * g.nz;
+        const long long xo[3] = {(long long)wrap_m(x, g.nx) * g.pl, (long long)x * g.pl, (long long)wrap_p(x, g.nx) * g.pl};
+        const int yo[3] = {wrap_m(y, g.ny) * g.nz, y * g.nz, wrap_p(y, g.ny) * g.nz};
+        const int zm = z == 0 ? g.nz - 1 : z - 1, zp2 = z + 2 == g.nz ? 0 : z + 2;
+        const double* Tc = T + (size_t)c * g.n;
+        double t[3][3][4], k[2][2][3];
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const double* row = Tc + xo[p] + yo[j];
+                t[p][j][0] = __ldg(row + zm);
+                const double2 m = __ldg(reinterpret_cast<const double2*>(row + z));
+                t[p][j][1] = m.x;
+                t[p][j][2] = m.y;
+                t[p][j][3] = __ldg(row + zp2);
+            }
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const double* row = kap + xo[p] + yo[j];
+                k[p][j][0] = __ldg(row + zm);
+                const double2 m = __ldg(reinterpret_cast<const double2*>(row + z));
+                k[p][j][1] = m.x;
+                k[p][j][2] = m.y;
+            }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {           // vertex z + h
+            double w[3][9], ks[2][4];
+#pragma unroll
+            for (int p = 0; p < 3; ++p)
+#pragma unroll
+                for (int j = 0; j < 3; ++j)
+#pragma unroll
+                    for (int m = 0; m < 3; ++m) w[p][j * 3 + m] = t[p][j][h + m];
+#pragma unroll
+            for (int p = 0; p < 2; ++p)
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+#pragma unroll
+                    for (int m = 0; m < 2; ++m) ks[p][j * 2 + m] = k[p][j][h + m];
+            double kt;
+            if (lt.equal) {
+                const KSum<double> sm = ksum<double>(ks);
+                kt = apply_compact<double>(w, ks, sm, lt.s12);
+            } else {
+                kt = apply_generic<double>(w, ks, lt.kt);
+            }
+            double f;
+            if (fext) {
+                f = __ldg(fext + (size_t)c * g.n + vp + h);
+            } else {
+                f = 0.0;
+#pragma unroll
+                for (int a = 0; a < 8; ++a) {
+                    const int q = 1 - (a & 1), jj = 1 - ((a >> 1) & 1), kk = 1 - ((a >> 2) & 1);
+                    f = __dadd_rn(f, __dmul_rn(lt.f0[a * 3 + c], ks[q][jj * 2 + kk]));
+                }
+            }
+            const double r = (f - fmean[c]) - kt;
+            r32[(size_t)c * g.n + vp + h] = (float)r;
+            acc[c] += r * r;
+            acc[3 + c] += f * f;
+            acc[6 + c] += t[1][1][1 + h];
+        }
+    }
+    reduce_finalize<9>(acc, partials, counter, red_out);
+}
+
 // Single-case fp64 K T (apply_K, solver.py:111-119) and macro load (solver.py:347-363).
 __global__ void __launch_bounds__(128) k_apply64(Geo g, int xb, LevelTemplate lt, const double* __restrict__ kap,
                                                  const double* __restrict__ T, double* __restrict__ out,
@@ -1921,6 +2007,12 @@ void launch_coarse_solve(cudaStream_t s, int n, const float* G, const float* f, 
 }
 void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
                   const double* fext, const double* fmean, float* r32, Red& red, double* out9) {
+    static const bool old = getenv("OTM_OLD_RES64") != nullptr;
+    if (!old && g.nz % 2 == 0 && g.nz >= 2) {
+        const long long th = 3 * (g.n >> 1);
+        k_res64b<<<nblk(th, 256), 256, 0, s>>>(g, lt, kap, T, fext, fmean, r32, red.partials, red.counter, out9);
+        return;
+    }
     if (fast_tiling(g, lt)) {
         int nch;
         const int xb = fast_xb(g);
