@@ -92,6 +92,65 @@ __global__ void __launch_bounds__(128) k_filter(Geo g, int xb, FilterTaps taps, 
     }
 }
 
+// High-parallelism filter (reach 1): one thread per z pair, 27 window loads up front,
+// taps in the reference's order (bit-exact, see k_filter).  nz even.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_filter_b(Geo g, FilterTaps taps, const double* __restrict__ in,
+                                                  double* __restrict__ out, double* __restrict__ kappa64,
+                                                  float* __restrict__ kappa32, SimpParams sp, double* partials,
+                                                  unsigned* counter, double* red_out) {
+    const long long npair = g.n >> 1;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double acc3[3] = {0.0, 0.0, 0.0};
+    if (i < npair) {
+        const long long vp = i * 2;
+        const int x = (int)(vp / g.pl), rem = (int)(vp - (long long)x * g.pl);
+        const int y = rem / g.nz, z = rem - y * g.nz;
+        const long long xo[3] = {(long long)wrap_m(x, g.nx) * g.pl, (long long)x * g.pl, (long long)wrap_p(x, g.nx) * g.pl};
+        const int yo[3] = {wrap_m(y, g.ny) * g.nz, y * g.nz, wrap_p(y, g.ny) * g.nz};
+        const int zm = z == 0 ? g.nz - 1 : z - 1, zp2 = z + 2 == g.nz ? 0 : z + 2;
+        double t[3][3][4];
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const double* row = in + xo[p] + yo[j];
+                t[p][j][0] = __ldg(row + zm);
+                const double2 m = __ldg(reinterpret_cast<const double2*>(row + z));
+                t[p][j][1] = m.x;
+                t[p][j][2] = m.y;
+                t[p][j][3] = __ldg(row + zp2);
+            }
+        double res[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            double s = 0.0;
+#pragma unroll
+            for (int slot = 0; slot < 27; ++slot) {
+                const double wt = taps.w27[slot];
+                if (wt != 0.0) {
+                    const int src = MODE == 1 ? 26 - slot : slot;
+                    const int p = src / 9, j = (src / 3) % 3, m = src % 3;
+                    s = __dadd_rn(s, __dmul_rn(wt, t[p][j][h + m]));
+                }
+            }
+            res[h] = s;
+        }
+        *reinterpret_cast<double2*>(out + vp) = make_double2(res[0], res[1]);
+        if (MODE == 2) {
+            double k0 = sp.kmin + pow(res[0], sp.p) * (sp.k0 - sp.kmin);
+            double k1 = sp.kmin + pow(res[1], sp.p) * (sp.k0 - sp.kmin);
+            *reinterpret_cast<double2*>(kappa64 + vp) = make_double2(k0, k1);
+            *reinterpret_cast<float2*>(kappa32 + vp) = make_float2((float)k0, (float)k1);
+            const double r0 = t[1][1][1], r1 = t[1][1][2];
+            acc3[0] = r0 + r1;
+            acc3[1] = pow(r0, sp.p) + pow(r1, sp.p);
+            acc3[2] = res[0] + res[1];
+        }
+    }
+    if (MODE == 2) reduce_finalize<3>(acc3, partials, counter, red_out);
+}
+
 // Generic-reach filter (radius > 2): one vertex per thread, taps from global memory.
 __global__ void k_filter_generic(Geo g, int ntaps, const int* __restrict__ offs,
                                  const double* __restrict__ wts, int adjoint,
@@ -223,27 +282,29 @@ __global__ void __launch_bounds__(1024) k_coarse_setup(Geo g, const float* __res
         Z[i] = (r == c && r > 0) ? 1.0 : 0.0;
     }
     __syncthreads();
-    // Gauss-Jordan on the SPD block A[1:,1:] (no pivoting needed)
+    // Gauss-Jordan on the SPD block A[1:,1:] (no pivoting needed).  Thread t owns
+    // column t of A (t < n) or column t-n of Z: row-p reads are broadcasts and the
+    // column updates are consecutive across lanes, so shared memory never conflicts.
     const int m = n - 1;
-    __shared__ double piv;
     for (int p = 1; p <= m; ++p) {
-        if (threadIdx.x == 0) piv = A[(size_t)p * n + p];
-        __syncthreads();
-        for (int c = 1 + threadIdx.x; c < n; c += blockDim.x) {
-            A[(size_t)p * n + c] /= piv;
-            Z[(size_t)p * n + c] /= piv;
+        const double piv = A[(size_t)p * n + p];
+        __syncthreads();                       // everyone has read the pivot
+        for (int t = threadIdx.x; t < 2 * n; t += blockDim.x) {
+            double* M = t < n ? A : Z;
+            const int cidx = t < n ? t : t - n;
+            if (cidx >= 1) M[(size_t)p * n + cidx] /= piv;
         }
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
-            const int r = 1 + idx / m, c = 1 + idx % m;
-            if (r == p) continue;
-            const double f = A[(size_t)r * n + p];
-            if (c != p) A[(size_t)r * n + c] -= f * A[(size_t)p * n + c];
-            Z[(size_t)r * n + c] -= f * Z[(size_t)p * n + c];
+        __syncthreads();                       // row p normalised
+        for (int t = threadIdx.x; t < 2 * n; t += blockDim.x) {
+            double* M = t < n ? A : Z;
+            const int cidx = t < n ? t : t - n;
+            if (cidx < 1 || (t < n && cidx == p)) continue;   // column p of A is read below, never written
+            const double rowp = M[(size_t)p * n + cidx];
+            for (int r = 1; r <= m; ++r) {
+                if (r == p) continue;
+                M[(size_t)r * n + cidx] -= A[(size_t)r * n + p] * rowp;
+            }
         }
-        __syncthreads();
-        for (int r = 1 + threadIdx.x; r < n; r += blockDim.x)
-            if (r != p) A[(size_t)r * n + p] = 0.0;
         __syncthreads();
     }
     // G = P Z P with P = I - 11^T/n
@@ -1943,6 +2004,17 @@ static inline dim3 stencil_grid(const Geo& g, int* xb) {
 
 void launch_filter(cudaStream_t s, const Geo& g, const FilterSetup& fs, int adjoint, const double* in,
                    double* out, Red& red) {
+    if (fs.window && g.nz % 2 == 0) {
+        FilterTaps taps;
+        for (int i = 0; i < 27; ++i) taps.w27[i] = fs.w27[i];
+        SimpParams sp{};
+        const long long th = g.n >> 1;
+        if (adjoint)
+            k_filter_b<1><<<nblk(th, 256), 256, 0, s>>>(g, taps, in, out, nullptr, nullptr, sp, nullptr, nullptr, nullptr);
+        else
+            k_filter_b<0><<<nblk(th, 256), 256, 0, s>>>(g, taps, in, out, nullptr, nullptr, sp, nullptr, nullptr, nullptr);
+        return;
+    }
     if (fs.window) {
         int xb;
         const dim3 grid = stencil_grid(g, &xb);
@@ -1960,6 +2032,13 @@ void launch_filter(cudaStream_t s, const Geo& g, const FilterSetup& fs, int adjo
 
 void launch_filter_simp(cudaStream_t s, const Geo& g, const FilterSetup& fs, const SimpParams& sp,
                         const double* rho, double* rho_f, double* k64, float* k32, Red& red, double* out3) {
+    if (fs.window && g.nz % 2 == 0) {
+        FilterTaps taps;
+        for (int i = 0; i < 27; ++i) taps.w27[i] = fs.w27[i];
+        const long long th = g.n >> 1;
+        k_filter_b<2><<<nblk(th, 256), 256, 0, s>>>(g, taps, rho, rho_f, k64, k32, sp, red.partials, red.counter, out3);
+        return;
+    }
     if (fs.window) {
         int xb;
         const dim3 grid = stencil_grid(g, &xb);
@@ -2007,8 +2086,8 @@ void launch_coarse_solve(cudaStream_t s, int n, const float* G, const float* f, 
 }
 void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
                   const double* fext, const double* fmean, float* r32, Red& red, double* out9) {
-    static const bool old = getenv("OTM_OLD_RES64") != nullptr;
-    if (!old && g.nz % 2 == 0 && g.nz >= 2) {
+    static const bool use_b = getenv("OTM_RES64B") != nullptr;   // measured slower (248 vs 106 us at 128^3)
+    if (use_b && g.nz % 2 == 0 && g.nz >= 2) {
         const long long th = 3 * (g.n >> 1);
         k_res64b<<<nblk(th, 256), 256, 0, s>>>(g, lt, kap, T, fext, fmean, r32, red.partials, red.counter, out9);
         return;
