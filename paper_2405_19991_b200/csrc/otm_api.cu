@@ -85,6 +85,7 @@ struct otm_ctx {
     std::string err;
     size_t bytes = 0;
     long long launches = 0;
+    long long stat_inner = 0, stat_outer = 0, stat_solves = 0;
     // inner-iteration graphs (plain, profiled)
     cudaGraphExec_t gexec = nullptr;
     cudaGraphExec_t gexec_prof = nullptr;
@@ -473,6 +474,10 @@ int otm_create(otm_ctx** out, int nx, int ny, int nz, const otm_params* pin) {
     *out = nullptr;
     otm_ctx* ctx = new otm_ctx();
     if (pin) ctx->P = *pin; else otm_default_params(&ctx->P);
+    // tuning overrides (experiments only)
+    if (getenv("OTM_INNER_RED")) ctx->P.inner_reduction = atof(getenv("OTM_INNER_RED"));
+    if (getenv("OTM_OMEGA")) ctx->P.jacobi_omega = atof(getenv("OTM_OMEGA"));
+    if (getenv("OTM_MAX_INNER")) ctx->P.max_inner = atoi(getenv("OTM_MAX_INNER"));
     const otm_params& P = ctx->P;
     if (nx < 1 || ny < 1 || nz < 1) {
         int rc = fail(ctx, OTM_EINVAL, "dims must be three positive integers");
@@ -574,6 +579,9 @@ int otm_create(otm_ctx** out, int nx, int ny, int nz, const otm_params* pin) {
 
 int otm_destroy(otm_ctx* ctx) {
     if (!ctx) return OTM_OK;
+    if (getenv("OTM_STATS") && ctx->stat_solves)
+        fprintf(stderr, "[otm] stats: solves %lld outer %lld inner %lld (%.2f inner/solve)\n", ctx->stat_solves,
+                ctx->stat_outer, ctx->stat_inner, (double)ctx->stat_inner / ctx->stat_solves);
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
     if (ctx->gexec_prof) cudaGraphExecDestroy(ctx->gexec_prof);
     if (ctx->gexec_loop) cudaGraphExecDestroy(ctx->gexec_loop);
@@ -735,6 +743,7 @@ int otm_solve(otm_ctx* ctx, const double* fext, double tol, int max_cycles, int*
     if (rc) return rc;
     static const bool debug = getenv("OTM_DEBUG") != nullptr;
     if (debug) fprintf(stderr, "[otm] solve start rel %.3e %.3e %.3e\n", rel[0], rel[1], rel[2]);
+    ctx->stat_solves++;
     bool zero_load[3];
     for (int c = 0; c < 3; ++c) zero_load[c] = fnorm[c] == 0.0;
     int status = OTM_OK;
@@ -766,6 +775,7 @@ int otm_solve(otm_ctx* ctx, const double* fext, double tol, int max_cycles, int*
             PcgScalars fin;
             std::memcpy(&fin, ctx->h + 160, sizeof fin);
             ctx->launches += (long long)fin.it * ctx->launches_per_inner;
+            ctx->stat_inner += fin.it;
             cycles = fin.cycles;
             for (int k = 0; k < 6; ++k) ctx->h[k] = fin.flags[k];
         } else
@@ -780,6 +790,7 @@ int otm_solve(otm_ctx* ctx, const double* fext, double tol, int max_cycles, int*
         }
         launch_Tupd(s, 3 * n, ctx->T64, ctx->d);
         ctx->launches++;
+        ctx->stat_outer++;
         const double inner_rr[3] = {ctx->h[3], ctx->h[4], ctx->h[5]};
         rc = residual();
         if (rc) return rc;
