@@ -1594,6 +1594,11 @@ struct Op3SmoothRes {     // arrays: 0 = f (halo), 1 = D^-1 (halo); operand = w 
     __device__ __forceinline__ float operand(const float* slot, int r, int col) const {
         return omega * *s3_at(slot, 1, r, col) * *s3_at(slot, 0, r, col);
     }
+    __device__ __forceinline__ float2 operand2(const float* slot, int r, int col) const {
+        const float2 d = *reinterpret_cast<const float2*>(s3_at(slot, 1, r, col));
+        const float2 f = *reinterpret_cast<const float2*>(s3_at(slot, 0, r, col));
+        return make_float2(omega * d.x * f.x, omega * d.y * f.y);
+    }
     __device__ __forceinline__ void sink(const float* slot, int c, long long v, int r, int col, const float (&kz)[2],
                                          const float (&zc)[2]) {
         const float2 f = *reinterpret_cast<const float2*>(s3_at(slot, 0, r, col));
@@ -1610,6 +1615,9 @@ struct Op3Jacobi {        // arrays: 0 = z (halo), 1 = f (center), 2 = D^-1 (cen
         acc = 0.0;
     }
     __device__ __forceinline__ float operand(const float* slot, int r, int col) const { return *s3_at(slot, 0, r, col); }
+    __device__ __forceinline__ float2 operand2(const float* slot, int r, int col) const {
+        return *reinterpret_cast<const float2*>(s3_at(slot, 0, r, col));
+    }
     __device__ __forceinline__ void sink(const float* slot, int c, long long v, int r, int col, const float (&kz)[2],
                                          const float (&zc)[2]) {
         const float2 fv = *reinterpret_cast<const float2*>(s3_at(slot, 1, r, col));
@@ -1628,6 +1636,9 @@ struct Op3Spmv {          // arrays: 0 = p (halo)
         acc = 0.0;
     }
     __device__ __forceinline__ float operand(const float* slot, int r, int col) const { return *s3_at(slot, 0, r, col); }
+    __device__ __forceinline__ float2 operand2(const float* slot, int r, int col) const {
+        return *reinterpret_cast<const float2*>(s3_at(slot, 0, r, col));
+    }
     __device__ __forceinline__ void sink(const float*, int c, long long v, int, int, const float (&kp)[2],
                                          const float (&pc)[2]) {
         *reinterpret_cast<float2*>(q + c * n + v) = make_float2(kp[0], kp[1]);
@@ -1635,6 +1646,7 @@ struct Op3Spmv {          // arrays: 0 = p (halo)
     }
 };
 
+template <bool K5>
 __global__ void __launch_bounds__(256, 3) k3_smooth_res(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
                                                         const float* f, const float* dinv, float omega, float* z,
                                                         float* res) {
@@ -1644,10 +1656,11 @@ __global__ void __launch_bounds__(256, 3) k3_smooth_res(Geo g, int xb, int nch, 
     su.kap = kap;
     Op3SmoothRes op{omega, z, res, g.n};
     int last;
-    march3<2>(g, lt, su, op, last);
+    if (K5) march5<2>(g, lt, su, op, last);
+    else march3<2>(g, lt, su, op, last);
 }
 
-template <bool DOT>
+template <bool DOT, bool K5>
 __global__ void __launch_bounds__(256, 3) k3_jacobi(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
                                                     const float* z, const float* f, const float* dinv, float omega,
                                                     float* zout, double* partials, unsigned* counter,
@@ -1659,7 +1672,8 @@ __global__ void __launch_bounds__(256, 3) k3_jacobi(Geo g, int xb, int nch, Leve
     su.kap = kap;
     Op3Jacobi<DOT> op{omega, zout, g.n, 0.0, {0.0, 0.0, 0.0}};
     int last;
-    march3<3>(g, lt, su, op, last);
+    if (K5) march5<3>(g, lt, su, op, last);
+    else march3<3>(g, lt, su, op, last);
     if (DOT) {
         if (last >= 0) op.acc3[last] += op.acc;
         double v3[3] = {op.acc3[0], op.acc3[1], op.acc3[2]};
@@ -1674,6 +1688,7 @@ __global__ void __launch_bounds__(256, 3) k3_jacobi(Geo g, int xb, int nch, Leve
     }
 }
 
+template <bool K5>
 __global__ void __launch_bounds__(256, 3) k3_spmv(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
                                                   const float* p, float* q, double* partials, unsigned* counter,
                                                   PcgScalars* sc) {
@@ -1682,7 +1697,8 @@ __global__ void __launch_bounds__(256, 3) k3_spmv(Geo g, int xb, int nch, LevelT
     su.kap = kap;
     Op3Spmv op{q, g.n, 0.0, {0.0, 0.0, 0.0}};
     int last;
-    march3<1>(g, lt, su, op, last);
+    if (K5) march5<1>(g, lt, su, op, last);
+    else march3<1>(g, lt, su, op, last);
     if (last >= 0) op.acc3[last] += op.acc;
     double v3[3] = {op.acc3[0], op.acc3[1], op.acc3[2]};
     if (reduce_finalize<3>(v3, partials, counter, sc->red + 3)) {
@@ -1694,9 +1710,10 @@ __global__ void __launch_bounds__(256, 3) k3_spmv(Geo g, int xb, int nch, LevelT
     }
 }
 
-static bool s3_enabled() {     // OTM_K=3
-    static const bool on = getenv("OTM_K") && atoi(getenv("OTM_K")) == 3;
-    return on;
+static int kernel_gen();
+static bool s3_enabled() {     // OTM_K=3 (separable k3) or 5 (k3 ring + 21-weight FFMA2)
+    const int k = kernel_gen();
+    return k == 3 || k == 5;
 }
 // persistent grid: resident blocks of the kernel x SMs (capped by the work units)
 template <class K>
@@ -2140,9 +2157,15 @@ void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, co
     }
     if (fast_tiling(g, lt) && s3_enabled()) {
         const size_t sm = s3_smem_bytes<2>();
-        s3_attr(k3_smooth_res, sm);
-        k3_smooth_res<<<s3_grid(k3_smooth_res, sm, g), dim3(32, kTileY), sm, s>>>(g, 0, 0, lt, kap, f, dinv, omega,
-                                                                                 z, res);
+        if (kernel_gen() == 5) {
+            s3_attr(k3_smooth_res<true>, sm);
+            k3_smooth_res<true><<<s3_grid(k3_smooth_res<true>, sm, g), dim3(32, kTileY), sm, s>>>(
+                g, 0, 0, lt, kap, f, dinv, omega, z, res);
+        } else {
+            s3_attr(k3_smooth_res<false>, sm);
+            k3_smooth_res<false><<<s3_grid(k3_smooth_res<false>, sm, g), dim3(32, kTileY), sm, s>>>(
+                g, 0, 0, lt, kap, f, dinv, omega, z, res);
+        }
         return;
     }
     if (fast_tiling(g, lt)) {
@@ -2183,15 +2206,18 @@ void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const 
     }
     if (fast_tiling(g, lt) && s3_enabled()) {
         const size_t sm = s3_smem_bytes<3>();
-        if (dot) {
-            s3_attr(k3_jacobi<true>, sm);
-            k3_jacobi<true><<<s3_grid(k3_jacobi<true>, sm, g), dim3(32, kTileY), sm, s>>>(
-                g, 0, 0, lt, kap, z, f, dinv, omega, zout, red.partials, red.counter, sc);
-        } else {
-            s3_attr(k3_jacobi<false>, sm);
-            k3_jacobi<false><<<s3_grid(k3_jacobi<false>, sm, g), dim3(32, kTileY), sm, s>>>(
-                g, 0, 0, lt, kap, z, f, dinv, omega, zout, nullptr, nullptr, sc);
-        }
+        const bool k5 = kernel_gen() == 5;
+#define OTM_J3(D, K)                                                                                     \
+    do {                                                                                                 \
+        s3_attr(k3_jacobi<D, K>, sm);                                                                     \
+        k3_jacobi<D, K><<<s3_grid(k3_jacobi<D, K>, sm, g), dim3(32, kTileY), sm, s>>>(                     \
+            g, 0, 0, lt, kap, z, f, dinv, omega, zout, D ? red.partials : nullptr, D ? red.counter : nullptr, sc); \
+    } while (0)
+        if (dot && k5) OTM_J3(true, true);
+        else if (dot) OTM_J3(true, false);
+        else if (k5) OTM_J3(false, true);
+        else OTM_J3(false, false);
+#undef OTM_J3
         return;
     }
     if (fast_tiling(g, lt)) {
@@ -2224,9 +2250,15 @@ void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const fl
     }
     if (fast_tiling(g, lt) && s3_enabled()) {
         const size_t sm = s3_smem_bytes<1>();
-        s3_attr(k3_spmv, sm);
-        k3_spmv<<<s3_grid(k3_spmv, sm, g), dim3(32, kTileY), sm, s>>>(g, 0, 0, lt, kap, p, q, red.partials,
-                                                                      red.counter, sc);
+        if (kernel_gen() == 5) {
+            s3_attr(k3_spmv<true>, sm);
+            k3_spmv<true><<<s3_grid(k3_spmv<true>, sm, g), dim3(32, kTileY), sm, s>>>(g, 0, 0, lt, kap, p, q,
+                                                                                      red.partials, red.counter, sc);
+        } else {
+            s3_attr(k3_spmv<false>, sm);
+            k3_spmv<false><<<s3_grid(k3_spmv<false>, sm, g), dim3(32, kTileY), sm, s>>>(g, 0, 0, lt, kap, p, q,
+                                                                                        red.partials, red.counter, sc);
+        }
         return;
     }
     if (fast_tiling(g, lt)) {

@@ -256,3 +256,141 @@ __device__ __forceinline__ void march4(const Geo& g, const LevelTemplate& lt, co
 }
 
 }  // namespace otm
+
+namespace otm {
+
+// ---------------------------------------------------------------------------
+// k5: one load case per thread (the k3 ring and register window: only the newly
+// arrived plane is read from shared memory) with the 21-weight paired-fp32
+// arithmetic of k4.  Window: operand planes x-1, x, x+1 (3 rows x 4 columns each)
+// and factor planes x-1, x in registers.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float2 apply21(const W21& w, const float (&Pm)[3][4], const float (&P0)[3][4],
+                                          const float (&Pp)[3][4]) {
+    auto L = [](const float (&P)[3][4], int j) { return f2(P[j][0], P[j][1]); };
+    auto C = [](const float (&P)[3][4], int j) { return f2(P[j][1], P[j][2]); };
+    auto R = [](const float (&P)[3][4], int j) { return f2(P[j][2], P[j][3]); };
+    float2 acc = fmul2(w.kv4, C(P0, 1));
+    float2 acc2 = ffma2(w.e[8], L(P0, 0), f2(0.f, 0.f));
+    acc = ffma2(w.e[9], R(P0, 0), acc);
+    acc2 = ffma2(w.e[10], L(P0, 2), acc2);
+    acc = ffma2(w.e[11], R(P0, 2), acc);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const float (&P)[3][4] = q == 0 ? Pm : Pp;
+        acc2 = ffma2(w.e[4 + q * 2], L(P, 1), acc2);
+        acc = ffma2(w.e[5 + q * 2], R(P, 1), acc);
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+            const int j = jj == 0 ? 0 : 2;
+            acc2 = ffma2(w.e[q * 2 + jj], C(P, j), acc2);
+            acc = ffma2(w.k[q | (jj << 1)], L(P, j), acc);
+            acc2 = ffma2(w.k[q | (jj << 1) | 4], R(P, j), acc2);
+        }
+    }
+    return fadd2(acc, acc2);
+}
+
+template <int NARR, class Op>
+__device__ __forceinline__ void march5_segment(const Geo& g, const LevelTemplate& lt, const S3Setup<NARR>& su,
+                                               Op& op, int c, int y0, int z0, int x0, int x1) {
+    extern __shared__ float4 s3_smem4[];
+    float* smem = reinterpret_cast<float*>(s3_smem4);
+    constexpr int SLOT = s3_slot_floats<NARR>();
+    S3Task mine[kMaxTasks];
+    s3_tasks<NARR>(g, su, c, y0, z0, mine);
+    const int nplanes = (x1 - x0) + 2;
+#pragma unroll
+    for (int s = 0; s < kAhead; ++s) {
+        if (s < nplanes) s3_issue<NARR>(g, su, c, x0 - 1 + s, smem + s * SLOT, mine);
+        cp_commit();
+    }
+    const int tr = threadIdx.y + 1;
+    const int col = 4 + 2 * threadIdx.x;
+    const long long vrow = (long long)(y0 + threadIdx.y) * g.nz + z0 + 2 * threadIdx.x;
+    const float2 s12 = f2((float)lt.s12, (float)lt.s12);
+    float Pm[3][4], P0[3][4], Pp[3][4], Ka[2][3], Kb[2][3];
+    auto readT = [&](const float* slot, float (&P)[3][4]) {
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            P[j][0] = op.operand(slot, tr - 1 + j, col - 1);
+            const float2 m = op.operand2(slot, tr - 1 + j, col);
+            P[j][1] = m.x;
+            P[j][2] = m.y;
+            P[j][3] = op.operand(slot, tr - 1 + j, col + 2);
+        }
+    };
+    auto readK = [&](const float* slot, float (&K)[2][3]) {
+        const float* kt = slot + NARR * kS3Tile;
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+            const int o = (tr - 1 + jj) * kS3Pitch + col;
+            K[jj][0] = kt[o - 1];
+            const float2 v = *reinterpret_cast<const float2*>(kt + o);
+            K[jj][1] = v.x;
+            K[jj][2] = v.y;
+        }
+    };
+    auto advance = [&](int s) {
+        cp_wait<kAhead - 1>();
+        __syncthreads();
+        if (s + kAhead < nplanes)
+            s3_issue<NARR>(g, su, c, x0 - 1 + s + kAhead, smem + ((s + kAhead) % kStages) * SLOT, mine);
+        cp_commit();
+    };
+    advance(0);
+    readT(smem, Pm);
+    readK(smem, Ka);
+    advance(1);
+    readT(smem + SLOT, P0);
+    for (int s = 2; s < nplanes; ++s) {
+        advance(s);
+        const float* slot = smem + (s % kStages) * SLOT;
+        const float* xslot = smem + ((s - 1) % kStages) * SLOT;
+        readT(slot, Pp);
+        readK(xslot, Kb);
+        W21 w;
+        w21_build(Ka, Kb, w);
+        const float2 kt = fmul2(s12, apply21(w, Pm, P0, Pp));
+        const int x = x0 + s - 2;
+        const float kt2[2] = {kt.x, kt.y};
+        const float ctr[2] = {P0[1][1], P0[1][2]};
+        op.sink(xslot, c, vrow + (long long)x * g.pl, tr, col, kt2, ctr);
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) { Pm[j][m] = P0[j][m]; P0[j][m] = Pp[j][m]; }
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+            for (int m = 0; m < 3; ++m) Ka[jj][m] = Kb[jj][m];
+    }
+    cp_wait<0>();
+    __syncthreads();
+}
+
+template <int NARR, class Op>
+__device__ __forceinline__ void march5(const Geo& g, const LevelTemplate& lt, const S3Setup<NARR>& su, Op& op,
+                                       int& last_case) {
+    const int tz = g.nz / kTileZ, ty = g.ny / kTileY;
+    const long long cols = 3LL * tz * ty;
+    const long long W = cols * g.nx;
+    const long long B = gridDim.x;
+    long long u = W * blockIdx.x / B;
+    const long long u1 = W * (blockIdx.x + 1) / B;
+    last_case = -1;
+    while (u < u1) {
+        const long long col = u / g.nx;
+        const int x0 = (int)(u - col * g.nx);
+        const int x1 = (int)min((long long)g.nx, x0 + (u1 - u));
+        const int c = (int)(col / ((long long)tz * ty));
+        const int rest = (int)(col - (long long)c * tz * ty);
+        const int y0 = (rest / tz) * kTileY, z0 = (rest - (rest / tz) * tz) * kTileZ;
+        op.begin_case(c, last_case);
+        march5_segment<NARR>(g, lt, su, op, c, y0, z0, x0, x1);
+        last_case = c;
+        u += x1 - x0;
+    }
+}
+
+}  // namespace otm
