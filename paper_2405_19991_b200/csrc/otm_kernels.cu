@@ -6,6 +6,7 @@
 #include "otm_stencil2.cuh"
 #include "otm_stencil3.cuh"
 #include "otm_stencil4.cuh"
+#include "otm_stencil6.cuh"
 
 #ifndef OTM_MINB
 #define OTM_MINB 2   // min resident blocks of the fp32 fast-path stencils (register cap 128)
@@ -1845,8 +1846,168 @@ __global__ void __launch_bounds__(256, 2) k4_spmv(Geo g, LevelTemplate lt, const
     }
 }
 
-static int kernel_gen() {     // OTM_K=2|3|4 selects the fast-path stencil generation (default 4)
-    static const int k = getenv("OTM_K") ? atoi(getenv("OTM_K")) : 4;
+// ---- k6: TMA-staged (otm_stencil6.cuh) ----
+struct Op6Base {
+    int tile; int nz;
+    __device__ __forceinline__ const float* at(const float* S, int a, int r, int z) const {
+        return S + a * tile + r * nz + z;
+    }
+};
+struct Op6SmoothRes : Op6Base {   // tiles 0..2 = f cases, 3 = D^-1; operand w D^-1 f
+    static constexpr int NT = 4;
+    float omega; float* zo; float* res; long long n;
+    __device__ __forceinline__ float op1(const float* S, int c, int r, int z) const {
+        return omega * *at(S, 3, r, z) * *at(S, c, r, z);
+    }
+    __device__ __forceinline__ float2 op2(const float* S, int c, int r, int z) const {
+        const float2 d = *reinterpret_cast<const float2*>(at(S, 3, r, z));
+        const float2 f = *reinterpret_cast<const float2*>(at(S, c, r, z));
+        return make_float2(omega * d.x * f.x, omega * d.y * f.y);
+    }
+    __device__ __forceinline__ void prefetch(int, long long) {}
+    __device__ __forceinline__ void sink(const float* S0, int c, long long v, int r, int z, float2 kz, float2 zc) {
+        const float2 f = *reinterpret_cast<const float2*>(at(S0, c, r, z));
+        *reinterpret_cast<float2*>(zo + c * n + v) = zc;
+        *reinterpret_cast<float2*>(res + c * n + v) = make_float2(f.x - kz.x, f.y - kz.y);
+    }
+};
+template <bool DOT>
+struct Op6Jacobi : Op6Base {      // tiles 0..2 = z cases; f, D^-1 prefetched
+    static constexpr int NT = 3;
+    const float* f; const float* dinv; float omega; float* zout; long long n; long long pl;
+    float2 fp[3], dp;
+    double acc[3];
+    __device__ __forceinline__ float op1(const float* S, int c, int r, int z) const { return *at(S, c, r, z); }
+    __device__ __forceinline__ float2 op2(const float* S, int c, int r, int z) const {
+        return *reinterpret_cast<const float2*>(at(S, c, r, z));
+    }
+    __device__ __forceinline__ void prefetch(int x, long long vrow) {
+        const long long v = vrow + (long long)x * pl;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) fp[c] = __ldg(reinterpret_cast<const float2*>(f + c * n + v));
+        dp = __ldg(reinterpret_cast<const float2*>(dinv + v));
+    }
+    __device__ __forceinline__ void sink(const float*, int c, long long v, int, int, float2 kz, float2 zc) {
+        const float z0 = zc.x + omega * dp.x * (fp[c].x - kz.x);
+        const float z1 = zc.y + omega * dp.y * (fp[c].y - kz.y);
+        *reinterpret_cast<float2*>(zout + c * n + v) = make_float2(z0, z1);
+        if (DOT) acc[c] += (double)fp[c].x * (double)z0 + (double)fp[c].y * (double)z1;
+    }
+};
+struct Op6Spmv : Op6Base {        // tiles 0..2 = p cases
+    static constexpr int NT = 3;
+    float* q; long long n; double acc[3];
+    __device__ __forceinline__ float op1(const float* S, int c, int r, int z) const { return *at(S, c, r, z); }
+    __device__ __forceinline__ float2 op2(const float* S, int c, int r, int z) const {
+        return *reinterpret_cast<const float2*>(at(S, c, r, z));
+    }
+    __device__ __forceinline__ void prefetch(int, long long) {}
+    __device__ __forceinline__ void sink(const float*, int c, long long v, int, int, float2 kp, float2 pc) {
+        *reinterpret_cast<float2*>(q + c * n + v) = kp;
+        acc[c] += (double)pc.x * (double)kp.x + (double)pc.y * (double)kp.y;
+    }
+};
+
+__global__ void __launch_bounds__(256, 2) k6_smooth_res(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
+                                                        float omega, float* z, float* res) {
+    Op6SmoothRes op;
+    op.tile = (k6_ty(g.nz) + 2) * g.nz; op.nz = g.nz;
+    op.omega = omega; op.zo = z; op.res = res; op.n = g.n;
+    march6(g, lt, maps, op);
+}
+
+template <bool DOT>
+__global__ void __launch_bounds__(256, 2) k6_jacobi(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
+                                                    const float* f, const float* dinv, float omega, float* zout,
+                                                    double* partials, unsigned* counter, PcgScalars* sc) {
+    Op6Jacobi<DOT> op;
+    op.tile = (k6_ty(g.nz) + 2) * g.nz; op.nz = g.nz;
+    op.f = f; op.dinv = dinv; op.omega = omega; op.zout = zout; op.n = g.n; op.pl = g.pl;
+    op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
+    march6(g, lt, maps, op);
+    if (DOT) {
+        double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
+        if (reduce_finalize<3>(v3, partials, counter, sc->red)) {
+            for (int cc = 0; cc < 3; ++cc) {
+                const double rz = sc->red[cc];
+                sc->beta[cc] = (sc->first || sc->rz[cc] == 0.0) ? 0.0 : rz / sc->rz[cc];
+                sc->rz[cc] = rz;
+            }
+            sc->first = 0;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256, 2) k6_spmv(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
+                                                  float* q, double* partials, unsigned* counter, PcgScalars* sc) {
+    Op6Spmv op;
+    op.tile = (k6_ty(g.nz) + 2) * g.nz; op.nz = g.nz;
+    op.q = q; op.n = g.n;
+    op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
+    march6(g, lt, maps, op);
+    double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
+    if (reduce_finalize<3>(v3, partials, counter, sc->red + 3)) {
+        for (int cc = 0; cc < 3; ++cc) {
+            const double pq = sc->red[3 + cc];
+            sc->pq[cc] = pq;
+            sc->alpha[cc] = (sc->active[cc] != 0.0 && pq > 0.0) ? sc->rz[cc] / pq : 0.0;
+        }
+    }
+}
+
+// host: tensor maps through the driver entry point (no libcuda link needed)
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_encodeTiled_t encode_fn() {
+    static PFN_encodeTiled_t fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_encodeTiled_t)p;
+    }
+    return fn;
+}
+static bool encode_map(CUtensorMap* m, const float* base, int nz, int ny, long long planes, int box_rows) {
+    PFN_encodeTiled_t fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)nz, (cuuint64_t)ny, (cuuint64_t)planes};
+    const cuuint64_t strides[2] = {(cuuint64_t)nz * 4, (cuuint64_t)nz * ny * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)nz, (cuuint32_t)box_rows, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// arr3: 3-case array (3 nx planes), d1: optional D^-1 (nx planes), kap: factors
+static bool k6_maps(K6Maps& M, const Geo& g, const float* arr3, const float* d1, const float* kap) {
+    const int TY = k6_ty(g.nz);
+    bool ok = encode_map(&M.main[0], arr3, g.nz, g.ny, 3LL * g.nx, TY) && encode_map(&M.halo[0], arr3, g.nz, g.ny, 3LL * g.nx, 1) &&
+              encode_map(&M.main[2], kap, g.nz, g.ny, g.nx, TY) && encode_map(&M.halo[2], kap, g.nz, g.ny, g.nx, 1);
+    if (d1) ok = ok && encode_map(&M.main[1], d1, g.nz, g.ny, g.nx, TY) && encode_map(&M.halo[1], d1, g.nz, g.ny, g.nx, 1);
+    else { M.main[1] = M.main[2]; M.halo[1] = M.halo[2]; }
+    return ok;
+}
+template <class K>
+static dim3 k6_grid(K kernel, size_t smem, const Geo& g) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem);
+    if (per_sm < 1) per_sm = 1;
+    const long long units = (long long)(g.ny / k6_ty(g.nz)) * g.nx;
+    long long b = (long long)per_sm * sms;
+    if (b > units) b = units;
+    return dim3((unsigned)b, 1, 1);
+}
+static dim3 k6_block(const Geo& g) { return dim3((unsigned)(g.nz / 2), (unsigned)k6_ty(g.nz), 1); }
+
+static int kernel_gen() {     // OTM_K=2|3|4|5|6 selects the fast-path stencil generation (default 6)
+    static const int k = getenv("OTM_K") ? atoi(getenv("OTM_K")) : 6;
     return k;
 }
 template <class K>
@@ -2144,7 +2305,16 @@ static inline bool small_level(const Geo& g) { return g.n <= 65536; }
 
 void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* f,
                        const float* dinv, float omega, float* z, float* res) {
-    if (fast_tiling(g, lt) && kernel_gen() == 4) {
+    if (kernel_gen() == 6 && k6_ok(g, lt)) {
+        K6Maps M;
+        if (k6_maps(M, g, f, dinv, kap)) {
+            const size_t sm = k6_smem_bytes(4, g.nz);
+            s3_attr(k6_smooth_res, sm);
+            k6_smooth_res<<<k6_grid(k6_smooth_res, sm, g), k6_block(g), sm, s>>>(g, lt, M, omega, z, res);
+            return;
+        }
+    }
+    if (fast_tiling(g, lt) && kernel_gen() >= 4) {
         const size_t sm = s4_smem_bytes<4>();
         s3_attr(k4_smooth_res, sm);
         k4_smooth_res<<<s4_grid(k4_smooth_res, sm, g), dim3(32, kTileY), sm, s>>>(g, lt, kap, f, dinv, omega, z, res);
@@ -2182,7 +2352,23 @@ void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, co
 void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* z,
                    const float* f, const float* dinv, float omega, float* zout, bool dot, Red& red,
                    PcgScalars* sc) {
-    if (fast_tiling(g, lt) && kernel_gen() == 4) {
+    if (kernel_gen() == 6 && k6_ok(g, lt)) {
+        K6Maps M;
+        if (k6_maps(M, g, z, nullptr, kap)) {
+            const size_t sm = k6_smem_bytes(3, g.nz);
+            if (dot) {
+                s3_attr(k6_jacobi<true>, sm);
+                k6_jacobi<true><<<k6_grid(k6_jacobi<true>, sm, g), k6_block(g), sm, s>>>(
+                    g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
+            } else {
+                s3_attr(k6_jacobi<false>, sm);
+                k6_jacobi<false><<<k6_grid(k6_jacobi<false>, sm, g), k6_block(g), sm, s>>>(
+                    g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
+            }
+            return;
+        }
+    }
+    if (fast_tiling(g, lt) && kernel_gen() >= 4 && kernel_gen() != 5) {
         const size_t sm = s4_smem_bytes<3>();
         if (dot) {
             s3_attr(k4_jacobi<true>, sm);
@@ -2241,7 +2427,16 @@ void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const 
 }
 void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* p,
                  float* q, Red& red, PcgScalars* sc) {
-    if (fast_tiling(g, lt) && kernel_gen() == 4) {
+    if (kernel_gen() == 6 && k6_ok(g, lt)) {
+        K6Maps M;
+        if (k6_maps(M, g, p, nullptr, kap)) {
+            const size_t sm = k6_smem_bytes(3, g.nz);
+            s3_attr(k6_spmv, sm);
+            k6_spmv<<<k6_grid(k6_spmv, sm, g), k6_block(g), sm, s>>>(g, lt, M, q, red.partials, red.counter, sc);
+            return;
+        }
+    }
+    if (fast_tiling(g, lt) && kernel_gen() >= 4 && kernel_gen() != 5) {
         const size_t sm = s4_smem_bytes<3>();
         s3_attr(k4_spmv, sm);
         k4_spmv<<<s4_grid(k4_spmv, sm, g), dim3(32, kTileY), sm, s>>>(g, lt, kap, p, q, red.partials, red.counter,
