@@ -1955,6 +1955,125 @@ __global__ void __launch_bounds__(256, 2) k6_spmv(Geo g, LevelTemplate lt, const
     }
 }
 
+// ---- k7: TMA + register window + shuffles, one case per thread (march7) ----
+struct Op7Base {
+    int tile; int nz;
+    __device__ __forceinline__ const float* at(const float* S, int a, int r, int z) const {
+        return S + a * tile + r * nz + z;
+    }
+};
+struct Op7SmoothRes : Op7Base {   // tiles: 0 = f of the block's case, 1 = D^-1
+    static constexpr int NT = 2;
+    float omega; float* zo; float* res; long long n;
+    __device__ __forceinline__ void begin_case(int, int) {}
+    __device__ __forceinline__ float op1(const float* S, int r, int z) const {
+        return omega * *at(S, 1, r, z) * *at(S, 0, r, z);
+    }
+    __device__ __forceinline__ float2 op2(const float* S, int r, int z) const {
+        const float2 d = *reinterpret_cast<const float2*>(at(S, 1, r, z));
+        const float2 f = *reinterpret_cast<const float2*>(at(S, 0, r, z));
+        return make_float2(omega * d.x * f.x, omega * d.y * f.y);
+    }
+    __device__ __forceinline__ void prefetch(int, int, long long) {}
+    __device__ __forceinline__ void sink(const float* S0, int c, long long v, int r, int z, float2 kz, float2 zc) {
+        const float2 f = *reinterpret_cast<const float2*>(at(S0, 0, r, z));
+        *reinterpret_cast<float2*>(zo + c * n + v) = zc;
+        *reinterpret_cast<float2*>(res + c * n + v) = make_float2(f.x - kz.x, f.y - kz.y);
+    }
+};
+template <bool DOT>
+struct Op7Jacobi : Op7Base {      // tile 0 = z of the block's case; f, D^-1 prefetched
+    static constexpr int NT = 1;
+    const float* f; const float* dinv; float omega; float* zout; long long n; long long pl;
+    float2 fp, dp;
+    double acc, acc3[3];
+    __device__ __forceinline__ void begin_case(int, int last) {
+        if (last >= 0) acc3[last] += acc;
+        acc = 0.0;
+    }
+    __device__ __forceinline__ float op1(const float* S, int r, int z) const { return *at(S, 0, r, z); }
+    __device__ __forceinline__ float2 op2(const float* S, int r, int z) const {
+        return *reinterpret_cast<const float2*>(at(S, 0, r, z));
+    }
+    __device__ __forceinline__ void prefetch(int c, int x, long long vrow) {
+        const long long v = vrow + (long long)x * pl;
+        fp = __ldg(reinterpret_cast<const float2*>(f + c * n + v));
+        dp = __ldg(reinterpret_cast<const float2*>(dinv + v));
+    }
+    __device__ __forceinline__ void sink(const float*, int c, long long v, int, int, float2 kz, float2 zc) {
+        const float z0 = zc.x + omega * dp.x * (fp.x - kz.x);
+        const float z1 = zc.y + omega * dp.y * (fp.y - kz.y);
+        *reinterpret_cast<float2*>(zout + c * n + v) = make_float2(z0, z1);
+        if (DOT) acc += (double)fp.x * (double)z0 + (double)fp.y * (double)z1;
+    }
+};
+struct Op7Spmv : Op7Base {        // tile 0 = p of the block's case
+    static constexpr int NT = 1;
+    float* q; long long n; double acc, acc3[3];
+    __device__ __forceinline__ void begin_case(int, int last) {
+        if (last >= 0) acc3[last] += acc;
+        acc = 0.0;
+    }
+    __device__ __forceinline__ float op1(const float* S, int r, int z) const { return *at(S, 0, r, z); }
+    __device__ __forceinline__ float2 op2(const float* S, int r, int z) const {
+        return *reinterpret_cast<const float2*>(at(S, 0, r, z));
+    }
+    __device__ __forceinline__ void prefetch(int, int, long long) {}
+    __device__ __forceinline__ void sink(const float*, int c, long long v, int, int, float2 kp, float2 pc) {
+        *reinterpret_cast<float2*>(q + c * n + v) = kp;
+        acc += (double)pc.x * (double)kp.x + (double)pc.y * (double)kp.y;
+    }
+};
+
+__global__ void __launch_bounds__(256, 2) k7_smooth_res(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
+                                                        float omega, float* z, float* res) {
+    Op7SmoothRes op;
+    op.tile = (k6_ty(g.nz) + 2) * g.nz; op.nz = g.nz;
+    op.omega = omega; op.zo = z; op.res = res; op.n = g.n;
+    int last;
+    march7(g, lt, maps, op, last);
+}
+template <bool DOT>
+__global__ void __launch_bounds__(256, 2) k7_jacobi(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
+                                                    const float* f, const float* dinv, float omega, float* zout,
+                                                    double* partials, unsigned* counter, PcgScalars* sc) {
+    Op7Jacobi<DOT> op;
+    op.tile = (k6_ty(g.nz) + 2) * g.nz; op.nz = g.nz;
+    op.f = f; op.dinv = dinv; op.omega = omega; op.zout = zout; op.n = g.n; op.pl = g.pl;
+    op.acc = 0.0; op.acc3[0] = op.acc3[1] = op.acc3[2] = 0.0;
+    int last;
+    march7(g, lt, maps, op, last);
+    if (DOT) {
+        if (last >= 0) op.acc3[last] += op.acc;
+        double v3[3] = {op.acc3[0], op.acc3[1], op.acc3[2]};
+        if (reduce_finalize<3>(v3, partials, counter, sc->red)) {
+            for (int cc = 0; cc < 3; ++cc) {
+                const double rz = sc->red[cc];
+                sc->beta[cc] = (sc->first || sc->rz[cc] == 0.0) ? 0.0 : rz / sc->rz[cc];
+                sc->rz[cc] = rz;
+            }
+            sc->first = 0;
+        }
+    }
+}
+__global__ void __launch_bounds__(256, 2) k7_spmv(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
+                                                  float* q, double* partials, unsigned* counter, PcgScalars* sc) {
+    Op7Spmv op;
+    op.tile = (k6_ty(g.nz) + 2) * g.nz; op.nz = g.nz;
+    op.q = q; op.n = g.n; op.acc = 0.0; op.acc3[0] = op.acc3[1] = op.acc3[2] = 0.0;
+    int last;
+    march7(g, lt, maps, op, last);
+    if (last >= 0) op.acc3[last] += op.acc;
+    double v3[3] = {op.acc3[0], op.acc3[1], op.acc3[2]};
+    if (reduce_finalize<3>(v3, partials, counter, sc->red + 3)) {
+        for (int cc = 0; cc < 3; ++cc) {
+            const double pq = sc->red[3 + cc];
+            sc->pq[cc] = pq;
+            sc->alpha[cc] = (sc->active[cc] != 0.0 && pq > 0.0) ? sc->rz[cc] / pq : 0.0;
+        }
+    }
+}
+
 // host: tensor maps through the driver entry point (no libcuda link needed)
 typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1991,6 +2110,18 @@ static bool k6_maps(K6Maps& M, const Geo& g, const float* arr3, const float* d1,
     if (d1) ok = ok && encode_map(&M.main[1], d1, g.nz, g.ny, g.nx, TY) && encode_map(&M.halo[1], d1, g.nz, g.ny, g.nx, 1);
     else { M.main[1] = M.main[2]; M.halo[1] = M.halo[2]; }
     return ok;
+}
+template <class K>
+static dim3 k7_grid(K kernel, size_t smem, const Geo& g) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem);
+    if (per_sm < 1) per_sm = 1;
+    const long long units = 3LL * (g.ny / k6_ty(g.nz)) * g.nx;
+    long long b = (long long)per_sm * sms;
+    if (b > units) b = units;
+    return dim3((unsigned)b, 1, 1);
 }
 template <class K>
 static dim3 k6_grid(K kernel, size_t smem, const Geo& g) {
@@ -2305,6 +2436,15 @@ static inline bool small_level(const Geo& g) { return g.n <= 65536; }
 
 void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* f,
                        const float* dinv, float omega, float* z, float* res) {
+    if (kernel_gen() == 7 && k6_ok(g, lt)) {
+        K6Maps M;
+        if (k6_maps(M, g, f, dinv, kap)) {
+            const size_t sm = k6_smem_bytes(2, g.nz);
+            s3_attr(k7_smooth_res, sm);
+            k7_smooth_res<<<k7_grid(k7_smooth_res, sm, g), k6_block(g), sm, s>>>(g, lt, M, omega, z, res);
+            return;
+        }
+    }
     if (kernel_gen() == 6 && k6_ok(g, lt)) {
         K6Maps M;
         if (k6_maps(M, g, f, dinv, kap)) {
@@ -2352,6 +2492,22 @@ void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, co
 void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* z,
                    const float* f, const float* dinv, float omega, float* zout, bool dot, Red& red,
                    PcgScalars* sc) {
+    if (kernel_gen() == 7 && k6_ok(g, lt)) {
+        K6Maps M;
+        if (k6_maps(M, g, z, nullptr, kap)) {
+            const size_t sm = k6_smem_bytes(1, g.nz);
+            if (dot) {
+                s3_attr(k7_jacobi<true>, sm);
+                k7_jacobi<true><<<k7_grid(k7_jacobi<true>, sm, g), k6_block(g), sm, s>>>(
+                    g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
+            } else {
+                s3_attr(k7_jacobi<false>, sm);
+                k7_jacobi<false><<<k7_grid(k7_jacobi<false>, sm, g), k6_block(g), sm, s>>>(
+                    g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
+            }
+            return;
+        }
+    }
     if (kernel_gen() == 6 && k6_ok(g, lt)) {
         K6Maps M;
         if (k6_maps(M, g, z, nullptr, kap)) {
@@ -2427,6 +2583,15 @@ void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const 
 }
 void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* p,
                  float* q, Red& red, PcgScalars* sc) {
+    if (kernel_gen() == 7 && k6_ok(g, lt)) {
+        K6Maps M;
+        if (k6_maps(M, g, p, nullptr, kap)) {
+            const size_t sm = k6_smem_bytes(1, g.nz);
+            s3_attr(k7_spmv, sm);
+            k7_spmv<<<k7_grid(k7_spmv, sm, g), k6_block(g), sm, s>>>(g, lt, M, q, red.partials, red.counter, sc);
+            return;
+        }
+    }
     if (kernel_gen() == 6 && k6_ok(g, lt)) {
         K6Maps M;
         if (k6_maps(M, g, p, nullptr, kap)) {

@@ -212,3 +212,152 @@ __device__ __forceinline__ void march6(const Geo& g, const LevelTemplate& lt, co
 }
 
 }  // namespace otm
+
+namespace otm {
+
+// ---------------------------------------------------------------------------
+// k7: TMA staging (as k6) + one load case per thread with the operand window kept
+// in registers across x (only the newly landed plane is read from shared memory)
+// + z neighbours by warp shuffles (one LDS.64 per row; the two warp-edge lanes
+// read their outer neighbour from shared memory) + 21-weight FFMA2 arithmetic.
+// Work units: (case, row tile, x plane), persistent contiguous ranges per block.
+// Staged tiles per plane: NT operand-side tiles of the block's case (T, or f and
+// D^-1) with TY+2 rows, then the factor tile with TY+1 rows.
+// ---------------------------------------------------------------------------
+template <class Op>
+__device__ __forceinline__ void march7(const Geo& g, const LevelTemplate& lt, const K6Maps& maps, Op& op,
+                                       int& last_case) {
+    extern __shared__ __align__(128) float4 k6_smem4[];
+    float* smem = reinterpret_cast<float*>(k6_smem4);
+    constexpr int NT = Op::NT;
+    const int TY = k6_ty(g.nz);
+    const int ROWS = TY + 2;
+    const int SLOT = k6_slot_floats(NT, g.nz);
+    const int TILE = ROWS * g.nz;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages6 * SLOT);
+    const int tid = threadIdx.x + blockDim.x * threadIdx.y;
+    const int lane = tid & 31;
+    if (tid == 0) {
+        for (int k = 0; k < kStages6; ++k) mbar_init(bars + k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    }
+    __syncthreads();
+    unsigned phase_bits = 0;
+    const unsigned plane_bytes = (unsigned)((NT * ROWS + TY + 1) * g.nz * 4);
+    const int tz = threadIdx.x * 2;
+    const int zl = tz == 0 ? g.nz - 1 : tz - 1;
+    const int zr = tz + 2 == g.nz ? 0 : tz + 2;
+    const int tr = threadIdx.y + 1;
+    const float2 s12 = f2((float)lt.s12, (float)lt.s12);
+    const int nty = g.ny / TY;
+    const long long W = 3LL * nty * g.nx;
+    const long long B = gridDim.x;
+    long long u = W * blockIdx.x / B;
+    const long long u1 = W * (blockIdx.x + 1) / B;
+    int seq = 0;
+    last_case = -1;
+    // operand row of the new plane: value pairs at (z-1, z), (z, z+1), (z+1, z+2) from one LDS.64 + shuffles
+    auto read_row = [&](const float* S, int r, float (&out)[4]) {
+        const float2 m = op.op2(S, r, tz);
+        float left = __shfl_up_sync(0xffffffffu, m.y, 1);
+        float right = __shfl_down_sync(0xffffffffu, m.x, 1);
+        if (lane == 0) left = op.op1(S, r, zl);
+        if (lane == 31) right = op.op1(S, r, zr);
+        out[0] = left; out[1] = m.x; out[2] = m.y; out[3] = right;
+    };
+    auto read_k = [&](const float* S, int r, float (&out)[3]) {
+        const float* K = S + NT * TILE + r * g.nz;
+        const float2 m = *reinterpret_cast<const float2*>(K + tz);
+        float left = __shfl_up_sync(0xffffffffu, m.y, 1);
+        if (lane == 0) left = K[zl];
+        out[0] = left; out[1] = m.x; out[2] = m.y;
+    };
+    while (u < u1) {
+        const long long colu = u / g.nx;
+        const int x0 = (int)(u - colu * g.nx);
+        const int x1 = (int)min((long long)g.nx, x0 + (u1 - u));
+        const int c = (int)(colu / nty);
+        const int y0 = (int)(colu - (long long)c * nty) * TY;
+        const int ym = y0 == 0 ? g.ny - 1 : y0 - 1;
+        const int yp = y0 + TY == g.ny ? 0 : y0 + TY;
+        const int nplanes = (x1 - x0) + 2;
+        op.begin_case(c, last_case);
+        auto issue = [&](int s) {
+            const int k = (seq + s) % kStages6;
+            float* S = smem + k * SLOT;
+            int x = x0 - 1 + s;
+            x = x < 0 ? x + g.nx : (x >= g.nx ? x - g.nx : x);
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            mbar_expect_tx(bars + k, plane_bytes);
+#pragma unroll
+            for (int a = 0; a < NT; ++a) {
+                float* T = S + a * TILE;
+                const int mi = a == 0 ? 0 : 1;                 // tile 0: the case array; tile 1: D^-1
+                const int xc = a == 0 ? c * g.nx + x : x;
+                tma_load_3d(T + g.nz, &maps.main[mi], 0, y0, xc, bars + k);
+                tma_load_3d(T, &maps.halo[mi], 0, ym, xc, bars + k);
+                tma_load_3d(T + (TY + 1) * g.nz, &maps.halo[mi], 0, yp, xc, bars + k);
+            }
+            float* K = S + NT * TILE;
+            tma_load_3d(K + g.nz, &maps.main[2], 0, y0, x, bars + k);
+            tma_load_3d(K, &maps.halo[2], 0, ym, x, bars + k);
+        };
+        if (tid == 0)
+            for (int s = 0; s < kAhead6 && s < nplanes; ++s) issue(s);
+        const long long vrow = (long long)(y0 + threadIdx.y) * g.nz + tz;
+        op.prefetch(c, x0, vrow);
+        float Pm[3][4], P0[3][4], Pp[3][4], Ka[2][3], Kb[2][3];
+        for (int s = 0; s < nplanes; ++s) {
+            const int k = (seq + s) % kStages6;
+            mbar_wait(bars + k, (phase_bits >> k) & 1u);
+            phase_bits ^= 1u << k;
+            __syncthreads();
+            if (tid == 0 && s + kAhead6 < nplanes) issue(s + kAhead6);
+            const float* Sk = smem + k * SLOT;
+            if (s == 0) {
+#pragma unroll
+                for (int j = 0; j < 3; ++j) read_row(Sk, tr - 1 + j, Pm[j]);
+#pragma unroll
+                for (int jj = 0; jj < 2; ++jj) read_k(Sk, tr - 1 + jj, Ka[jj]);
+                continue;
+            }
+            if (s == 1) {
+#pragma unroll
+                for (int j = 0; j < 3; ++j) read_row(Sk, tr - 1 + j, P0[j]);
+#pragma unroll
+                for (int jj = 0; jj < 2; ++jj) read_k(Sk, tr - 1 + jj, Kb[jj]);
+                continue;
+            }
+            // operand plane x+1 lands in Pp; factor planes x-1 (Ka) and x (Kb) are held
+#pragma unroll
+            for (int j = 0; j < 3; ++j) read_row(Sk, tr - 1 + j, Pp[j]);
+            W21 w;
+            w21_build(Ka, Kb, w);
+            const float2 kt = fmul2(s12, apply21(w, Pm, P0, Pp));
+            const int x = x0 + s - 2;
+            const float* S0 = smem + ((seq + s - 1) % kStages6) * SLOT;
+            op.sink(S0, c, vrow + (long long)x * g.pl, tr, tz, kt, f2(P0[1][1], P0[1][2]));
+            if (x + 1 < x1) op.prefetch(c, x + 1, vrow);
+            // slide: factor plane x+1 comes from the slot just landed
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+#pragma unroll
+                for (int m = 0; m < 4; ++m) { Pm[j][m] = P0[j][m]; P0[j][m] = Pp[j][m]; }
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+#pragma unroll
+                for (int m = 0; m < 3; ++m) Ka[jj][m] = Kb[jj][m];
+            }
+            if (s + 1 < nplanes) {
+#pragma unroll
+                for (int jj = 0; jj < 2; ++jj) read_k(Sk, tr - 1 + jj, Kb[jj]);
+            }
+        }
+        last_case = c;
+        seq = (seq + nplanes) % kStages6;
+        __syncthreads();
+        u += x1 - x0;
+    }
+}
+
+}  // namespace otm
