@@ -48,7 +48,7 @@ typedef struct otm_params {
     int direct_limit;      /* 40000 (solver.py:212) */
     /* B200 solver knobs (no reference counterpart) */
     double jacobi_omega;   /* damped-Jacobi weight of the V-cycle smoother, 0.8 */
-    double inner_reduction;/* fp32 inner PCG relative reduction floor per refinement step, 1e-4 */
+    double inner_reduction;/* fp32 inner PCG relative reduction floor per refinement step, 1e-5 */
     int max_inner;         /* cap on inner PCG iterations per refinement step, 40 */
     int device;            /* CUDA ordinal */
 } otm_params;

@@ -432,7 +432,7 @@ void otm_default_params(otm_params* p) {
     p->coarse_target = 64;
     p->direct_limit = 40000;
     p->jacobi_omega = 0.8;
-    p->inner_reduction = 1e-4;
+    p->inner_reduction = 1e-5;
     p->max_inner = 40;
     p->device = 0;
 }
