@@ -63,6 +63,8 @@ struct otm_ctx {
     SimpParams sp{};
     double* kap64 = nullptr;
     double* T64 = nullptr;
+    double* Tprev = nullptr;     // previous design iteration's fields (warm-start extrapolation)
+    int extrap_count = 0;
     double* rho_f = nullptr;   // last filtered density used by otm_build (for sensitivities)
     double* sensf = nullptr;   // design-loop scratch: sensitivity wrt rho_f, then wrt rho
     double* sens = nullptr;
@@ -587,7 +589,7 @@ int otm_destroy(otm_ctx* ctx) {
     if (ctx->gexec_loop) cudaGraphExecDestroy(ctx->gexec_loop);
     for (auto& s : ctx->slots) { cudaEventDestroy(s.a); cudaEventDestroy(s.b); }
     auto F = [](void* p) { if (p) cudaFree(p); };
-    F(ctx->kap64); F(ctx->T64); F(ctx->rho_f); F(ctx->sensf); F(ctx->sens); F(ctx->r); F(ctx->p); F(ctx->q); F(ctx->d);
+    F(ctx->kap64); F(ctx->T64); F(ctx->Tprev); F(ctx->rho_f); F(ctx->sensf); F(ctx->sens); F(ctx->r); F(ctx->p); F(ctx->q); F(ctx->d);
     for (size_t l = 0; l < ctx->L.size(); ++l) {
         F(ctx->L[l].kap); F(ctx->L[l].dinv); F(ctx->L[l].z); F(ctx->L[l].res);
         if (l > 0) F(ctx->L[l].f);
@@ -1113,6 +1115,16 @@ int otm_run_step(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, dou
     int rc = build_levels(ctx);
     if (rc) return rc;
     ctx->warm = st->warm != 0;
+    static const double theta = getenv("OTM_EXTRAP") ? atof(getenv("OTM_EXTRAP")) : 0.0;
+    if (theta != 0.0 && ctx->warm) {
+        if (!ctx->Tprev) {
+            CK(dalloc(ctx, &ctx->Tprev, 3 * n));
+            CK(cudaMemcpyAsync(ctx->Tprev, ctx->T64, 3 * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        } else {
+            launch_extrap(s, 3 * n, ctx->T64, ctx->Tprev, theta);
+            ctx->launches++;
+        }
+    }
     int cycles = 0;
     double resid[3];
     rc = otm_solve(ctx, nullptr, cfg->solver_tol, cfg->max_vcycles, &cycles, resid);

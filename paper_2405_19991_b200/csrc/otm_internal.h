@@ -143,6 +143,7 @@ void launch_upd(cudaStream_t s, long long n, float* d, float* r, const float* p,
 void launch_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* res, float* fc);
 void launch_prolong(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* zc, float* zf);
 void launch_loop_ctl(cudaStream_t s, PcgScalars* sc, unsigned long long handle);
+void launch_extrap(cudaStream_t s, long long n3, double* T, double* Tprev, double theta);
 void launch_Tupd(cudaStream_t s, long long n3, double* T, const float* d);
 void launch_submean(cudaStream_t s, long long n, double* T, const double* sumT);
 void launch_tensor(cudaStream_t s, const Geo& g, const double* T, const double* kap, Red& red, double* out6);

@@ -1074,6 +1074,15 @@ __global__ void k_loop_ctl(PcgScalars* sc, cudaGraphConditionalHandle h) {
     cudaGraphSetConditional(h, more ? 1u : 0u);
 }
 
+// Warm-start extrapolation across design iterations: T <- T + theta (T - T_prev), T_prev <- T.
+__global__ void k_extrap(long long n3, double* __restrict__ T, double* __restrict__ Tprev, double theta) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n3) return;
+    const double t = T[i];
+    T[i] = t + theta * (t - Tprev[i]);
+    Tprev[i] = t;
+}
+
 // T += d (fp64 accumulation of the fp32 correction)
 __global__ void k_Tupd(long long n3, double* __restrict__ T, const float* __restrict__ d) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -2659,6 +2668,9 @@ void launch_loop_ctl(cudaStream_t s, PcgScalars* sc, unsigned long long handle) 
     k_loop_ctl<<<1, 1, 0, s>>>(sc, (cudaGraphConditionalHandle)handle);
 }
 void launch_vtail(cudaStream_t s, const TailArgs& a) { k_vtail<<<1, 1024, 0, s>>>(a); }
+void launch_extrap(cudaStream_t s, long long n3, double* T, double* Tprev, double theta) {
+    k_extrap<<<nblk(n3, 256), 256, 0, s>>>(n3, T, Tprev, theta);
+}
 void launch_Tupd(cudaStream_t s, long long n3, double* T, const float* d) {
     k_Tupd<<<nblk(n3, 256), 256, 0, s>>>(n3, T, d);
 }

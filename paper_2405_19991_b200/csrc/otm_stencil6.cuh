@@ -171,12 +171,9 @@ __device__ __forceinline__ void march6(const Geo& g, const LevelTemplate& lt, co
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 auto row = [&](const float* S, int j, float2& L, float2& C, float2& R) {
-                    // one LDS.64 per row; z-1 / z+2 from the neighbouring lanes (warp-edge lanes read smem)
+                    const float a0 = op.op1(S, c, tr + j, zl);
                     const float2 m = op.op2(S, c, tr + j, tz);
-                    float a0 = __shfl_up_sync(0xffffffffu, m.y, 1);
-                    float a3 = __shfl_down_sync(0xffffffffu, m.x, 1);
-                    if (lane == 0) a0 = op.op1(S, c, tr + j, zl);
-                    if (lane == 31) a3 = op.op1(S, c, tr + j, zr);
+                    const float a3 = op.op1(S, c, tr + j, zr);
                     L = f2(a0, m.x);
                     C = m;
                     R = f2(m.y, a3);
