@@ -214,16 +214,20 @@ def _run_config_c(cfg: RunConfig) -> _lib.RunConfigC:
     return c
 
 
+def _check_supported(config: RunConfig):
+    if config.model is Model.MIN_VOLUME_MMA:
+        raise NotImplementedError("model 'mma' (minimum-volume MMA) is outside the B200 hot path")
+    if config.sens_smoothing:
+        raise NotImplementedError("sensitivity smoothing is off in the reference hot path and not ported")
+    if config.filter.kernel is not None:
+        raise NotImplementedError("custom filter kernels are not supported on the device path")
+
+
 class DesignRun:
     """Device-resident state of one run; ``step()`` advances one iteration."""
 
     def __init__(self, config: RunConfig, hier=None):
-        if config.model is Model.MIN_VOLUME_MMA:
-            raise NotImplementedError("model 'mma' (minimum-volume MMA) is outside the B200 hot path")
-        if config.sens_smoothing:
-            raise NotImplementedError("sensitivity smoothing is off in the reference hot path and not ported")
-        if config.filter.kernel is not None:
-            raise NotImplementedError("custom filter kernels are not supported on the device path")
+        _check_supported(config)
         self.config = config
         from .solver import GridHierarchy
         mp = config.material
@@ -286,6 +290,26 @@ class DesignRun:
         return self.hier.ctx.lib.otm_last_error(self.hier.ctx.h).decode()
 
 
+_HIER_CACHE: dict = {}
+
+
+def _cached_hierarchy(config: RunConfig):
+    """Reuse the device hierarchy (buffers, captured graphs) across runs of the same grid.
+
+    A run never depends on what a previous run left in it: otm_run_init starts cold
+    (T zeroed on the first evaluation) and every per-iteration buffer is rewritten."""
+    from .solver import GridHierarchy
+    mp = config.material
+    key = (tuple(int(d) for d in config.dims), float(mp.kappa0), float(mp.kappa_min), float(mp.penalty),
+           float(config.filter.radius), _dev.torch().cuda.current_device())
+    h = _HIER_CACHE.get(key)
+    if h is None:
+        _HIER_CACHE.clear()            # one grid at a time: 512^3 needs ~20 GB
+        h = GridHierarchy(config.dims, material=mp, filter_radius=config.filter.radius)
+        _HIER_CACHE[key] = h
+    return h
+
+
 def run_optimization(config: RunConfig, callback: Optional[Callable] = None,
                      device_result: bool = False) -> OptimizationResult:
     """The full design loop (optimize.py:257-379) on the device.
@@ -295,7 +319,8 @@ def run_optimization(config: RunConfig, callback: Optional[Callable] = None,
     if not report.feasible:
         warnings.warn(f"target tensor is not positive definite (leading minor {report.violated_minor} "
                       "fails); optimization may not reach it", RuntimeWarning)
-    run = DesignRun(config)
+    _check_supported(config)
+    run = DesignRun(config, hier=_cached_hierarchy(config))
 
     def result(converged):
         rho = run.rho if device_result else run.rho.cpu().numpy()
