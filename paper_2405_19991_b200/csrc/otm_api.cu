@@ -81,7 +81,11 @@ struct otm_ctx {
     bool no_coop = getenv("OTM_NO_COOP_OC") != nullptr;
     bool built = false;
     bool no_loop_graph = getenv("OTM_NO_LOOP_GRAPH") != nullptr;   // ncu cannot profile conditional graphs
-    bool no_tail = getenv("OTM_TAIL") == nullptr;   // single-CTA tail: opt-in, slower so far
+    bool eager = getenv("OTM_EAGER") != nullptr;                    // with OTM_NO_LOOP_GRAPH: no inner graph
+    // single-CTA V-cycle tail for the levels <= OTM_TAIL_VERTS vertices: opt-in, measured
+    // slower than per-level launches at 512 and 4096
+    bool no_tail = getenv("OTM_TAIL_VERTS") == nullptr;
+    long long tail_verts = getenv("OTM_TAIL_VERTS") ? atoll(getenv("OTM_TAIL_VERTS")) : 0;
     bool warm = false;
     bool have_T = false;
     std::string err;
@@ -248,7 +252,7 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false) {
     double vbytes = 0.0;
     // first level handled by the single-CTA tail (all coarser levels are tail too)
     int tl = nl - 1;
-    while (tl > 0 && ctx->L[tl - 1].g.n <= kTailMaxVerts && nl - (tl - 1) <= kTailMaxLevels) --tl;
+    while (tl > 0 && ctx->L[tl - 1].g.n <= ctx->tail_verts && nl - (tl - 1) <= kTailMaxLevels) --tl;
     const bool use_tail = tl < nl - 1 && !ctx->no_tail;
     const int top = use_tail ? tl : nl - 1;     // levels [0, top) are launched per level
     for (int l = 0; l < top; ++l) {
@@ -559,7 +563,7 @@ int otm_create(otm_ctx** out, int nx, int ny, int nz, const otm_params* pin) {
     }
     ctx->nc = (int)ctx->L.back().g.n;
     CK(dalloc(ctx, &ctx->G, (size_t)ctx->nc * ctx->nc));
-    CK(dalloc(ctx, &ctx->gj, 2 * (size_t)ctx->nc * ctx->nc + 2));
+    CK(dalloc(ctx, &ctx->gj, 2 * (size_t)ctx->nc * ctx->nc + ctx->nc + 2));
     const size_t mb = max_blocks(ctx);
     CK(dalloc(ctx, &ctx->red.partials, mb * 32));
     CK(dalloc(ctx, &ctx->red.counter, 4));
@@ -782,7 +786,12 @@ int otm_solve(otm_ctx* ctx, const double* fext, double tol, int max_cycles, int*
             for (int k = 0; k < 6; ++k) ctx->h[k] = fin.flags[k];
         } else
         for (int it = 0; it < ctx->P.max_inner; ++it) {
-            CK(cudaGraphLaunch(ctx->prof ? ctx->gexec_prof : ctx->gexec, s));
+            if (ctx->eager && !ctx->prof) {
+                int erc = enqueue_inner(ctx, false);       // profiler runs: plain stream launches
+                if (erc) return erc;
+            } else {
+                CK(cudaGraphLaunch(ctx->prof ? ctx->gexec_prof : ctx->gexec, s));
+            }
             ctx->launches += ctx->launches_per_inner;
             CK(cudaStreamSynchronize(s));
             if (ctx->prof) prof_harvest(ctx);

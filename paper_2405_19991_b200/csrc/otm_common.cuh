@@ -37,6 +37,11 @@ __device__ __forceinline__ int wrap_p(int i, int n) { return i + 1 == n ? 0 : i 
 // are bit-identical ("Determinism is a tested contract").
 // ---------------------------------------------------------------------------
 
+// Programmatic dependent launch: a kernel launched with programmatic stream
+// serialisation may start while its predecessor drains; it must not touch the
+// predecessor's outputs before this wait (a no-op for ordinary launches).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);

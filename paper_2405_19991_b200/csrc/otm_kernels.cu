@@ -17,6 +17,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <utility>
 #include <cstdlib>
 
 namespace otm {
@@ -283,27 +284,45 @@ __global__ void __launch_bounds__(1024) k_coarse_setup(Geo g, const float* __res
         Z[i] = (r == c && r > 0) ? 1.0 : 0.0;
     }
     __syncthreads();
-    // Gauss-Jordan on the SPD block A[1:,1:] (no pivoting needed).  Thread t owns
-    // column t of A (t < n) or column t-n of Z: row-p reads are broadcasts and the
-    // column updates are consecutive across lanes, so shared memory never conflicts.
+    // Gauss-Jordan on the SPD block A[1:,1:] (no pivoting needed), fully parallel per
+    // pivot: column p of A is copied aside, row p is normalised, then every thread
+    // updates a fixed column (t % 2n) of A|Z on rows t / 2n, t / 2n + rstep, ...
+    // (all loads of a thread issued before its stores).
     const int m = n - 1;
+    double* colp = Z + (size_t)n * n;          // n doubles after Z (smem or work)
+    const int ncols = 2 * n;
+    const int rstep = blockDim.x / ncols > 0 ? blockDim.x / ncols : 1;
     for (int p = 1; p <= m; ++p) {
         const double piv = A[(size_t)p * n + p];
-        __syncthreads();                       // everyone has read the pivot
-        for (int t = threadIdx.x; t < 2 * n; t += blockDim.x) {
+        for (int r = threadIdx.x; r < n; r += blockDim.x) colp[r] = (r >= 1 && r != p) ? A[(size_t)r * n + p] : 0.0;
+        __syncthreads();                       // pivot and column p read by everyone
+        for (int t = threadIdx.x; t < ncols; t += blockDim.x) {
             double* M = t < n ? A : Z;
             const int cidx = t < n ? t : t - n;
             if (cidx >= 1) M[(size_t)p * n + cidx] /= piv;
         }
         __syncthreads();                       // row p normalised
-        for (int t = threadIdx.x; t < 2 * n; t += blockDim.x) {
+        for (int w = threadIdx.x; w < rstep * ncols; w += blockDim.x) {
+            const int t = w % ncols;
             double* M = t < n ? A : Z;
             const int cidx = t < n ? t : t - n;
-            if (cidx < 1 || (t < n && cidx == p)) continue;   // column p of A is read below, never written
-            const double rowp = M[(size_t)p * n + cidx];
-            for (int r = 1; r <= m; ++r) {
-                if (r == p) continue;
-                M[(size_t)r * n + cidx] -= A[(size_t)r * n + p] * rowp;
+            if (cidx >= 1) {
+                const double rowp = M[(size_t)p * n + cidx];
+                for (int r0 = 1 + w / ncols; r0 <= m; r0 += 4 * rstep) {
+                    double v[4], c[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int r = r0 + u * rstep;
+                        const bool ok = r <= m;
+                        v[u] = ok ? M[(size_t)r * n + cidx] : 0.0;
+                        c[u] = ok ? colp[r] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int r = r0 + u * rstep;
+                        if (r <= m && r != p) M[(size_t)r * n + cidx] = v[u] - c[u] * rowp;
+                    }
+                }
             }
         }
         __syncthreads();
@@ -331,15 +350,108 @@ __global__ void __launch_bounds__(1024) k_coarse_setup(Geo g, const float* __res
     }
 }
 
+// Coarse pseudo-inverse for the common 4^3 coarsest level (n = 64): in-place
+// Gauss-Jordan inversion of the SPD block A[1:,1:] in shared memory (64 x 64
+// doubles; row/column 0 = the pinned vertex), 256 threads, two barriers per pivot,
+// a branch-free rank-1 update per pivot (~260 -> ~50 -> see DESIGN.md 4 for the
+// measured history of this kernel).
+__global__ void __launch_bounds__(256) k_coarse_setup64(Geo g, const float* __restrict__ k, CoarseTemplate ct,
+                                                         float* __restrict__ G) {
+    constexpr int N = 64;
+    extern __shared__ double sm[];
+    double* A = sm;                      // N x N
+    double* colp = sm + N * N;           // N: column p;  N..2N-1: row p;  2N: 1 / pivot
+    double* rowp = colp + N;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < N * N; i += blockDim.x) A[i] = 0.0;
+    __syncthreads();
+    if (tid < N) {                       // row-wise assembly (row r touches only its own row)
+        const int r = tid;
+        const int x = r / g.pl, rem = r - x * g.pl, y = rem / g.nz, z = rem - y * g.nz;
+        for (int a = 0; a < 8; ++a) {
+            const int ex = (x - (a & 1) + g.nx) % g.nx, ey = (y - ((a >> 1) & 1) + g.ny) % g.ny,
+                      ez = (z - ((a >> 2) & 1) + g.nz) % g.nz;
+            const double ke = (double)k[(ex * g.ny + ey) * g.nz + ez];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const int cx = (ex + (b & 1)) % g.nx, cy = (ey + ((b >> 1) & 1)) % g.ny,
+                          cz = (ez + ((b >> 2) & 1)) % g.nz;
+                A[r * N + (cx * g.ny + cy) * g.nz + cz] += ke * ct.kt[a ^ b];
+            }
+        }
+    }
+    __syncthreads();
+    // pinned vertex: zero row and column 0, so the uniform update below leaves them zero
+    if (tid < N) { A[tid] = 0.0; A[tid * N] = 0.0; }
+    __syncthreads();
+    // In-place Gauss-Jordan, branch-free: with E = A whose column p is e_p,
+    // u = d * row p (u[p] = d) and v = column p (v[p] = a_pp - 1), d = 1/a_pp,
+    // the step is A <- E - v u^T.  Thread: column c = tid % 64, rows tid/64 + 4k.
+    const int c = tid % N, g4 = tid / N;
+    double* u = rowp;
+    double* v = colp;
+    for (int p = 1; p < N; ++p) {
+        if (tid < N) {
+            const double a = A[tid * N + p];
+            v[tid] = tid == p ? a - 1.0 : a;
+        } else if (tid < 2 * N) {
+            const int cc = tid - N;
+            const double a = A[p * N + p];
+            double d = (double)__frcp_rn((float)a);      // fp32 seed + two Newton steps
+            d = d * (2.0 - a * d);
+            d = d * (2.0 - a * d);
+            u[cc] = cc == p ? d : A[p * N + cc] * d;
+        }
+        __syncthreads();
+        const double uc = u[c];
+        const bool colp_ = c == p;
+#pragma unroll
+        for (int q = 0; q < N / 4; ++q) {
+            const int r = g4 + 4 * q;
+            const double e = colp_ ? (r == p ? 1.0 : 0.0) : A[r * N + c];
+            A[r * N + c] = fma(-v[r], uc, e);
+        }
+        __syncthreads();
+    }
+    // Z = inverse on [1:,1:], zero on the pinned row/column;  G = P Z P, P = I - 11^T/N
+    __shared__ double rmean[N], cmean[N], gmean;
+    if (tid < N) {
+        double sr = 0.0;
+        for (int q = 1; q < N; ++q) sr += tid ? A[tid * N + q] : 0.0;
+        rmean[tid] = sr / N;
+    } else if (tid < 2 * N) {
+        const int cc = tid - N;
+        double t = 0.0;
+        for (int q = 1; q < N; ++q) t += cc ? A[q * N + cc] : 0.0;
+        cmean[cc] = t / N;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double sg = 0.0;
+        for (int q = 0; q < N; ++q) sg += rmean[q];
+        gmean = sg / N;
+    }
+    __syncthreads();
+    for (int i = tid; i < N * N; i += blockDim.x) {
+        const int r = i / N, cc = i % N;
+        const double zv = (r == 0 || cc == 0) ? 0.0 : A[i];
+        G[i] = (float)(zv - rmean[r] - cmean[cc] + gmean);
+    }
+}
+
 // z = G f per case (coarse_solve, solver.py:307-324); one block.
 __global__ void k_coarse_solve(int n, const float* __restrict__ G, const float* __restrict__ f,
                                float* __restrict__ z) {
-    for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) {
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int i = w0; i < 3 * n; i += nw) {                      // one warp per row, G rows coalesced
         const int c = i / n, r = i - (i / n) * n;
         const float* fr = f + (size_t)c * n;
         float s = 0.f;
-        for (int j = 0; j < n; ++j) s += G[(size_t)r * n + j] * fr[j];
-        z[i] = s;
+        for (int j = lane; j < n; j += 32) s += G[(size_t)r * n + j] * fr[j];
+        s = warp_sum(s);
+        if (lane == 0) z[i] = s;
     }
 }
 
@@ -762,6 +874,7 @@ __global__ void __launch_bounds__(128) k_spmv(Geo g, int xb, LevelTemplate lt, c
 
 // p = z + beta p   (float4: n is a multiple of 4 on every level >= 4^3; scalar tail otherwise)
 __global__ void k_pupd(long long n, const float* __restrict__ z, float* __restrict__ p, const PcgScalars* sc) {
+    pdl_wait();
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long n4 = n >> 2;
     const float b[3] = {(float)sc->beta[0], (float)sc->beta[1], (float)sc->beta[2]};
@@ -784,6 +897,7 @@ __global__ void k_pupd(long long n, const float* __restrict__ z, float* __restri
 __global__ void __launch_bounds__(256) k_upd(long long n, float* __restrict__ d, float* __restrict__ r,
                                              const float* __restrict__ p, const float* __restrict__ q,
                                              double* partials, unsigned* counter, PcgScalars* sc) {
+    pdl_wait();
     double acc[3] = {0.0, 0.0, 0.0};
     const float al[3] = {(float)sc->alpha[0], (float)sc->alpha[1], (float)sc->alpha[2]};
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -830,6 +944,7 @@ __global__ void __launch_bounds__(256) k_upd(long long n, float* __restrict__ d,
 // vertices), and updates it with 4 float2 read-modify-writes.
 __global__ void __launch_bounds__(256) k_prolong3b(Geo f, Geo c, const float* __restrict__ zc,
                                                    float* __restrict__ zf) {
+    pdl_wait();
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 3 * c.n) return;
     const int cc = (int)(i / c.n);
@@ -883,6 +998,7 @@ __global__ void __launch_bounds__(256) k_small(Geo g, LevelTemplate lt, const fl
                                                const float* __restrict__ dinv, float omega, float* __restrict__ o1,
                                                float* __restrict__ o2, double* partials, unsigned* counter,
                                                PcgScalars* sc) {
+    pdl_wait();
     // OP 0: smooth_res  (operand w D^-1 f; o1 = z0, o2 = f - K z0)
     // OP 1: jacobi      (operand a = z;    o1 = z + w D^-1 (f - K z); DOT: r.z -> beta)
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -948,6 +1064,7 @@ __global__ void __launch_bounds__(256) k_small(Geo g, LevelTemplate lt, const fl
 // restriction with every axis coarsened (3-D levels): unrolled 27-point gather
 __global__ void __launch_bounds__(256) k_restrict3(Geo f, Geo c, const float* __restrict__ res,
                                                    float* __restrict__ fc) {
+    pdl_wait();
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 3 * c.n) return;
     const int cc = (int)(i / c.n);
@@ -2253,12 +2370,14 @@ __global__ void __launch_bounds__(1024) k_vtail(TailArgs A) {
     {
         const TailLevel& C = A.L[A.nlev - 1];
         const int n = (int)C.g.n;
-        for (int i = tid; i < 3 * n; i += nt) {
+        const int lane = tid & 31;
+        for (int i = tid >> 5; i < 3 * n; i += nt >> 5) {      // one warp per row, G rows coalesced
             const int c = i / n, r = i - c * n;
             const float* fr = C.f + (size_t)c * n;
             float sum = 0.f;
-            for (int j = 0; j < n; ++j) sum += A.G[(size_t)r * n + j] * fr[j];
-            C.res[i] = sum;
+            for (int j = lane; j < n; j += 32) sum += A.G[(size_t)r * n + j] * fr[j];
+            sum = warp_sum(sum);
+            if (lane == 0) C.res[i] = sum;
         }
         __syncthreads();
     }
@@ -2303,6 +2422,28 @@ __global__ void __launch_bounds__(1024) k_vtail(TailArgs A) {
 // ===========================================================================
 
 static inline unsigned nblk(long long n, int bs) { return (unsigned)((n + bs - 1) / bs); }
+
+// Inner-loop kernels go through launch_pdl: programmatic stream serialisation lets
+// the next kernel's CTAs be scheduled while the previous grid drains (each such
+// kernel starts with pdl_wait()).  OTM_PDL=0 turns it off.
+static bool pdl_enabled() {
+    static const bool on = !(getenv("OTM_PDL") && atoi(getenv("OTM_PDL")) == 0);
+    return on;
+}
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 int stencil_chunks(const Geo& g, int* xb) {
     const long long blocks_plane = (g.pl + 127) / 128;
@@ -2392,7 +2533,17 @@ void launch_dinv(cudaStream_t s, const Geo& g, const float* k, float kdiag, floa
 }
 void launch_coarse_setup(cudaStream_t s, const Geo& g, const float* k, const CoarseTemplate& ct, double* work,
                          float* G) {
-    const size_t bytes = 2 * (size_t)g.n * g.n * sizeof(double);
+    if (g.n == 64 && !getenv("OTM_GENERIC_COARSE")) {
+        const size_t b64 = (64 * 64 + 2 * 64 + 1) * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_coarse_setup64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b64);
+            attr = true;
+        }
+        k_coarse_setup64<<<1, 256, b64, s>>>(g, k, ct, G);
+        return;
+    }
+    const size_t bytes = (2 * (size_t)g.n * g.n + g.n) * sizeof(double);
     const int use_smem = bytes <= 96 * 1024;
     if (use_smem) {
         cudaFuncSetAttribute(k_coarse_setup, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
@@ -2400,7 +2551,9 @@ void launch_coarse_setup(cudaStream_t s, const Geo& g, const float* k, const Coa
     k_coarse_setup<<<1, 1024, use_smem ? bytes : 0, s>>>(g, k, ct, work, G, use_smem);
 }
 void launch_coarse_solve(cudaStream_t s, int n, const float* G, const float* f, float* z) {
-    k_coarse_solve<<<1, 256, 0, s>>>(n, G, f, z);
+    const int rows = 3 * n;
+    const int blocks = rows <= 32 ? 1 : (rows + 31) / 32 > 148 ? 148 : (rows + 31) / 32;
+    launch_pdl(k_coarse_solve, blocks, 1024, 0, s, n, G, f, z);
 }
 void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
                   const double* fext, const double* fmean, float* r32, Red& red, double* out9) {
@@ -2459,7 +2612,7 @@ void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, co
         if (k6_maps(M, g, f, dinv, kap)) {
             const size_t sm = k6_smem_bytes(4, g.nz);
             s3_attr(k6_smooth_res, sm);
-            k6_smooth_res<<<k6_grid(k6_smooth_res, sm, g), k6_block(g), sm, s>>>(g, lt, M, omega, z, res);
+            launch_pdl(k6_smooth_res, k6_grid(k6_smooth_res, sm, g), k6_block(g), sm, s, g, lt, M, omega, z, res);
             return;
         }
     }
@@ -2470,7 +2623,7 @@ void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, co
         return;
     }
     if (!fast_tiling(g, lt) && small_level(g)) {
-        k_small<0, false><<<nblk(3 * g.n, 256), 256, 0, s>>>(g, lt, kap, nullptr, f, dinv, omega, z, res, nullptr,
+        launch_pdl(k_small<0, false>, nblk(3 * g.n, 256), 256, 0, s, g, lt, kap, nullptr, f, dinv, omega, z, res, nullptr,
                                                              nullptr, nullptr);
         return;
     }
@@ -2523,11 +2676,11 @@ void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const 
             const size_t sm = k6_smem_bytes(3, g.nz);
             if (dot) {
                 s3_attr(k6_jacobi<true>, sm);
-                k6_jacobi<true><<<k6_grid(k6_jacobi<true>, sm, g), k6_block(g), sm, s>>>(
+                launch_pdl(k6_jacobi<true>, k6_grid(k6_jacobi<true>, sm, g), k6_block(g), sm, s, 
                     g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
             } else {
                 s3_attr(k6_jacobi<false>, sm);
-                k6_jacobi<false><<<k6_grid(k6_jacobi<false>, sm, g), k6_block(g), sm, s>>>(
+                launch_pdl(k6_jacobi<false>, k6_grid(k6_jacobi<false>, sm, g), k6_block(g), sm, s, 
                     g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
             }
             return;
@@ -2548,10 +2701,10 @@ void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const 
     }
     if (!fast_tiling(g, lt) && small_level(g)) {
         if (dot)
-            k_small<1, true><<<nblk(3 * g.n, 256), 256, 0, s>>>(g, lt, kap, z, f, dinv, omega, zout, nullptr,
+            launch_pdl(k_small<1, true>, nblk(3 * g.n, 256), 256, 0, s, g, lt, kap, z, f, dinv, omega, zout, nullptr,
                                                                 red.partials, red.counter, sc);
         else
-            k_small<1, false><<<nblk(3 * g.n, 256), 256, 0, s>>>(g, lt, kap, z, f, dinv, omega, zout, nullptr,
+            launch_pdl(k_small<1, false>, nblk(3 * g.n, 256), 256, 0, s, g, lt, kap, z, f, dinv, omega, zout, nullptr,
                                                                  nullptr, nullptr, sc);
         return;
     }
@@ -2606,7 +2759,7 @@ void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const fl
         if (k6_maps(M, g, p, nullptr, kap)) {
             const size_t sm = k6_smem_bytes(3, g.nz);
             s3_attr(k6_spmv, sm);
-            k6_spmv<<<k6_grid(k6_spmv, sm, g), k6_block(g), sm, s>>>(g, lt, M, q, red.partials, red.counter, sc);
+            launch_pdl(k6_spmv, k6_grid(k6_spmv, sm, g), k6_block(g), sm, s, g, lt, M, q, red.partials, red.counter, sc);
             return;
         }
     }
@@ -2643,23 +2796,23 @@ void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const fl
 }
 void launch_pupd(cudaStream_t s, long long n, const float* z, float* p, const PcgScalars* sc) {
     const long long th = std::max<long long>(n >> 2, n & 3);
-    k_pupd<<<nblk(th, 256), 256, 0, s>>>(n, z, p, sc);
+    launch_pdl(k_pupd, nblk(th, 256), 256, 0, s, n, z, p, sc);
 }
 void launch_upd(cudaStream_t s, long long n, float* d, float* r, const float* p, const float* q, Red& red,
                 PcgScalars* sc) {
     const long long th = std::max<long long>(n >> 2, n & 3);
-    k_upd<<<nblk(th, 256), 256, 0, s>>>(n, d, r, p, q, red.partials, red.counter, sc);
+    launch_pdl(k_upd, nblk(th, 256), 256, 0, s, n, d, r, p, q, red.partials, red.counter, sc);
 }
 void launch_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* res, float* fc) {
     if (cf[0] && cf[1] && cf[2]) {
-        k_restrict3<<<nblk(3 * c.n, 256), 256, 0, s>>>(f, c, res, fc);
+        launch_pdl(k_restrict3, nblk(3 * c.n, 256), 256, 0, s, f, c, res, fc);
         return;
     }
     k_restrict<<<nblk(c.n, 256), 256, 0, s>>>(f, c, cf[0], cf[1], cf[2], res, fc);
 }
 void launch_prolong(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* zc, float* zf) {
     if (cf[0] && cf[1] && cf[2]) {
-        k_prolong3b<<<nblk(3 * c.n, 256), 256, 0, s>>>(f, c, zc, zf);
+        launch_pdl(k_prolong3b, nblk(3 * c.n, 256), 256, 0, s, f, c, zc, zf);
         return;
     }
     k_prolong<<<nblk(f.n, 256), 256, 0, s>>>(f, c, cf[0], cf[1], cf[2], zc, zf);

@@ -95,6 +95,7 @@ __device__ __forceinline__ void march6(const Geo& g, const LevelTemplate& lt, co
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
     }
     __syncthreads();
+    pdl_wait();                                            // predecessor outputs visible from here
     unsigned phase_bits = 0;                               // bit k: parity of slot k's next completion
     const unsigned plane_bytes = (unsigned)((NT * ROWS + TY + 1) * g.nz * 4);
     const int tz = threadIdx.x * 2;

@@ -336,3 +336,21 @@ def test_fast_path_solve_vs_oracle(otm, O, dims):
     res = otm.effective_tensor(h, T, rho, mp)
     kh = O.tensor_from_energies(O.pair_energies(To), rho, O.Material())
     assert np.abs(res.tensor.vec - kh).max() <= 1e-10 * np.linalg.norm(kh)
+
+
+@pytest.mark.parametrize("dims", [(16, 16, 16), (32, 32, 32)])
+def test_coarse_setup_kernels_agree(otm, dims, monkeypatch):
+    """The 4^3 coarse pseudo-inverse kernel (k_coarse_setup64) and the generic one give the
+    same preconditioner: identical PCG cycle counts and the same fields."""
+    rng = np.random.default_rng(7)
+    rho = rng.uniform(0.05, 1.0, dims)
+    mp = otm.MaterialParams()
+    h = otm.GridHierarchy(dims)
+    assert h.levels[-1].num_vertices == 64
+    T1, c1 = otm.solve_cases(h, rho, mp, tol=1e-9)
+    monkeypatch.setenv("OTM_GENERIC_COARSE", "1")
+    h2 = otm.GridHierarchy(dims)
+    T2, c2 = otm.solve_cases(h2, rho, mp, tol=1e-9)
+    assert c1 == c2
+    for i in range(3):
+        assert np.abs(T1[i] - T2[i]).max() <= 1e-7 * np.abs(T1[i]).max()
