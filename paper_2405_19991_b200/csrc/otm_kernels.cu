@@ -1425,6 +1425,7 @@ __global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* _
     cg::grid_group grid = cg::this_grid();
     __shared__ double sm[32][33];
     __shared__ double s_lp[kOcLam];
+    __shared__ double s_lpr[2];
     __shared__ int s_nlam, s_phase;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const double M = (double)n;
@@ -1438,6 +1439,15 @@ __global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* _
         grid.sync();
         if (threadIdx.x == 0) { s_phase = *(volatile int*)&C->phase; s_nlam = *(volatile int*)&C->nlam; }
         if (threadIdx.x < kOcLam) s_lp[threadIdx.x] = ((volatile double*)C->lam_pow)[threadIdx.x];
+        __syncthreads();
+        if (threadIdx.x == 0) {                          // range of the pass's nonzero lam^-damp
+            double lo = INFINITY, hi = 0.0;
+            for (int k = 0; k < s_nlam; ++k)
+                if (s_lp[k] != 0.0) { lo = fmin(lo, s_lp[k]); hi = fmax(hi, s_lp[k]); }
+            if (hi == 0.0) lo = 0.0;
+            s_lpr[0] = lo;
+            s_lpr[1] = hi;
+        }
         __syncthreads();
         if (s_phase == 3) {
             // exact candidate of the chosen multiplier (reference expression)
@@ -1481,26 +1491,70 @@ __global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* _
             continue;
         }
         // ---- one evaluation pass ----
+        // Vertices whose candidate is clamped to the same bound, or lies inside its
+        // bounds, for every multiplier of the pass ("settled") add to three per-thread
+        // sums (bound value, c_e for the linear part, free-step value); only the others
+        // ("mixed") evaluate the candidates: per lane when many lanes of a warp are
+        // mixed, else transposed (lane k = multiplier k, the vertex broadcast by shuffles).
+        // The clamp decisions are exact (fp64 products are monotone in lam^-damp).
+        const int nlam = s_nlam;
+        const double lpk = lane < nlam ? s_lp[lane] : 0.0;
+        const double lpmin = s_lpr[0], lpmax = s_lpr[1];
         double acc[kOcLam];
 #pragma unroll
         for (int k = 0; k < kOcLam; ++k) acc[k] = 0.0;
-        const int nlam = s_nlam;
-        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-             i += (long long)gridDim.x * blockDim.x) {
-            const double r = __ldg(rho + i);
-            const double desc = M * (-__ldg(sens + i));
-            const double lo = fmax(r - a.step, a.rmin), hi = fmin(r + a.step, 1.0);
-            const double lof = fmax(lo, r * a.floor_ratio);
-            const double ce = desc > 0.0 ? r * (a.sqrt_damp ? sqrt(desc) : pow(desc, a.damp)) : 0.0;
-            const double freev = desc > 0.0 ? hi : (desc < 0.0 ? lo : r);
+        double acck = 0.0, sC = 0.0, sL = 0.0, sF = 0.0;
+        const long long wstride = (long long)gridDim.x * nw * 32;
+        for (long long base = ((long long)blockIdx.x * nw + wid) * 32; base < n; base += wstride) {
+            const long long i = base + lane;
+            bool mixed = false;
+            double ce = 0.0, lof = 0.0, hi = 0.0, freev = 0.0;
+            if (i < n) {
+                const double r = __ldg(rho + i);
+                const double desc = M * (-__ldg(sens + i));
+                const double lo = fmax(r - a.step, a.rmin);
+                hi = fmin(r + a.step, 1.0);
+                lof = fmax(lo, r * a.floor_ratio);
+                ce = desc > 0.0 ? r * (a.sqrt_damp ? sqrt(desc) : pow(desc, a.damp)) : 0.0;
+                freev = desc > 0.0 ? hi : (desc < 0.0 ? lo : r);
+                const double tlo = ce * lpmin, thi = ce * lpmax;
+                if (thi <= lof) { sC += lof; sF += freev; }
+                else if (tlo >= hi) { sC += hi; sF += freev; }
+                else if (tlo >= lof && thi <= hi) { sL += ce; sF += freev; }
+                else mixed = true;
+            }
+            unsigned m = __ballot_sync(0xffffffffu, mixed);
+            if (!m) continue;
+            if (__popc(m) > 10) {
+                if (mixed) {
 #pragma unroll
-            for (int k = 0; k < kOcLam; ++k) {
-                const double lp = s_lp[k];
-                const double cand = lp == 0.0 ? freev : fmin(fmax(ce * lp, lof), hi);
-                acc[k] += k < nlam ? cand : 0.0;
+                    for (int k = 0; k < kOcLam; ++k) {
+                        const double lp = s_lp[k];
+                        const double cand = lp == 0.0 ? freev : fmin(fmax(ce * lp, lof), hi);
+                        acc[k] += k < nlam ? cand : 0.0;
+                    }
+                }
+            } else {
+                while (m) {
+                    const int j = __ffs(m) - 1;
+                    m &= m - 1;
+                    const double cej = __shfl_sync(0xffffffffu, ce, j);
+                    const double lofj = __shfl_sync(0xffffffffu, lof, j);
+                    const double hij = __shfl_sync(0xffffffffu, hi, j);
+                    const double fj = __shfl_sync(0xffffffffu, freev, j);
+                    const double cand = lpk == 0.0 ? fj : fmin(fmax(cej * lpk, lofj), hij);
+                    acck += lane < nlam ? cand : 0.0;
+                }
             }
         }
-        const double mine = warp_reduce_scatter32(acc);
+        double mine = acck + warp_reduce_scatter32(acc);
+        {
+            // warp_sum leaves the total in lane 0
+            const double C = __shfl_sync(0xffffffffu, warp_sum(sC), 0);
+            const double L = __shfl_sync(0xffffffffu, warp_sum(sL), 0);
+            const double F = __shfl_sync(0xffffffffu, warp_sum(sF), 0);
+            mine += lane < nlam ? (lpk == 0.0 ? F : C + lpk * L) : 0.0;
+        }
         sm[wid][lane] = mine;
         __syncthreads();
         if (threadIdx.x < 32) {

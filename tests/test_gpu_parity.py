@@ -354,3 +354,22 @@ def test_coarse_setup_kernels_agree(otm, dims, monkeypatch):
     assert c1 == c2
     for i in range(3):
         assert np.abs(T1[i] - T2[i]).max() <= 1e-7 * np.abs(T1[i]).max()
+
+
+def test_cooperative_oc_matches_host_search(otm, monkeypatch):
+    """The single-launch OC search (k_oc_coop, settled/mixed split of the candidate sums)
+    and the host-driven 32-candidate passes (k_oc_eval) pick the same multipliers: the
+    designs are bit-identical after 30 iterations."""
+    from paper_2405_19991_b200 import optimize
+    target = otm.ObjectiveSpec("mse", otm.ConductivityTensor([0.1, 0.1, 0.1, 0, 0, 0]))
+    out = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("OTM_NO_COOP_OC", env)
+        optimize._HIER_CACHE.clear()
+        cfg = otm.RunConfig(dims=(32, 32, 32), target=target, init=otm.InitPattern("iwp", 0.3, seed=0),
+                            max_iter=30, conv_threshold=0.0)
+        out.append(otm.run_optimization(cfg))
+    optimize._HIER_CACHE.clear()
+    assert np.array_equal(out[0].field.rho, out[1].field.rho)
+    assert [r.vstar for r in out[0].log] == [r.vstar for r in out[1].log]
