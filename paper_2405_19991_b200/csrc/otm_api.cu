@@ -91,7 +91,7 @@ struct otm_ctx {
     std::string err;
     size_t bytes = 0;
     long long launches = 0;
-    long long stat_inner = 0, stat_outer = 0, stat_solves = 0;
+    long long stat_inner = 0, stat_outer = 0, stat_solves = 0, stat_oc = 0, stat_oc_passes = 0, stat_oc_retry = 0;
     // inner-iteration graphs (plain, profiled)
     cudaGraphExec_t gexec = nullptr;
     cudaGraphExec_t gexec_prof = nullptr;
@@ -565,7 +565,7 @@ int otm_create(otm_ctx** out, int nx, int ny, int nz, const otm_params* pin) {
     CK(dalloc(ctx, &ctx->G, (size_t)ctx->nc * ctx->nc));
     CK(dalloc(ctx, &ctx->gj, 2 * (size_t)ctx->nc * ctx->nc + ctx->nc + 2));
     const size_t mb = max_blocks(ctx);
-    CK(dalloc(ctx, &ctx->red.partials, mb * 32));
+    CK(dalloc(ctx, &ctx->red.partials, mb * 32 * 2 + mb));     // k_oc_coop: 2 x partials + flags
     CK(dalloc(ctx, &ctx->red.counter, 4));
     CK(cudaMemset(ctx->red.counter, 0, 4 * sizeof(unsigned)));
     CK(dalloc(ctx, &ctx->sc, 1));
@@ -586,8 +586,10 @@ int otm_create(otm_ctx** out, int nx, int ny, int nz, const otm_params* pin) {
 int otm_destroy(otm_ctx* ctx) {
     if (!ctx) return OTM_OK;
     if (getenv("OTM_STATS") && ctx->stat_solves)
-        fprintf(stderr, "[otm] stats: solves %lld outer %lld inner %lld (%.2f inner/solve)\n", ctx->stat_solves,
-                ctx->stat_outer, ctx->stat_inner, (double)ctx->stat_inner / ctx->stat_solves);
+        fprintf(stderr, "[otm] stats: solves %lld outer %lld inner %lld (%.2f inner/solve); oc %lld passes %lld "
+                "(%.2f/update) retried %lld\n", ctx->stat_solves, ctx->stat_outer, ctx->stat_inner,
+                (double)ctx->stat_inner / ctx->stat_solves, ctx->stat_oc, ctx->stat_oc_passes,
+                ctx->stat_oc ? (double)ctx->stat_oc_passes / ctx->stat_oc : 0.0, ctx->stat_oc_retry);
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
     if (ctx->gexec_prof) cudaGraphExecDestroy(ctx->gexec_prof);
     if (ctx->gexec_loop) cudaGraphExecDestroy(ctx->gexec_loop);
@@ -951,6 +953,9 @@ static int oc_search_coop(otm_ctx* ctx, const double* rho, const double* sens, d
     OcCtl fin;
     std::memcpy(&fin, ctx->h + 256, sizeof fin);
     if (ctx->prof) ctx->prof_bytes[kProfOC] += (16.0 * fin.passes + 24.0 * (1 + fin.retried)) * ctx->g0.n;
+    ctx->stat_oc++;
+    ctx->stat_oc_passes += fin.passes;
+    ctx->stat_oc_retry += fin.retried;
     if (lam_out) *lam_out = fin.lam;
     if (active_out) *active_out = fin.active;
     if (changed_out) *changed_out = fin.changed;

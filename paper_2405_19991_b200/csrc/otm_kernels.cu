@@ -1421,37 +1421,56 @@ __device__ void oc_walk(OcCtl* C) {
 __global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* __restrict__ rho,
                                                     const double* __restrict__ sens, const OcArgs a,
                                                     double* rho_out, OcCtl* C, double* partials) {
+    // Every block keeps its own copy of the search state in shared memory and replays
+    // the same walk on the same fixed-order sums, so all blocks agree on the next
+    // multipliers with ONE grid barrier per pass.  Partial sums are double-buffered by
+    // pass parity (a block may start writing pass t+1 while another still reads pass t).
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     __shared__ double sm[32][33];
     __shared__ double s_lp[kOcLam];
     __shared__ double s_lpr[2];
-    __shared__ int s_nlam, s_phase;
+    __shared__ OcCtl sC;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const unsigned nb = gridDim.x;
     const double M = (double)n;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        C->passes = 0;
-        C->retried = 0;
-        oc_plan_first(C, a);
-        for (int k = 0; k < kOcLam; ++k) C->lam_pow[k] = k < C->nlam && C->lams[k] != 0.0 ? oc_lam_pow(a, C->lams[k]) : 0.0;
+    double* flags = partials + 2 * (size_t)nb * 32;
+    auto set_pows = [&]() {                       // all threads; sC.lams/nlam final
+        if (threadIdx.x < kOcLam) {
+            const int k = threadIdx.x;
+            sC.lam_pow[k] = k < sC.nlam && sC.lams[k] != 0.0 ? oc_lam_pow(a, sC.lams[k]) : 0.0;
+        }
+    };
+    if (threadIdx.x == 0) {
+        sC.V = C->V;
+        sC.V_retry = C->V_retry;
+        sC.bis_tol = C->bis_tol;
+        sC.passes = 0;
+        sC.retried = 0;
+        sC.changed = 0;
+        sC.active = 0;
+        sC.lam = 0.0;
+        oc_plan_first(&sC, a);
     }
+    __syncthreads();
+    set_pows();
+    int parity = 0;
     while (true) {
-        grid.sync();
-        if (threadIdx.x == 0) { s_phase = *(volatile int*)&C->phase; s_nlam = *(volatile int*)&C->nlam; }
-        if (threadIdx.x < kOcLam) s_lp[threadIdx.x] = ((volatile double*)C->lam_pow)[threadIdx.x];
+        __syncthreads();
+        if (threadIdx.x < kOcLam) s_lp[threadIdx.x] = sC.lam_pow[threadIdx.x];
         __syncthreads();
         if (threadIdx.x == 0) {                          // range of the pass's nonzero lam^-damp
             double lo = INFINITY, hi = 0.0;
-            for (int k = 0; k < s_nlam; ++k)
+            for (int k = 0; k < sC.nlam; ++k)
                 if (s_lp[k] != 0.0) { lo = fmin(lo, s_lp[k]); hi = fmax(hi, s_lp[k]); }
             if (hi == 0.0) lo = 0.0;
             s_lpr[0] = lo;
             s_lpr[1] = hi;
         }
         __syncthreads();
-        if (s_phase == 3) {
+        if (sC.phase == 3) {
             // exact candidate of the chosen multiplier (reference expression)
-            const double lam = *(volatile double*)&C->lam;
+            const double lam = sC.lam;
             int ch = 0;
             for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
                  i += (long long)gridDim.x * blockDim.x) {
@@ -1470,24 +1489,25 @@ __global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* _
                 rho_out[i] = out;
             }
             ch = __syncthreads_or(ch);
-            if (threadIdx.x == 0) partials[blockIdx.x] = ch ? 1.0 : 0.0;
+            if (threadIdx.x == 0) flags[(size_t)parity * nb + blockIdx.x] = ch ? 1.0 : 0.0;
             grid.sync();
-            if (blockIdx.x == 0 && threadIdx.x == 0) {
-                int any = 0;
-                for (unsigned b = 0; b < gridDim.x; ++b) any |= __ldcg(partials + b) != 0.0;
-                C->changed = any;
-                if (!any && !C->retried && !isnan(C->V_retry)) {
-                    C->retried = 1;
-                    C->V = C->V_retry;
-                    oc_plan_first(C, a);
-                    for (int k = 0; k < kOcLam; ++k)
-                        C->lam_pow[k] = k < C->nlam && C->lams[k] != 0.0 ? oc_lam_pow(a, C->lams[k]) : 0.0;
+            int any = 0;
+            for (unsigned b = threadIdx.x; b < nb; b += blockDim.x) any |= __ldcg(flags + (size_t)parity * nb + b) != 0.0;
+            any = __syncthreads_or(any);
+            parity ^= 1;
+            if (threadIdx.x == 0) {
+                sC.changed = any;
+                if (!any && !sC.retried && !isnan(sC.V_retry)) {
+                    sC.retried = 1;
+                    sC.V = sC.V_retry;
+                    oc_plan_first(&sC, a);
                 } else {
-                    C->phase = 4;
+                    sC.phase = 4;
                 }
             }
-            grid.sync();
-            if (*(volatile int*)&C->phase == 4) break;
+            __syncthreads();
+            if (sC.phase == 4) break;
+            set_pows();
             continue;
         }
         // ---- one evaluation pass ----
@@ -1497,13 +1517,13 @@ __global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* _
         // ("mixed") evaluate the candidates: per lane when many lanes of a warp are
         // mixed, else transposed (lane k = multiplier k, the vertex broadcast by shuffles).
         // The clamp decisions are exact (fp64 products are monotone in lam^-damp).
-        const int nlam = s_nlam;
+        const int nlam = sC.nlam;
         const double lpk = lane < nlam ? s_lp[lane] : 0.0;
         const double lpmin = s_lpr[0], lpmax = s_lpr[1];
         double acc[kOcLam];
 #pragma unroll
         for (int k = 0; k < kOcLam; ++k) acc[k] = 0.0;
-        double acck = 0.0, sC = 0.0, sL = 0.0, sF = 0.0;
+        double acck = 0.0, sCn = 0.0, sL = 0.0, sF = 0.0;
         const long long wstride = (long long)gridDim.x * nw * 32;
         for (long long base = ((long long)blockIdx.x * nw + wid) * 32; base < n; base += wstride) {
             const long long i = base + lane;
@@ -1518,8 +1538,8 @@ __global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* _
                 ce = desc > 0.0 ? r * (a.sqrt_damp ? sqrt(desc) : pow(desc, a.damp)) : 0.0;
                 freev = desc > 0.0 ? hi : (desc < 0.0 ? lo : r);
                 const double tlo = ce * lpmin, thi = ce * lpmax;
-                if (thi <= lof) { sC += lof; sF += freev; }
-                else if (tlo >= hi) { sC += hi; sF += freev; }
+                if (thi <= lof) { sCn += lof; sF += freev; }
+                else if (tlo >= hi) { sCn += hi; sF += freev; }
                 else if (tlo >= lof && thi <= hi) { sL += ce; sF += freev; }
                 else mixed = true;
             }
@@ -1550,37 +1570,53 @@ __global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* _
         double mine = acck + warp_reduce_scatter32(acc);
         {
             // warp_sum leaves the total in lane 0
-            const double C = __shfl_sync(0xffffffffu, warp_sum(sC), 0);
+            const double Cs = __shfl_sync(0xffffffffu, warp_sum(sCn), 0);
             const double L = __shfl_sync(0xffffffffu, warp_sum(sL), 0);
             const double F = __shfl_sync(0xffffffffu, warp_sum(sF), 0);
-            mine += lane < nlam ? (lpk == 0.0 ? F : C + lpk * L) : 0.0;
+            mine += lane < nlam ? (lpk == 0.0 ? F : Cs + lpk * L) : 0.0;
         }
         sm[wid][lane] = mine;
         __syncthreads();
+        double* part = partials + (size_t)parity * nb * 32;
         if (threadIdx.x < 32) {
             double t = 0.0;
             for (int w = 0; w < nw; ++w) t += sm[w][threadIdx.x];
-            partials[(size_t)blockIdx.x * 32 + threadIdx.x] = t;
+            part[(size_t)blockIdx.x * 32 + threadIdx.x] = t;
         }
         grid.sync();
-        if (blockIdx.x == 0) {
-            double t = 0.0;
-            for (unsigned b = wid; b < gridDim.x; b += nw) t += __ldcg(partials + (size_t)b * 32 + lane);
-            sm[wid][lane] = t;
-            __syncthreads();
-            if (threadIdx.x < 32) {
-                double u = 0.0;
-                for (int w = 0; w < nw; ++w) u += sm[w][threadIdx.x];
-                C->means[threadIdx.x] = u / M;
+        // every block: the same fixed-order sum of all blocks' partials
+        {
+            double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+            unsigned b = wid;
+            for (; b + 3 * nw < nb; b += 4 * nw) {
+                t0 += __ldcg(part + (size_t)b * 32 + lane);
+                t1 += __ldcg(part + (size_t)(b + nw) * 32 + lane);
+                t2 += __ldcg(part + (size_t)(b + 2 * nw) * 32 + lane);
+                t3 += __ldcg(part + (size_t)(b + 3 * nw) * 32 + lane);
             }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                __threadfence();
-                oc_walk(C);
-                for (int k = 0; k < kOcLam; ++k)
-                    C->lam_pow[k] = k < C->nlam && C->lams[k] != 0.0 ? oc_lam_pow(a, C->lams[k]) : 0.0;
-            }
+            for (; b < nb; b += nw) t0 += __ldcg(part + (size_t)b * 32 + lane);
+            sm[wid][lane] = (t0 + t1) + (t2 + t3);
         }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            double u = 0.0;
+            for (int w = 0; w < nw; ++w) u += sm[w][threadIdx.x];
+            sC.means[threadIdx.x] = u / M;
+        }
+        parity ^= 1;
+        __syncthreads();
+        if (threadIdx.x == 0) oc_walk(&sC);
+        __syncthreads();
+        set_pows();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        C->passes = sC.passes;
+        C->retried = sC.retried;
+        C->changed = sC.changed;
+        C->active = sC.active;
+        C->lam = sC.lam;
+        C->V = sC.V;
+        C->phase = sC.phase;
     }
 }
 
