@@ -86,6 +86,7 @@ struct otm_ctx {
     // slower than per-level launches at 512 and 4096
     bool no_tail = getenv("OTM_TAIL_VERTS") == nullptr;
     long long tail_verts = getenv("OTM_TAIL_VERTS") ? atoll(getenv("OTM_TAIL_VERTS")) : 0;
+    long long ctail_verts = getenv("OTM_CTAIL") ? atoll(getenv("OTM_CTAIL")) : 0;
     bool warm = false;
     bool have_T = false;
     std::string err;
@@ -251,9 +252,15 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false) {
     if (prof) prof_record(ctx, kProfVcycle, 0.0, true, sl_v);
     double vbytes = 0.0;
     // first level handled by the single-CTA tail (all coarser levels are tail too)
+    // (or the cooperative multi-CTA tail, OTM_CTAIL=<max vertices of its first level>)
+    const bool coop = ctx->ctail_verts > 0;
+    const long long tv = coop ? ctx->ctail_verts : ctx->tail_verts;
     int tl = nl - 1;
-    while (tl > 0 && ctx->L[tl - 1].g.n <= ctx->tail_verts && nl - (tl - 1) <= kTailMaxLevels) --tl;
-    const bool use_tail = tl < nl - 1 && !ctx->no_tail;
+    while (tl > 0 && ctx->L[tl - 1].g.n <= tv && nl - (tl - 1) <= kTailMaxLevels) --tl;
+    if (coop)
+        for (int l = tl + 1; l < nl; ++l)
+            if (!(ctx->L[l].cf[0] && ctx->L[l].cf[1] && ctx->L[l].cf[2])) tl = l;   // 3-D coarsening only
+    const bool use_tail = tl < nl - 1 && (coop || !ctx->no_tail);
     const int top = use_tail ? tl : nl - 1;     // levels [0, top) are launched per level
     for (int l = 0; l < top; ++l) {
         LevelBuf& A = ctx->L[l];
@@ -279,7 +286,11 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false) {
             T.lt = B.lt;
             T.kap = B.kap; T.dinv = B.dinv; T.f = B.f; T.z = B.z; T.res = B.res;
         }
-        launch_vtail(s, ta);
+        if (coop) {
+            if (launch_vtail_coop(s, ta)) return OTM_ECUDA;
+        } else {
+            launch_vtail(s, ta);
+        }
         launches += 1;
     } else {
         LevelBuf& C = ctx->L[nl - 1];

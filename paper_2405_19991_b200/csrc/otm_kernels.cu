@@ -7,6 +7,7 @@
 #include "otm_stencil3.cuh"
 #include "otm_stencil4.cuh"
 #include "otm_stencil6.cuh"
+#include "otm_stencil8.cuh"
 
 #ifndef OTM_MINB
 #define OTM_MINB 2   // min resident blocks of the fp32 fast-path stencils (register cap 128)
@@ -942,11 +943,13 @@ __global__ void __launch_bounds__(256) k_upd(long long n, float* __restrict__ d,
 // it owns the fine block (2X..2X+1, 2Y..2Y+1, 2Z..2Z+1), whose trilinear values
 // only involve the coarse corners X..X+1 x Y..Y+1 x Z..Z+1 (8 loads per 8 fine
 // vertices), and updates it with 4 float2 read-modify-writes.
-__global__ void __launch_bounds__(256) k_prolong3b(Geo f, Geo c, const float* __restrict__ zc,
-                                                   float* __restrict__ zf) {
-    pdl_wait();
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 3 * c.n) return;
+// loads of data written earlier in the same (cooperative) kernel must bypass L1
+template <bool CG>
+__device__ __forceinline__ float ldf(const float* p) { return CG ? __ldcg(p) : __ldg(p); }
+
+template <bool CG>
+__device__ __forceinline__ void prolong3b_body(const Geo& f, const Geo& c, const float* __restrict__ zc,
+                                               float* __restrict__ zf, long long i) {
     const int cc = (int)(i / c.n);
     const int v = (int)(i - (long long)cc * c.n);
     const int X = v / c.pl, rem = v - X * c.pl, Y = rem / c.nz, Z = rem - Y * c.nz;
@@ -959,7 +962,7 @@ __global__ void __launch_bounds__(256) k_prolong3b(Geo f, Geo c, const float* __
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
-            for (int k = 0; k < 2; ++k) q[p][j][k] = __ldg(a + (long long)xs[p] * c.pl + ys[j] * c.nz + zs[k]);
+            for (int k = 0; k < 2; ++k) q[p][j][k] = ldf<CG>(a + (long long)xs[p] * c.pl + ys[j] * c.nz + zs[k]);
     // interpolate along z: even fine z -> q0, odd -> (q0 + q1)/2
     float qz[2][2][2];
 #pragma unroll
@@ -984,14 +987,74 @@ __global__ void __launch_bounds__(256) k_prolong3b(Geo f, Geo c, const float* __
             }
             add = make_float2(vz0, vz1);
             float2* dst = reinterpret_cast<float2*>(out + (long long)(2 * X + a2) * f.pl + (2 * Y + b2) * f.nz + 2 * Z);
-            float2 cur = *dst;
+            float2 cur = CG ? __ldcg(dst) : *dst;
             cur.x += add.x;
             cur.y += add.y;
             *dst = cur;
         }
 }
 
+__global__ void __launch_bounds__(256) k_prolong3b(Geo f, Geo c, const float* __restrict__ zc,
+                                                   float* __restrict__ zf) {
+    pdl_wait();
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 3 * c.n) return;
+    prolong3b_body<false>(f, c, zc, zf, i);
+}
+
 // ---- small levels: one thread per (case, vertex), every load issued up front ----
+// one (case, vertex) item of the small-level smoother (OP 0: smooth_res, OP 1: jacobi)
+template <int OP, bool DOT, bool CG>
+__device__ __forceinline__ void small_item(const Geo& g, const LevelTemplate& lt, const float* __restrict__ kap,
+                                           const float* __restrict__ a, const float* __restrict__ f,
+                                           const float* __restrict__ dinv, float omega, float* __restrict__ o1,
+                                           float* __restrict__ o2, long long i, double (&dot3)[3]) {
+    const int c = (int)(i / g.n);
+    const int v = (int)(i - (long long)c * g.n);
+    const int x = v / g.pl, rem = v - x * g.pl, y = rem / g.nz, z = rem - y * g.nz;
+    const int xs[3] = {wrap_m(x, g.nx), x, wrap_p(x, g.nx)};
+    const int ys[3] = {wrap_m(y, g.ny) * g.nz, y * g.nz, wrap_p(y, g.ny) * g.nz};
+    const int zs[3] = {wrap_m(z, g.nz), z, wrap_p(z, g.nz)};
+    const float* src = (OP == 0 ? f : a) + (size_t)c * g.n;
+    float t[3][9], k[2][4];
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const int idx = xs[p] * g.pl + ys[j] + zs[q];
+                float val = ldf<CG>(src + idx);
+                if (OP == 0) val *= omega * ldf<CG>(dinv + idx);
+                t[p][j * 3 + q] = val;
+            }
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) k[p][j * 2 + q] = ldf<CG>(kap + xs[p] * g.pl + ys[j] + zs[q]);
+    float kt;
+    if (lt.equal) {
+        const KSum<float> s = ksum<float>(k);
+        kt = apply_compact<float>(t, k, s, (float)lt.s12);
+    } else {
+        float ktab[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) ktab[q] = (float)lt.kt[q];
+        kt = apply_generic<float>(t, k, ktab);
+    }
+    const float fv = ldf<CG>(f + (size_t)c * g.n + v);
+    if (OP == 0) {
+        o1[(size_t)c * g.n + v] = t[1][4];
+        o2[(size_t)c * g.n + v] = fv - kt;
+    } else {
+        const float zn = t[1][4] + omega * ldf<CG>(dinv + v) * (fv - kt);
+        o1[(size_t)c * g.n + v] = zn;
+        if (DOT) dot3[c] = (double)fv * (double)zn;
+    }
+}
+
 template <int OP, bool DOT>
 __global__ void __launch_bounds__(256) k_small(Geo g, LevelTemplate lt, const float* __restrict__ kap,
                                                const float* __restrict__ a, const float* __restrict__ f,
@@ -1003,52 +1066,7 @@ __global__ void __launch_bounds__(256) k_small(Geo g, LevelTemplate lt, const fl
     // OP 1: jacobi      (operand a = z;    o1 = z + w D^-1 (f - K z); DOT: r.z -> beta)
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     double dot3[3] = {0.0, 0.0, 0.0};
-    if (i < 3 * g.n) {
-        const int c = (int)(i / g.n);
-        const int v = (int)(i - (long long)c * g.n);
-        const int x = v / g.pl, rem = v - x * g.pl, y = rem / g.nz, z = rem - y * g.nz;
-        const int xs[3] = {wrap_m(x, g.nx), x, wrap_p(x, g.nx)};
-        const int ys[3] = {wrap_m(y, g.ny) * g.nz, y * g.nz, wrap_p(y, g.ny) * g.nz};
-        const int zs[3] = {wrap_m(z, g.nz), z, wrap_p(z, g.nz)};
-        const float* src = (OP == 0 ? f : a) + (size_t)c * g.n;
-        float t[3][9], k[2][4];
-#pragma unroll
-        for (int p = 0; p < 3; ++p)
-#pragma unroll
-            for (int j = 0; j < 3; ++j)
-#pragma unroll
-                for (int q = 0; q < 3; ++q) {
-                    const int idx = xs[p] * g.pl + ys[j] + zs[q];
-                    float val = __ldg(src + idx);
-                    if (OP == 0) val *= omega * __ldg(dinv + idx);
-                    t[p][j * 3 + q] = val;
-                }
-#pragma unroll
-        for (int p = 0; p < 2; ++p)
-#pragma unroll
-            for (int j = 0; j < 2; ++j)
-#pragma unroll
-                for (int q = 0; q < 2; ++q) k[p][j * 2 + q] = __ldg(kap + xs[p] * g.pl + ys[j] + zs[q]);
-        float kt;
-        if (lt.equal) {
-            const KSum<float> s = ksum<float>(k);
-            kt = apply_compact<float>(t, k, s, (float)lt.s12);
-        } else {
-            float ktab[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) ktab[q] = (float)lt.kt[q];
-            kt = apply_generic<float>(t, k, ktab);
-        }
-        const float fv = __ldg(f + (size_t)c * g.n + v);
-        if (OP == 0) {
-            o1[(size_t)c * g.n + v] = t[1][4];
-            o2[(size_t)c * g.n + v] = fv - kt;
-        } else {
-            const float zn = t[1][4] + omega * __ldg(dinv + v) * (fv - kt);
-            o1[(size_t)c * g.n + v] = zn;
-            if (DOT) dot3[c] = (double)fv * (double)zn;
-        }
-    }
+    if (i < 3 * g.n) small_item<OP, DOT, false>(g, lt, kap, a, f, dinv, omega, o1, o2, i, dot3);
     if (DOT) {
         if (reduce_finalize<3>(dot3, partials, counter, sc->red)) {
             for (int cc = 0; cc < 3; ++cc) {
@@ -1062,11 +1080,9 @@ __global__ void __launch_bounds__(256) k_small(Geo g, LevelTemplate lt, const fl
 }
 
 // restriction with every axis coarsened (3-D levels): unrolled 27-point gather
-__global__ void __launch_bounds__(256) k_restrict3(Geo f, Geo c, const float* __restrict__ res,
-                                                   float* __restrict__ fc) {
-    pdl_wait();
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 3 * c.n) return;
+template <bool CG>
+__device__ __forceinline__ void restrict3_body(const Geo& f, const Geo& c, const float* __restrict__ res,
+                                               float* __restrict__ fc, long long i) {
     const int cc = (int)(i / c.n);
     const int v = (int)(i - (long long)cc * c.n);
     const int X = v / c.pl, rem = v - X * c.pl, Y = rem / c.nz, Z = rem - Y * c.nz;
@@ -1081,7 +1097,7 @@ __global__ void __launch_bounds__(256) k_restrict3(Geo f, Geo c, const float* __
 #pragma unroll
         for (int b = 0; b < 3; ++b)
 #pragma unroll
-            for (int d = 0; d < 3; ++d) vals[(a * 3 + b) * 3 + d] = __ldg(r + (long long)xs[a] * f.pl + ys[b] + zs[d]);
+            for (int d = 0; d < 3; ++d) vals[(a * 3 + b) * 3 + d] = ldf<CG>(r + (long long)xs[a] * f.pl + ys[b] + zs[d]);
     float s = 0.f;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -1094,6 +1110,14 @@ __global__ void __launch_bounds__(256) k_restrict3(Geo f, Geo c, const float* __
         s += w[a] * sb;
     }
     fc[i] = s;
+}
+
+__global__ void __launch_bounds__(256) k_restrict3(Geo f, Geo c, const float* __restrict__ res,
+                                                   float* __restrict__ fc) {
+    pdl_wait();
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 3 * c.n) return;
+    restrict3_body<false>(f, c, res, fc, i);
 }
 
 // trilinear prolongation + correction, every axis coarsened: 8 coarse loads, weights 0/0.5/1
@@ -2063,13 +2087,18 @@ __global__ void __launch_bounds__(256, 2) k4_spmv(Geo g, LevelTemplate lt, const
 }
 
 // ---- k6: TMA-staged (otm_stencil6.cuh) ----
-struct Op6Base {
-    int tile; int nz;
+template <int NZv>
+struct Op6Base {                  // compile-time tile geometry: every shared-memory offset is an immediate
+    static constexpr int NZ = NZv;
+    static constexpr int nz = NZv;
+    static constexpr int tile = (512 / NZv + 2) * NZv;
     __device__ __forceinline__ const float* at(const float* S, int a, int r, int z) const {
         return S + a * tile + r * nz + z;
     }
 };
-struct Op6SmoothRes : Op6Base {   // tiles 0..2 = f cases, 3 = D^-1; operand w D^-1 f
+template <int NZv>
+struct Op6SmoothRes : Op6Base<NZv> {   // tiles 0..2 = f cases, 3 = D^-1; operand w D^-1 f
+    using Op6Base<NZv>::at;
     static constexpr int NT = 4;
     float omega; float* zo; float* res; long long n;
     __device__ __forceinline__ float op1(const float* S, int c, int r, int z) const {
@@ -2087,8 +2116,9 @@ struct Op6SmoothRes : Op6Base {   // tiles 0..2 = f cases, 3 = D^-1; operand w D
         *reinterpret_cast<float2*>(res + c * n + v) = make_float2(f.x - kz.x, f.y - kz.y);
     }
 };
-template <bool DOT>
-struct Op6Jacobi : Op6Base {      // tiles 0..2 = z cases; f, D^-1 prefetched
+template <bool DOT, int NZv>
+struct Op6Jacobi : Op6Base<NZv> {      // tiles 0..2 = z cases; f, D^-1 prefetched
+    using Op6Base<NZv>::at;
     static constexpr int NT = 3;
     const float* f; const float* dinv; float omega; float* zout; long long n; long long pl;
     float2 fp[3], dp;
@@ -2110,7 +2140,9 @@ struct Op6Jacobi : Op6Base {      // tiles 0..2 = z cases; f, D^-1 prefetched
         if (DOT) acc[c] += (double)fp[c].x * (double)z0 + (double)fp[c].y * (double)z1;
     }
 };
-struct Op6Spmv : Op6Base {        // tiles 0..2 = p cases
+template <int NZv>
+struct Op6Spmv : Op6Base<NZv> {        // tiles 0..2 = p cases
+    using Op6Base<NZv>::at;
     static constexpr int NT = 3;
     float* q; long long n; double acc[3];
     __device__ __forceinline__ float op1(const float* S, int c, int r, int z) const { return *at(S, c, r, z); }
@@ -2124,20 +2156,19 @@ struct Op6Spmv : Op6Base {        // tiles 0..2 = p cases
     }
 };
 
+template <int NZ>
 __global__ void __launch_bounds__(256, 2) k6_smooth_res(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
                                                         float omega, float* z, float* res) {
-    Op6SmoothRes op;
-    op.tile = (k6_ty(g.nz) + 2) * g.nz; op.nz = g.nz;
+    Op6SmoothRes<NZ> op;
     op.omega = omega; op.zo = z; op.res = res; op.n = g.n;
     march6(g, lt, maps, op);
 }
 
-template <bool DOT>
+template <bool DOT, int NZ>
 __global__ void __launch_bounds__(256, 2) k6_jacobi(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
                                                     const float* f, const float* dinv, float omega, float* zout,
                                                     double* partials, unsigned* counter, PcgScalars* sc) {
-    Op6Jacobi<DOT> op;
-    op.tile = (k6_ty(g.nz) + 2) * g.nz; op.nz = g.nz;
+    Op6Jacobi<DOT, NZ> op;
     op.f = f; op.dinv = dinv; op.omega = omega; op.zout = zout; op.n = g.n; op.pl = g.pl;
     op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
     march6(g, lt, maps, op);
@@ -2154,13 +2185,107 @@ __global__ void __launch_bounds__(256, 2) k6_jacobi(Geo g, LevelTemplate lt, con
     }
 }
 
+template <int NZ>
 __global__ void __launch_bounds__(256, 2) k6_spmv(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
                                                   float* q, double* partials, unsigned* counter, PcgScalars* sc) {
-    Op6Spmv op;
-    op.tile = (k6_ty(g.nz) + 2) * g.nz; op.nz = g.nz;
+    Op6Spmv<NZ> op;
     op.q = q; op.n = g.n;
     op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
     march6(g, lt, maps, op);
+    double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
+    if (reduce_finalize<3>(v3, partials, counter, sc->red + 3)) {
+        for (int cc = 0; cc < 3; ++cc) {
+            const double pq = sc->red[3 + cc];
+            sc->pq[cc] = pq;
+            sc->alpha[cc] = (sc->active[cc] != 0.0 && pq > 0.0) ? sc->rz[cc] / pq : 0.0;
+        }
+    }
+}
+
+// ---- k8: k6 staging + x register window for the three cases (march8) ----
+template <int NZ>
+__global__ void __launch_bounds__(256, 1) k8_smooth_res(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
+                                                        float omega, float* z, float* res) {
+    Op6SmoothRes<NZ> op;
+    op.omega = omega; op.zo = z; op.res = res; op.n = g.n;
+    march8(g, lt, maps, op);
+}
+
+template <bool DOT, int NZ>
+__global__ void __launch_bounds__(256, 1) k8_jacobi(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
+                                                    const float* f, const float* dinv, float omega, float* zout,
+                                                    double* partials, unsigned* counter, PcgScalars* sc) {
+    Op6Jacobi<DOT, NZ> op;
+    op.f = f; op.dinv = dinv; op.omega = omega; op.zout = zout; op.n = g.n; op.pl = g.pl;
+    op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
+    march8(g, lt, maps, op);
+    if (DOT) {
+        double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
+        if (reduce_finalize<3>(v3, partials, counter, sc->red)) {
+            for (int cc = 0; cc < 3; ++cc) {
+                const double rz = sc->red[cc];
+                sc->beta[cc] = (sc->first || sc->rz[cc] == 0.0) ? 0.0 : rz / sc->rz[cc];
+                sc->rz[cc] = rz;
+            }
+            sc->first = 0;
+        }
+    }
+}
+
+template <int NZ>
+__global__ void __launch_bounds__(256, 1) k8_spmv(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
+                                                  float* q, double* partials, unsigned* counter, PcgScalars* sc) {
+    Op6Spmv<NZ> op;
+    op.q = q; op.n = g.n;
+    op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
+    march8(g, lt, maps, op);
+    double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
+    if (reduce_finalize<3>(v3, partials, counter, sc->red + 3)) {
+        for (int cc = 0; cc < 3; ++cc) {
+            const double pq = sc->red[3 + cc];
+            sc->pq[cc] = pq;
+            sc->alpha[cc] = (sc->active[cc] != 0.0 && pq > 0.0) ? sc->rz[cc] / pq : 0.0;
+        }
+    }
+}
+
+// ---- k9: k6 staging + x register window for the three cases (march8) ----
+template <int NZ>
+__global__ void __launch_bounds__(256, 1) k9_smooth_res(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
+                                                        float omega, float* z, float* res) {
+    Op6SmoothRes<NZ> op;
+    op.omega = omega; op.zo = z; op.res = res; op.n = g.n;
+    march9(g, lt, maps, op);
+}
+
+template <bool DOT, int NZ>
+__global__ void __launch_bounds__(256, 1) k9_jacobi(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
+                                                    const float* f, const float* dinv, float omega, float* zout,
+                                                    double* partials, unsigned* counter, PcgScalars* sc) {
+    Op6Jacobi<DOT, NZ> op;
+    op.f = f; op.dinv = dinv; op.omega = omega; op.zout = zout; op.n = g.n; op.pl = g.pl;
+    op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
+    march9(g, lt, maps, op);
+    if (DOT) {
+        double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
+        if (reduce_finalize<3>(v3, partials, counter, sc->red)) {
+            for (int cc = 0; cc < 3; ++cc) {
+                const double rz = sc->red[cc];
+                sc->beta[cc] = (sc->first || sc->rz[cc] == 0.0) ? 0.0 : rz / sc->rz[cc];
+                sc->rz[cc] = rz;
+            }
+            sc->first = 0;
+        }
+    }
+}
+
+template <int NZ>
+__global__ void __launch_bounds__(256, 1) k9_spmv(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
+                                                  float* q, double* partials, unsigned* counter, PcgScalars* sc) {
+    Op6Spmv<NZ> op;
+    op.q = q; op.n = g.n;
+    op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
+    march9(g, lt, maps, op);
     double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
     if (reduce_finalize<3>(v3, partials, counter, sc->red + 3)) {
         for (int cc = 0; cc < 3; ++cc) {
@@ -2353,8 +2478,8 @@ static dim3 k6_grid(K kernel, size_t smem, const Geo& g) {
 }
 static dim3 k6_block(const Geo& g) { return dim3((unsigned)(g.nz / 2), (unsigned)k6_ty(g.nz), 1); }
 
-static int kernel_gen() {     // OTM_K=2|3|4|5|6 selects the fast-path stencil generation (default 6)
-    static const int k = getenv("OTM_K") ? atoi(getenv("OTM_K")) : 6;
+static int kernel_gen() {     // OTM_K=2..9 selects the fast-path stencil generation (default 8)
+    static const int k = getenv("OTM_K") ? atoi(getenv("OTM_K")) : 8;
     return k;
 }
 template <class K>
@@ -2504,6 +2629,55 @@ __global__ void __launch_bounds__(1024) k_vtail(TailArgs A) {
             L.res[i] = L.z[i] + om * L.dinv[v] * (L.f[i] - tail_apply(L, L.z, c, v));
         }
         __syncthreads();
+    }
+}
+
+// ===========================================================================
+// V-cycle tail as ONE cooperative launch: the levels from the first tail level
+// (<= kCTailVerts vertices, every axis coarsened) down to the coarse solve and
+// back up, phases separated by grid barriers instead of kernel boundaries.  The
+// per-item code is the same as the per-level kernels (k_small, k_restrict3,
+// k_prolong3b, k_coarse_solve); loads of arrays written inside this launch go to
+// L2 (ld.cg).  Output: the post-smoothed correction in L[0].res, as the per-level
+// sequence leaves it.
+// ===========================================================================
+__global__ void __launch_bounds__(256) k_vtail_coop(TailArgs A) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long nt = (long long)gridDim.x * blockDim.x;
+    const float om = A.omega;
+    double dummy[3];
+    for (int l = 0; l + 1 < A.nlev; ++l) {
+        const TailLevel& L = A.L[l];
+        const TailLevel& C = A.L[l + 1];
+        for (long long i = t0; i < 3 * L.g.n; i += nt)
+            small_item<0, false, true>(L.g, L.lt, L.kap, nullptr, L.f, L.dinv, om, L.z, L.res, i, dummy);
+        grid.sync();
+        for (long long i = t0; i < 3 * C.g.n; i += nt) restrict3_body<true>(L.g, C.g, L.res, C.f, i);
+        grid.sync();
+    }
+    {
+        const TailLevel& C = A.L[A.nlev - 1];
+        const int n = (int)C.g.n;
+        const int lane = threadIdx.x & 31;
+        for (long long w = t0 >> 5; w < 3 * n; w += nt >> 5) {
+            const int c = (int)(w / n), r = (int)(w - (long long)c * n);
+            float sum = 0.f;
+            for (int j = lane; j < n; j += 32) sum += __ldg(A.G + (size_t)r * n + j) * __ldcg(C.f + (size_t)c * n + j);
+            sum = warp_sum(sum);
+            if (lane == 0) C.res[w] = sum;
+        }
+        grid.sync();
+    }
+    for (int l = A.nlev - 2; l >= 0; --l) {
+        const TailLevel& L = A.L[l];
+        const TailLevel& C = A.L[l + 1];
+        for (long long i = t0; i < 3 * C.g.n; i += nt) prolong3b_body<true>(L.g, C.g, C.res, L.z, i);
+        grid.sync();
+        for (long long i = t0; i < 3 * L.g.n; i += nt)
+            small_item<1, false, true>(L.g, L.lt, L.kap, L.z, L.f, L.dinv, om, L.res, nullptr, i, dummy);
+        if (l > 0) grid.sync();
     }
 }
 
@@ -2697,12 +2871,81 @@ void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, co
             return;
         }
     }
+    if (kernel_gen() == 9 && k6_ok(g, lt)) {
+        K6Maps M;
+        if (k6_maps(M, g, f, dinv, kap)) {
+            switch (g.nz) {
+            case 64: {
+                constexpr int NZV = 64;
+                    const size_t sm = k9_smem_bytes(4, g.nz);
+                    s3_attr(k9_smooth_res<NZV>, sm);
+                    launch_pdl(k9_smooth_res<NZV>, k6_grid(k9_smooth_res<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, omega, z, res);
+            } break;
+            case 128: {
+                constexpr int NZV = 128;
+                    const size_t sm = k9_smem_bytes(4, g.nz);
+                    s3_attr(k9_smooth_res<NZV>, sm);
+                    launch_pdl(k9_smooth_res<NZV>, k6_grid(k9_smooth_res<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, omega, z, res);
+            } break;
+            default: {
+                constexpr int NZV = 256;
+                    const size_t sm = k9_smem_bytes(4, g.nz);
+                    s3_attr(k9_smooth_res<NZV>, sm);
+                    launch_pdl(k9_smooth_res<NZV>, k6_grid(k9_smooth_res<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, omega, z, res);
+            } break;
+            }
+            return;
+        }
+    }
+    if (kernel_gen() == 8 && k6_ok(g, lt)) {
+        K6Maps M;
+        if (k6_maps(M, g, f, dinv, kap)) {
+            switch (g.nz) {
+            case 64: {
+                constexpr int NZV = 64;
+                    const size_t sm = k8_smem_bytes(4, g.nz);
+                    s3_attr(k8_smooth_res<NZV>, sm);
+                    launch_pdl(k8_smooth_res<NZV>, k6_grid(k8_smooth_res<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, omega, z, res);
+            } break;
+            case 128: {
+                constexpr int NZV = 128;
+                    const size_t sm = k8_smem_bytes(4, g.nz);
+                    s3_attr(k8_smooth_res<NZV>, sm);
+                    launch_pdl(k8_smooth_res<NZV>, k6_grid(k8_smooth_res<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, omega, z, res);
+            } break;
+            default: {
+                constexpr int NZV = 256;
+                    const size_t sm = k8_smem_bytes(4, g.nz);
+                    s3_attr(k8_smooth_res<NZV>, sm);
+                    launch_pdl(k8_smooth_res<NZV>, k6_grid(k8_smooth_res<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, omega, z, res);
+            } break;
+            }
+            return;
+        }
+    }
     if (kernel_gen() == 6 && k6_ok(g, lt)) {
         K6Maps M;
         if (k6_maps(M, g, f, dinv, kap)) {
-            const size_t sm = k6_smem_bytes(4, g.nz);
-            s3_attr(k6_smooth_res, sm);
-            launch_pdl(k6_smooth_res, k6_grid(k6_smooth_res, sm, g), k6_block(g), sm, s, g, lt, M, omega, z, res);
+            switch (g.nz) {
+            case 64: {
+                constexpr int NZV = 64;
+                    const size_t sm = k6_smem_bytes(4, g.nz);
+                    s3_attr(k6_smooth_res<NZV>, sm);
+                    launch_pdl(k6_smooth_res<NZV>, k6_grid(k6_smooth_res<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, omega, z, res);
+            } break;
+            case 128: {
+                constexpr int NZV = 128;
+                    const size_t sm = k6_smem_bytes(4, g.nz);
+                    s3_attr(k6_smooth_res<NZV>, sm);
+                    launch_pdl(k6_smooth_res<NZV>, k6_grid(k6_smooth_res<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, omega, z, res);
+            } break;
+            default: {
+                constexpr int NZV = 256;
+                    const size_t sm = k6_smem_bytes(4, g.nz);
+                    s3_attr(k6_smooth_res<NZV>, sm);
+                    launch_pdl(k6_smooth_res<NZV>, k6_grid(k6_smooth_res<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, omega, z, res);
+            } break;
+            }
             return;
         }
     }
@@ -2760,18 +3003,143 @@ void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const 
             return;
         }
     }
+    if (kernel_gen() == 9 && k6_ok(g, lt)) {
+        K6Maps M;
+        if (k6_maps(M, g, z, nullptr, kap)) {
+            switch (g.nz) {
+            case 64: {
+                constexpr int NZV = 64;
+                    const size_t sm = k9_smem_bytes(3, g.nz);
+                    if (dot) {
+                        s3_attr(k9_jacobi<true, NZV>, sm);
+                        launch_pdl(k9_jacobi<true, NZV>, k6_grid(k9_jacobi<true, NZV>, sm, g), k6_block(g), sm, s,
+                            g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
+                    } else {
+                        s3_attr(k9_jacobi<false, NZV>, sm);
+                        launch_pdl(k9_jacobi<false, NZV>, k6_grid(k9_jacobi<false, NZV>, sm, g), k6_block(g), sm, s,
+                            g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
+                    }
+            } break;
+            case 128: {
+                constexpr int NZV = 128;
+                    const size_t sm = k9_smem_bytes(3, g.nz);
+                    if (dot) {
+                        s3_attr(k9_jacobi<true, NZV>, sm);
+                        launch_pdl(k9_jacobi<true, NZV>, k6_grid(k9_jacobi<true, NZV>, sm, g), k6_block(g), sm, s,
+                            g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
+                    } else {
+                        s3_attr(k9_jacobi<false, NZV>, sm);
+                        launch_pdl(k9_jacobi<false, NZV>, k6_grid(k9_jacobi<false, NZV>, sm, g), k6_block(g), sm, s,
+                            g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
+                    }
+            } break;
+            default: {
+                constexpr int NZV = 256;
+                    const size_t sm = k9_smem_bytes(3, g.nz);
+                    if (dot) {
+                        s3_attr(k9_jacobi<true, NZV>, sm);
+                        launch_pdl(k9_jacobi<true, NZV>, k6_grid(k9_jacobi<true, NZV>, sm, g), k6_block(g), sm, s,
+                            g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
+                    } else {
+                        s3_attr(k9_jacobi<false, NZV>, sm);
+                        launch_pdl(k9_jacobi<false, NZV>, k6_grid(k9_jacobi<false, NZV>, sm, g), k6_block(g), sm, s,
+                            g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
+                    }
+            } break;
+            }
+            return;
+        }
+    }
+    if (kernel_gen() == 8 && k6_ok(g, lt)) {
+        K6Maps M;
+        if (k6_maps(M, g, z, nullptr, kap)) {
+            switch (g.nz) {
+            case 64: {
+                constexpr int NZV = 64;
+                    const size_t sm = k8_smem_bytes(3, g.nz);
+                    if (dot) {
+                        s3_attr(k8_jacobi<true, NZV>, sm);
+                        launch_pdl(k8_jacobi<true, NZV>, k6_grid(k8_jacobi<true, NZV>, sm, g), k6_block(g), sm, s,
+                            g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
+                    } else {
+                        s3_attr(k8_jacobi<false, NZV>, sm);
+                        launch_pdl(k8_jacobi<false, NZV>, k6_grid(k8_jacobi<false, NZV>, sm, g), k6_block(g), sm, s,
+                            g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
+                    }
+            } break;
+            case 128: {
+                constexpr int NZV = 128;
+                    const size_t sm = k8_smem_bytes(3, g.nz);
+                    if (dot) {
+                        s3_attr(k8_jacobi<true, NZV>, sm);
+                        launch_pdl(k8_jacobi<true, NZV>, k6_grid(k8_jacobi<true, NZV>, sm, g), k6_block(g), sm, s,
+                            g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
+                    } else {
+                        s3_attr(k8_jacobi<false, NZV>, sm);
+                        launch_pdl(k8_jacobi<false, NZV>, k6_grid(k8_jacobi<false, NZV>, sm, g), k6_block(g), sm, s,
+                            g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
+                    }
+            } break;
+            default: {
+                constexpr int NZV = 256;
+                    const size_t sm = k8_smem_bytes(3, g.nz);
+                    if (dot) {
+                        s3_attr(k8_jacobi<true, NZV>, sm);
+                        launch_pdl(k8_jacobi<true, NZV>, k6_grid(k8_jacobi<true, NZV>, sm, g), k6_block(g), sm, s,
+                            g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
+                    } else {
+                        s3_attr(k8_jacobi<false, NZV>, sm);
+                        launch_pdl(k8_jacobi<false, NZV>, k6_grid(k8_jacobi<false, NZV>, sm, g), k6_block(g), sm, s,
+                            g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
+                    }
+            } break;
+            }
+            return;
+        }
+    }
     if (kernel_gen() == 6 && k6_ok(g, lt)) {
         K6Maps M;
         if (k6_maps(M, g, z, nullptr, kap)) {
-            const size_t sm = k6_smem_bytes(3, g.nz);
-            if (dot) {
-                s3_attr(k6_jacobi<true>, sm);
-                launch_pdl(k6_jacobi<true>, k6_grid(k6_jacobi<true>, sm, g), k6_block(g), sm, s, 
-                    g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
-            } else {
-                s3_attr(k6_jacobi<false>, sm);
-                launch_pdl(k6_jacobi<false>, k6_grid(k6_jacobi<false>, sm, g), k6_block(g), sm, s, 
-                    g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
+            switch (g.nz) {
+            case 64: {
+                constexpr int NZV = 64;
+                    const size_t sm = k6_smem_bytes(3, g.nz);
+                    if (dot) {
+                        s3_attr(k6_jacobi<true, NZV>, sm);
+                        launch_pdl(k6_jacobi<true, NZV>, k6_grid(k6_jacobi<true, NZV>, sm, g), k6_block(g), sm, s, 
+                            g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
+                    } else {
+                        s3_attr(k6_jacobi<false, NZV>, sm);
+                        launch_pdl(k6_jacobi<false, NZV>, k6_grid(k6_jacobi<false, NZV>, sm, g), k6_block(g), sm, s, 
+                            g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
+                    }
+            } break;
+            case 128: {
+                constexpr int NZV = 128;
+                    const size_t sm = k6_smem_bytes(3, g.nz);
+                    if (dot) {
+                        s3_attr(k6_jacobi<true, NZV>, sm);
+                        launch_pdl(k6_jacobi<true, NZV>, k6_grid(k6_jacobi<true, NZV>, sm, g), k6_block(g), sm, s, 
+                            g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
+                    } else {
+                        s3_attr(k6_jacobi<false, NZV>, sm);
+                        launch_pdl(k6_jacobi<false, NZV>, k6_grid(k6_jacobi<false, NZV>, sm, g), k6_block(g), sm, s, 
+                            g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
+                    }
+            } break;
+            default: {
+                constexpr int NZV = 256;
+                    const size_t sm = k6_smem_bytes(3, g.nz);
+                    if (dot) {
+                        s3_attr(k6_jacobi<true, NZV>, sm);
+                        launch_pdl(k6_jacobi<true, NZV>, k6_grid(k6_jacobi<true, NZV>, sm, g), k6_block(g), sm, s, 
+                            g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
+                    } else {
+                        s3_attr(k6_jacobi<false, NZV>, sm);
+                        launch_pdl(k6_jacobi<false, NZV>, k6_grid(k6_jacobi<false, NZV>, sm, g), k6_block(g), sm, s, 
+                            g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
+                    }
+            } break;
             }
             return;
         }
@@ -2844,12 +3212,81 @@ void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const fl
             return;
         }
     }
+    if (kernel_gen() == 9 && k6_ok(g, lt)) {
+        K6Maps M;
+        if (k6_maps(M, g, p, nullptr, kap)) {
+            switch (g.nz) {
+            case 64: {
+                constexpr int NZV = 64;
+                    const size_t sm = k9_smem_bytes(3, g.nz);
+                    s3_attr(k9_spmv<NZV>, sm);
+                    launch_pdl(k9_spmv<NZV>, k6_grid(k9_spmv<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, q, red.partials, red.counter, sc);
+            } break;
+            case 128: {
+                constexpr int NZV = 128;
+                    const size_t sm = k9_smem_bytes(3, g.nz);
+                    s3_attr(k9_spmv<NZV>, sm);
+                    launch_pdl(k9_spmv<NZV>, k6_grid(k9_spmv<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, q, red.partials, red.counter, sc);
+            } break;
+            default: {
+                constexpr int NZV = 256;
+                    const size_t sm = k9_smem_bytes(3, g.nz);
+                    s3_attr(k9_spmv<NZV>, sm);
+                    launch_pdl(k9_spmv<NZV>, k6_grid(k9_spmv<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, q, red.partials, red.counter, sc);
+            } break;
+            }
+            return;
+        }
+    }
+    if (kernel_gen() == 8 && k6_ok(g, lt)) {
+        K6Maps M;
+        if (k6_maps(M, g, p, nullptr, kap)) {
+            switch (g.nz) {
+            case 64: {
+                constexpr int NZV = 64;
+                    const size_t sm = k8_smem_bytes(3, g.nz);
+                    s3_attr(k8_spmv<NZV>, sm);
+                    launch_pdl(k8_spmv<NZV>, k6_grid(k8_spmv<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, q, red.partials, red.counter, sc);
+            } break;
+            case 128: {
+                constexpr int NZV = 128;
+                    const size_t sm = k8_smem_bytes(3, g.nz);
+                    s3_attr(k8_spmv<NZV>, sm);
+                    launch_pdl(k8_spmv<NZV>, k6_grid(k8_spmv<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, q, red.partials, red.counter, sc);
+            } break;
+            default: {
+                constexpr int NZV = 256;
+                    const size_t sm = k8_smem_bytes(3, g.nz);
+                    s3_attr(k8_spmv<NZV>, sm);
+                    launch_pdl(k8_spmv<NZV>, k6_grid(k8_spmv<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, q, red.partials, red.counter, sc);
+            } break;
+            }
+            return;
+        }
+    }
     if (kernel_gen() == 6 && k6_ok(g, lt)) {
         K6Maps M;
         if (k6_maps(M, g, p, nullptr, kap)) {
-            const size_t sm = k6_smem_bytes(3, g.nz);
-            s3_attr(k6_spmv, sm);
-            launch_pdl(k6_spmv, k6_grid(k6_spmv, sm, g), k6_block(g), sm, s, g, lt, M, q, red.partials, red.counter, sc);
+            switch (g.nz) {
+            case 64: {
+                constexpr int NZV = 64;
+                    const size_t sm = k6_smem_bytes(3, g.nz);
+                    s3_attr(k6_spmv<NZV>, sm);
+                    launch_pdl(k6_spmv<NZV>, k6_grid(k6_spmv<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, q, red.partials, red.counter, sc);
+            } break;
+            case 128: {
+                constexpr int NZV = 128;
+                    const size_t sm = k6_smem_bytes(3, g.nz);
+                    s3_attr(k6_spmv<NZV>, sm);
+                    launch_pdl(k6_spmv<NZV>, k6_grid(k6_spmv<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, q, red.partials, red.counter, sc);
+            } break;
+            default: {
+                constexpr int NZV = 256;
+                    const size_t sm = k6_smem_bytes(3, g.nz);
+                    s3_attr(k6_spmv<NZV>, sm);
+                    launch_pdl(k6_spmv<NZV>, k6_grid(k6_spmv<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, q, red.partials, red.counter, sc);
+            } break;
+            }
             return;
         }
     }
@@ -2911,6 +3348,22 @@ void launch_loop_ctl(cudaStream_t s, PcgScalars* sc, unsigned long long handle) 
     k_loop_ctl<<<1, 1, 0, s>>>(sc, (cudaGraphConditionalHandle)handle);
 }
 void launch_vtail(cudaStream_t s, const TailArgs& a) { k_vtail<<<1, 1024, 0, s>>>(a); }
+int launch_vtail_coop(cudaStream_t s, const TailArgs& a) {
+    static int blocks = 0;
+    if (!blocks) {
+        int dev = 0, sms = 148, per_sm = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vtail_coop, 256, 0);
+        const char* e = getenv("OTM_CTAIL_BPS");          // blocks per SM (tuning)
+        const int want = e ? atoi(e) : 1;
+        blocks = sms * std::max(1, std::min(per_sm, want));
+    }
+    TailArgs arg = a;
+    void* args[] = {(void*)&arg};
+    return cudaLaunchCooperativeKernel((void*)k_vtail_coop, dim3((unsigned)blocks), dim3(256), args, 0, s) ==
+                   cudaSuccess ? 0 : 1;
+}
 void launch_extrap(cudaStream_t s, long long n3, double* T, double* Tprev, double theta) {
     k_extrap<<<nblk(n3, 256), 256, 0, s>>>(n3, T, Tprev, theta);
 }

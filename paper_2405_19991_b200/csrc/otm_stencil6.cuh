@@ -83,10 +83,11 @@ __device__ __forceinline__ void march6(const Geo& g, const LevelTemplate& lt, co
     extern __shared__ __align__(128) float4 k6_smem4[];
     float* smem = reinterpret_cast<float*>(k6_smem4);
     constexpr int NT = Op::NT;
-    const int TY = k6_ty(g.nz);
-    const int ROWS = TY + 2;
-    const int SLOT = k6_slot_floats(NT, g.nz);
-    const int TILE = ROWS * g.nz;
+    constexpr int NZ = Op::NZ;
+    constexpr int TY = 512 / NZ;
+    constexpr int ROWS = TY + 2;
+    constexpr int SLOT = (NT * (TY + 2) + TY + 1) * NZ;
+    constexpr int TILE = ROWS * NZ;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages6 * SLOT);
     const int tid = threadIdx.x + blockDim.x * threadIdx.y;
     const int lane = tid & 31;
@@ -97,10 +98,10 @@ __device__ __forceinline__ void march6(const Geo& g, const LevelTemplate& lt, co
     __syncthreads();
     pdl_wait();                                            // predecessor outputs visible from here
     unsigned phase_bits = 0;                               // bit k: parity of slot k's next completion
-    const unsigned plane_bytes = (unsigned)((NT * ROWS + TY + 1) * g.nz * 4);
+    const unsigned plane_bytes = (unsigned)((NT * ROWS + TY + 1) * NZ * 4);
     const int tz = threadIdx.x * 2;
-    const int zl = tz == 0 ? g.nz - 1 : tz - 1;
-    const int zr = tz + 2 == g.nz ? 0 : tz + 2;
+    const int zl = tz == 0 ? NZ - 1 : tz - 1;
+    const int zr = tz + 2 == NZ ? 0 : tz + 2;
     const int tr = threadIdx.y + 1;
     const float2 s12 = f2((float)lt.s12, (float)lt.s12);
     const int nty = g.ny / TY;
@@ -129,17 +130,17 @@ __device__ __forceinline__ void march6(const Geo& g, const LevelTemplate& lt, co
                 float* T = S + a * TILE;
                 const int mi = a < 3 ? 0 : 1;
                 const int xc = a < 3 ? a * g.nx + x : x;
-                tma_load_3d(T + g.nz, &maps.main[mi], 0, y0, xc, bars + k);
+                tma_load_3d(T + NZ, &maps.main[mi], 0, y0, xc, bars + k);
                 tma_load_3d(T, &maps.halo[mi], 0, ym, xc, bars + k);
-                tma_load_3d(T + (TY + 1) * g.nz, &maps.halo[mi], 0, yp, xc, bars + k);
+                tma_load_3d(T + (TY + 1) * NZ, &maps.halo[mi], 0, yp, xc, bars + k);
             }
             float* K = S + NT * TILE;
-            tma_load_3d(K + g.nz, &maps.main[2], 0, y0, x, bars + k);
+            tma_load_3d(K + NZ, &maps.main[2], 0, y0, x, bars + k);
             tma_load_3d(K, &maps.halo[2], 0, ym, x, bars + k);
         };
         if (tid == 0)
             for (int s = 0; s < kAhead6 && s < nplanes; ++s) issue(s);
-        const long long vrow = (long long)(y0 + threadIdx.y) * g.nz + tz;
+        const long long vrow = (long long)(y0 + threadIdx.y) * NZ + tz;
         op.prefetch(x0, vrow);
         for (int s = 0; s < nplanes; ++s) {
             const int k = (seq + s) % kStages6;
@@ -159,7 +160,7 @@ __device__ __forceinline__ void march6(const Geo& g, const LevelTemplate& lt, co
                 const float* kb = S0 + NT * TILE;
 #pragma unroll
                 for (int jj = 0; jj < 2; ++jj) {
-                    const int o = (tr - 1 + jj) * g.nz;
+                    const int o = (tr - 1 + jj) * NZ;
                     Ka[jj][0] = ka[o + zl];
                     const float2 va = *reinterpret_cast<const float2*>(ka + o + tz);
                     Ka[jj][1] = va.x; Ka[jj][2] = va.y;
