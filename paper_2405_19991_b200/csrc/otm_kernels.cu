@@ -1120,6 +1120,42 @@ __global__ void __launch_bounds__(256) k_restrict3(Geo f, Geo c, const float* __
     restrict3_body<false>(f, c, res, fc, i);
 }
 
+// Restriction for coarse levels with c.nz % 32 == 0: a warp covers 32 consecutive
+// coarse z, so each fine row (2Z, 2Z+1) is one coalesced float2 load per lane and
+// the 2Z-1 neighbour comes from the lane below by a shuffle (lane 0 loads it).
+// Same weights and summation order as k_restrict3.
+__global__ void __launch_bounds__(256) k_restrict3w(Geo f, Geo c, const float* __restrict__ res,
+                                                    float* __restrict__ fc) {
+    pdl_wait();
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 3 * c.n) return;                      // c.n % 32 == 0: whole warps only
+    const int lane = threadIdx.x & 31;
+    const int cc = (int)(i / c.n);
+    const int v = (int)(i - (long long)cc * c.n);
+    const int X = v / c.pl, rem = v - X * c.pl, Y = rem / c.nz, Z = rem - Y * c.nz;
+    const int xs[3] = {wrap_m(2 * X, f.nx), 2 * X, wrap_p(2 * X, f.nx)};
+    const int ys[3] = {wrap_m(2 * Y, f.ny) * f.nz, 2 * Y * f.nz, wrap_p(2 * Y, f.ny) * f.nz};
+    const int zm = wrap_m(2 * Z, f.nz);
+    const float w[3] = {0.25f, 0.5f, 0.25f};
+    const float* r = res + (size_t)cc * f.n;
+    float s = 0.f;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        float sb = 0.f;
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            const float* row = r + (long long)xs[a] * f.pl + ys[b];
+            const float2 m = __ldg(reinterpret_cast<const float2*>(row + 2 * Z));
+            float left = __shfl_up_sync(0xffffffffu, m.y, 1);
+            if (lane == 0) left = __ldg(row + zm);
+            const float sz = w[0] * left + w[1] * m.x + w[2] * m.y;
+            sb += w[b] * sz;
+        }
+        s += w[a] * sb;
+    }
+    fc[i] = s;
+}
+
 // trilinear prolongation + correction, every axis coarsened: 8 coarse loads, weights 0/0.5/1
 __global__ void __launch_bounds__(256) k_prolong3(Geo f, Geo c, const float* __restrict__ zc,
                                                   float* __restrict__ zf) {
@@ -2452,6 +2488,17 @@ static bool k6_maps(K6Maps& M, const Geo& g, const float* arr3, const float* d1,
     else { M.main[1] = M.main[2]; M.halo[1] = M.halo[2]; }
     return ok;
 }
+static bool encode_map64(CUtensorMap* m, const double* base, int nz, int ny, long long planes, int box_rows) {
+    PFN_encodeTiled_t fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)nz, (cuuint64_t)ny, (cuuint64_t)planes};
+    const cuuint64_t strides[2] = {(cuuint64_t)nz * 8, (cuuint64_t)nz * ny * 8};
+    const cuuint32_t box[3] = {(cuuint32_t)nz, (cuuint32_t)box_rows, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)base, dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 template <class K>
 static dim3 k7_grid(K kernel, size_t smem, const Geo& g) {
     int dev = 0, sms = 148, per_sm = 1;
@@ -2826,6 +2873,37 @@ void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const d
         const long long th = 3 * (g.n >> 1);
         k_res64b<<<nblk(th, 256), 256, 0, s>>>(g, lt, kap, T, fext, fmean, r32, red.partials, red.counter, out9);
         return;
+    }
+    static const bool old64 = getenv("OTM_RES64_OLD") != nullptr;
+    if (!fext && !old64 && k6_ok(g, lt)) {
+        const int tyd = 256 / g.nz;
+        R64Maps M;
+        if (encode_map64(&M.Tm, T, g.nz, g.ny, 3LL * g.nx, tyd) && encode_map64(&M.Th, T, g.nz, g.ny, 3LL * g.nx, 1) &&
+            encode_map64(&M.Km, kap, g.nz, g.ny, g.nx, tyd) && encode_map64(&M.Kh, kap, g.nz, g.ny, g.nx, 1)) {
+            const size_t sm = r64_smem_bytes(g.nz);
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            const long long units = 3LL * (g.ny / tyd) * g.nx;
+            static const int bps = getenv("OTM_R64_BPS") ? atoi(getenv("OTM_R64_BPS")) : 2;
+            const unsigned blocks = (unsigned)std::min<long long>((long long)sms * bps, units);
+            const dim3 blk((unsigned)g.nz, (unsigned)tyd);
+            switch (g.nz) {
+            case 64:
+                s3_attr(k_res64w<64>, sm);
+                k_res64w<64><<<blocks, blk, sm, s>>>(g, lt, M, fmean, r32, red.partials, red.counter, out9);
+                break;
+            case 128:
+                s3_attr(k_res64w<128>, sm);
+                k_res64w<128><<<blocks, blk, sm, s>>>(g, lt, M, fmean, r32, red.partials, red.counter, out9);
+                break;
+            default:
+                s3_attr(k_res64w<256>, sm);
+                k_res64w<256><<<blocks, blk, sm, s>>>(g, lt, M, fmean, r32, red.partials, red.counter, out9);
+                break;
+            }
+            return;
+        }
     }
     if (fast_tiling(g, lt)) {
         int nch;
@@ -3332,7 +3410,10 @@ void launch_upd(cudaStream_t s, long long n, float* d, float* r, const float* p,
 }
 void launch_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* res, float* fc) {
     if (cf[0] && cf[1] && cf[2]) {
-        launch_pdl(k_restrict3, nblk(3 * c.n, 256), 256, 0, s, f, c, res, fc);
+        if (c.nz % 32 == 0 && !getenv("OTM_OLD_RESTRICT"))
+            launch_pdl(k_restrict3w, nblk(3 * c.n, 256), 256, 0, s, f, c, res, fc);
+        else
+            launch_pdl(k_restrict3, nblk(3 * c.n, 256), 256, 0, s, f, c, res, fc);
         return;
     }
     k_restrict<<<nblk(c.n, 256), 256, 0, s>>>(f, c, cf[0], cf[1], cf[2], res, fc);
