@@ -244,6 +244,7 @@ void prof_record(otm_ctx* ctx, int cls, double bytes, bool begin, int& slot_idx)
 // Stream work of one inner PCG iteration (captured into a graph).
 int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false) {
     cudaStream_t s = ctx->stream;
+    set_k8_work(ctx->red.counter + 4);
     const int nl = (int)ctx->L.size();
     const float om = (float)ctx->P.jacobi_omega;
     const double n0 = (double)ctx->g0.n;
@@ -577,8 +578,8 @@ int otm_create(otm_ctx** out, int nx, int ny, int nz, const otm_params* pin) {
     CK(dalloc(ctx, &ctx->gj, 2 * (size_t)ctx->nc * ctx->nc + ctx->nc + 2));
     const size_t mb = max_blocks(ctx);
     CK(dalloc(ctx, &ctx->red.partials, mb * 32 * 2 + mb));     // k_oc_coop: 2 x partials + flags
-    CK(dalloc(ctx, &ctx->red.counter, 4));
-    CK(cudaMemset(ctx->red.counter, 0, 4 * sizeof(unsigned)));
+    CK(dalloc(ctx, &ctx->red.counter, 8));
+    CK(cudaMemset(ctx->red.counter, 0, 8 * sizeof(unsigned)));
     CK(dalloc(ctx, &ctx->sc, 1));
     CK(cudaMemset(ctx->sc, 0, sizeof(PcgScalars)));
     CK(dalloc(ctx, &ctx->scal, 128));
@@ -596,6 +597,7 @@ int otm_create(otm_ctx** out, int nx, int ny, int nz, const otm_params* pin) {
 
 int otm_destroy(otm_ctx* ctx) {
     if (!ctx) return OTM_OK;
+    set_k8_work(nullptr);                 // re-set by the next enqueue of any context
     if (getenv("OTM_STATS") && ctx->stat_solves)
         fprintf(stderr, "[otm] stats: solves %lld outer %lld inner %lld (%.2f inner/solve); oc %lld passes %lld "
                 "(%.2f/update) retried %lld\n", ctx->stat_solves, ctx->stat_outer, ctx->stat_inner,

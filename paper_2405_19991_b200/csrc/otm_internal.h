@@ -110,6 +110,7 @@ struct TailArgs {
 int stencil_chunks(const Geo& g, int* xb);
 void launch_vtail(cudaStream_t s, const TailArgs& a);
 int launch_vtail_coop(cudaStream_t s, const TailArgs& a);   // 0 on success
+void set_k8_work(unsigned* p);   // work counter (2 unsigned, zeroed) used by the k8 kernels enqueued next
 
 void launch_filter(cudaStream_t s, const Geo& g, const FilterSetup& fs, int adjoint, const double* in,
                    double* out, Red& red);

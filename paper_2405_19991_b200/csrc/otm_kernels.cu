@@ -2123,18 +2123,19 @@ __global__ void __launch_bounds__(256, 2) k4_spmv(Geo g, LevelTemplate lt, const
 }
 
 // ---- k6: TMA-staged (otm_stencil6.cuh) ----
-template <int NZv>
+template <int NZv, int TYv = 512 / NZv>
 struct Op6Base {                  // compile-time tile geometry: every shared-memory offset is an immediate
     static constexpr int NZ = NZv;
+    static constexpr int TY = TYv;
     static constexpr int nz = NZv;
-    static constexpr int tile = (512 / NZv + 2) * NZv;
+    static constexpr int tile = (TYv + 2) * NZv;
     __device__ __forceinline__ const float* at(const float* S, int a, int r, int z) const {
         return S + a * tile + r * nz + z;
     }
 };
-template <int NZv>
-struct Op6SmoothRes : Op6Base<NZv> {   // tiles 0..2 = f cases, 3 = D^-1; operand w D^-1 f
-    using Op6Base<NZv>::at;
+template <int NZv, int TYv = 512 / NZv>
+struct Op6SmoothRes : Op6Base<NZv, TYv> {   // tiles 0..2 = f cases, 3 = D^-1; operand w D^-1 f
+    using Op6Base<NZv, TYv>::at;
     static constexpr int NT = 4;
     float omega; float* zo; float* res; long long n;
     __device__ __forceinline__ float op1(const float* S, int c, int r, int z) const {
@@ -2152,9 +2153,9 @@ struct Op6SmoothRes : Op6Base<NZv> {   // tiles 0..2 = f cases, 3 = D^-1; operan
         *reinterpret_cast<float2*>(res + c * n + v) = make_float2(f.x - kz.x, f.y - kz.y);
     }
 };
-template <bool DOT, int NZv>
-struct Op6Jacobi : Op6Base<NZv> {      // tiles 0..2 = z cases; f, D^-1 prefetched
-    using Op6Base<NZv>::at;
+template <bool DOT, int NZv, int TYv = 512 / NZv>
+struct Op6Jacobi : Op6Base<NZv, TYv> {      // tiles 0..2 = z cases; f, D^-1 prefetched
+    using Op6Base<NZv, TYv>::at;
     static constexpr int NT = 3;
     const float* f; const float* dinv; float omega; float* zout; long long n; long long pl;
     float2 fp[3], dp;
@@ -2176,9 +2177,9 @@ struct Op6Jacobi : Op6Base<NZv> {      // tiles 0..2 = z cases; f, D^-1 prefetch
         if (DOT) acc[c] += (double)fp[c].x * (double)z0 + (double)fp[c].y * (double)z1;
     }
 };
-template <int NZv>
-struct Op6Spmv : Op6Base<NZv> {        // tiles 0..2 = p cases
-    using Op6Base<NZv>::at;
+template <int NZv, int TYv = 512 / NZv>
+struct Op6Spmv : Op6Base<NZv, TYv> {        // tiles 0..2 = p cases
+    using Op6Base<NZv, TYv>::at;
     static constexpr int NT = 3;
     float* q; long long n; double acc[3];
     __device__ __forceinline__ float op1(const float* S, int c, int r, int z) const { return *at(S, c, r, z); }
@@ -2239,22 +2240,23 @@ __global__ void __launch_bounds__(256, 2) k6_spmv(Geo g, LevelTemplate lt, const
 }
 
 // ---- k8: k6 staging + x register window for the three cases (march8) ----
-template <int NZ>
-__global__ void __launch_bounds__(256, 1) k8_smooth_res(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
-                                                        float omega, float* z, float* res) {
-    Op6SmoothRes<NZ> op;
+template <int NZ, int TY>
+__global__ void __launch_bounds__(NZ / 2 * TY, 256 / (NZ / 2 * TY)) k8_smooth_res(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
+                                                        float omega, float* z, float* res, unsigned* work) {
+    Op6SmoothRes<NZ, TY> op;
     op.omega = omega; op.zo = z; op.res = res; op.n = g.n;
-    march8(g, lt, maps, op);
+    march8(g, lt, maps, op, work);
 }
 
-template <bool DOT, int NZ>
-__global__ void __launch_bounds__(256, 1) k8_jacobi(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
+template <bool DOT, int NZ, int TY>
+__global__ void __launch_bounds__(NZ / 2 * TY, 256 / (NZ / 2 * TY)) k8_jacobi(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
                                                     const float* f, const float* dinv, float omega, float* zout,
-                                                    double* partials, unsigned* counter, PcgScalars* sc) {
-    Op6Jacobi<DOT, NZ> op;
+                                                    double* partials, unsigned* counter, PcgScalars* sc,
+                                                    unsigned* work) {
+    Op6Jacobi<DOT, NZ, TY> op;
     op.f = f; op.dinv = dinv; op.omega = omega; op.zout = zout; op.n = g.n; op.pl = g.pl;
     op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
-    march8(g, lt, maps, op);
+    march8(g, lt, maps, op, work);
     if (DOT) {
         double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
         if (reduce_finalize<3>(v3, partials, counter, sc->red)) {
@@ -2268,13 +2270,14 @@ __global__ void __launch_bounds__(256, 1) k8_jacobi(Geo g, LevelTemplate lt, con
     }
 }
 
-template <int NZ>
-__global__ void __launch_bounds__(256, 1) k8_spmv(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
-                                                  float* q, double* partials, unsigned* counter, PcgScalars* sc) {
-    Op6Spmv<NZ> op;
+template <int NZ, int TY>
+__global__ void __launch_bounds__(NZ / 2 * TY, 256 / (NZ / 2 * TY)) k8_spmv(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
+                                                  float* q, double* partials, unsigned* counter, PcgScalars* sc,
+                                                    unsigned* work) {
+    Op6Spmv<NZ, TY> op;
     op.q = q; op.n = g.n;
     op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
-    march8(g, lt, maps, op);
+    march8(g, lt, maps, op, work);
     double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
     if (reduce_finalize<3>(v3, partials, counter, sc->red + 3)) {
         for (int cc = 0; cc < 3; ++cc) {
@@ -2480,8 +2483,8 @@ static bool encode_map(CUtensorMap* m, const float* base, int nz, int ny, long l
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 // arr3: 3-case array (3 nx planes), d1: optional D^-1 (nx planes), kap: factors
-static bool k6_maps(K6Maps& M, const Geo& g, const float* arr3, const float* d1, const float* kap) {
-    const int TY = k6_ty(g.nz);
+static bool k6_maps(K6Maps& M, const Geo& g, const float* arr3, const float* d1, const float* kap, int TY = 0) {
+    if (TY == 0) TY = k6_ty(g.nz);
     bool ok = encode_map(&M.main[0], arr3, g.nz, g.ny, 3LL * g.nx, TY) && encode_map(&M.halo[0], arr3, g.nz, g.ny, 3LL * g.nx, 1) &&
               encode_map(&M.main[2], kap, g.nz, g.ny, g.nx, TY) && encode_map(&M.halo[2], kap, g.nz, g.ny, g.nx, 1);
     if (d1) ok = ok && encode_map(&M.main[1], d1, g.nz, g.ny, g.nx, TY) && encode_map(&M.halo[1], d1, g.nz, g.ny, g.nx, 1);
@@ -2512,13 +2515,14 @@ static dim3 k7_grid(K kernel, size_t smem, const Geo& g) {
     return dim3((unsigned)b, 1, 1);
 }
 template <class K>
-static dim3 k6_grid(K kernel, size_t smem, const Geo& g) {
+static dim3 k6_grid(K kernel, size_t smem, const Geo& g, int TY = 0) {
     int dev = 0, sms = 148, per_sm = 1;
+    if (TY == 0) TY = k6_ty(g.nz);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, g.nz / 2 * TY, smem);
     if (per_sm < 1) per_sm = 1;
-    const long long units = (long long)(g.ny / k6_ty(g.nz)) * g.nx;
+    const long long units = (long long)(g.ny / TY) * g.nx;
     long long b = (long long)per_sm * sms;
     if (b > units) b = units;
     return dim3((unsigned)b, 1, 1);
@@ -2938,6 +2942,55 @@ void launch_sum3(cudaStream_t s, long long n, const double* f, Red& red, double*
 }
 static inline bool small_level(const Geo& g) { return g.n <= 65536; }
 
+
+// dynamic-chunk counter of the k8 kernels of the context being enqueued (two
+// zero-initialised unsigned; nullptr or OTM_K8_DYN=0: static split)
+static unsigned* g_k8_work = nullptr;
+void set_k8_work(unsigned* p) { g_k8_work = p; }
+static unsigned* k8_work() {
+    static const bool off = !(getenv("OTM_K8_DYN") && atoi(getenv("OTM_K8_DYN")) == 1);   // measured slower: opt-in
+    return off ? nullptr : g_k8_work;
+}
+// k8 launch helpers: TY = rows per tile; 512/nz (256 threads, 1 CTA/SM) or, with
+// OTM_K8_TY=256, 256/nz (128 threads, 2 CTAs/SM)
+static int k8_tyn() {
+    static const int v = getenv("OTM_K8_TY") ? atoi(getenv("OTM_K8_TY")) : 512;
+    return v == 256 ? 256 : 512;
+}
+template <int NZ, int TY>
+static void l8_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const K6Maps& M, float omega,
+                          float* z, float* res) {
+    const size_t sm = k8_smem_bytes(4, NZ, TY);
+    s3_attr(k8_smooth_res<NZ, TY>, sm);
+    launch_pdl(k8_smooth_res<NZ, TY>, k6_grid(k8_smooth_res<NZ, TY>, sm, g, TY), dim3(NZ / 2, TY), sm, s, g, lt, M,
+               omega, z, res, k8_work());
+}
+template <bool DOT, int NZ, int TY>
+static void l8_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const K6Maps& M, const float* f,
+                      const float* dinv, float omega, float* zout, double* partials, unsigned* counter,
+                      PcgScalars* sc) {
+    const size_t sm = k8_smem_bytes(3, NZ, TY);
+    s3_attr(k8_jacobi<DOT, NZ, TY>, sm);
+    launch_pdl(k8_jacobi<DOT, NZ, TY>, k6_grid(k8_jacobi<DOT, NZ, TY>, sm, g, TY), dim3(NZ / 2, TY), sm, s, g, lt,
+               M, f, dinv, omega, zout, partials, counter, sc, k8_work());
+}
+template <int NZ, int TY>
+static void l8_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const K6Maps& M, float* q, Red& red,
+                    PcgScalars* sc) {
+    const size_t sm = k8_smem_bytes(3, NZ, TY);
+    s3_attr(k8_spmv<NZ, TY>, sm);
+    launch_pdl(k8_spmv<NZ, TY>, k6_grid(k8_spmv<NZ, TY>, sm, g, TY), dim3(NZ / 2, TY), sm, s, g, lt, M, q,
+               red.partials, red.counter, sc, k8_work());
+}
+#define OTM_K8_SWITCH(CALL)                                             \
+    do {                                                                \
+        const bool half = k8_tyn() == 256;                              \
+        switch (g.nz) {                                                 \
+        case 64: if (half) CALL(64, 4); else CALL(64, 8); break;        \
+        case 128: if (half) CALL(128, 2); else CALL(128, 4); break;     \
+        default: if (half) CALL(256, 1); else CALL(256, 2); break;      \
+        }                                                               \
+    } while (0)
 void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* f,
                        const float* dinv, float omega, float* z, float* res) {
     if (kernel_gen() == 7 && k6_ok(g, lt)) {
@@ -2977,27 +3030,10 @@ void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, co
     }
     if (kernel_gen() == 8 && k6_ok(g, lt)) {
         K6Maps M;
-        if (k6_maps(M, g, f, dinv, kap)) {
-            switch (g.nz) {
-            case 64: {
-                constexpr int NZV = 64;
-                    const size_t sm = k8_smem_bytes(4, g.nz);
-                    s3_attr(k8_smooth_res<NZV>, sm);
-                    launch_pdl(k8_smooth_res<NZV>, k6_grid(k8_smooth_res<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, omega, z, res);
-            } break;
-            case 128: {
-                constexpr int NZV = 128;
-                    const size_t sm = k8_smem_bytes(4, g.nz);
-                    s3_attr(k8_smooth_res<NZV>, sm);
-                    launch_pdl(k8_smooth_res<NZV>, k6_grid(k8_smooth_res<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, omega, z, res);
-            } break;
-            default: {
-                constexpr int NZV = 256;
-                    const size_t sm = k8_smem_bytes(4, g.nz);
-                    s3_attr(k8_smooth_res<NZV>, sm);
-                    launch_pdl(k8_smooth_res<NZV>, k6_grid(k8_smooth_res<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, omega, z, res);
-            } break;
-            }
+        if (k6_maps(M, g, f, dinv, kap, k8_tyn() / g.nz)) {
+#define C_(NZ, TY) l8_smooth_res<NZ, TY>(s, g, lt, M, omega, z, res)
+            OTM_K8_SWITCH(C_);
+#undef C_
             return;
         }
     }
@@ -3130,47 +3166,15 @@ void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const 
     }
     if (kernel_gen() == 8 && k6_ok(g, lt)) {
         K6Maps M;
-        if (k6_maps(M, g, z, nullptr, kap)) {
-            switch (g.nz) {
-            case 64: {
-                constexpr int NZV = 64;
-                    const size_t sm = k8_smem_bytes(3, g.nz);
-                    if (dot) {
-                        s3_attr(k8_jacobi<true, NZV>, sm);
-                        launch_pdl(k8_jacobi<true, NZV>, k6_grid(k8_jacobi<true, NZV>, sm, g), k6_block(g), sm, s,
-                            g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
-                    } else {
-                        s3_attr(k8_jacobi<false, NZV>, sm);
-                        launch_pdl(k8_jacobi<false, NZV>, k6_grid(k8_jacobi<false, NZV>, sm, g), k6_block(g), sm, s,
-                            g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
-                    }
-            } break;
-            case 128: {
-                constexpr int NZV = 128;
-                    const size_t sm = k8_smem_bytes(3, g.nz);
-                    if (dot) {
-                        s3_attr(k8_jacobi<true, NZV>, sm);
-                        launch_pdl(k8_jacobi<true, NZV>, k6_grid(k8_jacobi<true, NZV>, sm, g), k6_block(g), sm, s,
-                            g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
-                    } else {
-                        s3_attr(k8_jacobi<false, NZV>, sm);
-                        launch_pdl(k8_jacobi<false, NZV>, k6_grid(k8_jacobi<false, NZV>, sm, g), k6_block(g), sm, s,
-                            g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
-                    }
-            } break;
-            default: {
-                constexpr int NZV = 256;
-                    const size_t sm = k8_smem_bytes(3, g.nz);
-                    if (dot) {
-                        s3_attr(k8_jacobi<true, NZV>, sm);
-                        launch_pdl(k8_jacobi<true, NZV>, k6_grid(k8_jacobi<true, NZV>, sm, g), k6_block(g), sm, s,
-                            g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
-                    } else {
-                        s3_attr(k8_jacobi<false, NZV>, sm);
-                        launch_pdl(k8_jacobi<false, NZV>, k6_grid(k8_jacobi<false, NZV>, sm, g), k6_block(g), sm, s,
-                            g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
-                    }
-            } break;
+        if (k6_maps(M, g, z, nullptr, kap, k8_tyn() / g.nz)) {
+            if (dot) {
+#define C_(NZ, TY) l8_jacobi<true, NZ, TY>(s, g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc)
+                OTM_K8_SWITCH(C_);
+#undef C_
+            } else {
+#define C_(NZ, TY) l8_jacobi<false, NZ, TY>(s, g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc)
+                OTM_K8_SWITCH(C_);
+#undef C_
             }
             return;
         }
@@ -3318,27 +3322,10 @@ void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const fl
     }
     if (kernel_gen() == 8 && k6_ok(g, lt)) {
         K6Maps M;
-        if (k6_maps(M, g, p, nullptr, kap)) {
-            switch (g.nz) {
-            case 64: {
-                constexpr int NZV = 64;
-                    const size_t sm = k8_smem_bytes(3, g.nz);
-                    s3_attr(k8_spmv<NZV>, sm);
-                    launch_pdl(k8_spmv<NZV>, k6_grid(k8_spmv<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, q, red.partials, red.counter, sc);
-            } break;
-            case 128: {
-                constexpr int NZV = 128;
-                    const size_t sm = k8_smem_bytes(3, g.nz);
-                    s3_attr(k8_spmv<NZV>, sm);
-                    launch_pdl(k8_spmv<NZV>, k6_grid(k8_spmv<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, q, red.partials, red.counter, sc);
-            } break;
-            default: {
-                constexpr int NZV = 256;
-                    const size_t sm = k8_smem_bytes(3, g.nz);
-                    s3_attr(k8_spmv<NZV>, sm);
-                    launch_pdl(k8_spmv<NZV>, k6_grid(k8_spmv<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, q, red.partials, red.counter, sc);
-            } break;
-            }
+        if (k6_maps(M, g, p, nullptr, kap, k8_tyn() / g.nz)) {
+#define C_(NZ, TY) l8_spmv<NZ, TY>(s, g, lt, M, q, red, sc)
+            OTM_K8_SWITCH(C_);
+#undef C_
             return;
         }
     }

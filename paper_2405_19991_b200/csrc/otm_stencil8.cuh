@@ -14,11 +14,13 @@
 namespace otm {
 
 constexpr int kStages8 = 9;
+constexpr int kChunk8 = 16;         // planes per dynamically scheduled chunk
 constexpr int kAhead8 = 7;          // kStages8 >= kAhead8 + 2: the slot refilled at step s held plane s-2
 static_assert(kStages8 >= kAhead8 + 2, "k8 ring too shallow");
 
-__host__ __device__ inline size_t k8_smem_bytes(int NT, int nz) {
-    return (size_t)kStages8 * k6_slot_floats(NT, nz) * 4 + kStages8 * 8;
+__host__ __device__ inline size_t k8_smem_bytes(int NT, int nz, int ty = 0) {
+    if (ty == 0) ty = 512 / nz;
+    return (size_t)kStages8 * ((NT * (ty + 2) + ty + 1) * nz) * 4 + kStages8 * 8;
 }
 
 struct K8Row {
@@ -91,12 +93,13 @@ __device__ __forceinline__ void k8_out(Op& op, const W21& w, const K8Row (&P)[3]
 }
 
 template <class Op>
-__device__ __forceinline__ void march8(const Geo& g, const LevelTemplate& lt, const K6Maps& maps, Op& op) {
+__device__ __forceinline__ void march8(const Geo& g, const LevelTemplate& lt, const K6Maps& maps, Op& op,
+                                       unsigned* work = nullptr) {
     extern __shared__ __align__(128) float4 k8_smem4[];
     float* smem = reinterpret_cast<float*>(k8_smem4);
     constexpr int NT = Op::NT;
     constexpr int NZ = Op::NZ;
-    constexpr int TY = 512 / NZ;
+    constexpr int TY = Op::TY;
     constexpr int ROWS = TY + 2;
     constexpr int SLOT = (NT * (TY + 2) + TY + 1) * NZ;
     constexpr int TILE = ROWS * NZ;
@@ -121,10 +124,28 @@ __device__ __forceinline__ void march8(const Geo& g, const LevelTemplate& lt, co
     long long u = W * blockIdx.x / B;
     const long long u1 = W * (blockIdx.x + 1) / B;
     int seq = 0;                                           // ring position of the segment's plane 0
-    while (u < u1) {
-        const int yt = (int)(u / g.nx);
-        const int x0 = (int)(u - (long long)yt * g.nx);
-        const int x1 = (int)min((long long)g.nx, x0 + (u1 - u));
+    // work distribution: static contiguous ranges, or (work != nullptr) chunks of
+    // kChunk8 planes of one row tile grabbed from a global counter, which balances
+    // CTAs that stream from the far HBM stacks more slowly
+    const int nct = (g.nx + kChunk8 - 1) / kChunk8;
+    const int nchunks = nty * nct;
+    __shared__ int s_chunk;
+    while (true) {
+        int yt, x0, x1;
+        if (work) {
+            if (tid == 0) s_chunk = (int)atomicAdd(work, 1u);
+            __syncthreads();
+            const int ch = s_chunk;
+            if (ch >= nchunks) break;
+            yt = ch / nct;
+            x0 = (ch - yt * nct) * kChunk8;
+            x1 = min(g.nx, x0 + kChunk8);
+        } else {
+            if (u >= u1) break;
+            yt = (int)(u / g.nx);
+            x0 = (int)(u - (long long)yt * g.nx);
+            x1 = (int)min((long long)g.nx, x0 + (u1 - u));
+        }
         const int y0 = yt * TY;
         const int ym = y0 == 0 ? g.ny - 1 : y0 - 1;
         const int yp = y0 + TY == g.ny ? 0 : y0 + TY;
@@ -196,6 +217,13 @@ __device__ __forceinline__ void march8(const Geo& g, const LevelTemplate& lt, co
         seq = (seq + nplanes) % kStages8;
         __syncthreads();
         u += x1 - x0;
+    }
+    if (work && tid == 0) {                                // last CTA out resets the counter
+        __threadfence();
+        if (atomicAdd(work + 1, 1u) == gridDim.x - 1) {
+            atomicExch(work, 0u);
+            atomicExch(work + 1, 0u);
+        }
     }
 }
 
