@@ -141,6 +141,10 @@ int otm_symmetrize(otm_ctx* ctx, double* a_dev);
 int otm_build(otm_ctx* ctx, const double* rho_filtered_dev);
 /* GridHierarchy.build with explicit element factors (solver.py:269). */
 int otm_build_kappa(otm_ctx* ctx, const double* kappa_dev);
+/* One V-cycle of the built hierarchy (the MG preconditioner, solver.py:206-215, with
+ * the damped-Jacobi smoother) on 3 fp32 fields: z3 = V(f3), both 3*n floats on the
+ * device.  Used by the slab solver for the agglomerated coarse levels. */
+int otm_vcycle(otm_ctx* ctx, const float* f3_dev, float* z3_dev);
 /* apply_K on level 0 in fp64 (solver.py:111-119). */
 int otm_apply_K(otm_ctx* ctx, const double* T_dev, double* out_dev);
 /* assemble_macro_load (solver.py:347-363) for case 0..2. */

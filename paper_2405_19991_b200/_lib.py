@@ -97,6 +97,28 @@ _SIGS = {
                                    C.POINTER(C.c_double)]),
     "otm_profile_reset": (C.c_int, [C.c_void_p]),
     "otm_launch_count": (C.c_longlong, [C.c_void_p]),
+    "otm_vcycle": (C.c_int, [C.c_void_p, dptr, dptr]),
+    # include/otm_slab.h: slab-decomposed solve pieces (multi-GPU)
+    "otm_slab_create": (C.c_void_p, [C.c_longlong]),
+    "otm_slab_destroy": (C.c_int, [C.c_void_p]),
+    "otm_slab_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "otm_slab_last_error": (C.c_char_p, [C.c_void_p]),
+    "otm_slab_stencil": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double), dptr,
+                                   dptr, dptr, dptr, C.c_double, dptr, dptr, C.POINTER(C.c_double)]),
+    "otm_slab_restrict": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, dptr, dptr]),
+    "otm_slab_prolong": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, dptr, dptr]),
+    "otm_slab_coarsen": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, dptr, dptr]),
+    "otm_slab_dinv": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double), dptr, dptr]),
+    "otm_slab_pupd": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, dptr, dptr, C.POINTER(C.c_double)]),
+    "otm_slab_upd": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, dptr, dptr, dptr, dptr,
+                               C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "otm_slab_load_sums": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double), dptr,
+                                     C.POINTER(C.c_double)]),
+    "otm_slab_res64": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double), dptr, dptr,
+                                 C.POINTER(C.c_double), dptr, C.POINTER(C.c_double)]),
+    "otm_slab_tupd": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, dptr, dptr, C.POINTER(C.c_double)]),
+    "otm_slab_tensor_sums": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double), dptr, dptr,
+                                       C.POINTER(C.c_double)]),
 }
 
 EXPORTED = tuple(_SIGS)

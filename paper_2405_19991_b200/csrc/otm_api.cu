@@ -135,6 +135,8 @@ cudaError_t dalloc(otm_ctx* ctx, T** p, size_t count) {
 
 // trilinear template of a level: K = sum_ax scale_ax * (stiffness (x) mass (x) mass)
 // (solver.py:43-54); depends only on the corner XOR pattern.
+}  // namespace
+
 void level_template(const double scale[3], LevelTemplate& lt) {
     const double st[2] = {1.0, -1.0};
     const double ms[2] = {1.0 / 3.0, 1.0 / 6.0};
@@ -159,6 +161,8 @@ void level_template(const double scale[3], LevelTemplate& lt) {
             lt.f0[a * 3 + i] = s;
         }
 }
+
+namespace {
 
 // cone taps (field.py:60-93)
 int setup_filter(otm_ctx* ctx, double radius) {
@@ -242,7 +246,7 @@ void prof_record(otm_ctx* ctx, int cls, double bytes, bool begin, int& slot_idx)
 }
 
 // Stream work of one inner PCG iteration (captured into a graph).
-int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false) {
+int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false, bool vonly = false) {
     cudaStream_t s = ctx->stream;
     set_k8_work(ctx->red.counter + 4);
     const int nl = (int)ctx->L.size();
@@ -304,18 +308,18 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false) {
         launch_prolong(s, A.g, B.g, B.cf, B.res, A.z);
         const double bj = 44.0 * (double)A.g.n;
         if (prof && l == 0) prof_record(ctx, kProfL0Stencil, bj, true, sl);
-        launch_jacobi(s, A.g, A.lt, A.kap, A.z, A.f, A.dinv, om, A.res, l == 0, ctx->red, ctx->sc);
+        launch_jacobi(s, A.g, A.lt, A.kap, A.z, A.f, A.dinv, om, A.res, l == 0 && !vonly, ctx->red, ctx->sc);
         if (prof && l == 0) prof_record(ctx, kProfL0Stencil, 0, false, sl);
         vbytes += 12.0 * B.g.n + 24.0 * A.g.n + bj;
         launches += 2;
     }
-    if (use_tail && tl == 0) {
+    if (use_tail && tl == 0 && !vonly) {
         // the whole hierarchy fits the tail: r.z and beta still come from a level-0 pass
         LevelBuf& A = ctx->L[0];
         launch_jacobi(s, A.g, A.lt, A.kap, A.res, A.f, A.dinv, 0.0f, A.z, true, ctx->red, ctx->sc);
         launches += 1;
     }
-    if (nl == 1) {
+    if (nl == 1 && !vonly) {
         // single-level hierarchy: the coarse solve is the whole preconditioner; still need r.z
         LevelBuf& A = ctx->L[0];
         launch_jacobi(s, A.g, A.lt, A.kap, A.res, A.f, A.dinv, 0.0f, A.z, true, ctx->red, ctx->sc);
@@ -325,6 +329,7 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false) {
         prof_record(ctx, kProfVcycle, 0, false, sl_v);
         ctx->slots[sl_v].bytes = vbytes;
     }
+    if (vonly) return OTM_OK;                  // V-cycle only: z in L[0].res
     float* z0 = (nl == 1 || (use_tail && tl == 0)) ? ctx->L[0].z : ctx->L[0].res;
     launch_pupd(s, ctx->g0.n, z0, ctx->p, ctx->sc);
     if (prof) prof_record(ctx, kProfL0Stencil, 28.0 * n0, true, sl);
@@ -689,6 +694,18 @@ int otm_build_kappa(otm_ctx* ctx, const double* kap) {
     launch_set_kappa(ctx->stream, ctx->g0.n, kap, ctx->kap64, ctx->L[0].kap);
     ctx->launches++;
     return build_levels(ctx);
+}
+
+int otm_vcycle(otm_ctx* ctx, const float* f3, float* z3) {
+    if (!ctx || !f3 || !z3) return OTM_EINVAL;
+    if (!ctx->built) return fail(ctx, OTM_ESTATE, "hierarchy not built; call build() first");
+    const size_t bytes = 3 * ctx->g0.n * sizeof(float);
+    CK(cudaMemcpyAsync(ctx->L[0].f, f3, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    int rc = enqueue_inner(ctx, false, false, true);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(z3, ctx->L[0].res, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    CKL();
+    return OTM_OK;
 }
 
 int otm_apply_K(otm_ctx* ctx, const double* T, double* out) {

@@ -1,0 +1,554 @@
+// libotm slab kernels: the level-0 .. agglomeration-level pieces of the homogenization
+// solve on an x-slab of the periodic grid.
+//
+// A slab owns nxl consecutive x planes of a level; every field is stored with one
+// ghost plane on each side, (nxl + 2) planes of ny * nz values (3 load cases
+// case-major: case c at c * (nxl + 2) * ny * nz).  Ghost planes are refreshed by
+// the caller (NCCL send/recv between neighbouring ranks) before any kernel that
+// reads them; kernels write interior planes only.  y and z stay periodic inside the
+// slab.  Element factors use the element = lower-corner vertex convention, so a
+// vertex needs the factor ghost on the left only.  Scalars (dot products, norms,
+// tensor sums) are per-slab fixed-order partial sums; the caller all-reduces them.
+#include "otm_common.cuh"
+#include "otm_internal.h"
+#include "../../include/otm.h"
+#include "../../include/otm_slab.h"
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+void level_template(const double scale[3], otm::LevelTemplate& lt);   // otm_api.cu
+
+namespace otm {
+namespace {
+
+struct SGeo {
+    int nxl, ny, nz;
+    int pl;             // ny * nz
+    long long ni;       // interior values per case: nxl * pl
+    long long na;       // allocated values per case: (nxl + 2) * pl
+};
+
+SGeo make_sgeo(int nxl, int ny, int nz) {
+    SGeo g;
+    g.nxl = nxl; g.ny = ny; g.nz = nz;
+    g.pl = ny * nz;
+    g.ni = (long long)nxl * g.pl;
+    g.na = (long long)(nxl + 2) * g.pl;
+    return g;
+}
+
+// interior item i (0 .. ni-1) -> local plane (1 .. nxl), y, z
+__device__ __forceinline__ void s_decode(const SGeo& g, long long i, int& x, int& y, int& z) {
+    x = (int)(i / g.pl);
+    const int rem = (int)(i - (long long)x * g.pl);
+    y = rem / g.nz;
+    z = rem - y * g.nz;
+    x += 1;
+}
+
+// 27 operand values around (x, y, z): x from the ghosted planes, y/z periodic
+template <int OP>
+__device__ __forceinline__ void s_gather(const SGeo& g, const float* __restrict__ a, const float* __restrict__ dinv,
+                                         float omega, int x, int y, int z, float (&t)[3][9]) {
+    const int ys[3] = {wrap_m(y, g.ny) * g.nz, y * g.nz, wrap_p(y, g.ny) * g.nz};
+    const int zs[3] = {wrap_m(z, g.nz), z, wrap_p(z, g.nz)};
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const long long idx = (long long)(x - 1 + p) * g.pl + ys[j] + zs[q];
+                float v = __ldg(a + idx);
+                if (OP == 0) v *= omega * __ldg(dinv + idx);
+                t[p][j * 3 + q] = v;
+            }
+}
+
+// factors of the 8 elements around the vertex: planes x-1, x; rows y-1, y; cols z-1, z
+__device__ __forceinline__ void s_kappa(const SGeo& g, const float* __restrict__ k, int x, int y, int z,
+                                        float (&kk)[2][4]) {
+    const int ys[2] = {wrap_m(y, g.ny) * g.nz, y * g.nz};
+    const int zs[2] = {wrap_m(z, g.nz), z};
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) kk[p][j * 2 + q] = __ldg(k + (long long)(x - 1 + p) * g.pl + ys[j] + zs[q]);
+}
+
+__device__ __forceinline__ float s_apply(const LevelTemplate& lt, const float (&t)[3][9], const float (&k)[2][4]) {
+    if (lt.equal) {
+        const KSum<float> s = ksum<float>(k);
+        return apply_compact<float>(t, k, s, (float)lt.s12);
+    }
+    float ktab[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) ktab[q] = (float)lt.kt[q];
+    return apply_generic<float>(t, k, ktab);
+}
+
+// OP 0 smooth_res: z = w D^-1 f, res = f - K z          (o1 = z, o2 = res)
+// OP 1 jacobi:     zout = z + w D^-1 (f - K z); dot f.zout (o1 = zout)
+// OP 2 spmv:       q = K p; dot p.q                       (o1 = q)
+template <int OP>
+__global__ void __launch_bounds__(256) ks_stencil(SGeo g, LevelTemplate lt, const float* __restrict__ kap,
+                                                  const float* __restrict__ a, const float* __restrict__ f,
+                                                  const float* __restrict__ dinv, float omega, float* __restrict__ o1,
+                                                  float* __restrict__ o2, int dot, double* partials,
+                                                  unsigned* counter, double* out3) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double d3[3] = {0.0, 0.0, 0.0};
+    if (i < 3 * g.ni) {
+        const int c = (int)(i / g.ni);
+        const long long v = i - (long long)c * g.ni;
+        int x, y, z;
+        s_decode(g, v, x, y, z);
+        const long long off = (long long)c * g.na;
+        const long long idx = (long long)x * g.pl + y * g.nz + z;
+        float t[3][9], k[2][4];
+        s_gather<OP>(g, (OP == 0 ? f : a) + off, dinv, omega, x, y, z, t);
+        s_kappa(g, kap, x, y, z, k);
+        const float kt = s_apply(lt, t, k);
+        if (OP == 0) {
+            o1[off + idx] = t[1][4];
+            o2[off + idx] = __ldg(f + off + idx) - kt;
+        } else if (OP == 1) {
+            const float fv = __ldg(f + off + idx);
+            const float zn = t[1][4] + omega * __ldg(dinv + idx) * (fv - kt);
+            o1[off + idx] = zn;
+            d3[c] = (double)fv * (double)zn;
+        } else {
+            o1[off + idx] = kt;
+            d3[c] = (double)t[1][4] * (double)kt;
+        }
+    }
+    if (dot && reduce_finalize<3>(d3, partials, counter, out3)) {}
+}
+
+// full-weighting restriction: coarse interior J <- fine local 2J-2 .. 2J (x), periodic y/z
+__global__ void ks_restrict(SGeo f, SGeo c, const float* __restrict__ res, float* __restrict__ fc) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 3 * c.ni) return;
+    const int cc = (int)(i / c.ni);
+    int X, Y, Z;
+    s_decode(c, i - (long long)cc * c.ni, X, Y, Z);
+    const int xs[3] = {2 * X - 2, 2 * X - 1, 2 * X};
+    const int ys[3] = {wrap_m(2 * Y, f.ny) * f.nz, 2 * Y * f.nz, wrap_p(2 * Y, f.ny) * f.nz};
+    const int zs[3] = {wrap_m(2 * Z, f.nz), 2 * Z, wrap_p(2 * Z, f.nz)};
+    const float w[3] = {0.25f, 0.5f, 0.25f};
+    const float* r = res + (long long)cc * f.na;
+    float s = 0.f;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        float sb = 0.f;
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            const float* row = r + (long long)xs[a] * f.pl + ys[b];
+            const float sz = w[0] * __ldg(row + zs[0]) + w[1] * __ldg(row + zs[1]) + w[2] * __ldg(row + zs[2]);
+            sb += w[b] * sz;
+        }
+        s += w[a] * sb;
+    }
+    fc[(long long)cc * c.na + (long long)X * c.pl + Y * c.nz + Z] = s;
+}
+
+// trilinear prolongation + correction: fine interior i <- coarse local (i+1)/2 (+1 for odd offsets)
+__global__ void ks_prolong(SGeo f, SGeo c, const float* __restrict__ zc, float* __restrict__ zf) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 3 * f.ni) return;
+    const int cc = (int)(i / f.ni);
+    int x, y, z;
+    s_decode(f, i - (long long)cc * f.ni, x, y, z);
+    // fine local x (1..nxl) is global 2*X0 + x - 1: even offsets (x odd) sit on coarse local (x+1)/2
+    const int J0 = (x + 1) >> 1;
+    const int J1 = (x & 1) ? J0 : J0 + 1;
+    const float wx1 = (x & 1) ? 0.f : 0.5f, wx0 = 1.f - wx1;
+    const int Y0 = y >> 1, Z0 = z >> 1;
+    const int Y1 = Y0 + 1 == c.ny ? 0 : Y0 + 1, Z1 = Z0 + 1 == c.nz ? 0 : Z0 + 1;
+    const float wy1 = (y & 1) ? 0.5f : 0.f, wz1 = (z & 1) ? 0.5f : 0.f;
+    const float wy0 = 1.f - wy1, wz0 = 1.f - wz1;
+    const float* a = zc + (long long)cc * c.na;
+    auto at = [&](int X, int Y, int Z) { return __ldg(a + (long long)X * c.pl + Y * c.nz + Z); };
+    const float s = wx0 * (wy0 * (wz0 * at(J0, Y0, Z0) + wz1 * at(J0, Y0, Z1)) +
+                           wy1 * (wz0 * at(J0, Y1, Z0) + wz1 * at(J0, Y1, Z1))) +
+                    wx1 * (wy0 * (wz0 * at(J1, Y0, Z0) + wz1 * at(J1, Y0, Z1)) +
+                           wy1 * (wz0 * at(J1, Y1, Z0) + wz1 * at(J1, Y1, Z1)));
+    zf[(long long)cc * f.na + (long long)x * f.pl + y * f.nz + z] += s;
+}
+
+// child-mean factors: coarse element J <- fine elements 2J-1, 2J (local x), 2x2 in y/z
+__global__ void ks_coarsen(SGeo f, SGeo c, const float* __restrict__ kf, float* __restrict__ kc) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= c.ni) return;
+    int X, Y, Z;
+    s_decode(c, i, X, Y, Z);
+    float s = 0.f;
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b)
+            for (int d = 0; d < 2; ++d) s += kf[(long long)(2 * X - 1 + a) * f.pl + (2 * Y + b) * f.nz + 2 * Z + d];
+    kc[(long long)X * c.pl + Y * c.nz + Z] = s / 8.f;
+}
+
+__global__ void ks_dinv(SGeo g, const float* __restrict__ k, float kdiag, float* __restrict__ dinv) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= g.ni) return;
+    int x, y, z;
+    s_decode(g, i, x, y, z);
+    const int ys[2] = {wrap_m(y, g.ny), y}, zs[2] = {wrap_m(z, g.nz), z};
+    float s = 0.f;
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b)
+            for (int d = 0; d < 2; ++d) s += k[(long long)(x - 1 + a) * g.pl + ys[b] * g.nz + zs[d]];
+    dinv[(long long)x * g.pl + y * g.nz + z] = 1.0f / (kdiag * s);
+}
+
+// p = z + beta p (interior)
+__global__ void ks_pupd(SGeo g, const float* __restrict__ z, float* __restrict__ p, double b0, double b1,
+                        double b2) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 3 * g.ni) return;
+    const int c = (int)(i / g.ni);
+    const long long idx = (long long)c * g.na + g.pl + (i - (long long)c * g.ni);
+    const float b = (float)(c == 0 ? b0 : (c == 1 ? b1 : b2));
+    p[idx] = z[idx] + b * p[idx];
+}
+
+// d += alpha p, r -= alpha q, partial r.r (interior)
+__global__ void __launch_bounds__(256) ks_upd(SGeo g, float* __restrict__ d, float* __restrict__ r,
+                                              const float* __restrict__ p, const float* __restrict__ q, double a0,
+                                              double a1, double a2, double* partials, unsigned* counter,
+                                              double* out3) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double d3[3] = {0.0, 0.0, 0.0};
+    if (i < 3 * g.ni) {
+        const int c = (int)(i / g.ni);
+        const long long idx = (long long)c * g.na + g.pl + (i - (long long)c * g.ni);
+        const float al = (float)(c == 0 ? a0 : (c == 1 ? a1 : a2));
+        d[idx] += al * p[idx];
+        const float rn = r[idx] - al * q[idx];
+        r[idx] = rn;
+        d3[c] = (double)rn * (double)rn;
+    }
+    reduce_finalize<3>(d3, partials, counter, out3);
+}
+
+// fp64 defect r = (f(kappa) - fmean) - K T (solver.py:398-401) and the loads'
+// partial sums: mode 0 -> sums of f per case (for the global mean); mode 1 -> r
+// (fp32, interior) and partial sums r^2, f^2, T per case.
+template <int MODE>
+__global__ void __launch_bounds__(128) ks_res64(SGeo g, LevelTemplate lt, const double* __restrict__ kap,
+                                                const double* __restrict__ T, const double* __restrict__ fmean,
+                                                float* __restrict__ r32, double* partials, unsigned* counter,
+                                                double* out9) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double acc[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc[q] = 0.0;
+    if (i < g.ni) {
+        int x, y, z;
+        s_decode(g, i, x, y, z);
+        const int ys[3] = {wrap_m(y, g.ny) * g.nz, y * g.nz, wrap_p(y, g.ny) * g.nz};
+        const int zs[3] = {wrap_m(z, g.nz), z, wrap_p(z, g.nz)};
+        double k[2][4];
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int q = 0; q < 2; ++q) k[p][j * 2 + q] = __ldg(kap + (long long)(x - 1 + p) * g.pl + ys[j] + zs[q]);
+        const long long idx = (long long)x * g.pl + y * g.nz + z;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            // loads: element (q, jj, kk) has v as corner a = (1-q) | (1-jj)<<1 | (1-kk)<<2 (k2_res64 order)
+            double f = 0.0;
+#pragma unroll
+            for (int a = 0; a < 8; ++a) {
+                const int q = 1 - (a & 1), jj = 1 - ((a >> 1) & 1), kk = 1 - ((a >> 2) & 1);
+                f = __dadd_rn(f, __dmul_rn(lt.f0[a * 3 + c], k[q][jj * 2 + kk]));
+            }
+            if (MODE == 0) {
+                acc[c] += f;
+                continue;
+            }
+            const double* Tc = T + (long long)c * g.na;
+            double t[3][9];
+#pragma unroll
+            for (int p = 0; p < 3; ++p)
+#pragma unroll
+                for (int j = 0; j < 3; ++j)
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) t[p][j * 3 + q] = __ldg(Tc + (long long)(x - 1 + p) * g.pl + ys[j] + zs[q]);
+            double kt;
+            if (lt.equal) {
+                const KSum<double> s = ksum<double>(k);
+                kt = apply_compact<double>(t, k, s, lt.s12);
+            } else {
+                kt = apply_generic<double>(t, k, lt.kt);
+            }
+            const double r = (f - fmean[c]) - kt;
+            r32[(long long)c * g.na + idx] = (float)r;
+            acc[c] += r * r;
+            acc[3 + c] += f * f;
+            acc[6 + c] += t[1][4];
+        }
+    }
+    reduce_finalize<9>(acc, partials, counter, out9);
+}
+
+// T += d (interior), optional subtraction of per-case means
+__global__ void ks_tupd(SGeo g, double* __restrict__ T, const float* __restrict__ d, double m0, double m1,
+                        double m2, int with_d) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 3 * g.ni) return;
+    const int c = (int)(i / g.ni);
+    const long long idx = (long long)c * g.na + g.pl + (i - (long long)c * g.ni);
+    const double m = c == 0 ? m0 : (c == 1 ? m1 : m2);
+    T[idx] = (T[idx] + (with_d ? (double)d[idx] : 0.0)) - m;
+}
+
+// partial sums kappa_e * E_c[e] (homogenize.py:103-122), element e = vertex e, corners e + c_a
+__global__ void __launch_bounds__(256) ks_tensor(SGeo g, const double* __restrict__ T, const double* __restrict__ kap,
+                                                 const double* __restrict__ kt, double* partials, unsigned* counter,
+                                                 double* out6) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    if (i < g.ni) {
+        int x, y, z;
+        s_decode(g, i, x, y, z);
+        const int ys[2] = {y, wrap_p(y, g.ny)}, zs[2] = {z, wrap_p(z, g.nz)};
+        // chi_i = e_i - T_i at the 8 corners (homogenize.py:103-110): corner a at (x + a&1, y + a>>1&1, z + a>>2&1)
+        double chi[3][8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const long long idx = (long long)(x + (a & 1)) * g.pl + ys[(a >> 1) & 1] * g.nz + zs[(a >> 2) & 1];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) chi[c][a] = (double)((a >> c) & 1) - __ldg(T + (long long)c * g.na + idx);
+        }
+        const double ke = __ldg(kap + (long long)x * g.pl + y * g.nz + z);
+        const int pr[6][2] = {{0, 0}, {1, 1}, {2, 2}, {0, 1}, {1, 2}, {0, 2}};
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            double e = 0.0;
+#pragma unroll
+            for (int a = 0; a < 8; ++a) {
+                double ka = 0.0;
+#pragma unroll
+                for (int b = 0; b < 8; ++b) ka += kt[a ^ b] * chi[pr[q][1]][b];
+                e += chi[pr[q][0]][a] * ka;
+            }
+            acc[q] = ke * e;
+        }
+    }
+    reduce_finalize<6>(acc, partials, counter, out6);
+}
+
+inline unsigned nb(long long n, int bs) { return (unsigned)((n + bs - 1) / bs); }
+
+}  // namespace
+}  // namespace otm
+
+using namespace otm;
+
+struct otm_slab_ws {
+    cudaStream_t stream = nullptr;
+    double* partials = nullptr;
+    unsigned* counter = nullptr;
+    double* out = nullptr;       // device scalars
+    double* h = nullptr;         // pinned host copy
+    size_t max_blocks = 0;
+    char err[256] = {0};
+};
+
+static int sfail(otm_slab_ws* w, const char* m) {
+    if (w) std::snprintf(w->err, sizeof w->err, "%s", m);
+    return OTM_ECUDA;
+}
+#define SCK(x)                                                   \
+    do {                                                         \
+        cudaError_t e_ = (x);                                    \
+        if (e_ != cudaSuccess) return sfail(w, cudaGetErrorString(e_)); \
+    } while (0)
+
+static int scheck(otm_slab_ws* w) {
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? OTM_OK : sfail(w, cudaGetErrorString(e));
+}
+static int sfetch(otm_slab_ws* w, int nq, double* out) {
+    SCK(cudaMemcpyAsync(w->h, w->out, nq * sizeof(double), cudaMemcpyDeviceToHost, w->stream));
+    SCK(cudaStreamSynchronize(w->stream));
+    std::memcpy(out, w->h, nq * sizeof(double));
+    return OTM_OK;
+}
+static LevelTemplate tmpl(const double scale[3]) {
+    LevelTemplate lt;
+    ::level_template(scale, lt);
+    return lt;
+}
+static bool blocks_ok(otm_slab_ws* w, long long items, int bs) {
+    return (size_t)nb(items, bs) <= w->max_blocks;
+}
+
+extern "C" {
+
+otm_slab_ws* otm_slab_create(long long max_items) {
+    otm_slab_ws* w = new otm_slab_ws();
+    w->max_blocks = (size_t)((max_items + 127) / 128) + 64;
+    if (cudaMalloc(&w->partials, w->max_blocks * 9 * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&w->counter, 4 * sizeof(unsigned)) != cudaSuccess ||
+        cudaMalloc(&w->out, 16 * sizeof(double)) != cudaSuccess ||
+        cudaMallocHost(&w->h, 16 * sizeof(double)) != cudaSuccess) {
+        delete w;
+        return nullptr;
+    }
+    cudaMemset(w->counter, 0, 4 * sizeof(unsigned));
+    return w;
+}
+
+int otm_slab_destroy(otm_slab_ws* w) {
+    if (!w) return OTM_OK;
+    cudaFree(w->partials);
+    cudaFree(w->counter);
+    cudaFree(w->out);
+    cudaFreeHost(w->h);
+    delete w;
+    return OTM_OK;
+}
+
+int otm_slab_set_stream(otm_slab_ws* w, void* stream) {
+    if (!w) return OTM_EINVAL;
+    w->stream = (cudaStream_t)stream;
+    return OTM_OK;
+}
+
+const char* otm_slab_last_error(otm_slab_ws* w) { return w ? w->err : "null workspace"; }
+
+int otm_slab_stencil(otm_slab_ws* w, int op, int nxl, int ny, int nz, const double scale[3], const float* kap,
+                     const float* a, const float* f, const float* dinv, double omega, float* o1, float* o2,
+                     double* dots3) {
+    if (!w || nxl < 1 || ny < 1 || nz < 1 || op < 0 || op > 2) return OTM_EINVAL;
+    const SGeo g = make_sgeo(nxl, ny, nz);
+    const LevelTemplate lt = tmpl(scale);
+    const long long items = 3 * g.ni;
+    if (!blocks_ok(w, items, 256)) return OTM_EINVAL;
+    const int dot = dots3 != nullptr && op > 0;
+    if (op == 0)
+        ks_stencil<0><<<nb(items, 256), 256, 0, w->stream>>>(g, lt, kap, nullptr, f, dinv, (float)omega, o1, o2, 0,
+                                                              w->partials, w->counter, w->out);
+    else if (op == 1)
+        ks_stencil<1><<<nb(items, 256), 256, 0, w->stream>>>(g, lt, kap, a, f, dinv, (float)omega, o1, nullptr, dot,
+                                                              w->partials, w->counter, w->out);
+    else
+        ks_stencil<2><<<nb(items, 256), 256, 0, w->stream>>>(g, lt, kap, a, nullptr, nullptr, 0.f, o1, nullptr, dot,
+                                                              w->partials, w->counter, w->out);
+    int rc = scheck(w);
+    if (rc || !dot) return rc;
+    return sfetch(w, 3, dots3);
+}
+
+int otm_slab_restrict(otm_slab_ws* w, int nxl_f, int ny_f, int nz_f, const float* res_f, float* f_c) {
+    if (!w || nxl_f < 2 || (nxl_f & 1) || (ny_f & 1) || (nz_f & 1)) return OTM_EINVAL;
+    const SGeo f = make_sgeo(nxl_f, ny_f, nz_f), c = make_sgeo(nxl_f / 2, ny_f / 2, nz_f / 2);
+    ks_restrict<<<nb(3 * c.ni, 256), 256, 0, w->stream>>>(f, c, res_f, f_c);
+    return scheck(w);
+}
+
+int otm_slab_prolong(otm_slab_ws* w, int nxl_f, int ny_f, int nz_f, const float* z_c, float* z_f) {
+    if (!w || nxl_f < 2 || (nxl_f & 1) || (ny_f & 1) || (nz_f & 1)) return OTM_EINVAL;
+    const SGeo f = make_sgeo(nxl_f, ny_f, nz_f), c = make_sgeo(nxl_f / 2, ny_f / 2, nz_f / 2);
+    ks_prolong<<<nb(3 * f.ni, 256), 256, 0, w->stream>>>(f, c, z_c, z_f);
+    return scheck(w);
+}
+
+int otm_slab_coarsen(otm_slab_ws* w, int nxl_f, int ny_f, int nz_f, const float* k_f, float* k_c) {
+    if (!w || nxl_f < 2 || (nxl_f & 1) || (ny_f & 1) || (nz_f & 1)) return OTM_EINVAL;
+    const SGeo f = make_sgeo(nxl_f, ny_f, nz_f), c = make_sgeo(nxl_f / 2, ny_f / 2, nz_f / 2);
+    ks_coarsen<<<nb(c.ni, 256), 256, 0, w->stream>>>(f, c, k_f, k_c);
+    return scheck(w);
+}
+
+int otm_slab_dinv(otm_slab_ws* w, int nxl, int ny, int nz, const double scale[3], const float* kap, float* dinv) {
+    if (!w || nxl < 1) return OTM_EINVAL;
+    const SGeo g = make_sgeo(nxl, ny, nz);
+    const LevelTemplate lt = tmpl(scale);
+    ks_dinv<<<nb(g.ni, 256), 256, 0, w->stream>>>(g, kap, (float)lt.kt[0], dinv);
+    return scheck(w);
+}
+
+int otm_slab_pupd(otm_slab_ws* w, int nxl, int ny, int nz, const float* z, float* p, const double beta3[3]) {
+    if (!w || nxl < 1) return OTM_EINVAL;
+    const SGeo g = make_sgeo(nxl, ny, nz);
+    ks_pupd<<<nb(3 * g.ni, 256), 256, 0, w->stream>>>(g, z, p, beta3[0], beta3[1], beta3[2]);
+    return scheck(w);
+}
+
+int otm_slab_upd(otm_slab_ws* w, int nxl, int ny, int nz, float* d, float* r, const float* p, const float* q,
+                 const double alpha3[3], double* rr3) {
+    if (!w || nxl < 1) return OTM_EINVAL;
+    const SGeo g = make_sgeo(nxl, ny, nz);
+    if (!blocks_ok(w, 3 * g.ni, 256)) return OTM_EINVAL;
+    ks_upd<<<nb(3 * g.ni, 256), 256, 0, w->stream>>>(g, d, r, p, q, alpha3[0], alpha3[1], alpha3[2], w->partials,
+                                                      w->counter, w->out);
+    int rc = scheck(w);
+    if (rc) return rc;
+    return sfetch(w, 3, rr3);
+}
+
+int otm_slab_load_sums(otm_slab_ws* w, int nxl, int ny, int nz, const double scale[3], const double* kap64,
+                       double* sums3) {
+    if (!w || nxl < 1) return OTM_EINVAL;
+    const SGeo g = make_sgeo(nxl, ny, nz);
+    if (!blocks_ok(w, g.ni, 128)) return OTM_EINVAL;
+    const LevelTemplate lt = tmpl(scale);
+    ks_res64<0><<<nb(g.ni, 128), 128, 0, w->stream>>>(g, lt, kap64, nullptr, nullptr, nullptr, w->partials,
+                                                       w->counter, w->out);
+    int rc = scheck(w);
+    if (rc) return rc;
+    double o[9];
+    rc = sfetch(w, 9, o);
+    if (rc) return rc;
+    for (int c = 0; c < 3; ++c) sums3[c] = o[c];
+    return OTM_OK;
+}
+
+int otm_slab_res64(otm_slab_ws* w, int nxl, int ny, int nz, const double scale[3], const double* kap64,
+                   const double* T, const double fmean3[3], float* r32, double* sums9) {
+    if (!w || nxl < 1) return OTM_EINVAL;
+    const SGeo g = make_sgeo(nxl, ny, nz);
+    if (!blocks_ok(w, g.ni, 128)) return OTM_EINVAL;
+    const LevelTemplate lt = tmpl(scale);
+    SCK(cudaMemcpyAsync(w->out + 9, fmean3, 3 * sizeof(double), cudaMemcpyHostToDevice, w->stream));
+    ks_res64<1><<<nb(g.ni, 128), 128, 0, w->stream>>>(g, lt, kap64, T, w->out + 9, r32, w->partials, w->counter,
+                                                       w->out);
+    int rc = scheck(w);
+    if (rc) return rc;
+    return sfetch(w, 9, sums9);
+}
+
+int otm_slab_tupd(otm_slab_ws* w, int nxl, int ny, int nz, double* T, const float* d, const double mean3[3]) {
+    if (!w || nxl < 1) return OTM_EINVAL;
+    const SGeo g = make_sgeo(nxl, ny, nz);
+    ks_tupd<<<nb(3 * g.ni, 256), 256, 0, w->stream>>>(g, T, d, mean3[0], mean3[1], mean3[2], d != nullptr);
+    return scheck(w);
+}
+
+int otm_slab_tensor_sums(otm_slab_ws* w, int nxl, int ny, int nz, const double scale[3], const double* T,
+                         const double* kap64, double* sums6) {
+    if (!w || nxl < 1) return OTM_EINVAL;
+    const SGeo g = make_sgeo(nxl, ny, nz);
+    if (!blocks_ok(w, g.ni, 256)) return OTM_EINVAL;
+    const LevelTemplate lt = tmpl(scale);
+    SCK(cudaMemcpyAsync(w->out + 8, lt.kt, 8 * sizeof(double), cudaMemcpyHostToDevice, w->stream));
+    ks_tensor<<<nb(g.ni, 256), 256, 0, w->stream>>>(g, T, kap64, w->out + 8, w->partials, w->counter, w->out);
+    int rc = scheck(w);
+    if (rc) return rc;
+    return sfetch(w, 6, sums6);
+}
+
+}  // extern "C"

@@ -1,0 +1,482 @@
+"""Slab-decomposed homogenization solve: the multi-GPU path.
+
+The periodic grid is cut along axis 0 (x, the slowest C-order axis of the
+reference's (nx, ny, nz) arrays) into one slab per rank.  Every level of the
+multigrid hierarchy whose planes still split evenly (>= 2 planes, even count per
+rank) is distributed the same way; fields carry one ghost plane per side,
+refreshed by a halo exchange with the two neighbouring ranks before every stencil
+that reads them.  The global couplings are scalars only: the PCG dot products,
+the defect norms, the load and temperature means and the tensor sums, all
+all-reduced.  The first level that no longer splits is agglomerated: its
+right-hand side is all-gathered and every rank runs the rest of the V-cycle
+redundantly with the single-GPU hierarchy (``otm_vcycle``), keeping its own slab
+of the correction.
+
+The algorithm is the single-GPU one (fp64 defect correction around an fp32
+MG-PCG with a damped-Jacobi V-cycle, solver.py:366-406 semantics for ``tol``), so
+a slab solve matches the single-GPU solve to the solver tolerance.
+
+Pieces:
+  * ``SlabSolver``   the orchestration, written against a backend and a comm;
+  * ``CudaSlabBackend`` the device kernels of include/otm_slab.h (libotm.so);
+  * ``DistComm``     one slab per process over torch.distributed (NCCL on GPUs,
+                     gloo on CPU), ``LocalComm`` several slabs in one process
+                     (single-GPU validation of the slab kernels; no collective).
+Tests run the orchestration with a numpy backend under gloo, world size 2
+(tests/test_slab_gloo.py), and the CUDA backend on one GPU with 1, 2 and 4
+local slabs against the single-GPU solver (tests/test_slab_gpu.py).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from .parallel import level_dims
+
+
+# --------------------------------------------------------------------------- geometry
+def level_scales(chain):
+    """Axis scales of every level (the rule of otm_api.cu build: norm*vol/h_a^2)."""
+    h = [1.0, 1.0, 1.0]
+    norm = 1.0
+    out = []
+    for li, d in enumerate(chain):
+        vol = h[0] * h[1] * h[2]
+        out.append(tuple(norm * vol / (h[a] * h[a]) for a in range(3)))
+        if li + 1 < len(chain):
+            for a in range(3):
+                if chain[li + 1][a] < d[a]:
+                    h[a] *= 2.0
+                    norm *= 0.5
+    return out
+
+
+@dataclass(frozen=True)
+class SlabLayout:
+    dims: tuple            # global level-0 dims
+    world: int
+    chain: tuple           # level dims
+    scales: tuple          # level axis scales
+    nlev_dist: int         # levels 0 .. nlev_dist-1 are distributed; level nlev_dist is agglomerated
+
+    @staticmethod
+    def make(dims, world, coarse_target=64):
+        chain = tuple(level_dims(dims, coarse_target))
+        nl = len(chain)
+        la = 0
+        while la < nl - 1:
+            nx = chain[la][0]
+            nxl = nx // world
+            if nx % world or nxl < 2 or nxl % 2 or any(n % 2 for n in chain[la]):
+                break
+            if any(chain[la + 1][a] * 2 != chain[la][a] for a in range(3)):
+                break                               # slab levels need 3-D coarsening
+            la += 1
+        if la == 0:
+            raise ValueError(f"dims {tuple(dims)} cannot be split into {world} even slabs of >= 2 planes")
+        sc = level_scales(chain)
+        if len(set(sc[la])) != 1:
+            raise ValueError("the agglomerated level needs equal axis scales")
+        return SlabLayout(tuple(dims), world, chain, tuple(sc), la)
+
+    def nxl(self, level):
+        return self.chain[level][0] // self.world
+
+
+# --------------------------------------------------------------------------- comms
+class LocalComm:
+    """All slabs live in this process (list index = rank); exchanges are copies."""
+
+    def __init__(self, world):
+        self.world = world
+        self.ranks = list(range(world))
+
+    def halo(self, ts):
+        W = len(ts)
+        last = [t.select(-3, t.shape[-3] - 2).clone() for t in ts]
+        first = [t.select(-3, 1).clone() for t in ts]
+        for i, t in enumerate(ts):
+            t.select(-3, 0).copy_(last[(i - 1) % W])
+            t.select(-3, t.shape[-3] - 1).copy_(first[(i + 1) % W])
+
+    def allreduce(self, vals):
+        out = np.zeros_like(np.asarray(vals[0], dtype=np.float64))
+        for v in vals:                      # rank order: deterministic
+            out = out + np.asarray(v, dtype=np.float64)
+        return out
+
+    def gather(self, ts):
+        import torch
+        return torch.cat([t.narrow(-3, 1, t.shape[-3] - 2) for t in ts], dim=-3)
+
+
+class DistComm:
+    """One slab per process over torch.distributed (NCCL for CUDA tensors, gloo for CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.ranks = [dist.get_rank(group)]
+
+    def halo(self, ts):
+        (t,) = ts
+        dist = self.dist
+        r, W = self.ranks[0], self.world
+        if W == 1:
+            t.select(-3, 0).copy_(t.select(-3, t.shape[-3] - 2))
+            t.select(-3, t.shape[-3] - 1).copy_(t.select(-3, 1))
+            return
+        last = t.select(-3, t.shape[-3] - 2).contiguous()
+        first = t.select(-3, 1).contiguous()
+        from_left = last.new_empty(last.shape)
+        from_right = first.new_empty(first.shape)
+        ops = [dist.P2POp(dist.isend, last, (r + 1) % W, self.group),
+               dist.P2POp(dist.isend, first, (r - 1) % W, self.group),
+               dist.P2POp(dist.irecv, from_left, (r - 1) % W, self.group),
+               dist.P2POp(dist.irecv, from_right, (r + 1) % W, self.group)]
+        for q in dist.batch_isend_irecv(ops):
+            q.wait()
+        t.select(-3, 0).copy_(from_left)
+        t.select(-3, t.shape[-3] - 1).copy_(from_right)
+
+    def allreduce(self, vals):
+        import torch
+        (v,) = vals
+        dev = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
+        tt = torch.tensor(np.asarray(v, dtype=np.float64), device=dev)
+        if self.world > 1:
+            self.dist.all_reduce(tt, op=self.dist.ReduceOp.SUM, group=self.group)
+        return tt.cpu().numpy()
+
+    def gather(self, ts):
+        import torch
+        (t,) = ts
+        inner = t.narrow(-3, 1, t.shape[-3] - 2).contiguous()
+        if self.world == 1:
+            return inner
+        parts = [torch.empty_like(inner) for _ in range(self.world)]
+        self.dist.all_gather(parts, inner, group=self.group)
+        return torch.cat(parts, dim=-3)
+
+
+# --------------------------------------------------------------------------- CUDA backend
+class CudaSlabBackend:
+    """The slab kernels of libotm.so (include/otm_slab.h) on torch-allocated device memory."""
+
+    def __init__(self, max_items):
+        from . import _dev, _lib
+        _dev.require_cuda()
+        self.t = _dev.torch()
+        self.lib = _lib.load()
+        self.ws = self.lib.otm_slab_create(int(max_items))
+        if not self.ws:
+            raise RuntimeError("otm_slab_create failed")
+        self.device = "cuda"
+        self.f32 = self.t.float32
+        self.f64 = self.t.float64
+
+    def __del__(self):
+        try:
+            self.lib.otm_slab_destroy(self.ws)
+        except Exception:
+            pass
+
+    def zeros(self, shape, dtype):
+        return self.t.zeros(shape, dtype=dtype, device="cuda")
+
+    def _rc(self, rc):
+        if rc != 0:
+            msg = self.lib.otm_slab_last_error(self.ws).decode()
+            raise (ValueError if rc == 1 else RuntimeError)(f"slab kernel failed ({rc}): {msg}")
+
+    def _sync_stream(self):
+        self.lib.otm_slab_set_stream(self.ws, C.c_void_p(self.t.cuda.current_stream().cuda_stream))
+
+    @staticmethod
+    def _d3(v):
+        return (C.c_double * 3)(*[float(x) for x in v])
+
+    @staticmethod
+    def _p(t):
+        return C.c_void_p(t.data_ptr()) if t is not None else None
+
+    def stencil(self, op, dims, scale, kap, a, f, dinv, omega, o1, o2=None, want_dots=False):
+        self._sync_stream()
+        out = (C.c_double * 3)()
+        self._rc(self.lib.otm_slab_stencil(self.ws, op, *dims, self._d3(scale), self._p(kap), self._p(a),
+                                           self._p(f), self._p(dinv), float(omega), self._p(o1), self._p(o2),
+                                           out if want_dots else None))
+        return np.array(out[:]) if want_dots else None
+
+    def restrict(self, dims_f, res_f, f_c):
+        self._sync_stream()
+        self._rc(self.lib.otm_slab_restrict(self.ws, *dims_f, self._p(res_f), self._p(f_c)))
+
+    def prolong(self, dims_f, z_c, z_f):
+        self._sync_stream()
+        self._rc(self.lib.otm_slab_prolong(self.ws, *dims_f, self._p(z_c), self._p(z_f)))
+
+    def coarsen(self, dims_f, k_f, k_c):
+        self._sync_stream()
+        self._rc(self.lib.otm_slab_coarsen(self.ws, *dims_f, self._p(k_f), self._p(k_c)))
+
+    def dinv(self, dims, scale, kap, out):
+        self._sync_stream()
+        self._rc(self.lib.otm_slab_dinv(self.ws, *dims, self._d3(scale), self._p(kap), self._p(out)))
+
+    def pupd(self, dims, z, p, beta):
+        self._sync_stream()
+        self._rc(self.lib.otm_slab_pupd(self.ws, *dims, self._p(z), self._p(p), self._d3(beta)))
+
+    def upd(self, dims, d, r, p, q, alpha):
+        self._sync_stream()
+        out = (C.c_double * 3)()
+        self._rc(self.lib.otm_slab_upd(self.ws, *dims, self._p(d), self._p(r), self._p(p), self._p(q),
+                                       self._d3(alpha), out))
+        return np.array(out[:])
+
+    def load_sums(self, dims, scale, kap64):
+        self._sync_stream()
+        out = (C.c_double * 3)()
+        self._rc(self.lib.otm_slab_load_sums(self.ws, *dims, self._d3(scale), self._p(kap64), out))
+        return np.array(out[:])
+
+    def res64(self, dims, scale, kap64, T, fmean, r32):
+        self._sync_stream()
+        out = (C.c_double * 9)()
+        self._rc(self.lib.otm_slab_res64(self.ws, *dims, self._d3(scale), self._p(kap64), self._p(T),
+                                         self._d3(fmean), self._p(r32), out))
+        return np.array(out[:])
+
+    def tupd(self, dims, T, d, mean):
+        self._sync_stream()
+        self._rc(self.lib.otm_slab_tupd(self.ws, *dims, self._p(T), self._p(d), self._d3(mean)))
+
+    def tensor_sums(self, dims, scale, T, kap64):
+        self._sync_stream()
+        out = (C.c_double * 6)()
+        self._rc(self.lib.otm_slab_tensor_sums(self.ws, *dims, self._d3(scale), self._p(T), self._p(kap64), out))
+        return np.array(out[:])
+
+    # agglomerated coarse levels: the single-GPU hierarchy of that level
+    def coarse_hierarchy(self, dims):
+        from ._dev import Context
+        return Context(dims)
+
+    def coarse_build(self, ctx, kap_full32):
+        k64 = kap_full32.to(self.f64).contiguous()
+        ctx.call("otm_build_kappa", C.c_void_p(k64.data_ptr()))
+
+    def coarse_vcycle(self, ctx, f_full, z_full):
+        ctx.call("otm_vcycle", C.c_void_p(f_full.data_ptr()), C.c_void_p(z_full.data_ptr()))
+
+
+# --------------------------------------------------------------------------- solver
+class _Lev:
+    pass
+
+
+class SlabSolver:
+    """Distributed solve_cases + effective tensor on x-slabs (homogenize.py:71-122)."""
+
+    def __init__(self, dims, comm, backend, kappa0=1.0, kappa_min=1e-4, penalty=3.0, omega=0.8,
+                 inner_reduction=1e-5, max_inner=40):
+        self.L = SlabLayout.make(dims, comm.world)
+        self.comm, self.B = comm, backend
+        self.kappa0, self.kappa_min, self.penalty = kappa0, kappa_min, penalty
+        self.omega, self.inner_reduction, self.max_inner = omega, inner_reduction, max_inner
+        self.ranks = list(comm.ranks)
+        B, L = backend, self.L
+        f32, f64 = B.f32, B.f64
+        self.slabs = []
+        for r in self.ranks:
+            s = _Lev()
+            s.rank = r
+            s.levels = []
+            for l in range(L.nlev_dist):
+                nx, ny, nz = L.chain[l]
+                nxl = nx // L.world
+                lv = _Lev()
+                lv.dims = (nxl, ny, nz)
+                lv.kap = B.zeros((nxl + 2, ny, nz), f32)
+                lv.dinv = B.zeros((nxl + 2, ny, nz), f32)
+                lv.f = B.zeros((3, nxl + 2, ny, nz), f32)
+                lv.z = B.zeros((3, nxl + 2, ny, nz), f32)
+                lv.res = B.zeros((3, nxl + 2, ny, nz), f32)
+                s.levels.append(lv)
+            nxl, ny, nz = s.levels[0].dims
+            s.kap64 = B.zeros((nxl + 2, ny, nz), f64)
+            s.T = B.zeros((3, nxl + 2, ny, nz), f64)
+            s.p = B.zeros((3, nxl + 2, ny, nz), f32)
+            s.q = B.zeros((3, nxl + 2, ny, nz), f32)
+            s.d = B.zeros((3, nxl + 2, ny, nz), f32)
+            # the agglomerated level's slab (with ghosts) for the coarse correction
+            cx, cy, cz = L.chain[L.nlev_dist]
+            cl = cx // L.world
+            s.cres = B.zeros((3, cl + 2, cy, cz), f32)
+            s.cf = B.zeros((3, cl + 2, cy, cz), f32)
+            s.ckap = B.zeros((cl + 2, cy, cz), f32)
+            self.slabs.append(s)
+        self.coarse = B.coarse_hierarchy(L.chain[L.nlev_dist])
+        self.coarse_scale = L.scales[L.nlev_dist][0]
+        self.n_total = int(np.prod(dims))
+        self.warm = False
+        self.fmean = np.zeros(3)
+
+    # ---- helpers
+    def _halo(self, get):
+        self.comm.halo([get(s) for s in self.slabs])
+
+    def _sum(self, vals):
+        return self.comm.allreduce(vals)
+
+    def x0(self, s, level=0):
+        return s.rank * self.L.nxl(level)
+
+    # ---- build (solver.py:269-305 on slabs)
+    def build_kappa(self, kap64_interiors):
+        """kap64_interiors: one (nxl, ny, nz) fp64 device array per local slab (level-0 element factors)."""
+        B, L = self.B, self.L
+        for s, k in zip(self.slabs, kap64_interiors):
+            s.kap64.narrow(0, 1, s.kap64.shape[0] - 2).copy_(k)
+        self._halo(lambda s: s.kap64)
+        for s in self.slabs:
+            s.levels[0].kap.copy_(s.kap64.to(B.f32))
+        for l in range(L.nlev_dist):
+            if l > 0:
+                for s in self.slabs:
+                    B.coarsen(s.levels[l - 1].dims, s.levels[l - 1].kap, s.levels[l].kap)
+                self._halo(lambda s, l=l: s.levels[l].kap)
+            for s in self.slabs:
+                lv = s.levels[l]
+                B.dinv(lv.dims, L.scales[l], lv.kap, lv.dinv)
+            self._halo(lambda s, l=l: s.levels[l].dinv)
+        for s in self.slabs:
+            top = s.levels[-1]
+            B.coarsen(top.dims, top.kap, s.ckap)
+        full = self.comm.gather([s.ckap for s in self.slabs])
+        B.coarse_build(self.coarse, full.contiguous())
+        self.warm = False
+
+    def build_density(self, rho_f_interiors):
+        """SIMP (element.py:91-94) on each slab's interior filtered density, then build."""
+        k = [self.kappa_min + (self.kappa0 - self.kappa_min) * r ** self.penalty for r in rho_f_interiors]
+        self.build_kappa(k)
+
+    # ---- V-cycle on slabs (solver.py:206-215 with the damped-Jacobi smoother)
+    def _vcycle(self):
+        B, L, om = self.B, self.L, self.omega
+        nd = L.nlev_dist
+        dots = [None] * len(self.slabs)
+        for l in range(nd):
+            self._halo(lambda s, l=l: s.levels[l].f)
+            for s in self.slabs:
+                lv = s.levels[l]
+                B.stencil(0, lv.dims, L.scales[l], lv.kap, None, lv.f, lv.dinv, om, lv.z, lv.res)
+            self._halo(lambda s, l=l: s.levels[l].res)
+            for s in self.slabs:
+                lv = s.levels[l]
+                dst = s.levels[l + 1].f if l + 1 < nd else s.cf
+                B.restrict(lv.dims, lv.res, dst)
+        # agglomerated levels: every rank runs the coarse V-cycle on the gathered right-hand side
+        f_full = self.comm.gather([s.cf for s in self.slabs]).contiguous()
+        z_full = B.zeros(tuple(f_full.shape), B.f32)
+        B.coarse_vcycle(self.coarse, f_full, z_full)
+        z_full.mul_(1.0 / self.coarse_scale)              # that hierarchy's level 0 carries scale 1
+        cl = self.L.nxl(nd)
+        nxc = self.L.chain[nd][0]
+        for s in self.slabs:
+            lo = s.rank * cl
+            idx = [(lo - 1 + i) % nxc for i in range(cl + 2)]
+            s.cres.copy_(z_full[:, idx])
+        for l in range(nd - 1, -1, -1):
+            for s in self.slabs:
+                lv = s.levels[l]
+                src = s.levels[l + 1].res if l + 1 < nd else s.cres
+                B.prolong(lv.dims, src, lv.z)
+            self._halo(lambda s, l=l: s.levels[l].z)
+            for s_i, s in enumerate(self.slabs):
+                lv = s.levels[l]
+                d = B.stencil(1, lv.dims, L.scales[l], lv.kap, lv.z, lv.f, lv.dinv, om, lv.res, None,
+                              want_dots=(l == 0))
+                if l == 0:
+                    dots[s_i] = d
+            if l > 0:
+                self._halo(lambda s, l=l: s.levels[l].res)
+        return self._sum(dots)                            # r . z per case
+
+    # ---- solve (solver.py:366-406 semantics, fp64 defect correction)
+    def solve(self, tol=1e-6, max_vcycles=200):
+        B, L = self.B, self.L
+        d0 = self.slabs[0].levels[0].dims
+        sc0 = L.scales[0]
+        self.fmean = self._sum([B.load_sums(d0, sc0, s.kap64) for s in self.slabs]) / self.n_total
+        if not self.warm:
+            for s in self.slabs:
+                s.T.zero_()
+        cycles = 0
+
+        def residual():
+            self._halo(lambda s: s.T)
+            sums = self._sum([B.res64(d0, sc0, s.kap64, s.T, self.fmean, s.levels[0].f) for s in self.slabs])
+            rr, ff = sums[0:3], sums[3:6]
+            fn = np.sqrt(ff)
+            rel = np.where(fn > 0, np.sqrt(rr) / np.where(fn > 0, fn, 1.0), 0.0)
+            self._sumT = sums[6:9]
+            return rel, fn, np.sqrt(rr)
+
+        rel, fn, rn = residual()
+        done = (fn == 0) | (rel <= tol)
+        while not done.all():
+            if cycles >= max_vcycles:
+                from ._dev import ConvergenceError
+                raise ConvergenceError(f"slab solve did not converge in {max_vcycles} cycles", float(rel.max()))
+            target2 = np.maximum(self.inner_reduction * rn, 0.5 * tol * fn) ** 2
+            active = ~done
+            for s in self.slabs:
+                s.d.zero_()
+                s.p.zero_()
+            rz_old = None
+            for it in range(self.max_inner):
+                rz = self._vcycle()
+                beta = np.zeros(3) if rz_old is None else np.where(rz_old != 0, rz / np.where(rz_old != 0, rz_old, 1), 0)
+                rz_old = rz
+                for s in self.slabs:
+                    B.pupd(d0, s.levels[0].res, s.p, beta)
+                self._halo(lambda s: s.p)
+                pq = self._sum([B.stencil(2, d0, sc0, s.levels[0].kap, s.p, None, None, 0.0, s.q, None,
+                                          want_dots=True) for s in self.slabs])
+                alpha = np.where(active & (pq > 0), rz / np.where(pq > 0, pq, 1), 0.0)
+                rr = self._sum([B.upd(d0, s.d, s.levels[0].f, s.p, s.q, alpha) for s in self.slabs])
+                cycles += int(active.sum())
+                active = active & (rr > target2)
+                if not active.any() or cycles >= max_vcycles:
+                    break
+            for s in self.slabs:
+                B.tupd(d0, s.T, s.d, np.zeros(3))
+            rel, fn, rn = residual()
+            done = (fn == 0) | (rel <= tol)
+        # mean projection of the solution (solver.py:404-406); sum T from the last defect pass
+        mean = self._sumT / self.n_total
+        for s in self.slabs:
+            B.tupd(d0, s.T, None, mean)
+        self.warm = True
+        self.cycles = cycles
+        return cycles
+
+    def tensor(self):
+        """kappa_H (homogenize.py:103-122): all-reduced element-energy sums / N."""
+        B, L = self.B, self.L
+        d0 = self.slabs[0].levels[0].dims
+        self._halo(lambda s: s.T)
+        sums = self._sum([B.tensor_sums(d0, L.scales[0], s.T, s.kap64) for s in self.slabs])
+        return sums / self.n_total
+
+    def fields(self):
+        """The full 3-case temperature fields (gathered; for tests)."""
+        return self.comm.gather([s.T for s in self.slabs])

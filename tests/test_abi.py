@@ -1,5 +1,6 @@
 """CPU-only checks of the C ABI: the library loads and exports every symbol that
-include/otm.h declares, and the ctypes table covers them (no device calls)."""
+include/*.h (otm.h, otm_slab.h) declares, and the ctypes table covers them (no
+device calls)."""
 
 import ctypes
 import os
@@ -9,12 +10,12 @@ import pytest
 
 from otm_testutil import ROOT
 
-HEADER = os.path.join(ROOT, "include", "otm.h")
+HEADERS = [os.path.join(ROOT, "include", h) for h in ("otm.h", "otm_slab.h")]
 LIB = os.path.join(ROOT, "paper_2405_19991_b200", "libotm.so")
 
 
 def declared():
-    text = open(HEADER).read()
+    text = "\n".join(open(h).read() for h in HEADERS)
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
     return sorted(set(re.findall(r"\b(otm_[A-Za-z0-9_]+)\s*\(", text)))
 
@@ -22,7 +23,8 @@ def declared():
 def test_header_declares_api():
     names = declared()
     for must in ("otm_create", "otm_solve", "otm_tensor", "otm_sensitivity", "otm_filter", "otm_oc_update",
-                 "otm_run_step", "otm_run_update", "otm_governor_update"):
+                 "otm_run_step", "otm_run_update", "otm_governor_update", "otm_vcycle", "otm_slab_stencil",
+                 "otm_slab_res64", "otm_slab_restrict", "otm_slab_prolong"):
         assert must in names
 
 
