@@ -22,9 +22,14 @@
  *   otm_slab_dinv        solver.py:119-128 (diagonal)
  *   otm_slab_res64       solver.py:386-401 (macro loads, mean projection, residual)
  *   otm_slab_tensor_sums homogenize.py:103-122 (kappa_H sums)
+ *   otm_slab_filter      field.py:230-236 (cone filter, forward / adjoint) + element.py:91-94
+ *   otm_slab_sensitivity homogenize.py:143-160
+ *   otm_slab_oc_sums/apply optimize.py:114-160 (candidate means / update)
  */
 #ifndef OTM_SLAB_H
 #define OTM_SLAB_H
+
+#include "otm.h"
 
 #ifdef __cplusplus
 extern "C" {
@@ -66,6 +71,22 @@ int otm_slab_tupd(otm_slab_ws* w, int nxl, int ny, int nz, double* T, const floa
 /* sums6 = sum_e kappa_e E_pq[e] over the slab's elements (T needs its right ghost) */
 int otm_slab_tensor_sums(otm_slab_ws* w, int nxl, int ny, int nz, const double scale[3], const double* T,
                          const double* kap64, double* sums6);
+
+/* Density filter on a slab (field.py:230-236, radius <= 2: one ghost plane), bit-identical
+ * taps.  mode 2: forward + SIMP (element.py:91-94): out = rho_f, kap64 = kappa(rho_f), sums3 =
+ * [sum rho, sum rho^p, sum rho_f]; mode 1: adjoint (kap64, sums3 unused).  in needs both ghosts. */
+int otm_slab_filter(otm_slab_ws* w, int mode, int nxl, int ny, int nz, double radius, double kappa0,
+                    double kappa_min, double penalty, const double* in, double* out, double* kap64,
+                    double* sums3);
+/* sens_f = kappa'(rho_f) (dG . E) / n_total (homogenize.py:143-160); T needs its right ghost. */
+int otm_slab_sensitivity(otm_slab_ws* w, int nxl, int ny, int nz, double n_total, double kappa0, double kappa_min,
+                         double penalty, const double* T, const double* rho_f, const double dG6[6], double* sens_f);
+/* OC candidate sums for nlam <= 32 multipliers (optimize.py:114-160; lam 0 = free step). */
+int otm_slab_oc_sums(otm_slab_ws* w, int nxl, int ny, int nz, double n_total, const otm_oc_params* pp,
+                     const double* rho, const double* sens, int nlam, const double* lams, double* sums32);
+/* rho_out = candidate of lam (reference expression); changed = number of vertices that moved. */
+int otm_slab_oc_apply(otm_slab_ws* w, int nxl, int ny, int nz, double n_total, const otm_oc_params* pp,
+                      const double* rho, const double* sens, double lam, double* rho_out, double* changed);
 
 #ifdef __cplusplus
 }

@@ -119,6 +119,14 @@ _SIGS = {
     "otm_slab_tupd": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, dptr, dptr, C.POINTER(C.c_double)]),
     "otm_slab_tensor_sums": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double), dptr, dptr,
                                        C.POINTER(C.c_double)]),
+    "otm_slab_filter": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                  C.c_double, C.c_double, dptr, dptr, dptr, C.POINTER(C.c_double)]),
+    "otm_slab_sensitivity": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                       C.c_double, dptr, dptr, C.POINTER(C.c_double), dptr]),
+    "otm_slab_oc_sums": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.POINTER(OCParamsC), dptr,
+                                   dptr, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "otm_slab_oc_apply": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double, C.POINTER(OCParamsC), dptr,
+                                    dptr, C.c_double, dptr, C.POINTER(C.c_double)]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -165,12 +165,14 @@ void level_template(const double scale[3], LevelTemplate& lt) {
 namespace {
 
 // cone taps (field.py:60-93)
-int setup_filter(otm_ctx* ctx, double radius) {
-    if (!(radius >= 1.0)) return fail(ctx, OTM_EINVAL, "filter radius must be >= 1");
+}  // namespace
+
+// normalised cone taps (field.py:60-93): offsets (dx, dy, dz) and weights w / w.sum()
+// with numpy's summation order, so the weights are bit-identical to field.py:93
+void filter_weights(double radius, std::vector<int>& offs, std::vector<double>& w) {
     const int reach = (int)std::ceil(radius) - 1;
-    std::vector<int> offs;
-    std::vector<double> w;
-    double tot = 0.0;
+    offs.clear();
+    w.clear();
     for (int dx = -reach; dx <= reach; ++dx)
         for (int dy = -reach; dy <= reach; ++dy)
             for (int dz = -reach; dz <= reach; ++dz) {
@@ -178,29 +180,33 @@ int setup_filter(otm_ctx* ctx, double radius) {
                 if (wt > 0.0) {
                     offs.push_back(dx); offs.push_back(dy); offs.push_back(dz);
                     w.push_back(wt);
-                    tot += wt;
                 }
             }
-    // w / w.sum() with numpy's summation order (pairwise_sum, n <= 128: eight
-    // strided accumulators, combined as a tree, then the tail) so the weights
-    // are bit-identical to field.py:93
-    (void)tot;
-    {
-        const size_t m = w.size();
-        double sum = 0.0;
-        if (m < 8) {
-            for (size_t i = 0; i < m; ++i) sum += w[i];
-        } else {
-            double r[8];
-            for (int j = 0; j < 8; ++j) r[j] = w[j];
-            size_t i = 8;
-            for (; i + 8 <= m; i += 8)
-                for (int j = 0; j < 8; ++j) r[j] += w[i + j];
-            sum = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-            for (; i < m; ++i) sum += w[i];
-        }
-        for (auto& x : w) x /= sum;
+    // numpy pairwise_sum for n <= 128: eight strided accumulators, combined as a tree, then the tail
+    const size_t m = w.size();
+    double sum = 0.0;
+    if (m < 8) {
+        for (size_t i = 0; i < m; ++i) sum += w[i];
+    } else {
+        double r[8];
+        for (int j = 0; j < 8; ++j) r[j] = w[j];
+        size_t i = 8;
+        for (; i + 8 <= m; i += 8)
+            for (int j = 0; j < 8; ++j) r[j] += w[i + j];
+        sum = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < m; ++i) sum += w[i];
     }
+    for (auto& x : w) x /= sum;
+}
+
+namespace {
+
+int setup_filter(otm_ctx* ctx, double radius) {
+    if (!(radius >= 1.0)) return fail(ctx, OTM_EINVAL, "filter radius must be >= 1");
+    const int reach = (int)std::ceil(radius) - 1;
+    std::vector<int> offs;
+    std::vector<double> w;
+    filter_weights(radius, offs, w);
     FilterSetup& fs = ctx->fs;
     fs.ntaps = (int)w.size();
     fs.window = reach <= 1 ? 1 : 0;

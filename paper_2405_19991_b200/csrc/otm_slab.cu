@@ -22,9 +22,14 @@
 #include <vector>
 
 void level_template(const double scale[3], otm::LevelTemplate& lt);   // otm_api.cu
+void filter_weights(double radius, std::vector<int>& offs, std::vector<double>& w);   // otm_api.cu
 
 namespace otm {
 namespace {
+
+struct W27 {
+    double w[27];
+};
 
 struct SGeo {
     int nxl, ny, nz;
@@ -349,6 +354,123 @@ __global__ void __launch_bounds__(256) ks_tensor(SGeo g, const double* __restric
     reduce_finalize<6>(acc, partials, counter, out6);
 }
 
+
+// density filter on a slab (field.py:230-236; reach <= 1, 27-slot weights in the
+// single-GPU tap order, so results are bit-identical).  MODE 2: forward + SIMP
+// (element.py:91-94) + partial sums of rho, rho^p, rho_f; MODE 1: adjoint.
+template <int MODE>
+__global__ void __launch_bounds__(256) ks_filter(SGeo g, W27 taps, const double* __restrict__ in,
+                                                 double* __restrict__ out, double* __restrict__ kap64,
+                                                 SimpParams sp, double* partials, unsigned* counter,
+                                                 double* out3) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double acc3[3] = {0.0, 0.0, 0.0};
+    if (i < g.ni) {
+        int x, y, z;
+        s_decode(g, i, x, y, z);
+        const int ys[3] = {wrap_m(y, g.ny) * g.nz, y * g.nz, wrap_p(y, g.ny) * g.nz};
+        const int zs[3] = {wrap_m(z, g.nz), z, wrap_p(z, g.nz)};
+        double sacc = 0.0;
+#pragma unroll
+        for (int slot = 0; slot < 27; ++slot) {
+            const double wt = taps.w[slot];
+            if (wt != 0.0) {
+                const int src = MODE == 1 ? 26 - slot : slot;
+                const int p = src / 9, j = (src / 3) % 3, m = src % 3;
+                sacc = __dadd_rn(sacc, __dmul_rn(wt, __ldg(in + (long long)(x - 1 + p) * g.pl + ys[j] + zs[m])));
+            }
+        }
+        const long long idx = (long long)x * g.pl + y * g.nz + z;
+        out[idx] = sacc;
+        if (MODE == 2) {
+            kap64[idx] = sp.kmin + pow(sacc, sp.p) * (sp.k0 - sp.kmin);
+            const double r = __ldg(in + idx);
+            acc3[0] = r;
+            acc3[1] = pow(r, sp.p);
+            acc3[2] = sacc;
+        }
+    }
+    if (MODE == 2) reduce_finalize<3>(acc3, partials, counter, out3);
+}
+
+// sens_f = kappa'(rho_f) (dG . E) / M (homogenize.py:143-160); element e = vertex e
+__global__ void __launch_bounds__(256) ks_sens(SGeo g, const double* __restrict__ T, const double* __restrict__ rf,
+                                               const double* __restrict__ kt, SimpParams sp, Dg dG, double M,
+                                               double* __restrict__ sens) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= g.ni) return;
+    int x, y, z;
+    s_decode(g, i, x, y, z);
+    const int ys[2] = {y, wrap_p(y, g.ny)}, zs[2] = {z, wrap_p(z, g.nz)};
+    double chi[3][8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        const long long idx = (long long)(x + (a & 1)) * g.pl + ys[(a >> 1) & 1] * g.nz + zs[(a >> 2) & 1];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) chi[c][a] = (double)((a >> c) & 1) - __ldg(T + (long long)c * g.na + idx);
+    }
+    const int pr[6][2] = {{0, 0}, {1, 1}, {2, 2}, {0, 1}, {1, 2}, {0, 2}};
+    double con = 0.0;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+        double e = 0.0;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            double ka = 0.0;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) ka += kt[a ^ b] * chi[pr[q][1]][b];
+            e += chi[pr[q][0]][a] * ka;
+        }
+        con += dG.v[q] * e;
+    }
+    const long long idx = (long long)x * g.pl + y * g.nz + z;
+    const double dk = sp.p * pow(rf[idx], sp.p - 1.0) * (sp.k0 - sp.kmin);
+    sens[idx] = dk * con / M;
+}
+
+// OC candidate sums for up to 32 multipliers (optimize.py:114-160, the reference's
+// candidate expression); lam == 0 is the free step.  APPLY: write the candidate of
+// lams[0] and count changed vertices.
+template <bool APPLY>
+__global__ void __launch_bounds__(256) ks_oc(SGeo g, const double* __restrict__ rho,
+                                             const double* __restrict__ sens, OcArgs a, double M, LamSet lams,
+                                             int nlam, double* __restrict__ rho_out, double* partials,
+                                             unsigned* counter, double* out32) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double acc[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) acc[k] = 0.0;
+    if (i < g.ni) {
+        int x, y, z;
+        s_decode(g, i, x, y, z);
+        const long long idx = (long long)x * g.pl + y * g.nz + z;
+        const double r = rho[idx];
+        const double desc = M * (-sens[idx]);
+        const double lo = fmax(r - a.step, a.rmin), hi = fmin(r + a.step, 1.0);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            if (k < nlam) {
+                const double lam = lams.v[k];
+                double out;
+                if (lam == 0.0) {
+                    out = desc > 0.0 ? hi : (desc < 0.0 ? lo : r);
+                } else {
+                    const double qv = fmax(desc / lam, 1e-10);
+                    const double ratio = a.sqrt_damp ? sqrt(qv) : pow(qv, a.damp);
+                    out = fmin(fmax(r * ratio, lo), hi);
+                }
+                if (APPLY) {
+                    rho_out[idx] = out;
+                    acc[0] = out != r ? 1.0 : 0.0;
+                    break;
+                }
+                acc[k] = out;
+            }
+        }
+    }
+    if (reduce_finalize32(acc, partials, counter, out32)) {}
+}
+
 inline unsigned nb(long long n, int bs) { return (unsigned)((n + bs - 1) / bs); }
 
 }  // namespace
@@ -362,6 +484,8 @@ struct otm_slab_ws {
     unsigned* counter = nullptr;
     double* out = nullptr;       // device scalars
     double* h = nullptr;         // pinned host copy
+    double* out32 = nullptr;     // 32 OC candidate sums (device) and their host copy
+    double* h32 = nullptr;
     size_t max_blocks = 0;
     char err[256] = {0};
 };
@@ -400,10 +524,12 @@ extern "C" {
 otm_slab_ws* otm_slab_create(long long max_items) {
     otm_slab_ws* w = new otm_slab_ws();
     w->max_blocks = (size_t)((max_items + 127) / 128) + 64;
-    if (cudaMalloc(&w->partials, w->max_blocks * 9 * sizeof(double)) != cudaSuccess ||
+    if (cudaMalloc(&w->partials, w->max_blocks * 32 * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&w->counter, 4 * sizeof(unsigned)) != cudaSuccess ||
         cudaMalloc(&w->out, 16 * sizeof(double)) != cudaSuccess ||
-        cudaMallocHost(&w->h, 16 * sizeof(double)) != cudaSuccess) {
+        cudaMallocHost(&w->h, 16 * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&w->out32, 32 * sizeof(double)) != cudaSuccess ||
+        cudaMallocHost(&w->h32, 32 * sizeof(double)) != cudaSuccess) {
         delete w;
         return nullptr;
     }
@@ -417,6 +543,8 @@ int otm_slab_destroy(otm_slab_ws* w) {
     cudaFree(w->counter);
     cudaFree(w->out);
     cudaFreeHost(w->h);
+    cudaFree(w->out32);
+    cudaFreeHost(w->h32);
     delete w;
     return OTM_OK;
 }
@@ -549,6 +677,102 @@ int otm_slab_tensor_sums(otm_slab_ws* w, int nxl, int ny, int nz, const double s
     int rc = scheck(w);
     if (rc) return rc;
     return sfetch(w, 6, sums6);
+}
+
+int otm_slab_filter(otm_slab_ws* w, int mode, int nxl, int ny, int nz, double radius, double kappa0,
+                    double kappa_min, double penalty, const double* in, double* out, double* kap64,
+                    double* sums3) {
+    if (!w || nxl < 1 || (mode != 1 && mode != 2) || !(radius >= 1.0) || radius > 2.0 ||
+        (mode == 2 && (!kap64 || !sums3)))
+        return OTM_EINVAL;
+    const SGeo g = make_sgeo(nxl, ny, nz);
+    if (!blocks_ok(w, g.ni, 256)) return OTM_EINVAL;
+    std::vector<int> offs;
+    std::vector<double> wt;
+    filter_weights(radius, offs, wt);
+    W27 taps;
+    for (int i = 0; i < 27; ++i) taps.w[i] = 0.0;
+    for (size_t i = 0; i < wt.size(); ++i) {
+        const int slot = (offs[3 * i] + 1) * 9 + (offs[3 * i + 1] + 1) * 3 + (offs[3 * i + 2] + 1);
+        taps.w[slot] = wt[i];
+    }
+    SimpParams sp;
+    sp.k0 = kappa0;
+    sp.kmin = kappa_min;
+    sp.p = penalty;
+    if (mode == 2)
+        ks_filter<2><<<nb(g.ni, 256), 256, 0, w->stream>>>(g, taps, in, out, kap64, sp, w->partials, w->counter,
+                                                            w->out);
+    else
+        ks_filter<1><<<nb(g.ni, 256), 256, 0, w->stream>>>(g, taps, in, out, nullptr, sp, w->partials, w->counter,
+                                                            w->out);
+    int rc = scheck(w);
+    if (rc || mode == 1) return rc;
+    return sfetch(w, 3, sums3);
+}
+
+int otm_slab_sensitivity(otm_slab_ws* w, int nxl, int ny, int nz, double n_total, double kappa0, double kappa_min,
+                         double penalty, const double* T, const double* rho_f, const double dG6[6], double* sens_f) {
+    if (!w || nxl < 1 || !(n_total > 0)) return OTM_EINVAL;
+    const SGeo g = make_sgeo(nxl, ny, nz);
+    const double unit[3] = {1.0, 1.0, 1.0};
+    const LevelTemplate lt = tmpl(unit);
+    SCK(cudaMemcpyAsync(w->out + 8, lt.kt, 8 * sizeof(double), cudaMemcpyHostToDevice, w->stream));
+    SimpParams sp;
+    sp.k0 = kappa0;
+    sp.kmin = kappa_min;
+    sp.p = penalty;
+    Dg dg;
+    for (int q = 0; q < 6; ++q) dg.v[q] = dG6[q];
+    ks_sens<<<nb(g.ni, 256), 256, 0, w->stream>>>(g, T, rho_f, w->out + 8, sp, dg, n_total, sens_f);
+    return scheck(w);
+}
+
+int otm_slab_oc_sums(otm_slab_ws* w, int nxl, int ny, int nz, double n_total, const otm_oc_params* pp,
+                     const double* rho, const double* sens, int nlam, const double* lams, double* sums32) {
+    if (!w || !pp || nxl < 1 || nlam < 1 || nlam > 32) return OTM_EINVAL;
+    const SGeo g = make_sgeo(nxl, ny, nz);
+    if ((size_t)nb(g.ni, 256) * 32 > w->max_blocks * 9) return OTM_EINVAL;
+    OcArgs a;
+    a.step = pp->step_limit;
+    a.rmin = pp->min_density;
+    a.damp = pp->damp;
+    a.floor_ratio = std::pow(1e-10, pp->damp);
+    a.sqrt_damp = pp->damp == 0.5;
+    LamSet ls;
+    for (int k = 0; k < 32; ++k) ls.v[k] = k < nlam ? lams[k] : 0.0;
+    ks_oc<false><<<nb(g.ni, 256), 256, 0, w->stream>>>(g, rho, sens, a, n_total, ls, nlam, nullptr, w->partials,
+                                                        w->counter, w->out32);
+    int rc = scheck(w);
+    if (rc) return rc;
+    SCK(cudaMemcpyAsync(w->h32, w->out32, 32 * sizeof(double), cudaMemcpyDeviceToHost, w->stream));
+    SCK(cudaStreamSynchronize(w->stream));
+    std::memcpy(sums32, w->h32, nlam * sizeof(double));
+    return OTM_OK;
+}
+
+int otm_slab_oc_apply(otm_slab_ws* w, int nxl, int ny, int nz, double n_total, const otm_oc_params* pp,
+                      const double* rho, const double* sens, double lam, double* rho_out, double* changed) {
+    if (!w || !pp || nxl < 1) return OTM_EINVAL;
+    const SGeo g = make_sgeo(nxl, ny, nz);
+    if ((size_t)nb(g.ni, 256) * 32 > w->max_blocks * 9) return OTM_EINVAL;
+    OcArgs a;
+    a.step = pp->step_limit;
+    a.rmin = pp->min_density;
+    a.damp = pp->damp;
+    a.floor_ratio = std::pow(1e-10, pp->damp);
+    a.sqrt_damp = pp->damp == 0.5;
+    LamSet ls;
+    for (int k = 0; k < 32; ++k) ls.v[k] = 0.0;
+    ls.v[0] = lam;
+    ks_oc<true><<<nb(g.ni, 256), 256, 0, w->stream>>>(g, rho, sens, a, n_total, ls, 1, rho_out, w->partials,
+                                                       w->counter, w->out32);
+    int rc = scheck(w);
+    if (rc) return rc;
+    SCK(cudaMemcpyAsync(w->h32, w->out32, sizeof(double), cudaMemcpyDeviceToHost, w->stream));
+    SCK(cudaStreamSynchronize(w->stream));
+    *changed = w->h32[0];
+    return OTM_OK;
 }
 
 }  // extern "C"

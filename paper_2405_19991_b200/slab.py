@@ -263,6 +263,35 @@ class CudaSlabBackend:
         self._rc(self.lib.otm_slab_tensor_sums(self.ws, *dims, self._d3(scale), self._p(T), self._p(kap64), out))
         return np.array(out[:])
 
+    def filter(self, mode, dims, radius, material, inp, out, kap64=None):
+        self._sync_stream()
+        sums = (C.c_double * 3)()
+        self._rc(self.lib.otm_slab_filter(self.ws, mode, *dims, float(radius), float(material[0]),
+                                          float(material[1]), float(material[2]), self._p(inp), self._p(out),
+                                          self._p(kap64), sums if mode == 2 else None))
+        return np.array(sums[:]) if mode == 2 else None
+
+    def sensitivity(self, dims, n_total, material, T, rho_f, dG, sens_f):
+        self._sync_stream()
+        self._rc(self.lib.otm_slab_sensitivity(self.ws, *dims, float(n_total), float(material[0]),
+                                               float(material[1]), float(material[2]), self._p(T),
+                                               self._p(rho_f), (C.c_double * 6)(*[float(v) for v in dG]),
+                                               self._p(sens_f)))
+
+    def oc_sums(self, dims, n_total, oc, rho, sens, lams):
+        self._sync_stream()
+        out = (C.c_double * 32)()
+        self._rc(self.lib.otm_slab_oc_sums(self.ws, *dims, float(n_total), C.byref(oc), self._p(rho), self._p(sens),
+                                           len(lams), (C.c_double * len(lams))(*lams), out))
+        return np.array(out[:len(lams)])
+
+    def oc_apply(self, dims, n_total, oc, rho, sens, lam, rho_out):
+        self._sync_stream()
+        ch = C.c_double()
+        self._rc(self.lib.otm_slab_oc_apply(self.ws, *dims, float(n_total), C.byref(oc), self._p(rho),
+                                            self._p(sens), float(lam), self._p(rho_out), C.byref(ch)))
+        return ch.value
+
     # agglomerated coarse levels: the single-GPU hierarchy of that level
     def coarse_hierarchy(self, dims):
         from ._dev import Context
@@ -361,7 +390,6 @@ class SlabSolver:
             B.coarsen(top.dims, top.kap, s.ckap)
         full = self.comm.gather([s.ckap for s in self.slabs])
         B.coarse_build(self.coarse, full.contiguous())
-        self.warm = False
 
     def build_density(self, rho_f_interiors):
         """SIMP (element.py:91-94) on each slab's interior filtered density, then build."""
@@ -480,3 +508,189 @@ class SlabSolver:
     def fields(self):
         """The full 3-case temperature fields (gathered; for tests)."""
         return self.comm.gather([s.T for s in self.slabs])
+
+
+# --------------------------------------------------------------------------- design loop
+class SlabDesignRun:
+    """run_optimization (optimize.py:257-379, model 'oc' with the adaptive-volume
+    governor) on x-slabs: every field is a ghosted slab, every scalar all-reduced,
+    and the host-side logic (objective, governor, OC multiplier search, convergence
+    rule) replayed identically on every rank from identical sums."""
+
+    def __init__(self, config, comm, backend, rho_interiors):
+        from . import _lib
+        from .optimize import KIND_CODE, Model, _check_supported
+        _check_supported(config)
+        if config.model is not Model.ADAPTIVE_OC:
+            raise NotImplementedError("the slab design loop runs the reference default model 'oc'")
+        if config.symmetry == "central":
+            raise NotImplementedError("central symmetry mirrors across slabs; not supported on the slab path")
+        if not (1.0 <= config.filter.radius <= 2.0):
+            raise NotImplementedError("the slab filter needs radius <= 2 (one ghost plane)")
+        self.cfg = config
+        self.comm, self.B = comm, backend
+        mp = config.material
+        self.material = (mp.kappa0, mp.kappa_min, mp.penalty)
+        self.solver = SlabSolver(config.dims, comm, backend, kappa0=mp.kappa0, kappa_min=mp.kappa_min,
+                                 penalty=mp.penalty)
+        self.n = self.solver.n_total
+        self.lib = _lib.load()
+        self.cc = _lib.RunConfigC()
+        from .optimize import _run_config_c
+        self.cc = _run_config_c(config)
+        self.st = _lib.RunStateC()
+        self.lib.otm_run_init(C.byref(self.st), C.byref(self.cc))
+        self.kind = KIND_CODE[config.target.kind]
+        self.oc = config.oc._to_c()
+        f64 = backend.f64
+        self.parts = []
+        for s, r in zip(self.solver.slabs, rho_interiors):
+            nxl, ny, nz = s.levels[0].dims
+            p = _Lev()
+            p.rho = backend.zeros((nxl + 2, ny, nz), f64)
+            p.rho.narrow(0, 1, nxl).copy_(r)
+            p.rho_f = backend.zeros((nxl + 2, ny, nz), f64)
+            p.kap = backend.zeros((nxl + 2, ny, nz), f64)        # ghosted like every slab field
+            p.sens_f = backend.zeros((nxl + 2, ny, nz), f64)
+            p.sens = backend.zeros((nxl + 2, ny, nz), f64)
+            self.parts.append(p)
+        self.log = []
+        self.kappa = None
+
+    @property
+    def finished(self):
+        return bool(self.st.finished)
+
+    def _halo(self, get):
+        self.comm.halo([get(p) for p in self.parts])
+
+    def _sum(self, vals):
+        return self.comm.allreduce(vals)
+
+    def evaluate(self):
+        import time
+        from .optimize import IterationRecord
+        B, cfg, st = self.B, self.cfg, self.st
+        t0 = time.perf_counter()
+        d0 = self.solver.slabs[0].levels[0].dims
+        it = st.iter + 1
+        self._halo(lambda p: p.rho)
+        sums = self._sum([B.filter(2, d0, cfg.filter.radius, self.material, p.rho, p.rho_f, p.kap)
+                          for p in self.parts])
+        mean_rho, mean_rho_p, mean_rf = sums / self.n
+        self.solver.build_kappa([p.kap.narrow(0, 1, p.kap.shape[0] - 2) for p in self.parts])
+        self.solver.solve(tol=cfg.solver_tol, max_vcycles=cfg.max_vcycles)
+        kap = self.solver.tensor()
+        g = C.c_double()
+        dG = (C.c_double * 6)()
+        self.lib.otm_objective(self.kind, (C.c_double * 6)(*self.cc.target), (C.c_double * 6)(*kap), C.byref(g), dG)
+        g = g.value
+        for s, p in zip(self.solver.slabs, self.parts):
+            B.sensitivity(d0, self.n, self.material, s.T, p.rho_f, dG[:], p.sens_f)
+        self._halo(lambda p: p.sens_f)
+        for p in self.parts:
+            B.filter(1, d0, cfg.filter.radius, self.material, p.sens_f, p.sens)
+        st.iter = it
+        # convergence (optimize.py:327-345), as otm_run_step
+        if st.have_g_last and abs(g - st.g_last) < cfg.conv_threshold:
+            st.plateau += 1
+        else:
+            st.plateau = 0
+        st.g_last = g
+        st.have_g_last = 1
+        conv = False
+        if g <= 1e-12:
+            conv = True
+        elif st.plateau >= 3:
+            cd = st.gov.gap * st.gov.df if st.gov.reduced else float("inf")
+            conv = cd < 1e-4 and g <= st.gov.bound
+        st.converged = int(conv)
+        st.g, st.mean_rho, st.mean_rho_p = g, mean_rho, mean_rho_p
+        if conv or it == cfg.max_iter:
+            st.finished = 1
+        rec = IterationRecord(it, g, mean_rho, mean_rf, st.gov.vstar, self.solver.cycles,
+                              (time.perf_counter() - t0) * 1e3)
+        self.log.append(rec)
+        from .homogenize import ConductivityTensor
+        self.kappa = ConductivityTensor(np.array(kap))
+        return rec
+
+    # OC multiplier search (optimize.py:114-160): the reference's free step, bracket
+    # (l2 *= 4, at most 200 steps) and bisection with its two stopping rules, with the
+    # candidate means evaluated 32 at a time (bracket values, or the depth-5 subtree of
+    # bisection midpoints) -- the same multipliers the reference visits
+    def _means(self, lams):
+        d0 = self.solver.slabs[0].levels[0].dims
+        return self._sum([self.B.oc_sums(d0, self.n, self.oc, p.rho, p.sens, lams) for p in self.parts]) / self.n
+
+    def _search(self, V):
+        tol = self.oc.bisection_tol
+        lams = [0.0] + [4.0 ** k for k in range(31)]
+        m = self._means(lams)
+        if m[0] <= V:
+            return 0.0
+        l2, it, k0 = 1.0, 0, 1
+        while True:
+            hit = False
+            for k in range(k0, len(lams)):
+                if m[k] <= V:
+                    hit = True
+                    break
+                l2 *= 4.0
+                it += 1
+                if it >= 200:
+                    hit = True
+                    break
+            if hit:
+                break
+            lams = [l2 * 4.0 ** j for j in range(min(32, 200 - it))]
+            m = self._means(lams)
+            k0 = 0
+        l1 = 1e-30
+        while True:
+            lo, hi, mids = [l1], [l2], []
+            for i in range(31):
+                mid = 0.5 * (lo[i] + hi[i])
+                mids.append(mid)
+                if 2 * i + 2 < 31:
+                    lo += [lo[i], mid]
+                    hi += [mid, hi[i]]
+            m = self._means(mids)
+            node = 0
+            while True:
+                if not ((l2 - l1) / (l1 + l2) > 1e-13):
+                    return 0.5 * (l1 + l2)
+                if node >= 31:
+                    break
+                mid = 0.5 * (l1 + l2)
+                cur = m[node]
+                if cur > V:
+                    l1, node = mid, 2 * node + 2
+                else:
+                    l2, node = mid, 2 * node + 1
+                if abs(cur - V) <= tol:
+                    return 0.5 * (l1 + l2)
+
+    def _oc_update(self, V):
+        d0 = self.solver.slabs[0].levels[0].dims
+        lam = self._search(V)
+        changed = self._sum([np.array([self.B.oc_apply(d0, self.n, self.oc, p.rho, p.sens, lam, p.rho)])
+                             for p in self.parts])
+        return changed[0] > 0
+
+    def update(self):
+        st, cfg = self.st, self.cfg
+        vb = self.lib.otm_governor_update(C.byref(st.gov), st.g, st.mean_rho, st.mean_rho_p)
+        vb = min(vb, st.mean_rho + 0.5 * cfg.oc.step_limit)
+        if not self._oc_update(vb):
+            self._oc_update(st.mean_rho - 0.25 * cfg.oc.step_limit)
+
+    def step(self):
+        rec = self.evaluate()
+        if not self.finished:
+            self.update()
+        return rec
+
+    def density(self):
+        """The full density field (gathered)."""
+        return self.comm.gather([p.rho for p in self.parts])

@@ -41,3 +41,28 @@ def test_slab_solve_matches_single_gpu(dims, world):
     k = solver.tensor()
     assert np.abs(k - k_ref).max() <= 1e-9 * np.linalg.norm(k_ref)
     assert cycles > 0
+
+
+def test_slab_design_run_tracks_single_gpu():
+    """12 OC iterations of the slab design loop (2 slabs) against run_optimization."""
+    import torch
+    import paper_2405_19991_b200 as otm
+    from paper_2405_19991_b200.slab import CudaSlabBackend, LocalComm, SlabDesignRun
+    dims = (32, 32, 32)
+    target = otm.ObjectiveSpec("mse", otm.ConductivityTensor([0.1, 0.1, 0.1, 0, 0, 0]))
+    cfg = otm.RunConfig(dims=dims, target=target, init=otm.InitPattern("iwp", 0.3, seed=0), max_iter=12,
+                        conv_threshold=0.0, solver_tol=1e-10)
+    ref = otm.run_optimization(cfg)
+    seed = otm.init_density(dims, cfg.init).rho
+    W = 2
+    nxl = dims[0] // W
+    run = SlabDesignRun(cfg, LocalComm(W), CudaSlabBackend(3 * int(np.prod(dims))),
+                        [torch.from_numpy(np.ascontiguousarray(seed[r * nxl:(r + 1) * nxl])).cuda() for r in range(W)])
+    while not run.finished:
+        run.step()
+    assert len(run.log) == len(ref.log) == 12
+    for a, b in zip(run.log, ref.log):
+        assert abs(a.g - b.g) <= 1e-6 * max(abs(b.g), 1e-12)
+        assert abs(a.volfrac - b.volfrac) <= 1e-9
+    rho = run.density().cpu().numpy()
+    assert np.abs(rho - ref.field.rho).max() <= 1e-6
