@@ -212,6 +212,56 @@ class NumpySlabBackend:
         ke = K[1:-1]
         return np.array([float((ke * np.einsum("...a,...a->...", W[i], KW[j])).sum()) for i, j in O.PAIRS])
 
+    def filter(self, mode, dims, radius, material, inp, out, kap64=None):
+        offs, w = O.filter_taps(radius)
+        R = self._n(inp)
+        nxl = dims[0]
+        acc = np.zeros((nxl,) + R.shape[1:])
+        for o, wk in zip(offs, w):
+            dx, dy, dz = (-o[0], -o[1], -o[2]) if mode == 1 else o
+            acc += wk * _sh(R[1 + dx:1 + dx + nxl], dy, dz)
+        self._w(out, acc)
+        if mode != 2:
+            return None
+        k0, kmin, p = material
+        self._w(kap64, kmin + acc ** p * (k0 - kmin))
+        r = R[1:-1]
+        return np.array([r.sum(), (r ** p).sum(), acc.sum()])
+
+    def sensitivity(self, dims, n_total, material, T, rho_f, dG, sens_f):
+        k0, kmin, p = material
+        Tn = self._n(T)
+        nxl = dims[0]
+        Kt = O.voxel_template((1.0, 1.0, 1.0))
+        W = []
+        for i in range(3):
+            W.append(np.stack([O.CORNER_BITS[a, i] - _sh(Tn[i, 1 + _bits(a)[0]:1 + _bits(a)[0] + nxl],
+                                                          _bits(a)[1], _bits(a)[2]) for a in range(8)], axis=-1))
+        KW = [w @ Kt for w in W]
+        con = sum(dG[q] * np.einsum("...a,...a->...", W[i], KW[j]) for q, (i, j) in enumerate(O.PAIRS))
+        rf = self._n(rho_f)[1:-1]
+        self._w(sens_f, p * rf ** (p - 1.0) * (k0 - kmin) * con / n_total)
+
+    @staticmethod
+    def _cand(r, s, n_total, oc, lam):
+        desc = n_total * (-s)
+        lo = np.maximum(r - oc.step_limit, oc.min_density)
+        hi = np.minimum(r + oc.step_limit, 1.0)
+        if lam == 0.0:
+            return np.where(desc > 0, hi, np.where(desc < 0, lo, r))
+        return np.minimum(np.maximum(r * np.maximum(desc / lam, 1e-10) ** oc.damp, lo), hi)
+
+    def oc_sums(self, dims, n_total, oc, rho, sens, lams):
+        r, s = self._n(rho)[1:-1], self._n(sens)[1:-1]
+        return np.array([self._cand(r, s, n_total, oc, lam).sum() for lam in lams])
+
+    def oc_apply(self, dims, n_total, oc, rho, sens, lam, rho_out):
+        r, s = self._n(rho)[1:-1], self._n(sens)[1:-1]
+        new = self._cand(r, s, n_total, oc, lam)
+        changed = float((new != r).sum())
+        self._w(rho_out, new)
+        return changed
+
     # agglomerated levels: exact pinned pseudo-inverse G = P Z P at scale 1
     def coarse_hierarchy(self, dims):
         return {"dims": tuple(dims)}

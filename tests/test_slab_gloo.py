@@ -76,3 +76,53 @@ def test_distributed_slab_solve_matches_oracle(world, dims):
     for rank, cycles, k, T in res[1:]:
         assert cycles == res[0][1]
         assert np.array_equal(k, res[0][2])
+
+
+def _design_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import otm_oracle as O
+        from paper_2405_19991_b200.slab import DistComm, SlabDesignRun
+        from slab_numpy import NumpySlabBackend
+        import paper_2405_19991_b200 as otm
+        dims = (16, 8, 8)
+        cfg = otm.RunConfig(dims=dims, target=otm.ObjectiveSpec("mse", otm.ConductivityTensor([0.1, 0.1, 0.1, 0, 0, 0])),
+                            init=otm.InitPattern("iwp", 0.3, seed=0), max_iter=4, conv_threshold=0.0, solver_tol=1e-10)
+        seed = O.seed_density(dims, "iwp", 0.3)
+        nxl = dims[0] // world
+        run = SlabDesignRun(cfg, DistComm(), NumpySlabBackend(),
+                            [torch.from_numpy(np.ascontiguousarray(seed[rank * nxl:(rank + 1) * nxl]))])
+        while not run.finished:
+            run.step()
+        q.put((rank, [r.g for r in run.log], [r.volfrac for r in run.log], run.density().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_design_loop_matches_oracle():
+    """4 OC iterations of the slab design loop on 2 gloo ranks vs the CPU oracle run."""
+    from oracle import otm_oracle as O
+    dims = (16, 8, 8)
+    rho_ref, _, log_ref, _ = O.optimize(O.Run(dims=dims, target=[0.1, 0.1, 0.1, 0, 0, 0], init=("iwp", 0.3, 0),
+                                              max_iter=4, conv_threshold=0.0, solver_tol=1e-10))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_design_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=300) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, gs, vs, rho in out:
+        assert len(gs) == 4
+        for a, b in zip(gs, [r.g for r in log_ref]):
+            assert abs(a - b) <= 1e-6 * max(abs(b), 1e-12)
+        # the oracle returns the density evaluated last (no update after the final evaluation)
+        assert np.abs(rho - rho_ref).max() <= 1e-8
+    assert out[0][1] == out[1][1]
