@@ -39,6 +39,7 @@ CONFIGS = {
     "c2": dict(dims=(64, 64, 64), target=[0.3, 0.2, 0.1, 0, 0, 0], vf=0.5),
     "c3": dict(dims=(128, 128, 128), target=TARGET_C3, vf=0.5),
     "c4": dict(dims=(256, 256, 256), target=TARGET_C3, vf=0.5),
+    "c5": dict(dims=(512, 512, 512), target=[0.1, 0.1, 0.1, 0, 0, 0], vf=0.3),
 }
 METRIC = "seconds/structure at 128³; MG-PCG stencil GB/s vs B200 HBM peak"
 
@@ -297,6 +298,77 @@ def run_gpu(args):
         torch.distributed.destroy_process_group()
 
 
+
+# --------------------------------------------------------------------------- slab leg
+def run_slab(args):
+    """--mode slab: ONE structure decomposed into x-slabs over the ranks (strong
+    scaling; SlabDesignRun over NCCL, paper_2405_19991_b200/slab.py).  N=1 runs a
+    single slab in-process."""
+    import numpy as np
+    import torch
+
+    world, rank, local = dist_init()
+    torch.cuda.set_device(local)
+    import paper_2405_19991_b200 as otm
+    from paper_2405_19991_b200.slab import CudaSlabBackend, DistComm, LocalComm, SlabDesignRun
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = DistComm()
+    else:
+        comm = LocalComm(1)
+    name = args.config
+    dims = CONFIGS[name]["dims"]
+    seed = otm.init_density(dims, otm.InitPattern("iwp", CONFIGS[name]["vf"], seed=0)).rho
+    nxl = dims[0] // world
+    part = torch.from_numpy(np.ascontiguousarray(seed[rank * nxl:(rank + 1) * nxl])).cuda()
+    backend = CudaSlabBackend(3 * nxl * dims[1] * dims[2])
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def one_structure():
+        cfg = make_config(otm, name, args.iters, 0.0)
+        run = SlabDesignRun(cfg, comm, backend, [part])
+        while not run.finished:
+            run.step()
+        return run
+
+    for _ in range(args.warmup):
+        one_structure()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    total = 0.0
+    iters = []
+    for _ in range(args.steps):
+        barrier()
+        ev[0].record()
+        run = one_structure()
+        ev[1].record()
+        ev[1].synchronize()
+        total += ev[0].elapsed_time(ev[1])
+        iters.append(len(run.log))
+    barrier()
+    t_max = total
+    if world > 1:
+        tt = torch.tensor([total], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_max = float(tt.item())
+    value = t_max / 1e3 / args.steps
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "s/structure", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic (IWP seed from init_density)",
+                "config": {"workload": f"{name} {dims} target {CONFIGS[name]['target']}, {args.iters} OC iterations, "
+                                       f"one structure on {world} x-slabs",
+                           "mode": "slab", "iterations_per_step": iters,
+                           "parallelism": f"x-slabs x{world}, NCCL halos + all-reduce"}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -307,9 +379,13 @@ def main():
     ap.add_argument("--iters", type=int, default=500, help="OC iterations per structure")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-prof", action="store_true", help="no in-region kernel events")
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "slab"],
+                    help="N>1: independent structures per rank (default) or one structure on x-slabs")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.mode == "slab":
+        run_slab(args)
     else:
         run_gpu(args)
 
