@@ -8,6 +8,7 @@
 #include "otm_stencil4.cuh"
 #include "otm_stencil6.cuh"
 #include "otm_stencil8.cuh"
+#include "otm_stencil10.cuh"
 
 #ifndef OTM_MINB
 #define OTM_MINB 2   // min resident blocks of the fp32 fast-path stencils (register cap 128)
@@ -2288,6 +2289,54 @@ __global__ void __launch_bounds__(NZ / 2 * TY, 256 / (NZ / 2 * TY)) k8_spmv(Geo 
     }
 }
 
+// ---- k10: push x-march, operand consumed once per plane (otm_stencil10.cuh) ----
+template <int NZ, int TY>
+__global__ void __launch_bounds__(NZ / 2 * TY, 2) k10_smooth_res(Geo g, float s12, const __grid_constant__ K10Maps maps,
+                                                                float omega, float* z, float* res) {
+    K10Op<K10_SMOOTH, NZ, TY, false> op;
+    op.omega = omega; op.out0 = z; op.out1 = res; op.n = g.n;
+    march10(g, s12, maps, op);
+}
+
+template <bool DOT, int NZ, int TY>
+__global__ void __launch_bounds__(NZ / 2 * TY, 2) k10_jacobi(Geo g, float s12, const __grid_constant__ K10Maps maps,
+                                                            float omega, float* zout, double* partials,
+                                                            unsigned* counter, PcgScalars* sc) {
+    K10Op<K10_JACOBI, NZ, TY, DOT> op;
+    op.omega = omega; op.out0 = zout; op.out1 = nullptr; op.n = g.n;
+    op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
+    march10(g, s12, maps, op);
+    if (DOT) {
+        double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
+        if (reduce_finalize<3>(v3, partials, counter, sc->red)) {
+            for (int cc = 0; cc < 3; ++cc) {
+                const double rz = sc->red[cc];
+                sc->beta[cc] = (sc->first || sc->rz[cc] == 0.0) ? 0.0 : rz / sc->rz[cc];
+                sc->rz[cc] = rz;
+            }
+            sc->first = 0;
+        }
+    }
+}
+
+template <int NZ, int TY>
+__global__ void __launch_bounds__(NZ / 2 * TY, 2) k10_spmv(Geo g, float s12, const __grid_constant__ K10Maps maps,
+                                                          float* q, double* partials, unsigned* counter,
+                                                          PcgScalars* sc) {
+    K10Op<K10_SPMV, NZ, TY, true> op;
+    op.omega = 0.f; op.out0 = q; op.out1 = nullptr; op.n = g.n;
+    op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
+    march10(g, s12, maps, op);
+    double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
+    if (reduce_finalize<3>(v3, partials, counter, sc->red + 3)) {
+        for (int cc = 0; cc < 3; ++cc) {
+            const double pq = sc->red[3 + cc];
+            sc->pq[cc] = pq;
+            sc->alpha[cc] = (sc->active[cc] != 0.0 && pq > 0.0) ? sc->rz[cc] / pq : 0.0;
+        }
+    }
+}
+
 // ---- k9: k6 staging + x register window for the three cases (march8) ----
 template <int NZ>
 __global__ void __launch_bounds__(256, 1) k9_smooth_res(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
@@ -2529,8 +2578,8 @@ static dim3 k6_grid(K kernel, size_t smem, const Geo& g, int TY = 0) {
 }
 static dim3 k6_block(const Geo& g) { return dim3((unsigned)(g.nz / 2), (unsigned)k6_ty(g.nz), 1); }
 
-static int kernel_gen() {     // OTM_K=2..9 selects the fast-path stencil generation (default 8)
-    static const int k = getenv("OTM_K") ? atoi(getenv("OTM_K")) : 8;
+static int kernel_gen() {     // OTM_K=2..10 selects the fast-path stencil generation (default 10)
+    static const int k = getenv("OTM_K") ? atoi(getenv("OTM_K")) : 10;
     return k;
 }
 template <class K>
@@ -2991,8 +3040,97 @@ static void l8_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const
         default: if (half) CALL(256, 1); else CALL(256, 2); break;      \
         }                                                               \
     } while (0)
+// ---- k10 host side: 4-D (z, case, y, x) maps so one box moves the three cases ----
+static bool encode_map4(CUtensorMap* m, const float* base, const Geo& g, int box_rows) {
+    PFN_encodeTiled_t fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[4] = {(cuuint64_t)g.nz, 3, (cuuint64_t)g.ny, (cuuint64_t)g.nx};
+    const cuuint64_t strides[3] = {(cuuint64_t)g.n * 4, (cuuint64_t)g.nz * 4, (cuuint64_t)g.pl * 4};
+    const cuuint32_t box[4] = {(cuuint32_t)g.nz, 3, (cuuint32_t)box_rows, 1};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)base, dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+static int k10_ty(int nz) { return 512 / nz; }
+static bool k10_ok(const Geo& g, const LevelTemplate& lt) {
+    return lt.equal && (g.nz == 64 || g.nz == 128 || g.nz == 256) && g.ny % k10_ty(g.nz) == 0 &&
+           g.ny >= 2 * k10_ty(g.nz) && g.nx >= 2 && g.n >= 32768;
+}
+// op3: 3-case operand (halo), d: D^-1 (smooth_res: halo, jacobi: centre), f3: jacobi right-hand side
+static bool k10_maps(K10Maps& M, const Geo& g, const float* op3, const float* d, const float* f3, const float* kap) {
+    const int TY = k10_ty(g.nz);
+    bool ok = encode_map4(&M.op_full, op3, g, TY + 2) && encode_map4(&M.op_main, op3, g, TY) &&
+              encode_map4(&M.op_halo, op3, g, 1) && encode_map(&M.k_full, kap, g.nz, g.ny, g.nx, TY + 1) &&
+              encode_map(&M.k_main, kap, g.nz, g.ny, g.nx, TY) && encode_map(&M.k_halo, kap, g.nz, g.ny, g.nx, 1);
+    if (d)
+        ok = ok && encode_map(&M.d_full, d, g.nz, g.ny, g.nx, TY + 2) && encode_map(&M.d_main, d, g.nz, g.ny, g.nx, TY) &&
+             encode_map(&M.d_halo, d, g.nz, g.ny, g.nx, 1);
+    else
+        M.d_full = M.d_main = M.d_halo = M.k_main;
+    if (f3) ok = ok && encode_map4(&M.f_main, f3, g, TY);
+    else M.f_main = M.op_main;
+    return ok;
+}
+template <class K>
+static dim3 k10_grid(K kernel, size_t smem, const Geo& g, int TY) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, g.nz / 2 * TY, smem);
+    if (per_sm < 1) per_sm = 1;
+    const long long units = (long long)(g.ny / TY) * g.nx;
+    long long b = (long long)per_sm * sms;
+    if (b > units) b = units;
+    return dim3((unsigned)b, 1, 1);
+}
+template <int NZ>
+static void l10_smooth_res(cudaStream_t s, const Geo& g, float s12, const K10Maps& M, float omega, float* z,
+                           float* res) {
+    constexpr int TY = 512 / NZ;
+    const size_t sm = K10Geo<K10_SMOOTH, NZ, TY>::SMEM;
+    s3_attr(k10_smooth_res<NZ, TY>, sm);
+    launch_pdl(k10_smooth_res<NZ, TY>, k10_grid(k10_smooth_res<NZ, TY>, sm, g, TY), dim3(NZ / 2, TY), sm, s, g,
+               s12, M, omega, z, res);
+}
+template <bool DOT, int NZ>
+static void l10_jacobi(cudaStream_t s, const Geo& g, float s12, const K10Maps& M, float omega, float* zout,
+                       double* partials, unsigned* counter, PcgScalars* sc) {
+    constexpr int TY = 512 / NZ;
+    const size_t sm = K10Geo<K10_JACOBI, NZ, TY>::SMEM;
+    s3_attr(k10_jacobi<DOT, NZ, TY>, sm);
+    launch_pdl(k10_jacobi<DOT, NZ, TY>, k10_grid(k10_jacobi<DOT, NZ, TY>, sm, g, TY), dim3(NZ / 2, TY), sm, s, g,
+               s12, M, omega, zout, partials, counter, sc);
+}
+template <int NZ>
+static void l10_spmv(cudaStream_t s, const Geo& g, float s12, const K10Maps& M, float* q, Red& red,
+                     PcgScalars* sc) {
+    constexpr int TY = 512 / NZ;
+    const size_t sm = K10Geo<K10_SPMV, NZ, TY>::SMEM;
+    s3_attr(k10_spmv<NZ, TY>, sm);
+    launch_pdl(k10_spmv<NZ, TY>, k10_grid(k10_spmv<NZ, TY>, sm, g, TY), dim3(NZ / 2, TY), sm, s, g, s12, M, q,
+               red.partials, red.counter, sc);
+}
+#define OTM_K10_SWITCH(CALL)               \
+    do {                                   \
+        switch (g.nz) {                    \
+        case 64: CALL(64); break;          \
+        case 128: CALL(128); break;        \
+        default: CALL(256); break;         \
+        }                                  \
+    } while (0)
+
 void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* f,
                        const float* dinv, float omega, float* z, float* res) {
+    if (kernel_gen() == 10 && k10_ok(g, lt)) {
+        K10Maps M;
+        if (k10_maps(M, g, f, dinv, nullptr, kap)) {
+#define C_(NZ) l10_smooth_res<NZ>(s, g, (float)lt.s12, M, omega, z, res)
+            OTM_K10_SWITCH(C_);
+#undef C_
+            return;
+        }
+    }
     if (kernel_gen() == 7 && k6_ok(g, lt)) {
         K6Maps M;
         if (k6_maps(M, g, f, dinv, kap)) {
@@ -3101,6 +3239,21 @@ void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, co
 void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* z,
                    const float* f, const float* dinv, float omega, float* zout, bool dot, Red& red,
                    PcgScalars* sc) {
+    if (kernel_gen() == 10 && k10_ok(g, lt)) {
+        K10Maps M;
+        if (k10_maps(M, g, z, dinv, f, kap)) {
+            if (dot) {
+#define C_(NZ) l10_jacobi<true, NZ>(s, g, (float)lt.s12, M, omega, zout, red.partials, red.counter, sc)
+                OTM_K10_SWITCH(C_);
+#undef C_
+            } else {
+#define C_(NZ) l10_jacobi<false, NZ>(s, g, (float)lt.s12, M, omega, zout, nullptr, nullptr, sc)
+                OTM_K10_SWITCH(C_);
+#undef C_
+            }
+            return;
+        }
+    }
     if (kernel_gen() == 7 && k6_ok(g, lt)) {
         K6Maps M;
         if (k6_maps(M, g, z, nullptr, kap)) {
@@ -3285,6 +3438,15 @@ void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const 
 }
 void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* p,
                  float* q, Red& red, PcgScalars* sc) {
+    if (kernel_gen() == 10 && k10_ok(g, lt)) {
+        K10Maps M;
+        if (k10_maps(M, g, p, nullptr, nullptr, kap)) {
+#define C_(NZ) l10_spmv<NZ>(s, g, (float)lt.s12, M, q, red, sc)
+            OTM_K10_SWITCH(C_);
+#undef C_
+            return;
+        }
+    }
     if (kernel_gen() == 7 && k6_ok(g, lt)) {
         K6Maps M;
         if (k6_maps(M, g, p, nullptr, kap)) {
