@@ -87,6 +87,10 @@ struct otm_ctx {
     bool no_tail = getenv("OTM_TAIL_VERTS") == nullptr;
     long long tail_verts = getenv("OTM_TAIL_VERTS") ? atoll(getenv("OTM_TAIL_VERTS")) : 0;
     long long ctail_verts = getenv("OTM_CTAIL") ? atoll(getenv("OTM_CTAIL")) : 0;
+    // single-launch bottom (8^3, or 16^3 with OTM_VBOT=16 -- measured slower: one SM is
+    // too slow for the 16^3 stencils -- down to the 4^3 direct solve in shared memory);
+    // OTM_VBOT=0 off, OTM_VBOT=8 only from 8^3
+    int vbot_max = getenv("OTM_VBOT") ? atoi(getenv("OTM_VBOT")) : 8;
     bool warm = false;
     bool have_T = false;
     std::string err;
@@ -271,8 +275,20 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false, bool vonly = fa
     if (coop)
         for (int l = tl + 1; l < nl; ++l)
             if (!(ctx->L[l].cf[0] && ctx->L[l].cf[1] && ctx->L[l].cf[2])) tl = l;   // 3-D coarsening only
-    const bool use_tail = tl < nl - 1 && (coop || !ctx->no_tail);
-    const int top = use_tail ? tl : nl - 1;     // levels [0, top) are launched per level
+    bool use_tail = tl < nl - 1 && (coop || !ctx->no_tail);
+    // first level of the single-launch bottom: N^3 (N = 16 or 8) halving to 4^3, equal scales
+    int vb = -1;
+    for (int l = 1; l < nl && ctx->vbot_max >= 8 && !use_tail; ++l) {
+        const Geo& g = ctx->L[l].g;
+        const int N = g.nx;
+        if (!((N == 16 && ctx->vbot_max >= 16) || N == 8) || g.ny != N || g.nz != N) continue;
+        if (nl - l != (N == 16 ? 3 : 2)) continue;
+        bool ok = true;
+        for (int k = l; k < nl; ++k) ok = ok && ctx->L[k].lt.equal && ctx->L[k].g.nx == (N >> (k - l)) &&
+                                       ctx->L[k].g.ny == (N >> (k - l)) && ctx->L[k].g.nz == (N >> (k - l));
+        if (ok) { vb = l; break; }
+    }
+    const int top = use_tail ? tl : (vb > 0 ? vb : nl - 1);     // levels [0, top) are launched per level
     for (int l = 0; l < top; ++l) {
         LevelBuf& A = ctx->L[l];
         LevelBuf& B = ctx->L[l + 1];
@@ -302,6 +318,21 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false, bool vonly = fa
         } else {
             launch_vtail(s, ta);
         }
+        launches += 1;
+    } else if (vb > 0) {
+        VBotArgs va{};
+        va.nlev = nl - vb;
+        va.omega = om;
+        for (int k = 0; k < va.nlev; ++k) {
+            const LevelBuf& B = ctx->L[vb + k];
+            va.s12[k] = (float)B.lt.s12;
+            va.kap[k] = B.kap;
+            va.dinv[k] = B.dinv;
+        }
+        va.f0 = ctx->L[vb].f;
+        va.out0 = ctx->L[vb].res;
+        va.G = ctx->G;
+        launch_vbottom(s, ctx->L[vb].g.nx, va);
         launches += 1;
     } else {
         LevelBuf& C = ctx->L[nl - 1];
@@ -337,11 +368,11 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false, bool vonly = fa
     }
     if (vonly) return OTM_OK;                  // V-cycle only: z in L[0].res
     float* z0 = (nl == 1 || (use_tail && tl == 0)) ? ctx->L[0].z : ctx->L[0].res;
-    launch_pupd(s, ctx->g0.n, z0, ctx->p, ctx->sc);
+    launch_pupd(s, ctx->g0.n, z0, ctx->p, ctx->d, ctx->sc);
     if (prof) prof_record(ctx, kProfL0Stencil, 28.0 * n0, true, sl);
     launch_spmv(s, ctx->g0, ctx->L[0].lt, ctx->L[0].kap, ctx->p, ctx->q, ctx->red, ctx->sc);
     if (prof) prof_record(ctx, kProfL0Stencil, 0, false, sl);
-    launch_upd(s, ctx->g0.n, ctx->d, ctx->r, ctx->p, ctx->q, ctx->red, ctx->sc);
+    launch_upd(s, ctx->g0.n, ctx->r, ctx->q, ctx->red, ctx->sc);
     launches += 3;
     if (!in_loop) cudaMemcpyAsync(ctx->h, ctx->sc->flags, 8 * sizeof(double), cudaMemcpyDeviceToHost, s);
     ctx->launches_per_inner = launches + (in_loop ? 1 : 0);
@@ -837,7 +868,7 @@ int otm_solve(otm_ctx* ctx, const double* fext, double tol, int max_cycles, int*
             active_n = (int)(ctx->h[0] != 0.0) + (int)(ctx->h[1] != 0.0) + (int)(ctx->h[2] != 0.0);
             if (active_n == 0 || cycles >= max_cycles) break;
         }
-        launch_Tupd(s, 3 * n, ctx->T64, ctx->d);
+        launch_Tupd(s, n, ctx->T64, ctx->d, ctx->p, ctx->sc);
         ctx->launches++;
         ctx->stat_outer++;
         const double inner_rr[3] = {ctx->h[3], ctx->h[4], ctx->h[5]};

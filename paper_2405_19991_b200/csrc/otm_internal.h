@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include "otm_common.cuh"
+#include "otm_vbottom.cuh"
 
 namespace otm {
 
@@ -109,6 +110,7 @@ struct TailArgs {
 
 int stencil_chunks(const Geo& g, int* xb);
 void launch_vtail(cudaStream_t s, const TailArgs& a);
+void launch_vbottom(cudaStream_t s, int N, const VBotArgs& a);   // N = 16 or 8
 int launch_vtail_coop(cudaStream_t s, const TailArgs& a);   // 0 on success
 void set_k8_work(unsigned* p);   // work counter (2 unsigned, zeroed) used by the k8 kernels enqueued next
 
@@ -139,14 +141,13 @@ void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const 
                    PcgScalars* sc);
 void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* p,
                  float* q, Red& red, PcgScalars* sc);
-void launch_pupd(cudaStream_t s, long long n, const float* z, float* p, const PcgScalars* sc);
-void launch_upd(cudaStream_t s, long long n, float* d, float* r, const float* p, const float* q, Red& red,
-                PcgScalars* sc);
+void launch_pupd(cudaStream_t s, long long n, const float* z, float* p, float* d, const PcgScalars* sc);
+void launch_upd(cudaStream_t s, long long n, float* r, const float* q, Red& red, PcgScalars* sc);
 void launch_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* res, float* fc);
 void launch_prolong(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* zc, float* zf);
 void launch_loop_ctl(cudaStream_t s, PcgScalars* sc, unsigned long long handle);
 void launch_extrap(cudaStream_t s, long long n3, double* T, double* Tprev, double theta);
-void launch_Tupd(cudaStream_t s, long long n3, double* T, const float* d);
+void launch_Tupd(cudaStream_t s, long long n, double* T, const float* d, const float* p, const PcgScalars* sc);
 void launch_submean(cudaStream_t s, long long n, double* T, const double* sumT);
 void launch_tensor(cudaStream_t s, const Geo& g, const double* T, const double* kap, Red& red, double* out6);
 void launch_pair_energy(cudaStream_t s, const Geo& g, const double* T, double* E);

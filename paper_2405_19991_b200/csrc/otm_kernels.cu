@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <utility>
 #include <cstdlib>
+#include <cstdio>
 
 namespace otm {
 
@@ -875,29 +876,40 @@ __global__ void __launch_bounds__(128) k_spmv(Geo g, int xb, LevelTemplate lt, c
 }
 
 // p = z + beta p   (float4: n is a multiple of 4 on every level >= 4^3; scalar tail otherwise)
-__global__ void k_pupd(long long n, const float* __restrict__ z, float* __restrict__ p, const PcgScalars* sc) {
+// p = z + beta p, with the previous iteration's d += alpha p folded in (k_upd no
+// longer touches d: one read-modify-write pass less per PCG iteration; the last
+// iteration's alpha p goes into T in k_Tupd)
+__global__ void k_pupd(long long n, const float* __restrict__ z, float* __restrict__ p, float* __restrict__ d,
+                       const PcgScalars* sc) {
     pdl_wait();
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long n4 = n >> 2;
     const float b[3] = {(float)sc->beta[0], (float)sc->beta[1], (float)sc->beta[2]};
+    const float al[3] = {(float)sc->alpha[0], (float)sc->alpha[1], (float)sc->alpha[2]};
     if (i < n4) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const float4 zv = __ldg(reinterpret_cast<const float4*>(z + c * n) + i);
             float4* pp = reinterpret_cast<float4*>(p + c * n) + i;
+            float4* dp = reinterpret_cast<float4*>(d + c * n) + i;
             const float4 pv = *pp;
+            float4 dv = *dp;
+            dv.x += al[c] * pv.x; dv.y += al[c] * pv.y; dv.z += al[c] * pv.z; dv.w += al[c] * pv.w;
+            *dp = dv;
             *pp = make_float4(zv.x + b[c] * pv.x, zv.y + b[c] * pv.y, zv.z + b[c] * pv.z, zv.w + b[c] * pv.w);
         }
     }
     const long long t = (n4 << 2) + i;     // scalar tail
     if (i < (n & 3)) {
-        for (int c = 0; c < 3; ++c) p[c * n + t] = z[c * n + t] + b[c] * p[c * n + t];
+        for (int c = 0; c < 3; ++c) {
+            d[c * n + t] += al[c] * p[c * n + t];
+            p[c * n + t] = z[c * n + t] + b[c] * p[c * n + t];
+        }
     }
 }
 
-// d += alpha p ; r -= alpha q ; r.r partial sums -> convergence flags
-__global__ void __launch_bounds__(256) k_upd(long long n, float* __restrict__ d, float* __restrict__ r,
-                                             const float* __restrict__ p, const float* __restrict__ q,
+// r -= alpha q ; r.r partial sums -> convergence flags (d is updated by the next k_pupd)
+__global__ void __launch_bounds__(256) k_upd(long long n, float* __restrict__ r, const float* __restrict__ q,
                                              double* partials, unsigned* counter, PcgScalars* sc) {
     pdl_wait();
     double acc[3] = {0.0, 0.0, 0.0};
@@ -907,14 +919,10 @@ __global__ void __launch_bounds__(256) k_upd(long long n, float* __restrict__ d,
     if (i < n4) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const float4 pv = __ldg(reinterpret_cast<const float4*>(p + c * n) + i);
             const float4 qv = __ldg(reinterpret_cast<const float4*>(q + c * n) + i);
-            float4* dp = reinterpret_cast<float4*>(d + c * n) + i;
             float4* rp = reinterpret_cast<float4*>(r + c * n) + i;
-            float4 dv = *dp, rv = *rp;
-            dv.x += al[c] * pv.x; dv.y += al[c] * pv.y; dv.z += al[c] * pv.z; dv.w += al[c] * pv.w;
+            float4 rv = *rp;
             rv.x -= al[c] * qv.x; rv.y -= al[c] * qv.y; rv.z -= al[c] * qv.z; rv.w -= al[c] * qv.w;
-            *dp = dv;
             *rp = rv;
             acc[c] += ((double)rv.x * rv.x + (double)rv.y * rv.y) + ((double)rv.z * rv.z + (double)rv.w * rv.w);
         }
@@ -922,7 +930,6 @@ __global__ void __launch_bounds__(256) k_upd(long long n, float* __restrict__ d,
     if (i < (n & 3)) {
         const long long t = (n4 << 2) + i;
         for (int c = 0; c < 3; ++c) {
-            d[c * n + t] += al[c] * p[c * n + t];
             const float rn = r[c * n + t] - al[c] * q[c * n + t];
             r[c * n + t] = rn;
             acc[c] += (double)rn * rn;
@@ -1261,10 +1268,14 @@ __global__ void k_extrap(long long n3, double* __restrict__ T, double* __restric
     Tprev[i] = t;
 }
 
-// T += d (fp64 accumulation of the fp32 correction)
-__global__ void k_Tupd(long long n3, double* __restrict__ T, const float* __restrict__ d) {
+// T += d + alpha p (fp64 accumulation of the fp32 correction; alpha p of the last
+// PCG iteration has not been folded into d by a following k_pupd)
+__global__ void k_Tupd(long long n, double* __restrict__ T, const float* __restrict__ d, const float* __restrict__ p,
+                       const PcgScalars* __restrict__ sc) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n3) T[i] += (double)d[i];
+    if (i >= 3 * n) return;
+    const int c = (int)(i / n);
+    T[i] += (double)(d[i] + (float)sc->alpha[c] * p[i]);
 }
 
 // T -= mean(T) per case (solver.py:398)
@@ -2290,19 +2301,20 @@ __global__ void __launch_bounds__(NZ / 2 * TY, 256 / (NZ / 2 * TY)) k8_spmv(Geo 
 }
 
 // ---- k10: push x-march, operand consumed once per plane (otm_stencil10.cuh) ----
-template <int NZ, int TY>
-__global__ void __launch_bounds__(NZ / 2 * TY, 2) k10_smooth_res(Geo g, float s12, const __grid_constant__ K10Maps maps,
-                                                                float omega, float* z, float* res) {
-    K10Op<K10_SMOOTH, NZ, TY, false> op;
+// CPS = CTAs per SM the ring is sized for (TY rows x NZ/2 threads per CTA)
+template <int NZ, int TY, int CPS>
+__global__ void __launch_bounds__(NZ / 2 * TY, CPS) k10_smooth_res(Geo g, float s12, const __grid_constant__ K10Maps maps,
+                                                                  float omega, float* z, float* res) {
+    K10Op<K10_SMOOTH, NZ, TY, false, CPS> op;
     op.omega = omega; op.out0 = z; op.out1 = res; op.n = g.n;
     march10(g, s12, maps, op);
 }
 
-template <bool DOT, int NZ, int TY>
-__global__ void __launch_bounds__(NZ / 2 * TY, 2) k10_jacobi(Geo g, float s12, const __grid_constant__ K10Maps maps,
-                                                            float omega, float* zout, double* partials,
-                                                            unsigned* counter, PcgScalars* sc) {
-    K10Op<K10_JACOBI, NZ, TY, DOT> op;
+template <bool DOT, int NZ, int TY, int CPS>
+__global__ void __launch_bounds__(NZ / 2 * TY, CPS) k10_jacobi(Geo g, float s12, const __grid_constant__ K10Maps maps,
+                                                              float omega, float* zout, double* partials,
+                                                              unsigned* counter, PcgScalars* sc) {
+    K10Op<K10_JACOBI, NZ, TY, DOT, CPS> op;
     op.omega = omega; op.out0 = zout; op.out1 = nullptr; op.n = g.n;
     op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
     march10(g, s12, maps, op);
@@ -2319,11 +2331,11 @@ __global__ void __launch_bounds__(NZ / 2 * TY, 2) k10_jacobi(Geo g, float s12, c
     }
 }
 
-template <int NZ, int TY>
-__global__ void __launch_bounds__(NZ / 2 * TY, 2) k10_spmv(Geo g, float s12, const __grid_constant__ K10Maps maps,
-                                                          float* q, double* partials, unsigned* counter,
-                                                          PcgScalars* sc) {
-    K10Op<K10_SPMV, NZ, TY, true> op;
+template <int NZ, int TY, int CPS>
+__global__ void __launch_bounds__(NZ / 2 * TY, CPS) k10_spmv(Geo g, float s12, const __grid_constant__ K10Maps maps,
+                                                            float* q, double* partials, unsigned* counter,
+                                                            PcgScalars* sc) {
+    K10Op<K10_SPMV, NZ, TY, true, CPS> op;
     op.omega = 0.f; op.out0 = q; op.out1 = nullptr; op.n = g.n;
     op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
     march10(g, s12, maps, op);
@@ -2520,16 +2532,27 @@ static PFN_encodeTiled_t encode_fn() {
     }
     return fn;
 }
+// a failed tensor-map encode silently demotes the level stencils to the generic
+// kernels: say so once on stderr
+static bool tma_check(CUresult r, const char* what) {
+    static bool warned = false;
+    if (r != CUDA_SUCCESS && !warned) {
+        warned = true;
+        fprintf(stderr, "[otm] cuTensorMapEncodeTiled (%s) failed with CUresult %d: TMA stencils disabled\n", what,
+                (int)r);
+    }
+    return r == CUDA_SUCCESS;
+}
 static bool encode_map(CUtensorMap* m, const float* base, int nz, int ny, long long planes, int box_rows) {
     PFN_encodeTiled_t fn = encode_fn();
-    if (!fn) return false;
+    if (!fn) return tma_check(CUDA_ERROR_NOT_FOUND, "entry point");
     const cuuint64_t dims[3] = {(cuuint64_t)nz, (cuuint64_t)ny, (cuuint64_t)planes};
     const cuuint64_t strides[2] = {(cuuint64_t)nz * 4, (cuuint64_t)nz * ny * 4};
     const cuuint32_t box[3] = {(cuuint32_t)nz, (cuuint32_t)box_rows, 1};
     const cuuint32_t es[3] = {1, 1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, es,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    return tma_check(fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE), "3-d");
 }
 // arr3: 3-case array (3 nx planes), d1: optional D^-1 (nx planes), kap: factors
 static bool k6_maps(K6Maps& M, const Geo& g, const float* arr3, const float* d1, const float* kap, int TY = 0) {
@@ -3043,16 +3066,17 @@ static void l8_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const
 // ---- k10 host side: 4-D (z, case, y, x) maps so one box moves the three cases ----
 static bool encode_map4(CUtensorMap* m, const float* base, const Geo& g, int box_rows) {
     PFN_encodeTiled_t fn = encode_fn();
-    if (!fn) return false;
+    if (!fn) return tma_check(CUDA_ERROR_NOT_FOUND, "entry point");
     const cuuint64_t dims[4] = {(cuuint64_t)g.nz, 3, (cuuint64_t)g.ny, (cuuint64_t)g.nx};
     const cuuint64_t strides[3] = {(cuuint64_t)g.n * 4, (cuuint64_t)g.nz * 4, (cuuint64_t)g.pl * 4};
     const cuuint32_t box[4] = {(cuuint32_t)g.nz, 3, (cuuint32_t)box_rows, 1};
     const cuuint32_t es[4] = {1, 1, 1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)base, dims, strides, box, es,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    return tma_check(fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)base, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE), "4-d");
 }
-static int k10_ty(int nz) { return 512 / nz; }
+static int k10_ty_env();
+static int k10_ty(int nz) { return nz == 128 && (k10_ty_env() == 2 || k10_ty_env() == 8) ? k10_ty_env() : 512 / nz; }
 static bool k10_ok(const Geo& g, const LevelTemplate& lt) {
     return lt.equal && (g.nz == 64 || g.nz == 128 || g.nz == 256) && g.ny % k10_ty(g.nz) == 0 &&
            g.ny >= 2 * k10_ty(g.nz) && g.nx >= 2 && g.n >= 32768;
@@ -3084,40 +3108,46 @@ static dim3 k10_grid(K kernel, size_t smem, const Geo& g, int TY) {
     if (b > units) b = units;
     return dim3((unsigned)b, 1, 1);
 }
-template <int NZ>
+template <int NZ, int TY, int CPS>
 static void l10_smooth_res(cudaStream_t s, const Geo& g, float s12, const K10Maps& M, float omega, float* z,
                            float* res) {
-    constexpr int TY = 512 / NZ;
-    const size_t sm = K10Geo<K10_SMOOTH, NZ, TY>::SMEM;
-    s3_attr(k10_smooth_res<NZ, TY>, sm);
-    launch_pdl(k10_smooth_res<NZ, TY>, k10_grid(k10_smooth_res<NZ, TY>, sm, g, TY), dim3(NZ / 2, TY), sm, s, g,
-               s12, M, omega, z, res);
+    const size_t sm = K10Geo<K10_SMOOTH, NZ, TY, CPS>::SMEM;
+    s3_attr(k10_smooth_res<NZ, TY, CPS>, sm);
+    launch_pdl(k10_smooth_res<NZ, TY, CPS>, k10_grid(k10_smooth_res<NZ, TY, CPS>, sm, g, TY), dim3(NZ / 2, TY), sm,
+               s, g, s12, M, omega, z, res);
 }
-template <bool DOT, int NZ>
+template <bool DOT, int NZ, int TY, int CPS>
 static void l10_jacobi(cudaStream_t s, const Geo& g, float s12, const K10Maps& M, float omega, float* zout,
                        double* partials, unsigned* counter, PcgScalars* sc) {
-    constexpr int TY = 512 / NZ;
-    const size_t sm = K10Geo<K10_JACOBI, NZ, TY>::SMEM;
-    s3_attr(k10_jacobi<DOT, NZ, TY>, sm);
-    launch_pdl(k10_jacobi<DOT, NZ, TY>, k10_grid(k10_jacobi<DOT, NZ, TY>, sm, g, TY), dim3(NZ / 2, TY), sm, s, g,
-               s12, M, omega, zout, partials, counter, sc);
+    const size_t sm = K10Geo<K10_JACOBI, NZ, TY, CPS>::SMEM;
+    s3_attr(k10_jacobi<DOT, NZ, TY, CPS>, sm);
+    launch_pdl(k10_jacobi<DOT, NZ, TY, CPS>, k10_grid(k10_jacobi<DOT, NZ, TY, CPS>, sm, g, TY), dim3(NZ / 2, TY),
+               sm, s, g, s12, M, omega, zout, partials, counter, sc);
 }
-template <int NZ>
+template <int NZ, int TY, int CPS>
 static void l10_spmv(cudaStream_t s, const Geo& g, float s12, const K10Maps& M, float* q, Red& red,
                      PcgScalars* sc) {
-    constexpr int TY = 512 / NZ;
-    const size_t sm = K10Geo<K10_SPMV, NZ, TY>::SMEM;
-    s3_attr(k10_spmv<NZ, TY>, sm);
-    launch_pdl(k10_spmv<NZ, TY>, k10_grid(k10_spmv<NZ, TY>, sm, g, TY), dim3(NZ / 2, TY), sm, s, g, s12, M, q,
-               red.partials, red.counter, sc);
+    const size_t sm = K10Geo<K10_SPMV, NZ, TY, CPS>::SMEM;
+    s3_attr(k10_spmv<NZ, TY, CPS>, sm);
+    launch_pdl(k10_spmv<NZ, TY, CPS>, k10_grid(k10_spmv<NZ, TY, CPS>, sm, g, TY), dim3(NZ / 2, TY), sm, s, g, s12,
+               M, q, red.partials, red.counter, sc);
 }
-#define OTM_K10_SWITCH(CALL)               \
-    do {                                   \
-        switch (g.nz) {                    \
-        case 64: CALL(64); break;          \
-        case 128: CALL(128); break;        \
-        default: CALL(256); break;         \
-        }                                  \
+// tile rows per CTA (OTM_K10_TY: 2/4/8 at nz = 128, tuning) and CTAs per SM
+static int k10_ty_env() {
+    static const int v = getenv("OTM_K10_TY") ? atoi(getenv("OTM_K10_TY")) : 0;
+    return v;
+}
+#define OTM_K10_SWITCH(CALL)                                                   \
+    do {                                                                       \
+        switch (g.nz) {                                                        \
+        case 64: CALL(64, 8, 2); break;                                        \
+        case 128:                                                              \
+            if (k10_ty_env() == 2) CALL(128, 2, 4);                            \
+            else if (k10_ty_env() == 8) CALL(128, 8, 1);                       \
+            else CALL(128, 4, 2);                                              \
+            break;                                                             \
+        default: CALL(256, 2, 2); break;                                       \
+        }                                                                      \
     } while (0)
 
 void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* f,
@@ -3125,7 +3155,7 @@ void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, co
     if (kernel_gen() == 10 && k10_ok(g, lt)) {
         K10Maps M;
         if (k10_maps(M, g, f, dinv, nullptr, kap)) {
-#define C_(NZ) l10_smooth_res<NZ>(s, g, (float)lt.s12, M, omega, z, res)
+#define C_(NZ, TY, CPS) l10_smooth_res<NZ, TY, CPS>(s, g, (float)lt.s12, M, omega, z, res)
             OTM_K10_SWITCH(C_);
 #undef C_
             return;
@@ -3243,11 +3273,11 @@ void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const 
         K10Maps M;
         if (k10_maps(M, g, z, dinv, f, kap)) {
             if (dot) {
-#define C_(NZ) l10_jacobi<true, NZ>(s, g, (float)lt.s12, M, omega, zout, red.partials, red.counter, sc)
+#define C_(NZ, TY, CPS) l10_jacobi<true, NZ, TY, CPS>(s, g, (float)lt.s12, M, omega, zout, red.partials, red.counter, sc)
                 OTM_K10_SWITCH(C_);
 #undef C_
             } else {
-#define C_(NZ) l10_jacobi<false, NZ>(s, g, (float)lt.s12, M, omega, zout, nullptr, nullptr, sc)
+#define C_(NZ, TY, CPS) l10_jacobi<false, NZ, TY, CPS>(s, g, (float)lt.s12, M, omega, zout, nullptr, nullptr, sc)
                 OTM_K10_SWITCH(C_);
 #undef C_
             }
@@ -3441,7 +3471,7 @@ void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const fl
     if (kernel_gen() == 10 && k10_ok(g, lt)) {
         K10Maps M;
         if (k10_maps(M, g, p, nullptr, nullptr, kap)) {
-#define C_(NZ) l10_spmv<NZ>(s, g, (float)lt.s12, M, q, red, sc)
+#define C_(NZ, TY, CPS) l10_spmv<NZ, TY, CPS>(s, g, (float)lt.s12, M, q, red, sc)
             OTM_K10_SWITCH(C_);
 #undef C_
             return;
@@ -3548,14 +3578,13 @@ void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const fl
     const dim3 grid = stencil_grid(g, &xb);
     k_spmv<<<grid, 128, 0, s>>>(g, xb, lt, kap, p, q, red.partials, red.counter, sc);
 }
-void launch_pupd(cudaStream_t s, long long n, const float* z, float* p, const PcgScalars* sc) {
+void launch_pupd(cudaStream_t s, long long n, const float* z, float* p, float* d, const PcgScalars* sc) {
     const long long th = std::max<long long>(n >> 2, n & 3);
-    launch_pdl(k_pupd, nblk(th, 256), 256, 0, s, n, z, p, sc);
+    launch_pdl(k_pupd, nblk(th, 256), 256, 0, s, n, z, p, d, sc);
 }
-void launch_upd(cudaStream_t s, long long n, float* d, float* r, const float* p, const float* q, Red& red,
-                PcgScalars* sc) {
+void launch_upd(cudaStream_t s, long long n, float* r, const float* q, Red& red, PcgScalars* sc) {
     const long long th = std::max<long long>(n >> 2, n & 3);
-    launch_pdl(k_upd, nblk(th, 256), 256, 0, s, n, d, r, p, q, red.partials, red.counter, sc);
+    launch_pdl(k_upd, nblk(th, 256), 256, 0, s, n, r, q, red.partials, red.counter, sc);
 }
 void launch_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* res, float* fc) {
     if (cf[0] && cf[1] && cf[2]) {
@@ -3578,6 +3607,17 @@ void launch_loop_ctl(cudaStream_t s, PcgScalars* sc, unsigned long long handle) 
     k_loop_ctl<<<1, 1, 0, s>>>(sc, (cudaGraphConditionalHandle)handle);
 }
 void launch_vtail(cudaStream_t s, const TailArgs& a) { k_vtail<<<1, 1024, 0, s>>>(a); }
+void launch_vbottom(cudaStream_t s, int N, const VBotArgs& a) {
+    if (N == 16) {
+        const size_t sm = (size_t)vbot_smem_floats(16) * 4;
+        s3_attr(k_vbottom<16>, sm);
+        launch_pdl(k_vbottom<16>, dim3(1), dim3(1024), sm, s, a);
+    } else {
+        const size_t sm = (size_t)vbot_smem_floats(8) * 4;
+        s3_attr(k_vbottom<8>, sm);
+        launch_pdl(k_vbottom<8>, dim3(1), dim3(1024), sm, s, a);
+    }
+}
 int launch_vtail_coop(cudaStream_t s, const TailArgs& a) {
     static int blocks = 0;
     if (!blocks) {
@@ -3597,8 +3637,8 @@ int launch_vtail_coop(cudaStream_t s, const TailArgs& a) {
 void launch_extrap(cudaStream_t s, long long n3, double* T, double* Tprev, double theta) {
     k_extrap<<<nblk(n3, 256), 256, 0, s>>>(n3, T, Tprev, theta);
 }
-void launch_Tupd(cudaStream_t s, long long n3, double* T, const float* d) {
-    k_Tupd<<<nblk(n3, 256), 256, 0, s>>>(n3, T, d);
+void launch_Tupd(cudaStream_t s, long long n, double* T, const float* d, const float* p, const PcgScalars* sc) {
+    k_Tupd<<<nblk(3 * n, 256), 256, 0, s>>>(n, T, d, p, sc);
 }
 void launch_submean(cudaStream_t s, long long n, double* T, const double* sumT) {
     k_submean<<<nblk(3 * n, 256), 256, 0, s>>>(n, T, sumT);

@@ -38,7 +38,7 @@ struct K10Maps {
 
 enum { K10_SMOOTH = 0, K10_JACOBI = 1, K10_SPMV = 2 };
 
-template <int MODE, int NZ, int TY>
+template <int MODE, int NZ, int TY, int CPS = 2>
 struct K10Geo {
     static constexpr bool HAS_D = MODE == K10_SMOOTH;
     static constexpr bool HAS_C = MODE == K10_JACOBI;
@@ -49,7 +49,7 @@ struct K10Geo {
     static constexpr int DC = F + (HAS_C ? TY * 3 * NZ : 0);
     static constexpr int SLOT = DC + (HAS_C ? TY * NZ : 0);          // floats
     static constexpr int SLOT_BYTES = SLOT * 4;
-    static constexpr int BUDGET = 110 * 1024;                       // two CTAs per SM
+    static constexpr int BUDGET = (224 * 1024) / CPS - 2048;          // CPS CTAs per SM
     static constexpr int STAGES0 = BUDGET / (SLOT_BYTES + 8);
     static constexpr int STAGES = STAGES0 > 10 ? 10 : STAGES0;
     static constexpr int AHEAD = STAGES - 2;                          // slot refilled at step s held plane s-2
@@ -134,10 +134,10 @@ __device__ __forceinline__ float2 k10_x(const K10W& w, const K10Row (&R)[3], flo
     return fadd2(a, b);
 }
 
-template <int MODE_, int NZ_, int TY_, bool DOT = true>
+template <int MODE_, int NZ_, int TY_, bool DOT = true, int CPS = 2>
 struct K10Op {
     static constexpr int MODE = MODE_, NZ = NZ_, TY = TY_, H = NZ_ / 2;
-    using G = K10Geo<MODE, NZ, TY>;
+    using G = K10Geo<MODE, NZ, TY, CPS>;
     float omega;
     float* out0;          // smooth_res: z0 ; jacobi: z_out ; spmv: q
     float* out1;          // smooth_res: res
@@ -175,7 +175,7 @@ struct K10Op {
         o[H] = v.y;
     }
     // finished (K p) of case c at the pair, ctr = operand at the pair; Sp = slot of that plane
-    __device__ __forceinline__ void sink(const float* Sp, int c, long long v, int ty, int tx, float2 kt, float2 ctr) {
+    __device__ __forceinline__ void sink(const float* Sp, int c, int v, int ty, int tx, float2 kt, float2 ctr) {
         if (MODE == K10_SPMV) {
             put(out0 + c * n + v, kt);
             if (DOT) acc[c] += (double)ctr.x * (double)kt.x + (double)ctr.y * (double)kt.y;
@@ -192,6 +192,16 @@ struct K10Op {
             if (DOT) acc[c] += (double)f.x * (double)z0 + (double)f.y * (double)z1;
         }
     }
+};
+
+// Rotating per-thread state of the march: partial sums of out(p) and out(p+1),
+// the centre operand and 4 s12 K_v of out(p), the x-weights of element plane p-1.
+// Two instances alternate roles every plane (A -> B -> A), so the hot loop has no
+// register copies.
+struct K10State {
+    float2 Sc[3], Sn[3], C0[3];
+    float2 kv4s;
+    K10W w;
 };
 
 template <class Op>
@@ -221,7 +231,8 @@ __device__ __forceinline__ void march10(const Geo& g, float s12f, const K10Maps&
     const long long W = (long long)nty * g.nx;
     long long u = W * blockIdx.x / gridDim.x;
     const long long u1 = W * (blockIdx.x + 1) / gridDim.x;
-    int seq = 0;
+    int kc = 0;                                  // ring slot of the next plane to land
+    int ki = 0;                                  // ring slot of the next plane to issue
     while (u < u1) {
         const int yt = (int)(u / g.nx);
         const int x0 = (int)(u - (long long)yt * g.nx);
@@ -231,10 +242,11 @@ __device__ __forceinline__ void march10(const Geo& g, float s12f, const K10Maps&
         const int ym = y0 == 0 ? g.ny - 1 : y0 - 1;
         const int yp = y0 + TY == g.ny ? 0 : y0 + TY;
         const int nplanes = (x1 - x0) + 2;
-        auto issue = [&](int s) {
-            const int k = (seq + s) % STAGES;
+        int sissue = 0;                          // next segment plane to issue
+        auto issue_next = [&]() {                // thread 0 only
+            const int k = ki;
             float* S = smem + k * SLOT;
-            int x = x0 - 1 + s;
+            int x = x0 - 1 + sissue;
             x = x < 0 ? x + g.nx : (x >= g.nx ? x - g.nx : x);
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             mbar_expect_tx(bars + k, (unsigned)G::SLOT_BYTES);
@@ -258,80 +270,100 @@ __device__ __forceinline__ void march10(const Geo& g, float s12f, const K10Maps&
                 tma_load_4d(S + G::F, &maps.f_main, 0, 0, y0, x, bars + k);
                 tma_load_3d(S + G::DC, &maps.d_main, 0, y0, x, bars + k);
             }
+            ++sissue;
+            ki = ki + 1 == STAGES ? 0 : ki + 1;
         };
-        auto arrive = [&](int s) -> const float* {
-            const int k = (seq + s) % STAGES;
+        // wait for the next plane, retire the previous step everywhere, refill the
+        // slot of plane s-2; returns the landed slot, *prev = the slot before it
+        const float* Sprev = nullptr;
+        auto arrive = [&]() -> const float* {
+            const int k = kc;
             mbar_wait(bars + k, (phase_bits >> k) & 1u);
             phase_bits ^= 1u << k;
             __syncthreads();
-            if (tid == 0 && s + AHEAD < nplanes) issue(s + AHEAD);
+            if (tid == 0 && sissue < nplanes) issue_next();
+            kc = kc + 1 == STAGES ? 0 : kc + 1;
             return smem + k * SLOT;
         };
         if (tid == 0)
-            for (int s = 0; s < AHEAD && s < nplanes; ++s) issue(s);
-        const long long vrow = (long long)(y0 + ty) * NZ + cols.tx;
-        float2 Sc[3], Sn[3], C0[3];          // partial sums of out(s), out(s+1); centre of out(s)
-        float2 kv4s = f2(0.f, 0.f);          // 4 s12 K_v of out(s)
-        K10W wp;                             // x-weights of element plane s-1
-        // one landed plane: s = segment step, plane x0-1+s
-        auto step = [&](int s, bool doN, bool doQ, bool doP) {
-            const float* S = arrive(s);
-            K10W w;
-            k10_weights<NZ>(S + G::K, ty, cols, w);
+            while (sissue < AHEAD && sissue < nplanes) issue_next();
+        // output offsets of the thread's pair (32-bit: fields < 2^31 floats)
+        const int vrow = (y0 + ty) * NZ + cols.tx;
+        // one landed plane (segment step s, plane x0-1+s) moving state I -> O
+        auto step = [&](int s, const K10State& I, K10State& O, bool doN, bool doQ, bool doP) {
+            const float* S = arrive();
+            k10_weights<NZ>(S + G::K, ty, cols, O.w);
             op.plane(S, ty, cols);
             float2 q[2][2];
-            float2 kv4n = kv4s;
+            O.kv4s = I.kv4s;
             if (doQ) {
 #pragma unroll
                 for (int jj = 0; jj < 2; ++jj)
 #pragma unroll
-                    for (int kk = 0; kk < 2; ++kk) q[jj][kk] = fadd2(wp.c[jj][kk], w.c[jj][kk]);
-                kv4n = fmul2(fadd2(wp.kvh, w.kvh), s48);
+                    for (int kk = 0; kk < 2; ++kk) q[jj][kk] = fadd2(I.w.c[jj][kk], O.w.c[jj][kk]);
+                O.kv4s = fmul2(fadd2(I.w.kvh, O.w.kvh), s48);
             }
-            const float* Sp = smem + ((seq + s + STAGES - 1) % STAGES) * SLOT;
-            const long long vp = vrow + (long long)(x0 + s - 2) * g.pl;
+            const int vp = vrow + (x0 + s - 2) * g.pl;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 K10Row R[3];
                 op.rows(S, c, ty, cols, R);
                 if (doN) {
-                    const float2 tot = k10_x(wp, R, Sc[c]);
-                    op.sink(Sp, c, vp, ty, cols.tx, ffma2(kv4s, C0[c], fmul2(ns12, tot)), C0[c]);
+                    const float2 tot = k10_x(I.w, R, I.Sc[c]);
+                    op.sink(Sprev, c, vp, ty, cols.tx, ffma2(I.kv4s, I.C0[c], fmul2(ns12, tot)), I.C0[c]);
                 }
-                float2 nc = Sn[c];
+                float2 nc = I.Sn[c];
                 if (doQ) {
                     float2 a = ffma2(q[0][0], R[0].L, nc);
                     float2 b = fmul2(q[0][1], R[0].R);
                     a = ffma2(q[1][0], R[2].L, a);
                     b = ffma2(q[1][1], R[2].R, b);
                     nc = fadd2(a, b);
-                    C0[c] = R[1].C;
+                    O.C0[c] = R[1].C;
+                } else {
+                    O.C0[c] = I.C0[c];
                 }
-                Sc[c] = nc;
-                if (doP) Sn[c] = k10_x(w, R, f2(0.f, 0.f));
+                O.Sc[c] = nc;
+                O.Sn[c] = doP ? k10_x(O.w, R, f2(0.f, 0.f)) : f2(0.f, 0.f);
             }
-            kv4s = kv4n;
-            wp = w;
+            Sprev = S;
         };
+        K10State A, B;
         // prologue: plane x0-1 only starts out(x0)
         {
-            const float* S = arrive(0);
-            k10_weights<NZ>(S + G::K, ty, cols, wp);
+            const float* S = arrive();
+            k10_weights<NZ>(S + G::K, ty, cols, A.w);
             op.plane(S, ty, cols);
+            A.kv4s = f2(0.f, 0.f);
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 K10Row R[3];
                 op.rows(S, c, ty, cols, R);
-                Sn[c] = k10_x(wp, R, f2(0.f, 0.f));
+                A.Sn[c] = k10_x(A.w, R, f2(0.f, 0.f));
+                A.Sc[c] = f2(0.f, 0.f);
+                A.C0[c] = f2(0.f, 0.f);
             }
+            Sprev = S;
         }
         // step 1: out(x0) gets its centre plane
-        step(1, false, true, nplanes > 3);
-        // steady state: finish out(p-1), centre of out(p), start out(p+1) while it exists
-        for (int s = 2; s < nplanes - 1; ++s) step(s, true, true, s <= nplanes - 3);
-        // the last landed plane only finishes out(x1-1)
-        step(nplanes - 1, true, false, false);
-        seq = (seq + nplanes) % STAGES;
+        step(1, A, B, false, true, nplanes > 3);
+        // steady state, two planes per trip: finish out(p-1), centre of out(p), start out(p+1)
+        int s = 2;
+        for (; s + 1 < nplanes - 2; s += 2) {
+            step(s, B, A, true, true, true);
+            step(s + 1, A, B, true, true, true);
+        }
+        // tail: at most one more steady plane, then plane nplanes-2 (no start) and the last plane
+        if (s < nplanes - 2) {
+            step(s, B, A, true, true, true);
+            step(s + 1, A, B, true, true, false);
+            step(s + 2, B, A, true, false, false);
+        } else if (s == nplanes - 2) {
+            step(s, B, A, true, true, false);
+            step(s + 1, A, B, true, false, false);
+        } else {
+            step(s, B, A, true, false, false);
+        }
         __syncthreads();
         u += x1 - x0;
     }
