@@ -154,6 +154,20 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def traffic_bytes():
+    """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per launch of the
+    level-0 stencil class, mean over smooth_res / jacobi / spmv, from the committed
+    ncu --set full capture (profiles/r*_traffic.json, newest round); None without one."""
+    import glob
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r*_traffic.json")))
+    if not files:
+        return None
+    try:
+        return json.load(open(files[-1]))["mean_dram_bytes"]
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 # --------------------------------------------------------------------------- GPU leg
 def run_gpu(args):
     import numpy as np
@@ -276,7 +290,7 @@ def run_gpu(args):
                    "l2": "flushed (256 MB write) before every timed step",
                    "solver": "fp64 defect correction + fp32 MG-PCG (damped Jacobi V-cycle), tol 1e-6"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": None,
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic_bytes(),
                      "kernel": "level-0 stencils (smooth_res + jacobi + spmv), 3 load cases fp32",
                      "bytes_per_vertex": "44 (smooth_res, jacobi) / 28 (spmv)", "peak_kind": peak_kind,
                      "measured": "CUDA events on the library stream around every level-0 stencil launch, "
