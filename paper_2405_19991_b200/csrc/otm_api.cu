@@ -91,6 +91,11 @@ struct otm_ctx {
     // too slow for the 16^3 stencils -- down to the 4^3 direct solve in shared memory);
     // OTM_VBOT=0 off, OTM_VBOT=8 only from 8^3
     int vbot_max = getenv("OTM_VBOT") ? atoi(getenv("OTM_VBOT")) : 8;
+    // OTM_NOZ0=1: on k10 levels the pre-smoothing does not store z0 and the post-smoothing
+    // rebuilds it from f, D^-1 and P e (24 B/vertex less HBM traffic per V-cycle, but
+    // measured 11 us SLOWER per 128^3 V-cycle: the wider shared-memory slots halve the
+    // ring depth and add loads to a latency-bound kernel) -- opt-in experiment
+    bool keep_z0 = getenv("OTM_NOZ0") == nullptr;
     bool warm = false;
     bool have_T = false;
     std::string err;
@@ -289,12 +294,17 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false, bool vonly = fa
         if (ok) { vb = l; break; }
     }
     const int top = use_tail ? tl : (vb > 0 ? vb : nl - 1);     // levels [0, top) are launched per level
+    bool noz0[64] = {};
     for (int l = 0; l < top; ++l) {
         LevelBuf& A = ctx->L[l];
         LevelBuf& B = ctx->L[l + 1];
-        const double bsm = 44.0 * (double)A.g.n;
+        noz0[l] = !ctx->keep_z0 && B.cf[0] && B.cf[1] && B.cf[2] && k10_level(A.g, A.lt);
+        const double bsm = (noz0[l] ? 32.0 : 44.0) * (double)A.g.n;
         if (prof && l == 0) prof_record(ctx, kProfL0Stencil, bsm, true, sl);
-        launch_smooth_res(s, A.g, A.lt, A.kap, A.f, A.dinv, om, A.z, A.res);
+        if (!noz0[l] || !launch_smooth_res_nz(s, A.g, A.lt, A.kap, A.f, A.dinv, om, A.res)) {
+            noz0[l] = false;
+            launch_smooth_res(s, A.g, A.lt, A.kap, A.f, A.dinv, om, A.z, A.res);
+        }
         if (prof && l == 0) prof_record(ctx, kProfL0Stencil, 0, false, sl);
         launch_restrict(s, A.g, B.g, B.cf, A.res, B.f);
         vbytes += bsm + 12.0 * A.g.n + 12.0 * B.g.n;
@@ -342,10 +352,16 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false, bool vonly = fa
     for (int l = top - 1; l >= 0; --l) {
         LevelBuf& A = ctx->L[l];
         LevelBuf& B = ctx->L[l + 1];
-        launch_prolong(s, A.g, B.g, B.cf, B.res, A.z);
         const double bj = 44.0 * (double)A.g.n;
-        if (prof && l == 0) prof_record(ctx, kProfL0Stencil, bj, true, sl);
-        launch_jacobi(s, A.g, A.lt, A.kap, A.z, A.f, A.dinv, om, A.res, l == 0 && !vonly, ctx->red, ctx->sc);
+        if (noz0[l]) {
+            launch_prolong_assign(s, A.g, B.g, B.res, A.z);
+            if (prof && l == 0) prof_record(ctx, kProfL0Stencil, bj, true, sl);
+            launch_jacobi_p(s, A.g, A.lt, A.kap, A.z, A.f, A.dinv, om, A.res, l == 0 && !vonly, ctx->red, ctx->sc);
+        } else {
+            launch_prolong(s, A.g, B.g, B.cf, B.res, A.z);
+            if (prof && l == 0) prof_record(ctx, kProfL0Stencil, bj, true, sl);
+            launch_jacobi(s, A.g, A.lt, A.kap, A.z, A.f, A.dinv, om, A.res, l == 0 && !vonly, ctx->red, ctx->sc);
+        }
         if (prof && l == 0) prof_record(ctx, kProfL0Stencil, 0, false, sl);
         vbytes += 12.0 * B.g.n + 24.0 * A.g.n + bj;
         launches += 2;

@@ -139,6 +139,13 @@ void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, co
 void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* z,
                    const float* f, const float* dinv, float omega, float* zout, bool dot, Red& red,
                    PcgScalars* sc);
+bool k10_level(const Geo& g, const LevelTemplate& lt);
+bool launch_smooth_res_nz(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* f,
+                          const float* dinv, float omega, float* res);
+bool launch_jacobi_p(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* pe,
+                     const float* f, const float* dinv, float omega, float* zout, bool dot, Red& red,
+                     PcgScalars* sc);
+void launch_prolong_assign(cudaStream_t s, const Geo& f, const Geo& c, const float* zc, float* zf);
 void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* p,
                  float* q, Red& red, PcgScalars* sc);
 void launch_pupd(cudaStream_t s, long long n, const float* z, float* p, float* d, const PcgScalars* sc);

@@ -955,7 +955,7 @@ __global__ void __launch_bounds__(256) k_upd(long long n, float* __restrict__ r,
 template <bool CG>
 __device__ __forceinline__ float ldf(const float* p) { return CG ? __ldcg(p) : __ldg(p); }
 
-template <bool CG>
+template <bool CG, bool ASSIGN = false>
 __device__ __forceinline__ void prolong3b_body(const Geo& f, const Geo& c, const float* __restrict__ zc,
                                                float* __restrict__ zf, long long i) {
     const int cc = (int)(i / c.n);
@@ -995,19 +995,24 @@ __device__ __forceinline__ void prolong3b_body(const Geo& f, const Geo& c, const
             }
             add = make_float2(vz0, vz1);
             float2* dst = reinterpret_cast<float2*>(out + (long long)(2 * X + a2) * f.pl + (2 * Y + b2) * f.nz + 2 * Z);
-            float2 cur = CG ? __ldcg(dst) : *dst;
-            cur.x += add.x;
-            cur.y += add.y;
-            *dst = cur;
+            if (ASSIGN) {
+                *dst = add;                       // z = P zc (the k10 legs recompute z0 on the fly)
+            } else {
+                float2 cur = CG ? __ldcg(dst) : *dst;
+                cur.x += add.x;
+                cur.y += add.y;
+                *dst = cur;
+            }
         }
 }
 
+template <bool ASSIGN>
 __global__ void __launch_bounds__(256) k_prolong3b(Geo f, Geo c, const float* __restrict__ zc,
                                                    float* __restrict__ zf) {
     pdl_wait();
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 3 * c.n) return;
-    prolong3b_body<false>(f, c, zc, zf, i);
+    prolong3b_body<false, ASSIGN>(f, c, zc, zf, i);
 }
 
 // ---- small levels: one thread per (case, vertex), every load issued up front ----
@@ -2302,10 +2307,10 @@ __global__ void __launch_bounds__(NZ / 2 * TY, 256 / (NZ / 2 * TY)) k8_spmv(Geo 
 
 // ---- k10: push x-march, operand consumed once per plane (otm_stencil10.cuh) ----
 // CPS = CTAs per SM the ring is sized for (TY rows x NZ/2 threads per CTA)
-template <int NZ, int TY, int CPS>
+template <int NZ, int TY, int CPS, bool WZ>
 __global__ void __launch_bounds__(NZ / 2 * TY, CPS) k10_smooth_res(Geo g, float s12, const __grid_constant__ K10Maps maps,
                                                                   float omega, float* z, float* res) {
-    K10Op<K10_SMOOTH, NZ, TY, false, CPS> op;
+    K10Op<K10_SMOOTH, NZ, TY, false, CPS, WZ> op;
     op.omega = omega; op.out0 = z; op.out1 = res; op.n = g.n;
     march10(g, s12, maps, op);
 }
@@ -2315,6 +2320,27 @@ __global__ void __launch_bounds__(NZ / 2 * TY, CPS) k10_jacobi(Geo g, float s12,
                                                               float omega, float* zout, double* partials,
                                                               unsigned* counter, PcgScalars* sc) {
     K10Op<K10_JACOBI, NZ, TY, DOT, CPS> op;
+    op.omega = omega; op.out0 = zout; op.out1 = nullptr; op.n = g.n;
+    op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
+    march10(g, s12, maps, op);
+    if (DOT) {
+        double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
+        if (reduce_finalize<3>(v3, partials, counter, sc->red)) {
+            for (int cc = 0; cc < 3; ++cc) {
+                const double rz = sc->red[cc];
+                sc->beta[cc] = (sc->first || sc->rz[cc] == 0.0) ? 0.0 : rz / sc->rz[cc];
+                sc->rz[cc] = rz;
+            }
+            sc->first = 0;
+        }
+    }
+}
+
+template <bool DOT, int NZ, int TY, int CPS>
+__global__ void __launch_bounds__(NZ / 2 * TY, CPS) k10_jacobi_p(Geo g, float s12, const __grid_constant__ K10Maps maps,
+                                                                float omega, float* zout, double* partials,
+                                                                unsigned* counter, PcgScalars* sc) {
+    K10Op<K10_JACOBI_P, NZ, TY, DOT, CPS> op;
     op.omega = omega; op.out0 = zout; op.out1 = nullptr; op.n = g.n;
     op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
     march10(g, s12, maps, op);
@@ -3092,8 +3118,11 @@ static bool k10_maps(K10Maps& M, const Geo& g, const float* op3, const float* d,
              encode_map(&M.d_halo, d, g.nz, g.ny, g.nx, 1);
     else
         M.d_full = M.d_main = M.d_halo = M.k_main;
-    if (f3) ok = ok && encode_map4(&M.f_main, f3, g, TY);
-    else M.f_main = M.op_main;
+    if (f3)
+        ok = ok && encode_map4(&M.f_main, f3, g, TY) && encode_map4(&M.f_full, f3, g, TY + 2) &&
+             encode_map4(&M.f_halo, f3, g, 1);
+    else
+        M.f_main = M.f_full = M.f_halo = M.op_main;
     return ok;
 }
 template <class K>
@@ -3108,13 +3137,21 @@ static dim3 k10_grid(K kernel, size_t smem, const Geo& g, int TY) {
     if (b > units) b = units;
     return dim3((unsigned)b, 1, 1);
 }
-template <int NZ, int TY, int CPS>
+template <int NZ, int TY, int CPS, bool WZ = true>
 static void l10_smooth_res(cudaStream_t s, const Geo& g, float s12, const K10Maps& M, float omega, float* z,
                            float* res) {
     const size_t sm = K10Geo<K10_SMOOTH, NZ, TY, CPS>::SMEM;
-    s3_attr(k10_smooth_res<NZ, TY, CPS>, sm);
-    launch_pdl(k10_smooth_res<NZ, TY, CPS>, k10_grid(k10_smooth_res<NZ, TY, CPS>, sm, g, TY), dim3(NZ / 2, TY), sm,
-               s, g, s12, M, omega, z, res);
+    s3_attr(k10_smooth_res<NZ, TY, CPS, WZ>, sm);
+    launch_pdl(k10_smooth_res<NZ, TY, CPS, WZ>, k10_grid(k10_smooth_res<NZ, TY, CPS, WZ>, sm, g, TY),
+               dim3(NZ / 2, TY), sm, s, g, s12, M, omega, z, res);
+}
+template <bool DOT, int NZ, int TY, int CPS>
+static void l10_jacobi_p(cudaStream_t s, const Geo& g, float s12, const K10Maps& M, float omega, float* zout,
+                         double* partials, unsigned* counter, PcgScalars* sc) {
+    const size_t sm = K10Geo<K10_JACOBI_P, NZ, TY, CPS>::SMEM;
+    s3_attr(k10_jacobi_p<DOT, NZ, TY, CPS>, sm);
+    launch_pdl(k10_jacobi_p<DOT, NZ, TY, CPS>, k10_grid(k10_jacobi_p<DOT, NZ, TY, CPS>, sm, g, TY),
+               dim3(NZ / 2, TY), sm, s, g, s12, M, omega, zout, partials, counter, sc);
 }
 template <bool DOT, int NZ, int TY, int CPS>
 static void l10_jacobi(cudaStream_t s, const Geo& g, float s12, const K10Maps& M, float omega, float* zout,
@@ -3150,6 +3187,39 @@ static int k10_ty_env() {
         }                                                                      \
     } while (0)
 
+// Level legs without a stored z0 (k10 levels only, see K10_JACOBI_P):
+//   down: res = f - K (w D^-1 f)          [launch_smooth_res_nz]
+//   up:   z = P e (assign)                 [launch_prolong_assign]
+//         zout = z' + w D^-1 (f - K z'),  z' = w D^-1 f + z   [launch_jacobi_p]
+bool k10_level(const Geo& g, const LevelTemplate& lt) { return kernel_gen() == 10 && k10_ok(g, lt); }
+bool launch_smooth_res_nz(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* f,
+                          const float* dinv, float omega, float* res) {
+    K10Maps M;
+    if (!k10_level(g, lt) || !k10_maps(M, g, f, dinv, nullptr, kap)) return false;
+#define C_(NZ, TY, CPS) l10_smooth_res<NZ, TY, CPS, false>(s, g, (float)lt.s12, M, omega, nullptr, res)
+    OTM_K10_SWITCH(C_);
+#undef C_
+    return true;
+}
+bool launch_jacobi_p(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* pe,
+                     const float* f, const float* dinv, float omega, float* zout, bool dot, Red& red,
+                     PcgScalars* sc) {
+    K10Maps M;
+    if (!k10_level(g, lt) || !k10_maps(M, g, pe, dinv, f, kap)) return false;
+    if (dot) {
+#define C_(NZ, TY, CPS) l10_jacobi_p<true, NZ, TY, CPS>(s, g, (float)lt.s12, M, omega, zout, red.partials, red.counter, sc)
+        OTM_K10_SWITCH(C_);
+#undef C_
+    } else {
+#define C_(NZ, TY, CPS) l10_jacobi_p<false, NZ, TY, CPS>(s, g, (float)lt.s12, M, omega, zout, nullptr, nullptr, sc)
+        OTM_K10_SWITCH(C_);
+#undef C_
+    }
+    return true;
+}
+void launch_prolong_assign(cudaStream_t s, const Geo& f, const Geo& c, const float* zc, float* zf) {
+    launch_pdl(k_prolong3b<true>, nblk(3 * c.n, 256), 256, 0, s, f, c, zc, zf);
+}
 void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* f,
                        const float* dinv, float omega, float* z, float* res) {
     if (kernel_gen() == 10 && k10_ok(g, lt)) {
@@ -3598,7 +3668,7 @@ void launch_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3]
 }
 void launch_prolong(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* zc, float* zf) {
     if (cf[0] && cf[1] && cf[2]) {
-        launch_pdl(k_prolong3b, nblk(3 * c.n, 256), 256, 0, s, f, c, zc, zf);
+        launch_pdl(k_prolong3b<false>, nblk(3 * c.n, 256), 256, 0, s, f, c, zc, zf);
         return;
     }
     k_prolong<<<nblk(f.n, 256), 256, 0, s>>>(f, c, cf[0], cf[1], cf[2], zc, zf);
