@@ -23,6 +23,7 @@ Multi-GPU (torchrun): every rank designs its own structure (replicas; the slab
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -65,6 +66,8 @@ class Clocks:
         self.proc = None
 
     def start(self):
+        if os.environ.get("OTM_BENCH_NOCLK"):
+            return
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
@@ -219,6 +222,8 @@ def run_gpu(args):
     iters_done = []
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     total_ms = 0.0
+    gc.collect()
+    gc.disable()                         # as timeit does: no collector pauses inside timed steps
     for _ in range(args.steps):
         flush.fill_(1.0)                 # evict L2 between steps
         barrier()
@@ -231,6 +236,7 @@ def run_gpu(args):
         total_ms += ms
         iters_done.append(len(run.log))
     barrier()
+    gc.enable()
     clk = clocks.stop()
     launches = lib.otm_launch_count(ctx.h) - launches0
     # max over ranks
@@ -262,6 +268,8 @@ def run_gpu(args):
     achieved = l0["gbs"]
     # ---- e2e through the public API with host buffers ----
     e2e_ms = []
+    gc.collect()
+    gc.disable()
     for s in range(3):                                   # first call includes context setup
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -270,6 +278,7 @@ def run_gpu(args):
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
         assert isinstance(res.field.rho, np.ndarray)
+    gc.enable()
     e2e = statistics.median(e2e_ms) / 1e3
     if world > 1:
         tt = torch.tensor([e2e], device="cuda", dtype=torch.float64)
@@ -286,7 +295,8 @@ def run_gpu(args):
         "data": "synthetic (IWP seed from init_density, vf 0.5)",
         "config": {"workload": f"{name} {dims} target {CONFIGS[name]['target']} (k11,k22,k33,k12,k23,k13), "
                                f"vf {CONFIGS[name]['vf']}, {args.iters} OC iterations per structure",
-                   "iterations_per_step": iters_done, "parallelism": f"replicas x{world}",
+                   "iterations_per_step": iters_done, "step_ms": [round(x, 2) for x in step_ms],
+                   "parallelism": f"replicas x{world}",
                    "l2": "flushed (256 MB write) before every timed step",
                    "solver": "fp64 defect correction + fp32 MG-PCG (damped Jacobi V-cycle), tol 1e-6"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
