@@ -98,6 +98,7 @@ struct otm_ctx {
     bool keep_z0 = getenv("OTM_NOZ0") == nullptr;
     bool warm = false;
     bool have_T = false;
+    bool oc_pending = false;     // a cooperative OC search result still in flight to h + 384
     std::string err;
     size_t bytes = 0;
     long long launches = 0;
@@ -668,9 +669,15 @@ int otm_create(otm_ctx** out, int nx, int ny, int nz, const otm_params* pin) {
     return OTM_OK;
 }
 
+static void oc_settle(otm_ctx* ctx);
+
 int otm_destroy(otm_ctx* ctx) {
     if (!ctx) return OTM_OK;
     set_k8_work(nullptr);                 // re-set by the next enqueue of any context
+    if (ctx->oc_pending) {
+        cudaStreamSynchronize(ctx->stream);
+        oc_settle(ctx);
+    }
     if (getenv("OTM_STATS") && ctx->stat_solves)
         fprintf(stderr, "[otm] stats: solves %lld outer %lld inner %lld (%.2f inner/solve); oc %lld passes %lld "
                 "(%.2f/update) retried %lld\n", ctx->stat_solves, ctx->stat_outer, ctx->stat_inner,
@@ -1024,9 +1031,26 @@ int otm_means(otm_ctx* ctx, const double* rho, double p, double out[2]) {
 
 // Cooperative single-launch search (k_oc_coop); V_retry = NaN disables the
 // frozen-state retry.  Returns OTM_ECUDA if the cooperative launch is unavailable.
+static void oc_account(otm_ctx* ctx, const OcCtl& fin) {
+    if (ctx->prof) ctx->prof_bytes[kProfOC] += (16.0 * fin.passes + 24.0 * (1 + fin.retried)) * ctx->g0.n;
+    ctx->stat_oc++;
+    ctx->stat_oc_passes += fin.passes;
+    ctx->stat_oc_retry += fin.retried;
+    static const bool debug = getenv("OTM_DEBUG") != nullptr;
+    if (debug) fprintf(stderr, "[otm] oc: passes %d retried %d lam %.6e active %d\n", fin.passes, fin.retried,
+                       fin.lam, fin.active);
+}
+// statistics of a search whose result was not waited for (read at the next host sync)
+static void oc_settle(otm_ctx* ctx) {
+    if (!ctx->oc_pending) return;
+    ctx->oc_pending = false;
+    OcCtl fin;
+    std::memcpy(&fin, ctx->h + 384, sizeof fin);
+    oc_account(ctx, fin);
+}
 static int oc_search_coop(otm_ctx* ctx, const double* rho, const double* sens, double V, double V_retry,
                           const otm_oc_params* pp, double* rho_out, double* lam_out, int* active_out,
-                          int* changed_out, int* retried_out) {
+                          int* changed_out, int* retried_out, bool wait = true) {
     cudaStream_t s = ctx->stream;
     OcArgs a;
     a.step = pp->step_limit;
@@ -1049,21 +1073,21 @@ static int oc_search_coop(otm_ctx* ctx, const double* rho, const double* sens, d
         }
     }
     ctx->launches++;
+    if (!wait && !ctx->prof) {
+        // the design loop does not need the result on the host: no round trip here
+        CK(cudaMemcpyAsync(ctx->h + 384, ctx->ocl, sizeof init, cudaMemcpyDeviceToHost, s));
+        ctx->oc_pending = true;
+        return OTM_OK;
+    }
     CK(cudaMemcpyAsync(ctx->h + 256, ctx->ocl, sizeof init, cudaMemcpyDeviceToHost, s));
     CK(stream_wait(s));
     OcCtl fin;
     std::memcpy(&fin, ctx->h + 256, sizeof fin);
-    if (ctx->prof) ctx->prof_bytes[kProfOC] += (16.0 * fin.passes + 24.0 * (1 + fin.retried)) * ctx->g0.n;
-    ctx->stat_oc++;
-    ctx->stat_oc_passes += fin.passes;
-    ctx->stat_oc_retry += fin.retried;
+    oc_account(ctx, fin);
     if (lam_out) *lam_out = fin.lam;
     if (active_out) *active_out = fin.active;
     if (changed_out) *changed_out = fin.changed;
     if (retried_out) *retried_out = fin.retried;
-    static const bool debug = getenv("OTM_DEBUG") != nullptr;
-    if (debug) fprintf(stderr, "[otm] oc: passes %d retried %d lam %.6e active %d\n", fin.passes, fin.retried,
-                       fin.lam, fin.active);
     return OTM_OK;
 }
 
@@ -1253,13 +1277,13 @@ int otm_run_step(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, dou
     if (rc) return rc;
     st->warm = 1;
     double kap[6];
+    // the filter sums ride on the tensor readback (one host round trip)
+    CK(cudaMemcpyAsync(ctx->h + 512, ctx->scal + 56, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
     rc = otm_tensor(ctx, kap);
     if (rc) return rc;
-    // the filter sums were synchronised with the tensor readback
-    CK(cudaMemcpyAsync(ctx->h, ctx->scal + 56, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK(stream_wait(s));
-    const double mean_rho = ctx->h[0] / (double)n, mean_rho_p = ctx->h[1] / (double)n,
-                 mean_rf = ctx->h[2] / (double)n;
+    oc_settle(ctx);
+    const double mean_rho = ctx->h[512] / (double)n, mean_rho_p = ctx->h[513] / (double)n,
+                 mean_rf = ctx->h[514] / (double)n;
     double g, dG[6];
     if (otm_objective(cfg->objective, cfg->target, kap, &g, dG)) return fail(ctx, OTM_EINVAL, "objective failed");
     rc = otm_sensitivity(ctx, dG, ctx->sensf);
@@ -1272,7 +1296,7 @@ int otm_run_step(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, dou
         ctx->launches++;
     }
     if (sens_out) CK(cudaMemcpyAsync(sens_out, ctx->sens, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    CK(stream_wait(s));
+    CKL();                                  // outputs are stream-ordered on the context stream
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     rec->iter = it;
     rec->g = g;
@@ -1318,8 +1342,8 @@ int otm_run_update(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, d
         // governor + OC step + frozen-state retry in one cooperative launch
         double vb = otm_governor_update(&st->gov, st->g, mean_rho, st->mean_rho_p);
         vb = std::min(vb, mean_rho + 0.5 * cfg->oc.step_limit);
-        rc = oc_search_coop(ctx, rho, ctx->sens, vb, mean_rho - 0.25 * cfg->oc.step_limit, &cfg->oc, rho, &lam,
-                            &active, &changed, nullptr);
+        rc = oc_search_coop(ctx, rho, ctx->sens, vb, mean_rho - 0.25 * cfg->oc.step_limit, &cfg->oc, rho, nullptr,
+                            nullptr, nullptr, nullptr, false);
         if (rc == OTM_OK) {
             if (cfg->symmetry == 1) {
                 launch_symmetrize(ctx->stream, ctx->g0, rho);
