@@ -91,6 +91,11 @@ struct otm_ctx {
     // too slow for the 16^3 stencils -- down to the 4^3 direct solve in shared memory);
     // OTM_VBOT=0 off, OTM_VBOT=8 only from 8^3
     int vbot_max = getenv("OTM_VBOT") ? atoi(getenv("OTM_VBOT")) : 8;
+    // OTM_VT32=1: the 32^3 -> 4^3 tail as one 16-CTA cluster launch (otm_vtail32.cuh).
+    // Correct (same operator, tests/test_preconditioner_gpu.py) but measured SLOWER:
+    // 62 vs 45 us per 64^3 V-cycle -- 16 SMs run what the per-level launches spread
+    // over 148, and the bottom on CTA 0 idles the other 15 at the cluster barriers.
+    bool vt32 = getenv("OTM_VT32") && atoi(getenv("OTM_VT32")) == 1;
     // OTM_NOZ0=1: on k10 levels the pre-smoothing does not store z0 and the post-smoothing
     // rebuilds it from f, D^-1 and P e (24 B/vertex less HBM traffic per V-cycle, but
     // measured 11 us SLOWER per 128^3 V-cycle: the wider shared-memory slots halve the
@@ -294,7 +299,18 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false, bool vonly = fa
                                        ctx->L[k].g.ny == (N >> (k - l)) && ctx->L[k].g.nz == (N >> (k - l));
         if (ok) { vb = l; break; }
     }
-    const int top = use_tail ? tl : (vb > 0 ? vb : nl - 1);     // levels [0, top) are launched per level
+    // first level of the cluster tail: 32^3 halving to 4^3 (4 levels), equal scales, not level 0
+    int vt = -1;
+    if (ctx->vt32 && !use_tail && nl >= 5) {
+        const int l = nl - 4;
+        bool ok = true;
+        for (int k = l; k < nl; ++k)
+            ok = ok && ctx->L[k].lt.equal && ctx->L[k].g.nx == (32 >> (k - l)) && ctx->L[k].g.ny == (32 >> (k - l)) &&
+                 ctx->L[k].g.nz == (32 >> (k - l));
+        if (ok) vt = l;
+    }
+    int top = use_tail ? tl : (vb > 0 ? vb : nl - 1);     // levels [0, top) are launched per level
+    if (vt > 0) top = vt;
     bool noz0[64] = {};
     for (int l = 0; l < top; ++l) {
         LevelBuf& A = ctx->L[l];
@@ -330,6 +346,22 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false, bool vonly = fa
             launch_vtail(s, ta);
         }
         launches += 1;
+    } else if (vt > 0 && launch_vtail32(s, [&] {
+                   VTailArgs a{};
+                   a.omega = om;
+                   for (int k = 0; k < 4; ++k) a.s12[k] = (float)ctx->L[vt + k].lt.s12;
+                   for (int k = 0; k < 3; ++k) {
+                       a.kap[k] = ctx->L[vt + k].kap;
+                       a.dinv[k] = ctx->L[vt + k].dinv;
+                   }
+                   a.f32 = ctx->L[vt].f;
+                   a.out32 = ctx->L[vt].res;
+                   a.G = ctx->G;
+                   return a;
+               }())) {
+        launches += 1;
+    } else if (vt > 0) {
+        return fail(ctx, OTM_ECUDA, "cluster tail launch failed (unset OTM_VT32)");
     } else if (vb > 0) {
         VBotArgs va{};
         va.nlev = nl - vb;

@@ -6,6 +6,7 @@
 
 #include "otm_common.cuh"
 #include "otm_vbottom.cuh"
+#include "otm_vtail32.cuh"
 
 namespace otm {
 
@@ -110,7 +111,8 @@ struct TailArgs {
 
 int stencil_chunks(const Geo& g, int* xb);
 void launch_vtail(cudaStream_t s, const TailArgs& a);
-void launch_vbottom(cudaStream_t s, int N, const VBotArgs& a);   // N = 16 or 8
+void launch_vbottom(cudaStream_t s, int N, const VBotArgs& a);
+bool launch_vtail32(cudaStream_t s, const VTailArgs& a);   // false: unavailable, nothing launched   // N = 16 or 8
 int launch_vtail_coop(cudaStream_t s, const TailArgs& a);   // 0 on success
 void set_k8_work(unsigned* p);   // work counter (2 unsigned, zeroed) used by the k8 kernels enqueued next
 

@@ -9,6 +9,7 @@
 #include "otm_stencil6.cuh"
 #include "otm_stencil8.cuh"
 #include "otm_stencil10.cuh"
+#include "otm_vtail32.cuh"
 
 #ifndef OTM_MINB
 #define OTM_MINB 2   // min resident blocks of the fp32 fast-path stencils (register cap 128)
@@ -3677,6 +3678,35 @@ void launch_loop_ctl(cudaStream_t s, PcgScalars* sc, unsigned long long handle) 
     k_loop_ctl<<<1, 1, 0, s>>>(sc, (cudaGraphConditionalHandle)handle);
 }
 void launch_vtail(cudaStream_t s, const TailArgs& a) { k_vtail<<<1, 1024, 0, s>>>(a); }
+// one 16-CTA cluster (non-portable size); false if the device cannot schedule it
+bool launch_vtail32(cudaStream_t s, const VTailArgs& a) {
+    static int ok = -1;
+    const size_t sm = (size_t)VtLay::FLOATS * 4;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kVtCtas);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kVtCtas;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    if (ok < 0) {
+        ok = cudaFuncSetAttribute(k_vtail32<>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+             cudaFuncSetAttribute(k_vtail32<>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) == cudaSuccess;
+        int nclusters = 0;
+        if (ok) ok = cudaOccupancyMaxActiveClusters(&nclusters, (void*)k_vtail32<>, &cfg) == cudaSuccess && nclusters > 0;
+        cudaGetLastError();
+        if (!ok) fprintf(stderr, "[otm] 16-CTA cluster tail unavailable: per-level launches\n");
+    }
+    if (!ok) return false;
+    return cudaLaunchKernelEx(&cfg, k_vtail32<>, a) == cudaSuccess;
+}
 void launch_vbottom(cudaStream_t s, int N, const VBotArgs& a) {
     if (N == 16) {
         const size_t sm = (size_t)vbot_smem_floats(16) * 4;

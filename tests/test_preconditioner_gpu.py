@@ -5,8 +5,8 @@ PCG relies on, at BASELINE sizes:
 
   * symmetry:   <V a, b> = <a, V b>      (fp32 arithmetic: 2e-5 relative)
   * positivity: <V a, a> > 0 on mean-free fields
-  * the kernel variants (V-cycle bottom on/off, stored/rebuilt z0) are the same
-    linear operator up to fp32 rounding (2e-5 relative)
+  * the kernel variants (V-cycle bottom on/off, stored/rebuilt z0, 16-CTA cluster
+    tail) are the same linear operator up to fp32 rounding (2e-5 relative)
 """
 
 import ctypes as C
@@ -66,7 +66,7 @@ def test_vcycle_symmetric_positive(dims):
         assert float((va[c] * a[c]).sum()) > 0.0
 
 
-@pytest.mark.parametrize("env", [{"OTM_VBOT": "0"}, {"OTM_NOZ0": "1"}])
+@pytest.mark.parametrize("env", [{"OTM_VBOT": "0"}, {"OTM_NOZ0": "1"}, {"OTM_VT32": "1"}])
 def test_vcycle_variants_same_operator(env, monkeypatch):
     dims = (128, 128, 128)
     n = int(np.prod(dims))
