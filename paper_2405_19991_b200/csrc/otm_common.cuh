@@ -40,7 +40,16 @@ __device__ __forceinline__ int wrap_p(int i, int n) { return i + 1 == n ? 0 : i 
 // Programmatic dependent launch: a kernel launched with programmatic stream
 // serialisation may start while its predecessor drains; it must not touch the
 // predecessor's outputs before this wait (a no-op for ordinary launches).
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// Right after the wait the kernel also triggers its own dependents, so the next
+// kernel's launch and CTA rasterisation overlap this kernel's execution (without a
+// trigger the dependent grid only launches once every block here has exited).  The
+// dependent still waits for this grid's completion before touching its outputs.
+__device__ __forceinline__ void pdl_wait() {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#ifndef OTM_NO_PDL_TRIGGER
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+#endif
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
