@@ -112,6 +112,8 @@ struct otm_ctx {
     cudaGraphExec_t gexec = nullptr;
     cudaGraphExec_t gexec_prof = nullptr;
     cudaGraphExec_t gexec_loop = nullptr;     // whole inner loop: conditional WHILE node
+    cudaGraphExec_t gexec_build = nullptr;    // hierarchy build (factors, D^-1, coarse inverse)
+    long long build_launches = 0;
     int launches_per_inner = 0;
     // profiling
     bool prof = false;
@@ -470,7 +472,9 @@ int capture_loop(otm_ctx* ctx) {
 // instead of blocking in cudaStreamSynchronize: the thread is never descheduled
 // between the GPU finishing and the next enqueue (blocking waits showed rare
 // multi-millisecond wake-ups).  OTM_SPIN=0 restores blocking waits.
-static cudaError_t stream_wait(cudaStream_t s) {
+static double g_wait_ms = 0.0;        // host time spent waiting for the device (OTM_STATS)
+static long long g_waits = 0;
+static cudaError_t stream_wait_impl(cudaStream_t s) {
     static const bool spin = !(getenv("OTM_SPIN") && atoi(getenv("OTM_SPIN")) == 0);
     if (spin) {
         for (long it = 0; it < (1L << 26); ++it) {
@@ -479,6 +483,15 @@ static cudaError_t stream_wait(cudaStream_t s) {
         }
     }
     return cudaStreamSynchronize(s);
+}
+static cudaError_t stream_wait(cudaStream_t s) {
+    static const bool stats = getenv("OTM_STATS") != nullptr;
+    if (!stats) return stream_wait_impl(s);
+    const auto t0 = std::chrono::steady_clock::now();
+    const cudaError_t e = stream_wait_impl(s);
+    g_wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    ++g_waits;
+    return e;
 }
 
 int sync_scalars(otm_ctx* ctx, const double* dev, int count) {
@@ -519,7 +532,7 @@ struct ProfScope {
     }
 };
 
-int build_levels(otm_ctx* ctx) {
+int enqueue_build(otm_ctx* ctx) {
     cudaStream_t s = ctx->stream;
     const int nl = (int)ctx->L.size();
     for (int l = 1; l < nl; ++l) {
@@ -534,6 +547,33 @@ int build_levels(otm_ctx* ctx) {
     for (int i = 0; i < 8; ++i) ct.kt[i] = ctx->L[nl - 1].lt.kt[i];
     launch_coarse_setup(s, ctx->L[nl - 1].g, ctx->L[nl - 1].kap, ct, ctx->gj, ctx->G);
     ctx->launches++;
+    return OTM_OK;
+}
+
+// GridHierarchy.build on the device: child-mean factors, D^-1 per level and the coarse
+// pseudo-inverse -- 2 L launches with fixed arguments, replayed as one captured graph
+// (one host call instead of ~12 launches per design iteration; OTM_NO_BUILD_GRAPH=1: eager)
+int build_levels(otm_ctx* ctx) {
+    static const bool eager = getenv("OTM_NO_BUILD_GRAPH") != nullptr;
+    cudaStream_t s = ctx->stream;
+    if (eager || ctx->prof || ctx->no_loop_graph) {
+        int rc = enqueue_build(ctx);
+        if (rc) return rc;
+    } else {
+        if (!ctx->gexec_build) {
+            cudaGraph_t g;
+            CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            const long long l0 = ctx->launches;
+            enqueue_build(ctx);
+            ctx->build_launches = ctx->launches - l0;
+            ctx->launches = l0;
+            CK(cudaStreamEndCapture(s, &g));
+            CK(cudaGraphInstantiate(&ctx->gexec_build, g, 0));
+            cudaGraphDestroy(g);
+        }
+        CK(cudaGraphLaunch(ctx->gexec_build, s));
+        ctx->launches += ctx->build_launches;
+    }
     CKL();
     ctx->built = true;
     return OTM_OK;
@@ -715,9 +755,12 @@ int otm_destroy(otm_ctx* ctx) {
                 "(%.2f/update) retried %lld\n", ctx->stat_solves, ctx->stat_outer, ctx->stat_inner,
                 (double)ctx->stat_inner / ctx->stat_solves, ctx->stat_oc, ctx->stat_oc_passes,
                 ctx->stat_oc ? (double)ctx->stat_oc_passes / ctx->stat_oc : 0.0, ctx->stat_oc_retry);
+    if (getenv("OTM_STATS"))
+        fprintf(stderr, "[otm] host waits: %lld, %.1f ms waiting for the device (process total)\n", g_waits, g_wait_ms);
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
     if (ctx->gexec_prof) cudaGraphExecDestroy(ctx->gexec_prof);
     if (ctx->gexec_loop) cudaGraphExecDestroy(ctx->gexec_loop);
+    if (ctx->gexec_build) cudaGraphExecDestroy(ctx->gexec_build);
     for (auto& s : ctx->slots) { cudaEventDestroy(s.a); cudaEventDestroy(s.b); }
     auto F = [](void* p) { if (p) cudaFree(p); };
     F(ctx->kap64); F(ctx->T64); F(ctx->Tprev); F(ctx->rho_f); F(ctx->sensf); F(ctx->sens); F(ctx->r); F(ctx->p); F(ctx->q); F(ctx->d);

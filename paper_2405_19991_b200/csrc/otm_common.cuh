@@ -26,6 +26,20 @@ __host__ __device__ inline Geo make_geo(int nx, int ny, int nz) {
     return g;
 }
 
+// x^p of the SIMP law (element.py:91-100): the integral penalties by multiplication
+// (one or two roundings, within an ulp of numpy's pow; fp64 pow is a ~100-instruction
+// log/exp sequence that made the filter+SIMP and sensitivity kernels issue-bound)
+__device__ __forceinline__ double simp_pow(double x, double p) {
+    if (p == 3.0) return x * x * x;
+    if (p == 2.0) return x * x;
+    if (p == 1.0) return x;
+    if (p == 4.0) {
+        const double x2 = x * x;
+        return x2 * x2;
+    }
+    return pow(x, p);
+}
+
 __device__ __forceinline__ int wrap_m(int i, int n) { return i == 0 ? n - 1 : i - 1; }
 __device__ __forceinline__ int wrap_p(int i, int n) { return i + 1 == n ? 0 : i + 1; }
 

@@ -80,12 +80,12 @@ __global__ void __launch_bounds__(128) k_filter(Geo g, int xb, FilterTaps taps, 
             const long long v = (long long)x * g.pl + t;
             out[v] = s;
             if (MODE == 2) {
-                const double kap = sp.kmin + pow(s, sp.p) * (sp.k0 - sp.kmin);
+                const double kap = sp.kmin + simp_pow(s, sp.p) * (sp.k0 - sp.kmin);
                 kappa64[v] = kap;
                 kappa32[v] = (float)kap;
                 const double r = w[1][4];
                 acc_r += r;
-                acc_rp += pow(r, sp.p);
+                acc_rp += simp_pow(r, sp.p);
                 acc_rf += s;
             }
 #pragma unroll
@@ -144,13 +144,13 @@ __global__ void __launch_bounds__(256) k_filter_b(Geo g, FilterTaps taps, const 
         }
         *reinterpret_cast<double2*>(out + vp) = make_double2(res[0], res[1]);
         if (MODE == 2) {
-            double k0 = sp.kmin + pow(res[0], sp.p) * (sp.k0 - sp.kmin);
-            double k1 = sp.kmin + pow(res[1], sp.p) * (sp.k0 - sp.kmin);
+            double k0 = sp.kmin + simp_pow(res[0], sp.p) * (sp.k0 - sp.kmin);
+            double k1 = sp.kmin + simp_pow(res[1], sp.p) * (sp.k0 - sp.kmin);
             *reinterpret_cast<double2*>(kappa64 + vp) = make_double2(k0, k1);
             *reinterpret_cast<float2*>(kappa32 + vp) = make_float2((float)k0, (float)k1);
             const double r0 = t[1][1][1], r1 = t[1][1][2];
             acc3[0] = r0 + r1;
-            acc3[1] = pow(r0, sp.p) + pow(r1, sp.p);
+            acc3[1] = simp_pow(r0, sp.p) + simp_pow(r1, sp.p);
             acc3[2] = res[0] + res[1];
         }
     }
@@ -180,7 +180,7 @@ __global__ void k_simp(long long n, const double* __restrict__ rf, double* __res
                        float* __restrict__ k32, SimpParams sp) {
     const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
-    const double kap = sp.kmin + pow(rf[v], sp.p) * (sp.k0 - sp.kmin);
+    const double kap = sp.kmin + simp_pow(rf[v], sp.p) * (sp.k0 - sp.kmin);
     k64[v] = kap;
     k32[v] = (float)kap;
 }
@@ -201,7 +201,7 @@ __global__ void k_means(long long n, const double* __restrict__ rho, double p, d
          i += (long long)gridDim.x * blockDim.x) {
         const double r = rho[i];
         v2[0] += r;
-        v2[1] += pow(r, p);
+        v2[1] += simp_pow(r, p);
     }
     reduce_finalize<2>(v2, partials, counter, out);
 }
@@ -1365,7 +1365,7 @@ __global__ void k_sens(Geo g, const double* __restrict__ T, const double* __rest
     double con = 0.0;
 #pragma unroll
     for (int c = 0; c < 6; ++c) con += dG.v[c] * E[c];
-    const double dk = sp.p * pow(rf[e], sp.p - 1.0) * (sp.k0 - sp.kmin);
+    const double dk = sp.p * simp_pow(rf[e], sp.p - 1.0) * (sp.k0 - sp.kmin);
     sens[e] = dk * con / (double)g.n;
 }
 

@@ -383,10 +383,10 @@ __global__ void __launch_bounds__(256) ks_filter(SGeo g, W27 taps, const double*
         const long long idx = (long long)x * g.pl + y * g.nz + z;
         out[idx] = sacc;
         if (MODE == 2) {
-            kap64[idx] = sp.kmin + pow(sacc, sp.p) * (sp.k0 - sp.kmin);
+            kap64[idx] = sp.kmin + simp_pow(sacc, sp.p) * (sp.k0 - sp.kmin);
             const double r = __ldg(in + idx);
             acc3[0] = r;
-            acc3[1] = pow(r, sp.p);
+            acc3[1] = simp_pow(r, sp.p);
             acc3[2] = sacc;
         }
     }
@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(256) ks_sens(SGeo g, const double* __restrict_
         con += dG.v[q] * e;
     }
     const long long idx = (long long)x * g.pl + y * g.nz + z;
-    const double dk = sp.p * pow(rf[idx], sp.p - 1.0) * (sp.k0 - sp.kmin);
+    const double dk = sp.p * simp_pow(rf[idx], sp.p - 1.0) * (sp.k0 - sp.kmin);
     sens[idx] = dk * con / M;
 }
 
