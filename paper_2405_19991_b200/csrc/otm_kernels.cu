@@ -2980,9 +2980,23 @@ void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const d
     static const bool old64 = getenv("OTM_RES64_OLD") != nullptr;
     if (!fext && !old64 && k6_ok(g, lt)) {
         const int tyd = 256 / g.nz;
-        R64Maps M;
-        if (encode_map64(&M.Tm, T, g.nz, g.ny, 3LL * g.nx, tyd) && encode_map64(&M.Th, T, g.nz, g.ny, 3LL * g.nx, 1) &&
-            encode_map64(&M.Km, kap, g.nz, g.ny, g.nx, tyd) && encode_map64(&M.Kh, kap, g.nz, g.ny, g.nx, 1)) {
+        // tensor maps of the last (T, kappa, grid) are reused: encoding costs a few us of
+        // host time per map, on the critical path between two host waits
+        static R64Maps M;
+        static const double *lastT = nullptr, *lastK = nullptr;
+        static int lastdims[3] = {0, 0, 0};
+        static bool lastok = false;
+        if (T != lastT || kap != lastK || g.nx != lastdims[0] || g.ny != lastdims[1] || g.nz != lastdims[2]) {
+            lastok = encode_map64(&M.Tm, T, g.nz, g.ny, 3LL * g.nx, tyd) &&
+                     encode_map64(&M.Th, T, g.nz, g.ny, 3LL * g.nx, 1) &&
+                     encode_map64(&M.Km, kap, g.nz, g.ny, g.nx, tyd) && encode_map64(&M.Kh, kap, g.nz, g.ny, g.nx, 1);
+            lastT = T;
+            lastK = kap;
+            lastdims[0] = g.nx;
+            lastdims[1] = g.ny;
+            lastdims[2] = g.nz;
+        }
+        if (lastok) {
             const size_t sm = r64_smem_bytes(g.nz);
             int dev = 0, sms = 148;
             cudaGetDevice(&dev);
@@ -3104,9 +3118,13 @@ static bool encode_map4(CUtensorMap* m, const float* base, const Geo& g, int box
 }
 static int k10_ty_env();
 static int k10_ty(int nz) { return nz == 128 && (k10_ty_env() == 2 || k10_ty_env() == 8) ? k10_ty_env() : 512 / nz; }
+static long long k10_min_n() {           // smallest level on the k10 path (OTM_K10_MINN, tuning)
+    static const long long v = getenv("OTM_K10_MINN") ? atoll(getenv("OTM_K10_MINN")) : 32768;
+    return v;
+}
 static bool k10_ok(const Geo& g, const LevelTemplate& lt) {
     return lt.equal && (g.nz == 64 || g.nz == 128 || g.nz == 256) && g.ny % k10_ty(g.nz) == 0 &&
-           g.ny >= 2 * k10_ty(g.nz) && g.nx >= 2 && g.n >= 32768;
+           g.ny >= 2 * k10_ty(g.nz) && g.nx >= 2 && g.n >= k10_min_n();
 }
 // op3: 3-case operand (halo), d: D^-1 (smooth_res: halo, jacobi: centre), f3: jacobi right-hand side
 static bool k10_maps(K10Maps& M, const Geo& g, const float* op3, const float* d, const float* f3, const float* kap) {

@@ -106,18 +106,23 @@ int main(int argc, char** argv) {
     cudaStream_t s;
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
 
+    const Geo gc = make_geo(n / 2, n / 2, n / 2);
+    const int cf[3] = {1, 1, 1};
     auto run = [&](int which) {
         if (which == 0) launch_smooth_res(s, g, lt, dk, df, dd, omega, o0, o1);
         else if (which == 1) launch_jacobi(s, g, lt, dk, dz, df, dd, omega, o0, true, red, sc);
-        else launch_spmv(s, g, lt, dk, dp, o0, red, sc);
+        else if (which == 2) launch_spmv(s, g, lt, dk, dp, o0, red, sc);
+        else if (which == 3) launch_restrict(s, g, gc, cf, dp, o1);
+        else launch_prolong(s, g, gc, cf, df, o0);
     };
-    const char* names[3] = {"smooth_res", "jacobi", "spmv"};
-    const double bpv[3] = {44, 44, 28};
-    for (int which = 0; which < 3; ++which) {
+    const char* names[5] = {"smooth_res", "jacobi", "spmv", "restrict", "prolong"};
+    const double bpv[5] = {44, 44, 28, 13.5, 25.5};
+    const int nkern = getenv("L0_TRANSFER") ? 5 : 3;
+    for (int which = 0; which < nkern; ++which) {
         run(which);
         CK(cudaStreamSynchronize(s));
         CK(cudaGetLastError());
-        if (check) {
+        if (check && which < 3) {
             std::vector<float> g0(3 * N), g1(3 * N);
             CK(cudaMemcpy(g0.data(), o0, 3 * N * 4, cudaMemcpyDeviceToHost));
             CK(cudaMemcpy(g1.data(), o1, 3 * N * 4, cudaMemcpyDeviceToHost));
