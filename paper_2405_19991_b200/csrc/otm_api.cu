@@ -114,6 +114,11 @@ struct otm_ctx {
     cudaGraphExec_t gexec_loop = nullptr;     // whole inner loop: conditional WHILE node
     cudaGraphExec_t gexec_build = nullptr;    // hierarchy build (factors, D^-1, coarse inverse)
     long long build_launches = 0;
+    // the design loop runs the build on a side stream, overlapped with the first fp64
+    // defect pass of the solve (which only needs the level-0 factors)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_build = nullptr;
+    bool build_pending = false;
     int launches_per_inner = 0;
     // profiling
     bool prof = false;
@@ -553,9 +558,28 @@ int enqueue_build(otm_ctx* ctx) {
 // GridHierarchy.build on the device: child-mean factors, D^-1 per level and the coarse
 // pseudo-inverse -- 2 L launches with fixed arguments, replayed as one captured graph
 // (one host call instead of ~12 launches per design iteration; OTM_NO_BUILD_GRAPH=1: eager)
-int build_levels(otm_ctx* ctx) {
+// consumers of the level data order themselves after a pending side-stream build
+void join_build(otm_ctx* ctx) {
+    if (!ctx->build_pending) return;
+    cudaStreamWaitEvent(ctx->stream, ctx->ev_build, 0);
+    ctx->build_pending = false;
+}
+
+int build_levels(otm_ctx* ctx, bool async = false) {
     static const bool eager = getenv("OTM_NO_BUILD_GRAPH") != nullptr;
+    static const bool no_async = getenv("OTM_NO_BUILD_OVERLAP") != nullptr;
     cudaStream_t s = ctx->stream;
+    join_build(ctx);
+    if (async && !no_async && !eager && !ctx->prof && !ctx->no_loop_graph && ctx->gexec_build && ctx->side) {
+        CK(cudaEventRecord(ctx->ev_fork, s));
+        CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+        CK(cudaGraphLaunch(ctx->gexec_build, ctx->side));
+        CK(cudaEventRecord(ctx->ev_build, ctx->side));
+        ctx->launches += ctx->build_launches;
+        ctx->build_pending = true;
+        ctx->built = true;
+        return OTM_OK;
+    }
     if (eager || ctx->prof || ctx->no_loop_graph) {
         int rc = enqueue_build(ctx);
         if (rc) return rc;
@@ -737,6 +761,9 @@ int otm_create(otm_ctx** out, int nx, int ny, int nz, const otm_params* pin) {
     CK(cudaMemset(ctx->p, 0, 3 * n * sizeof(float)));
     CK(cudaEventCreate(&ctx->ev_a));
     CK(cudaEventCreate(&ctx->ev_b));
+    CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_build, cudaEventDisableTiming));
     CK(cudaDeviceSynchronize());
     return OTM_OK;
 }
@@ -771,6 +798,12 @@ int otm_destroy(otm_ctx* ctx) {
     F(ctx->G); F(ctx->gj); F(ctx->red.partials); F(ctx->red.counter); F(ctx->sc); F(ctx->scal);
     F(ctx->changed); F(ctx->ocl); F(ctx->fs.offs_dev); F(ctx->fs.wts_dev);
     if (ctx->h) cudaFreeHost(ctx->h);
+    if (ctx->side) {
+        cudaStreamSynchronize(ctx->side);
+        cudaStreamDestroy(ctx->side);
+    }
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_build) cudaEventDestroy(ctx->ev_build);
     if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
     if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -849,6 +882,7 @@ int otm_build_kappa(otm_ctx* ctx, const double* kap) {
 int otm_vcycle(otm_ctx* ctx, const float* f3, float* z3) {
     if (!ctx || !f3 || !z3) return OTM_EINVAL;
     if (!ctx->built) return fail(ctx, OTM_ESTATE, "hierarchy not built; call build() first");
+    join_build(ctx);
     const size_t bytes = 3 * ctx->g0.n * sizeof(float);
     CK(cudaMemcpyAsync(ctx->L[0].f, f3, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
     int rc = enqueue_inner(ctx, false, false, true);
@@ -929,6 +963,7 @@ int otm_solve(otm_ctx* ctx, const double* fext, double tol, int max_cycles, int*
     };
     int rc = residual();
     if (rc) return rc;
+    join_build(ctx);                           // the V-cycles need the level data
     static const bool debug = getenv("OTM_DEBUG") != nullptr;
     if (debug) fprintf(stderr, "[otm] solve start rel %.3e %.3e %.3e\n", rel[0], rel[1], rel[2]);
     ctx->stat_solves++;
@@ -1326,7 +1361,7 @@ int otm_run_step(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, dou
     }
     ctx->launches++;
     CKL();
-    int rc = build_levels(ctx);
+    int rc = build_levels(ctx, true);
     if (rc) return rc;
     ctx->warm = st->warm != 0;
     static const double theta = getenv("OTM_EXTRAP") ? atof(getenv("OTM_EXTRAP")) : 0.0;
