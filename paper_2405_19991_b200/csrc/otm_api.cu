@@ -119,6 +119,7 @@ struct otm_ctx {
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_build = nullptr;
     bool build_pending = false;
+    bool T_center_pending = false;   // T64 not yet shifted to zero mean (otm_get_T does it)
     int launches_per_inner = 0;
     // profiling
     bool prof = false;
@@ -1031,8 +1032,10 @@ int otm_solve(otm_ctx* ctx, const double* fext, double tol, int max_cycles, int*
                     std::sqrt(inner_rr[2]) / fnorm[2], rel[0], rel[1], rel[2]);
     }
     // mean-free T (solver.py:398); zero loads short-circuit to T = 0 (solver.py:382-385)
-    launch_submean(s, n, ctx->T64, ctx->scal + 6);
-    ctx->launches++;
+    // T -= mean(T) (solver.py:398) is deferred to otm_get_T: K T, the tensor and the
+    // sensitivities are invariant under a constant shift, so the design loop never
+    // needs the centred fields (one fp64 pass less per design iteration)
+    ctx->T_center_pending = true;
     for (int c = 0; c < 3; ++c)
         if (zero_load[c]) CK(cudaMemsetAsync(ctx->T64 + (size_t)c * n, 0, n * sizeof(double), s));
     CKL();
@@ -1054,6 +1057,12 @@ int otm_solve(otm_ctx* ctx, const double* fext, double tol, int max_cycles, int*
 
 int otm_get_T(otm_ctx* ctx, double* T) {
     if (!ctx || !T) return OTM_EINVAL;
+    if (ctx->T_center_pending) {
+        launch_sum3(ctx->stream, ctx->g0.n, ctx->T64, ctx->red, ctx->scal + 100);      // means
+        launch_submean_means(ctx->stream, ctx->g0.n, ctx->T64, ctx->scal + 100);
+        ctx->launches += 2;
+        ctx->T_center_pending = false;
+    }
     if (T != ctx->T64)
         CK(cudaMemcpyAsync(T, ctx->T64, 3 * ctx->g0.n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
     return OTM_OK;

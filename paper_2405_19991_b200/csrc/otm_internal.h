@@ -157,6 +157,7 @@ void launch_prolong(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3],
 void launch_loop_ctl(cudaStream_t s, PcgScalars* sc, unsigned long long handle);
 void launch_extrap(cudaStream_t s, long long n3, double* T, double* Tprev, double theta);
 void launch_Tupd(cudaStream_t s, long long n, double* T, const float* d, const float* p, const PcgScalars* sc);
+void launch_submean_means(cudaStream_t s, long long n, double* T, const double* means);
 void launch_submean(cudaStream_t s, long long n, double* T, const double* sumT);
 void launch_tensor(cudaStream_t s, const Geo& g, const double* T, const double* kap, Red& red, double* out6);
 void launch_pair_energy(cudaStream_t s, const Geo& g, const double* T, double* E);

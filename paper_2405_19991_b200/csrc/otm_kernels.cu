@@ -1284,6 +1284,13 @@ __global__ void k_Tupd(long long n, double* __restrict__ T, const float* __restr
     T[i] += (double)(d[i] + (float)sc->alpha[c] * p[i]);
 }
 
+// T -= mean per case, means given
+__global__ void k_submean_means(long long n, double* __restrict__ T, const double* __restrict__ means) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 3 * n) return;
+    T[i] -= means[i / n];
+}
+
 // T -= mean(T) per case (solver.py:398)
 __global__ void k_submean(long long n, double* __restrict__ T, const double* __restrict__ sumT) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -3757,6 +3764,9 @@ void launch_extrap(cudaStream_t s, long long n3, double* T, double* Tprev, doubl
 }
 void launch_Tupd(cudaStream_t s, long long n, double* T, const float* d, const float* p, const PcgScalars* sc) {
     k_Tupd<<<nblk(3 * n, 256), 256, 0, s>>>(n, T, d, p, sc);
+}
+void launch_submean_means(cudaStream_t s, long long n, double* T, const double* means) {
+    k_submean_means<<<nblk(3 * n, 256), 256, 0, s>>>(n, T, means);
 }
 void launch_submean(cudaStream_t s, long long n, double* T, const double* sumT) {
     k_submean<<<nblk(3 * n, 256), 256, 0, s>>>(n, T, sumT);
