@@ -148,6 +148,9 @@ bool launch_jacobi_p(cudaStream_t s, const Geo& g, const LevelTemplate& lt, cons
                      const float* f, const float* dinv, float omega, float* zout, bool dot, Red& red,
                      PcgScalars* sc);
 void launch_prolong_assign(cudaStream_t s, const Geo& f, const Geo& c, const float* zc, float* zf);
+bool launch_k10_range(cudaStream_t s, int op, const Geo& g, const LevelTemplate& lt, int xa, int xb,
+                      const float* kap, const float* a, const float* f, const float* dinv, float omega, float* o1,
+                      float* o2, bool dot, Red& red, PcgScalars* sc);
 void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* p,
                  float* q, Red& red, PcgScalars* sc);
 void launch_pupd(cudaStream_t s, long long n, const float* z, float* p, float* d, const PcgScalars* sc);

@@ -3184,6 +3184,8 @@ static bool k10_ok(const Geo& g, const LevelTemplate& lt) {
 // op3: 3-case operand (halo), d: D^-1 (smooth_res: halo, jacobi: centre), f3: jacobi right-hand side
 static bool k10_maps(K10Maps& M, const Geo& g, const float* op3, const float* d, const float* f3, const float* kap) {
     const int TY = k10_ty(g.nz);
+    M.xa = 0;
+    M.xb = g.nx;
     bool ok = encode_map4(&M.op_full, op3, g, TY + 2) && encode_map4(&M.op_main, op3, g, TY) &&
               encode_map4(&M.op_halo, op3, g, 1) && encode_map(&M.k_full, kap, g.nz, g.ny, g.nx, TY + 1) &&
               encode_map(&M.k_main, kap, g.nz, g.ny, g.nx, TY) && encode_map(&M.k_halo, kap, g.nz, g.ny, g.nx, 1);
@@ -3199,6 +3201,7 @@ static bool k10_maps(K10Maps& M, const Geo& g, const float* op3, const float* d,
         M.f_main = M.f_full = M.f_halo = M.op_main;
     return ok;
 }
+static int g_k10_nxr = 0;            // output plane count of the launch being issued (0: all nx)
 template <class K>
 static dim3 k10_grid(K kernel, size_t smem, const Geo& g, int TY) {
     int dev = 0, sms = 148, per_sm = 1;
@@ -3206,7 +3209,7 @@ static dim3 k10_grid(K kernel, size_t smem, const Geo& g, int TY) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, g.nz / 2 * TY, smem);
     if (per_sm < 1) per_sm = 1;
-    const long long units = (long long)(g.ny / TY) * g.nx;
+    const long long units = (long long)(g.ny / TY) * (g_k10_nxr > 0 ? g_k10_nxr : g.nx);
     long long b = (long long)per_sm * sms;
     if (b > units) b = units;
     return dim3((unsigned)b, 1, 1);
@@ -3293,6 +3296,44 @@ bool launch_jacobi_p(cudaStream_t s, const Geo& g, const LevelTemplate& lt, cons
 }
 void launch_prolong_assign(cudaStream_t s, const Geo& f, const Geo& c, const float* zc, float* zf) {
     launch_pdl(k_prolong3b<true>, nblk(3 * c.n, 256), 256, 0, s, f, c, zc, zf);
+}
+
+// k10 on the output planes [xa, xb) of a field stored with its x neighbours (slab
+// with ghost planes: xa >= 1, xb <= nx - 1, no x wrap).  op 0 smooth_res (o1 = z0,
+// o2 = res), 1 Jacobi (o1; r.z partial sums -> sc->red[0..2]), 2 K p (o1; p.q partial
+// sums -> sc->red[3..5]).  false: not eligible (caller uses its generic kernels).
+bool launch_k10_range(cudaStream_t s, int op, const Geo& g, const LevelTemplate& lt, int xa, int xb,
+                      const float* kap, const float* a, const float* f, const float* dinv, float omega, float* o1,
+                      float* o2, bool dot, Red& red, PcgScalars* sc) {
+    if (kernel_gen() != 10 || !k10_ok(g, lt) || xa < 1 || xb > g.nx - 1 || xb <= xa) return false;
+    K10Maps M;
+    const float* op3 = op == 0 ? f : a;
+    if (!k10_maps(M, g, op3, dinv, op == 1 ? f : nullptr, kap)) return false;
+    M.xa = xa;
+    M.xb = xb;
+    g_k10_nxr = xb - xa;
+    const float s12 = (float)lt.s12;
+    if (op == 0) {
+#define C_(NZ, TY, CPS) l10_smooth_res<NZ, TY, CPS>(s, g, s12, M, omega, o1, o2)
+        OTM_K10_SWITCH(C_);
+#undef C_
+    } else if (op == 1) {
+        if (dot) {
+#define C_(NZ, TY, CPS) l10_jacobi<true, NZ, TY, CPS>(s, g, s12, M, omega, o1, red.partials, red.counter, sc)
+            OTM_K10_SWITCH(C_);
+#undef C_
+        } else {
+#define C_(NZ, TY, CPS) l10_jacobi<false, NZ, TY, CPS>(s, g, s12, M, omega, o1, nullptr, nullptr, sc)
+            OTM_K10_SWITCH(C_);
+#undef C_
+        }
+    } else {
+#define C_(NZ, TY, CPS) l10_spmv<NZ, TY, CPS>(s, g, s12, M, o1, red, sc)
+        OTM_K10_SWITCH(C_);
+#undef C_
+    }
+    g_k10_nxr = 0;
+    return true;
 }
 void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* f,
                        const float* dinv, float omega, float* z, float* res) {

@@ -486,6 +486,7 @@ struct otm_slab_ws {
     double* h = nullptr;         // pinned host copy
     double* out32 = nullptr;     // 32 OC candidate sums (device) and their host copy
     double* h32 = nullptr;
+    PcgScalars* sc = nullptr;    // scratch scalars of the k10 level kernels (their dot sums land in red[])
     size_t max_blocks = 0;
     char err[256] = {0};
 };
@@ -529,11 +530,13 @@ otm_slab_ws* otm_slab_create(long long max_items) {
         cudaMalloc(&w->out, 16 * sizeof(double)) != cudaSuccess ||
         cudaMallocHost(&w->h, 16 * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&w->out32, 32 * sizeof(double)) != cudaSuccess ||
-        cudaMallocHost(&w->h32, 32 * sizeof(double)) != cudaSuccess) {
+        cudaMallocHost(&w->h32, 32 * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&w->sc, sizeof(PcgScalars)) != cudaSuccess) {
         delete w;
         return nullptr;
     }
     cudaMemset(w->counter, 0, 4 * sizeof(unsigned));
+    cudaMemset(w->sc, 0, sizeof(PcgScalars));
     return w;
 }
 
@@ -545,6 +548,7 @@ int otm_slab_destroy(otm_slab_ws* w) {
     cudaFreeHost(w->h);
     cudaFree(w->out32);
     cudaFreeHost(w->h32);
+    cudaFree(w->sc);
     delete w;
     return OTM_OK;
 }
@@ -566,6 +570,22 @@ int otm_slab_stencil(otm_slab_ws* w, int op, int nxl, int ny, int nz, const doub
     const long long items = 3 * g.ni;
     if (!blocks_ok(w, items, 256)) return OTM_EINVAL;
     const int dot = dots3 != nullptr && op > 0;
+    {
+        // fast path: the single-GPU k10 march on the interior planes [1, nxl] of the
+        // ghost-padded slab (the x neighbours are the ghost planes; y, z periodic)
+        const Geo gg = make_geo(nxl + 2, ny, nz);
+        Red red{w->partials, w->counter};
+        if (launch_k10_range(w->stream, op, gg, lt, 1, nxl + 1, kap, a, f, dinv, (float)omega, o1, o2, dot != 0,
+                             red, w->sc)) {
+            int rc = scheck(w);
+            if (rc || !dot) return rc;
+            SCK(cudaMemcpyAsync(w->h, reinterpret_cast<const double*>(w->sc) + (op == 1 ? 0 : 3), 3 * sizeof(double),
+                                cudaMemcpyDeviceToHost, w->stream));
+            SCK(cudaStreamSynchronize(w->stream));
+            std::memcpy(dots3, w->h, 3 * sizeof(double));
+            return OTM_OK;
+        }
+    }
     if (op == 0)
         ks_stencil<0><<<nb(items, 256), 256, 0, w->stream>>>(g, lt, kap, nullptr, f, dinv, (float)omega, o1, o2, 0,
                                                               w->partials, w->counter, w->out);

@@ -34,6 +34,8 @@ struct K10Maps {
     CUtensorMap d_full, d_main, d_halo;      // 3-D (z, y, x) D^-1: TY+2 / TY / 1 rows
     CUtensorMap f_full, f_main, f_halo;      // 4-D right-hand side: TY+2 / TY / 1 rows
     CUtensorMap k_full, k_main, k_halo;      // 3-D factors: TY+1 / TY / 1 rows
+    int xa, xb;                              // output x planes [xa, xb): [0, nx) periodic, or a slab's
+                                             // interior [1, nxl + 1) between its ghost planes
 };
 
 // K10_JACOBI_P: post-smoothing whose operand z = w D^-1 f + P e is rebuilt on the fly
@@ -244,15 +246,16 @@ __device__ __forceinline__ void march10(const Geo& g, float s12f, const K10Maps&
     const float2 ns12 = f2(-s12f, -s12f);
     const float2 s48 = f2(4.f * s12f, 4.f * s12f);
     const int nty = g.ny / TY;
-    const long long W = (long long)nty * g.nx;
+    const int nxr = maps.xb - maps.xa;
+    const long long W = (long long)nty * nxr;
     long long u = W * blockIdx.x / gridDim.x;
     const long long u1 = W * (blockIdx.x + 1) / gridDim.x;
     int kc = 0;                                  // ring slot of the next plane to land
     int ki = 0;                                  // ring slot of the next plane to issue
     while (u < u1) {
-        const int yt = (int)(u / g.nx);
-        const int x0 = (int)(u - (long long)yt * g.nx);
-        const int x1 = (int)min((long long)g.nx, x0 + (u1 - u));
+        const int yt = (int)(u / nxr);
+        const int x0 = maps.xa + (int)(u - (long long)yt * nxr);
+        const int x1 = (int)min((long long)maps.xb, x0 + (u1 - u));
         const int y0 = yt * TY;
         const bool seam = (y0 == 0) || (y0 + TY == g.ny);
         const int ym = y0 == 0 ? g.ny - 1 : y0 - 1;
