@@ -108,9 +108,8 @@ __global__ void __launch_bounds__(256) ks_stencil(SGeo g, LevelTemplate lt, cons
                                                   const float* __restrict__ dinv, float omega, float* __restrict__ o1,
                                                   float* __restrict__ o2, int dot, double* partials,
                                                   unsigned* counter, double* out3) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     double d3[3] = {0.0, 0.0, 0.0};
-    if (i < 3 * g.ni) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < 3 * g.ni; i += (long long)gridDim.x * blockDim.x) {
         const int c = (int)(i / g.ni);
         const long long v = i - (long long)c * g.ni;
         int x, y, z;
@@ -128,10 +127,10 @@ __global__ void __launch_bounds__(256) ks_stencil(SGeo g, LevelTemplate lt, cons
             const float fv = __ldg(f + off + idx);
             const float zn = t[1][4] + omega * __ldg(dinv + idx) * (fv - kt);
             o1[off + idx] = zn;
-            d3[c] = (double)fv * (double)zn;
+            d3[c] += (double)fv * (double)zn;
         } else {
             o1[off + idx] = kt;
-            d3[c] = (double)t[1][4] * (double)kt;
+            d3[c] += (double)t[1][4] * (double)kt;
         }
     }
     if (dot && reduce_finalize<3>(d3, partials, counter, out3)) {}
@@ -230,16 +229,15 @@ __global__ void __launch_bounds__(256) ks_upd(SGeo g, float* __restrict__ d, flo
                                               const float* __restrict__ p, const float* __restrict__ q, double a0,
                                               double a1, double a2, double* partials, unsigned* counter,
                                               double* out3) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     double d3[3] = {0.0, 0.0, 0.0};
-    if (i < 3 * g.ni) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < 3 * g.ni; i += (long long)gridDim.x * blockDim.x) {
         const int c = (int)(i / g.ni);
         const long long idx = (long long)c * g.na + g.pl + (i - (long long)c * g.ni);
         const float al = (float)(c == 0 ? a0 : (c == 1 ? a1 : a2));
         d[idx] += al * p[idx];
         const float rn = r[idx] - al * q[idx];
         r[idx] = rn;
-        d3[c] = (double)rn * (double)rn;
+        d3[c] += (double)rn * (double)rn;
     }
     reduce_finalize<3>(d3, partials, counter, out3);
 }
@@ -252,11 +250,10 @@ __global__ void __launch_bounds__(128) ks_res64(SGeo g, LevelTemplate lt, const 
                                                 const double* __restrict__ T, const double* __restrict__ fmean,
                                                 float* __restrict__ r32, double* partials, unsigned* counter,
                                                 double* out9) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     double acc[9];
 #pragma unroll
     for (int q = 0; q < 9; ++q) acc[q] = 0.0;
-    if (i < g.ni) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < g.ni; i += (long long)gridDim.x * blockDim.x) {
         int x, y, z;
         s_decode(g, i, x, y, z);
         const int ys[3] = {wrap_m(y, g.ny) * g.nz, y * g.nz, wrap_p(y, g.ny) * g.nz};
@@ -322,9 +319,8 @@ __global__ void ks_tupd(SGeo g, double* __restrict__ T, const float* __restrict_
 __global__ void __launch_bounds__(256) ks_tensor(SGeo g, const double* __restrict__ T, const double* __restrict__ kap,
                                                  const double* __restrict__ kt, double* partials, unsigned* counter,
                                                  double* out6) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     double acc[6] = {0, 0, 0, 0, 0, 0};
-    if (i < g.ni) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < g.ni; i += (long long)gridDim.x * blockDim.x) {
         int x, y, z;
         s_decode(g, i, x, y, z);
         const int ys[2] = {y, wrap_p(y, g.ny)}, zs[2] = {z, wrap_p(z, g.nz)};
@@ -348,7 +344,7 @@ __global__ void __launch_bounds__(256) ks_tensor(SGeo g, const double* __restric
                 for (int b = 0; b < 8; ++b) ka += kt[a ^ b] * chi[pr[q][1]][b];
                 e += chi[pr[q][0]][a] * ka;
             }
-            acc[q] = ke * e;
+            acc[q] += ke * e;
         }
     }
     reduce_finalize<6>(acc, partials, counter, out6);
@@ -363,9 +359,8 @@ __global__ void __launch_bounds__(256) ks_filter(SGeo g, W27 taps, const double*
                                                  double* __restrict__ out, double* __restrict__ kap64,
                                                  SimpParams sp, double* partials, unsigned* counter,
                                                  double* out3) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     double acc3[3] = {0.0, 0.0, 0.0};
-    if (i < g.ni) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < g.ni; i += (long long)gridDim.x * blockDim.x) {
         int x, y, z;
         s_decode(g, i, x, y, z);
         const int ys[3] = {wrap_m(y, g.ny) * g.nz, y * g.nz, wrap_p(y, g.ny) * g.nz};
@@ -385,9 +380,9 @@ __global__ void __launch_bounds__(256) ks_filter(SGeo g, W27 taps, const double*
         if (MODE == 2) {
             kap64[idx] = sp.kmin + simp_pow(sacc, sp.p) * (sp.k0 - sp.kmin);
             const double r = __ldg(in + idx);
-            acc3[0] = r;
-            acc3[1] = simp_pow(r, sp.p);
-            acc3[2] = sacc;
+            acc3[0] += r;
+            acc3[1] += simp_pow(r, sp.p);
+            acc3[2] += sacc;
         }
     }
     if (MODE == 2) reduce_finalize<3>(acc3, partials, counter, out3);
@@ -436,11 +431,10 @@ __global__ void __launch_bounds__(256) ks_oc(SGeo g, const double* __restrict__ 
                                              const double* __restrict__ sens, OcArgs a, double M, LamSet lams,
                                              int nlam, double* __restrict__ rho_out, double* partials,
                                              unsigned* counter, double* out32) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     double acc[32];
 #pragma unroll
     for (int k = 0; k < 32; ++k) acc[k] = 0.0;
-    if (i < g.ni) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < g.ni; i += (long long)gridDim.x * blockDim.x) {
         int x, y, z;
         s_decode(g, i, x, y, z);
         const long long idx = (long long)x * g.pl + y * g.nz + z;
@@ -461,10 +455,10 @@ __global__ void __launch_bounds__(256) ks_oc(SGeo g, const double* __restrict__ 
                 }
                 if (APPLY) {
                     rho_out[idx] = out;
-                    acc[0] = out != r ? 1.0 : 0.0;
+                    acc[0] += out != r ? 1.0 : 0.0;
                     break;
                 }
-                acc[k] = out;
+                acc[k] += out;
             }
         }
     }
@@ -472,6 +466,10 @@ __global__ void __launch_bounds__(256) ks_oc(SGeo g, const double* __restrict__ 
 }
 
 inline unsigned nb(long long n, int bs) { return (unsigned)((n + bs - 1) / bs); }
+// reducing kernels are grid-stride with a bounded grid: one partial per block and one
+// ticket atomic per block (an unbounded one-item-per-thread grid serialised ~10^5
+// atomics on the ticket counter)
+inline unsigned nbr(long long n, int bs) { const unsigned b = nb(n, bs); return b < 1184u ? b : 1184u; }
 
 }  // namespace
 }  // namespace otm
@@ -587,13 +585,13 @@ int otm_slab_stencil(otm_slab_ws* w, int op, int nxl, int ny, int nz, const doub
         }
     }
     if (op == 0)
-        ks_stencil<0><<<nb(items, 256), 256, 0, w->stream>>>(g, lt, kap, nullptr, f, dinv, (float)omega, o1, o2, 0,
+        ks_stencil<0><<<nbr(items, 256), 256, 0, w->stream>>>(g, lt, kap, nullptr, f, dinv, (float)omega, o1, o2, 0,
                                                               w->partials, w->counter, w->out);
     else if (op == 1)
-        ks_stencil<1><<<nb(items, 256), 256, 0, w->stream>>>(g, lt, kap, a, f, dinv, (float)omega, o1, nullptr, dot,
+        ks_stencil<1><<<nbr(items, 256), 256, 0, w->stream>>>(g, lt, kap, a, f, dinv, (float)omega, o1, nullptr, dot,
                                                               w->partials, w->counter, w->out);
     else
-        ks_stencil<2><<<nb(items, 256), 256, 0, w->stream>>>(g, lt, kap, a, nullptr, nullptr, 0.f, o1, nullptr, dot,
+        ks_stencil<2><<<nbr(items, 256), 256, 0, w->stream>>>(g, lt, kap, a, nullptr, nullptr, 0.f, o1, nullptr, dot,
                                                               w->partials, w->counter, w->out);
     int rc = scheck(w);
     if (rc || !dot) return rc;
@@ -641,7 +639,7 @@ int otm_slab_upd(otm_slab_ws* w, int nxl, int ny, int nz, float* d, float* r, co
     if (!w || nxl < 1) return OTM_EINVAL;
     const SGeo g = make_sgeo(nxl, ny, nz);
     if (!blocks_ok(w, 3 * g.ni, 256)) return OTM_EINVAL;
-    ks_upd<<<nb(3 * g.ni, 256), 256, 0, w->stream>>>(g, d, r, p, q, alpha3[0], alpha3[1], alpha3[2], w->partials,
+    ks_upd<<<nbr(3 * g.ni, 256), 256, 0, w->stream>>>(g, d, r, p, q, alpha3[0], alpha3[1], alpha3[2], w->partials,
                                                       w->counter, w->out);
     int rc = scheck(w);
     if (rc) return rc;
@@ -654,7 +652,7 @@ int otm_slab_load_sums(otm_slab_ws* w, int nxl, int ny, int nz, const double sca
     const SGeo g = make_sgeo(nxl, ny, nz);
     if (!blocks_ok(w, g.ni, 128)) return OTM_EINVAL;
     const LevelTemplate lt = tmpl(scale);
-    ks_res64<0><<<nb(g.ni, 128), 128, 0, w->stream>>>(g, lt, kap64, nullptr, nullptr, nullptr, w->partials,
+    ks_res64<0><<<nbr(g.ni, 128), 128, 0, w->stream>>>(g, lt, kap64, nullptr, nullptr, nullptr, w->partials,
                                                        w->counter, w->out);
     int rc = scheck(w);
     if (rc) return rc;
@@ -672,7 +670,7 @@ int otm_slab_res64(otm_slab_ws* w, int nxl, int ny, int nz, const double scale[3
     if (!blocks_ok(w, g.ni, 128)) return OTM_EINVAL;
     const LevelTemplate lt = tmpl(scale);
     SCK(cudaMemcpyAsync(w->out + 9, fmean3, 3 * sizeof(double), cudaMemcpyHostToDevice, w->stream));
-    ks_res64<1><<<nb(g.ni, 128), 128, 0, w->stream>>>(g, lt, kap64, T, w->out + 9, r32, w->partials, w->counter,
+    ks_res64<1><<<nbr(g.ni, 128), 128, 0, w->stream>>>(g, lt, kap64, T, w->out + 9, r32, w->partials, w->counter,
                                                        w->out);
     int rc = scheck(w);
     if (rc) return rc;
@@ -693,7 +691,7 @@ int otm_slab_tensor_sums(otm_slab_ws* w, int nxl, int ny, int nz, const double s
     if (!blocks_ok(w, g.ni, 256)) return OTM_EINVAL;
     const LevelTemplate lt = tmpl(scale);
     SCK(cudaMemcpyAsync(w->out + 8, lt.kt, 8 * sizeof(double), cudaMemcpyHostToDevice, w->stream));
-    ks_tensor<<<nb(g.ni, 256), 256, 0, w->stream>>>(g, T, kap64, w->out + 8, w->partials, w->counter, w->out);
+    ks_tensor<<<nbr(g.ni, 256), 256, 0, w->stream>>>(g, T, kap64, w->out + 8, w->partials, w->counter, w->out);
     int rc = scheck(w);
     if (rc) return rc;
     return sfetch(w, 6, sums6);
@@ -721,7 +719,7 @@ int otm_slab_filter(otm_slab_ws* w, int mode, int nxl, int ny, int nz, double ra
     sp.kmin = kappa_min;
     sp.p = penalty;
     if (mode == 2)
-        ks_filter<2><<<nb(g.ni, 256), 256, 0, w->stream>>>(g, taps, in, out, kap64, sp, w->partials, w->counter,
+        ks_filter<2><<<nbr(g.ni, 256), 256, 0, w->stream>>>(g, taps, in, out, kap64, sp, w->partials, w->counter,
                                                             w->out);
     else
         ks_filter<1><<<nb(g.ni, 256), 256, 0, w->stream>>>(g, taps, in, out, nullptr, sp, w->partials, w->counter,
@@ -761,7 +759,7 @@ int otm_slab_oc_sums(otm_slab_ws* w, int nxl, int ny, int nz, double n_total, co
     a.sqrt_damp = pp->damp == 0.5;
     LamSet ls;
     for (int k = 0; k < 32; ++k) ls.v[k] = k < nlam ? lams[k] : 0.0;
-    ks_oc<false><<<nb(g.ni, 256), 256, 0, w->stream>>>(g, rho, sens, a, n_total, ls, nlam, nullptr, w->partials,
+    ks_oc<false><<<nbr(g.ni, 256), 256, 0, w->stream>>>(g, rho, sens, a, n_total, ls, nlam, nullptr, w->partials,
                                                         w->counter, w->out32);
     int rc = scheck(w);
     if (rc) return rc;
@@ -785,7 +783,7 @@ int otm_slab_oc_apply(otm_slab_ws* w, int nxl, int ny, int nz, double n_total, c
     LamSet ls;
     for (int k = 0; k < 32; ++k) ls.v[k] = 0.0;
     ls.v[0] = lam;
-    ks_oc<true><<<nb(g.ni, 256), 256, 0, w->stream>>>(g, rho, sens, a, n_total, ls, 1, rho_out, w->partials,
+    ks_oc<true><<<nbr(g.ni, 256), 256, 0, w->stream>>>(g, rho, sens, a, n_total, ls, 1, rho_out, w->partials,
                                                        w->counter, w->out32);
     int rc = scheck(w);
     if (rc) return rc;
