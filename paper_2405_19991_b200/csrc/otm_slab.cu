@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <vector>
 
 void level_template(const double scale[3], otm::LevelTemplate& lt);   // otm_api.cu
@@ -185,6 +186,91 @@ __global__ void ks_prolong(SGeo f, SGeo c, const float* __restrict__ zc, float* 
                     wx1 * (wy0 * (wz0 * at(J1, Y0, Z0) + wz1 * at(J1, Y0, Z1)) +
                            wy1 * (wz0 * at(J1, Y1, Z0) + wz1 * at(J1, Y1, Z1)));
     zf[(long long)cc * f.na + (long long)x * f.pl + y * f.nz + z] += s;
+}
+
+// prolongation + correction, one thread per coarse interior vertex (case, X, Y, Z):
+// the fine block x = 2X-1 (on coarse X), 2X (between X and X+1, the right ghost),
+// y = 2Y, 2Y+1, z pair (2Z, 2Z+1) as float2 read-modify-writes (as k_prolong3b)
+__global__ void ks_prolong_b(SGeo f, SGeo c, const float* __restrict__ zc, float* __restrict__ zf) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 3 * c.ni) return;
+    const int cc = (int)(i / c.ni);
+    int X, Y, Z;
+    s_decode(c, i - (long long)cc * c.ni, X, Y, Z);
+    const int Y1 = Y + 1 == c.ny ? 0 : Y + 1, Z1 = Z + 1 == c.nz ? 0 : Z + 1;
+    const float* a = zc + (long long)cc * c.na;
+    float q[2][2][2];
+    const int xs[2] = {X, X + 1}, ys[2] = {Y, Y1}, zs[2] = {Z, Z1};
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) q[p][j][k] = __ldg(a + (long long)xs[p] * c.pl + ys[j] * c.nz + zs[k]);
+    float* out = zf + (long long)cc * f.na;
+#pragma unroll
+    for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+        for (int b2 = 0; b2 < 2; ++b2) {
+            float v[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {                  // fine z = 2Z + h
+                float qy[2];
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    const float z0 = q[p][0][0] * (h ? 0.5f : 1.f) + (h ? 0.5f * q[p][0][1] : 0.f);
+                    const float z1 = q[p][1][0] * (h ? 0.5f : 1.f) + (h ? 0.5f * q[p][1][1] : 0.f);
+                    qy[p] = b2 ? 0.5f * (z0 + z1) : z0;
+                }
+                v[h] = a2 ? 0.5f * (qy[0] + qy[1]) : qy[0];
+            }
+            float2* dst = reinterpret_cast<float2*>(out + (long long)(2 * X - 1 + a2) * f.pl + (2 * Y + b2) * f.nz + 2 * Z);
+            float2 cur = *dst;
+            cur.x += v[0];
+            cur.y += v[1];
+            *dst = cur;
+        }
+}
+
+// p = z + beta p on the interior, float4, blockIdx.y = case (pl % 4 == 0)
+__global__ void ks_pupd4(SGeo g, const float* __restrict__ z, float* __restrict__ p, double b0, double b1, double b2) {
+    const int c = blockIdx.y;
+    const float b = (float)(c == 0 ? b0 : (c == 1 ? b1 : b2));
+    const long long base = (long long)c * g.na + g.pl;
+    const float4* zz = reinterpret_cast<const float4*>(z + base);
+    float4* pp = reinterpret_cast<float4*>(p + base);
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < g.ni / 4; i += (long long)gridDim.x * blockDim.x) {
+        const float4 zv = __ldg(zz + i);
+        const float4 pv = pp[i];
+        pp[i] = make_float4(zv.x + b * pv.x, zv.y + b * pv.y, zv.z + b * pv.z, zv.w + b * pv.w);
+    }
+}
+
+// d += alpha p, r -= alpha q, partial r.r; float4, blockIdx.y = case (pl % 4 == 0)
+__global__ void __launch_bounds__(256) ks_upd4(SGeo g, float* __restrict__ d, float* __restrict__ r,
+                                               const float* __restrict__ p, const float* __restrict__ q, double a0,
+                                               double a1, double a2, double* partials, unsigned* counter,
+                                               double* out3) {
+    const int c = blockIdx.y;
+    const float al = (float)(c == 0 ? a0 : (c == 1 ? a1 : a2));
+    const long long base = (long long)c * g.na + g.pl;
+    float4* dd = reinterpret_cast<float4*>(d + base);
+    float4* rr = reinterpret_cast<float4*>(r + base);
+    const float4* pp = reinterpret_cast<const float4*>(p + base);
+    const float4* qq = reinterpret_cast<const float4*>(q + base);
+    double d3[3] = {0.0, 0.0, 0.0};
+    double acc = 0.0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < g.ni / 4; i += (long long)gridDim.x * blockDim.x) {
+        const float4 pv = __ldg(pp + i), qv = __ldg(qq + i);
+        float4 dv = dd[i], rv = rr[i];
+        dv.x += al * pv.x; dv.y += al * pv.y; dv.z += al * pv.z; dv.w += al * pv.w;
+        rv.x -= al * qv.x; rv.y -= al * qv.y; rv.z -= al * qv.z; rv.w -= al * qv.w;
+        dd[i] = dv;
+        rr[i] = rv;
+        acc += ((double)rv.x * rv.x + (double)rv.y * rv.y) + ((double)rv.z * rv.z + (double)rv.w * rv.w);
+    }
+    d3[c] = acc;
+    reduce_finalize<3>(d3, partials, counter, out3);
 }
 
 // child-mean factors: coarse element J <- fine elements 2J-1, 2J (local x), 2x2 in y/z
@@ -608,7 +694,10 @@ int otm_slab_restrict(otm_slab_ws* w, int nxl_f, int ny_f, int nz_f, const float
 int otm_slab_prolong(otm_slab_ws* w, int nxl_f, int ny_f, int nz_f, const float* z_c, float* z_f) {
     if (!w || nxl_f < 2 || (nxl_f & 1) || (ny_f & 1) || (nz_f & 1)) return OTM_EINVAL;
     const SGeo f = make_sgeo(nxl_f, ny_f, nz_f), c = make_sgeo(nxl_f / 2, ny_f / 2, nz_f / 2);
-    ks_prolong<<<nb(3 * f.ni, 256), 256, 0, w->stream>>>(f, c, z_c, z_f);
+    if (nz_f % 2 == 0 && ny_f % 2 == 0)
+        ks_prolong_b<<<nb(3 * c.ni, 256), 256, 0, w->stream>>>(f, c, z_c, z_f);
+    else
+        ks_prolong<<<nb(3 * f.ni, 256), 256, 0, w->stream>>>(f, c, z_c, z_f);
     return scheck(w);
 }
 
@@ -630,7 +719,11 @@ int otm_slab_dinv(otm_slab_ws* w, int nxl, int ny, int nz, const double scale[3]
 int otm_slab_pupd(otm_slab_ws* w, int nxl, int ny, int nz, const float* z, float* p, const double beta3[3]) {
     if (!w || nxl < 1) return OTM_EINVAL;
     const SGeo g = make_sgeo(nxl, ny, nz);
-    ks_pupd<<<nb(3 * g.ni, 256), 256, 0, w->stream>>>(g, z, p, beta3[0], beta3[1], beta3[2]);
+    if (g.pl % 4 == 0)
+        ks_pupd4<<<dim3(std::min<unsigned>(nb(g.ni / 4, 256), 592u), 3), 256, 0, w->stream>>>(g, z, p, beta3[0],
+                                                                                          beta3[1], beta3[2]);
+    else
+        ks_pupd<<<nb(3 * g.ni, 256), 256, 0, w->stream>>>(g, z, p, beta3[0], beta3[1], beta3[2]);
     return scheck(w);
 }
 
@@ -639,8 +732,12 @@ int otm_slab_upd(otm_slab_ws* w, int nxl, int ny, int nz, float* d, float* r, co
     if (!w || nxl < 1) return OTM_EINVAL;
     const SGeo g = make_sgeo(nxl, ny, nz);
     if (!blocks_ok(w, 3 * g.ni, 256)) return OTM_EINVAL;
-    ks_upd<<<nbr(3 * g.ni, 256), 256, 0, w->stream>>>(g, d, r, p, q, alpha3[0], alpha3[1], alpha3[2], w->partials,
-                                                      w->counter, w->out);
+    if (g.pl % 4 == 0)
+        ks_upd4<<<dim3(std::min<unsigned>(nb(g.ni / 4, 256), 394u), 3), 256, 0, w->stream>>>(
+            g, d, r, p, q, alpha3[0], alpha3[1], alpha3[2], w->partials, w->counter, w->out);
+    else
+        ks_upd<<<nbr(3 * g.ni, 256), 256, 0, w->stream>>>(g, d, r, p, q, alpha3[0], alpha3[1], alpha3[2],
+                                                          w->partials, w->counter, w->out);
     int rc = scheck(w);
     if (rc) return rc;
     return sfetch(w, 3, rr3);
