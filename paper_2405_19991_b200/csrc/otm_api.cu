@@ -119,7 +119,8 @@ struct otm_ctx {
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_build = nullptr;
     bool build_pending = false;
-    bool T_center_pending = false;   // T64 not yet shifted to zero mean (otm_get_T does it)
+    bool T_center_pending = false;
+    unsigned long long loop_handle = 0;   // set while the inner-loop graph is captured   // T64 not yet shifted to zero mean (otm_get_T does it)
     int launches_per_inner = 0;
     // profiling
     bool prof = false;
@@ -429,10 +430,10 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false, bool vonly = fa
     if (prof) prof_record(ctx, kProfL0Stencil, 28.0 * n0, true, sl);
     launch_spmv(s, ctx->g0, ctx->L[0].lt, ctx->L[0].kap, ctx->p, ctx->q, ctx->red, ctx->sc);
     if (prof) prof_record(ctx, kProfL0Stencil, 0, false, sl);
-    launch_upd(s, ctx->g0.n, ctx->r, ctx->q, ctx->red, ctx->sc);
+    launch_upd(s, ctx->g0.n, ctx->r, ctx->q, ctx->red, ctx->sc, in_loop ? ctx->loop_handle : 0ULL);
     launches += 3;
     if (!in_loop) cudaMemcpyAsync(ctx->h, ctx->sc->flags, 8 * sizeof(double), cudaMemcpyDeviceToHost, s);
-    ctx->launches_per_inner = launches + (in_loop ? 1 : 0);
+    ctx->launches_per_inner = launches;
     return OTM_OK;
 }
 
@@ -465,8 +466,9 @@ int capture_loop(otm_ctx* ctx) {
     CK(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     CK(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    ctx->loop_handle = (unsigned long long)h;      // k_upd's last block runs the loop control
     enqueue_inner(ctx, false, true);
-    launch_loop_ctl(ctx->stream, ctx->sc, (unsigned long long)h);
+    ctx->loop_handle = 0;
     cudaGraph_t captured;
     CK(cudaStreamEndCapture(ctx->stream, &captured));
     CK(cudaGraphInstantiate(&ctx->gexec_loop, g, 0));

@@ -154,7 +154,10 @@ bool launch_k10_range(cudaStream_t s, int op, const Geo& g, const LevelTemplate&
 void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* p,
                  float* q, Red& red, PcgScalars* sc);
 void launch_pupd(cudaStream_t s, long long n, const float* z, float* p, float* d, const PcgScalars* sc);
-void launch_upd(cudaStream_t s, long long n, float* r, const float* q, Red& red, PcgScalars* sc);
+// loop != 0: the conditional-WHILE handle of the inner-loop graph (the kernel's last
+// block also runs the loop control)
+void launch_upd(cudaStream_t s, long long n, float* r, const float* q, Red& red, PcgScalars* sc,
+                unsigned long long loop = 0);
 void launch_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* res, float* fc);
 void launch_prolong(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* zc, float* zf);
 void launch_loop_ctl(cudaStream_t s, PcgScalars* sc, unsigned long long handle);

@@ -911,7 +911,8 @@ __global__ void k_pupd(long long n, const float* __restrict__ z, float* __restri
 
 // r -= alpha q ; r.r partial sums -> convergence flags (d is updated by the next k_pupd)
 __global__ void __launch_bounds__(256) k_upd(long long n, float* __restrict__ r, const float* __restrict__ q,
-                                             double* partials, unsigned* counter, PcgScalars* sc) {
+                                             double* partials, unsigned* counter, PcgScalars* sc,
+                                             unsigned long long loop) {
     pdl_wait();
     double acc[3] = {0.0, 0.0, 0.0};
     const float al[3] = {(float)sc->alpha[0], (float)sc->alpha[1], (float)sc->alpha[2]};
@@ -945,6 +946,17 @@ __global__ void __launch_bounds__(256) k_upd(long long n, float* __restrict__ r,
         sc->flags[3] = sc->rr[0];
         sc->flags[4] = sc->rr[1];
         sc->flags[5] = sc->rr[2];
+        if (loop) {
+            // the inner-loop control (formerly a separate 1-thread launch): count the
+            // preconditioner applications, decide whether the WHILE node runs again
+            sc->cycles += sc->nact;
+            int nact = 0;
+            for (int c = 0; c < 3; ++c) nact += sc->active[c] != 0.0;
+            sc->nact = nact;
+            sc->it += 1;
+            const bool more = nact > 0 && sc->it < sc->max_it && sc->cycles < sc->max_cycles;
+            cudaGraphSetConditional((cudaGraphConditionalHandle)loop, more ? 1u : 0u);
+        }
     }
 }
 
@@ -3767,9 +3779,10 @@ void launch_pupd(cudaStream_t s, long long n, const float* z, float* p, float* d
     const long long th = std::max<long long>(n >> 2, n & 3);
     launch_pdl(k_pupd, nblk(th, 256), 256, 0, s, n, z, p, d, sc);
 }
-void launch_upd(cudaStream_t s, long long n, float* r, const float* q, Red& red, PcgScalars* sc) {
+void launch_upd(cudaStream_t s, long long n, float* r, const float* q, Red& red, PcgScalars* sc,
+                unsigned long long loop) {
     const long long th = std::max<long long>(n >> 2, n & 3);
-    launch_pdl(k_upd, nblk(th, 256), 256, 0, s, n, r, q, red.partials, red.counter, sc);
+    launch_pdl(k_upd, nblk(th, 256), 256, 0, s, n, r, q, red.partials, red.counter, sc, loop);
 }
 void launch_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* res, float* fc) {
     if (cf[0] && cf[1] && cf[2]) {
