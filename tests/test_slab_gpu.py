@@ -25,7 +25,10 @@ def _solve_slabs(dims, world, rho_f, tol):
 
 
 @pytest.mark.parametrize("dims,world", [((32, 32, 32), 1), ((32, 32, 32), 2), ((32, 32, 32), 4),
-                                        ((64, 32, 32), 4), ((16, 16, 16), 2)])
+                                        ((64, 32, 32), 4), ((16, 16, 16), 2),
+                                        # nz = 64 / 128: the slab stencils run the k10 march on the
+                                        # interior planes (launch_k10_range)
+                                        ((32, 64, 64), 2), ((64, 64, 64), 4), ((16, 32, 128), 2)])
 def test_slab_solve_matches_single_gpu(dims, world):
     import paper_2405_19991_b200 as otm
     rng = np.random.default_rng(world + dims[0])
