@@ -622,7 +622,7 @@ void otm_default_params(otm_params* p) {
     p->filter_radius = 1.5;
     p->coarse_target = 64;
     p->direct_limit = 40000;
-    p->jacobi_omega = 0.8;
+    p->jacobi_omega = 1.0;
     p->inner_reduction = 1e-5;
     p->max_inner = 40;
     p->device = 0;

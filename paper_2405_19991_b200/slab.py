@@ -313,7 +313,7 @@ class _Lev:
 class SlabSolver:
     """Distributed solve_cases + effective tensor on x-slabs (homogenize.py:71-122)."""
 
-    def __init__(self, dims, comm, backend, kappa0=1.0, kappa_min=1e-4, penalty=3.0, omega=0.8,
+    def __init__(self, dims, comm, backend, kappa0=1.0, kappa_min=1e-4, penalty=3.0, omega=1.0,
                  inner_reduction=1e-5, max_inner=40):
         self.L = SlabLayout.make(dims, comm.world)
         self.comm, self.B = comm, backend
