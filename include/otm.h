@@ -47,7 +47,7 @@ typedef struct otm_params {
     int coarse_target;     /* 64    (solver.py:211) */
     int direct_limit;      /* 40000 (solver.py:212) */
     /* B200 solver knobs (no reference counterpart) */
-    double jacobi_omega;   /* Jacobi weight of the V-cycle smoother, 1.0 (0.8-1.05 measured: >= 0.9 saves 5 % of the PCG iterations) */
+    double jacobi_omega;   /* level-0 Jacobi weight of the V-cycle smoother, 0.95 (coarse levels: 1.25) */
     double inner_reduction;/* fp32 inner PCG relative reduction floor per refinement step, 1e-5 */
     int max_inner;         /* cap on inner PCG iterations per refinement step, 40 */
     int device;            /* CUDA ordinal */
