@@ -3172,7 +3172,31 @@ static void l8_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const
         }                                                               \
     } while (0)
 // ---- k10 host side: 4-D (z, case, y, x) maps so one box moves the three cases ----
+// nz > 256 (a box dimension holds at most 256 elements): z split into (256, nz / 256)
+// map dimensions, so the box still lands as [row][case][nz] (k10_ld_c3 / k10_ld_1)
+static bool encode_map4_split(CUtensorMap* m, const float* base, const Geo& g, int box_rows, bool cases) {
+    PFN_encodeTiled_t fn = encode_fn();
+    if (!fn) return tma_check(CUDA_ERROR_NOT_FOUND, "entry point");
+    const cuuint32_t h = (cuuint32_t)(g.nz / 256);
+    const cuuint64_t dims5[5] = {256, h, 3, (cuuint64_t)g.ny, (cuuint64_t)g.nx};
+    const cuuint64_t strides5[4] = {256 * 4, (cuuint64_t)g.n * 4, (cuuint64_t)g.nz * 4, (cuuint64_t)g.pl * 4};
+    const cuuint32_t box5[5] = {256, h, 3, (cuuint32_t)box_rows, 1};
+    const cuuint64_t dims4[4] = {256, h, (cuuint64_t)g.ny, (cuuint64_t)g.nx};
+    const cuuint64_t strides4[3] = {256 * 4, (cuuint64_t)g.nz * 4, (cuuint64_t)g.pl * 4};
+    const cuuint32_t box4[4] = {256, h, (cuuint32_t)box_rows, 1};
+    const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    return tma_check(fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, cases ? 5 : 4, (void*)base, cases ? dims5 : dims4,
+                        cases ? strides5 : strides4, cases ? box5 : box4, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE), cases ? "5-d split" : "4-d split");
+}
+// single-field (z, y, x) map of the k10 march (split along z for nz > 256)
+static bool encode_map1(CUtensorMap* m, const float* base, const Geo& g, int box_rows) {
+    if (g.nz > 256) return encode_map4_split(m, base, g, box_rows, false);
+    return encode_map(m, base, g.nz, g.ny, g.nx, box_rows);
+}
 static bool encode_map4(CUtensorMap* m, const float* base, const Geo& g, int box_rows) {
+    if (g.nz > 256) return encode_map4_split(m, base, g, box_rows, true);
     PFN_encodeTiled_t fn = encode_fn();
     if (!fn) return tma_check(CUDA_ERROR_NOT_FOUND, "entry point");
     const cuuint64_t dims[4] = {(cuuint64_t)g.nz, 3, (cuuint64_t)g.ny, (cuuint64_t)g.nx};
@@ -3184,13 +3208,20 @@ static bool encode_map4(CUtensorMap* m, const float* base, const Geo& g, int box
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE), "4-d");
 }
 static int k10_ty_env();
-static int k10_ty(int nz) { return nz == 128 && (k10_ty_env() == 2 || k10_ty_env() == 8) ? k10_ty_env() : 512 / nz; }
+static int k10_ty(int nz) {
+    if (nz == 512) return 2;
+    return nz == 128 && (k10_ty_env() == 2 || k10_ty_env() == 8) ? k10_ty_env() : 512 / nz;
+}
 static long long k10_min_n() {           // smallest level on the k10 path (OTM_K10_MINN, tuning)
     static const long long v = getenv("OTM_K10_MINN") ? atoll(getenv("OTM_K10_MINN")) : 32768;
     return v;
 }
+static bool k10_512() {                 // nz = 512 on k10 (z-split TMA maps); OTM_K10_512=0 disables
+    static const bool v = !(getenv("OTM_K10_512") && atoi(getenv("OTM_K10_512")) == 0);
+    return v;
+}
 static bool k10_ok(const Geo& g, const LevelTemplate& lt) {
-    return lt.equal && (g.nz == 64 || g.nz == 128 || g.nz == 256) && g.ny % k10_ty(g.nz) == 0 &&
+    return lt.equal && (g.nz == 64 || g.nz == 128 || g.nz == 256 || (g.nz == 512 && k10_512())) && g.ny % k10_ty(g.nz) == 0 &&
            g.ny >= 2 * k10_ty(g.nz) && g.nx >= 2 && g.n >= k10_min_n();
 }
 // op3: 3-case operand (halo), d: D^-1 (smooth_res: halo, jacobi: centre), f3: jacobi right-hand side
@@ -3199,11 +3230,11 @@ static bool k10_maps(K10Maps& M, const Geo& g, const float* op3, const float* d,
     M.xa = 0;
     M.xb = g.nx;
     bool ok = encode_map4(&M.op_full, op3, g, TY + 2) && encode_map4(&M.op_main, op3, g, TY) &&
-              encode_map4(&M.op_halo, op3, g, 1) && encode_map(&M.k_full, kap, g.nz, g.ny, g.nx, TY + 1) &&
-              encode_map(&M.k_main, kap, g.nz, g.ny, g.nx, TY) && encode_map(&M.k_halo, kap, g.nz, g.ny, g.nx, 1);
+              encode_map4(&M.op_halo, op3, g, 1) && encode_map1(&M.k_full, kap, g, TY + 1) &&
+              encode_map1(&M.k_main, kap, g, TY) && encode_map1(&M.k_halo, kap, g, 1);
     if (d)
-        ok = ok && encode_map(&M.d_full, d, g.nz, g.ny, g.nx, TY + 2) && encode_map(&M.d_main, d, g.nz, g.ny, g.nx, TY) &&
-             encode_map(&M.d_halo, d, g.nz, g.ny, g.nx, 1);
+        ok = ok && encode_map1(&M.d_full, d, g, TY + 2) && encode_map1(&M.d_main, d, g, TY) &&
+             encode_map1(&M.d_halo, d, g, 1);
     else
         M.d_full = M.d_main = M.d_halo = M.k_main;
     if (f3)
@@ -3272,6 +3303,7 @@ static int k10_ty_env() {
             else if (k10_ty_env() == 8) CALL(128, 8, 1);                       \
             else CALL(128, 4, 2);                                              \
             break;                                                             \
+        case 512: CALL(512, 2, 1); break;                                      \
         default: CALL(256, 2, 2); break;                                       \
         }                                                                      \
     } while (0)

@@ -73,6 +73,30 @@ __device__ __forceinline__ void tma_load_4d(float* dst, const CUtensorMap* map, 
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_5d(float* dst, const CUtensorMap* map, int z, int h, int c, int y, int x,
+                                            uint64_t* bar) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n"
+        ::"r"(d), "l"(map), "r"(z), "r"(h), "r"(c), "r"(y), "r"(x), "r"(b)
+        : "memory");
+}
+
+// Row loads of the march.  A TMA box dimension holds at most 256 elements, so for
+// NZ > 256 the host splits z into (256, NZ / 256) map dimensions (strides 1 and 256
+// elements): the box still lands as [row][case][NZ] contiguous, the same layout.
+template <int NZ>
+__device__ __forceinline__ void k10_ld_c3(float* dst, const CUtensorMap* map, int y, int x, uint64_t* bar) {
+    if constexpr (NZ > 256) tma_load_5d(dst, map, 0, 0, 0, y, x, bar);
+    else tma_load_4d(dst, map, 0, 0, y, x, bar);
+}
+template <int NZ>
+__device__ __forceinline__ void k10_ld_1(float* dst, const CUtensorMap* map, int y, int x, uint64_t* bar) {
+    if constexpr (NZ > 256) tma_load_4d(dst, map, 0, 0, y, x, bar);
+    else tma_load_3d(dst, map, 0, y, x, bar);
+}
+
 // Thread mapping: thread tx of a row owns the vertex pair (z, z + H), H = NZ/2,
 // so every paired-fp32 (FFMA2) operand -- the pair's left, centre and right
 // neighbours -- is two independent 32-bit shared-memory loads straight into the
@@ -271,32 +295,32 @@ __device__ __forceinline__ void march10(const Geo& g, float s12f, const K10Maps&
             mbar_expect_tx(bars + k, (unsigned)G::SLOT_BYTES);
             if (G::HAS_FH) {
                 if (!seam) {
-                    tma_load_4d(S + G::F, &maps.f_full, 0, 0, y0 - 1, x, bars + k);
+                    k10_ld_c3<NZ>(S + G::F, &maps.f_full, y0 - 1, x, bars + k);
                 } else {
-                    tma_load_4d(S + G::F, &maps.f_halo, 0, 0, ym, x, bars + k);
-                    tma_load_4d(S + G::F + 3 * NZ, &maps.f_main, 0, 0, y0, x, bars + k);
-                    tma_load_4d(S + G::F + (TY + 1) * 3 * NZ, &maps.f_halo, 0, 0, yp, x, bars + k);
+                    k10_ld_c3<NZ>(S + G::F, &maps.f_halo, ym, x, bars + k);
+                    k10_ld_c3<NZ>(S + G::F + 3 * NZ, &maps.f_main, y0, x, bars + k);
+                    k10_ld_c3<NZ>(S + G::F + (TY + 1) * 3 * NZ, &maps.f_halo, yp, x, bars + k);
                 }
             }
             if (!seam) {
-                tma_load_4d(S + G::OP, &maps.op_full, 0, 0, y0 - 1, x, bars + k);
-                if (G::HAS_D) tma_load_3d(S + G::D, &maps.d_full, 0, y0 - 1, x, bars + k);
-                tma_load_3d(S + G::K, &maps.k_full, 0, y0 - 1, x, bars + k);
+                k10_ld_c3<NZ>(S + G::OP, &maps.op_full, y0 - 1, x, bars + k);
+                if (G::HAS_D) k10_ld_1<NZ>(S + G::D, &maps.d_full, y0 - 1, x, bars + k);
+                k10_ld_1<NZ>(S + G::K, &maps.k_full, y0 - 1, x, bars + k);
             } else {
-                tma_load_4d(S + G::OP, &maps.op_halo, 0, 0, ym, x, bars + k);
-                tma_load_4d(S + G::OP + 3 * NZ, &maps.op_main, 0, 0, y0, x, bars + k);
-                tma_load_4d(S + G::OP + (TY + 1) * 3 * NZ, &maps.op_halo, 0, 0, yp, x, bars + k);
+                k10_ld_c3<NZ>(S + G::OP, &maps.op_halo, ym, x, bars + k);
+                k10_ld_c3<NZ>(S + G::OP + 3 * NZ, &maps.op_main, y0, x, bars + k);
+                k10_ld_c3<NZ>(S + G::OP + (TY + 1) * 3 * NZ, &maps.op_halo, yp, x, bars + k);
                 if (G::HAS_D) {
-                    tma_load_3d(S + G::D, &maps.d_halo, 0, ym, x, bars + k);
-                    tma_load_3d(S + G::D + NZ, &maps.d_main, 0, y0, x, bars + k);
-                    tma_load_3d(S + G::D + (TY + 1) * NZ, &maps.d_halo, 0, yp, x, bars + k);
+                    k10_ld_1<NZ>(S + G::D, &maps.d_halo, ym, x, bars + k);
+                    k10_ld_1<NZ>(S + G::D + NZ, &maps.d_main, y0, x, bars + k);
+                    k10_ld_1<NZ>(S + G::D + (TY + 1) * NZ, &maps.d_halo, yp, x, bars + k);
                 }
-                tma_load_3d(S + G::K, &maps.k_halo, 0, ym, x, bars + k);
-                tma_load_3d(S + G::K + NZ, &maps.k_main, 0, y0, x, bars + k);
+                k10_ld_1<NZ>(S + G::K, &maps.k_halo, ym, x, bars + k);
+                k10_ld_1<NZ>(S + G::K + NZ, &maps.k_main, y0, x, bars + k);
             }
             if (G::HAS_C) {
-                tma_load_4d(S + G::F, &maps.f_main, 0, 0, y0, x, bars + k);
-                tma_load_3d(S + G::DC, &maps.d_main, 0, y0, x, bars + k);
+                k10_ld_c3<NZ>(S + G::F, &maps.f_main, y0, x, bars + k);
+                k10_ld_1<NZ>(S + G::DC, &maps.d_main, y0, x, bars + k);
             }
             ++sissue;
             ki = ki + 1 == STAGES ? 0 : ki + 1;
