@@ -2660,6 +2660,15 @@ static bool k6_maps(K6Maps& M, const Geo& g, const float* arr3, const float* d1,
 static bool encode_map64(CUtensorMap* m, const double* base, int nz, int ny, long long planes, int box_rows) {
     PFN_encodeTiled_t fn = encode_fn();
     if (!fn) return false;
+    if (nz > 256) {                       // z split into (256, nz / 256): box dims hold <= 256 elements
+        const cuuint64_t d4[4] = {256, (cuuint64_t)(nz / 256), (cuuint64_t)ny, (cuuint64_t)planes};
+        const cuuint64_t s4[3] = {256 * 8, (cuuint64_t)nz * 8, (cuuint64_t)nz * ny * 8};
+        const cuuint32_t b4[4] = {256, (cuuint32_t)(nz / 256), (cuuint32_t)box_rows, 1};
+        const cuuint32_t e4[4] = {1, 1, 1, 1};
+        return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)base, d4, s4, b4, e4, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
     const cuuint64_t dims[3] = {(cuuint64_t)nz, (cuuint64_t)ny, (cuuint64_t)planes};
     const cuuint64_t strides[2] = {(cuuint64_t)nz * 8, (cuuint64_t)nz * ny * 8};
     const cuuint32_t box[3] = {(cuuint32_t)nz, (cuuint32_t)box_rows, 1};
@@ -3045,8 +3054,10 @@ void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const d
         return;
     }
     static const bool old64 = getenv("OTM_RES64_OLD") != nullptr;
-    if (!fext && !old64 && k6_ok(g, lt)) {
-        const int tyd = 256 / g.nz;
+    static const bool r512 = !(getenv("OTM_RES64_512") && atoi(getenv("OTM_RES64_512")) == 0);
+    const bool w512 = r512 && lt.equal && g.nz == 512 && g.nx >= 2;
+    if (!fext && !old64 && (k6_ok(g, lt) || w512)) {
+        const int tyd = g.nz >= 256 ? 1 : 256 / g.nz;
         // tensor maps of the last (T, kappa, grid) are reused: encoding costs a few us of
         // host time per map, on the critical path between two host waits
         static R64Maps M;
@@ -3070,9 +3081,13 @@ void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const d
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             const long long units = 3LL * (g.ny / tyd) * g.nx;
             static const int bps = getenv("OTM_R64_BPS") ? atoi(getenv("OTM_R64_BPS")) : 2;
-            const unsigned blocks = (unsigned)std::min<long long>((long long)sms * bps, units);
+            const unsigned blocks = (unsigned)std::min<long long>((long long)sms * (g.nz > 256 ? 1 : bps), units);
             const dim3 blk((unsigned)g.nz, (unsigned)tyd);
             switch (g.nz) {
+            case 512:
+                s3_attr(k_res64w<512>, sm);
+                k_res64w<512><<<blocks, blk, sm, s>>>(g, lt, M, fmean, r32, red.partials, red.counter, out9);
+                break;
             case 64:
                 s3_attr(k_res64w<64>, sm);
                 k_res64w<64><<<blocks, blk, sm, s>>>(g, lt, M, fmean, r32, red.partials, red.counter, out9);

@@ -391,14 +391,16 @@ static_assert(kStagesR >= kAheadR + 2, "res64 ring too shallow");
 
 template <int NZ>
 struct R64Geo {
-    static constexpr int TYD = 256 / NZ;                   // rows per tile (one vertex per thread)
+    static constexpr int TYD = NZ >= 256 ? 1 : 256 / NZ;   // rows per tile (one vertex per thread)
+    static constexpr int THREADS = NZ * TYD;
+    static constexpr int MINB = THREADS > 256 ? 1 : 2;     // CTAs per SM
     static constexpr int TROWS = TYD + 2;
     static constexpr int KROWS = TYD + 1;
     static constexpr int SLOT = (TROWS + KROWS) * NZ;     // doubles
 };
 
 __host__ __device__ inline size_t r64_smem_bytes(int nz) {
-    const int tyd = 256 / nz;
+    const int tyd = nz >= 256 ? 1 : 256 / nz;
     return (size_t)kStagesR * (2 * tyd + 3) * nz * 8 + kStagesR * 8;
 }
 
@@ -407,8 +409,24 @@ struct R64Maps {
     CUtensorMap Km, Kh;      // kappa (fp64)
 };
 
+// nz = 512: 512 threads, 1 CTA per SM, and z-split (256, 2) maps (a TMA box
+// dimension holds at most 256 elements; the box still lands as [row][nz])
+__device__ __forceinline__ void r64_tma4(void* dst, const CUtensorMap* map, int z, int h, int y, int x, uint64_t* bar) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n"
+        ::"r"(d), "l"(map), "r"(z), "r"(h), "r"(y), "r"(x), "r"(b)
+        : "memory");
+}
 template <int NZ>
-__global__ void __launch_bounds__(256, 2) k_res64w(Geo g, LevelTemplate lt, const __grid_constant__ R64Maps maps,
+__device__ __forceinline__ void r64_ld(double* dst, const CUtensorMap* map, int y, int x, uint64_t* bar) {
+    if constexpr (NZ > 256) r64_tma4(dst, map, 0, 0, y, x, bar);
+    else tma_load_3d(reinterpret_cast<float*>(dst), map, 0, y, x, bar);
+}
+
+template <int NZ>
+__global__ void __launch_bounds__(R64Geo<NZ>::THREADS, R64Geo<NZ>::MINB) k_res64w(Geo g, LevelTemplate lt, const __grid_constant__ R64Maps maps,
                                                    const double* __restrict__ fmean, float* __restrict__ r32,
                                                    double* partials, unsigned* counter, double* out9) {
     using RG = R64Geo<NZ>;
@@ -457,12 +475,12 @@ __global__ void __launch_bounds__(256, 2) k_res64w(Geo g, LevelTemplate lt, cons
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             mbar_expect_tx(bars + k, plane_bytes);
             const int xc = c * g.nx + x;
-            tma_load_3d(reinterpret_cast<float*>(S + NZ), &maps.Tm, 0, y0, xc, bars + k);
-            tma_load_3d(reinterpret_cast<float*>(S), &maps.Th, 0, ym, xc, bars + k);
-            tma_load_3d(reinterpret_cast<float*>(S + (TYD + 1) * NZ), &maps.Th, 0, yp, xc, bars + k);
+            r64_ld<NZ>(S + NZ, &maps.Tm, y0, xc, bars + k);
+            r64_ld<NZ>(S, &maps.Th, ym, xc, bars + k);
+            r64_ld<NZ>(S + (TYD + 1) * NZ, &maps.Th, yp, xc, bars + k);
             double* K = S + TROWS * NZ;
-            tma_load_3d(reinterpret_cast<float*>(K + NZ), &maps.Km, 0, y0, x, bars + k);
-            tma_load_3d(reinterpret_cast<float*>(K), &maps.Kh, 0, ym, x, bars + k);
+            r64_ld<NZ>(K + NZ, &maps.Km, y0, x, bars + k);
+            r64_ld<NZ>(K, &maps.Kh, ym, x, bars + k);
         };
         auto arrive = [&](int s) -> const double* {
             const int k = (seq + s) % kStagesR;
