@@ -1367,13 +1367,17 @@ __global__ void k_submean(long long n, double* __restrict__ T, const double* __r
 // pairs (00,11,22,01,12,02).  K0 w = (5 w + N1 w - sum w) / 12.
 __device__ __forceinline__ void element_energies(const Geo& g, long long e, const double* __restrict__ T,
                                                  double (&E)[6]) {
-    const int x = (int)(e / g.pl), rem = (int)(e - (long long)x * g.pl);
-    const int y = rem / g.nz, z = rem - y * g.nz;
-    const int xp = wrap_p(x, g.nx), yp = wrap_p(y, g.ny), zp = wrap_p(z, g.nz);
-    long long vid[8];
+    // 32-bit index arithmetic (every field here has < 2^31 vertices): the 64-bit
+    // divisions and per-corner 64-bit products were a third of the kernel's instructions
+    const unsigned ue = (unsigned)e, upl = (unsigned)g.pl, unz = (unsigned)g.nz;
+    const unsigned x = ue / upl, rem = ue - x * upl;
+    const unsigned y = rem / unz, z = rem - y * unz;
+    const unsigned xp = x + 1 == (unsigned)g.nx ? 0u : x + 1, yp = y + 1 == (unsigned)g.ny ? 0u : y + 1,
+                   zp = z + 1 == unz ? 0u : z + 1;
+    const unsigned ox[2] = {x * upl, xp * upl}, oy[2] = {y * unz, yp * unz}, oz[2] = {z, zp};
+    unsigned vid[8];
 #pragma unroll
-    for (int a = 0; a < 8; ++a)
-        vid[a] = ((long long)((a & 1) ? xp : x) * g.ny + ((a >> 1) & 1 ? yp : y)) * g.nz + ((a >> 2) & 1 ? zp : z);
+    for (int a = 0; a < 8; ++a) vid[a] = ox[a & 1] + oy[(a >> 1) & 1] + oz[(a >> 2) & 1];
     double w[3][8], kw[3][8];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
