@@ -1402,7 +1402,7 @@ __device__ __forceinline__ void element_energies(const Geo& g, long long e, cons
     }
 }
 
-__global__ void k_tensor(Geo g, const double* __restrict__ T, const double* __restrict__ kap, double* partials,
+__global__ void __launch_bounds__(256, 3) k_tensor(Geo g, const double* __restrict__ T, const double* __restrict__ kap, double* partials,
                          unsigned* counter, double* out) {
     double acc[6] = {0, 0, 0, 0, 0, 0};
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < g.n;
@@ -1427,7 +1427,7 @@ __global__ void k_pair_energy(Geo g, const double* __restrict__ T, double* __res
 }
 
 // sens_f = kappa'(rho_f) * (dG . E) / M   (homogenize.py:143-160, element.py:97-100)
-__global__ void k_sens(Geo g, const double* __restrict__ T, const double* __restrict__ rf, SimpParams sp,
+__global__ void __launch_bounds__(256, 4) k_sens(Geo g, const double* __restrict__ T, const double* __restrict__ rf, SimpParams sp,
                        Dg dG, double* __restrict__ sens) {
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= g.n) return;
