@@ -110,9 +110,11 @@ __global__ void __launch_bounds__(256) k_filter_b(Geo g, FilterTaps taps, const 
     double acc3[3] = {0.0, 0.0, 0.0};
     if (i < npair) {
         const long long vp = i * 2;
-        const int x = (int)(vp / g.pl), rem = (int)(vp - (long long)x * g.pl);
+        // 32-bit index arithmetic (fields < 2^31 vertices; see element_energies)
+        const unsigned uv = (unsigned)vp, upl = (unsigned)g.pl;
+        const int x = (int)(uv / upl), rem = (int)(uv - (unsigned)x * upl);
         const int y = rem / g.nz, z = rem - y * g.nz;
-        const long long xo[3] = {(long long)wrap_m(x, g.nx) * g.pl, (long long)x * g.pl, (long long)wrap_p(x, g.nx) * g.pl};
+        const unsigned xo[3] = {(unsigned)wrap_m(x, g.nx) * upl, (unsigned)x * upl, (unsigned)wrap_p(x, g.nx) * upl};
         const int yo[3] = {wrap_m(y, g.ny) * g.nz, y * g.nz, wrap_p(y, g.ny) * g.nz};
         const int zm = z == 0 ? g.nz - 1 : z - 1, zp2 = z + 2 == g.nz ? 0 : z + 2;
         double t[3][3][4];
@@ -120,7 +122,7 @@ __global__ void __launch_bounds__(256) k_filter_b(Geo g, FilterTaps taps, const 
         for (int p = 0; p < 3; ++p)
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
-                const double* row = in + xo[p] + yo[j];
+                const double* row = in + (xo[p] + (unsigned)yo[j]);
                 t[p][j][0] = __ldg(row + zm);
                 const double2 m = __ldg(reinterpret_cast<const double2*>(row + z));
                 t[p][j][1] = m.x;
