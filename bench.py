@@ -75,6 +75,15 @@ class Clocks:
         except Exception:
             self.proc = None
 
+    def mark(self):
+        """Samples before this call (warm-up) are dropped by stop()."""
+        self.skip = 0
+        try:
+            with open(self.path) as fh:
+                self.skip = sum(1 for _ in fh)
+        except OSError:
+            pass
+
     def stop(self):
         if self.proc is None:
             return None
@@ -85,7 +94,9 @@ class Clocks:
             self.proc.kill()
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
+        for k, line in enumerate(open(self.path)):
+            if k < getattr(self, "skip", 0):
+                continue
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
                 continue
@@ -254,13 +265,17 @@ def run_gpu(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
+    # the clock sampler starts before the warm-up: nvidia-smi's own start-up (NVML
+    # init) stalled CUDA API calls of the design loop for up to ~0.3 s when it landed
+    # inside a timed step; only the samples taken from the timed region on are kept
+    clocks = Clocks(local)
+    clocks.start()
     for _ in range(args.warmup):
         one_structure()
     barrier()
     # ---- timed region (device events on the library stream, no instrumentation) ----
     launches0 = lib.otm_launch_count(ctx.h)
-    clocks = Clocks(local)
-    clocks.start()
+    clocks.mark()
     step_ms = []
     iters_done = []
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
