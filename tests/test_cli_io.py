@@ -102,7 +102,6 @@ class TestCliParsing:
         assert proc.returncode == 0 and "run" in proc.stdout and "gallery" in proc.stdout
 
 
-@pytest.mark.usefixtures()
 class TestCliGpu:
     pytestmark = gpu
 
