@@ -63,8 +63,6 @@ struct otm_ctx {
     SimpParams sp{};
     double* kap64 = nullptr;
     double* T64 = nullptr;
-    double* Tprev = nullptr;     // previous design iteration's fields (warm-start extrapolation)
-    int extrap_count = 0;
     double* rho_f = nullptr;   // last filtered density used by otm_build (for sensitivities)
     double* sensf = nullptr;   // design-loop scratch: sensitivity wrt rho_f, then wrt rho
     double* sens = nullptr;
@@ -82,25 +80,10 @@ struct otm_ctx {
     bool built = false;
     bool no_loop_graph = getenv("OTM_NO_LOOP_GRAPH") != nullptr;   // ncu cannot profile conditional graphs
     bool eager = getenv("OTM_EAGER") != nullptr;                    // with OTM_NO_LOOP_GRAPH: no inner graph
-    // single-CTA V-cycle tail for the levels <= OTM_TAIL_VERTS vertices: opt-in, measured
-    // slower than per-level launches at 512 and 4096
-    bool no_tail = getenv("OTM_TAIL_VERTS") == nullptr;
-    long long tail_verts = getenv("OTM_TAIL_VERTS") ? atoll(getenv("OTM_TAIL_VERTS")) : 0;
-    long long ctail_verts = getenv("OTM_CTAIL") ? atoll(getenv("OTM_CTAIL")) : 0;
     // single-launch bottom (8^3, or 16^3 with OTM_VBOT=16 -- measured slower: one SM is
     // too slow for the 16^3 stencils -- down to the 4^3 direct solve in shared memory);
     // OTM_VBOT=0 off, OTM_VBOT=8 only from 8^3
     int vbot_max = getenv("OTM_VBOT") ? atoi(getenv("OTM_VBOT")) : 8;
-    // OTM_VT32=1: the 32^3 -> 4^3 tail as one 16-CTA cluster launch (otm_vtail32.cuh).
-    // Correct (same operator, tests/test_preconditioner_gpu.py) but measured SLOWER:
-    // 62 vs 45 us per 64^3 V-cycle -- 16 SMs run what the per-level launches spread
-    // over 148, and the bottom on CTA 0 idles the other 15 at the cluster barriers.
-    bool vt32 = getenv("OTM_VT32") && atoi(getenv("OTM_VT32")) == 1;
-    // OTM_NOZ0=1: on k10 levels the pre-smoothing does not store z0 and the post-smoothing
-    // rebuilds it from f, D^-1 and P e (24 B/vertex less HBM traffic per V-cycle, but
-    // measured 11 us SLOWER per 128^3 V-cycle: the wider shared-memory slots halve the
-    // ring depth and add loads to a latency-bound kernel) -- opt-in experiment
-    bool keep_z0 = getenv("OTM_NOZ0") == nullptr;
     bool warm = false;
     bool have_T = false;
     bool oc_pending = false;     // a cooperative OC search result still in flight to h + 384
@@ -278,7 +261,6 @@ void prof_record(otm_ctx* ctx, int cls, double bytes, bool begin, int& slot_idx)
 // Stream work of one inner PCG iteration (captured into a graph).
 int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false, bool vonly = false) {
     cudaStream_t s = ctx->stream;
-    set_k8_work(ctx->red.counter + 4);
     const int nl = (int)ctx->L.size();
     const float om0 = (float)ctx->P.jacobi_omega;
     // Jacobi weight of the coarse levels: 1.25 (the rediscretised child-mean operators
@@ -293,19 +275,9 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false, bool vonly = fa
     int launches = 0;
     if (prof) prof_record(ctx, kProfVcycle, 0.0, true, sl_v);
     double vbytes = 0.0;
-    // first level handled by the single-CTA tail (all coarser levels are tail too)
-    // (or the cooperative multi-CTA tail, OTM_CTAIL=<max vertices of its first level>)
-    const bool coop = ctx->ctail_verts > 0;
-    const long long tv = coop ? ctx->ctail_verts : ctx->tail_verts;
-    int tl = nl - 1;
-    while (tl > 0 && ctx->L[tl - 1].g.n <= tv && nl - (tl - 1) <= kTailMaxLevels) --tl;
-    if (coop)
-        for (int l = tl + 1; l < nl; ++l)
-            if (!(ctx->L[l].cf[0] && ctx->L[l].cf[1] && ctx->L[l].cf[2])) tl = l;   // 3-D coarsening only
-    bool use_tail = tl < nl - 1 && (coop || !ctx->no_tail);
     // first level of the single-launch bottom: N^3 (N = 16 or 8) halving to 4^3, equal scales
     int vb = -1;
-    for (int l = 1; l < nl && ctx->vbot_max >= 8 && !use_tail; ++l) {
+    for (int l = 1; l < nl && ctx->vbot_max >= 8; ++l) {
         const Geo& g = ctx->L[l].g;
         const int N = g.nx;
         if (!((N == 16 && ctx->vbot_max >= 16) || N == 8) || g.ny != N || g.nz != N) continue;
@@ -315,70 +287,19 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false, bool vonly = fa
                                        ctx->L[k].g.ny == (N >> (k - l)) && ctx->L[k].g.nz == (N >> (k - l));
         if (ok) { vb = l; break; }
     }
-    // first level of the cluster tail: 32^3 halving to 4^3 (4 levels), equal scales, not level 0
-    int vt = -1;
-    if (ctx->vt32 && !use_tail && nl >= 5) {
-        const int l = nl - 4;
-        bool ok = true;
-        for (int k = l; k < nl; ++k)
-            ok = ok && ctx->L[k].lt.equal && ctx->L[k].g.nx == (32 >> (k - l)) && ctx->L[k].g.ny == (32 >> (k - l)) &&
-                 ctx->L[k].g.nz == (32 >> (k - l));
-        if (ok) vt = l;
-    }
-    int top = use_tail ? tl : (vb > 0 ? vb : nl - 1);     // levels [0, top) are launched per level
-    if (vt > 0) top = vt;
-    bool noz0[64] = {};
+    const int top = vb > 0 ? vb : nl - 1;     // levels [0, top) are launched per level
     for (int l = 0; l < top; ++l) {
         LevelBuf& A = ctx->L[l];
         LevelBuf& B = ctx->L[l + 1];
-        noz0[l] = !ctx->keep_z0 && B.cf[0] && B.cf[1] && B.cf[2] && k10_level(A.g, A.lt);
-        const double bsm = (noz0[l] ? 32.0 : 44.0) * (double)A.g.n;
+        const double bsm = 44.0 * (double)A.g.n;
         if (prof && l == 0) prof_record(ctx, kProfL0Stencil, bsm, true, sl);
-        if (!noz0[l] || !launch_smooth_res_nz(s, A.g, A.lt, A.kap, A.f, A.dinv, oml(l), A.res)) {
-            noz0[l] = false;
-            launch_smooth_res(s, A.g, A.lt, A.kap, A.f, A.dinv, oml(l), A.z, A.res);
-        }
+        launch_smooth_res(s, A.g, A.lt, A.kap, A.f, A.dinv, oml(l), A.z, A.res);
         if (prof && l == 0) prof_record(ctx, kProfL0Stencil, 0, false, sl);
         launch_restrict(s, A.g, B.g, B.cf, A.res, B.f);
         vbytes += bsm + 12.0 * A.g.n + 12.0 * B.g.n;
         launches += 2;
     }
-    if (use_tail) {
-        TailArgs ta;
-        ta.nlev = nl - tl;
-        ta.omega = om;
-        ta.G = ctx->G;
-        for (int k = 0; k < ta.nlev; ++k) {
-            const LevelBuf& B = ctx->L[tl + k];
-            TailLevel& T = ta.L[k];
-            T.g = B.g;
-            for (int a = 0; a < 3; ++a) T.cf[a] = B.cf[a];
-            T.lt = B.lt;
-            T.kap = B.kap; T.dinv = B.dinv; T.f = B.f; T.z = B.z; T.res = B.res;
-        }
-        if (coop) {
-            if (launch_vtail_coop(s, ta)) return OTM_ECUDA;
-        } else {
-            launch_vtail(s, ta);
-        }
-        launches += 1;
-    } else if (vt > 0 && launch_vtail32(s, [&] {
-                   VTailArgs a{};
-                   a.omega = om;
-                   for (int k = 0; k < 4; ++k) a.s12[k] = (float)ctx->L[vt + k].lt.s12;
-                   for (int k = 0; k < 3; ++k) {
-                       a.kap[k] = ctx->L[vt + k].kap;
-                       a.dinv[k] = ctx->L[vt + k].dinv;
-                   }
-                   a.f32 = ctx->L[vt].f;
-                   a.out32 = ctx->L[vt].res;
-                   a.G = ctx->G;
-                   return a;
-               }())) {
-        launches += 1;
-    } else if (vt > 0) {
-        return fail(ctx, OTM_ECUDA, "cluster tail launch failed (unset OTM_VT32)");
-    } else if (vb > 0) {
+    if (vb > 0) {
         VBotArgs va{};
         va.nlev = nl - vb;
         va.omega = om;
@@ -402,24 +323,12 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false, bool vonly = fa
         LevelBuf& A = ctx->L[l];
         LevelBuf& B = ctx->L[l + 1];
         const double bj = 44.0 * (double)A.g.n;
-        if (noz0[l]) {
-            launch_prolong_assign(s, A.g, B.g, B.res, A.z);
-            if (prof && l == 0) prof_record(ctx, kProfL0Stencil, bj, true, sl);
-            launch_jacobi_p(s, A.g, A.lt, A.kap, A.z, A.f, A.dinv, oml(l), A.res, l == 0 && !vonly, ctx->red, ctx->sc);
-        } else {
-            launch_prolong(s, A.g, B.g, B.cf, B.res, A.z);
-            if (prof && l == 0) prof_record(ctx, kProfL0Stencil, bj, true, sl);
-            launch_jacobi(s, A.g, A.lt, A.kap, A.z, A.f, A.dinv, oml(l), A.res, l == 0 && !vonly, ctx->red, ctx->sc);
-        }
+        launch_prolong(s, A.g, B.g, B.cf, B.res, A.z);
+        if (prof && l == 0) prof_record(ctx, kProfL0Stencil, bj, true, sl);
+        launch_jacobi(s, A.g, A.lt, A.kap, A.z, A.f, A.dinv, oml(l), A.res, l == 0 && !vonly, ctx->red, ctx->sc);
         if (prof && l == 0) prof_record(ctx, kProfL0Stencil, 0, false, sl);
         vbytes += 12.0 * B.g.n + 24.0 * A.g.n + bj;
         launches += 2;
-    }
-    if (use_tail && tl == 0 && !vonly) {
-        // the whole hierarchy fits the tail: r.z and beta still come from a level-0 pass
-        LevelBuf& A = ctx->L[0];
-        launch_jacobi(s, A.g, A.lt, A.kap, A.res, A.f, A.dinv, 0.0f, A.z, true, ctx->red, ctx->sc);
-        launches += 1;
     }
     if (nl == 1 && !vonly) {
         // single-level hierarchy: the coarse solve is the whole preconditioner; still need r.z
@@ -432,7 +341,7 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false, bool vonly = fa
         ctx->slots[sl_v].bytes = vbytes;
     }
     if (vonly) return OTM_OK;                  // V-cycle only: z in L[0].res
-    float* z0 = (nl == 1 || (use_tail && tl == 0)) ? ctx->L[0].z : ctx->L[0].res;
+    float* z0 = nl == 1 ? ctx->L[0].z : ctx->L[0].res;
     launch_pupd(s, ctx->g0.n, z0, ctx->p, ctx->d, ctx->sc);
     if (prof) prof_record(ctx, kProfL0Stencil, 28.0 * n0, true, sl);
     launch_spmv(s, ctx->g0, ctx->L[0].lt, ctx->L[0].kap, ctx->p, ctx->q, ctx->red, ctx->sc);
@@ -782,7 +691,6 @@ static void oc_settle(otm_ctx* ctx);
 
 int otm_destroy(otm_ctx* ctx) {
     if (!ctx) return OTM_OK;
-    set_k8_work(nullptr);                 // re-set by the next enqueue of any context
     if (ctx->oc_pending) {
         cudaStreamSynchronize(ctx->stream);
         oc_settle(ctx);
@@ -800,7 +708,7 @@ int otm_destroy(otm_ctx* ctx) {
     if (ctx->gexec_build) cudaGraphExecDestroy(ctx->gexec_build);
     for (auto& s : ctx->slots) { cudaEventDestroy(s.a); cudaEventDestroy(s.b); }
     auto F = [](void* p) { if (p) cudaFree(p); };
-    F(ctx->kap64); F(ctx->T64); F(ctx->Tprev); F(ctx->rho_f); F(ctx->sensf); F(ctx->sens); F(ctx->r); F(ctx->p); F(ctx->q); F(ctx->d);
+    F(ctx->kap64); F(ctx->T64); F(ctx->rho_f); F(ctx->sensf); F(ctx->sens); F(ctx->r); F(ctx->p); F(ctx->q); F(ctx->d);
     for (size_t l = 0; l < ctx->L.size(); ++l) {
         F(ctx->L[l].kap); F(ctx->L[l].dinv); F(ctx->L[l].z); F(ctx->L[l].res);
         if (l > 0) F(ctx->L[l].f);
@@ -1382,16 +1290,6 @@ int otm_run_step(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, dou
     int rc = build_levels(ctx, true);
     if (rc) return rc;
     ctx->warm = st->warm != 0;
-    static const double theta = getenv("OTM_EXTRAP") ? atof(getenv("OTM_EXTRAP")) : 0.0;
-    if (theta != 0.0 && ctx->warm) {
-        if (!ctx->Tprev) {
-            CK(dalloc(ctx, &ctx->Tprev, 3 * n));
-            CK(cudaMemcpyAsync(ctx->Tprev, ctx->T64, 3 * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-        } else {
-            launch_extrap(s, 3 * n, ctx->T64, ctx->Tprev, theta);
-            ctx->launches++;
-        }
-    }
     int cycles = 0;
     double resid[3];
     rc = otm_solve(ctx, nullptr, cfg->solver_tol, cfg->max_vcycles, &cycles, resid);

@@ -6,7 +6,6 @@
 
 #include "otm_common.cuh"
 #include "otm_vbottom.cuh"
-#include "otm_vtail32.cuh"
 
 namespace otm {
 
@@ -89,32 +88,8 @@ struct FilterSetup {
     double* wts_dev;
 };
 
-// Tail of the V-cycle (all levels with few vertices) run by one CTA.
-constexpr int kTailMaxLevels = 6;
-constexpr int kTailMaxVerts = 4096;
-struct TailLevel {
-    Geo g;
-    int cf[3];            // axes coarsened from the finer level
-    LevelTemplate lt;
-    float* kap;
-    float* dinv;
-    float* f;
-    float* z;
-    float* res;
-};
-struct TailArgs {
-    int nlev;             // levels in the tail; the last one is the coarsest (direct solve)
-    float omega;
-    const float* G;
-    TailLevel L[kTailMaxLevels];
-};
-
 int stencil_chunks(const Geo& g, int* xb);
-void launch_vtail(cudaStream_t s, const TailArgs& a);
-void launch_vbottom(cudaStream_t s, int N, const VBotArgs& a);
-bool launch_vtail32(cudaStream_t s, const VTailArgs& a);   // false: unavailable, nothing launched   // N = 16 or 8
-int launch_vtail_coop(cudaStream_t s, const TailArgs& a);   // 0 on success
-void set_k8_work(unsigned* p);   // work counter (2 unsigned, zeroed) used by the k8 kernels enqueued next
+void launch_vbottom(cudaStream_t s, int N, const VBotArgs& a);   // N = 16 or 8
 
 void launch_filter(cudaStream_t s, const Geo& g, const FilterSetup& fs, int adjoint, const double* in,
                    double* out, Red& red);
@@ -142,12 +117,6 @@ void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const 
                    const float* f, const float* dinv, float omega, float* zout, bool dot, Red& red,
                    PcgScalars* sc);
 bool k10_level(const Geo& g, const LevelTemplate& lt);
-bool launch_smooth_res_nz(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* f,
-                          const float* dinv, float omega, float* res);
-bool launch_jacobi_p(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* pe,
-                     const float* f, const float* dinv, float omega, float* zout, bool dot, Red& red,
-                     PcgScalars* sc);
-void launch_prolong_assign(cudaStream_t s, const Geo& f, const Geo& c, const float* zc, float* zf);
 bool launch_k10_range(cudaStream_t s, int op, const Geo& g, const LevelTemplate& lt, int xa, int xb,
                       const float* kap, const float* a, const float* f, const float* dinv, float omega, float* o1,
                       float* o2, bool dot, Red& red, PcgScalars* sc);
@@ -161,7 +130,6 @@ void launch_upd(cudaStream_t s, long long n, float* r, const float* q, Red& red,
 void launch_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* res, float* fc);
 void launch_prolong(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* zc, float* zf);
 void launch_loop_ctl(cudaStream_t s, PcgScalars* sc, unsigned long long handle);
-void launch_extrap(cudaStream_t s, long long n3, double* T, double* Tprev, double theta);
 void launch_Tupd(cudaStream_t s, long long n, double* T, const float* d, const float* p, const PcgScalars* sc);
 void launch_submean_means(cudaStream_t s, long long n, double* T, const double* means);
 void launch_submean(cudaStream_t s, long long n, double* T, const double* sumT);

@@ -3,13 +3,8 @@
 // (paths relative to /root/reference/pkg/src/opentm/).
 #include "otm_common.cuh"
 #include "otm_internal.h"
-#include "otm_stencil2.cuh"
-#include "otm_stencil3.cuh"
-#include "otm_stencil4.cuh"
-#include "otm_stencil6.cuh"
-#include "otm_stencil8.cuh"
+#include "otm_res64w.cuh"
 #include "otm_stencil10.cuh"
-#include "otm_vtail32.cuh"
 
 #ifndef OTM_MINB
 #define OTM_MINB 2   // min resident blocks of the fp32 fast-path stencils (register cap 128)
@@ -536,92 +531,6 @@ __global__ void __launch_bounds__(128) k_res64(Geo g, int xb, LevelTemplate lt, 
 #pragma unroll
                 for (int i = 0; i < 4; ++i) k[0][i] = k[1][i];
             }
-        }
-    }
-    reduce_finalize<9>(acc, partials, counter, red_out);
-}
-
-// fp64 defect, high-parallelism form: one thread per (case, x, y, z pair), every
-// operand / factor load issued up front (double2 where aligned), no x-march.
-// Requires nz even.  Same outputs and sums as k_res64.
-__global__ void __launch_bounds__(256) k_res64b(Geo g, LevelTemplate lt, const double* __restrict__ kap,
-                                                const double* __restrict__ T, const double* __restrict__ fext,
-                                                const double* __restrict__ fmean, float* __restrict__ r32,
-                                                double* partials, unsigned* counter, double* red_out) {
-    const long long npair = g.n >> 1;
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    double acc[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) acc[q] = 0.0;
-    if (i < 3 * npair) {
-        const int c = (int)(i / npair);
-        const long long vp = (i - (long long)c * npair) * 2;     // even vertex index
-        const int x = (int)(vp / g.pl), rem = (int)(vp - (long long)x * g.pl);
-        const int y = rem / g.nz, z = rem - y * g.nz;
-        const long long xo[3] = {(long long)wrap_m(x, g.nx) * g.pl, (long long)x * g.pl, (long long)wrap_p(x, g.nx) * g.pl};
-        const int yo[3] = {wrap_m(y, g.ny) * g.nz, y * g.nz, wrap_p(y, g.ny) * g.nz};
-        const int zm = z == 0 ? g.nz - 1 : z - 1, zp2 = z + 2 == g.nz ? 0 : z + 2;
-        const double* Tc = T + (size_t)c * g.n;
-        double t[3][3][4], k[2][2][3];
-#pragma unroll
-        for (int p = 0; p < 3; ++p)
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                const double* row = Tc + xo[p] + yo[j];
-                t[p][j][0] = __ldg(row + zm);
-                const double2 m = __ldg(reinterpret_cast<const double2*>(row + z));
-                t[p][j][1] = m.x;
-                t[p][j][2] = m.y;
-                t[p][j][3] = __ldg(row + zp2);
-            }
-#pragma unroll
-        for (int p = 0; p < 2; ++p)
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const double* row = kap + xo[p] + yo[j];
-                k[p][j][0] = __ldg(row + zm);
-                const double2 m = __ldg(reinterpret_cast<const double2*>(row + z));
-                k[p][j][1] = m.x;
-                k[p][j][2] = m.y;
-            }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {           // vertex z + h
-            double w[3][9], ks[2][4];
-#pragma unroll
-            for (int p = 0; p < 3; ++p)
-#pragma unroll
-                for (int j = 0; j < 3; ++j)
-#pragma unroll
-                    for (int m = 0; m < 3; ++m) w[p][j * 3 + m] = t[p][j][h + m];
-#pragma unroll
-            for (int p = 0; p < 2; ++p)
-#pragma unroll
-                for (int j = 0; j < 2; ++j)
-#pragma unroll
-                    for (int m = 0; m < 2; ++m) ks[p][j * 2 + m] = k[p][j][h + m];
-            double kt;
-            if (lt.equal) {
-                const KSum<double> sm = ksum<double>(ks);
-                kt = apply_compact<double>(w, ks, sm, lt.s12);
-            } else {
-                kt = apply_generic<double>(w, ks, lt.kt);
-            }
-            double f;
-            if (fext) {
-                f = __ldg(fext + (size_t)c * g.n + vp + h);
-            } else {
-                f = 0.0;
-#pragma unroll
-                for (int a = 0; a < 8; ++a) {
-                    const int q = 1 - (a & 1), jj = 1 - ((a >> 1) & 1), kk = 1 - ((a >> 2) & 1);
-                    f = __dadd_rn(f, __dmul_rn(lt.f0[a * 3 + c], ks[q][jj * 2 + kk]));
-                }
-            }
-            const double r = (f - fmean[c]) - kt;
-            r32[(size_t)c * g.n + vp + h] = (float)r;
-            acc[c] += r * r;
-            acc[3 + c] += f * f;
-            acc[6 + c] += t[1][1][1 + h];
         }
     }
     reduce_finalize<9>(acc, partials, counter, red_out);
@@ -1184,54 +1093,6 @@ __global__ void __launch_bounds__(256) k_restrict3w(Geo f, Geo c, const float* _
     fc[i] = s;
 }
 
-// Restriction marching in x (c.nz % 32 == 0): a thread owns coarse (case, Y, Z) for
-// XC consecutive coarse planes; the y/z-restricted value of every fine plane is
-// computed once (3 float2 row loads + one shuffle) and shared by the two coarse
-// planes it feeds, so each coarse vertex costs 6 row loads instead of 9.  Measured
-// slower than k_restrict3w (10.7 vs 9.8 us at 128^3, 86 vs 72 us at 256^3: the serial
-// march costs more parallelism than the saved L2 reads are worth); OTM_RESTRICT_X=1.
-template <int XC>
-__global__ void __launch_bounds__(256) k_restrict3x(Geo f, Geo c, const float* __restrict__ res,
-                                                    float* __restrict__ fc) {
-    pdl_wait();
-    const long long cols = 3LL * c.pl;
-    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const int nch = (c.nx + XC - 1) / XC;
-    if (t >= cols * nch) return;                     // cols % 32 == 0: whole warps only
-    const int ch = (int)(t / cols);
-    const long long col = t - (long long)ch * cols;
-    const int cc = (int)(col / c.pl);
-    const int rem = (int)(col - (long long)cc * c.pl);
-    const int Y = rem / c.nz, Z = rem - Y * c.nz;
-    const int lane = threadIdx.x & 31;
-    const int ys[3] = {wrap_m(2 * Y, f.ny) * f.nz, 2 * Y * f.nz, wrap_p(2 * Y, f.ny) * f.nz};
-    const int zm = wrap_m(2 * Z, f.nz);
-    const float* r = res + (size_t)cc * f.n;
-    auto yz = [&](int xf) {                          // y/z full weighting of fine plane xf
-        const float* pl = r + (long long)xf * f.pl;
-        float s = 0.f;
-#pragma unroll
-        for (int b = 0; b < 3; ++b) {
-            const float* row = pl + ys[b];
-            const float2 m = __ldg(reinterpret_cast<const float2*>(row + 2 * Z));
-            float left = __shfl_up_sync(0xffffffffu, m.y, 1);
-            if (lane == 0) left = __ldg(row + zm);
-            const float sz = 0.25f * left + 0.5f * m.x + 0.25f * m.y;
-            s += (b == 1 ? 0.5f : 0.25f) * sz;
-        }
-        return s;
-    };
-    const int X0 = ch * XC, X1 = min(c.nx, X0 + XC);
-    float prev = yz(wrap_m(2 * X0, f.nx));           // fine plane 2 X0 - 1
-    float* out = fc + (size_t)cc * c.n + (long long)Y * c.nz + Z;
-    for (int X = X0; X < X1; ++X) {
-        const float a = yz(2 * X);
-        const float b = yz(wrap_p(2 * X, f.nx));
-        out[(long long)X * c.pl] = 0.25f * prev + 0.5f * a + 0.25f * b;
-        prev = b;
-    }
-}
-
 // trilinear prolongation + correction, every axis coarsened: 8 coarse loads, weights 0/0.5/1
 __global__ void __launch_bounds__(256) k_prolong3(Geo f, Geo c, const float* __restrict__ zc,
                                                   float* __restrict__ zf) {
@@ -1328,16 +1189,6 @@ __global__ void k_loop_ctl(PcgScalars* sc, cudaGraphConditionalHandle h) {
 }
 
 // Warm-start extrapolation across design iterations: T <- T + theta (T - T_prev), T_prev <- T.
-__global__ void k_extrap(long long n3, double* __restrict__ T, double* __restrict__ Tprev, double theta) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n3) return;
-    const double t = T[i];
-    T[i] = t + theta * (t - Tprev[i]);
-    Tprev[i] = t;
-}
-
-// T += d + alpha p (fp64 accumulation of the fp32 correction; alpha p of the last
-// PCG iteration has not been folded into d by a following k_pupd)
 __global__ void k_Tupd(long long n, double* __restrict__ T, const float* __restrict__ d, const float* __restrict__ p,
                        const PcgScalars* __restrict__ sc) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1796,589 +1647,8 @@ __global__ void k_oc_apply(long long n, const double* __restrict__ rho, const do
 }
 
 // ===========================================================================
-// Fast-path level stencils (otm_stencil2.cuh): one case x two z per thread
+// Level stencils
 // ===========================================================================
-struct OpF {           // plain fp32 operand a[c*n+v], factors kap[v]
-    const float* a; const float* kap; long long n;
-    __device__ __forceinline__ float t1(int c, long long v) const { return __ldg(a + c * n + v); }
-    __device__ __forceinline__ float2 t2(int c, long long v) const {
-        return __ldg(reinterpret_cast<const float2*>(a + c * n + v));
-    }
-    __device__ __forceinline__ float k1(long long v) const { return __ldg(kap + v); }
-    __device__ __forceinline__ float2 k2(long long v) const { return __ldg(reinterpret_cast<const float2*>(kap + v)); }
-};
-
-struct OpSmoothRes2 : OpF {   // operand = omega * dinv * f (Jacobi sweep from zero)
-    const float* dinv; float omega; float* z; float* res;
-    __device__ __forceinline__ float t1(int c, long long v) const {
-        return omega * __ldg(dinv + v) * __ldg(a + c * n + v);
-    }
-    __device__ __forceinline__ float2 t2(int c, long long v) const {
-        const float2 f = __ldg(reinterpret_cast<const float2*>(a + c * n + v));
-        const float2 d = __ldg(reinterpret_cast<const float2*>(dinv + v));
-        return make_float2(omega * d.x * f.x, omega * d.y * f.y);
-    }
-    __device__ __forceinline__ void sink(int c, long long v, const float (&kz)[2], const float (&zc)[2],
-                                         const float (&)[2][3], const float (&)[2][3]) {
-        const float2 f = __ldg(reinterpret_cast<const float2*>(a + c * n + v));
-        *reinterpret_cast<float2*>(z + c * n + v) = make_float2(zc[0], zc[1]);
-        *reinterpret_cast<float2*>(res + c * n + v) = make_float2(f.x - kz[0], f.y - kz[1]);
-    }
-};
-
-template <bool DOT>
-struct OpJacobi2 : OpF {      // operand = z ; zout = z + omega dinv (f - K z)
-    const float* f; const float* dinv; float omega; float* zout; double acc;
-    __device__ __forceinline__ void sink(int c, long long v, const float (&kz)[2], const float (&zc)[2],
-                                         const float (&)[2][3], const float (&)[2][3]) {
-        const float2 fv = __ldg(reinterpret_cast<const float2*>(f + c * n + v));
-        const float2 d = __ldg(reinterpret_cast<const float2*>(dinv + v));
-        const float z0 = zc[0] + omega * d.x * (fv.x - kz[0]);
-        const float z1 = zc[1] + omega * d.y * (fv.y - kz[1]);
-        *reinterpret_cast<float2*>(zout + c * n + v) = make_float2(z0, z1);
-        if (DOT) acc += (double)fv.x * (double)z0 + (double)fv.y * (double)z1;
-    }
-};
-
-struct OpSpmv2 : OpF {        // q = K p ; acc = p.q
-    float* q; double acc;
-    __device__ __forceinline__ void sink(int c, long long v, const float (&kp)[2], const float (&pc)[2],
-                                         const float (&)[2][3], const float (&)[2][3]) {
-        *reinterpret_cast<float2*>(q + c * n + v) = make_float2(kp[0], kp[1]);
-        acc += (double)pc[0] * (double)kp[0] + (double)pc[1] * (double)kp[1];
-    }
-};
-
-struct OpRes64 {              // fp64 defect r = (f(kappa) - fmean) - K T
-    const double* T; const double* kap; const double* fext; const double* fmean; float* r32; long long n;
-    const double* f0; double acc[3];
-    __device__ __forceinline__ double t1(int c, long long v) const { return __ldg(T + c * n + v); }
-    __device__ __forceinline__ double2 t2(int c, long long v) const {
-        return __ldg(reinterpret_cast<const double2*>(T + c * n + v));
-    }
-    __device__ __forceinline__ double k1(long long v) const { return __ldg(kap + v); }
-    __device__ __forceinline__ double2 k2(long long v) const { return __ldg(reinterpret_cast<const double2*>(kap + v)); }
-    __device__ __forceinline__ void sink(int c, long long v, const double (&kt)[2], const double (&tc)[2],
-                                         const double (&K0)[2][3], const double (&K1)[2][3]) {
-        double fv[2];
-        if (fext) {
-            const double2 e = __ldg(reinterpret_cast<const double2*>(fext + c * n + v));
-            fv[0] = e.x; fv[1] = e.y;
-        } else {
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                double f = 0.0;
-#pragma unroll
-                for (int a = 0; a < 8; ++a) {
-                    const int q = 1 - (a & 1), jj = 1 - ((a >> 1) & 1), kk = 1 - ((a >> 2) & 1);
-                    const double ke = q == 0 ? K0[jj][i + kk] : K1[jj][i + kk];
-                    f = __dadd_rn(f, __dmul_rn(f0[a * 3 + c], ke));
-                }
-                fv[i] = f;
-            }
-        }
-        const double fm = fmean[c];
-        const double r0 = (fv[0] - fm) - kt[0], r1 = (fv[1] - fm) - kt[1];
-        *reinterpret_cast<float2*>(r32 + c * n + v) = make_float2((float)r0, (float)r1);
-        acc[0] += r0 * r0 + r1 * r1;
-        acc[1] += fv[0] * fv[0] + fv[1] * fv[1];
-        acc[2] += tc[0] + tc[1];
-    }
-};
-
-__global__ void __launch_bounds__(256, OTM_MINB) k2_smooth_res(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
-                                                        const float* f, const float* dinv, float omega, float* z,
-                                                        float* res) {
-    OpSmoothRes2 op;
-    op.a = f; op.kap = kap; op.n = g.n; op.dinv = dinv; op.omega = omega; op.z = z; op.res = res;
-    march2<float>(g, xb, nch, lt, op);
-}
-
-template <bool DOT>
-__global__ void __launch_bounds__(256, OTM_MINB) k2_jacobi(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
-                                                    const float* z, const float* f, const float* dinv, float omega,
-                                                    float* zout, double* partials, unsigned* counter,
-                                                    PcgScalars* sc) {
-    OpJacobi2<DOT> op;
-    op.a = z; op.kap = kap; op.n = g.n; op.f = f; op.dinv = dinv; op.omega = omega; op.zout = zout; op.acc = 0.0;
-    march2<float>(g, xb, nch, lt, op);
-    if (DOT) {
-        double v3[3] = {0.0, 0.0, 0.0};
-        const int c = blockIdx.z / nch;
-        v3[c] = op.acc;
-        if (reduce_finalize<3>(v3, partials, counter, sc->red)) {
-            for (int cc = 0; cc < 3; ++cc) {
-                const double rz = sc->red[cc];
-                sc->beta[cc] = (sc->first || sc->rz[cc] == 0.0) ? 0.0 : rz / sc->rz[cc];
-                sc->rz[cc] = rz;
-            }
-            sc->first = 0;
-        }
-    }
-}
-
-__global__ void __launch_bounds__(256, OTM_MINB) k2_spmv(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
-                                                  const float* p, float* q, double* partials, unsigned* counter,
-                                                  PcgScalars* sc) {
-    OpSpmv2 op;
-    op.a = p; op.kap = kap; op.n = g.n; op.q = q; op.acc = 0.0;
-    march2<float>(g, xb, nch, lt, op);
-    double v3[3] = {0.0, 0.0, 0.0};
-    v3[blockIdx.z / nch] = op.acc;
-    if (reduce_finalize<3>(v3, partials, counter, sc->red + 3)) {
-        for (int c = 0; c < 3; ++c) {
-            const double pq = sc->red[3 + c];
-            sc->pq[c] = pq;
-            sc->alpha[c] = (sc->active[c] != 0.0 && pq > 0.0) ? sc->rz[c] / pq : 0.0;
-        }
-    }
-}
-
-__global__ void __launch_bounds__(256, 2) k2_res64(Geo g, int xb, int nch, LevelTemplate lt, const double* kap,
-                                                   const double* T, const double* fext, const double* fmean,
-                                                   float* r32, double* partials, unsigned* counter, double* out9) {
-    OpRes64 op;
-    op.T = T; op.kap = kap; op.fext = fext; op.fmean = fmean; op.r32 = r32; op.n = g.n; op.f0 = lt.f0;
-    op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
-    march2<double>(g, xb, nch, lt, op);
-    double v9[9];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) v9[i] = 0.0;
-    const int c = blockIdx.z / nch;
-    v9[c] = op.acc[0];
-    v9[3 + c] = op.acc[1];
-    v9[6 + c] = op.acc[2];
-    reduce_finalize<9>(v9, partials, counter, out9);
-}
-
-// ---- shared-memory-ring versions (otm_stencil3.cuh) ----
-__device__ __forceinline__ const float* s3_at(const float* slot, int a, int r, int col) {
-    return slot + a * kS3Tile + r * kS3Pitch + col;
-}
-
-struct Op3SmoothRes {     // arrays: 0 = f (halo), 1 = D^-1 (halo); operand = w D^-1 f
-    float omega; float* z; float* res; long long n;
-    __device__ __forceinline__ void begin_case(int, int) {}
-    __device__ __forceinline__ float operand(const float* slot, int r, int col) const {
-        return omega * *s3_at(slot, 1, r, col) * *s3_at(slot, 0, r, col);
-    }
-    __device__ __forceinline__ float2 operand2(const float* slot, int r, int col) const {
-        const float2 d = *reinterpret_cast<const float2*>(s3_at(slot, 1, r, col));
-        const float2 f = *reinterpret_cast<const float2*>(s3_at(slot, 0, r, col));
-        return make_float2(omega * d.x * f.x, omega * d.y * f.y);
-    }
-    __device__ __forceinline__ void sink(const float* slot, int c, long long v, int r, int col, const float (&kz)[2],
-                                         const float (&zc)[2]) {
-        const float2 f = *reinterpret_cast<const float2*>(s3_at(slot, 0, r, col));
-        *reinterpret_cast<float2*>(z + c * n + v) = make_float2(zc[0], zc[1]);
-        *reinterpret_cast<float2*>(res + c * n + v) = make_float2(f.x - kz[0], f.y - kz[1]);
-    }
-};
-
-template <bool DOT>
-struct Op3Jacobi {        // arrays: 0 = z (halo), 1 = f (center), 2 = D^-1 (center)
-    float omega; float* zout; long long n; double acc; double acc3[3];
-    __device__ __forceinline__ void begin_case(int c, int last) {
-        if (last >= 0) acc3[last] += acc;
-        acc = 0.0;
-    }
-    __device__ __forceinline__ float operand(const float* slot, int r, int col) const { return *s3_at(slot, 0, r, col); }
-    __device__ __forceinline__ float2 operand2(const float* slot, int r, int col) const {
-        return *reinterpret_cast<const float2*>(s3_at(slot, 0, r, col));
-    }
-    __device__ __forceinline__ void sink(const float* slot, int c, long long v, int r, int col, const float (&kz)[2],
-                                         const float (&zc)[2]) {
-        const float2 fv = *reinterpret_cast<const float2*>(s3_at(slot, 1, r, col));
-        const float2 d = *reinterpret_cast<const float2*>(s3_at(slot, 2, r, col));
-        const float z0 = zc[0] + omega * d.x * (fv.x - kz[0]);
-        const float z1 = zc[1] + omega * d.y * (fv.y - kz[1]);
-        *reinterpret_cast<float2*>(zout + c * n + v) = make_float2(z0, z1);
-        if (DOT) acc += (double)fv.x * (double)z0 + (double)fv.y * (double)z1;
-    }
-};
-
-struct Op3Spmv {          // arrays: 0 = p (halo)
-    float* q; long long n; double acc; double acc3[3];
-    __device__ __forceinline__ void begin_case(int c, int last) {
-        if (last >= 0) acc3[last] += acc;
-        acc = 0.0;
-    }
-    __device__ __forceinline__ float operand(const float* slot, int r, int col) const { return *s3_at(slot, 0, r, col); }
-    __device__ __forceinline__ float2 operand2(const float* slot, int r, int col) const {
-        return *reinterpret_cast<const float2*>(s3_at(slot, 0, r, col));
-    }
-    __device__ __forceinline__ void sink(const float*, int c, long long v, int, int, const float (&kp)[2],
-                                         const float (&pc)[2]) {
-        *reinterpret_cast<float2*>(q + c * n + v) = make_float2(kp[0], kp[1]);
-        acc += (double)pc[0] * (double)kp[0] + (double)pc[1] * (double)kp[1];
-    }
-};
-
-template <bool K5>
-__global__ void __launch_bounds__(256, 3) k3_smooth_res(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
-                                                        const float* f, const float* dinv, float omega, float* z,
-                                                        float* res) {
-    S3Setup<2> su;
-    su.arr[0] = S3Array{f, 1, S3Halo};
-    su.arr[1] = S3Array{dinv, 0, S3Halo};
-    su.kap = kap;
-    Op3SmoothRes op{omega, z, res, g.n};
-    int last;
-    if (K5) march5<2>(g, lt, su, op, last);
-    else march3<2>(g, lt, su, op, last);
-}
-
-template <bool DOT, bool K5>
-__global__ void __launch_bounds__(256, 3) k3_jacobi(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
-                                                    const float* z, const float* f, const float* dinv, float omega,
-                                                    float* zout, double* partials, unsigned* counter,
-                                                    PcgScalars* sc) {
-    S3Setup<3> su;
-    su.arr[0] = S3Array{z, 1, S3Halo};
-    su.arr[1] = S3Array{f, 1, S3Center};
-    su.arr[2] = S3Array{dinv, 0, S3Center};
-    su.kap = kap;
-    Op3Jacobi<DOT> op{omega, zout, g.n, 0.0, {0.0, 0.0, 0.0}};
-    int last;
-    if (K5) march5<3>(g, lt, su, op, last);
-    else march3<3>(g, lt, su, op, last);
-    if (DOT) {
-        if (last >= 0) op.acc3[last] += op.acc;
-        double v3[3] = {op.acc3[0], op.acc3[1], op.acc3[2]};
-        if (reduce_finalize<3>(v3, partials, counter, sc->red)) {
-            for (int cc = 0; cc < 3; ++cc) {
-                const double rz = sc->red[cc];
-                sc->beta[cc] = (sc->first || sc->rz[cc] == 0.0) ? 0.0 : rz / sc->rz[cc];
-                sc->rz[cc] = rz;
-            }
-            sc->first = 0;
-        }
-    }
-}
-
-template <bool K5>
-__global__ void __launch_bounds__(256, 3) k3_spmv(Geo g, int xb, int nch, LevelTemplate lt, const float* kap,
-                                                  const float* p, float* q, double* partials, unsigned* counter,
-                                                  PcgScalars* sc) {
-    S3Setup<1> su;
-    su.arr[0] = S3Array{p, 1, S3Halo};
-    su.kap = kap;
-    Op3Spmv op{q, g.n, 0.0, {0.0, 0.0, 0.0}};
-    int last;
-    if (K5) march5<1>(g, lt, su, op, last);
-    else march3<1>(g, lt, su, op, last);
-    if (last >= 0) op.acc3[last] += op.acc;
-    double v3[3] = {op.acc3[0], op.acc3[1], op.acc3[2]};
-    if (reduce_finalize<3>(v3, partials, counter, sc->red + 3)) {
-        for (int cc = 0; cc < 3; ++cc) {
-            const double pq = sc->red[3 + cc];
-            sc->pq[cc] = pq;
-            sc->alpha[cc] = (sc->active[cc] != 0.0 && pq > 0.0) ? sc->rz[cc] / pq : 0.0;
-        }
-    }
-}
-
-static int kernel_gen();
-static bool s3_enabled() {     // OTM_K=3 (separable k3) or 5 (k3 ring + 21-weight FFMA2)
-    const int k = kernel_gen();
-    return k == 3 || k == 5;
-}
-// persistent grid: resident blocks of the kernel x SMs (capped by the work units)
-template <class K>
-static dim3 s3_grid(K kernel, size_t smem, const Geo& g) {
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem);
-    if (per_sm < 1) per_sm = 1;
-    const long long units = 3LL * (g.nz / kTileZ) * (g.ny / kTileY) * g.nx;
-    long long b = (long long)per_sm * sms;
-    if (b > units) b = units;
-    return dim3((unsigned)b, 1, 1);
-}
-template <class K>
-static void s3_attr(K kernel, size_t bytes) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-}
-
-// ---- k4: three cases per thread, 21 weights, FFMA2 (otm_stencil4.cuh) ----
-struct Op4SmoothRes {     // tiles: f case 0..2 (halo), D^-1 (halo); operand = w D^-1 f
-    static constexpr int NT = 4;
-    float omega; float* z; float* res; long long n;
-    __device__ __forceinline__ float op1(const float* S, int c, int r, int col) const {
-        return omega * *s3_at(S, 3, r, col) * *s3_at(S, c, r, col);
-    }
-    __device__ __forceinline__ float2 op2(const float* S, int c, int r, int col) const {
-        const float2 d = *reinterpret_cast<const float2*>(s3_at(S, 3, r, col));
-        const float2 f = *reinterpret_cast<const float2*>(s3_at(S, c, r, col));
-        return make_float2(omega * d.x * f.x, omega * d.y * f.y);
-    }
-    __device__ __forceinline__ void prefetch(int, long long) {}
-    __device__ __forceinline__ void sink(const float* S0, int c, long long v, int r, int col, float2 kz, float2 zc) {
-        const float2 f = *reinterpret_cast<const float2*>(s3_at(S0, c, r, col));
-        *reinterpret_cast<float2*>(z + c * n + v) = zc;
-        *reinterpret_cast<float2*>(res + c * n + v) = make_float2(f.x - kz.x, f.y - kz.y);
-    }
-};
-
-template <bool DOT>
-struct Op4Jacobi {        // tiles: z case 0..2 (halo); f and D^-1 prefetched into registers
-    static constexpr int NT = 3;
-    const float* f; const float* dinv; float omega; float* zout; long long n;
-    float2 fp[3], dp;
-    double acc[3];
-    __device__ __forceinline__ float op1(const float* S, int c, int r, int col) const { return *s3_at(S, c, r, col); }
-    __device__ __forceinline__ float2 op2(const float* S, int c, int r, int col) const {
-        return *reinterpret_cast<const float2*>(s3_at(S, c, r, col));
-    }
-    long long pl;
-    __device__ __forceinline__ void prefetch(int x, long long vrow) {
-        const long long v = vrow + (long long)x * pl;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) fp[c] = __ldg(reinterpret_cast<const float2*>(f + c * n + v));
-        dp = __ldg(reinterpret_cast<const float2*>(dinv + v));
-    }
-    __device__ __forceinline__ void sink(const float*, int c, long long v, int, int, float2 kz, float2 zc) {
-        const float z0 = zc.x + omega * dp.x * (fp[c].x - kz.x);
-        const float z1 = zc.y + omega * dp.y * (fp[c].y - kz.y);
-        *reinterpret_cast<float2*>(zout + c * n + v) = make_float2(z0, z1);
-        if (DOT) acc[c] += (double)fp[c].x * (double)z0 + (double)fp[c].y * (double)z1;
-    }
-};
-
-struct Op4Spmv {          // tiles: p case 0..2 (halo)
-    static constexpr int NT = 3;
-    float* q; long long n; double acc[3];
-    __device__ __forceinline__ float op1(const float* S, int c, int r, int col) const { return *s3_at(S, c, r, col); }
-    __device__ __forceinline__ float2 op2(const float* S, int c, int r, int col) const {
-        return *reinterpret_cast<const float2*>(s3_at(S, c, r, col));
-    }
-    __device__ __forceinline__ void prefetch(int, long long) {}
-    __device__ __forceinline__ void sink(const float*, int c, long long v, int, int, float2 kp, float2 pc) {
-        *reinterpret_cast<float2*>(q + c * n + v) = kp;
-        acc[c] += (double)pc.x * (double)kp.x + (double)pc.y * (double)kp.y;
-    }
-};
-
-__global__ void __launch_bounds__(256, 2) k4_smooth_res(Geo g, LevelTemplate lt, const float* kap, const float* f,
-                                                        const float* dinv, float omega, float* z, float* res) {
-    S4Setup su;
-    su.arr[0] = f; su.arr[1] = f + g.n; su.arr[2] = f + 2 * g.n; su.arr[3] = dinv;
-    su.narr = 4;
-    su.kap = kap;
-    Op4SmoothRes op{omega, z, res, g.n};
-    march4(g, lt, su, op);
-}
-
-template <bool DOT>
-__global__ void __launch_bounds__(256, 2) k4_jacobi(Geo g, LevelTemplate lt, const float* kap, const float* z,
-                                                    const float* f, const float* dinv, float omega, float* zout,
-                                                    double* partials, unsigned* counter, PcgScalars* sc) {
-    S4Setup su;
-    su.arr[0] = z; su.arr[1] = z + g.n; su.arr[2] = z + 2 * g.n; su.arr[3] = nullptr;
-    su.narr = 3;
-    su.kap = kap;
-    Op4Jacobi<DOT> op;
-    op.f = f; op.dinv = dinv; op.omega = omega; op.zout = zout; op.n = g.n; op.pl = g.pl;
-    op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
-    march4(g, lt, su, op);
-    if (DOT) {
-        double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
-        if (reduce_finalize<3>(v3, partials, counter, sc->red)) {
-            for (int cc = 0; cc < 3; ++cc) {
-                const double rz = sc->red[cc];
-                sc->beta[cc] = (sc->first || sc->rz[cc] == 0.0) ? 0.0 : rz / sc->rz[cc];
-                sc->rz[cc] = rz;
-            }
-            sc->first = 0;
-        }
-    }
-}
-
-__global__ void __launch_bounds__(256, 2) k4_spmv(Geo g, LevelTemplate lt, const float* kap, const float* p,
-                                                  float* q, double* partials, unsigned* counter, PcgScalars* sc) {
-    S4Setup su;
-    su.arr[0] = p; su.arr[1] = p + g.n; su.arr[2] = p + 2 * g.n; su.arr[3] = nullptr;
-    su.narr = 3;
-    su.kap = kap;
-    Op4Spmv op{q, g.n, {0.0, 0.0, 0.0}};
-    march4(g, lt, su, op);
-    double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
-    if (reduce_finalize<3>(v3, partials, counter, sc->red + 3)) {
-        for (int cc = 0; cc < 3; ++cc) {
-            const double pq = sc->red[3 + cc];
-            sc->pq[cc] = pq;
-            sc->alpha[cc] = (sc->active[cc] != 0.0 && pq > 0.0) ? sc->rz[cc] / pq : 0.0;
-        }
-    }
-}
-
-// ---- k6: TMA-staged (otm_stencil6.cuh) ----
-template <int NZv, int TYv = 512 / NZv>
-struct Op6Base {                  // compile-time tile geometry: every shared-memory offset is an immediate
-    static constexpr int NZ = NZv;
-    static constexpr int TY = TYv;
-    static constexpr int nz = NZv;
-    static constexpr int tile = (TYv + 2) * NZv;
-    __device__ __forceinline__ const float* at(const float* S, int a, int r, int z) const {
-        return S + a * tile + r * nz + z;
-    }
-};
-template <int NZv, int TYv = 512 / NZv>
-struct Op6SmoothRes : Op6Base<NZv, TYv> {   // tiles 0..2 = f cases, 3 = D^-1; operand w D^-1 f
-    using Op6Base<NZv, TYv>::at;
-    static constexpr int NT = 4;
-    float omega; float* zo; float* res; long long n;
-    __device__ __forceinline__ float op1(const float* S, int c, int r, int z) const {
-        return omega * *at(S, 3, r, z) * *at(S, c, r, z);
-    }
-    __device__ __forceinline__ float2 op2(const float* S, int c, int r, int z) const {
-        const float2 d = *reinterpret_cast<const float2*>(at(S, 3, r, z));
-        const float2 f = *reinterpret_cast<const float2*>(at(S, c, r, z));
-        return make_float2(omega * d.x * f.x, omega * d.y * f.y);
-    }
-    __device__ __forceinline__ void prefetch(int, long long) {}
-    __device__ __forceinline__ void sink(const float* S0, int c, long long v, int r, int z, float2 kz, float2 zc) {
-        const float2 f = *reinterpret_cast<const float2*>(at(S0, c, r, z));
-        *reinterpret_cast<float2*>(zo + c * n + v) = zc;
-        *reinterpret_cast<float2*>(res + c * n + v) = make_float2(f.x - kz.x, f.y - kz.y);
-    }
-};
-template <bool DOT, int NZv, int TYv = 512 / NZv>
-struct Op6Jacobi : Op6Base<NZv, TYv> {      // tiles 0..2 = z cases; f, D^-1 prefetched
-    using Op6Base<NZv, TYv>::at;
-    static constexpr int NT = 3;
-    const float* f; const float* dinv; float omega; float* zout; long long n; long long pl;
-    float2 fp[3], dp;
-    double acc[3];
-    __device__ __forceinline__ float op1(const float* S, int c, int r, int z) const { return *at(S, c, r, z); }
-    __device__ __forceinline__ float2 op2(const float* S, int c, int r, int z) const {
-        return *reinterpret_cast<const float2*>(at(S, c, r, z));
-    }
-    __device__ __forceinline__ void prefetch(int x, long long vrow) {
-        const long long v = vrow + (long long)x * pl;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) fp[c] = __ldg(reinterpret_cast<const float2*>(f + c * n + v));
-        dp = __ldg(reinterpret_cast<const float2*>(dinv + v));
-    }
-    __device__ __forceinline__ void sink(const float*, int c, long long v, int, int, float2 kz, float2 zc) {
-        const float z0 = zc.x + omega * dp.x * (fp[c].x - kz.x);
-        const float z1 = zc.y + omega * dp.y * (fp[c].y - kz.y);
-        *reinterpret_cast<float2*>(zout + c * n + v) = make_float2(z0, z1);
-        if (DOT) acc[c] += (double)fp[c].x * (double)z0 + (double)fp[c].y * (double)z1;
-    }
-};
-template <int NZv, int TYv = 512 / NZv>
-struct Op6Spmv : Op6Base<NZv, TYv> {        // tiles 0..2 = p cases
-    using Op6Base<NZv, TYv>::at;
-    static constexpr int NT = 3;
-    float* q; long long n; double acc[3];
-    __device__ __forceinline__ float op1(const float* S, int c, int r, int z) const { return *at(S, c, r, z); }
-    __device__ __forceinline__ float2 op2(const float* S, int c, int r, int z) const {
-        return *reinterpret_cast<const float2*>(at(S, c, r, z));
-    }
-    __device__ __forceinline__ void prefetch(int, long long) {}
-    __device__ __forceinline__ void sink(const float*, int c, long long v, int, int, float2 kp, float2 pc) {
-        *reinterpret_cast<float2*>(q + c * n + v) = kp;
-        acc[c] += (double)pc.x * (double)kp.x + (double)pc.y * (double)kp.y;
-    }
-};
-
-template <int NZ>
-__global__ void __launch_bounds__(256, 2) k6_smooth_res(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
-                                                        float omega, float* z, float* res) {
-    Op6SmoothRes<NZ> op;
-    op.omega = omega; op.zo = z; op.res = res; op.n = g.n;
-    march6(g, lt, maps, op);
-}
-
-template <bool DOT, int NZ>
-__global__ void __launch_bounds__(256, 2) k6_jacobi(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
-                                                    const float* f, const float* dinv, float omega, float* zout,
-                                                    double* partials, unsigned* counter, PcgScalars* sc) {
-    Op6Jacobi<DOT, NZ> op;
-    op.f = f; op.dinv = dinv; op.omega = omega; op.zout = zout; op.n = g.n; op.pl = g.pl;
-    op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
-    march6(g, lt, maps, op);
-    if (DOT) {
-        double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
-        if (reduce_finalize<3>(v3, partials, counter, sc->red)) {
-            for (int cc = 0; cc < 3; ++cc) {
-                const double rz = sc->red[cc];
-                sc->beta[cc] = (sc->first || sc->rz[cc] == 0.0) ? 0.0 : rz / sc->rz[cc];
-                sc->rz[cc] = rz;
-            }
-            sc->first = 0;
-        }
-    }
-}
-
-template <int NZ>
-__global__ void __launch_bounds__(256, 2) k6_spmv(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
-                                                  float* q, double* partials, unsigned* counter, PcgScalars* sc) {
-    Op6Spmv<NZ> op;
-    op.q = q; op.n = g.n;
-    op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
-    march6(g, lt, maps, op);
-    double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
-    if (reduce_finalize<3>(v3, partials, counter, sc->red + 3)) {
-        for (int cc = 0; cc < 3; ++cc) {
-            const double pq = sc->red[3 + cc];
-            sc->pq[cc] = pq;
-            sc->alpha[cc] = (sc->active[cc] != 0.0 && pq > 0.0) ? sc->rz[cc] / pq : 0.0;
-        }
-    }
-}
-
-// ---- k8: k6 staging + x register window for the three cases (march8) ----
-template <int NZ, int TY>
-__global__ void __launch_bounds__(NZ / 2 * TY, 256 / (NZ / 2 * TY)) k8_smooth_res(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
-                                                        float omega, float* z, float* res, unsigned* work) {
-    Op6SmoothRes<NZ, TY> op;
-    op.omega = omega; op.zo = z; op.res = res; op.n = g.n;
-    march8(g, lt, maps, op, work);
-}
-
-template <bool DOT, int NZ, int TY>
-__global__ void __launch_bounds__(NZ / 2 * TY, 256 / (NZ / 2 * TY)) k8_jacobi(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
-                                                    const float* f, const float* dinv, float omega, float* zout,
-                                                    double* partials, unsigned* counter, PcgScalars* sc,
-                                                    unsigned* work) {
-    Op6Jacobi<DOT, NZ, TY> op;
-    op.f = f; op.dinv = dinv; op.omega = omega; op.zout = zout; op.n = g.n; op.pl = g.pl;
-    op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
-    march8(g, lt, maps, op, work);
-    if (DOT) {
-        double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
-        if (reduce_finalize<3>(v3, partials, counter, sc->red)) {
-            for (int cc = 0; cc < 3; ++cc) {
-                const double rz = sc->red[cc];
-                sc->beta[cc] = (sc->first || sc->rz[cc] == 0.0) ? 0.0 : rz / sc->rz[cc];
-                sc->rz[cc] = rz;
-            }
-            sc->first = 0;
-        }
-    }
-}
-
-template <int NZ, int TY>
-__global__ void __launch_bounds__(NZ / 2 * TY, 256 / (NZ / 2 * TY)) k8_spmv(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
-                                                  float* q, double* partials, unsigned* counter, PcgScalars* sc,
-                                                    unsigned* work) {
-    Op6Spmv<NZ, TY> op;
-    op.q = q; op.n = g.n;
-    op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
-    march8(g, lt, maps, op, work);
-    double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
-    if (reduce_finalize<3>(v3, partials, counter, sc->red + 3)) {
-        for (int cc = 0; cc < 3; ++cc) {
-            const double pq = sc->red[3 + cc];
-            sc->pq[cc] = pq;
-            sc->alpha[cc] = (sc->active[cc] != 0.0 && pq > 0.0) ? sc->rz[cc] / pq : 0.0;
-        }
-    }
-}
-
 // ---- k10: push x-march, operand consumed once per plane (otm_stencil10.cuh) ----
 // CPS = CTAs per SM the ring is sized for (TY rows x NZ/2 threads per CTA)
 template <int NZ, int TY, int CPS, bool WZ>
@@ -2410,27 +1680,6 @@ __global__ void __launch_bounds__(NZ / 2 * TY, CPS) k10_jacobi(Geo g, float s12,
     }
 }
 
-template <bool DOT, int NZ, int TY, int CPS>
-__global__ void __launch_bounds__(NZ / 2 * TY, CPS) k10_jacobi_p(Geo g, float s12, const __grid_constant__ K10Maps maps,
-                                                                float omega, float* zout, double* partials,
-                                                                unsigned* counter, PcgScalars* sc) {
-    K10Op<K10_JACOBI_P, NZ, TY, DOT, CPS> op;
-    op.omega = omega; op.out0 = zout; op.out1 = nullptr; op.n = g.n;
-    op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
-    march10(g, s12, maps, op);
-    if (DOT) {
-        double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
-        if (reduce_finalize<3>(v3, partials, counter, sc->red)) {
-            for (int cc = 0; cc < 3; ++cc) {
-                const double rz = sc->red[cc];
-                sc->beta[cc] = (sc->first || sc->rz[cc] == 0.0) ? 0.0 : rz / sc->rz[cc];
-                sc->rz[cc] = rz;
-            }
-            sc->first = 0;
-        }
-    }
-}
-
 template <int NZ, int TY, int CPS>
 __global__ void __launch_bounds__(NZ / 2 * TY, CPS) k10_spmv(Geo g, float s12, const __grid_constant__ K10Maps maps,
                                                             float* q, double* partials, unsigned* counter,
@@ -2440,172 +1689,6 @@ __global__ void __launch_bounds__(NZ / 2 * TY, CPS) k10_spmv(Geo g, float s12, c
     op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
     march10(g, s12, maps, op);
     double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
-    if (reduce_finalize<3>(v3, partials, counter, sc->red + 3)) {
-        for (int cc = 0; cc < 3; ++cc) {
-            const double pq = sc->red[3 + cc];
-            sc->pq[cc] = pq;
-            sc->alpha[cc] = (sc->active[cc] != 0.0 && pq > 0.0) ? sc->rz[cc] / pq : 0.0;
-        }
-    }
-}
-
-// ---- k9: k6 staging + x register window for the three cases (march8) ----
-template <int NZ>
-__global__ void __launch_bounds__(256, 1) k9_smooth_res(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
-                                                        float omega, float* z, float* res) {
-    Op6SmoothRes<NZ> op;
-    op.omega = omega; op.zo = z; op.res = res; op.n = g.n;
-    march9(g, lt, maps, op);
-}
-
-template <bool DOT, int NZ>
-__global__ void __launch_bounds__(256, 1) k9_jacobi(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
-                                                    const float* f, const float* dinv, float omega, float* zout,
-                                                    double* partials, unsigned* counter, PcgScalars* sc) {
-    Op6Jacobi<DOT, NZ> op;
-    op.f = f; op.dinv = dinv; op.omega = omega; op.zout = zout; op.n = g.n; op.pl = g.pl;
-    op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
-    march9(g, lt, maps, op);
-    if (DOT) {
-        double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
-        if (reduce_finalize<3>(v3, partials, counter, sc->red)) {
-            for (int cc = 0; cc < 3; ++cc) {
-                const double rz = sc->red[cc];
-                sc->beta[cc] = (sc->first || sc->rz[cc] == 0.0) ? 0.0 : rz / sc->rz[cc];
-                sc->rz[cc] = rz;
-            }
-            sc->first = 0;
-        }
-    }
-}
-
-template <int NZ>
-__global__ void __launch_bounds__(256, 1) k9_spmv(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
-                                                  float* q, double* partials, unsigned* counter, PcgScalars* sc) {
-    Op6Spmv<NZ> op;
-    op.q = q; op.n = g.n;
-    op.acc[0] = op.acc[1] = op.acc[2] = 0.0;
-    march9(g, lt, maps, op);
-    double v3[3] = {op.acc[0], op.acc[1], op.acc[2]};
-    if (reduce_finalize<3>(v3, partials, counter, sc->red + 3)) {
-        for (int cc = 0; cc < 3; ++cc) {
-            const double pq = sc->red[3 + cc];
-            sc->pq[cc] = pq;
-            sc->alpha[cc] = (sc->active[cc] != 0.0 && pq > 0.0) ? sc->rz[cc] / pq : 0.0;
-        }
-    }
-}
-
-// ---- k7: TMA + register window + shuffles, one case per thread (march7) ----
-struct Op7Base {
-    int tile; int nz;
-    __device__ __forceinline__ const float* at(const float* S, int a, int r, int z) const {
-        return S + a * tile + r * nz + z;
-    }
-};
-struct Op7SmoothRes : Op7Base {   // tiles: 0 = f of the block's case, 1 = D^-1
-    static constexpr int NT = 2;
-    float omega; float* zo; float* res; long long n;
-    __device__ __forceinline__ void begin_case(int, int) {}
-    __device__ __forceinline__ float op1(const float* S, int r, int z) const {
-        return omega * *at(S, 1, r, z) * *at(S, 0, r, z);
-    }
-    __device__ __forceinline__ float2 op2(const float* S, int r, int z) const {
-        const float2 d = *reinterpret_cast<const float2*>(at(S, 1, r, z));
-        const float2 f = *reinterpret_cast<const float2*>(at(S, 0, r, z));
-        return make_float2(omega * d.x * f.x, omega * d.y * f.y);
-    }
-    __device__ __forceinline__ void prefetch(int, int, long long) {}
-    __device__ __forceinline__ void sink(const float* S0, int c, long long v, int r, int z, float2 kz, float2 zc) {
-        const float2 f = *reinterpret_cast<const float2*>(at(S0, 0, r, z));
-        *reinterpret_cast<float2*>(zo + c * n + v) = zc;
-        *reinterpret_cast<float2*>(res + c * n + v) = make_float2(f.x - kz.x, f.y - kz.y);
-    }
-};
-template <bool DOT>
-struct Op7Jacobi : Op7Base {      // tile 0 = z of the block's case; f, D^-1 prefetched
-    static constexpr int NT = 1;
-    const float* f; const float* dinv; float omega; float* zout; long long n; long long pl;
-    float2 fp, dp;
-    double acc, acc3[3];
-    __device__ __forceinline__ void begin_case(int, int last) {
-        if (last >= 0) acc3[last] += acc;
-        acc = 0.0;
-    }
-    __device__ __forceinline__ float op1(const float* S, int r, int z) const { return *at(S, 0, r, z); }
-    __device__ __forceinline__ float2 op2(const float* S, int r, int z) const {
-        return *reinterpret_cast<const float2*>(at(S, 0, r, z));
-    }
-    __device__ __forceinline__ void prefetch(int c, int x, long long vrow) {
-        const long long v = vrow + (long long)x * pl;
-        fp = __ldg(reinterpret_cast<const float2*>(f + c * n + v));
-        dp = __ldg(reinterpret_cast<const float2*>(dinv + v));
-    }
-    __device__ __forceinline__ void sink(const float*, int c, long long v, int, int, float2 kz, float2 zc) {
-        const float z0 = zc.x + omega * dp.x * (fp.x - kz.x);
-        const float z1 = zc.y + omega * dp.y * (fp.y - kz.y);
-        *reinterpret_cast<float2*>(zout + c * n + v) = make_float2(z0, z1);
-        if (DOT) acc += (double)fp.x * (double)z0 + (double)fp.y * (double)z1;
-    }
-};
-struct Op7Spmv : Op7Base {        // tile 0 = p of the block's case
-    static constexpr int NT = 1;
-    float* q; long long n; double acc, acc3[3];
-    __device__ __forceinline__ void begin_case(int, int last) {
-        if (last >= 0) acc3[last] += acc;
-        acc = 0.0;
-    }
-    __device__ __forceinline__ float op1(const float* S, int r, int z) const { return *at(S, 0, r, z); }
-    __device__ __forceinline__ float2 op2(const float* S, int r, int z) const {
-        return *reinterpret_cast<const float2*>(at(S, 0, r, z));
-    }
-    __device__ __forceinline__ void prefetch(int, int, long long) {}
-    __device__ __forceinline__ void sink(const float*, int c, long long v, int, int, float2 kp, float2 pc) {
-        *reinterpret_cast<float2*>(q + c * n + v) = kp;
-        acc += (double)pc.x * (double)kp.x + (double)pc.y * (double)kp.y;
-    }
-};
-
-__global__ void __launch_bounds__(256, 2) k7_smooth_res(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
-                                                        float omega, float* z, float* res) {
-    Op7SmoothRes op;
-    op.tile = (k6_ty(g.nz) + 2) * g.nz; op.nz = g.nz;
-    op.omega = omega; op.zo = z; op.res = res; op.n = g.n;
-    int last;
-    march7(g, lt, maps, op, last);
-}
-template <bool DOT>
-__global__ void __launch_bounds__(256, 2) k7_jacobi(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
-                                                    const float* f, const float* dinv, float omega, float* zout,
-                                                    double* partials, unsigned* counter, PcgScalars* sc) {
-    Op7Jacobi<DOT> op;
-    op.tile = (k6_ty(g.nz) + 2) * g.nz; op.nz = g.nz;
-    op.f = f; op.dinv = dinv; op.omega = omega; op.zout = zout; op.n = g.n; op.pl = g.pl;
-    op.acc = 0.0; op.acc3[0] = op.acc3[1] = op.acc3[2] = 0.0;
-    int last;
-    march7(g, lt, maps, op, last);
-    if (DOT) {
-        if (last >= 0) op.acc3[last] += op.acc;
-        double v3[3] = {op.acc3[0], op.acc3[1], op.acc3[2]};
-        if (reduce_finalize<3>(v3, partials, counter, sc->red)) {
-            for (int cc = 0; cc < 3; ++cc) {
-                const double rz = sc->red[cc];
-                sc->beta[cc] = (sc->first || sc->rz[cc] == 0.0) ? 0.0 : rz / sc->rz[cc];
-                sc->rz[cc] = rz;
-            }
-            sc->first = 0;
-        }
-    }
-}
-__global__ void __launch_bounds__(256, 2) k7_spmv(Geo g, LevelTemplate lt, const __grid_constant__ K6Maps maps,
-                                                  float* q, double* partials, unsigned* counter, PcgScalars* sc) {
-    Op7Spmv op;
-    op.tile = (k6_ty(g.nz) + 2) * g.nz; op.nz = g.nz;
-    op.q = q; op.n = g.n; op.acc = 0.0; op.acc3[0] = op.acc3[1] = op.acc3[2] = 0.0;
-    int last;
-    march7(g, lt, maps, op, last);
-    if (last >= 0) op.acc3[last] += op.acc;
-    double v3[3] = {op.acc3[0], op.acc3[1], op.acc3[2]};
     if (reduce_finalize<3>(v3, partials, counter, sc->red + 3)) {
         for (int cc = 0; cc < 3; ++cc) {
             const double pq = sc->red[3 + cc];
@@ -2654,15 +1737,6 @@ static bool encode_map(CUtensorMap* m, const float* base, int nz, int ny, long l
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE), "3-d");
 }
-// arr3: 3-case array (3 nx planes), d1: optional D^-1 (nx planes), kap: factors
-static bool k6_maps(K6Maps& M, const Geo& g, const float* arr3, const float* d1, const float* kap, int TY = 0) {
-    if (TY == 0) TY = k6_ty(g.nz);
-    bool ok = encode_map(&M.main[0], arr3, g.nz, g.ny, 3LL * g.nx, TY) && encode_map(&M.halo[0], arr3, g.nz, g.ny, 3LL * g.nx, 1) &&
-              encode_map(&M.main[2], kap, g.nz, g.ny, g.nx, TY) && encode_map(&M.halo[2], kap, g.nz, g.ny, g.nx, 1);
-    if (d1) ok = ok && encode_map(&M.main[1], d1, g.nz, g.ny, g.nx, TY) && encode_map(&M.halo[1], d1, g.nz, g.ny, g.nx, 1);
-    else { M.main[1] = M.main[2]; M.halo[1] = M.halo[2]; }
-    return ok;
-}
 static bool encode_map64(CUtensorMap* m, const double* base, int nz, int ny, long long planes, int box_rows) {
     PFN_encodeTiled_t fn = encode_fn();
     if (!fn) return false;
@@ -2683,236 +1757,6 @@ static bool encode_map64(CUtensorMap* m, const double* base, int nz, int ny, lon
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-template <class K>
-static dim3 k7_grid(K kernel, size_t smem, const Geo& g) {
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem);
-    if (per_sm < 1) per_sm = 1;
-    const long long units = 3LL * (g.ny / k6_ty(g.nz)) * g.nx;
-    long long b = (long long)per_sm * sms;
-    if (b > units) b = units;
-    return dim3((unsigned)b, 1, 1);
-}
-template <class K>
-static dim3 k6_grid(K kernel, size_t smem, const Geo& g, int TY = 0) {
-    int dev = 0, sms = 148, per_sm = 1;
-    if (TY == 0) TY = k6_ty(g.nz);
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, g.nz / 2 * TY, smem);
-    if (per_sm < 1) per_sm = 1;
-    const long long units = (long long)(g.ny / TY) * g.nx;
-    long long b = (long long)per_sm * sms;
-    if (b > units) b = units;
-    return dim3((unsigned)b, 1, 1);
-}
-static dim3 k6_block(const Geo& g) { return dim3((unsigned)(g.nz / 2), (unsigned)k6_ty(g.nz), 1); }
-
-static int kernel_gen() {     // OTM_K=2..10 selects the fast-path stencil generation (default 10)
-    static const int k = getenv("OTM_K") ? atoi(getenv("OTM_K")) : 10;
-    return k;
-}
-template <class K>
-static dim3 s4_grid(K kernel, size_t smem, const Geo& g) {
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem);
-    if (per_sm < 1) per_sm = 1;
-    const long long units = (long long)(g.nz / kTileZ) * (g.ny / kTileY) * g.nx;
-    long long b = (long long)per_sm * sms;
-    if (b > units) b = units;
-    return dim3((unsigned)b, 1, 1);
-}
-
-static inline dim3 fast_grid(const Geo& g, int xb, int* nch) {
-    *nch = (g.nx + xb - 1) / xb;
-    return dim3((unsigned)(g.nz / kTileZ), (unsigned)(g.ny / kTileY), (unsigned)(3 * *nch));
-}
-static inline int fast_xb(const Geo& g) {
-    static const int env_xb = getenv("OTM_XB") ? atoi(getenv("OTM_XB")) : 0;   // tuning experiments
-    if (env_xb > 0) return env_xb < g.nx ? env_xb : g.nx;
-    // about 3.5 waves of 3 x 148 resident blocks, but never fewer than 4 planes per chunk
-    const long long per_chunk = 3LL * (g.nz / kTileZ) * (g.ny / kTileY);
-    long long chunks = (4LL * 3 * 148 + per_chunk - 1) / per_chunk;
-    int xb = (int)((g.nx + chunks - 1) / chunks);
-    return xb < 4 ? (g.nx < 4 ? g.nx : 4) : xb;
-}
-
-// ===========================================================================
-// V-cycle tail in one CTA: every level with <= kTailMaxVerts vertices, from the
-// smoothing of the first tail level down to the coarse solve and back up.  The
-// phases are separated by block barriers (global writes of the block are visible
-// to the block after __syncthreads); plain loads, no read-only cache path.
-// ===========================================================================
-__device__ float tail_apply(const TailLevel& L, const float* src, int c, int v) {
-    const Geo& g = L.g;
-    const int x = v / g.pl, rem = v - x * g.pl, y = rem / g.nz, z = rem - y * g.nz;
-    const int xs[3] = {wrap_m(x, g.nx), x, wrap_p(x, g.nx)};
-    const int ys[3] = {wrap_m(y, g.ny), y, wrap_p(y, g.ny)};
-    const int zs[3] = {wrap_m(z, g.nz), z, wrap_p(z, g.nz)};
-    const float* a = src + (size_t)c * g.n;
-    float t[3][3][3];
-    for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j)
-            for (int k = 0; k < 3; ++k) t[i][j][k] = a[(xs[i] * g.ny + ys[j]) * g.nz + zs[k]];
-    float acc = 0.f;
-    // elements (q, jj, kk) at (x-1+q, y-1+jj, z-1+kk); vertex is corner a = (1-q)|(1-jj)<<1|(1-kk)<<2
-    for (int q = 0; q < 2; ++q)
-        for (int jj = 0; jj < 2; ++jj)
-            for (int kk = 0; kk < 2; ++kk) {
-                const float ke = L.kap[(xs[q] * g.ny + ys[jj]) * g.nz + zs[kk]];
-                const int av = (1 - q) | ((1 - jj) << 1) | ((1 - kk) << 2);
-                float e = 0.f;
-                for (int b = 0; b < 8; ++b)
-                    e += (float)L.lt.kt[av ^ b] * t[q + (b & 1)][jj + ((b >> 1) & 1)][kk + ((b >> 2) & 1)];
-                acc += ke * e;
-            }
-    return acc;
-}
-
-__global__ void __launch_bounds__(1024) k_vtail(TailArgs A) {
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const float om = A.omega;
-    // down: z0 = w D^-1 f, res = f - K z0, restrict
-    for (int l = 0; l + 1 < A.nlev; ++l) {
-        const TailLevel& L = A.L[l];
-        const int n = (int)L.g.n;
-        for (int i = tid; i < 3 * n; i += nt) L.z[i] = om * L.dinv[i % n] * L.f[i];
-        __syncthreads();
-        for (int i = tid; i < 3 * n; i += nt) {
-            const int c = i / n, v = i - c * n;
-            L.res[i] = L.f[i] - tail_apply(L, L.z, c, v);
-        }
-        __syncthreads();
-        const TailLevel& C = A.L[l + 1];
-        const int nc = (int)C.g.n;
-        for (int i = tid; i < 3 * nc; i += nt) {
-            const int c = i / nc, v = i - c * nc;
-            const int X = v / C.g.pl, rem = v - X * C.g.pl, Y = rem / C.g.nz, Z = rem - Y * C.g.nz;
-            float sum = 0.f;
-            for (int dx = -1; dx <= 1; ++dx) {
-                if (!C.cf[0] && dx) continue;
-                const float wx = C.cf[0] ? (dx ? 0.25f : 0.5f) : 1.f;
-                const int x = C.cf[0] ? (2 * X + dx + L.g.nx) % L.g.nx : X;
-                for (int dy = -1; dy <= 1; ++dy) {
-                    if (!C.cf[1] && dy) continue;
-                    const float wy = C.cf[1] ? (dy ? 0.25f : 0.5f) : 1.f;
-                    const int y = C.cf[1] ? (2 * Y + dy + L.g.ny) % L.g.ny : Y;
-                    for (int dz = -1; dz <= 1; ++dz) {
-                        if (!C.cf[2] && dz) continue;
-                        const float wz = C.cf[2] ? (dz ? 0.25f : 0.5f) : 1.f;
-                        const int z = C.cf[2] ? (2 * Z + dz + L.g.nz) % L.g.nz : Z;
-                        sum += wx * wy * wz * L.res[(size_t)c * L.g.n + (x * L.g.ny + y) * L.g.nz + z];
-                    }
-                }
-            }
-            C.f[i] = sum;
-        }
-        __syncthreads();
-    }
-    // coarse solve: res_L = G f_L
-    {
-        const TailLevel& C = A.L[A.nlev - 1];
-        const int n = (int)C.g.n;
-        const int lane = tid & 31;
-        for (int i = tid >> 5; i < 3 * n; i += nt >> 5) {      // one warp per row, G rows coalesced
-            const int c = i / n, r = i - c * n;
-            const float* fr = C.f + (size_t)c * n;
-            float sum = 0.f;
-            for (int j = lane; j < n; j += 32) sum += A.G[(size_t)r * n + j] * fr[j];
-            sum = warp_sum(sum);
-            if (lane == 0) C.res[i] = sum;
-        }
-        __syncthreads();
-    }
-    // up: z += P res_{l+1}; res = z + w D^-1 (f - K z)
-    for (int l = A.nlev - 2; l >= 0; --l) {
-        const TailLevel& L = A.L[l];
-        const TailLevel& C = A.L[l + 1];
-        const int n = (int)L.g.n;
-        for (int i = tid; i < 3 * n; i += nt) {
-            const int c = i / n, v = i - c * n;
-            const int x = v / L.g.pl, rem = v - x * L.g.pl, y = rem / L.g.nz, z = rem - y * L.g.nz;
-            int xi[2], yi[2], zi[2];
-            float wx[2], wy[2], wz[2];
-            int nx_ = 1, ny_ = 1, nz_ = 1;
-            auto ax = [](int i0, int coars, int ncrs, int* idx, float* w, int& cnt) {
-                if (!coars) { idx[0] = i0; w[0] = 1.f; cnt = 1; return; }
-                const int J = i0 >> 1;
-                if (i0 & 1) { idx[0] = J; idx[1] = J + 1 == ncrs ? 0 : J + 1; w[0] = w[1] = .5f; cnt = 2; }
-                else { idx[0] = J; w[0] = 1.f; cnt = 1; }
-            };
-            ax(x, C.cf[0], C.g.nx, xi, wx, nx_);
-            ax(y, C.cf[1], C.g.ny, yi, wy, ny_);
-            ax(z, C.cf[2], C.g.nz, zi, wz, nz_);
-            float sum = 0.f;
-            for (int a = 0; a < nx_; ++a)
-                for (int b = 0; b < ny_; ++b)
-                    for (int d = 0; d < nz_; ++d)
-                        sum += wx[a] * wy[b] * wz[d] * C.res[(size_t)c * C.g.n + (xi[a] * C.g.ny + yi[b]) * C.g.nz + zi[d]];
-            L.z[i] += sum;
-        }
-        __syncthreads();
-        for (int i = tid; i < 3 * n; i += nt) {
-            const int c = i / n, v = i - c * n;
-            L.res[i] = L.z[i] + om * L.dinv[v] * (L.f[i] - tail_apply(L, L.z, c, v));
-        }
-        __syncthreads();
-    }
-}
-
-// ===========================================================================
-// V-cycle tail as ONE cooperative launch: the levels from the first tail level
-// (<= kCTailVerts vertices, every axis coarsened) down to the coarse solve and
-// back up, phases separated by grid barriers instead of kernel boundaries.  The
-// per-item code is the same as the per-level kernels (k_small, k_restrict3,
-// k_prolong3b, k_coarse_solve); loads of arrays written inside this launch go to
-// L2 (ld.cg).  Output: the post-smoothed correction in L[0].res, as the per-level
-// sequence leaves it.
-// ===========================================================================
-__global__ void __launch_bounds__(256) k_vtail_coop(TailArgs A) {
-    namespace cg = cooperative_groups;
-    cg::grid_group grid = cg::this_grid();
-    const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long nt = (long long)gridDim.x * blockDim.x;
-    const float om = A.omega;
-    double dummy[3];
-    for (int l = 0; l + 1 < A.nlev; ++l) {
-        const TailLevel& L = A.L[l];
-        const TailLevel& C = A.L[l + 1];
-        for (long long i = t0; i < 3 * L.g.n; i += nt)
-            small_item<0, false, true>(L.g, L.lt, L.kap, nullptr, L.f, L.dinv, om, L.z, L.res, i, dummy);
-        grid.sync();
-        for (long long i = t0; i < 3 * C.g.n; i += nt) restrict3_body<true>(L.g, C.g, L.res, C.f, i);
-        grid.sync();
-    }
-    {
-        const TailLevel& C = A.L[A.nlev - 1];
-        const int n = (int)C.g.n;
-        const int lane = threadIdx.x & 31;
-        for (long long w = t0 >> 5; w < 3 * n; w += nt >> 5) {
-            const int c = (int)(w / n), r = (int)(w - (long long)c * n);
-            float sum = 0.f;
-            for (int j = lane; j < n; j += 32) sum += __ldg(A.G + (size_t)r * n + j) * __ldcg(C.f + (size_t)c * n + j);
-            sum = warp_sum(sum);
-            if (lane == 0) C.res[w] = sum;
-        }
-        grid.sync();
-    }
-    for (int l = A.nlev - 2; l >= 0; --l) {
-        const TailLevel& L = A.L[l];
-        const TailLevel& C = A.L[l + 1];
-        for (long long i = t0; i < 3 * C.g.n; i += nt) prolong3b_body<true>(L.g, C.g, C.res, L.z, i);
-        grid.sync();
-        for (long long i = t0; i < 3 * L.g.n; i += nt)
-            small_item<1, false, true>(L.g, L.lt, L.kap, L.z, L.f, L.dinv, om, L.res, nullptr, i, dummy);
-        if (l > 0) grid.sync();
-    }
-}
-
 // ===========================================================================
 // Host launchers
 // ===========================================================================
@@ -2939,6 +1783,12 @@ static void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
     cfg.attrs = at;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
     cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
+// opt a kernel into more than 48 KB of dynamic shared memory (once per kernel)
+template <class K>
+static void smem_attr(K kernel, size_t bytes) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
 int stencil_chunks(const Geo& g, int* xb) {
@@ -3053,16 +1903,9 @@ void launch_coarse_solve(cudaStream_t s, int n, const float* G, const float* f, 
 }
 void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
                   const double* fext, const double* fmean, float* r32, Red& red, double* out9) {
-    static const bool use_b = getenv("OTM_RES64B") != nullptr;   // measured slower (248 vs 106 us at 128^3)
-    if (use_b && g.nz % 2 == 0 && g.nz >= 2) {
-        const long long th = 3 * (g.n >> 1);
-        k_res64b<<<nblk(th, 256), 256, 0, s>>>(g, lt, kap, T, fext, fmean, r32, red.partials, red.counter, out9);
-        return;
-    }
-    static const bool old64 = getenv("OTM_RES64_OLD") != nullptr;
     static const bool r512 = !(getenv("OTM_RES64_512") && atoi(getenv("OTM_RES64_512")) == 0);
     const bool w512 = r512 && lt.equal && g.nz == 512 && g.nx >= 2;
-    if (!fext && !old64 && (k6_ok(g, lt) || w512)) {
+    if (!fext && (tma_tiling(g, lt) || w512)) {
         const int tyd = g.nz >= 256 ? 1 : 256 / g.nz;
         // tensor maps of the last (T, kappa, grid) are reused: encoding costs a few us of
         // host time per map, on the critical path between two host waits
@@ -3091,32 +1934,24 @@ void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const d
             const dim3 blk((unsigned)g.nz, (unsigned)tyd);
             switch (g.nz) {
             case 512:
-                s3_attr(k_res64w<512>, sm);
+                smem_attr(k_res64w<512>, sm);
                 k_res64w<512><<<blocks, blk, sm, s>>>(g, lt, M, fmean, r32, red.partials, red.counter, out9);
                 break;
             case 64:
-                s3_attr(k_res64w<64>, sm);
+                smem_attr(k_res64w<64>, sm);
                 k_res64w<64><<<blocks, blk, sm, s>>>(g, lt, M, fmean, r32, red.partials, red.counter, out9);
                 break;
             case 128:
-                s3_attr(k_res64w<128>, sm);
+                smem_attr(k_res64w<128>, sm);
                 k_res64w<128><<<blocks, blk, sm, s>>>(g, lt, M, fmean, r32, red.partials, red.counter, out9);
                 break;
             default:
-                s3_attr(k_res64w<256>, sm);
+                smem_attr(k_res64w<256>, sm);
                 k_res64w<256><<<blocks, blk, sm, s>>>(g, lt, M, fmean, r32, red.partials, red.counter, out9);
                 break;
             }
             return;
         }
-    }
-    if (fast_tiling(g, lt)) {
-        int nch;
-        const int xb = fast_xb(g);
-        const dim3 grid = fast_grid(g, xb, &nch);
-        k2_res64<<<grid, dim3(32, kTileY), 0, s>>>(g, xb, nch, lt, kap, T, fext, fmean, r32, red.partials,
-                                                   red.counter, out9);
-        return;
     }
     int xb;
     const dim3 grid = stencil_grid(g, &xb);
@@ -3144,57 +1979,6 @@ void launch_sum3(cudaStream_t s, long long n, const double* f, Red& red, double*
 static inline bool small_level(const Geo& g) { return g.n <= 65536; }
 
 
-// dynamic-chunk counter of the k8 kernels of the context being enqueued (two
-// zero-initialised unsigned; nullptr or OTM_K8_DYN=0: static split)
-static unsigned* g_k8_work = nullptr;
-void set_k8_work(unsigned* p) { g_k8_work = p; }
-static unsigned* k8_work() {
-    static const bool off = !(getenv("OTM_K8_DYN") && atoi(getenv("OTM_K8_DYN")) == 1);   // measured slower: opt-in
-    return off ? nullptr : g_k8_work;
-}
-// k8 launch helpers: TY = rows per tile; 512/nz (256 threads, 1 CTA/SM) or, with
-// OTM_K8_TY=256, 256/nz (128 threads, 2 CTAs/SM)
-static int k8_tyn() {
-    static const int v = getenv("OTM_K8_TY") ? atoi(getenv("OTM_K8_TY")) : 512;
-    return v == 256 ? 256 : 512;
-}
-template <int NZ, int TY>
-static void l8_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const K6Maps& M, float omega,
-                          float* z, float* res) {
-    const size_t sm = k8_smem_bytes(4, NZ, TY);
-    s3_attr(k8_smooth_res<NZ, TY>, sm);
-    launch_pdl(k8_smooth_res<NZ, TY>, k6_grid(k8_smooth_res<NZ, TY>, sm, g, TY), dim3(NZ / 2, TY), sm, s, g, lt, M,
-               omega, z, res, k8_work());
-}
-template <bool DOT, int NZ, int TY>
-static void l8_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const K6Maps& M, const float* f,
-                      const float* dinv, float omega, float* zout, double* partials, unsigned* counter,
-                      PcgScalars* sc) {
-    const size_t sm = k8_smem_bytes(3, NZ, TY);
-    s3_attr(k8_jacobi<DOT, NZ, TY>, sm);
-    launch_pdl(k8_jacobi<DOT, NZ, TY>, k6_grid(k8_jacobi<DOT, NZ, TY>, sm, g, TY), dim3(NZ / 2, TY), sm, s, g, lt,
-               M, f, dinv, omega, zout, partials, counter, sc, k8_work());
-}
-template <int NZ, int TY>
-static void l8_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const K6Maps& M, float* q, Red& red,
-                    PcgScalars* sc) {
-    const size_t sm = k8_smem_bytes(3, NZ, TY);
-    s3_attr(k8_spmv<NZ, TY>, sm);
-    launch_pdl(k8_spmv<NZ, TY>, k6_grid(k8_spmv<NZ, TY>, sm, g, TY), dim3(NZ / 2, TY), sm, s, g, lt, M, q,
-               red.partials, red.counter, sc, k8_work());
-}
-#define OTM_K8_SWITCH(CALL)                                             \
-    do {                                                                \
-        const bool half = k8_tyn() == 256;                              \
-        switch (g.nz) {                                                 \
-        case 64: if (half) CALL(64, 4); else CALL(64, 8); break;        \
-        case 128: if (half) CALL(128, 2); else CALL(128, 4); break;     \
-        default: if (half) CALL(256, 1); else CALL(256, 2); break;      \
-        }                                                               \
-    } while (0)
-// ---- k10 host side: 4-D (z, case, y, x) maps so one box moves the three cases ----
-// nz > 256 (a box dimension holds at most 256 elements): z split into (256, nz / 256)
-// map dimensions, so the box still lands as [row][case][nz] (k10_ld_c3 / k10_ld_1)
 static bool encode_map4_split(CUtensorMap* m, const float* base, const Geo& g, int box_rows, bool cases) {
     PFN_encodeTiled_t fn = encode_fn();
     if (!fn) return tma_check(CUDA_ERROR_NOT_FOUND, "entry point");
@@ -3228,11 +2012,7 @@ static bool encode_map4(CUtensorMap* m, const float* base, const Geo& g, int box
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE), "4-d");
 }
-static int k10_ty_env();
-static int k10_ty(int nz) {
-    if (nz == 512) return 2;
-    return nz == 128 && (k10_ty_env() == 2 || k10_ty_env() == 8) ? k10_ty_env() : 512 / nz;
-}
+static int k10_ty(int nz) { return nz == 512 ? 2 : 512 / nz; }   // rows per CTA tile
 static long long k10_min_n() {           // smallest level on the k10 path (OTM_K10_MINN, tuning)
     static const long long v = getenv("OTM_K10_MINN") ? atoll(getenv("OTM_K10_MINN")) : 32768;
     return v;
@@ -3282,23 +2062,15 @@ template <int NZ, int TY, int CPS, bool WZ = true>
 static void l10_smooth_res(cudaStream_t s, const Geo& g, float s12, const K10Maps& M, float omega, float* z,
                            float* res) {
     const size_t sm = K10Geo<K10_SMOOTH, NZ, TY, CPS>::SMEM;
-    s3_attr(k10_smooth_res<NZ, TY, CPS, WZ>, sm);
+    smem_attr(k10_smooth_res<NZ, TY, CPS, WZ>, sm);
     launch_pdl(k10_smooth_res<NZ, TY, CPS, WZ>, k10_grid(k10_smooth_res<NZ, TY, CPS, WZ>, sm, g, TY),
                dim3(NZ / 2, TY), sm, s, g, s12, M, omega, z, res);
-}
-template <bool DOT, int NZ, int TY, int CPS>
-static void l10_jacobi_p(cudaStream_t s, const Geo& g, float s12, const K10Maps& M, float omega, float* zout,
-                         double* partials, unsigned* counter, PcgScalars* sc) {
-    const size_t sm = K10Geo<K10_JACOBI_P, NZ, TY, CPS>::SMEM;
-    s3_attr(k10_jacobi_p<DOT, NZ, TY, CPS>, sm);
-    launch_pdl(k10_jacobi_p<DOT, NZ, TY, CPS>, k10_grid(k10_jacobi_p<DOT, NZ, TY, CPS>, sm, g, TY),
-               dim3(NZ / 2, TY), sm, s, g, s12, M, omega, zout, partials, counter, sc);
 }
 template <bool DOT, int NZ, int TY, int CPS>
 static void l10_jacobi(cudaStream_t s, const Geo& g, float s12, const K10Maps& M, float omega, float* zout,
                        double* partials, unsigned* counter, PcgScalars* sc) {
     const size_t sm = K10Geo<K10_JACOBI, NZ, TY, CPS>::SMEM;
-    s3_attr(k10_jacobi<DOT, NZ, TY, CPS>, sm);
+    smem_attr(k10_jacobi<DOT, NZ, TY, CPS>, sm);
     launch_pdl(k10_jacobi<DOT, NZ, TY, CPS>, k10_grid(k10_jacobi<DOT, NZ, TY, CPS>, sm, g, TY), dim3(NZ / 2, TY),
                sm, s, g, s12, M, omega, zout, partials, counter, sc);
 }
@@ -3306,71 +2078,26 @@ template <int NZ, int TY, int CPS>
 static void l10_spmv(cudaStream_t s, const Geo& g, float s12, const K10Maps& M, float* q, Red& red,
                      PcgScalars* sc) {
     const size_t sm = K10Geo<K10_SPMV, NZ, TY, CPS>::SMEM;
-    s3_attr(k10_spmv<NZ, TY, CPS>, sm);
+    smem_attr(k10_spmv<NZ, TY, CPS>, sm);
     launch_pdl(k10_spmv<NZ, TY, CPS>, k10_grid(k10_spmv<NZ, TY, CPS>, sm, g, TY), dim3(NZ / 2, TY), sm, s, g, s12,
                M, q, red.partials, red.counter, sc);
 }
 // tile rows per CTA (OTM_K10_TY: 2/4/8 at nz = 128, tuning) and CTAs per SM
-static int k10_ty_env() {
-    static const int v = getenv("OTM_K10_TY") ? atoi(getenv("OTM_K10_TY")) : 0;
-    return v;
-}
 #define OTM_K10_SWITCH(CALL)                                                   \
     do {                                                                       \
         switch (g.nz) {                                                        \
         case 64: CALL(64, 8, 2); break;                                        \
-        case 128:                                                              \
-            if (k10_ty_env() == 2) CALL(128, 2, 4);                            \
-            else if (k10_ty_env() == 8) CALL(128, 8, 1);                       \
-            else CALL(128, 4, 2);                                              \
-            break;                                                             \
+        case 128: CALL(128, 4, 2); break;                                      \
         case 512: CALL(512, 2, 1); break;                                      \
         default: CALL(256, 2, 2); break;                                       \
         }                                                                      \
     } while (0)
 
-// Level legs without a stored z0 (k10 levels only, see K10_JACOBI_P):
-//   down: res = f - K (w D^-1 f)          [launch_smooth_res_nz]
-//   up:   z = P e (assign)                 [launch_prolong_assign]
-//         zout = z' + w D^-1 (f - K z'),  z' = w D^-1 f + z   [launch_jacobi_p]
-bool k10_level(const Geo& g, const LevelTemplate& lt) { return kernel_gen() == 10 && k10_ok(g, lt); }
-bool launch_smooth_res_nz(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* f,
-                          const float* dinv, float omega, float* res) {
-    K10Maps M;
-    if (!k10_level(g, lt) || !k10_maps(M, g, f, dinv, nullptr, kap)) return false;
-#define C_(NZ, TY, CPS) l10_smooth_res<NZ, TY, CPS, false>(s, g, (float)lt.s12, M, omega, nullptr, res)
-    OTM_K10_SWITCH(C_);
-#undef C_
-    return true;
-}
-bool launch_jacobi_p(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* pe,
-                     const float* f, const float* dinv, float omega, float* zout, bool dot, Red& red,
-                     PcgScalars* sc) {
-    K10Maps M;
-    if (!k10_level(g, lt) || !k10_maps(M, g, pe, dinv, f, kap)) return false;
-    if (dot) {
-#define C_(NZ, TY, CPS) l10_jacobi_p<true, NZ, TY, CPS>(s, g, (float)lt.s12, M, omega, zout, red.partials, red.counter, sc)
-        OTM_K10_SWITCH(C_);
-#undef C_
-    } else {
-#define C_(NZ, TY, CPS) l10_jacobi_p<false, NZ, TY, CPS>(s, g, (float)lt.s12, M, omega, zout, nullptr, nullptr, sc)
-        OTM_K10_SWITCH(C_);
-#undef C_
-    }
-    return true;
-}
-void launch_prolong_assign(cudaStream_t s, const Geo& f, const Geo& c, const float* zc, float* zf) {
-    launch_pdl(k_prolong3b<true>, nblk(3 * c.n, 256), 256, 0, s, f, c, zc, zf);
-}
-
-// k10 on the output planes [xa, xb) of a field stored with its x neighbours (slab
-// with ghost planes: xa >= 1, xb <= nx - 1, no x wrap).  op 0 smooth_res (o1 = z0,
-// o2 = res), 1 Jacobi (o1; r.z partial sums -> sc->red[0..2]), 2 K p (o1; p.q partial
-// sums -> sc->red[3..5]).  false: not eligible (caller uses its generic kernels).
+bool k10_level(const Geo& g, const LevelTemplate& lt) { return k10_ok(g, lt); }
 bool launch_k10_range(cudaStream_t s, int op, const Geo& g, const LevelTemplate& lt, int xa, int xb,
                       const float* kap, const float* a, const float* f, const float* dinv, float omega, float* o1,
                       float* o2, bool dot, Red& red, PcgScalars* sc) {
-    if (kernel_gen() != 10 || !k10_ok(g, lt) || xa < 1 || xb > g.nx - 1 || xb <= xa) return false;
+    if (!k10_ok(g, lt) || xa < 1 || xb > g.nx - 1 || xb <= xa) return false;
     K10Maps M;
     const float* op3 = op == 0 ? f : a;
     if (!k10_maps(M, g, op3, dinv, op == 1 ? f : nullptr, kap)) return false;
@@ -3402,7 +2129,7 @@ bool launch_k10_range(cudaStream_t s, int op, const Geo& g, const LevelTemplate&
 }
 void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* f,
                        const float* dinv, float omega, float* z, float* res) {
-    if (kernel_gen() == 10 && k10_ok(g, lt)) {
+    if (k10_ok(g, lt)) {
         K10Maps M;
         if (k10_maps(M, g, f, dinv, nullptr, kap)) {
 #define C_(NZ, TY, CPS) l10_smooth_res<NZ, TY, CPS>(s, g, (float)lt.s12, M, omega, z, res)
@@ -3411,105 +2138,9 @@ void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, co
             return;
         }
     }
-    if (kernel_gen() == 7 && k6_ok(g, lt)) {
-        K6Maps M;
-        if (k6_maps(M, g, f, dinv, kap)) {
-            const size_t sm = k6_smem_bytes(2, g.nz);
-            s3_attr(k7_smooth_res, sm);
-            k7_smooth_res<<<k7_grid(k7_smooth_res, sm, g), k6_block(g), sm, s>>>(g, lt, M, omega, z, res);
-            return;
-        }
-    }
-    if (kernel_gen() == 9 && k6_ok(g, lt)) {
-        K6Maps M;
-        if (k6_maps(M, g, f, dinv, kap)) {
-            switch (g.nz) {
-            case 64: {
-                constexpr int NZV = 64;
-                    const size_t sm = k9_smem_bytes(4, g.nz);
-                    s3_attr(k9_smooth_res<NZV>, sm);
-                    launch_pdl(k9_smooth_res<NZV>, k6_grid(k9_smooth_res<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, omega, z, res);
-            } break;
-            case 128: {
-                constexpr int NZV = 128;
-                    const size_t sm = k9_smem_bytes(4, g.nz);
-                    s3_attr(k9_smooth_res<NZV>, sm);
-                    launch_pdl(k9_smooth_res<NZV>, k6_grid(k9_smooth_res<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, omega, z, res);
-            } break;
-            default: {
-                constexpr int NZV = 256;
-                    const size_t sm = k9_smem_bytes(4, g.nz);
-                    s3_attr(k9_smooth_res<NZV>, sm);
-                    launch_pdl(k9_smooth_res<NZV>, k6_grid(k9_smooth_res<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, omega, z, res);
-            } break;
-            }
-            return;
-        }
-    }
-    if (kernel_gen() == 8 && k6_ok(g, lt)) {
-        K6Maps M;
-        if (k6_maps(M, g, f, dinv, kap, k8_tyn() / g.nz)) {
-#define C_(NZ, TY) l8_smooth_res<NZ, TY>(s, g, lt, M, omega, z, res)
-            OTM_K8_SWITCH(C_);
-#undef C_
-            return;
-        }
-    }
-    if (kernel_gen() == 6 && k6_ok(g, lt)) {
-        K6Maps M;
-        if (k6_maps(M, g, f, dinv, kap)) {
-            switch (g.nz) {
-            case 64: {
-                constexpr int NZV = 64;
-                    const size_t sm = k6_smem_bytes(4, g.nz);
-                    s3_attr(k6_smooth_res<NZV>, sm);
-                    launch_pdl(k6_smooth_res<NZV>, k6_grid(k6_smooth_res<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, omega, z, res);
-            } break;
-            case 128: {
-                constexpr int NZV = 128;
-                    const size_t sm = k6_smem_bytes(4, g.nz);
-                    s3_attr(k6_smooth_res<NZV>, sm);
-                    launch_pdl(k6_smooth_res<NZV>, k6_grid(k6_smooth_res<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, omega, z, res);
-            } break;
-            default: {
-                constexpr int NZV = 256;
-                    const size_t sm = k6_smem_bytes(4, g.nz);
-                    s3_attr(k6_smooth_res<NZV>, sm);
-                    launch_pdl(k6_smooth_res<NZV>, k6_grid(k6_smooth_res<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, omega, z, res);
-            } break;
-            }
-            return;
-        }
-    }
-    if (fast_tiling(g, lt) && kernel_gen() >= 4) {
-        const size_t sm = s4_smem_bytes<4>();
-        s3_attr(k4_smooth_res, sm);
-        k4_smooth_res<<<s4_grid(k4_smooth_res, sm, g), dim3(32, kTileY), sm, s>>>(g, lt, kap, f, dinv, omega, z, res);
-        return;
-    }
-    if (!fast_tiling(g, lt) && small_level(g)) {
+    if (small_level(g)) {
         launch_pdl(k_small<0, false>, nblk(3 * g.n, 256), 256, 0, s, g, lt, kap, nullptr, f, dinv, omega, z, res, nullptr,
-                                                             nullptr, nullptr);
-        return;
-    }
-    if (fast_tiling(g, lt) && s3_enabled()) {
-        const size_t sm = s3_smem_bytes<2>();
-        if (kernel_gen() == 5) {
-            s3_attr(k3_smooth_res<true>, sm);
-            k3_smooth_res<true><<<s3_grid(k3_smooth_res<true>, sm, g), dim3(32, kTileY), sm, s>>>(
-                g, 0, 0, lt, kap, f, dinv, omega, z, res);
-        } else {
-            s3_attr(k3_smooth_res<false>, sm);
-            k3_smooth_res<false><<<s3_grid(k3_smooth_res<false>, sm, g), dim3(32, kTileY), sm, s>>>(
-                g, 0, 0, lt, kap, f, dinv, omega, z, res);
-        }
-        return;
-    }
-    if (fast_tiling(g, lt)) {
-        int nch;
-        const int xb = fast_xb(g);
-        const dim3 grid = fast_grid(g, xb, &nch);
-        k2_smooth_res<<<grid, dim3(32, kTileY), 0, s>>>(g, xb, nch, lt, kap, f, dinv, omega, z, res);
+                   nullptr, nullptr);
         return;
     }
     int xb;
@@ -3519,7 +2150,7 @@ void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, co
 void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* z,
                    const float* f, const float* dinv, float omega, float* zout, bool dot, Red& red,
                    PcgScalars* sc) {
-    if (kernel_gen() == 10 && k10_ok(g, lt)) {
+    if (k10_ok(g, lt)) {
         K10Maps M;
         if (k10_maps(M, g, z, dinv, f, kap)) {
             if (dot) {
@@ -3534,179 +2165,13 @@ void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const 
             return;
         }
     }
-    if (kernel_gen() == 7 && k6_ok(g, lt)) {
-        K6Maps M;
-        if (k6_maps(M, g, z, nullptr, kap)) {
-            const size_t sm = k6_smem_bytes(1, g.nz);
-            if (dot) {
-                s3_attr(k7_jacobi<true>, sm);
-                k7_jacobi<true><<<k7_grid(k7_jacobi<true>, sm, g), k6_block(g), sm, s>>>(
-                    g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
-            } else {
-                s3_attr(k7_jacobi<false>, sm);
-                k7_jacobi<false><<<k7_grid(k7_jacobi<false>, sm, g), k6_block(g), sm, s>>>(
-                    g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
-            }
-            return;
-        }
-    }
-    if (kernel_gen() == 9 && k6_ok(g, lt)) {
-        K6Maps M;
-        if (k6_maps(M, g, z, nullptr, kap)) {
-            switch (g.nz) {
-            case 64: {
-                constexpr int NZV = 64;
-                    const size_t sm = k9_smem_bytes(3, g.nz);
-                    if (dot) {
-                        s3_attr(k9_jacobi<true, NZV>, sm);
-                        launch_pdl(k9_jacobi<true, NZV>, k6_grid(k9_jacobi<true, NZV>, sm, g), k6_block(g), sm, s,
-                            g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
-                    } else {
-                        s3_attr(k9_jacobi<false, NZV>, sm);
-                        launch_pdl(k9_jacobi<false, NZV>, k6_grid(k9_jacobi<false, NZV>, sm, g), k6_block(g), sm, s,
-                            g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
-                    }
-            } break;
-            case 128: {
-                constexpr int NZV = 128;
-                    const size_t sm = k9_smem_bytes(3, g.nz);
-                    if (dot) {
-                        s3_attr(k9_jacobi<true, NZV>, sm);
-                        launch_pdl(k9_jacobi<true, NZV>, k6_grid(k9_jacobi<true, NZV>, sm, g), k6_block(g), sm, s,
-                            g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
-                    } else {
-                        s3_attr(k9_jacobi<false, NZV>, sm);
-                        launch_pdl(k9_jacobi<false, NZV>, k6_grid(k9_jacobi<false, NZV>, sm, g), k6_block(g), sm, s,
-                            g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
-                    }
-            } break;
-            default: {
-                constexpr int NZV = 256;
-                    const size_t sm = k9_smem_bytes(3, g.nz);
-                    if (dot) {
-                        s3_attr(k9_jacobi<true, NZV>, sm);
-                        launch_pdl(k9_jacobi<true, NZV>, k6_grid(k9_jacobi<true, NZV>, sm, g), k6_block(g), sm, s,
-                            g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
-                    } else {
-                        s3_attr(k9_jacobi<false, NZV>, sm);
-                        launch_pdl(k9_jacobi<false, NZV>, k6_grid(k9_jacobi<false, NZV>, sm, g), k6_block(g), sm, s,
-                            g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
-                    }
-            } break;
-            }
-            return;
-        }
-    }
-    if (kernel_gen() == 8 && k6_ok(g, lt)) {
-        K6Maps M;
-        if (k6_maps(M, g, z, nullptr, kap, k8_tyn() / g.nz)) {
-            if (dot) {
-#define C_(NZ, TY) l8_jacobi<true, NZ, TY>(s, g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc)
-                OTM_K8_SWITCH(C_);
-#undef C_
-            } else {
-#define C_(NZ, TY) l8_jacobi<false, NZ, TY>(s, g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc)
-                OTM_K8_SWITCH(C_);
-#undef C_
-            }
-            return;
-        }
-    }
-    if (kernel_gen() == 6 && k6_ok(g, lt)) {
-        K6Maps M;
-        if (k6_maps(M, g, z, nullptr, kap)) {
-            switch (g.nz) {
-            case 64: {
-                constexpr int NZV = 64;
-                    const size_t sm = k6_smem_bytes(3, g.nz);
-                    if (dot) {
-                        s3_attr(k6_jacobi<true, NZV>, sm);
-                        launch_pdl(k6_jacobi<true, NZV>, k6_grid(k6_jacobi<true, NZV>, sm, g), k6_block(g), sm, s, 
-                            g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
-                    } else {
-                        s3_attr(k6_jacobi<false, NZV>, sm);
-                        launch_pdl(k6_jacobi<false, NZV>, k6_grid(k6_jacobi<false, NZV>, sm, g), k6_block(g), sm, s, 
-                            g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
-                    }
-            } break;
-            case 128: {
-                constexpr int NZV = 128;
-                    const size_t sm = k6_smem_bytes(3, g.nz);
-                    if (dot) {
-                        s3_attr(k6_jacobi<true, NZV>, sm);
-                        launch_pdl(k6_jacobi<true, NZV>, k6_grid(k6_jacobi<true, NZV>, sm, g), k6_block(g), sm, s, 
-                            g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
-                    } else {
-                        s3_attr(k6_jacobi<false, NZV>, sm);
-                        launch_pdl(k6_jacobi<false, NZV>, k6_grid(k6_jacobi<false, NZV>, sm, g), k6_block(g), sm, s, 
-                            g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
-                    }
-            } break;
-            default: {
-                constexpr int NZV = 256;
-                    const size_t sm = k6_smem_bytes(3, g.nz);
-                    if (dot) {
-                        s3_attr(k6_jacobi<true, NZV>, sm);
-                        launch_pdl(k6_jacobi<true, NZV>, k6_grid(k6_jacobi<true, NZV>, sm, g), k6_block(g), sm, s, 
-                            g, lt, M, f, dinv, omega, zout, red.partials, red.counter, sc);
-                    } else {
-                        s3_attr(k6_jacobi<false, NZV>, sm);
-                        launch_pdl(k6_jacobi<false, NZV>, k6_grid(k6_jacobi<false, NZV>, sm, g), k6_block(g), sm, s, 
-                            g, lt, M, f, dinv, omega, zout, nullptr, nullptr, sc);
-                    }
-            } break;
-            }
-            return;
-        }
-    }
-    if (fast_tiling(g, lt) && kernel_gen() >= 4 && kernel_gen() != 5) {
-        const size_t sm = s4_smem_bytes<3>();
-        if (dot) {
-            s3_attr(k4_jacobi<true>, sm);
-            k4_jacobi<true><<<s4_grid(k4_jacobi<true>, sm, g), dim3(32, kTileY), sm, s>>>(
-                g, lt, kap, z, f, dinv, omega, zout, red.partials, red.counter, sc);
-        } else {
-            s3_attr(k4_jacobi<false>, sm);
-            k4_jacobi<false><<<s4_grid(k4_jacobi<false>, sm, g), dim3(32, kTileY), sm, s>>>(
-                g, lt, kap, z, f, dinv, omega, zout, nullptr, nullptr, sc);
-        }
-        return;
-    }
-    if (!fast_tiling(g, lt) && small_level(g)) {
+    if (small_level(g)) {
         if (dot)
             launch_pdl(k_small<1, true>, nblk(3 * g.n, 256), 256, 0, s, g, lt, kap, z, f, dinv, omega, zout, nullptr,
-                                                                red.partials, red.counter, sc);
+                       red.partials, red.counter, sc);
         else
             launch_pdl(k_small<1, false>, nblk(3 * g.n, 256), 256, 0, s, g, lt, kap, z, f, dinv, omega, zout, nullptr,
-                                                                 nullptr, nullptr, sc);
-        return;
-    }
-    if (fast_tiling(g, lt) && s3_enabled()) {
-        const size_t sm = s3_smem_bytes<3>();
-        const bool k5 = kernel_gen() == 5;
-#define OTM_J3(D, K)                                                                                     \
-    do {                                                                                                 \
-        s3_attr(k3_jacobi<D, K>, sm);                                                                     \
-        k3_jacobi<D, K><<<s3_grid(k3_jacobi<D, K>, sm, g), dim3(32, kTileY), sm, s>>>(                     \
-            g, 0, 0, lt, kap, z, f, dinv, omega, zout, D ? red.partials : nullptr, D ? red.counter : nullptr, sc); \
-    } while (0)
-        if (dot && k5) OTM_J3(true, true);
-        else if (dot) OTM_J3(true, false);
-        else if (k5) OTM_J3(false, true);
-        else OTM_J3(false, false);
-#undef OTM_J3
-        return;
-    }
-    if (fast_tiling(g, lt)) {
-        int nch;
-        const int xb = fast_xb(g);
-        const dim3 grid = fast_grid(g, xb, &nch);
-        if (dot)
-            k2_jacobi<true><<<grid, dim3(32, kTileY), 0, s>>>(g, xb, nch, lt, kap, z, f, dinv, omega, zout,
-                                                              red.partials, red.counter, sc);
-        else
-            k2_jacobi<false><<<grid, dim3(32, kTileY), 0, s>>>(g, xb, nch, lt, kap, z, f, dinv, omega, zout,
-                                                               nullptr, nullptr, sc);
+                       nullptr, nullptr, sc);
         return;
     }
     int xb;
@@ -3718,7 +2183,7 @@ void launch_jacobi(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const 
 }
 void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* p,
                  float* q, Red& red, PcgScalars* sc) {
-    if (kernel_gen() == 10 && k10_ok(g, lt)) {
+    if (k10_ok(g, lt)) {
         K10Maps M;
         if (k10_maps(M, g, p, nullptr, nullptr, kap)) {
 #define C_(NZ, TY, CPS) l10_spmv<NZ, TY, CPS>(s, g, (float)lt.s12, M, q, red, sc)
@@ -3726,103 +2191,6 @@ void launch_spmv(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const fl
 #undef C_
             return;
         }
-    }
-    if (kernel_gen() == 7 && k6_ok(g, lt)) {
-        K6Maps M;
-        if (k6_maps(M, g, p, nullptr, kap)) {
-            const size_t sm = k6_smem_bytes(1, g.nz);
-            s3_attr(k7_spmv, sm);
-            k7_spmv<<<k7_grid(k7_spmv, sm, g), k6_block(g), sm, s>>>(g, lt, M, q, red.partials, red.counter, sc);
-            return;
-        }
-    }
-    if (kernel_gen() == 9 && k6_ok(g, lt)) {
-        K6Maps M;
-        if (k6_maps(M, g, p, nullptr, kap)) {
-            switch (g.nz) {
-            case 64: {
-                constexpr int NZV = 64;
-                    const size_t sm = k9_smem_bytes(3, g.nz);
-                    s3_attr(k9_spmv<NZV>, sm);
-                    launch_pdl(k9_spmv<NZV>, k6_grid(k9_spmv<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, q, red.partials, red.counter, sc);
-            } break;
-            case 128: {
-                constexpr int NZV = 128;
-                    const size_t sm = k9_smem_bytes(3, g.nz);
-                    s3_attr(k9_spmv<NZV>, sm);
-                    launch_pdl(k9_spmv<NZV>, k6_grid(k9_spmv<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, q, red.partials, red.counter, sc);
-            } break;
-            default: {
-                constexpr int NZV = 256;
-                    const size_t sm = k9_smem_bytes(3, g.nz);
-                    s3_attr(k9_spmv<NZV>, sm);
-                    launch_pdl(k9_spmv<NZV>, k6_grid(k9_spmv<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, q, red.partials, red.counter, sc);
-            } break;
-            }
-            return;
-        }
-    }
-    if (kernel_gen() == 8 && k6_ok(g, lt)) {
-        K6Maps M;
-        if (k6_maps(M, g, p, nullptr, kap, k8_tyn() / g.nz)) {
-#define C_(NZ, TY) l8_spmv<NZ, TY>(s, g, lt, M, q, red, sc)
-            OTM_K8_SWITCH(C_);
-#undef C_
-            return;
-        }
-    }
-    if (kernel_gen() == 6 && k6_ok(g, lt)) {
-        K6Maps M;
-        if (k6_maps(M, g, p, nullptr, kap)) {
-            switch (g.nz) {
-            case 64: {
-                constexpr int NZV = 64;
-                    const size_t sm = k6_smem_bytes(3, g.nz);
-                    s3_attr(k6_spmv<NZV>, sm);
-                    launch_pdl(k6_spmv<NZV>, k6_grid(k6_spmv<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, q, red.partials, red.counter, sc);
-            } break;
-            case 128: {
-                constexpr int NZV = 128;
-                    const size_t sm = k6_smem_bytes(3, g.nz);
-                    s3_attr(k6_spmv<NZV>, sm);
-                    launch_pdl(k6_spmv<NZV>, k6_grid(k6_spmv<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, q, red.partials, red.counter, sc);
-            } break;
-            default: {
-                constexpr int NZV = 256;
-                    const size_t sm = k6_smem_bytes(3, g.nz);
-                    s3_attr(k6_spmv<NZV>, sm);
-                    launch_pdl(k6_spmv<NZV>, k6_grid(k6_spmv<NZV>, sm, g), k6_block(g), sm, s, g, lt, M, q, red.partials, red.counter, sc);
-            } break;
-            }
-            return;
-        }
-    }
-    if (fast_tiling(g, lt) && kernel_gen() >= 4 && kernel_gen() != 5) {
-        const size_t sm = s4_smem_bytes<3>();
-        s3_attr(k4_spmv, sm);
-        k4_spmv<<<s4_grid(k4_spmv, sm, g), dim3(32, kTileY), sm, s>>>(g, lt, kap, p, q, red.partials, red.counter,
-                                                                      sc);
-        return;
-    }
-    if (fast_tiling(g, lt) && s3_enabled()) {
-        const size_t sm = s3_smem_bytes<1>();
-        if (kernel_gen() == 5) {
-            s3_attr(k3_spmv<true>, sm);
-            k3_spmv<true><<<s3_grid(k3_spmv<true>, sm, g), dim3(32, kTileY), sm, s>>>(g, 0, 0, lt, kap, p, q,
-                                                                                      red.partials, red.counter, sc);
-        } else {
-            s3_attr(k3_spmv<false>, sm);
-            k3_spmv<false><<<s3_grid(k3_spmv<false>, sm, g), dim3(32, kTileY), sm, s>>>(g, 0, 0, lt, kap, p, q,
-                                                                                        red.partials, red.counter, sc);
-        }
-        return;
-    }
-    if (fast_tiling(g, lt)) {
-        int nch;
-        const int xb = fast_xb(g);
-        const dim3 grid = fast_grid(g, xb, &nch);
-        k2_spmv<<<grid, dim3(32, kTileY), 0, s>>>(g, xb, nch, lt, kap, p, q, red.partials, red.counter, sc);
-        return;
     }
     int xb;
     const dim3 grid = stencil_grid(g, &xb);
@@ -3839,11 +2207,7 @@ void launch_upd(cudaStream_t s, long long n, float* r, const float* q, Red& red,
 }
 void launch_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* res, float* fc) {
     if (cf[0] && cf[1] && cf[2]) {
-        static const int rx = getenv("OTM_RESTRICT_X") ? atoi(getenv("OTM_RESTRICT_X")) : 0;
-        if (rx > 0 && c.nz % 32 == 0 && !getenv("OTM_OLD_RESTRICT")) {
-            const long long th = 3LL * c.pl * ((c.nx + 3) / 4);
-            launch_pdl(k_restrict3x<4>, nblk(th, 256), 256, 0, s, f, c, res, fc);
-        } else if (c.nz % 32 == 0 && !getenv("OTM_OLD_RESTRICT"))
+        if (c.nz % 32 == 0)
             launch_pdl(k_restrict3w, nblk(3 * c.n, 256), 256, 0, s, f, c, res, fc);
         else
             launch_pdl(k_restrict3, nblk(3 * c.n, 256), 256, 0, s, f, c, res, fc);
@@ -3861,65 +2225,16 @@ void launch_prolong(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3],
 void launch_loop_ctl(cudaStream_t s, PcgScalars* sc, unsigned long long handle) {
     k_loop_ctl<<<1, 1, 0, s>>>(sc, (cudaGraphConditionalHandle)handle);
 }
-void launch_vtail(cudaStream_t s, const TailArgs& a) { k_vtail<<<1, 1024, 0, s>>>(a); }
-// one 16-CTA cluster (non-portable size); false if the device cannot schedule it
-bool launch_vtail32(cudaStream_t s, const VTailArgs& a) {
-    static int ok = -1;
-    const size_t sm = (size_t)VtLay::FLOATS * 4;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(kVtCtas);
-    cfg.blockDim = dim3(512);
-    cfg.dynamicSmemBytes = sm;
-    cfg.stream = s;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = kVtCtas;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 2;
-    if (ok < 0) {
-        ok = cudaFuncSetAttribute(k_vtail32<>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
-             cudaFuncSetAttribute(k_vtail32<>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) == cudaSuccess;
-        int nclusters = 0;
-        if (ok) ok = cudaOccupancyMaxActiveClusters(&nclusters, (void*)k_vtail32<>, &cfg) == cudaSuccess && nclusters > 0;
-        cudaGetLastError();
-        if (!ok) fprintf(stderr, "[otm] 16-CTA cluster tail unavailable: per-level launches\n");
-    }
-    if (!ok) return false;
-    return cudaLaunchKernelEx(&cfg, k_vtail32<>, a) == cudaSuccess;
-}
 void launch_vbottom(cudaStream_t s, int N, const VBotArgs& a) {
     if (N == 16) {
         const size_t sm = (size_t)vbot_smem_floats(16) * 4;
-        s3_attr(k_vbottom<16>, sm);
+        smem_attr(k_vbottom<16>, sm);
         launch_pdl(k_vbottom<16>, dim3(1), dim3(1024), sm, s, a);
     } else {
         const size_t sm = (size_t)vbot_smem_floats(8) * 4;
-        s3_attr(k_vbottom<8>, sm);
+        smem_attr(k_vbottom<8>, sm);
         launch_pdl(k_vbottom<8>, dim3(1), dim3(1024), sm, s, a);
     }
-}
-int launch_vtail_coop(cudaStream_t s, const TailArgs& a) {
-    static int blocks = 0;
-    if (!blocks) {
-        int dev = 0, sms = 148, per_sm = 1;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vtail_coop, 256, 0);
-        const char* e = getenv("OTM_CTAIL_BPS");          // blocks per SM (tuning)
-        const int want = e ? atoi(e) : 1;
-        blocks = sms * std::max(1, std::min(per_sm, want));
-    }
-    TailArgs arg = a;
-    void* args[] = {(void*)&arg};
-    return cudaLaunchCooperativeKernel((void*)k_vtail_coop, dim3((unsigned)blocks), dim3(256), args, 0, s) ==
-                   cudaSuccess ? 0 : 1;
-}
-void launch_extrap(cudaStream_t s, long long n3, double* T, double* Tprev, double theta) {
-    k_extrap<<<nblk(n3, 256), 256, 0, s>>>(n3, T, Tprev, theta);
 }
 void launch_Tupd(cudaStream_t s, long long n, double* T, const float* d, const float* p, const PcgScalars* sc) {
     k_Tupd<<<nblk(3 * n, 256), 256, 0, s>>>(n, T, d, p, sc);

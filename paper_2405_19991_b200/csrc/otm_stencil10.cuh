@@ -25,7 +25,7 @@
 //   DC  TY x NZ           D^-1, centre rows          (jacobi)
 #pragma once
 
-#include "otm_stencil8.cuh"
+#include "otm_tma.cuh"
 
 namespace otm {
 

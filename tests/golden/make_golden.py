@@ -218,12 +218,65 @@ def gen_big(ot):
              wall_s=wall)
 
 
+def _run_logged(ot, name, dims, target, vf, max_iter, filt=1.5):
+    """Full reference run; stores the per-iteration log, the tensor after every
+    iteration and per-iteration wall times (the CPU-baseline sample)."""
+    from opentm.optimize import RunConfig, run_optimization
+    obj = ot.ObjectiveSpec("mse", ot.ConductivityTensor(np.array(target, float)))
+    cfg = RunConfig(dims=dims, target=obj, filter=ot.FilterSpec(filt),
+                    init=ot.InitPattern("iwp", vf, seed=0), max_iter=max_iter)
+    kap, stamps = [], [time.perf_counter()]
+
+    def cb(it, fld, result, g):
+        kap.append(result.tensor.vec.copy())
+        stamps.append(time.perf_counter())
+
+    t0 = time.perf_counter()
+    res = run_optimization(cfg, callback=cb)
+    wall = time.perf_counter() - t0
+    log = res.log
+    rho = res.field.rho
+    save(name, dims=np.array(dims), target=np.array(target, float), vf=vf, filter_radius=filt,
+         max_iter=max_iter, g=np.array([r.g for r in log]),
+         volfrac=np.array([r.volfrac for r in log]),
+         volfrac_filtered=np.array([r.volfrac_filtered for r in log]),
+         vstar=np.array([r.vstar for r in log]), vcycles=np.array([r.vcycles for r in log]),
+         iter_ms=np.array([r.ms for r in log]), kappa=np.array(kap),
+         iter_wall_s=np.diff(np.array(stamps)), kappa_final=res.kappa.vec,
+         rho_sum=float(rho.sum()), rho_sq=float((rho * rho).sum()),
+         rho_final=(rho.astype(np.float32) if rho.size <= 40000 else np.zeros(0)),
+         converged=res.converged, iterations=res.iterations, wall_s=wall)
+
+
+def gen_long(ot, which):
+    """Multi-iteration trajectories of the headline configs."""
+    if which == "c1conv":   # config 1 to convergence (reference: it 237, g 9.98e-5)
+        _run_logged(ot, "traj_c1_conv.npz", (32, 32, 32), [0.1, 0.1, 0.1, 0, 0, 0], 0.3, 500)
+    elif which == "c2":     # config 2, 30 iterations
+        _run_logged(ot, "traj_c2_30.npz", (64, 64, 64), [0.3, 0.2, 0.1, 0, 0, 0], 0.5, 30)
+    elif which == "c3":     # config 3, 3 iterations
+        _run_logged(ot, "traj_c3_3.npz", (128, 128, 128), [0.3, 0.2, 0.1, 0.1, 0.05, 0.05], 0.5, 3)
+    elif which == "c3x10":  # config 3, 10 iterations
+        _run_logged(ot, "traj_c3_10.npz", (128, 128, 128), [0.3, 0.2, 0.1, 0.1, 0.05, 0.05], 0.5, 10)
+    elif which == "flat":   # tests/test_acceptance.py:144-158 (100x100x1, r = 2, NaN targets)
+        _run_logged(ot, "traj_flat100.npz", (100, 100, 1), [0.4, 0.2, np.nan, 0.05, np.nan, np.nan],
+                    0.5, 500, filt=2.0)
+    else:
+        raise ValueError(which)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
     ap.add_argument("--only", default=None)
+    ap.add_argument("--long", default=None, help="c1conv | c2 | c3 | c3x10 | flat")
     args = ap.parse_args()
     ot = _ref()
+    if args.long:
+        t0 = time.perf_counter()
+        gen_long(ot, args.long)
+        print(f"  [long {args.long}] {time.perf_counter() - t0:.1f}s")
+        return
     steps = {"element": gen_element, "filter": gen_filter, "operator": gen_operator,
              "solve": gen_solve, "homog": gen_homog, "oc": gen_oc, "traj": gen_trajectory}
     if args.big:

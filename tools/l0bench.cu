@@ -1,6 +1,6 @@
 // Level-stencil microbenchmark + correctness check against a host fp64 element
 // assembly of K (K0 = template of element.py:59-88, kt[a ^ b]).  Links libotm.so;
-// OTM_K selects the stencil generation.  Usage: l0bench [n=128] [reps=50]
+// Usage: l0bench [n=128] [reps=50]
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -std=c++17 -I paper_2405_19991_b200/csrc \
 //        tools/l0bench.cu -L paper_2405_19991_b200 -lotm -Xlinker -rpath,'$ORIGIN/../paper_2405_19991_b200' -o tools/l0bench
 #include <cuda_runtime.h>
