@@ -321,9 +321,12 @@ def test_already_optimal(otm):
     assert otm.run_optimization(cfg).log[0].g < 1e-9
 
 
-@pytest.mark.parametrize("dims", [(8, 8, 64), (12, 16, 128), (64, 64, 64)])
+@pytest.mark.parametrize("dims", [(8, 8, 64), (12, 16, 128), (16, 16, 128), (8, 8, 512), (64, 64, 64)])
 def test_fast_path_solve_vs_oracle(otm, O, dims):
-    """Grids whose z/y extents take the vectorised stencil path (nz % 64 == 0, ny % 8 == 0)."""
+    """Solves against the oracle on grids that reach the TMA level stencils (k10: nz in
+    {64, 128, 256, 512}, >= 32768 vertices) and the fp64 defect k_res64w: (16, 16, 128)
+    and (8, 8, 512) (z-split tensor maps) are on k10 at level 0; (8, 8, 64) and
+    (12, 16, 128) run the generic level kernels."""
     rng = np.random.default_rng(sum(dims))
     rho = rng.uniform(0.05, 1.0, dims)
     mp = otm.MaterialParams()
