@@ -161,6 +161,31 @@ int otm_solve(otm_ctx* ctx, const double* f_dev, double tol, int max_cycles,
               int* cycles_out, double residual_out[3]);
 /* The mean-free corrective fields (3*n doubles). */
 int otm_get_T(otm_ctx* ctx, double* T_dev);
+/* GridHierarchy.residual_history (solver.py:247, 395-401) of the last otm_solve: one
+ * relative residual per preconditioner application (the worst over the cases it
+ * served; the last entry of every fp64 refinement step is the true fp64 residual).
+ * Copies min(count, cap) values to out (host) and returns count. */
+int otm_residual_history(const otm_ctx* ctx, double* out, int cap);
+
+/* ---- API-level multigrid pieces (solver.py:85-338), fp64, any level ----------
+ * The reference exposes its V-cycle parts as functions over mutable level arrays
+ * (GridLevel.T/f/r).  These run them on caller-owned fp64 device fields of level
+ * `level` (n_l doubles).  They use the reference's own smoother (8-colour GS);
+ * the design loop does not call them (it runs the batched MG-PCG above). */
+/* GridLevel.kappa: the level's child-mean element factors (solver.py:257-267). */
+int otm_level_kappa(otm_ctx* ctx, int level, double* kappa_dev);
+/* apply_K on any level (solver.py:111-119); f_dev != NULL gives f - K T (solver.py:334). */
+int otm_level_apply(otm_ctx* ctx, int level, const double* T_dev, const double* f_dev, double* out_dev);
+/* relax_gs8 (solver.py:131-164): colour-ordered Gauss-Seidel on T_dev in place.
+ * OTM_EINVAL for odd axes > 1, as the reference's ValueError. */
+int otm_relax_gs8(otm_ctx* ctx, int level, double* T_dev, const double* f_dev, int sweeps);
+/* restrict (solver.py:167-177): fc_dev (level_f + 1) = full-weighting R r_dev. */
+int otm_restrict(otm_ctx* ctx, int level_f, const double* r_dev, double* fc_dev);
+/* prolong_correct (solver.py:194-200): Tf_dev += P Tc_dev (Tc on level_f + 1). */
+int otm_prolong_correct(otm_ctx* ctx, int level_f, double* Tf_dev, const double* Tc_dev);
+/* coarse_solve (solver.py:307-324): T_dev = pinned direct solve of the coarsest level
+ * with the load mean projected out, mean-free result. */
+int otm_coarse_solve(otm_ctx* ctx, const double* f_dev, double* T_dev);
 /* effective_tensor (homogenize.py:103-130): packed [k11,k22,k33,k12,k23,k13]. */
 int otm_tensor(otm_ctx* ctx, double kappa_out[6]);
 /* pair_energy cache (6*n doubles, homogenize.py:116-120), for API compatibility. */

@@ -79,6 +79,13 @@ _SIGS = {
     "otm_solve": (C.c_int, [C.c_void_p, dptr, C.c_double, C.c_int, C.POINTER(C.c_int),
                             C.POINTER(C.c_double)]),
     "otm_get_T": (C.c_int, [C.c_void_p, dptr]),
+    "otm_residual_history": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_int]),
+    "otm_level_kappa": (C.c_int, [C.c_void_p, C.c_int, dptr]),
+    "otm_level_apply": (C.c_int, [C.c_void_p, C.c_int, dptr, dptr, dptr]),
+    "otm_relax_gs8": (C.c_int, [C.c_void_p, C.c_int, dptr, dptr, C.c_int]),
+    "otm_restrict": (C.c_int, [C.c_void_p, C.c_int, dptr, dptr]),
+    "otm_prolong_correct": (C.c_int, [C.c_void_p, C.c_int, dptr, dptr]),
+    "otm_coarse_solve": (C.c_int, [C.c_void_p, dptr, dptr]),
     "otm_tensor": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "otm_pair_energy": (C.c_int, [C.c_void_p, dptr]),
     "otm_sensitivity": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), dptr]),

@@ -28,6 +28,8 @@ using namespace otm;
 
 #define OTM_VERSION "0.1.0-b200"
 
+constexpr int kHistCap = 1024;   // inner PCG iterations recorded per inner loop
+
 namespace {
 
 struct LevelBuf {
@@ -86,6 +88,17 @@ struct otm_ctx {
     int vbot_max = getenv("OTM_VBOT") ? atoi(getenv("OTM_VBOT")) : 8;
     bool warm = false;
     bool have_T = false;
+    // per-V-cycle residual history of the last solve (GridHierarchy.residual_history,
+    // solver.py:247, 395-401); the design loop does not read it back
+    double* hist = nullptr;      // device: r.r per inner iteration and case
+    double* h_hist = nullptr;    // pinned mirror
+    bool want_hist = true;
+    std::vector<double> hist_rel;
+    // fp64 level factors and coarse inverse of the API-level multigrid operations
+    // (otm_levelops.cu), rebuilt lazily after every build
+    std::vector<double*> lk64;
+    double* minv64 = nullptr;
+    bool lv_valid = false;
     bool oc_pending = false;     // a cooperative OC search result still in flight to h + 384
     std::string err;
     size_t bytes = 0;
@@ -464,7 +477,15 @@ int enqueue_build(otm_ctx* ctx) {
         ctx->launches++;
     }
     for (int l = 0; l < nl; ++l) {
-        launch_dinv(s, ctx->L[l].g, ctx->L[l].kap, (float)ctx->L[l].lt.kt[0], ctx->L[l].dinv);
+        // diagonal template weight: on a flat axis (n = 1) the couplings to the corner
+        // across that axis wrap onto the vertex itself (_fold, solver.py:56-63), so the
+        // diagonal is sum of kt[d] over every corner offset d inside the flat axes
+        const Geo& g = ctx->L[l].g;
+        const int flat = (g.nx == 1 ? 1 : 0) | (g.ny == 1 ? 2 : 0) | (g.nz == 1 ? 4 : 0);
+        double kdiag = 0.0;
+        for (int d = 0; d < 8; ++d)
+            if ((d & ~flat) == 0) kdiag += ctx->L[l].lt.kt[d];
+        launch_dinv(s, g, ctx->L[l].kap, (float)kdiag, ctx->L[l].dinv);
         ctx->launches++;
     }
     CoarseTemplate ct;
@@ -485,6 +506,7 @@ void join_build(otm_ctx* ctx) {
 }
 
 int build_levels(otm_ctx* ctx, bool async = false) {
+    ctx->lv_valid = false;
     static const bool eager = getenv("OTM_NO_BUILD_GRAPH") != nullptr;
     static const bool no_async = getenv("OTM_NO_BUILD_OVERLAP") != nullptr;
     cudaStream_t s = ctx->stream;
@@ -676,6 +698,8 @@ int otm_create(otm_ctx** out, int nx, int ny, int nz, const otm_params* pin) {
     CK(dalloc(ctx, &ctx->changed, 4));
     CK(dalloc(ctx, &ctx->ocl, 1));
     CK(cudaMallocHost((void**)&ctx->h, 1024 * sizeof(double)));
+    CK(dalloc(ctx, &ctx->hist, 3 * kHistCap));
+    CK(cudaMallocHost((void**)&ctx->h_hist, 3 * kHistCap * sizeof(double)));
     CK(cudaMemset(ctx->T64, 0, 3 * n * sizeof(double)));
     CK(cudaMemset(ctx->p, 0, 3 * n * sizeof(float)));
     CK(cudaEventCreate(&ctx->ev_a));
@@ -716,6 +740,10 @@ int otm_destroy(otm_ctx* ctx) {
     F(ctx->G); F(ctx->gj); F(ctx->red.partials); F(ctx->red.counter); F(ctx->sc); F(ctx->scal);
     F(ctx->changed); F(ctx->ocl); F(ctx->fs.offs_dev); F(ctx->fs.wts_dev);
     if (ctx->h) cudaFreeHost(ctx->h);
+    if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
+    for (size_t l = 1; l < ctx->lk64.size(); ++l) F(ctx->lk64[l]);
+    F(ctx->minv64);
+    F(ctx->hist);
     if (ctx->side) {
         cudaStreamSynchronize(ctx->side);
         cudaStreamDestroy(ctx->side);
@@ -888,8 +916,15 @@ int otm_solve(otm_ctx* ctx, const double* fext, double tol, int max_cycles, int*
     bool zero_load[3];
     for (int c = 0; c < 3; ++c) zero_load[c] = fnorm[c] == 0.0;
     int status = OTM_OK;
+    int ccyc[3] = {0, 0, 0};                   // V-cycles per case (each case has max_cycles)
+    ctx->hist_rel.clear();
+    auto over_budget = [&]() {
+        for (int c = 0; c < 3; ++c)
+            if (!done[c] && ccyc[c] >= max_cycles) return true;
+        return false;
+    };
     while (!(done[0] && done[1] && done[2])) {
-        if (cycles >= max_cycles) { status = OTM_ENOCONV; break; }
+        if (over_budget()) { status = OTM_ENOCONV; break; }
         // inner fp32 MG-PCG on K d = r
         PcgScalars init;
         std::memset(&init, 0, sizeof init);
@@ -900,6 +935,7 @@ int otm_solve(otm_ctx* ctx, const double* fext, double tol, int max_cycles, int*
             const double tgt = std::max(ctx->P.inner_reduction * rnorm[c], tolf * tol * fnorm[c]);
             init.target2[c] = tgt * tgt;
             init.active[c] = done[c] ? 0.0 : 1.0;
+            init.ccyc[c] = ccyc[c];
         }
         init.first = 1;
         init.it = 0;
@@ -907,42 +943,75 @@ int otm_solve(otm_ctx* ctx, const double* fext, double tol, int max_cycles, int*
         init.cycles = cycles;
         init.max_cycles = max_cycles;
         init.nact = (int)!done[0] + (int)!done[1] + (int)!done[2];
+        init.hist = ctx->hist;
+        init.hcap = kHistCap;
+        init.hcount = 0;
         std::memcpy(ctx->h + 64, &init, sizeof init);
         CK(cudaMemcpyAsync(ctx->sc, ctx->h + 64, sizeof init, cudaMemcpyHostToDevice, s));
         CK(cudaMemsetAsync(ctx->d, 0, 3 * n * sizeof(float), s));
         CK(cudaMemsetAsync(ctx->p, 0, 3 * n * sizeof(float), s));
-        int active_n = (int)!done[0] + (int)!done[1] + (int)!done[2];
         if (ctx->gexec_loop && !ctx->prof) {
             CK(cudaGraphLaunch(ctx->gexec_loop, s));
-            CK(cudaMemcpyAsync(ctx->h + 160, ctx->sc, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
-            CK(stream_wait(s));
-            PcgScalars fin;
-            std::memcpy(&fin, ctx->h + 160, sizeof fin);
-            ctx->launches += (long long)fin.it * ctx->launches_per_inner;
-            ctx->stat_inner += fin.it;
-            cycles = fin.cycles;
-            for (int k = 0; k < 6; ++k) ctx->h[k] = fin.flags[k];
-        } else
-        for (int it = 0; it < ctx->P.max_inner; ++it) {
-            if (ctx->eager && !ctx->prof) {
-                int erc = enqueue_inner(ctx, false);       // profiler runs: plain stream launches
-                if (erc) return erc;
-            } else {
-                CK(cudaGraphLaunch(ctx->prof ? ctx->gexec_prof : ctx->gexec, s));
+        } else {
+            // one iteration per launch (profiling / eager runs): the same device-side
+            // counters, read back after every iteration
+            int worst = 0;
+            for (int it = 0; it < ctx->P.max_inner; ++it) {
+                if (ctx->eager && !ctx->prof) {
+                    int erc = enqueue_inner(ctx, false);       // profiler runs: plain stream launches
+                    if (erc) return erc;
+                } else {
+                    CK(cudaGraphLaunch(ctx->prof ? ctx->gexec_prof : ctx->gexec, s));
+                }
+                ctx->launches += ctx->launches_per_inner;
+                CK(cudaMemcpyAsync(ctx->h + 160, ctx->sc, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
+                CK(stream_wait(s));
+                if (ctx->prof) prof_harvest(ctx);
+                PcgScalars cur;
+                std::memcpy(&cur, ctx->h + 160, sizeof cur);
+                worst = 0;
+                for (int c = 0; c < 3; ++c)
+                    if (cur.active[c] != 0.0) worst = std::max(worst, cur.ccyc[c]);
+                if (cur.nact == 0 || worst >= max_cycles) break;
             }
-            ctx->launches += ctx->launches_per_inner;
-            CK(stream_wait(s));
-            if (ctx->prof) prof_harvest(ctx);
-            cycles += active_n;
-            active_n = (int)(ctx->h[0] != 0.0) + (int)(ctx->h[1] != 0.0) + (int)(ctx->h[2] != 0.0);
-            if (active_n == 0 || cycles >= max_cycles) break;
+        }
+        CK(cudaMemcpyAsync(ctx->h + 160, ctx->sc, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
+        if (ctx->want_hist) CK(cudaMemcpyAsync(ctx->h_hist, ctx->hist, 3 * kHistCap * sizeof(double),
+                                               cudaMemcpyDeviceToHost, s));
+        CK(stream_wait(s));
+        PcgScalars fin;
+        std::memcpy(&fin, ctx->h + 160, sizeof fin);
+        if (ctx->gexec_loop && !ctx->prof) ctx->launches += (long long)fin.it * ctx->launches_per_inner;
+        ctx->stat_inner += fin.it;
+        cycles = fin.cycles;
+        for (int c = 0; c < 3; ++c) ccyc[c] = fin.ccyc[c];
+        for (int k = 0; k < 6; ++k) ctx->h[k] = fin.flags[k];
+        if (ctx->want_hist) {
+            // per V-cycle: the worst relative inner residual over the cases it served
+            for (int k = 0; k < std::min(fin.hcount, kHistCap); ++k) {
+                double w = 0.0;
+                for (int c = 0; c < 3; ++c) {
+                    const double rr = ctx->h_hist[3 * k + c];
+                    if (rr >= 0.0 && fnorm[c] > 0.0) w = std::max(w, std::sqrt(rr) / fnorm[c]);
+                }
+                ctx->hist_rel.push_back(w);
+            }
         }
         launch_Tupd(s, n, ctx->T64, ctx->d, ctx->p, ctx->sc);
         ctx->launches++;
         ctx->stat_outer++;
         const double inner_rr[3] = {ctx->h[3], ctx->h[4], ctx->h[5]};
+        bool was_active[3];
+        for (int c = 0; c < 3; ++c) was_active[c] = !done[c];
         rc = residual();
         if (rc) return rc;
+        if (ctx->want_hist && !ctx->hist_rel.empty()) {
+            // the outer step ends on the true fp64 residual (solver.py:399-401)
+            double w = 0.0;
+            for (int c = 0; c < 3; ++c)
+                if (was_active[c]) w = std::max(w, rel[c]);
+            ctx->hist_rel.back() = w;
+        }
         if (debug)
             fprintf(stderr, "[otm]   outer: cycles %d  inner-est %.3e %.3e %.3e  true rel %.3e %.3e %.3e\n", cycles,
                     std::sqrt(inner_rr[0]) / fnorm[0], std::sqrt(inner_rr[1]) / fnorm[1],
@@ -970,6 +1039,115 @@ int otm_solve(otm_ctx* ctx, const double* fext, double tol, int max_cycles, int*
         return fail(ctx, OTM_ENOCONV, buf);
     }
     return OTM_OK;
+}
+
+// ---- API-level multigrid operations (solver.py:85-338), fp64 ------------------
+
+static int lv_prepare(otm_ctx* ctx) {
+    if (!ctx->built) return fail(ctx, OTM_ESTATE, "hierarchy not built; call build() first");
+    if (ctx->lv_valid) return OTM_OK;
+    join_build(ctx);
+    cudaStream_t s = ctx->stream;
+    const size_t nl = ctx->L.size();
+    if (ctx->lk64.empty()) {
+        ctx->lk64.assign(nl, nullptr);
+        for (size_t l = 1; l < nl; ++l) CK(dalloc(ctx, &ctx->lk64[l], ctx->L[l].g.n));
+        const long long nc = ctx->L.back().g.n;
+        if (nc > 1) CK(dalloc(ctx, &ctx->minv64, (size_t)(nc - 1) * (nc - 1)));
+    }
+    ctx->lk64[0] = ctx->kap64;
+    for (size_t l = 1; l < nl; ++l)
+        launch_lv_coarsen(s, ctx->L[l - 1].g, ctx->L[l].g, ctx->L[l].cf, ctx->lk64[l - 1], ctx->lk64[l]);
+    const LevelBuf& C = ctx->L.back();
+    if (C.g.n > 1) launch_lv_coarse_factor(s, C.g, C.lt, ctx->lk64[nl - 1], ctx->minv64);
+    CKL();
+    ctx->lv_valid = true;
+    return OTM_OK;
+}
+
+static int lv_level(otm_ctx* ctx, int level) {
+    if (level < 0 || level >= (int)ctx->L.size()) return fail(ctx, OTM_EINVAL, "level index out of range");
+    return lv_prepare(ctx);
+}
+
+int otm_level_kappa(otm_ctx* ctx, int level, double* kappa) {
+    if (!ctx || !kappa) return OTM_EINVAL;
+    int rc = lv_level(ctx, level);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(kappa, ctx->lk64[level], ctx->L[level].g.n * sizeof(double), cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+    return OTM_OK;
+}
+
+int otm_level_apply(otm_ctx* ctx, int level, const double* T, const double* f, double* out) {
+    if (!ctx || !T || !out) return OTM_EINVAL;
+    int rc = lv_level(ctx, level);
+    if (rc) return rc;
+    const LevelBuf& A = ctx->L[level];
+    launch_lv_apply(ctx->stream, A.g, A.lt, ctx->lk64[level], T, f, out);
+    ctx->launches++;
+    CKL();
+    return OTM_OK;
+}
+
+int otm_relax_gs8(otm_ctx* ctx, int level, double* T, const double* f, int sweeps) {
+    if (!ctx || !T || !f) return OTM_EINVAL;
+    int rc = lv_level(ctx, level);
+    if (rc) return rc;
+    const LevelBuf& A = ctx->L[level];
+    const int d[3] = {A.g.nx, A.g.ny, A.g.nz};
+    for (int a = 0; a < 3; ++a)
+        if (d[a] > 1 && d[a] % 2) {
+            char buf[128];
+            snprintf(buf, sizeof buf, "relaxation needs even axes, got dims (%d, %d, %d)", d[0], d[1], d[2]);
+            return fail(ctx, OTM_EINVAL, buf);
+        }
+    launch_lv_gs8(ctx->stream, A.g, A.lt, ctx->lk64[level], f, T, sweeps);
+    CKL();
+    return OTM_OK;
+}
+
+int otm_restrict(otm_ctx* ctx, int level_f, const double* r, double* fc) {
+    if (!ctx || !r || !fc) return OTM_EINVAL;
+    if (level_f + 1 >= (int)ctx->L.size()) return fail(ctx, OTM_EINVAL, "no coarser level");
+    int rc = lv_level(ctx, level_f);
+    if (rc) return rc;
+    const LevelBuf& B = ctx->L[level_f + 1];
+    launch_lv_restrict(ctx->stream, ctx->L[level_f].g, B.g, B.cf, r, fc);
+    CKL();
+    return OTM_OK;
+}
+
+int otm_prolong_correct(otm_ctx* ctx, int level_f, double* Tf, const double* Tc) {
+    if (!ctx || !Tf || !Tc) return OTM_EINVAL;
+    if (level_f + 1 >= (int)ctx->L.size()) return fail(ctx, OTM_EINVAL, "no coarser level");
+    int rc = lv_level(ctx, level_f);
+    if (rc) return rc;
+    const LevelBuf& B = ctx->L[level_f + 1];
+    launch_lv_prolong(ctx->stream, ctx->L[level_f].g, B.g, B.cf, Tc, Tf);
+    CKL();
+    return OTM_OK;
+}
+
+int otm_coarse_solve(otm_ctx* ctx, const double* f, double* T) {
+    if (!ctx || !f || !T) return OTM_EINVAL;
+    int rc = lv_prepare(ctx);
+    if (rc) return rc;
+    const int n = (int)ctx->L.back().g.n;
+    if (n == 1) {
+        CK(cudaMemsetAsync(T, 0, sizeof(double), ctx->stream));
+        return OTM_OK;
+    }
+    launch_lv_coarse_solve(ctx->stream, n, ctx->minv64, f, T);
+    CKL();
+    return OTM_OK;
+}
+
+int otm_residual_history(const otm_ctx* ctx, double* out, int cap) {
+    if (!ctx) return -1;
+    const int n = (int)ctx->hist_rel.size();
+    for (int k = 0; k < n && k < cap && out; ++k) out[k] = ctx->hist_rel[k];
+    return n;
 }
 
 int otm_get_T(otm_ctx* ctx, double* T) {
@@ -1292,7 +1470,9 @@ int otm_run_step(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, dou
     ctx->warm = st->warm != 0;
     int cycles = 0;
     double resid[3];
+    ctx->want_hist = false;                    // the design loop never reads the history back
     rc = otm_solve(ctx, nullptr, cfg->solver_tol, cfg->max_vcycles, &cycles, resid);
+    ctx->want_hist = true;
     if (rc == OTM_ENOCONV) {
         char buf[256];
         snprintf(buf, sizeof buf, "solver failed at iteration %d: %s", it, ctx->err.c_str());

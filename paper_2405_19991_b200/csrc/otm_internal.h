@@ -70,8 +70,11 @@ struct PcgScalars {
     int it;              // device-side inner loop control (conditional graph node)
     int max_it;
     int cycles;          // preconditioner applications summed over active cases
-    int max_cycles;
+    int max_cycles;      // budget PER CASE (homogenize.py:85-90 gives every case its own)
     int nact;            // cases active at the start of the current iteration
+    int ccyc[3];         // preconditioner applications of each case
+    int hcount, hcap;    // residual history of the current inner loop: hist[3 * it + c] = r.r
+    double* hist;        // (-1 for a case that was not active in that iteration)
 };
 
 // Deterministic two-stage reduction workspace.
@@ -129,7 +132,6 @@ void launch_upd(cudaStream_t s, long long n, float* r, const float* q, Red& red,
                 unsigned long long loop = 0);
 void launch_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* res, float* fc);
 void launch_prolong(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* zc, float* zf);
-void launch_loop_ctl(cudaStream_t s, PcgScalars* sc, unsigned long long handle);
 void launch_Tupd(cudaStream_t s, long long n, double* T, const float* d, const float* p, const PcgScalars* sc);
 void launch_submean_means(cudaStream_t s, long long n, double* T, const double* means);
 void launch_submean(cudaStream_t s, long long n, double* T, const double* sumT);
@@ -143,5 +145,16 @@ int launch_oc_coop(cudaStream_t s, long long n, const double* rho, const double*
                    double* rho_out, OcCtl* ctl, double* partials);
 void launch_oc_apply(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a,
                      double lam, double* rho_out, int* changed);
+
+// API-level multigrid operations in fp64 (otm_levelops.cu; solver.py:85-338)
+void launch_lv_apply(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
+                     const double* f, double* out);   // f != NULL: out = f - K T
+void launch_lv_gs8(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* f, double* T,
+                   int sweeps);
+void launch_lv_coarsen(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const double* kf, double* kc);
+void launch_lv_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const double* r, double* fc);
+void launch_lv_prolong(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const double* Tc, double* Tf);
+void launch_lv_coarse_factor(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, double* M);
+void launch_lv_coarse_solve(cudaStream_t s, int n, const double* Minv, const double* f, double* T);
 
 }  // namespace otm

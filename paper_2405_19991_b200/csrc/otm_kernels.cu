@@ -849,23 +849,36 @@ __global__ void __launch_bounds__(256) k_upd(long long n, float* __restrict__ r,
         }
     }
     if (reduce_finalize<3>(acc, partials, counter, sc->red + 6)) {
+        bool was[3];
         for (int c = 0; c < 3; ++c) {
+            was[c] = sc->active[c] != 0.0;
             sc->rr[c] = sc->red[6 + c];
-            if (sc->active[c] != 0.0 && sc->rr[c] <= sc->target2[c]) sc->active[c] = 0.0;
+            if (was[c] && sc->rr[c] <= sc->target2[c]) sc->active[c] = 0.0;
             sc->flags[c] = sc->active[c];
         }
         sc->flags[3] = sc->rr[0];
         sc->flags[4] = sc->rr[1];
         sc->flags[5] = sc->rr[2];
+        if (sc->hist && sc->hcount < sc->hcap) {
+            for (int c = 0; c < 3; ++c) sc->hist[3 * sc->hcount + c] = was[c] ? sc->rr[c] : -1.0;
+            sc->hcount += 1;
+        }
+        // the inner-loop control: count the preconditioner applications (in total and
+        // per case), decide whether the WHILE node runs again; every case has its own
+        // budget of max_cycles V-cycles (homogenize.py:85-90)
+        int nact = 0, worst = 0;
+        for (int c = 0; c < 3; ++c) {
+            sc->ccyc[c] += was[c];
+            if (sc->active[c] != 0.0) {
+                ++nact;
+                worst = max(worst, sc->ccyc[c]);
+            }
+        }
+        sc->cycles += sc->nact;
+        sc->nact = nact;
+        sc->it += 1;
         if (loop) {
-            // the inner-loop control (formerly a separate 1-thread launch): count the
-            // preconditioner applications, decide whether the WHILE node runs again
-            sc->cycles += sc->nact;
-            int nact = 0;
-            for (int c = 0; c < 3; ++c) nact += sc->active[c] != 0.0;
-            sc->nact = nact;
-            sc->it += 1;
-            const bool more = nact > 0 && sc->it < sc->max_it && sc->cycles < sc->max_cycles;
+            const bool more = nact > 0 && sc->it < sc->max_it && worst < sc->max_cycles;
             cudaGraphSetConditional((cudaGraphConditionalHandle)loop, more ? 1u : 0u);
         }
     }
@@ -1174,18 +1187,6 @@ __global__ void k_prolong(Geo f, Geo c, int cx, int cy, int cz, const float* __r
                     s += wx[i] * wy[j] * wz[k] * a[((long long)xs[i] * c.ny + ys[j]) * c.nz + zs[k]];
         zf[(size_t)cc * f.n + v] += s;
     }
-}
-
-// Inner-loop control, last node of the WHILE body: count the V-cycles spent, and
-// keep looping while a case is active and the budgets allow.
-__global__ void k_loop_ctl(PcgScalars* sc, cudaGraphConditionalHandle h) {
-    sc->cycles += sc->nact;
-    int nact = 0;
-    for (int c = 0; c < 3; ++c) nact += sc->active[c] != 0.0;
-    sc->nact = nact;
-    sc->it += 1;
-    const bool more = nact > 0 && sc->it < sc->max_it && sc->cycles < sc->max_cycles;
-    cudaGraphSetConditional(h, more ? 1u : 0u);
 }
 
 // Warm-start extrapolation across design iterations: T <- T + theta (T - T_prev), T_prev <- T.
@@ -2221,9 +2222,6 @@ void launch_prolong(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3],
         return;
     }
     k_prolong<<<nblk(f.n, 256), 256, 0, s>>>(f, c, cf[0], cf[1], cf[2], zc, zf);
-}
-void launch_loop_ctl(cudaStream_t s, PcgScalars* sc, unsigned long long handle) {
-    k_loop_ctl<<<1, 1, 0, s>>>(sc, (cudaGraphConditionalHandle)handle);
 }
 void launch_vbottom(cudaStream_t s, int N, const VBotArgs& a) {
     if (N == 16) {

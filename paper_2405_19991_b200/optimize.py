@@ -314,16 +314,23 @@ def run_optimization(config: RunConfig, callback: Optional[Callable] = None,
                      device_result: bool = False) -> OptimizationResult:
     """The full design loop (optimize.py:257-379) on the device.
 
-    The returned field is numpy (as in the reference) unless ``device_result``."""
+    The returned field is numpy (as in the reference) unless ``device_result`` or the
+    run was seeded from a device tensor.  ``callback(it, fld, result, g)`` receives,
+    as in the reference (optimize.py:324-325), the live density field and a
+    ``HomogenizationResult`` of this iteration: numpy arrays (``fld.rho``,
+    ``result.T_fields``, ``result.rho_filtered``) for host runs, device tensors for
+    device runs; ``tensor_sensitivity(result, dG)`` works on it."""
     report = feasibility_check(config.target.target)
     if not report.feasible:
         warnings.warn(f"target tensor is not positive definite (leading minor {report.violated_minor} "
                       "fails); optimization may not reach it", RuntimeWarning)
     _check_supported(config)
     run = DesignRun(config, hier=_cached_hierarchy(config))
+    on_device = device_result or hasattr(config.init_field, "data_ptr")
+    host_fld = None
 
     def result(converged):
-        rho = run.rho if device_result else run.rho.cpu().numpy()
+        rho = run.rho if on_device else run.rho.cpu().numpy()
         fld = DensityField(config.dims, rho, rho * 0)
         kap = run.kappa if run.kappa is not None else ConductivityTensor(np.full(6, np.nan))
         return OptimizationResult(field=fld, kappa=kap, log=run.log, converged=converged,
@@ -336,10 +343,29 @@ def run_optimization(config: RunConfig, callback: Optional[Callable] = None,
         if rc != _lib.OTM_OK:
             run.hier.ctx.check(rc)
         if callback is not None:
-            # the live device field at evaluation time, as in optimize.py:324-325
-            fld = DensityField(config.dims, run.rho, run.sens)
-            res = HomogenizationResult(tensor=run.kappa, T_fields=[], rho_filtered=run.rho_f,
-                                       params=config.material, vcycles=rec.vcycles)
+            h = run.hier
+            T = h.ctx.empty(3, *config.dims)
+            h.ctx.call("otm_get_T", _dev.ptr(T))
+            if on_device:
+                fld = DensityField(config.dims, run.rho, run.sens)
+                res = HomogenizationResult(tensor=run.kappa, T_fields=[T[i] for i in range(3)],
+                                           rho_filtered=run.rho_f.clone(), params=config.material,
+                                           vcycles=rec.vcycles, _hier=h, _version=h.ctx.version)
+            else:
+                # one DensityField mutated in place across iterations, as the reference's
+                # fld; its grad holds the (symmetrised) sensitivity only under central
+                # symmetry (optimize.py:308-311)
+                if host_fld is None:
+                    host_fld = DensityField(config.dims, run.rho.cpu().numpy(), np.zeros(config.dims))
+                else:
+                    host_fld.rho[...] = run.rho.cpu().numpy()
+                if config.symmetry == "central":
+                    host_fld.grad[...] = run.sens.cpu().numpy()
+                fld = host_fld
+                Th = T.cpu().numpy()
+                res = HomogenizationResult(tensor=run.kappa, T_fields=[Th[i] for i in range(3)],
+                                           rho_filtered=run.rho_f.cpu().numpy(), params=config.material,
+                                           vcycles=rec.vcycles, _hier=h, _version=h.ctx.version)
             callback(rec.iter, fld, res, rec.g)
         if not run.finished:
             run.update()

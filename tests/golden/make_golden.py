@@ -218,13 +218,20 @@ def gen_big(ot):
              wall_s=wall)
 
 
+SOLVER_TOL = None   # --tol: the same runs at another solver tolerance (chaos envelope)
+
+
 def _run_logged(ot, name, dims, target, vf, max_iter, filt=1.5):
     """Full reference run; stores the per-iteration log, the tensor after every
     iteration and per-iteration wall times (the CPU-baseline sample)."""
     from opentm.optimize import RunConfig, run_optimization
     obj = ot.ObjectiveSpec("mse", ot.ConductivityTensor(np.array(target, float)))
+    extra = {}
+    if SOLVER_TOL is not None:
+        extra["solver_tol"] = SOLVER_TOL
+        name = name.replace(".npz", f"_tol{SOLVER_TOL:.0e}.npz".replace("-0", "-"))
     cfg = RunConfig(dims=dims, target=obj, filter=ot.FilterSpec(filt),
-                    init=ot.InitPattern("iwp", vf, seed=0), max_iter=max_iter)
+                    init=ot.InitPattern("iwp", vf, seed=0), max_iter=max_iter, **extra)
     kap, stamps = [], [time.perf_counter()]
 
     def cb(it, fld, result, g):
@@ -265,12 +272,56 @@ def gen_long(ot, which):
         raise ValueError(which)
 
 
+def gen_io(ot):
+    """Reference-rendered bytes of every output file (io.py:125-171) for a synthetic
+    result, plus the CLI's gallery target list (cli.py:251-283)."""
+    import tempfile
+    from opentm.cli import enumerate_gallery_targets
+    from opentm.io import write_outputs
+    from opentm.optimize import IterationRecord, Model, OCParams, OptimizationResult, RunConfig
+    rng = np.random.default_rng(105)
+    rho = rng.uniform(0, 1, (5, 4, 3))
+    target = np.array([0.3, 0.2, np.nan, 0.05, np.nan, 0.01])
+    kap = np.array([0.31, 0.19, 0.11, 0.049, 0.002, 0.0101])
+    cfg = RunConfig(dims=(5, 4, 3), target=ot.ObjectiveSpec("rel", ot.ConductivityTensor(target)),
+                    material=ot.MaterialParams(1.0, 1e-3, 3.5), filter=ot.FilterSpec(2.0),
+                    init=ot.InitPattern("random", 0.4, seed=7), model=Model("fixed"), volume_bound=0.4,
+                    oc=OCParams(0.002, 0.03, 0.5), max_iter=9, symmetry="central", solver_tol=1e-7)
+    its = np.arange(1, 5)
+    gs = rng.uniform(1e-6, 1, 4)
+    vols = rng.uniform(0.2, 0.6, 4)
+    vst = rng.uniform(0.2, 0.6, 4)
+    cyc = np.array([12, 7, 9, 30])
+    ms = rng.uniform(0.5, 900.0, 4)
+    log = [IterationRecord(int(i), float(g), float(v), float(v) * 0.9, float(s), int(c), float(m))
+           for i, g, v, s, c, m in zip(its, gs, vols, vst, cyc, ms)]
+    res = OptimizationResult(field=ot.DensityField((5, 4, 3), rho, np.zeros((5, 4, 3))),
+                             kappa=ot.ConductivityTensor(kap), log=log, converged=False, iterations=4, config=cfg)
+    out = {"rho": rho, "target": target, "kappa": kap, "its": its, "gs": gs, "vols": vols, "vst": vst,
+           "cyc": cyc, "ms": ms}
+    with tempfile.TemporaryDirectory() as d:
+        write_outputs(res, d, vtk=True, manifest_extra={"aborted": True, "config_file": None})
+        for name in ("rho.otm", "kappa.txt", "log.csv", "manifest.json", "rho.vti"):
+            out["file_" + name.replace(".", "_")] = np.frombuffer(open(os.path.join(d, name), "rb").read(),
+                                                                  dtype=np.uint8)
+    raw, feas = enumerate_gallery_targets([0.3, 0.2, 0.1], 0.05)
+    out["gallery_raw"] = np.array(raw)
+    out["gallery_feasible"] = np.array(feas)
+    raw2, feas2 = enumerate_gallery_targets([0.5, 0.3, 0.2], 0.04)
+    out["gallery2_raw"] = np.array(raw2)
+    out["gallery2_feasible"] = np.array(feas2)
+    save("io.npz", **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
     ap.add_argument("--only", default=None)
     ap.add_argument("--long", default=None, help="c1conv | c2 | c3 | c3x10 | flat")
+    ap.add_argument("--tol", type=float, default=None, help="solver_tol of the --long run")
     args = ap.parse_args()
+    global SOLVER_TOL
+    SOLVER_TOL = args.tol
     ot = _ref()
     if args.long:
         t0 = time.perf_counter()
@@ -278,7 +329,7 @@ def main():
         print(f"  [long {args.long}] {time.perf_counter() - t0:.1f}s")
         return
     steps = {"element": gen_element, "filter": gen_filter, "operator": gen_operator,
-             "solve": gen_solve, "homog": gen_homog, "oc": gen_oc, "traj": gen_trajectory}
+             "solve": gen_solve, "homog": gen_homog, "oc": gen_oc, "traj": gen_trajectory, "io": gen_io}
     if args.big:
         steps["big"] = gen_big
     for name, fn in steps.items():

@@ -157,3 +157,58 @@ class TestCliGpu:
         lines = (tmp_path / "summary.csv").read_text().strip().splitlines()
         assert len(lines) == 62 and all(l.endswith(",ok") for l in lines[1:])
         assert (tmp_path / "case_060" / "manifest.json").exists()
+
+
+class TestReferenceBytes:
+    """Every output file byte-identical to what the reference's own writers produce
+    for the same result (tests/golden/io.npz, make_golden.py gen_io)."""
+
+    def _result(self):
+        from otm_testutil import golden
+        import paper_2405_19991_b200 as otm
+        from paper_2405_19991_b200.optimize import IterationRecord, OptimizationResult
+        g = golden("io.npz")
+        cfg = otm.RunConfig(dims=(5, 4, 3), target=otm.ObjectiveSpec("rel", otm.ConductivityTensor(g["target"])),
+                            material=otm.MaterialParams(1.0, 1e-3, 3.5), filter=otm.FilterSpec(2.0),
+                            init=otm.InitPattern("random", 0.4, seed=7), model="fixed", volume_bound=0.4,
+                            oc=otm.OCParams(0.002, 0.03, 0.5), max_iter=9, symmetry="central", solver_tol=1e-7)
+        log = [IterationRecord(int(i), float(gg), float(v), float(v) * 0.9, float(s), int(c), float(m))
+               for i, gg, v, s, c, m in zip(g["its"], g["gs"], g["vols"], g["vst"], g["cyc"], g["ms"])]
+        res = OptimizationResult(field=otm.DensityField((5, 4, 3), g["rho"], np.zeros((5, 4, 3))),
+                                 kappa=otm.ConductivityTensor(g["kappa"]), log=log, converged=False, iterations=4,
+                                 config=cfg)
+        return g, res
+
+    def test_write_outputs_bytes(self, tmp_path):
+        from paper_2405_19991_b200.io import write_outputs
+        g, res = self._result()
+        written = write_outputs(res, tmp_path, vtk=True, manifest_extra={"aborted": True, "config_file": None})
+        assert sorted(written) == sorted(["rho.otm", "kappa.txt", "log.csv", "manifest.json", "rho.vti"])
+        for name in written:
+            want = g["file_" + name.replace(".", "_")].tobytes()
+            assert (tmp_path / name).read_bytes() == want, name
+        assert not list(tmp_path.glob("*.tmp"))
+
+    def test_gallery_targets_identical(self):
+        from otm_testutil import golden
+        g = golden("io.npz")
+        for tag, diag, step in (("gallery", [0.3, 0.2, 0.1], 0.05), ("gallery2", [0.5, 0.3, 0.2], 0.04)):
+            raw, feas = enumerate_gallery_targets(diag, step)
+            assert np.array_equal(np.array(raw), g[f"{tag}_raw"])
+            assert np.array_equal(np.array(feas), g[f"{tag}_feasible"])
+
+    def test_config_precedence(self, tmp_path):
+        """defaults < --config file < explicit flags, overridden keys reported."""
+        from paper_2405_19991_b200.cli import _parser, build_run_config, merge_run_options
+        cfgf = tmp_path / "c.json"
+        cfgf.write_text(json.dumps({"reso": [8, 8, 16], "target": "0.2,0.2,x,0,0,0", "max-iter": 7,
+                                    "kappa": [1.0, 0.001], "vtk": True}))
+        args = _parser().parse_args(["run", "--config", str(cfgf), "--max-iter", "9", "--out", str(tmp_path)])
+        merged, over = merge_run_options(args)
+        assert merged["reso"] == (8, 8, 16) and merged["max_iter"] == 9 and merged["vtk"] is True
+        assert over == ["max_iter"]
+        cfg = build_run_config(merged)
+        assert cfg.material.kappa_min == 0.001 and np.isnan(cfg.target.target.vec[2])
+        bad = tmp_path / "bad.json"
+        bad.write_text(json.dumps({"resolution": 8}))
+        assert main(["run", "--config", str(bad), "--out", str(tmp_path)]) == EXIT_USAGE
