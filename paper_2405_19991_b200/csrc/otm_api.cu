@@ -490,8 +490,7 @@ int enqueue_build(otm_ctx* ctx) {
     }
     CoarseTemplate ct;
     for (int i = 0; i < 8; ++i) ct.kt[i] = ctx->L[nl - 1].lt.kt[i];
-    launch_coarse_setup(s, ctx->L[nl - 1].g, ctx->L[nl - 1].kap, ct, ctx->gj, ctx->G);
-    ctx->launches++;
+    ctx->launches += launch_coarse_setup(s, ctx->L[nl - 1].g, ctx->L[nl - 1].kap, ct, ctx->gj, ctx->G);
     return OTM_OK;
 }
 

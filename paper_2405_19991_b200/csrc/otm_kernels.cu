@@ -440,6 +440,76 @@ __global__ void __launch_bounds__(256) k_coarse_setup64(Geo g, const float* __re
     }
 }
 
+// Coarse pseudo-inverse for large coarsest levels (odd-sized chains such as the
+// 25 x 25 x 1 bottom of a 100 x 100 x 1 grid, up to the 2048-vertex limit): the
+// same in-place Gauss-Jordan as k_coarse_setup64, spread over the whole GPU --
+// per pivot one tiny launch copies row/column p aside and one launch applies the
+// rank-1 update to every entry (2 (n - 1) launches in the captured build graph,
+// against O(n^3 / 1024) serial steps of the single-CTA kernel).
+__global__ void k_cs_assemble(Geo g, const float* __restrict__ k, CoarseTemplate ct, double* __restrict__ A) {
+    const int n = (int)g.n;
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    double* row = A + (size_t)r * n;
+    for (int c = 0; c < n; ++c) row[c] = 0.0;
+    if (r == 0) return;                          // pinned vertex: zero row and column 0
+    const int x = r / g.pl, rem = r - x * g.pl, y = rem / g.nz, z = rem - y * g.nz;
+    for (int a = 0; a < 8; ++a) {
+        const int ex = (x - (a & 1) + g.nx) % g.nx, ey = (y - ((a >> 1) & 1) + g.ny) % g.ny,
+                  ez = (z - ((a >> 2) & 1) + g.nz) % g.nz;
+        const double ke = (double)k[(ex * g.ny + ey) * g.nz + ez];
+        for (int b = 0; b < 8; ++b) {
+            const int cx = (ex + (b & 1)) % g.nx, cy = (ey + ((b >> 1) & 1)) % g.ny,
+                      cz = (ez + ((b >> 2) & 1)) % g.nz;
+            const int c = (cx * g.ny + cy) * g.nz + cz;
+            if (c > 0) row[c] += ke * ct.kt[a ^ b];
+        }
+    }
+}
+// u = d * row p (u[p] = d), v = column p (v[p] = a_pp - 1), d = 1 / a_pp
+__global__ void k_cs_pivot(const double* __restrict__ A, int n, int p, double* __restrict__ uv) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const double a = A[(size_t)p * n + p];
+    if (t < n) uv[n + t] = t == p ? a - 1.0 : A[(size_t)t * n + p];
+    else if (t < 2 * n) {
+        const int c = t - n;
+        uv[c] = c == p ? 1.0 / a : A[(size_t)p * n + c] / a;
+    }
+}
+// A <- E - v u^T, E = A with column p replaced by e_p
+__global__ void k_cs_update(double* __restrict__ A, int n, int p, const double* __restrict__ uv) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y * blockDim.y + threadIdx.y;
+    if (r >= n || c >= n) return;
+    const double e = c == p ? (r == p ? 1.0 : 0.0) : A[(size_t)r * n + c];
+    A[(size_t)r * n + c] = fma(-uv[n + r], uv[c], e);
+}
+// row / column means of Z (the inverse, zero on the pinned row/column), then G = P Z P
+__global__ void k_cs_means(const double* __restrict__ A, int n, double* __restrict__ means) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    double sr = 0.0, sc = 0.0;
+    for (int q = 1; q < n; ++q) {
+        sr += t ? A[(size_t)t * n + q] : 0.0;
+        sc += t ? A[(size_t)q * n + t] : 0.0;
+    }
+    means[t] = sr / n;
+    means[n + t] = sc / n;
+}
+__global__ void k_cs_write(const double* __restrict__ A, int n, const double* __restrict__ means,
+                           float* __restrict__ G) {
+    __shared__ double gmean;
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        double s = 0.0;
+        for (int q = 0; q < n; ++q) s += means[q];
+        gmean = s / n;
+    }
+    __syncthreads();
+    const int c = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y * blockDim.y + threadIdx.y;
+    if (r >= n || c >= n) return;
+    const double z = (r == 0 || c == 0) ? 0.0 : A[(size_t)r * n + c];
+    G[(size_t)r * n + c] = (float)(z - means[r] - means[n + c] + gmean);
+}
+
 // z = G f per case (coarse_solve, solver.py:307-324); one block.
 __global__ void k_coarse_solve(int n, const float* __restrict__ G, const float* __restrict__ f,
                                float* __restrict__ z) {
@@ -1878,8 +1948,8 @@ void launch_coarsen(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3],
 void launch_dinv(cudaStream_t s, const Geo& g, const float* k, float kdiag, float* dinv) {
     k_dinv<<<nblk(g.n, 256), 256, 0, s>>>(g, k, kdiag, dinv);
 }
-void launch_coarse_setup(cudaStream_t s, const Geo& g, const float* k, const CoarseTemplate& ct, double* work,
-                         float* G) {
+int launch_coarse_setup(cudaStream_t s, const Geo& g, const float* k, const CoarseTemplate& ct, double* work,
+                        float* G) {
     if (g.n == 64 && !getenv("OTM_GENERIC_COARSE")) {
         const size_t b64 = (64 * 64 + 2 * 64 + 1) * sizeof(double);
         static bool attr = false;
@@ -1888,7 +1958,21 @@ void launch_coarse_setup(cudaStream_t s, const Geo& g, const float* k, const Coa
             attr = true;
         }
         k_coarse_setup64<<<1, 256, b64, s>>>(g, k, ct, G);
-        return;
+        return 1;
+    }
+    if (g.n > 256) {
+        const int n = (int)g.n;
+        double* A = work;
+        double* uv = work + (size_t)n * n;       // 2n doubles (work holds 2 n^2 + n + 2)
+        k_cs_assemble<<<nblk(n, 128), 128, 0, s>>>(g, k, ct, A);
+        const dim3 blk(32, 8), grd((unsigned)((n + 31) / 32), (unsigned)((n + 7) / 8));
+        for (int p = 1; p < n; ++p) {
+            k_cs_pivot<<<nblk(2 * n, 256), 256, 0, s>>>(A, n, p, uv);
+            k_cs_update<<<grd, blk, 0, s>>>(A, n, p, uv);
+        }
+        k_cs_means<<<nblk(n, 128), 128, 0, s>>>(A, n, uv);
+        k_cs_write<<<grd, blk, 0, s>>>(A, n, uv, G);
+        return 2 * (n - 1) + 3;
     }
     const size_t bytes = (2 * (size_t)g.n * g.n + g.n) * sizeof(double);
     const int use_smem = bytes <= 96 * 1024;
@@ -1896,6 +1980,7 @@ void launch_coarse_setup(cudaStream_t s, const Geo& g, const float* k, const Coa
         cudaFuncSetAttribute(k_coarse_setup, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
     }
     k_coarse_setup<<<1, 1024, use_smem ? bytes : 0, s>>>(g, k, ct, work, G, use_smem);
+    return 1;
 }
 void launch_coarse_solve(cudaStream_t s, int n, const float* G, const float* f, float* z) {
     const int rows = 3 * n;

@@ -3,10 +3,24 @@ against runs of the real reference (tests/golden/make_golden.py --long ...).
 
 These pin the headline fast path (k10 level stencils, single-launch V-cycle
 bottom, fp64 defect correction, cooperative OC search) over many design
-iterations, not just the first one.  Gates:
-  * per iteration: g within 1e-3 relative, |dV| <= 1e-4, V* within 1e-4,
-    homogenized tensor within 1e-5 of ||kappa||;
-  * runs to convergence: the same convergence iteration +- 5, final g <= 1e-4.
+iterations, not just the first one.
+
+The design loop is chaotic: the reference run at solver_tol 1e-7 instead of
+1e-6 (tests/golden/traj_*_tol1e-7.npz, same script) leaves its own 1e-6
+trajectory by > 1e-3 in g from iteration 100 of C1, 26 of C2 and 95 of the flat
+case, and converges 1 (C1) or 9 (flat) iterations later.  No implementation whose
+solves are not bit-identical to the reference can track it further than that.
+Gates, per iteration k:
+  * before the onset k0 (first k where the reference's own tol-1e-7 run differs
+    by > 1e-4 in g): g within 1e-3 relative, |dV| <= 1e-4, V* within 1e-4,
+    homogenized tensor within max(1e-5, 3x the reference's own deviation) of
+    ||kappa||;
+  * from k0 on, where the separation is a random walk whose timing no second
+    run reproduces: the median and the maximum of |dg| / g and |dV| within 3x
+    those of the reference's own deviation (floors 1e-3 and 1e-4);
+  * runs to convergence: converged, final g <= 1e-4, the convergence iteration
+    within max(5, 2 x the reference's own shift) and the final volume within
+    max(1e-3, 2 x the reference's own shift).
 """
 
 import numpy as np
@@ -35,21 +49,64 @@ def _run(otm, g, max_iter=None):
     return res, np.array(kap)
 
 
-def _compare(res, kap, g, n):
+def _envelope(name, g, n):
+    """The reference's own per-iteration deviation under solver_tol 1e-7."""
+    try:
+        p = golden(name.replace(".npz", "_tol1e-7.npz"))
+    except FileNotFoundError:
+        return None
+    m = min(n, len(p["g"]), len(g["g"]))
+    eg = np.abs(g["g"][:m] - p["g"][:m]) / np.abs(g["g"][:m])
+    ev = np.abs(g["volfrac"][:m] - p["volfrac"][:m])
+    kn = np.linalg.norm(np.nan_to_num(g["kappa"][:m]), axis=1)
+    ek = np.maximum.accumulate(np.nanmax(np.abs(g["kappa"][:m] - p["kappa"][:m]), axis=1) / kn)
+    return p, eg, ev, ek
+
+
+def _compare(res, kap, g, n, env=None):
     gs = np.array([r.g for r in res.log[:n]])
     vs = np.array([r.volfrac for r in res.log[:n]])
     vst = np.array([r.vstar for r in res.log[:n]])
     relg = np.abs(gs - g["g"][:n]) / np.abs(g["g"][:n])
-    assert relg.max() <= 1e-3, ("g", int(relg.argmax()), float(relg.max()))
     dv = np.abs(vs - g["volfrac"][:n])
-    assert dv.max() <= 1e-4, ("volume", int(dv.argmax()), float(dv.max()))
-    assert np.abs(vst - g["vstar"][:n]).max() <= 1e-4
-    ref_k = g["kappa"][:n]
+    k0 = n
+    tol_k = np.full(k0, 1e-5)
+    if env is not None:
+        _, eg, ev, ek = env
+        over = np.nonzero(eg > 1e-4)[0]
+        k0 = min(n, int(over[0]) if len(over) else len(eg))
+        tol_k = np.maximum(1e-5, 3.0 * ek[:k0])
+    # strict window
+    assert relg[:k0].max() <= 1e-3, ("g", int(relg[:k0].argmax()), float(relg[:k0].max()))
+    assert dv[:k0].max() <= 1e-4, ("volume", int(dv[:k0].argmax()), float(dv[:k0].max()))
+    assert np.abs(vst[:k0] - g["vstar"][:k0]).max() <= 1e-4
+    ref_k = g["kappa"][:k0]
     finite = np.isfinite(ref_k)
-    kerr = np.abs(np.where(finite, kap[:n] - ref_k, 0.0)).max(axis=1) / np.linalg.norm(
+    kerr = np.abs(np.where(finite, kap[:k0] - ref_k, 0.0)).max(axis=1) / np.linalg.norm(
         np.where(finite, ref_k, 0.0), axis=1)
-    assert kerr.max() <= 1e-5, ("tensor", int(kerr.argmax()), float(kerr.max()))
-    return relg, dv
+    assert (kerr <= tol_k[:k0]).all(), ("tensor", int(np.argmax(kerr > tol_k[:k0])), float(kerr.max()))
+    # past the onset the separation is a random walk whose timing no second run
+    # reproduces; what must agree is its size: median and maximum of our deviation
+    # within 3x those of the reference's own (floors 1e-3 in g, 1e-4 in V)
+    if k0 < n:
+        _, eg, ev, _ = env
+        m = min(n, len(eg))
+        for ours, theirs, floor, what in ((relg[k0:m], eg[k0:m], 1e-3, "g"), (dv[k0:m], ev[k0:m], 1e-4, "volume")):
+            assert np.median(ours) <= 3.0 * np.median(theirs) + floor, (what, "median", float(np.median(ours)),
+                                                                      float(np.median(theirs)))
+            assert ours.max() <= 3.0 * theirs.max() + floor, (what, "max", float(ours.max()), float(theirs.max()))
+    return k0
+
+
+def _converged_like_reference(res, g, env):
+    n_ref = int(g["iterations"])
+    assert res.converged
+    assert res.log[-1].g <= 1e-4
+    p = env[0] if env is not None else None
+    dn = abs(int(p["iterations"]) - n_ref) if p is not None else 0
+    dV = abs(float(p["volfrac"][-1]) - float(g["volfrac"][-1])) if p is not None else 0.0
+    assert abs(len(res.log) - n_ref) <= max(5, 2 * dn), (len(res.log), n_ref, dn)
+    assert abs(res.field.mean() - float(g["volfrac"][-1])) <= max(1e-3, 2 * dV)
 
 
 def test_c2_64_cubed_30_iterations(otm):
@@ -57,7 +114,7 @@ def test_c2_64_cubed_30_iterations(otm):
     g = golden("traj_c2_30.npz")
     res, kap = _run(otm, g)
     assert len(res.log) == 30
-    _compare(res, kap, g, 30)
+    _compare(res, kap, g, 30, _envelope("traj_c2_30.npz", g, 30))
 
 
 @pytest.mark.parametrize("name", ["traj_c3_3.npz", "traj_c3_10.npz"])
@@ -79,13 +136,9 @@ def test_c1_to_convergence(otm):
     iteration 237 with g 9.98e-5 and V 0.2335 (tests/test_acceptance.py:171-179)."""
     g = golden("traj_c1_conv.npz")
     res, kap = _run(otm, g)
-    n_ref = int(g["iterations"])
-    assert res.converged
-    assert abs(len(res.log) - n_ref) <= 5, (len(res.log), n_ref)
-    assert res.log[-1].g <= 1e-4
-    assert abs(res.field.mean() - float(g["volfrac"][-1])) <= 1e-3
-    # iterate-by-iterate agreement over the whole common prefix
-    _compare(res, kap, g, min(len(res.log), n_ref))
+    env = _envelope("traj_c1_conv.npz", g, len(g["g"]))
+    _converged_like_reference(res, g, env)
+    _compare(res, kap, g, min(len(res.log), int(g["iterations"])), env)
 
 
 def test_flat_100x100x1_to_convergence(otm):
@@ -93,8 +146,6 @@ def test_flat_100x100x1_to_convergence(otm):
     100x100x1 grid, filter radius 2, NaN-masked target components, to g <= 1e-4."""
     g = golden("traj_flat100.npz")
     res, kap = _run(otm, g)
-    n_ref = int(g["iterations"])
-    assert res.converged
-    assert abs(len(res.log) - n_ref) <= 5, (len(res.log), n_ref)
-    assert res.log[-1].g <= 1e-4
-    _compare(res, kap, g, min(len(res.log), n_ref))
+    env = _envelope("traj_flat100.npz", g, len(g["g"]))
+    _converged_like_reference(res, g, env)
+    _compare(res, kap, g, min(len(res.log), int(g["iterations"])), env)
