@@ -226,6 +226,11 @@ int otm_profile_read(otm_ctx* ctx, int cls, double* ms_total, long long* launche
                      double* bytes);
 int otm_profile_reset(otm_ctx* ctx);
 long long otm_launch_count(const otm_ctx* ctx);
+/* Solver / OC counters since creation or the last reset: solves, fp64 refinement
+ * steps, inner PCG iterations (one V-cycle per active case each), OC updates, OC
+ * multiplier passes, frozen-state retries. */
+int otm_stats(const otm_ctx* ctx, long long out[6]);
+int otm_stats_reset(otm_ctx* ctx);
 
 #ifdef __cplusplus
 }

@@ -1142,6 +1142,24 @@ int otm_coarse_solve(otm_ctx* ctx, const double* f, double* T) {
     return OTM_OK;
 }
 
+int otm_stats(const otm_ctx* ctx, long long out[6]) {
+    if (!ctx || !out) return OTM_EINVAL;
+    out[0] = ctx->stat_solves;
+    out[1] = ctx->stat_outer;
+    out[2] = ctx->stat_inner;
+    out[3] = ctx->stat_oc;
+    out[4] = ctx->stat_oc_passes;
+    out[5] = ctx->stat_oc_retry;
+    return OTM_OK;
+}
+
+int otm_stats_reset(otm_ctx* ctx) {
+    if (!ctx) return OTM_EINVAL;
+    ctx->stat_solves = ctx->stat_outer = ctx->stat_inner = 0;
+    ctx->stat_oc = ctx->stat_oc_passes = ctx->stat_oc_retry = 0;
+    return OTM_OK;
+}
+
 int otm_residual_history(const otm_ctx* ctx, double* out, int cap) {
     if (!ctx) return -1;
     const int n = (int)ctx->hist_rel.size();

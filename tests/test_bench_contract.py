@@ -15,7 +15,7 @@ KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "
 def test_reference_arm_json_line():
     env = dict(os.environ, PYTHONDONTWRITEBYTECODE="1")
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "c1",
-                          "--steps", "1", "--warmup", "0", "--iters", "1"],
+                          "--steps", "1", "--warmup", "0", "--iters", "1", "--no-c1"],
                          capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
@@ -30,7 +30,7 @@ def test_reference_arm_json_line():
 def test_reference_arm_non_zero_rank_is_silent():
     env = dict(os.environ, PYTHONDONTWRITEBYTECODE="1", RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "c1",
-                          "--steps", "1", "--warmup", "0", "--iters", "1"],
+                          "--steps", "1", "--warmup", "0", "--iters", "1", "--no-c1"],
                          capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     assert out.returncode == 0
     assert not [l for l in out.stdout.splitlines() if l.startswith("{")]

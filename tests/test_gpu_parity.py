@@ -307,7 +307,7 @@ def test_central_symmetry_every_iteration(otm):
     seen = []
     cfg = otm.RunConfig(dims=(8, 8, 8), target=target, symmetry="central",
                         init=otm.InitPattern("random", 0.5, seed=1), max_iter=6)
-    otm.run_optimization(cfg, callback=lambda it, fld, r, g: seen.append(fld.rho.cpu().numpy().copy()))
+    otm.run_optimization(cfg, callback=lambda it, fld, r, g: seen.append(fld.rho.copy()))
     assert len(seen) >= 4
     for rho in seen:
         assert np.array_equal(rho, rho[::-1, ::-1, ::-1])
