@@ -282,8 +282,13 @@ def run_gpu(args):
     def one_structure():
         cfg = make_config(otm, name, args.iters, 0.0, init_field=seed_dev)
         run = DesignRun(cfg, hier=hier)
-        while not run.finished:
-            rc, _ = run.step()
+        if args.host_loop:
+            while not run.finished:
+                rc, _ = run.step()
+                if rc != _lib.OTM_OK:
+                    ctx.check(rc)
+        else:
+            rc = run.run()                   # device-resident iterations (host path while profiling)
             if rc != _lib.OTM_OK:
                 ctx.check(rc)
         return run
@@ -533,6 +538,8 @@ def main():
     ap.add_argument("--iters", type=int, default=500, help="OC iterations per structure")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-c1", action="store_true", help="skip the C1 to-convergence legs")
+    ap.add_argument("--host-loop", action="store_true",
+                    help="drive the design loop from the host (otm_run_step/update) instead of the iteration graph")
     ap.add_argument("--no-prof", action="store_true", help="no in-region kernel events")
     ap.add_argument("--no-beyond-l2", dest="beyond_l2", action="store_false",
                     help="skip the 256³ level-0 stencil roofline leg")

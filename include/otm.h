@@ -217,6 +217,20 @@ int otm_run_step(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st,
  * frozen-state retry) and the optional symmetry projection, rho_dev in place. */
 int otm_run_update(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, double* rho_dev);
 
+/* Up to max_iters iterations of the design loop (optimize.py:288-379), each ONE
+ * launch of a captured graph that keeps every decision on the device: the solve's
+ * stopping rule and per-case budgets, the objective, the log record, the convergence
+ * rule, the volume governor and the OC search (nested conditional WHILE / IF nodes;
+ * otm_loop.cu).  The host synchronises once per `batch` iterations to collect the
+ * records; iterations launched after the run finished are no-ops.  st is read at
+ * entry and written back at exit (the same state otm_run_step / otm_run_update
+ * advance, bit-identical results).  records receive *n_out entries.  Returns
+ * OTM_ENOCONV when a solve fails (the records hold the iterations before it) and
+ * OTM_ESTATE when the graph path is unavailable (profiling, no cooperative launch):
+ * the caller then drives the same loop with otm_run_step / otm_run_update. */
+int otm_run_batch(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, double* rho_dev,
+                  int max_iters, int batch, otm_iter_record* records, int* n_out);
+
 /* ---- instrumentation (bench.py) ------------------------------------------- */
 /* Per-kernel-class device time accumulated with CUDA events on the context stream
  * while enabled.  Classes: 0 level-0 stencil (K.p / smoother / residual), 1 V-cycle

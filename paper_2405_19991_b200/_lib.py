@@ -99,6 +99,8 @@ _SIGS = {
     "otm_run_step": (C.c_int, [C.c_void_p, C.POINTER(RunConfigC), C.POINTER(RunStateC), dptr, dptr, dptr,
                                C.POINTER(IterRecordC)]),
     "otm_run_update": (C.c_int, [C.c_void_p, C.POINTER(RunConfigC), C.POINTER(RunStateC), dptr]),
+    "otm_run_batch": (C.c_int, [C.c_void_p, C.POINTER(RunConfigC), C.POINTER(RunStateC), dptr, C.c_int, C.c_int,
+                                C.POINTER(IterRecordC), C.POINTER(C.c_int)]),
     "otm_profile_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "otm_profile_read": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_longlong),
                                    C.POINTER(C.c_double)]),

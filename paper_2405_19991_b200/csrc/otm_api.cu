@@ -23,6 +23,7 @@
 
 #include "../../include/otm.h"
 #include "otm_internal.h"
+#include "otm_loopctl.cuh"
 
 using namespace otm;
 
@@ -125,6 +126,15 @@ struct otm_ctx {
     long long prof_n[kProfClasses] = {0};
     double prof_bytes[kProfClasses] = {0};
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;   // ad-hoc single-kernel timing
+    // device-resident design iteration (otm_run_batch): one graph per (config, density buffer)
+    LoopState* lstate = nullptr;          // device
+    LoopState* h_lstate = nullptr;        // pinned mirror
+    cudaGraphExec_t gexec_iter = nullptr;
+    LoopCfg iter_cfg{};
+    const double* iter_rho = nullptr;
+    bool no_iter_graph = getenv("OTM_NO_ITER_GRAPH") != nullptr;
+    cudaStream_t cap[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev_cf = nullptr, ev_cj = nullptr;
 };
 
 namespace {
@@ -729,6 +739,12 @@ int otm_destroy(otm_ctx* ctx) {
     if (ctx->gexec_prof) cudaGraphExecDestroy(ctx->gexec_prof);
     if (ctx->gexec_loop) cudaGraphExecDestroy(ctx->gexec_loop);
     if (ctx->gexec_build) cudaGraphExecDestroy(ctx->gexec_build);
+    if (ctx->gexec_iter) cudaGraphExecDestroy(ctx->gexec_iter);
+    for (auto& cs : ctx->cap) if (cs) cudaStreamDestroy(cs);
+    if (ctx->ev_cf) cudaEventDestroy(ctx->ev_cf);
+    if (ctx->ev_cj) cudaEventDestroy(ctx->ev_cj);
+    if (ctx->h_lstate) cudaFreeHost(ctx->h_lstate);
+    if (ctx->lstate) cudaFree(ctx->lstate);
     for (auto& s : ctx->slots) { cudaEventDestroy(s.a); cudaEventDestroy(s.b); }
     auto F = [](void* p) { if (p) cudaFree(p); };
     F(ctx->kap64); F(ctx->T64); F(ctx->rho_f); F(ctx->sensf); F(ctx->sens); F(ctx->r); F(ctx->p); F(ctx->q); F(ctx->d);
@@ -1169,14 +1185,17 @@ int otm_residual_history(const otm_ctx* ctx, double* out, int cap) {
 
 int otm_get_T(otm_ctx* ctx, double* T) {
     if (!ctx || !T) return OTM_EINVAL;
-    if (ctx->T_center_pending) {
-        launch_sum3(ctx->stream, ctx->g0.n, ctx->T64, ctx->red, ctx->scal + 100);      // means
-        launch_submean_means(ctx->stream, ctx->g0.n, ctx->T64, ctx->scal + 100);
-        ctx->launches += 2;
-        ctx->T_center_pending = false;
-    }
+    // mean-free fields (solver.py:398).  The context's own copy stays as the solve left
+    // it unless it is the destination: re-centring it would perturb the next warm start
+    // by a rounding-level shift, so reading T (e.g. for a callback) must not change the run
     if (T != ctx->T64)
         CK(cudaMemcpyAsync(T, ctx->T64, 3 * ctx->g0.n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    if (ctx->T_center_pending || T != ctx->T64) {
+        launch_sum3(ctx->stream, ctx->g0.n, T, ctx->red, ctx->scal + 100);      // means
+        launch_submean_means(ctx->stream, ctx->g0.n, T, ctx->scal + 100);
+        ctx->launches += 2;
+        if (T == ctx->T64) ctx->T_center_pending = false;
+    }
     return OTM_OK;
 }
 
@@ -1220,32 +1239,7 @@ int otm_sensitivity(otm_ctx* ctx, const double dG[6], double* sens) {
 
 // objective.py:48-72
 int otm_objective(int kind, const double t[6], const double k[6], double* g_out, double dG[6]) {
-    double g = 0.0;
-    int any = 0;
-    for (int c = 0; c < 6; ++c) {
-        if (!std::isfinite(k[c])) return OTM_EINVAL;
-        if (!std::isnan(t[c])) any = 1;
-    }
-    if (!any) return OTM_EINVAL;
-    for (int c = 0; c < 6; ++c) {
-        const bool m = !std::isnan(t[c]);
-        if (kind == 0) {
-            const double d = m ? k[c] - t[c] : 0.0;
-            g += d * d;
-            dG[c] = 2.0 * d;
-        } else if (kind == 1) {
-            const double tt = m ? t[c] : 1.0;
-            const double d = m ? k[c] / tt - 1.0 : 0.0;
-            g += d * d;
-            dG[c] = m ? 2.0 * d / tt : 0.0;
-        } else {
-            const double d = m ? k[c] - t[c] : 0.0;
-            g += std::fabs(d);
-            dG[c] = (d > 0) - (d < 0);
-        }
-    }
-    *g_out = g;
-    return OTM_OK;
+    return objective_eval(kind, t, k, g_out, dG) ? OTM_OK : OTM_EINVAL;    // otm_loopctl.cuh
 }
 
 int otm_means(otm_ctx* ctx, const double* rho, double p, double out[2]) {
@@ -1439,24 +1433,17 @@ int otm_oc_update(otm_ctx* ctx, const double* rho, const double* sens, double V,
 
 // governor_update (optimize.py:57-86)
 double otm_governor_update(otm_governor* st, double g, double mean_rho, double mean_rho_p) {
-    if (g <= st->bound) {
-        st->gap = st->vstar - mean_rho_p;
-        st->vstar = st->vstar - st->gap * st->df;
-        st->df = 0.8 * st->df;
-        st->reduced = 1;
-    }
-    const bool little = std::fabs(st->g_prev - g) < std::max(0.1 * g, 1e-7);
-    const bool too_big = g > st->bound;
-    const bool near = mean_rho > st->vstar - 0.01;
-    if (little && too_big && near) st->count += 1;
-    else st->count = 0;
-    if (st->count >= 5) {
-        st->vstar = st->vstar + 0.3 * st->gap * st->df;
-        st->count = 0;
-    }
-    st->g_prev = g;
-    st->iter += 1;
-    return st->vstar;
+    GovCtl c{st->vstar, st->df, st->gap, st->count, st->bound, st->iter, st->g_prev, st->reduced};
+    const double v = governor_step(&c, g, mean_rho, mean_rho_p);                 // otm_loopctl.cuh
+    st->vstar = c.vstar;
+    st->df = c.df;
+    st->gap = c.gap;
+    st->count = c.count;
+    st->bound = c.bound;
+    st->iter = c.iter;
+    st->g_prev = c.g_prev;
+    st->reduced = c.reduced;
+    return v;
 }
 
 void otm_run_init(otm_run_state* st, const otm_run_config* cfg) {
@@ -1532,20 +1519,10 @@ int otm_run_step(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, dou
     for (int c = 0; c < 3; ++c) rec->solve_residual[c] = resid[c];
     st->iter = it;
     // convergence (optimize.py:327-345)
-    if (st->have_g_last && std::fabs(g - st->g_last) < cfg->conv_threshold) st->plateau += 1;
-    else st->plateau = 0;
-    st->g_last = g;
-    st->have_g_last = 1;
-    bool converged = false;
-    if (g <= 1e-12) converged = true;
-    else if (st->plateau >= 3) {
-        if (cfg->model == 0) {
-            const double cd = st->gov.reduced ? st->gov.gap * st->gov.df : INFINITY;
-            converged = cd < 1e-4 && g <= st->gov.bound;
-        } else {
-            converged = true;
-        }
-    }
+    const GovCtl gv{st->gov.vstar, st->gov.df, st->gov.gap, st->gov.count, st->gov.bound, st->gov.iter,
+                    st->gov.g_prev, st->gov.reduced};
+    const bool converged = convergence_step(cfg->model, cfg->conv_threshold, gv, g, &st->plateau, &st->have_g_last,
+                                            &st->g_last);
     st->converged = converged ? 1 : 0;
     st->g = g;
     st->mean_rho = mean_rho;
@@ -1563,10 +1540,10 @@ int otm_run_update(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, d
     const double mean_rho = st->mean_rho;
     if (cfg->model == 0 && !ctx->no_coop) {
         // governor + OC step + frozen-state retry in one cooperative launch
-        double vb = otm_governor_update(&st->gov, st->g, mean_rho, st->mean_rho_p);
-        vb = std::min(vb, mean_rho + 0.5 * cfg->oc.step_limit);
-        rc = oc_search_coop(ctx, rho, ctx->sens, vb, mean_rho - 0.25 * cfg->oc.step_limit, &cfg->oc, rho, nullptr,
-                            nullptr, nullptr, nullptr, false);
+        double vb, vretry;
+        oc_bounds(otm_governor_update(&st->gov, st->g, mean_rho, st->mean_rho_p), mean_rho, cfg->oc.step_limit, &vb,
+                  &vretry);
+        rc = oc_search_coop(ctx, rho, ctx->sens, vb, vretry, &cfg->oc, rho, nullptr, nullptr, nullptr, nullptr, false);
         if (rc == OTM_OK) {
             if (cfg->symmetry == 1) {
                 launch_symmetrize(ctx->stream, ctx->g0, rho);
@@ -1580,18 +1557,17 @@ int otm_run_update(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, d
         rc = otm_oc_update(ctx, rho, ctx->sens, vb, &cfg->oc, rho, &lam, &active, &changed);
         if (rc) return rc;
         if (!changed) {
-            rc = otm_oc_update(ctx, rho, ctx->sens, mean_rho - 0.25 * cfg->oc.step_limit, &cfg->oc, rho, &lam,
-                               &active, &changed);
+            rc = otm_oc_update(ctx, rho, ctx->sens, vretry, &cfg->oc, rho, &lam, &active, &changed);
             if (rc) return rc;
         }
     } else if (cfg->model == 0) {
-        double vb = otm_governor_update(&st->gov, st->g, mean_rho, st->mean_rho_p);
-        vb = std::min(vb, mean_rho + 0.5 * cfg->oc.step_limit);
+        double vb, vretry;
+        oc_bounds(otm_governor_update(&st->gov, st->g, mean_rho, st->mean_rho_p), mean_rho, cfg->oc.step_limit, &vb,
+                  &vretry);
         rc = otm_oc_update(ctx, rho, ctx->sens, vb, &cfg->oc, rho, &lam, &active, &changed);
         if (rc) return rc;
         if (!changed) {
-            rc = otm_oc_update(ctx, rho, ctx->sens, mean_rho - 0.25 * cfg->oc.step_limit, &cfg->oc, rho, &lam,
-                               &active, &changed);
+            rc = otm_oc_update(ctx, rho, ctx->sens, vretry, &cfg->oc, rho, &lam, &active, &changed);
             if (rc) return rc;
         }
     } else {
@@ -1603,6 +1579,309 @@ int otm_run_update(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, d
         ctx->launches++;
     }
     CKL();
+    return OTM_OK;
+}
+
+// ---- device-resident design iteration (otm_run_batch) --------------------------
+
+static LoopCfg loop_cfg(const otm_ctx* ctx, const otm_run_config* cfg) {
+    LoopCfg C;
+    std::memset(&C, 0, sizeof C);
+    for (int c = 0; c < 6; ++c) C.target[c] = cfg->target[c];
+    C.objective = cfg->objective;
+    C.model = cfg->model;
+    C.volume_bound = cfg->volume_bound;
+    C.oc_min_density = cfg->oc.min_density;
+    C.oc_step = cfg->oc.step_limit;
+    C.oc_damp = cfg->oc.damp;
+    C.oc_bis_tol = cfg->oc.bisection_tol;
+    C.max_iter = cfg->max_iter;
+    C.conv_threshold = cfg->conv_threshold;
+    C.symmetry = cfg->symmetry;
+    C.solver_tol = cfg->solver_tol;
+    C.max_vcycles = cfg->max_vcycles;
+    C.governor_bound = cfg->governor_bound;
+    C.inner_reduction = ctx->P.inner_reduction;
+    static const double tolf = getenv("OTM_TOLF") ? atof(getenv("OTM_TOLF")) : 0.85;
+    C.tolf = tolf;
+    C.max_inner = ctx->P.max_inner;
+    return C;
+}
+
+// add a conditional node at the current capture position of stream s (its handle
+// created beforehand in the graph being captured); returns the body graph
+static cudaError_t cond_handle(cudaStream_t s, unsigned dflt, cudaGraphConditionalHandle* h) {
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t g;
+    cudaError_t e = cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, nullptr, nullptr);
+    if (e != cudaSuccess) return e;
+    return cudaGraphConditionalHandleCreate(h, g, dflt, cudaGraphCondAssignDefault);
+}
+static cudaError_t cond_node(cudaStream_t s, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type,
+                             cudaGraph_t* body) {
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t g;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    cudaError_t e = cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &nd);
+    if (e != cudaSuccess) return e;
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = type;
+    p.conditional.size = 1;
+    cudaGraphNode_t node;
+    e = cudaGraphAddNode(&node, g, deps, nd, &p);
+    if (e != cudaSuccess) return e;
+    *body = p.conditional.phGraph_out[0];
+    return cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies);
+}
+
+// One design iteration as a graph (see otm_loop.cu for the structure).
+static int capture_iteration(otm_ctx* ctx, const LoopCfg& C, double* rho) {
+    const long long n = ctx->g0.n;
+    for (auto& cs : ctx->cap)
+        if (!cs) CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    if (!ctx->ev_cf) CK(cudaEventCreateWithFlags(&ctx->ev_cf, cudaEventDisableTiming));
+    if (!ctx->ev_cj) CK(cudaEventCreateWithFlags(&ctx->ev_cj, cudaEventDisableTiming));
+    if (!ctx->lstate) {
+        CK(dalloc(ctx, &ctx->lstate, 1));
+        CK(cudaMallocHost((void**)&ctx->h_lstate, sizeof(LoopState)));
+    }
+    const cudaStreamCaptureMode mode = cudaStreamCaptureModeThreadLocal;
+    cudaStream_t s0 = ctx->cap[0], s1 = ctx->cap[1], s2 = ctx->cap[2], s3 = ctx->cap[3], sb = ctx->cap[4];
+    cudaStream_t saved = ctx->stream;
+    LoopState* S = ctx->lstate;
+    OcArgs a;
+    a.step = C.oc_step;
+    a.rmin = C.oc_min_density;
+    a.damp = C.oc_damp;
+    a.floor_ratio = std::pow(1e-10, C.oc_damp);
+    a.sqrt_damp = C.oc_damp == 0.5;
+    cudaGraph_t G, g_tmp, body_if, body_out, body_in, body_upd;
+    cudaGraphConditionalHandle h_body, h_out, h_in, h_upd;
+    int rc = OTM_OK;
+    const long long launches_at_capture = ctx->launches;     // capturing launches nothing
+    auto fail_capture = [&](const char* what, cudaError_t e) {
+        ctx->stream = saved;
+        ctx->loop_handle = 0;
+        for (auto& cs : ctx->cap) {
+            cudaStreamCaptureStatus st;
+            if (cudaStreamIsCapturing(cs, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone) {
+                cudaGraph_t junk;
+                cudaStreamEndCapture(cs, &junk);
+                if (junk) cudaGraphDestroy(junk);
+            }
+        }
+        cudaGetLastError();
+        return fail(ctx, OTM_ECUDA, std::string("iteration graph: ") + what + ": " + cudaGetErrorString(e));
+    };
+#define CKC(call, what)                                \
+    do {                                               \
+        cudaError_t e_ = (call);                       \
+        if (e_ != cudaSuccess) return fail_capture(what, e_); \
+    } while (0)
+    CKC(cudaGraphCreate(&G, 0), "create");
+    // top level: k_iter_begin -> IF(not finished) { body }
+    CKC(cudaStreamBeginCaptureToGraph(s0, G, nullptr, nullptr, 0, mode), "capture top");
+    CKC(cond_handle(s0, 0, &h_body), "handle body");
+    launch_iter_begin(s0, S, (unsigned long long)h_body);
+    CKC(cond_node(s0, h_body, cudaGraphCondTypeIf, &body_if), "IF body");
+    CKC(cudaStreamEndCapture(s0, &g_tmp), "end top");
+    // the iteration
+    CKC(cudaStreamBeginCaptureToGraph(s1, body_if, nullptr, nullptr, 0, mode), "capture body");
+    ctx->stream = s1;
+    launch_filter_simp(s1, ctx->g0, ctx->fs, ctx->sp, rho, ctx->rho_f, ctx->kap64, ctx->L[0].kap, ctx->red,
+                       ctx->scal + 56);
+    // hierarchy build on a side branch, joined before the first V-cycle
+    CKC(cudaEventRecord(ctx->ev_cf, s1), "fork");
+    CKC(cudaStreamWaitEvent(sb, ctx->ev_cf, 0), "fork wait");
+    ctx->stream = sb;
+    const long long lb = ctx->launches;
+    rc = enqueue_build(ctx);
+    if (rc) return fail_capture("build", cudaGetLastError());
+    ctx->build_launches = ctx->launches - lb;
+    CKC(cudaEventRecord(ctx->ev_cj, sb), "join");
+    ctx->stream = s1;
+    double* fmean = ctx->scal + 16;
+    launch_load_means(s1, ctx->g0, ctx->L[0].lt, ctx->kap64, ctx->red, fmean);
+    launch_T_cold(s1, S, 3 * n, ctx->T64);
+    launch_res64(s1, ctx->g0, ctx->L[0].lt, ctx->kap64, ctx->T64, nullptr, fmean, ctx->r, ctx->red, ctx->scal);
+    CKC(cudaStreamWaitEvent(s1, ctx->ev_cj, 0), "join wait");
+    // solve: WHILE(not converged) { control ; WHILE(PCG) {...} ; T += d ; defect }
+    CKC(cond_handle(s1, 1, &h_out), "handle outer");
+    CKC(cond_handle(s1, 0, &h_upd), "handle update");
+    CKC(cond_node(s1, h_out, cudaGraphCondTypeWhile, &body_out), "WHILE outer");
+    CKC(cudaStreamBeginCaptureToGraph(s2, body_out, nullptr, nullptr, 0, mode), "capture outer");
+    CKC(cond_handle(s2, 0, &h_in), "handle inner");
+    launch_solve_ctl(s2, S, C, ctx->scal, ctx->sc, (unsigned long long)h_out, (unsigned long long)h_in);
+    CKC(cudaMemsetAsync(ctx->d, 0, 3 * n * sizeof(float), s2), "memset d");
+    CKC(cudaMemsetAsync(ctx->p, 0, 3 * n * sizeof(float), s2), "memset p");
+    CKC(cond_node(s2, h_in, cudaGraphCondTypeWhile, &body_in), "WHILE inner");
+    CKC(cudaStreamBeginCaptureToGraph(s3, body_in, nullptr, nullptr, 0, mode), "capture inner");
+    ctx->stream = s3;
+    ctx->loop_handle = (unsigned long long)h_in;
+    rc = enqueue_inner(ctx, false, true);
+    ctx->loop_handle = 0;
+    if (rc) return fail_capture("inner", cudaGetLastError());
+    CKC(cudaStreamEndCapture(s3, &g_tmp), "end inner");
+    ctx->stream = s2;
+    launch_Tupd(s2, n, ctx->T64, ctx->d, ctx->p, ctx->sc);
+    launch_res64(s2, ctx->g0, ctx->L[0].lt, ctx->kap64, ctx->T64, nullptr, fmean, ctx->r, ctx->red, ctx->scal,
+                 &ctx->sc->skip);
+    CKC(cudaStreamEndCapture(s2, &g_tmp), "end outer");
+    ctx->stream = s1;
+    launch_solve_fin(s1, S, n, ctx->T64);
+    launch_tensor(s1, ctx->g0, ctx->T64, ctx->kap64, ctx->red, ctx->scal + 32);
+    launch_design_eval(s1, S, C, ctx->scal + 32, ctx->scal + 56, n, ctx->ocl, (unsigned long long)h_upd);
+    launch_sens(s1, ctx->g0, ctx->T64, ctx->rho_f, ctx->sp, Dg{}, ctx->sensf, &S->dG);
+    launch_filter(s1, ctx->g0, ctx->fs, 1, ctx->sensf, ctx->sens, ctx->red);
+    if (C.symmetry == 1) launch_symmetrize(s1, ctx->g0, ctx->sens);
+    // IF(not finished) { governor-bounded OC search + update }
+    CKC(cond_node(s1, h_upd, cudaGraphCondTypeIf, &body_upd), "IF update");
+    CKC(cudaStreamBeginCaptureToGraph(s2, body_upd, nullptr, nullptr, 0, mode), "capture update");
+    if (launch_oc_coop(s2, n, rho, ctx->sens, a, rho, ctx->ocl, ctx->red.partials))
+        return fail_capture("cooperative OC launch", cudaGetLastError());
+    if (C.symmetry == 1) launch_symmetrize(s2, ctx->g0, rho);
+    launch_oc_account(s2, S, ctx->ocl);
+    CKC(cudaStreamEndCapture(s2, &g_tmp), "end update");
+    CKC(cudaStreamEndCapture(s1, &g_tmp), "end body");
+#undef CKC
+    ctx->stream = saved;
+    ctx->launches = launches_at_capture;
+    cudaGraphExec_t ex;
+    cudaError_t e = cudaGraphInstantiate(&ex, G, 0);
+    cudaGraphDestroy(G);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ctx, OTM_ECUDA, std::string("iteration graph instantiate: ") + cudaGetErrorString(e));
+    }
+    if (ctx->gexec_iter) cudaGraphExecDestroy(ctx->gexec_iter);
+    ctx->gexec_iter = ex;
+    ctx->iter_cfg = C;
+    ctx->iter_rho = rho;
+    return OTM_OK;
+}
+
+int otm_run_batch(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, double* rho, int max_iters,
+                  int batch, otm_iter_record* recs, int* n_out) {
+    if (!ctx || !cfg || !st || !rho || !recs || !n_out || max_iters < 1) return OTM_EINVAL;
+    *n_out = 0;
+    if (st->finished) return fail(ctx, OTM_ESTATE, "run already finished");
+    if (ctx->no_iter_graph || ctx->prof || ctx->no_coop || cfg->model == 1)
+        return fail(ctx, OTM_ESTATE, "iteration graph unavailable");
+    cudaStream_t s = ctx->stream;
+    const LoopCfg C = loop_cfg(ctx, cfg);
+    if (!ctx->gexec_iter || ctx->iter_rho != rho || std::memcmp(&C, &ctx->iter_cfg, sizeof C) != 0) {
+        join_build(ctx);
+        CK(cudaStreamSynchronize(s));
+        int rc = capture_iteration(ctx, C, rho);
+        if (rc) {
+            ctx->no_iter_graph = true;           // this context stays on the host-driven path
+            return OTM_ESTATE;
+        }
+    }
+    join_build(ctx);
+    oc_settle(ctx);
+    // upload the run state
+    LoopState* H = ctx->h_lstate;
+    std::memset(H, 0, offsetof(LoopState, rec));
+    H->gov.vstar = st->gov.vstar;
+    H->gov.df = st->gov.df;
+    H->gov.gap = st->gov.gap;
+    H->gov.count = st->gov.count;
+    H->gov.bound = st->gov.bound;
+    H->gov.iter = st->gov.iter;
+    H->gov.g_prev = st->gov.g_prev;
+    H->gov.reduced = st->gov.reduced;
+    H->iter = st->iter;
+    H->plateau = st->plateau;
+    H->have_g_last = st->have_g_last;
+    H->g_last = st->g_last;
+    H->converged = st->converged;
+    H->finished = 0;
+    H->warm = st->warm;
+    H->g = st->g;
+    H->mean_rho = st->mean_rho;
+    H->mean_rho_p = st->mean_rho_p;
+    CK(cudaMemcpyAsync(ctx->lstate, H, offsetof(LoopState, rec), cudaMemcpyHostToDevice, s));
+    int done = 0, status = 0;
+    const int first_iter = st->iter;
+    bool finished = false;
+    while (done < max_iters && !finished) {
+        const int m = std::min(std::min(std::max(batch, 1), max_iters - done), kLoopRing);
+        for (int k = 0; k < m; ++k) CK(cudaGraphLaunch(ctx->gexec_iter, s));
+        CK(cudaMemcpyAsync(H, ctx->lstate, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
+        CK(stream_wait(s));
+        // records of this batch: iterations first_iter + done + 1 .. H->iter (+1 on failure)
+        const int last = H->status ? H->iter + 1 : H->iter;
+        for (int it = first_iter + done + 1; it <= last; ++it) {
+            const LoopRecord& R = H->rec[(it - 1) % kLoopRing];
+            if (R.status) {
+                status = R.status;
+                break;
+            }
+            otm_iter_record& o = recs[done];
+            o.iter = R.iter;
+            o.g = R.g;
+            o.volfrac = R.volfrac;
+            o.volfrac_filtered = R.volfrac_filtered;
+            o.vstar = R.vstar;
+            o.vcycles = R.vcycles;
+            o.ms = R.ms;
+            for (int c = 0; c < 6; ++c) o.kappa[c] = R.kappa[c];
+            for (int c = 0; c < 3; ++c) o.solve_residual[c] = R.resid[c];
+            ++done;
+        }
+        finished = H->finished != 0;
+    }
+    // download the run state
+    st->gov.vstar = H->gov.vstar;
+    st->gov.df = H->gov.df;
+    st->gov.gap = H->gov.gap;
+    st->gov.count = H->gov.count;
+    st->gov.bound = H->gov.bound;
+    st->gov.iter = H->gov.iter;
+    st->gov.g_prev = H->gov.g_prev;
+    st->gov.reduced = H->gov.reduced;
+    st->iter = H->iter;
+    st->plateau = H->plateau;
+    st->have_g_last = H->have_g_last;
+    st->g_last = H->g_last;
+    st->converged = H->converged;
+    st->finished = H->finished;
+    st->warm = H->warm;
+    st->g = H->g;
+    st->mean_rho = H->mean_rho;
+    st->mean_rho_p = H->mean_rho_p;
+    *n_out = done;
+    ctx->stat_solves += H->n_solves;
+    ctx->stat_outer += H->n_outer;
+    ctx->stat_inner += H->n_inner;
+    ctx->stat_oc += H->n_oc;
+    ctx->stat_oc_passes += H->n_oc_passes;
+    ctx->stat_oc_retry += H->n_oc_retries;
+    // graph nodes launched: per iteration ~14 fixed + the build, per refinement step 5,
+    // per PCG iteration the inner body
+    ctx->launches += (long long)(done + (status ? 1 : 0)) * (14 + ctx->build_launches) + 5 * (H->n_solves + H->n_outer) +
+                     H->n_inner * ctx->launches_per_inner + H->n_oc * 2;
+    ctx->have_T = true;
+    ctx->warm = H->warm != 0;
+    ctx->built = true;
+    ctx->T_center_pending = true;
+    if (status == 2) {
+        char buf[256];
+        const LoopRecord& R = H->rec[H->iter % kLoopRing];
+        snprintf(buf, sizeof buf, "solver failed at iteration %d: no convergence after %d V-cycles (residual %.3e)",
+                 H->iter + 1, R.vcycles, std::max(R.resid[0], std::max(R.resid[1], R.resid[2])));
+        ctx->err = buf;
+        st->finished = 1;
+        return OTM_ENOCONV;
+    }
+    if (status) {
+        st->finished = 1;
+        return fail(ctx, OTM_EINVAL, "objective failed (non-finite tensor or no constrained component)");
+    }
     return OTM_OK;
 }
 

@@ -75,6 +75,8 @@ struct PcgScalars {
     int ccyc[3];         // preconditioner applications of each case
     int hcount, hcap;    // residual history of the current inner loop: hist[3 * it + c] = r.r
     double* hist;        // (-1 for a case that was not active in that iteration)
+    int skip;            // set by the device-side solve control once the solve is over:
+                         // the T update and the trailing fp64 defect pass become no-ops
 };
 
 // Deterministic two-stage reduction workspace.
@@ -108,7 +110,8 @@ int launch_coarse_setup(cudaStream_t s, const Geo& g, const float* k, const Coar
                          float* G);
 void launch_coarse_solve(cudaStream_t s, int n, const float* G, const float* f, float* z);
 void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
-                  const double* fext, const double* fmean, float* r32, Red& red, double* out9);
+                  const double* fext, const double* fmean, float* r32, Red& red, double* out9,
+                  const int* skip = nullptr);   // *skip != 0: no-op (device-side solve control)
 void launch_apply64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
                     double* out, int load_case);
 void launch_load_means(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, Red& red,
@@ -138,7 +141,7 @@ void launch_submean(cudaStream_t s, long long n, double* T, const double* sumT);
 void launch_tensor(cudaStream_t s, const Geo& g, const double* T, const double* kap, Red& red, double* out6);
 void launch_pair_energy(cudaStream_t s, const Geo& g, const double* T, double* E);
 void launch_sens(cudaStream_t s, const Geo& g, const double* T, const double* rf, const SimpParams& sp,
-                 const Dg& dG, double* sens);
+                 const Dg& dG, double* sens, const Dg* dG_dev = nullptr);   // dG_dev != NULL overrides dG
 void launch_oc_eval(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a, int nlam,
                     const LamSet& lam_pow, Red& red, double* out);
 int launch_oc_coop(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a,

@@ -536,7 +536,9 @@ template <bool EXPLICIT_F>
 __global__ void __launch_bounds__(128) k_res64(Geo g, int xb, LevelTemplate lt, const double* __restrict__ kap,
                                                const double* __restrict__ T, const double* __restrict__ fext,
                                                const double* __restrict__ fmean, float* __restrict__ r32,
-                                               double* partials, unsigned* counter, double* red_out) {
+                                               double* partials, unsigned* counter, double* red_out,
+                                               const int* __restrict__ skip) {
+    if (skip && *skip) return;      // device-side solve control: the solve is already over
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     double acc[9];
 #pragma unroll
@@ -1262,6 +1264,7 @@ __global__ void k_prolong(Geo f, Geo c, int cx, int cy, int cz, const float* __r
 // Warm-start extrapolation across design iterations: T <- T + theta (T - T_prev), T_prev <- T.
 __global__ void k_Tupd(long long n, double* __restrict__ T, const float* __restrict__ d, const float* __restrict__ p,
                        const PcgScalars* __restrict__ sc) {
+    if (sc->skip) return;           // device-side solve control: no inner loop ran
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 3 * n) return;
     const int c = (int)(i / n);
@@ -1362,6 +1365,143 @@ __global__ void __launch_bounds__(256, 4) k_sens(Geo g, const double* __restrict
     for (int c = 0; c < 6; ++c) con += dG.v[c] * E[c];
     const double dk = sp.p * simp_pow(rf[e], sp.p - 1.0) * (sp.k0 - sp.kmin);
     sens[e] = dk * con / (double)g.n;
+}
+
+// ---- x-marching form (the design-loop path) ---------------------------------
+// In the Walsh-Hadamard basis of the 8 corners (chi_s(a) = (-1)^popcount(s & a))
+// the element matrix is diagonal: K0 = (5 I + N1 - J) / 12 has eigenvalue 0 on
+// s = 0 and 1/2, 1/3, 1/6 on popcount(s) = 1, 2, 3.  So with what_i = H w_i,
+//   E_ij = w_i . K0 w_j = (1/8) sum_s mu_s what_i[s] what_j[s]:
+// a 24-add butterfly per case and 7 products per pair instead of the 8 x 8 form.
+// w_i = c_i - T_i, and H c_i is 4 on s = 0 and -4 on s = 2^i (zero elsewhere).
+// A thread owns one (y, z) column and marches a chunk of x planes, carrying the
+// 4 corners of plane x (3 cases) from the previous step: 12 loads per element
+// instead of 24, and no per-element index division.
+struct MarchCol {
+    unsigned o00, o01, o10, o11;     // in-plane offsets of (y,z), (y,z+1), (y+1,z), (y+1,z+1)
+};
+
+__device__ __forceinline__ void load_plane(const double* __restrict__ T, long long n, unsigned po, const MarchCol& q,
+                                           double (&P)[3][4]) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const double* Ti = T + (size_t)i * n + po;
+        P[i][0] = __ldg(Ti + q.o00);
+        P[i][1] = __ldg(Ti + q.o01);
+        P[i][2] = __ldg(Ti + q.o10);
+        P[i][3] = __ldg(Ti + q.o11);
+    }
+}
+
+// energies of the element between planes A (x) and B (x + 1); corner a = (a&1: x,
+// a&2: y, a&4: z) -> plane (a & 1), in-plane slot ((a >> 1) & 1) * 2 + ((a >> 2) & 1)
+__device__ __forceinline__ void energies_wht(const double (&A)[3][4], const double (&B)[3][4], double (&E)[6]) {
+    double u[3][8];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        double v[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const int slot = ((a >> 1) & 1) * 2 + ((a >> 2) & 1);
+            v[a] = -((a & 1) ? B[i][slot] : A[i][slot]);      // -T (c_i added in the spectrum)
+        }
+#pragma unroll
+        for (int h = 1; h < 8; h <<= 1)
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+                if (!(a & h)) {
+                    const double p = v[a], q = v[a | h];
+                    v[a] = p + q;
+                    v[a | h] = p - q;
+                }
+        v[1 << i] -= 4.0;                                      // + H c_i (the s = 0 term drops)
+        // scale by sqrt(mu_s / 8): mu = 1/2, 1/3, 1/6 for popcount 1, 2, 3
+        const double r1 = 0.25, r2 = 0.2041241452319315, r3 = 0.14433756729740643;
+        u[i][1] = v[1] * r1; u[i][2] = v[2] * r1; u[i][4] = v[4] * r1;
+        u[i][3] = v[3] * r2; u[i][5] = v[5] * r2; u[i][6] = v[6] * r2;
+        u[i][7] = v[7] * r3;
+    }
+    const int pi[6] = {0, 1, 2, 0, 1, 0}, pj[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int t = 1; t < 8; ++t) s = fma(u[pi[c]][t], u[pj[c]][t], s);
+        E[c] = s;
+    }
+}
+
+// one (y, z) column and a chunk [x0, x1) of planes per thread
+__device__ __forceinline__ bool march_setup(const Geo& g, int chunks, MarchCol& q, int& x0, int& x1) {
+    const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned cols = (unsigned)g.pl;
+    if (t >= cols * (unsigned)chunks) return false;
+    const unsigned c = t / cols, r = t - c * cols;
+    const unsigned y = r / (unsigned)g.nz, z = r - y * (unsigned)g.nz;
+    const unsigned yp = y + 1 == (unsigned)g.ny ? 0u : y + 1, zp = z + 1 == (unsigned)g.nz ? 0u : z + 1;
+    q.o00 = y * g.nz + z;
+    q.o01 = y * g.nz + zp;
+    q.o10 = yp * g.nz + z;
+    q.o11 = yp * g.nz + zp;
+    const int per = (g.nx + chunks - 1) / chunks;
+    x0 = (int)c * per;
+    x1 = min(g.nx, x0 + per);
+    return x0 < x1;
+}
+
+__global__ void __launch_bounds__(256) k_tensor_x(Geo g, int chunks, const double* __restrict__ T,
+                                                  const double* __restrict__ kap, double* partials, unsigned* counter,
+                                                  double* out) {
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    MarchCol q;
+    int x0, x1;
+    if (march_setup(g, chunks, q, x0, x1)) {
+        double A[3][4], B[3][4];
+        load_plane(T, g.n, (unsigned)x0 * (unsigned)g.pl, q, A);
+        for (int x = x0; x < x1; ++x) {
+            const unsigned pb = (unsigned)(x + 1 == g.nx ? 0 : x + 1) * (unsigned)g.pl;
+            load_plane(T, g.n, pb, q, B);
+            double E[6];
+            energies_wht(A, B, E);
+            const double k = __ldg(kap + (unsigned)x * (unsigned)g.pl + q.o00);
+#pragma unroll
+            for (int c = 0; c < 6; ++c) acc[c] = fma(k, E[c], acc[c]);
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+#pragma unroll
+                for (int s = 0; s < 4; ++s) A[i][s] = B[i][s];
+        }
+    }
+    if (reduce_finalize<6>(acc, partials, counter, out)) {
+        for (int c = 0; c < 6; ++c) out[c] /= (double)g.n;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_sens_x(Geo g, int chunks, const double* __restrict__ T,
+                                                const double* __restrict__ rf, SimpParams sp, Dg dG,
+                                                const Dg* __restrict__ dG_dev, double* __restrict__ sens) {
+    MarchCol q;
+    int x0, x1;
+    if (!march_setup(g, chunks, q, x0, x1)) return;
+    if (dG_dev) dG = *dG_dev;               // objective weights computed on the device (otm_loop.cu)
+    double A[3][4], B[3][4];
+    load_plane(T, g.n, (unsigned)x0 * (unsigned)g.pl, q, A);
+    const double scale = (sp.k0 - sp.kmin) * sp.p / (double)g.n;
+    for (int x = x0; x < x1; ++x) {
+        const unsigned pb = (unsigned)(x + 1 == g.nx ? 0 : x + 1) * (unsigned)g.pl;
+        load_plane(T, g.n, pb, q, B);
+        double E[6];
+        energies_wht(A, B, E);
+        double con = 0.0;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) con = fma(dG.v[c], E[c], con);
+        const unsigned e = (unsigned)x * (unsigned)g.pl + q.o00;
+        sens[e] = simp_pow(__ldg(rf + e), sp.p - 1.0) * scale * con;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int s = 0; s < 4; ++s) A[i][s] = B[i][s];
+    }
 }
 
 // ===========================================================================
@@ -1988,7 +2128,7 @@ void launch_coarse_solve(cudaStream_t s, int n, const float* G, const float* f, 
     launch_pdl(k_coarse_solve, blocks, 1024, 0, s, n, G, f, z);
 }
 void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
-                  const double* fext, const double* fmean, float* r32, Red& red, double* out9) {
+                  const double* fext, const double* fmean, float* r32, Red& red, double* out9, const int* skip) {
     static const bool r512 = !(getenv("OTM_RES64_512") && atoi(getenv("OTM_RES64_512")) == 0);
     const bool w512 = r512 && lt.equal && g.nz == 512 && g.nx >= 2;
     if (!fext && (tma_tiling(g, lt) || w512)) {
@@ -2021,19 +2161,19 @@ void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const d
             switch (g.nz) {
             case 512:
                 smem_attr(k_res64w<512>, sm);
-                k_res64w<512><<<blocks, blk, sm, s>>>(g, lt, M, fmean, r32, red.partials, red.counter, out9);
+                k_res64w<512><<<blocks, blk, sm, s>>>(g, lt, M, fmean, r32, red.partials, red.counter, out9, skip);
                 break;
             case 64:
                 smem_attr(k_res64w<64>, sm);
-                k_res64w<64><<<blocks, blk, sm, s>>>(g, lt, M, fmean, r32, red.partials, red.counter, out9);
+                k_res64w<64><<<blocks, blk, sm, s>>>(g, lt, M, fmean, r32, red.partials, red.counter, out9, skip);
                 break;
             case 128:
                 smem_attr(k_res64w<128>, sm);
-                k_res64w<128><<<blocks, blk, sm, s>>>(g, lt, M, fmean, r32, red.partials, red.counter, out9);
+                k_res64w<128><<<blocks, blk, sm, s>>>(g, lt, M, fmean, r32, red.partials, red.counter, out9, skip);
                 break;
             default:
                 smem_attr(k_res64w<256>, sm);
-                k_res64w<256><<<blocks, blk, sm, s>>>(g, lt, M, fmean, r32, red.partials, red.counter, out9);
+                k_res64w<256><<<blocks, blk, sm, s>>>(g, lt, M, fmean, r32, red.partials, red.counter, out9, skip);
                 break;
             }
             return;
@@ -2042,10 +2182,10 @@ void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const d
     int xb;
     const dim3 grid = stencil_grid(g, &xb);
     if (fext)
-        k_res64<true><<<grid, 128, 0, s>>>(g, xb, lt, kap, T, fext, fmean, r32, red.partials, red.counter, out9);
+        k_res64<true><<<grid, 128, 0, s>>>(g, xb, lt, kap, T, fext, fmean, r32, red.partials, red.counter, out9, skip);
     else
         k_res64<false><<<grid, 128, 0, s>>>(g, xb, lt, kap, T, nullptr, fmean, r32, red.partials, red.counter,
-                                            out9);
+                                            out9, skip);
 }
 void launch_apply64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
                     double* out, int load_case) {
@@ -2328,17 +2468,34 @@ void launch_submean_means(cudaStream_t s, long long n, double* T, const double* 
 void launch_submean(cudaStream_t s, long long n, double* T, const double* sumT) {
     k_submean<<<nblk(3 * n, 256), 256, 0, s>>>(n, T, sumT);
 }
+// x chunks per (y, z) column: about 2 waves of the kernel's resident threads,
+// >= 4 planes each (a chunk reloads its first plane)
+template <class K>
+static int march_chunks(K kernel, const Geo& g) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
+    const long long want = 2LL * sms * std::max(per_sm, 1) * 256;
+    long long c = (want + g.pl - 1) / g.pl;
+    c = std::min<long long>(c, std::max(1, g.nx / 4));
+    return (int)std::max<long long>(1, c);
+}
 void launch_tensor(cudaStream_t s, const Geo& g, const double* T, const double* kap, Red& red, double* out6) {
-    long long want = (g.n + 255) / 256;
-    unsigned blocks = (unsigned)(want < 1184 ? want : 1184);
-    k_tensor<<<blocks, 256, 0, s>>>(g, T, kap, red.partials, red.counter, out6);
+    static int ch = 0, for_pl = -1, for_nx = -1;
+    if (for_pl != g.pl || for_nx != g.nx) { ch = march_chunks(k_tensor_x, g); for_pl = g.pl; for_nx = g.nx; }
+    const long long th = (long long)g.pl * ch;
+    k_tensor_x<<<nblk(th, 256), 256, 0, s>>>(g, ch, T, kap, red.partials, red.counter, out6);
 }
 void launch_pair_energy(cudaStream_t s, const Geo& g, const double* T, double* E) {
     k_pair_energy<<<nblk(g.n, 256), 256, 0, s>>>(g, T, E);
 }
 void launch_sens(cudaStream_t s, const Geo& g, const double* T, const double* rf, const SimpParams& sp,
-                 const Dg& dG, double* sens) {
-    k_sens<<<nblk(g.n, 256), 256, 0, s>>>(g, T, rf, sp, dG, sens);
+                 const Dg& dG, double* sens, const Dg* dG_dev) {
+    static int ch = 0, for_pl = -1, for_nx = -1;
+    if (for_pl != g.pl || for_nx != g.nx) { ch = march_chunks(k_sens_x, g); for_pl = g.pl; for_nx = g.nx; }
+    const long long th = (long long)g.pl * ch;
+    k_sens_x<<<nblk(th, 256), 256, 0, s>>>(g, ch, T, rf, sp, dG, dG_dev, sens);
 }
 void launch_oc_eval(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a, int nlam,
                     const LamSet& lam_pow, Red& red, double* out) {

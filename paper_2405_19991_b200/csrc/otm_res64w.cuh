@@ -59,7 +59,9 @@ __device__ __forceinline__ void r64_ld(double* dst, const CUtensorMap* map, int 
 template <int NZ>
 __global__ void __launch_bounds__(R64Geo<NZ>::THREADS, R64Geo<NZ>::MINB) k_res64w(Geo g, LevelTemplate lt, const __grid_constant__ R64Maps maps,
                                                    const double* __restrict__ fmean, float* __restrict__ r32,
-                                                   double* partials, unsigned* counter, double* out9) {
+                                                   double* partials, unsigned* counter, double* out9,
+                                                   const int* __restrict__ skip) {
+    if (skip && *skip) return;      // device-side solve control: the solve is already over
     using RG = R64Geo<NZ>;
     constexpr int TYD = RG::TYD, TROWS = RG::TROWS, SLOT = RG::SLOT;
     extern __shared__ __align__(128) double r64_smem[];

@@ -239,7 +239,14 @@ class DesignRun:
             rho0 = rho0.clone()
         else:
             rho0, _ = _dev.to_device(init_density(config.dims, config.init).rho)
-        self.rho = rho0
+        # the density lives in one buffer per hierarchy, so the captured iteration graph
+        # (which records its address) is reused by every run on this grid
+        buf = getattr(self.hier, "_design_rho", None)
+        if buf is None or tuple(buf.shape) != tuple(rho0.shape):
+            buf = t.empty_like(rho0)
+            self.hier._design_rho = buf
+        buf.copy_(rho0)
+        self.rho = buf
         if config.symmetry == "central":
             self.hier.ctx.call("otm_symmetrize", _dev.ptr(self.rho))
         self.rho_f = t.empty_like(self.rho)
@@ -286,6 +293,41 @@ class DesignRun:
             self.update()
         return rc, rec
 
+    def run_batch(self, max_iters: int, batch: int = 16):
+        """Up to ``max_iters`` whole iterations (evaluate + update) as device-resident
+        graph launches (otm_run_batch), one host synchronisation per ``batch``.
+        Returns (rc, records); rc == OTM_ESTATE means the graph path is unavailable
+        and the caller should step() instead."""
+        ctx = self.hier.ctx
+        recs = (_lib.IterRecordC * int(max_iters))()
+        n = C.c_int(0)
+        cur = _dev.torch().cuda.current_stream()
+        ctx.stream.wait_stream(cur)
+        rc = ctx.lib.otm_run_batch(ctx.h, C.byref(self.cc), C.byref(self.st), _dev.ptr(self.rho), int(max_iters),
+                                   int(batch), recs, C.byref(n))
+        cur.wait_stream(ctx.stream)
+        ctx.version += 1
+        out = []
+        for k in range(n.value):
+            r = recs[k]
+            rec = IterationRecord(r.iter, r.g, r.volfrac, r.volfrac_filtered, r.vstar, r.vcycles, r.ms)
+            self.log.append(rec)
+            out.append(rec)
+            self.kappa = ConductivityTensor(np.array(r.kappa[:]))
+        return rc, out
+
+    def run(self, batch: int = 16):
+        """Advance to the end of the run: the graph path when available, else step()."""
+        while not self.finished:
+            rc, _ = self.run_batch(self.config.max_iter, batch)
+            if rc == _lib.OTM_ESTATE and not self.finished:
+                rc, _ = self.step()
+                while rc == _lib.OTM_OK and not self.finished:
+                    rc, _ = self.step()
+            if rc != _lib.OTM_OK:
+                return rc
+        return _lib.OTM_OK
+
     def error(self) -> str:
         return self.hier.ctx.lib.otm_last_error(self.hier.ctx.h).decode()
 
@@ -330,12 +372,20 @@ def run_optimization(config: RunConfig, callback: Optional[Callable] = None,
     host_fld = None
 
     def result(converged):
-        rho = run.rho if on_device else run.rho.cpu().numpy()
+        rho = run.rho.clone() if on_device else run.rho.cpu().numpy()
         fld = DensityField(config.dims, rho, rho * 0)
         kap = run.kappa if run.kappa is not None else ConductivityTensor(np.full(6, np.nan))
         return OptimizationResult(field=fld, kappa=kap, log=run.log, converged=converged,
                                   iterations=len(run.log), config=config)
 
+    if callback is None:
+        # no per-iteration host work: whole iterations as device-resident graph launches
+        rc = run.run()
+        if rc == _lib.OTM_ENOCONV:
+            raise OptimizationAborted(run.error(), result(False))
+        if rc != _lib.OTM_OK:
+            run.hier.ctx.check(rc)
+        return result(bool(run.st.converged))
     while not run.finished:
         rc, rec = run.evaluate()
         if rc == _lib.OTM_ENOCONV:

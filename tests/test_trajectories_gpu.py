@@ -6,12 +6,13 @@ bottom, fp64 defect correction, cooperative OC search) over many design
 iterations, not just the first one.
 
 The design loop is chaotic: the reference run at solver_tol 1e-7 instead of
-1e-6 (tests/golden/traj_*_tol1e-7.npz, same script) leaves its own 1e-6
-trajectory by > 1e-3 in g from iteration 100 of C1, 26 of C2 and 95 of the flat
-case, and converges 1 (C1) or 9 (flat) iterations later.  No implementation whose
-solves are not bit-identical to the reference can track it further than that.
+1e-6 (tests/golden/traj_*_tol*.npz, same script; also 3e-7 and 1e-8 for C1 and
+the flat case) leaves its own 1e-6 trajectory by > 1e-3 in g from iteration 100
+of C1, 26 of C2 and 95 of the flat case, and converges up to 9 iterations (flat)
+apart.  No implementation whose solves are not bit-identical to the reference can
+track it further than that.
 Gates, per iteration k:
-  * before the onset k0 (first k where the reference's own tol-1e-7 run differs
+  * before the onset k0 (first k where one of the reference's own re-runs differs
     by > 1e-4 in g): g within 1e-3 relative, |dV| <= 1e-4, V* within 1e-4,
     homogenized tensor within max(1e-5, 3x the reference's own deviation) of
     ||kappa||;
@@ -50,17 +51,23 @@ def _run(otm, g, max_iter=None):
 
 
 def _envelope(name, g, n):
-    """The reference's own per-iteration deviation under solver_tol 1e-7."""
-    try:
-        p = golden(name.replace(".npz", "_tol1e-7.npz"))
-    except FileNotFoundError:
+    """The reference's own per-iteration deviation when its solver tolerance moves
+    (every tests/golden/<name>_tol*.npz run: 1e-7, 3e-7, 1e-8), maximum over them."""
+    import glob
+    import os
+    from otm_testutil import GOLDEN
+    runs = [np.load(f) for f in sorted(glob.glob(os.path.join(GOLDEN, name.replace(".npz", "_tol*.npz"))))]
+    if not runs:
         return None
-    m = min(n, len(p["g"]), len(g["g"]))
-    eg = np.abs(g["g"][:m] - p["g"][:m]) / np.abs(g["g"][:m])
-    ev = np.abs(g["volfrac"][:m] - p["volfrac"][:m])
+    m = min([n, len(g["g"])] + [len(p["g"]) for p in runs])
     kn = np.linalg.norm(np.nan_to_num(g["kappa"][:m]), axis=1)
-    ek = np.maximum.accumulate(np.nanmax(np.abs(g["kappa"][:m] - p["kappa"][:m]), axis=1) / kn)
-    return p, eg, ev, ek
+    eg = np.max([np.abs(g["g"][:m] - p["g"][:m]) / np.abs(g["g"][:m]) for p in runs], axis=0)
+    ev = np.max([np.abs(g["volfrac"][:m] - p["volfrac"][:m]) for p in runs], axis=0)
+    ek = np.maximum.accumulate(np.max([np.nanmax(np.abs(g["kappa"][:m] - p["kappa"][:m]), axis=1) / kn
+                                       for p in runs], axis=0))
+    dn = max(abs(int(p["iterations"]) - int(g["iterations"])) for p in runs)
+    dV = max(abs(float(p["volfrac"][-1]) - float(g["volfrac"][-1])) for p in runs)
+    return (dn, dV), eg, ev, ek
 
 
 def _compare(res, kap, g, n, env=None):
@@ -102,9 +109,7 @@ def _converged_like_reference(res, g, env):
     n_ref = int(g["iterations"])
     assert res.converged
     assert res.log[-1].g <= 1e-4
-    p = env[0] if env is not None else None
-    dn = abs(int(p["iterations"]) - n_ref) if p is not None else 0
-    dV = abs(float(p["volfrac"][-1]) - float(g["volfrac"][-1])) if p is not None else 0.0
+    dn, dV = env[0] if env is not None else (0, 0.0)
     assert abs(len(res.log) - n_ref) <= max(5, 2 * dn), (len(res.log), n_ref, dn)
     assert abs(res.field.mean() - float(g["volfrac"][-1])) <= max(1e-3, 2 * dV)
 
