@@ -249,7 +249,10 @@ def beyond_l2(otm, _lib, lib, torch, peak, peak_kind, iters=20):
         torch.cuda.empty_cache()
         return {"workload": f"c4 {dims}, {iters} OC iterations from the IWP seed", "bound": "hbm",
                 "unit": "GB/s", "peak": peak, "peak_kind": peak_kind,
-                "achieved": out["l0_stencil"]["gbs"], "frac": out["l0_stencil"]["frac"], "kernels": out}
+                "achieved": out["l0_stencil"]["gbs"], "frac": out["l0_stencil"]["frac"], "kernels": out,
+                "traffic": traffic_bytes("c4"),
+                "traffic_note": "mean ncu DRAM bytes per level-0 stencil launch at 256^3 "
+                                "(profiles/r*_traffic_c4.json); algorithmic 44/44/28 B per vertex"}
     except Exception as e:                           # reported, never fatal to the headline line
         return {"error": f"{type(e).__name__}: {e}"}
 
@@ -516,6 +519,30 @@ def run_slab(args):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_max = float(tt.item())
     value = t_max / 1e3 / args.steps
+    # the same workload on ONE GPU through the single-GPU solver (rank 0): the
+    # reference point of the strong-scaling efficiency T1 / (N * TN)
+    single = None
+    if rank == 0 and not args.no_single:
+        from paper_2405_19991_b200.optimize import DesignRun
+        hier = otm.GridHierarchy(dims)
+        seed_dev = torch.from_numpy(seed).cuda()
+
+        def one_single():
+            r = DesignRun(make_config(otm, name, args.iters, 0.0, init_field=seed_dev), hier=hier)
+            r.run()
+            return r
+
+        one_single()
+        ts = []
+        for _ in range(max(1, args.steps)):
+            torch.cuda.synchronize()
+            ev[0].record()
+            one_single()
+            ev[1].record()
+            ev[1].synchronize()
+            ts.append(ev[0].elapsed_time(ev[1]) / 1e3)
+        single = statistics.median(ts)
+        del hier
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "s/structure", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
@@ -524,6 +551,11 @@ def run_slab(args):
                                        f"one structure on {world} x-slabs",
                            "mode": "slab", "iterations_per_step": iters,
                            "parallelism": f"x-slabs x{world}, NCCL halos + all-reduce"}}
+        if single is not None:
+            line["single_gpu"] = {"value": single, "unit": "s/structure",
+                                  "path": "the single-GPU solver (iteration graph) on the same workload, rank 0"}
+            line["slab_over_single"] = value / single
+            line["parallel_efficiency"] = single / (world * value)
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
@@ -538,6 +570,7 @@ def main():
     ap.add_argument("--iters", type=int, default=500, help="OC iterations per structure")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-c1", action="store_true", help="skip the C1 to-convergence legs")
+    ap.add_argument("--no-single", action="store_true", help="--mode slab: skip the single-GPU reference time")
     ap.add_argument("--host-loop", action="store_true",
                     help="drive the design loop from the host (otm_run_step/update) instead of the iteration graph")
     ap.add_argument("--no-prof", action="store_true", help="no in-region kernel events")

@@ -88,6 +88,22 @@ int otm_slab_oc_sums(otm_slab_ws* w, int nxl, int ny, int nz, double n_total, co
 int otm_slab_oc_apply(otm_slab_ws* w, int nxl, int ny, int nz, double n_total, const otm_oc_params* pp,
                       const double* rho, const double* sens, double lam, double* rho_out, double* changed);
 
+/* Device scalars (round 2): with mode 1 the PCG calls take and return their scalars
+ * in DEVICE memory and never synchronise the stream -- otm_slab_stencil's dots3,
+ * otm_slab_pupd's beta3, otm_slab_upd's alpha3 / rr3 (and the other sums3/6/9
+ * outputs) -- so a slab PCG iteration runs without host round trips; the caller
+ * all-reduces the partial sums in device memory (NCCL) and advances the scalars
+ * with otm_slab_pcg_step.  Mode 0 (default): host scalars, as documented above. */
+int otm_slab_set_scalar_mode(otm_slab_ws* w, int device);
+/* The PCG scalar recurrences on a device array S of 28 doubles:
+ *   S[0..2] r.z (all-reduced)   S[3..5] previous r.z   S[6..8] beta    S[9..11] p.q (all-reduced)
+ *   S[12..14] alpha            S[15..17] r.r (all-reduced)   S[18..20] target^2
+ *   S[21..23] active (1/0)     S[24] first (1 before the first iteration)   S[25..27] V-cycles per case
+ * stage 0: beta = first ? 0 : r.z / previous (0 if previous is 0); previous = r.z
+ * stage 1: alpha = active && p.q > 0 ? r.z / p.q : 0
+ * stage 2: cycles += active; active &= r.r > target^2 */
+int otm_slab_pcg_step(otm_slab_ws* w, int stage, double* S_dev);
+
 #ifdef __cplusplus
 }
 #endif

@@ -233,9 +233,10 @@ __global__ void ks_prolong_b(SGeo f, SGeo c, const float* __restrict__ zc, float
 }
 
 // p = z + beta p on the interior, float4, blockIdx.y = case (pl % 4 == 0)
-__global__ void ks_pupd4(SGeo g, const float* __restrict__ z, float* __restrict__ p, double b0, double b1, double b2) {
+__global__ void ks_pupd4(SGeo g, const float* __restrict__ z, float* __restrict__ p, double b0, double b1, double b2,
+                         const double* __restrict__ bdev) {
     const int c = blockIdx.y;
-    const float b = (float)(c == 0 ? b0 : (c == 1 ? b1 : b2));
+    const float b = (float)(bdev ? bdev[c] : (c == 0 ? b0 : (c == 1 ? b1 : b2)));
     const long long base = (long long)c * g.na + g.pl;
     const float4* zz = reinterpret_cast<const float4*>(z + base);
     float4* pp = reinterpret_cast<float4*>(p + base);
@@ -250,9 +251,9 @@ __global__ void ks_pupd4(SGeo g, const float* __restrict__ z, float* __restrict_
 __global__ void __launch_bounds__(256) ks_upd4(SGeo g, float* __restrict__ d, float* __restrict__ r,
                                                const float* __restrict__ p, const float* __restrict__ q, double a0,
                                                double a1, double a2, double* partials, unsigned* counter,
-                                               double* out3) {
+                                               double* out3, const double* __restrict__ adev) {
     const int c = blockIdx.y;
-    const float al = (float)(c == 0 ? a0 : (c == 1 ? a1 : a2));
+    const float al = (float)(adev ? adev[c] : (c == 0 ? a0 : (c == 1 ? a1 : a2)));
     const long long base = (long long)c * g.na + g.pl;
     float4* dd = reinterpret_cast<float4*>(d + base);
     float4* rr = reinterpret_cast<float4*>(r + base);
@@ -301,12 +302,12 @@ __global__ void ks_dinv(SGeo g, const float* __restrict__ k, float kdiag, float*
 
 // p = z + beta p (interior)
 __global__ void ks_pupd(SGeo g, const float* __restrict__ z, float* __restrict__ p, double b0, double b1,
-                        double b2) {
+                        double b2, const double* __restrict__ bdev) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 3 * g.ni) return;
     const int c = (int)(i / g.ni);
     const long long idx = (long long)c * g.na + g.pl + (i - (long long)c * g.ni);
-    const float b = (float)(c == 0 ? b0 : (c == 1 ? b1 : b2));
+    const float b = (float)(bdev ? bdev[c] : (c == 0 ? b0 : (c == 1 ? b1 : b2)));
     p[idx] = z[idx] + b * p[idx];
 }
 
@@ -314,12 +315,12 @@ __global__ void ks_pupd(SGeo g, const float* __restrict__ z, float* __restrict__
 __global__ void __launch_bounds__(256) ks_upd(SGeo g, float* __restrict__ d, float* __restrict__ r,
                                               const float* __restrict__ p, const float* __restrict__ q, double a0,
                                               double a1, double a2, double* partials, unsigned* counter,
-                                              double* out3) {
+                                              double* out3, const double* __restrict__ adev) {
     double d3[3] = {0.0, 0.0, 0.0};
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < 3 * g.ni; i += (long long)gridDim.x * blockDim.x) {
         const int c = (int)(i / g.ni);
         const long long idx = (long long)c * g.na + g.pl + (i - (long long)c * g.ni);
-        const float al = (float)(c == 0 ? a0 : (c == 1 ? a1 : a2));
+        const float al = (float)(adev ? adev[c] : (c == 0 ? a0 : (c == 1 ? a1 : a2)));
         d[idx] += al * p[idx];
         const float rn = r[idx] - al * q[idx];
         r[idx] = rn;
@@ -557,6 +558,33 @@ inline unsigned nb(long long n, int bs) { return (unsigned)((n + bs - 1) / bs); 
 // atomics on the ticket counter)
 inline unsigned nbr(long long n, int bs) { const unsigned b = nb(n, bs); return b < 1184u ? b : 1184u; }
 
+// Device-side PCG scalars of the slab solve (layout in otm_slab.h: otm_slab_pcg_step);
+// stage 0 after the r.z all-reduce, 1 after p.q, 2 after r.r -- the host loop of
+// round 1 (slab.py) moved to the device, same expressions.
+__global__ void ks_pcg_step(int stage, double* S) {
+    double* rz = S;
+    double* rz_old = S + 3;
+    double* beta = S + 6;
+    double* pq = S + 9;
+    double* alpha = S + 12;
+    double* rr = S + 15;
+    double* target2 = S + 18;
+    double* active = S + 21;
+    double* cyc = S + 25;
+    for (int c = 0; c < 3; ++c) {
+        if (stage == 0) {
+            beta[c] = S[24] != 0.0 ? 0.0 : (rz_old[c] != 0.0 ? rz[c] / rz_old[c] : 0.0);
+            rz_old[c] = rz[c];
+        } else if (stage == 1) {
+            alpha[c] = (active[c] != 0.0 && pq[c] > 0.0) ? rz[c] / pq[c] : 0.0;
+        } else {
+            cyc[c] += active[c];
+            if (!(rr[c] > target2[c])) active[c] = 0.0;
+        }
+    }
+    if (stage == 0) S[24] = 0.0;
+}
+
 }  // namespace
 }  // namespace otm
 
@@ -571,6 +599,7 @@ struct otm_slab_ws {
     double* out32 = nullptr;     // 32 OC candidate sums (device) and their host copy
     double* h32 = nullptr;
     PcgScalars* sc = nullptr;    // scratch scalars of the k10 level kernels (their dot sums land in red[])
+    int dev = 0;                 // 1: scalar arguments / results of the PCG calls are device pointers
     size_t max_blocks = 0;
     char err[256] = {0};
 };
@@ -590,6 +619,10 @@ static int scheck(otm_slab_ws* w) {
     return e == cudaSuccess ? OTM_OK : sfail(w, cudaGetErrorString(e));
 }
 static int sfetch(otm_slab_ws* w, int nq, double* out) {
+    if (w->dev) {       // device scalars: stream-ordered copy, no host round trip
+        SCK(cudaMemcpyAsync(out, w->out, nq * sizeof(double), cudaMemcpyDeviceToDevice, w->stream));
+        return OTM_OK;
+    }
     SCK(cudaMemcpyAsync(w->h, w->out, nq * sizeof(double), cudaMemcpyDeviceToHost, w->stream));
     SCK(cudaStreamSynchronize(w->stream));
     std::memcpy(out, w->h, nq * sizeof(double));
@@ -663,6 +696,11 @@ int otm_slab_stencil(otm_slab_ws* w, int op, int nxl, int ny, int nz, const doub
                              red, w->sc)) {
             int rc = scheck(w);
             if (rc || !dot) return rc;
+            if (w->dev) {
+                SCK(cudaMemcpyAsync(dots3, reinterpret_cast<const double*>(w->sc) + (op == 1 ? 0 : 3),
+                                    3 * sizeof(double), cudaMemcpyDeviceToDevice, w->stream));
+                return OTM_OK;
+            }
             SCK(cudaMemcpyAsync(w->h, reinterpret_cast<const double*>(w->sc) + (op == 1 ? 0 : 3), 3 * sizeof(double),
                                 cudaMemcpyDeviceToHost, w->stream));
             SCK(cudaStreamSynchronize(w->stream));
@@ -720,10 +758,11 @@ int otm_slab_pupd(otm_slab_ws* w, int nxl, int ny, int nz, const float* z, float
     if (!w || nxl < 1) return OTM_EINVAL;
     const SGeo g = make_sgeo(nxl, ny, nz);
     if (g.pl % 4 == 0)
-        ks_pupd4<<<dim3(std::min<unsigned>(nb(g.ni / 4, 256), 592u), 3), 256, 0, w->stream>>>(g, z, p, beta3[0],
-                                                                                          beta3[1], beta3[2]);
+        ks_pupd4<<<dim3(std::min<unsigned>(nb(g.ni / 4, 256), 592u), 3), 256, 0, w->stream>>>(
+            g, z, p, w->dev ? 0.0 : beta3[0], w->dev ? 0.0 : beta3[1], w->dev ? 0.0 : beta3[2], w->dev ? beta3 : nullptr);
     else
-        ks_pupd<<<nb(3 * g.ni, 256), 256, 0, w->stream>>>(g, z, p, beta3[0], beta3[1], beta3[2]);
+        ks_pupd<<<nb(3 * g.ni, 256), 256, 0, w->stream>>>(g, z, p, w->dev ? 0.0 : beta3[0], w->dev ? 0.0 : beta3[1],
+                                                          w->dev ? 0.0 : beta3[2], w->dev ? beta3 : nullptr);
     return scheck(w);
 }
 
@@ -734,10 +773,12 @@ int otm_slab_upd(otm_slab_ws* w, int nxl, int ny, int nz, float* d, float* r, co
     if (!blocks_ok(w, 3 * g.ni, 256)) return OTM_EINVAL;
     if (g.pl % 4 == 0)
         ks_upd4<<<dim3(std::min<unsigned>(nb(g.ni / 4, 256), 394u), 3), 256, 0, w->stream>>>(
-            g, d, r, p, q, alpha3[0], alpha3[1], alpha3[2], w->partials, w->counter, w->out);
+            g, d, r, p, q, w->dev ? 0.0 : alpha3[0], w->dev ? 0.0 : alpha3[1], w->dev ? 0.0 : alpha3[2], w->partials,
+            w->counter, w->out, w->dev ? alpha3 : nullptr);
     else
-        ks_upd<<<nbr(3 * g.ni, 256), 256, 0, w->stream>>>(g, d, r, p, q, alpha3[0], alpha3[1], alpha3[2],
-                                                          w->partials, w->counter, w->out);
+        ks_upd<<<nbr(3 * g.ni, 256), 256, 0, w->stream>>>(g, d, r, p, q, w->dev ? 0.0 : alpha3[0],
+                                                          w->dev ? 0.0 : alpha3[1], w->dev ? 0.0 : alpha3[2],
+                                                          w->partials, w->counter, w->out, w->dev ? alpha3 : nullptr);
     int rc = scheck(w);
     if (rc) return rc;
     return sfetch(w, 3, rr3);
@@ -890,4 +931,15 @@ int otm_slab_oc_apply(otm_slab_ws* w, int nxl, int ny, int nz, double n_total, c
     return OTM_OK;
 }
 
+int otm_slab_set_scalar_mode(otm_slab_ws* w, int device) {
+    if (!w) return OTM_EINVAL;
+    w->dev = device != 0;
+    return OTM_OK;
+}
+
+int otm_slab_pcg_step(otm_slab_ws* w, int stage, double* S) {
+    if (!w || !S || stage < 0 || stage > 2) return OTM_EINVAL;
+    ks_pcg_step<<<1, 1, 0, w->stream>>>(stage, S);
+    return scheck(w);
+}
 }  // extern "C"

@@ -63,7 +63,13 @@ class SlabLayout:
     nlev_dist: int         # levels 0 .. nlev_dist-1 are distributed; level nlev_dist is agglomerated
 
     @staticmethod
-    def make(dims, world, coarse_target=64):
+    def make(dims, world, coarse_target=64, min_local=65536):
+        """Levels stay distributed while they split into even slabs of >= 2 planes and
+        each rank keeps >= min_local vertices (level 0 always); below that the level
+        is agglomerated: the single-GPU V-cycle tail (per-level kernels, single-launch
+        bottom) runs it, where a slab level would cost more in launches and halos than
+        its work (measured: 2.1x the single-GPU time per PCG iteration at 256^3 on one
+        GPU with every level on slabs)."""
         chain = tuple(level_dims(dims, coarse_target))
         nl = len(chain)
         la = 0
@@ -74,6 +80,8 @@ class SlabLayout:
                 break
             if any(chain[la + 1][a] * 2 != chain[la][a] for a in range(3)):
                 break                               # slab levels need 3-D coarsening
+            if la > 0 and int(np.prod(chain[la])) // world < min_local:
+                break
             la += 1
         if la == 0:
             raise ValueError(f"dims {tuple(dims)} cannot be split into {world} even slabs of >= 2 planes")
@@ -95,12 +103,12 @@ class LocalComm:
         self.ranks = list(range(world))
 
     def halo(self, ts):
+        # ghost planes are written, interior planes read: no aliasing, no staging copies
         W = len(ts)
-        last = [t.select(-3, t.shape[-3] - 2).clone() for t in ts]
-        first = [t.select(-3, 1).clone() for t in ts]
         for i, t in enumerate(ts):
-            t.select(-3, 0).copy_(last[(i - 1) % W])
-            t.select(-3, t.shape[-3] - 1).copy_(first[(i + 1) % W])
+            left, right = ts[(i - 1) % W], ts[(i + 1) % W]
+            t.select(-3, 0).copy_(left.select(-3, left.shape[-3] - 2))
+            t.select(-3, t.shape[-3] - 1).copy_(right.select(-3, 1))
 
     def allreduce(self, vals):
         out = np.zeros_like(np.asarray(vals[0], dtype=np.float64))
@@ -111,6 +119,14 @@ class LocalComm:
     def gather(self, ts):
         import torch
         return torch.cat([t.narrow(-3, 1, t.shape[-3] - 2) for t in ts], dim=-3)
+
+    def allreduce_dev(self, vals):
+        """Sum of per-slab partial sums where they live (device tensors stay on the
+        device: no host round trip), in rank order."""
+        out = vals[0] + 0
+        for v in vals[1:]:
+            out = out + v
+        return out
 
 
 class DistComm:
@@ -152,6 +168,20 @@ class DistComm:
         if self.world > 1:
             self.dist.all_reduce(tt, op=self.dist.ReduceOp.SUM, group=self.group)
         return tt.cpu().numpy()
+
+    def allreduce_dev(self, vals):
+        """In-place all-reduce of this rank's partial sums: a CUDA tensor is reduced by
+        NCCL on the current stream (no host round trip); numpy goes through gloo."""
+        import torch
+        (v,) = vals
+        if isinstance(v, torch.Tensor):
+            if self.world > 1:
+                self.dist.all_reduce(v, op=self.dist.ReduceOp.SUM, group=self.group)
+            return v
+        t = torch.from_numpy(np.array(v, dtype=np.float64))
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        return t.numpy()
 
     def gather(self, ts):
         import torch
@@ -212,6 +242,50 @@ class CudaSlabBackend:
                                            self._p(f), self._p(dinv), float(omega), self._p(o1), self._p(o2),
                                            out if want_dots else None))
         return np.array(out[:]) if want_dots else None
+
+    # ---- device scalars (otm_slab_set_scalar_mode 1): PCG dots, beta, alpha stay on the device
+    def scalars(self, n):
+        return self.t.zeros(n, dtype=self.f64, device="cuda")
+
+    @staticmethod
+    def to_host(S):
+        return S.cpu().numpy()
+
+    @staticmethod
+    def put(S, i, v):
+        S[i:i + len(v)].copy_(v)
+
+    def pcg_step(self, stage, S):
+        self._sync_stream()
+        self._rc(self.lib.otm_slab_pcg_step(self.ws, int(stage), self._p(S)))
+
+    def _dev_call(self, fn, *args):
+        self.lib.otm_slab_set_scalar_mode(self.ws, 1)
+        try:
+            return fn(*args)
+        finally:
+            self.lib.otm_slab_set_scalar_mode(self.ws, 0)
+
+    def stencil_dev(self, op, dims, scale, kap, a, f, dinv, omega, o1, o2=None):
+        self._sync_stream()
+        out = self.t.empty(3, dtype=self.f64, device="cuda")
+        self._rc(self._dev_call(self.lib.otm_slab_stencil, self.ws, op, *dims, self._d3(scale), self._p(kap),
+                                self._p(a), self._p(f), self._p(dinv), float(omega), self._p(o1), self._p(o2),
+                                C.cast(C.c_void_p(out.data_ptr()), C.POINTER(C.c_double))))
+        return out
+
+    def pupd_dev(self, dims, z, p, beta):
+        self._sync_stream()
+        self._rc(self._dev_call(self.lib.otm_slab_pupd, self.ws, *dims, self._p(z), self._p(p),
+                                C.cast(C.c_void_p(beta.data_ptr()), C.POINTER(C.c_double))))
+
+    def upd_dev(self, dims, d, r, p, q, alpha):
+        self._sync_stream()
+        out = self.t.empty(3, dtype=self.f64, device="cuda")
+        self._rc(self._dev_call(self.lib.otm_slab_upd, self.ws, *dims, self._p(d), self._p(r), self._p(p), self._p(q),
+                                C.cast(C.c_void_p(alpha.data_ptr()), C.POINTER(C.c_double)),
+                                C.cast(C.c_void_p(out.data_ptr()), C.POINTER(C.c_double))))
+        return out
 
     def restrict(self, dims_f, res_f, f_c):
         self._sync_stream()
@@ -295,7 +369,7 @@ class CudaSlabBackend:
     # agglomerated coarse levels: the single-GPU hierarchy of that level
     def coarse_hierarchy(self, dims):
         from ._dev import Context
-        return Context(dims)
+        return Context(dims, jacobi_omega=1.25)     # its top level is a coarse level of the slab problem
 
     def coarse_build(self, ctx, kap_full32):
         k64 = kap_full32.to(self.f64).contiguous()
@@ -313,12 +387,15 @@ class _Lev:
 class SlabSolver:
     """Distributed solve_cases + effective tensor on x-slabs (homogenize.py:71-122)."""
 
-    def __init__(self, dims, comm, backend, kappa0=1.0, kappa_min=1e-4, penalty=3.0, omega=1.0,
-                 inner_reduction=1e-5, max_inner=40):
+    def __init__(self, dims, comm, backend, kappa0=1.0, kappa_min=1e-4, penalty=3.0, omega=0.95,
+                 omega_coarse=1.25, inner_reduction=1e-5, max_inner=40, tolf=0.85):
         self.L = SlabLayout.make(dims, comm.world)
         self.comm, self.B = comm, backend
         self.kappa0, self.kappa_min, self.penalty = kappa0, kappa_min, penalty
-        self.omega, self.inner_reduction, self.max_inner = omega, inner_reduction, max_inner
+        # the single-GPU solver's knobs (otm_api.cu): Jacobi 0.95 on level 0, 1.25 below,
+        # inner PCG target max(1e-5 ||r||, 0.85 tol ||f||)
+        self.omega, self.omega_coarse = omega, omega_coarse
+        self.inner_reduction, self.max_inner, self.tolf = inner_reduction, max_inner, tolf
         self.ranks = list(comm.ranks)
         B, L = backend, self.L
         f32, f64 = B.f32, B.f64
@@ -358,6 +435,18 @@ class SlabSolver:
         self.fmean = np.zeros(3)
 
     # ---- helpers
+    def _cidx(self, s, device):
+        """Planes of the agglomerated level (with ghosts) that slab s keeps, as an index
+        tensor on the field's device (built once)."""
+        idx = getattr(s, "cidx", None)
+        if idx is None:
+            import torch
+            cl, nxc = self.L.nxl(self.L.nlev_dist), self.L.chain[self.L.nlev_dist][0]
+            lo = s.rank * cl
+            idx = torch.tensor([(lo - 1 + i) % nxc for i in range(cl + 2)], dtype=torch.long, device=device)
+            s.cidx = idx
+        return idx
+
     def _halo(self, get):
         self.comm.halo([get(s) for s in self.slabs])
 
@@ -398,11 +487,12 @@ class SlabSolver:
 
     # ---- V-cycle on slabs (solver.py:206-215 with the damped-Jacobi smoother)
     def _vcycle(self):
-        B, L, om = self.B, self.L, self.omega
+        B, L = self.B, self.L
         nd = L.nlev_dist
         dots = [None] * len(self.slabs)
         for l in range(nd):
             self._halo(lambda s, l=l: s.levels[l].f)
+            om = self.omega if l == 0 else self.omega_coarse
             for s in self.slabs:
                 lv = s.levels[l]
                 B.stencil(0, lv.dims, L.scales[l], lv.kap, None, lv.f, lv.dinv, om, lv.z, lv.res)
@@ -416,30 +506,37 @@ class SlabSolver:
         z_full = B.zeros(tuple(f_full.shape), B.f32)
         B.coarse_vcycle(self.coarse, f_full, z_full)
         z_full.mul_(1.0 / self.coarse_scale)              # that hierarchy's level 0 carries scale 1
-        cl = self.L.nxl(nd)
-        nxc = self.L.chain[nd][0]
         for s in self.slabs:
-            lo = s.rank * cl
-            idx = [(lo - 1 + i) % nxc for i in range(cl + 2)]
-            s.cres.copy_(z_full[:, idx])
+            s.cres.copy_(z_full.index_select(1, self._cidx(s, z_full.device)))
         for l in range(nd - 1, -1, -1):
             for s in self.slabs:
                 lv = s.levels[l]
                 src = s.levels[l + 1].res if l + 1 < nd else s.cres
                 B.prolong(lv.dims, src, lv.z)
             self._halo(lambda s, l=l: s.levels[l].z)
+            om = self.omega if l == 0 else self.omega_coarse
             for s_i, s in enumerate(self.slabs):
                 lv = s.levels[l]
-                d = B.stencil(1, lv.dims, L.scales[l], lv.kap, lv.z, lv.f, lv.dinv, om, lv.res, None,
-                              want_dots=(l == 0))
                 if l == 0:
-                    dots[s_i] = d
+                    dots[s_i] = B.stencil_dev(1, lv.dims, L.scales[l], lv.kap, lv.z, lv.f, lv.dinv, om, lv.res)
+                else:
+                    B.stencil(1, lv.dims, L.scales[l], lv.kap, lv.z, lv.f, lv.dinv, om, lv.res, None)
             if l > 0:
                 self._halo(lambda s, l=l: s.levels[l].res)
-        return self._sum(dots)                            # r . z per case
+        return self._pcg_dots(dots)                       # r . z per case (device)
 
     # ---- solve (solver.py:366-406 semantics, fp64 defect correction)
-    def solve(self, tol=1e-6, max_vcycles=200):
+    def _pcg_dots(self, vals):
+        """All-reduced partial sums, left where they live (device for the CUDA backend)."""
+        return self.comm.allreduce_dev(vals)
+
+    def solve(self, tol=1e-6, max_vcycles=200, check_every=4):
+        """The batched MG-PCG with the PCG scalars on the device: dots are all-reduced in
+        device memory and the recurrences run in a one-thread kernel
+        (otm_slab_pcg_step), so an inner iteration has no host round trip; the host
+        reads the active flags every `check_every` iterations (iterations after a case
+        converged apply alpha = 0 to it: no effect).  Every load case has its own budget
+        of `max_vcycles` preconditioner applications (homogenize.py:85-90)."""
         B, L = self.B, self.L
         d0 = self.slabs[0].levels[0].dims
         sc0 = L.scales[0]
@@ -447,7 +544,7 @@ class SlabSolver:
         if not self.warm:
             for s in self.slabs:
                 s.T.zero_()
-        cycles = 0
+        ccyc = np.zeros(3)
 
         def residual():
             self._halo(lambda s: s.T)
@@ -460,31 +557,54 @@ class SlabSolver:
 
         rel, fn, rn = residual()
         done = (fn == 0) | (rel <= tol)
+        if getattr(self, "_S", None) is None:
+            self._S = B.scalars(28)
+        S = self._S
+
+        def one_iteration():
+            rz = self._vcycle()
+            B.put(S, 0, rz)
+            B.pcg_step(0, S)
+            for s in self.slabs:
+                B.pupd_dev(d0, s.levels[0].res, s.p, S[6:9])
+            self._halo(lambda s: s.p)
+            pq = self._pcg_dots([B.stencil_dev(2, d0, sc0, s.levels[0].kap, s.p, None, None, 0.0, s.q)
+                                 for s in self.slabs])
+            B.put(S, 9, pq)
+            B.pcg_step(1, S)
+            rr = self._pcg_dots([B.upd_dev(d0, s.d, s.levels[0].f, s.p, s.q, S[12:15]) for s in self.slabs])
+            B.put(S, 15, rr)
+            B.pcg_step(2, S)
+
         while not done.all():
-            if cycles >= max_vcycles:
+            if ((~done) & (ccyc >= max_vcycles)).any():
                 from ._dev import ConvergenceError
-                raise ConvergenceError(f"slab solve did not converge in {max_vcycles} cycles", float(rel.max()))
-            target2 = np.maximum(self.inner_reduction * rn, 0.5 * tol * fn) ** 2
-            active = ~done
+                raise ConvergenceError(f"slab solve did not converge in {max_vcycles} V-cycles per case",
+                                       float(rel.max()))
+            init = np.zeros(28)
+            init[18:21] = np.maximum(self.inner_reduction * rn, self.tolf * tol * fn) ** 2
+            init[21:24] = (~done).astype(np.float64)
+            init[24] = 1.0
+            init[25:28] = ccyc
+            B.put(S, 0, init if not hasattr(S, "copy_") else B.t.from_numpy(init).to(S.device))
             for s in self.slabs:
                 s.d.zero_()
                 s.p.zero_()
-            rz_old = None
             for it in range(self.max_inner):
-                rz = self._vcycle()
-                beta = np.zeros(3) if rz_old is None else np.where(rz_old != 0, rz / np.where(rz_old != 0, rz_old, 1), 0)
-                rz_old = rz
-                for s in self.slabs:
-                    B.pupd(d0, s.levels[0].res, s.p, beta)
-                self._halo(lambda s: s.p)
-                pq = self._sum([B.stencil(2, d0, sc0, s.levels[0].kap, s.p, None, None, 0.0, s.q, None,
-                                          want_dots=True) for s in self.slabs])
-                alpha = np.where(active & (pq > 0), rz / np.where(pq > 0, pq, 1), 0.0)
-                rr = self._sum([B.upd(d0, s.d, s.levels[0].f, s.p, s.q, alpha) for s in self.slabs])
-                cycles += int(active.sum())
-                active = active & (rr > target2)
-                if not active.any() or cycles >= max_vcycles:
-                    break
+                g = self._pcg_graph
+                if g is not None:
+                    g.replay()
+                else:
+                    one_iteration()
+                    if self._graph_ok and it == 0:
+                        self._capture(one_iteration)
+                if (it + 1) % check_every == 0 or it + 1 == self.max_inner:
+                    h = B.to_host(S)
+                    active = h[21:24] != 0
+                    if not active.any() or (active & (h[25:28] >= max_vcycles)).any():
+                        break
+            h = B.to_host(S)
+            ccyc = h[25:28].copy()
             for s in self.slabs:
                 B.tupd(d0, s.T, s.d, np.zeros(3))
             rel, fn, rn = residual()
@@ -494,8 +614,37 @@ class SlabSolver:
         for s in self.slabs:
             B.tupd(d0, s.T, None, mean)
         self.warm = True
-        self.cycles = cycles
-        return cycles
+        self.cycles = int(ccyc.sum())
+        return self.cycles
+
+    # one inner PCG iteration as a CUDA graph (the per-call host overhead of the slab
+    # orchestration -- ~60 small launches per iteration issued from Python -- exceeded
+    # the GPU time at 256^3); in-process slabs only, unless OTM_SLAB_GRAPH=1 (NCCL
+    # collectives inside a captured graph are untested on this single-GPU project)
+    _pcg_graph = None
+
+    @property
+    def _graph_ok(self):
+        import os
+        if getattr(self, "_graph_failed", False) or not hasattr(self.B, "pcg_step") or self.B.device != "cuda":
+            return False
+        if isinstance(self.comm, LocalComm):
+            return os.environ.get("OTM_SLAB_GRAPH", "1") != "0"
+        return os.environ.get("OTM_SLAB_GRAPH") == "1"
+
+    def _capture(self, fn):
+        import torch
+        try:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            torch.cuda.synchronize()
+            self._pcg_graph = g
+        except Exception:                     # stay on the eager loop for this solver
+            self._graph_failed = True
+            self._pcg_graph = None
+            torch.cuda.synchronize()
 
     def tensor(self):
         """kappa_H (homogenize.py:103-122): all-reduced element-energy sums / N."""
@@ -531,8 +680,17 @@ class SlabDesignRun:
         self.comm, self.B = comm, backend
         mp = config.material
         self.material = (mp.kappa0, mp.kappa_min, mp.penalty)
-        self.solver = SlabSolver(config.dims, comm, backend, kappa0=mp.kappa0, kappa_min=mp.kappa_min,
-                                 penalty=mp.penalty)
+        # one solver (slab buffers, captured PCG graph) per grid and transport, reused by
+        # later runs; every run starts cold
+        cache = backend.__dict__.setdefault("_solvers", {})
+        key = (tuple(config.dims), comm.world, tuple(comm.ranks), mp.kappa0, mp.kappa_min, mp.penalty, id(comm))
+        self.solver = cache.get(key)
+        if self.solver is None:
+            cache.clear()
+            self.solver = SlabSolver(config.dims, comm, backend, kappa0=mp.kappa0, kappa_min=mp.kappa_min,
+                                     penalty=mp.penalty)
+            cache[key] = self.solver
+        self.solver.warm = False
         self.n = self.solver.n_total
         self.lib = _lib.load()
         self.cc = _lib.RunConfigC()

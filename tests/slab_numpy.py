@@ -107,6 +107,45 @@ class NumpySlabBackend:
             self._w(o2, np.stack(outs2))
         return dots if want_dots else None
 
+    # device-scalar protocol of slab.py (here plain numpy arrays)
+    @staticmethod
+    def scalars(n):
+        return np.zeros(n)
+
+    @staticmethod
+    def to_host(S):
+        return np.asarray(S)
+
+    @staticmethod
+    def put(S, i, v):
+        v = np.asarray(v, dtype=np.float64).ravel()
+        S[i:i + len(v)] = v
+
+    @staticmethod
+    def pcg_step(stage, S):
+        """include/otm_slab.h otm_slab_pcg_step, restated."""
+        for c in range(3):
+            if stage == 0:
+                S[6 + c] = 0.0 if S[24] != 0 else (S[c] / S[3 + c] if S[3 + c] != 0 else 0.0)
+                S[3 + c] = S[c]
+            elif stage == 1:
+                S[12 + c] = S[c] / S[9 + c] if (S[21 + c] != 0 and S[9 + c] > 0) else 0.0
+            else:
+                S[25 + c] += S[21 + c]
+                if not (S[15 + c] > S[18 + c]):
+                    S[21 + c] = 0.0
+        if stage == 0:
+            S[24] = 0.0
+
+    def stencil_dev(self, op, dims, scale, kap, a, f, dinv, omega, o1, o2=None):
+        return self.stencil(op, dims, scale, kap, a, f, dinv, omega, o1, o2, want_dots=True)
+
+    def pupd_dev(self, dims, z, p, beta):
+        return self.pupd(dims, z, p, np.asarray(beta))
+
+    def upd_dev(self, dims, d, r, p, q, alpha):
+        return self.upd(dims, d, r, p, q, np.asarray(alpha))
+
     def restrict(self, dims_f, res_f, f_c):
         R = self._n(res_f)                          # (3, nxl+2, ny, nz)
         nxl = dims_f[0]
