@@ -1456,20 +1456,27 @@ __global__ void __launch_bounds__(256) k_tensor_x(Geo g, int chunks, const doubl
     MarchCol q;
     int x0, x1;
     if (march_setup(g, chunks, q, x0, x1)) {
-        double A[3][4], B[3][4];
+        // planes x and x + 1 in registers, plane x + 2 prefetched while x is consumed
+        double A[3][4], B[3][4], Cn[3][4];
         load_plane(T, g.n, (unsigned)x0 * (unsigned)g.pl, q, A);
+        load_plane(T, g.n, (unsigned)(x0 + 1 == g.nx ? 0 : x0 + 1) * (unsigned)g.pl, q, B);
         for (int x = x0; x < x1; ++x) {
-            const unsigned pb = (unsigned)(x + 1 == g.nx ? 0 : x + 1) * (unsigned)g.pl;
-            load_plane(T, g.n, pb, q, B);
+            if (x + 1 < x1) {
+                const int xn = x + 2 >= g.nx ? x + 2 - g.nx : x + 2;
+                load_plane(T, g.n, (unsigned)xn * (unsigned)g.pl, q, Cn);
+            }
+            const double k = __ldg(kap + (unsigned)x * (unsigned)g.pl + q.o00);
             double E[6];
             energies_wht(A, B, E);
-            const double k = __ldg(kap + (unsigned)x * (unsigned)g.pl + q.o00);
 #pragma unroll
             for (int c = 0; c < 6; ++c) acc[c] = fma(k, E[c], acc[c]);
 #pragma unroll
             for (int i = 0; i < 3; ++i)
 #pragma unroll
-                for (int s = 0; s < 4; ++s) A[i][s] = B[i][s];
+                for (int s = 0; s < 4; ++s) {
+                    A[i][s] = B[i][s];
+                    B[i][s] = Cn[i][s];
+                }
         }
     }
     if (reduce_finalize<6>(acc, partials, counter, out)) {
@@ -1484,23 +1491,30 @@ __global__ void __launch_bounds__(256) k_sens_x(Geo g, int chunks, const double*
     int x0, x1;
     if (!march_setup(g, chunks, q, x0, x1)) return;
     if (dG_dev) dG = *dG_dev;               // objective weights computed on the device (otm_loop.cu)
-    double A[3][4], B[3][4];
+    double A[3][4], B[3][4], Cn[3][4];
     load_plane(T, g.n, (unsigned)x0 * (unsigned)g.pl, q, A);
+    load_plane(T, g.n, (unsigned)(x0 + 1 == g.nx ? 0 : x0 + 1) * (unsigned)g.pl, q, B);
     const double scale = (sp.k0 - sp.kmin) * sp.p / (double)g.n;
     for (int x = x0; x < x1; ++x) {
-        const unsigned pb = (unsigned)(x + 1 == g.nx ? 0 : x + 1) * (unsigned)g.pl;
-        load_plane(T, g.n, pb, q, B);
+        if (x + 1 < x1) {
+            const int xn = x + 2 >= g.nx ? x + 2 - g.nx : x + 2;
+            load_plane(T, g.n, (unsigned)xn * (unsigned)g.pl, q, Cn);
+        }
+        const unsigned e = (unsigned)x * (unsigned)g.pl + q.o00;
+        const double rfe = __ldg(rf + e);
         double E[6];
         energies_wht(A, B, E);
         double con = 0.0;
 #pragma unroll
         for (int c = 0; c < 6; ++c) con = fma(dG.v[c], E[c], con);
-        const unsigned e = (unsigned)x * (unsigned)g.pl + q.o00;
-        sens[e] = simp_pow(__ldg(rf + e), sp.p - 1.0) * scale * con;
+        sens[e] = simp_pow(rfe, sp.p - 1.0) * scale * con;
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
-            for (int s = 0; s < 4; ++s) A[i][s] = B[i][s];
+            for (int s = 0; s < 4; ++s) {
+                A[i][s] = B[i][s];
+                B[i][s] = Cn[i][s];
+            }
     }
 }
 
@@ -2272,6 +2286,13 @@ static bool k10_maps(K10Maps& M, const Geo& g, const float* op3, const float* d,
     return ok;
 }
 static int g_k10_nxr = 0;            // output plane count of the launch being issued (0: all nx)
+// Lockstep tile order: CTA b takes row tile b % nty and x chunk b / nty, so the CTAs
+// resident together cover contiguous bands of row tiles marching the same x planes
+// and a tile's y-halo rows -- its neighbours' main rows -- are read from L2, not HBM
+// (ncu at 256^3 / 512^3 with contiguous x ranges: 1.38x / 1.40x the algorithmic DRAM
+// bytes).  One CTA per (tile, chunk); chunks of >= 8 planes.  OTM_K10_LOCK=0: the
+// contiguous per-CTA ranges of round 1.
+static int g_k10_lock = 0;
 template <class K>
 static dim3 k10_grid(K kernel, size_t smem, const Geo& g, int TY) {
     int dev = 0, sms = 148, per_sm = 1;
@@ -2279,8 +2300,22 @@ static dim3 k10_grid(K kernel, size_t smem, const Geo& g, int TY) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, g.nz / 2 * TY, smem);
     if (per_sm < 1) per_sm = 1;
-    const long long units = (long long)(g.ny / TY) * (g_k10_nxr > 0 ? g_k10_nxr : g.nx);
-    long long b = (long long)per_sm * sms;
+    const int nxr = g_k10_nxr > 0 ? g_k10_nxr : g.nx;
+    const long long nty = g.ny / TY;
+    const long long units = nty * nxr;
+    const long long slots = (long long)per_sm * sms;
+    static const bool lock_on = !(getenv("OTM_K10_LOCK") && atoi(getenv("OTM_K10_LOCK")) == 0);
+    g_k10_lock = 0;
+    // only where a 3-case field (12 B per vertex) no longer fits half of the 126 MB L2:
+    // below that the halo rows are L2 hits in any order and the contiguous ranges keep
+    // every SM busy
+    if (lock_on && (long long)g.nz * g.ny * nxr * 12 > (64LL << 20)) {
+        long long k = std::max<long long>(1, slots / nty);
+        k = std::min<long long>(k, std::max(1, nxr / 8));
+        g_k10_lock = (int)k;
+        return dim3((unsigned)(nty * k), 1, 1);
+    }
+    long long b = slots;
     if (b > units) b = units;
     return dim3((unsigned)b, 1, 1);
 }
@@ -2289,24 +2324,31 @@ static void l10_smooth_res(cudaStream_t s, const Geo& g, float s12, const K10Map
                            float* res) {
     const size_t sm = K10Geo<K10_SMOOTH, NZ, TY, CPS>::SMEM;
     smem_attr(k10_smooth_res<NZ, TY, CPS, WZ>, sm);
-    launch_pdl(k10_smooth_res<NZ, TY, CPS, WZ>, k10_grid(k10_smooth_res<NZ, TY, CPS, WZ>, sm, g, TY),
-               dim3(NZ / 2, TY), sm, s, g, s12, M, omega, z, res);
+    const dim3 grid = k10_grid(k10_smooth_res<NZ, TY, CPS, WZ>, sm, g, TY);
+    K10Maps Ml = M;
+    Ml.lock = g_k10_lock;
+    launch_pdl(k10_smooth_res<NZ, TY, CPS, WZ>, grid, dim3(NZ / 2, TY), sm, s, g, s12, Ml, omega, z, res);
 }
 template <bool DOT, int NZ, int TY, int CPS>
 static void l10_jacobi(cudaStream_t s, const Geo& g, float s12, const K10Maps& M, float omega, float* zout,
                        double* partials, unsigned* counter, PcgScalars* sc) {
     const size_t sm = K10Geo<K10_JACOBI, NZ, TY, CPS>::SMEM;
     smem_attr(k10_jacobi<DOT, NZ, TY, CPS>, sm);
-    launch_pdl(k10_jacobi<DOT, NZ, TY, CPS>, k10_grid(k10_jacobi<DOT, NZ, TY, CPS>, sm, g, TY), dim3(NZ / 2, TY),
-               sm, s, g, s12, M, omega, zout, partials, counter, sc);
+    const dim3 grid = k10_grid(k10_jacobi<DOT, NZ, TY, CPS>, sm, g, TY);
+    K10Maps Ml = M;
+    Ml.lock = g_k10_lock;
+    launch_pdl(k10_jacobi<DOT, NZ, TY, CPS>, grid, dim3(NZ / 2, TY), sm, s, g, s12, Ml, omega, zout, partials,
+               counter, sc);
 }
 template <int NZ, int TY, int CPS>
 static void l10_spmv(cudaStream_t s, const Geo& g, float s12, const K10Maps& M, float* q, Red& red,
                      PcgScalars* sc) {
     const size_t sm = K10Geo<K10_SPMV, NZ, TY, CPS>::SMEM;
     smem_attr(k10_spmv<NZ, TY, CPS>, sm);
-    launch_pdl(k10_spmv<NZ, TY, CPS>, k10_grid(k10_spmv<NZ, TY, CPS>, sm, g, TY), dim3(NZ / 2, TY), sm, s, g, s12,
-               M, q, red.partials, red.counter, sc);
+    const dim3 grid = k10_grid(k10_spmv<NZ, TY, CPS>, sm, g, TY);
+    K10Maps Ml = M;
+    Ml.lock = g_k10_lock;
+    launch_pdl(k10_spmv<NZ, TY, CPS>, grid, dim3(NZ / 2, TY), sm, s, g, s12, Ml, q, red.partials, red.counter, sc);
 }
 // tile rows per CTA (OTM_K10_TY: 2/4/8 at nz = 128, tuning) and CTAs per SM
 #define OTM_K10_SWITCH(CALL)                                                   \

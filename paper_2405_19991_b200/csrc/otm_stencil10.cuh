@@ -34,6 +34,9 @@ struct K10Maps {
     CUtensorMap d_full, d_main, d_halo;      // 3-D (z, y, x) D^-1: TY+2 / TY / 1 rows
     CUtensorMap f_full, f_main, f_halo;      // 4-D right-hand side: TY+2 / TY / 1 rows
     CUtensorMap k_full, k_main, k_halo;      // 3-D factors: TY+1 / TY / 1 rows
+    int lock;                                // > 0: CTA b owns row tile b % nty, x chunk b / nty of `lock`
+                                             // chunks (row-tile neighbours march the same planes at the
+                                             // same time, so y-halo rows hit L2); 0: contiguous ranges
     int xa, xb;                              // output x planes [xa, xb): [0, nx) periodic, or a slab's
                                              // interior [1, nxl + 1) between its ghost planes
 };
@@ -272,8 +275,15 @@ __device__ __forceinline__ void march10(const Geo& g, float s12f, const K10Maps&
     const int nty = g.ny / TY;
     const int nxr = maps.xb - maps.xa;
     const long long W = (long long)nty * nxr;
-    long long u = W * blockIdx.x / gridDim.x;
-    const long long u1 = W * (blockIdx.x + 1) / gridDim.x;
+    long long u, u1;
+    if (maps.lock > 0) {
+        const int yt = (int)(blockIdx.x % (unsigned)nty), c = (int)(blockIdx.x / (unsigned)nty);
+        u = (long long)yt * nxr + (long long)nxr * c / maps.lock;
+        u1 = (long long)yt * nxr + (long long)nxr * (c + 1) / maps.lock;
+    } else {
+        u = W * blockIdx.x / gridDim.x;
+        u1 = W * (blockIdx.x + 1) / gridDim.x;
+    }
     int kc = 0;                                  // ring slot of the next plane to land
     int ki = 0;                                  // ring slot of the next plane to issue
     while (u < u1) {
