@@ -2170,7 +2170,17 @@ void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const d
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             const long long units = 3LL * (g.ny / tyd) * g.nx;
             static const int bps = getenv("OTM_R64_BPS") ? atoi(getenv("OTM_R64_BPS")) : 2;
-            const unsigned blocks = (unsigned)std::min<long long>((long long)sms * (g.nz > 256 ? 1 : bps), units);
+            const long long slots = (long long)sms * (g.nz > 256 ? 1 : bps);
+            unsigned blocks = (unsigned)std::min<long long>(slots, units);
+            // lockstep row order beyond L2 (T, one 8-byte case per vertex, > 64 MB)
+            static const bool lock_on = !(getenv("OTM_K10_LOCK") && atoi(getenv("OTM_K10_LOCK")) == 0);
+            M.lock = 0;
+            if (lock_on && g.n * 8 > (64LL << 20)) {
+                const long long rows = 3LL * (g.ny / tyd);
+                const long long k = std::max<long long>(1, std::min<long long>((4 * slots + rows / 2) / rows, g.nx / 8));
+                M.lock = (int)k;
+                blocks = (unsigned)(rows * k);
+            }
             const dim3 blk((unsigned)g.nz, (unsigned)tyd);
             switch (g.nz) {
             case 512:

@@ -38,6 +38,10 @@ __host__ __device__ inline size_t r64_smem_bytes(int nz) {
 struct R64Maps {
     CUtensorMap Tm, Th;      // T (3 cases stacked along x): main (TYD rows) / halo (1 row)
     CUtensorMap Km, Kh;      // kappa (fp64)
+    int lock;                // > 0: CTA b owns (case, row tile) b % (3 nty) and x chunk b / (3 nty) of
+                             // `lock`: row-tile neighbours march the same planes together, so the halo
+                             // rows hit L2 (contiguous ranges re-read them from HBM: 3.0x the
+                             // algorithmic bytes at 512^3 with one-row tiles)
 };
 
 // nz = 512: 512 threads, 1 CTA per SM, and z-split (256, 2) maps (a TMA box
@@ -83,8 +87,16 @@ __global__ void __launch_bounds__(R64Geo<NZ>::THREADS, R64Geo<NZ>::MINB) k_res64
     const int nty = g.ny / TYD;
     const long long W = 3LL * nty * g.nx;
     const long long B = gridDim.x;
-    long long u = W * blockIdx.x / B;
-    const long long u1 = W * (blockIdx.x + 1) / B;
+    long long u, u1;
+    if (maps.lock > 0) {
+        const unsigned rows = 3u * (unsigned)nty;
+        const long long p = blockIdx.x % rows, ch = blockIdx.x / rows;
+        u = p * g.nx + (long long)g.nx * ch / maps.lock;
+        u1 = p * g.nx + (long long)g.nx * (ch + 1) / maps.lock;
+    } else {
+        u = W * blockIdx.x / B;
+        u1 = W * (blockIdx.x + 1) / B;
+    }
     double acc[9];
 #pragma unroll
     for (int i = 0; i < 9; ++i) acc[i] = 0.0;

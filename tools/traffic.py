@@ -19,7 +19,8 @@ rep, cfg, nx = sys.argv[1], sys.argv[2], int(sys.argv[3])
 n = nx ** 3
 ALG = {"k10_smooth_res": 44, "k10_jacobi": 44, "k10_spmv": 28, "k_res64w": 44,
        "k_tensor_x": 32, "k_sens_x": 40, "k_filter_b<2>": 28, "k_filter_b<1>": 16}
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--print-units", "base"], capture_output=True,
+                     text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h = rows[0]
 per, times = {}, {}
@@ -36,20 +37,12 @@ for row in rows[2:]:
         m = re.search(r"(k_tensor_x|k_sens_x|k_filter_b<[12]>)", name)
         if not m:
             continue
-    b = float(row[h.index("dram__bytes_read.sum")]) + float(row[h.index("dram__bytes_write.sum")])
+    num = lambda c: float(row[h.index(c)].replace(",", ""))          # base units (bytes, ns)
+    b = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
     unit = 1.0
-    u = rows[1][h.index("dram__bytes_read.sum")]
-    if u.strip().lower().startswith("mbyte"):
-        unit = 1e6
-    elif u.strip().lower().startswith("gbyte"):
-        unit = 1e9
-    elif u.strip().lower().startswith("kbyte"):
-        unit = 1e3
     key = f"{m.group(1)}<{m.group(2)}>" if m.lastindex and m.lastindex >= 2 else m.group(1)
     per.setdefault(key, []).append(b * unit)
-    t = float(row[h.index("gpu__time_duration.sum")])
-    tu = rows[1][h.index("gpu__time_duration.sum")].strip().lower()
-    times.setdefault(key, []).append(t * (1e-3 if tu.startswith("ns") else (1.0 if tu.startswith("us") else 1e3)))
+    times.setdefault(key, []).append(num("gpu__time_duration.sum") * 1e-3)
 out = {"source": f"ncu --set full --clock-control none of the finest-level kernels of {cfg} ({nx}^3), {rep}",
        "per_launch_dram_bytes": {k: statistics.mean(v) for k, v in per.items()},
        "per_launch_algorithmic_bytes": {k: ALG.get(k, ALG.get(k.split("<")[0], 0)) * n for k in per},
