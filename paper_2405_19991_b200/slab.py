@@ -34,7 +34,15 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .parallel import level_dims
+
+
+def level_dims(dims, coarse_target: int = 64):
+    """The reference level chain (solver.py:217-231): halve every axis > 1 while the
+    level has more than coarse_target vertices and those axes are even."""
+    chain = [tuple(int(n) for n in dims)]
+    while int(np.prod(chain[-1])) > coarse_target and all(n % 2 == 0 for n in chain[-1] if n > 1):
+        chain.append(tuple(n // 2 if n > 1 else 1 for n in chain[-1]))
+    return chain
 
 
 # --------------------------------------------------------------------------- geometry

@@ -12,8 +12,14 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2405_19991_b200.parallel import (SlabPlan, allreduce_sum, gather_level, halo_exchange, level_dims,
-                                            owned_part, with_ghosts)
+from paper_2405_19991_b200.slab import DistComm, LocalComm, SlabLayout, level_dims
+
+
+def _ghosted(local):
+    """(nxl, ...) -> (nxl + 2, ...) with empty ghost planes."""
+    out = torch.zeros((local.shape[0] + 2,) + tuple(local.shape[1:]), dtype=local.dtype)
+    out[1:-1] = local
+    return out
 
 
 def _free_port():
@@ -34,12 +40,14 @@ def _worker(rank, world, port, dims, seed, q):
         kap = rng.uniform(1e-4, 1.0, dims)
         T = rng.standard_normal(dims)
         rho = rng.uniform(0.0, 1.0, dims)
-        plan = SlabPlan(dims, world, rank)
-        lev = plan.levels[0]
-        # each rank only ever sees its own slab; ghosts come from the exchange
-        kap_p = halo_exchange(with_ghosts(torch.from_numpy(kap[lev.x0:lev.x1].copy())), plan).numpy()
-        T_p = halo_exchange(with_ghosts(torch.from_numpy(T[lev.x0:lev.x1].copy())), plan).numpy()
-        rho_p = halo_exchange(with_ghosts(torch.from_numpy(rho[lev.x0:lev.x1].copy())), plan).numpy()
+        comm = DistComm()
+        nxl = dims[0] // world
+        x0, x1 = rank * nxl, (rank + 1) * nxl
+        # each rank only ever sees its own slab; ghosts come from the exchange (slab.py)
+        pads = [_ghosted(torch.from_numpy(a[x0:x1].copy())) for a in (kap, T, rho)]
+        for p in pads:
+            comm.halo([p])
+        kap_p, T_p, rho_p = (p.numpy() for p in pads)
         # operator and loads on the padded slab (the oracle wraps x periodically, which only
         # touches the ghost planes whose results are discarded)
         hp = O.Hierarchy(kap_p.shape, coarse_target=10 ** 9)
@@ -47,9 +55,13 @@ def _worker(rank, world, port, dims, seed, q):
         KT_local = hp.levels[0].apply(T_p)[1:-1]
         f_local = np.stack([O.macro_load(hp, i)[1:-1] for i in range(3)])
         filt_local = O.filter_fwd(rho_p)[1:-1]
-        # a global scalar: sum of kappa * (K T) over owned vertices, all-reduced
-        s = allreduce_sum(torch.tensor([float((kap[lev.x0:lev.x1] * KT_local).sum())], dtype=torch.float64))
-        full_KT = gather_level(torch.from_numpy(np.ascontiguousarray(KT_local)), plan).numpy()
+        # a global scalar: sum of kappa * (K T) over owned vertices, all-reduced (host and
+        # device-scalar protocols)
+        s = comm.allreduce([np.array([float((kap[x0:x1] * KT_local).sum())])])
+        s2 = comm.allreduce_dev([np.array([float((kap[x0:x1] * KT_local).sum())])])
+        assert s[0] == s2[0]
+        full_KT = comm.gather([_ghosted(torch.from_numpy(np.ascontiguousarray(KT_local)))]).numpy()
+        lev = type("L", (), {"x0": x0, "x1": x1})
         q.put((rank, KT_local, f_local, filt_local, float(s[0]), full_KT, (lev.x0, lev.x1)))
     finally:
         dist.destroy_process_group()
@@ -91,25 +103,21 @@ def test_slab_exchange_reproduces_single_domain(world, dims):
         assert np.abs(full_KT - KT).max() <= 1e-13 * np.abs(KT).max()
 
 
-def test_plan_levels_and_agglomeration():
-    p = SlabPlan((256, 256, 256), 8, 3)
-    dims = [l.dims for l in p.levels]
-    assert dims == level_dims((256, 256, 256))
+def test_layout_levels_and_agglomeration():
+    L = SlabLayout.make((256, 256, 256), 8, min_local=0)
+    assert list(L.chain) == level_dims((256, 256, 256))
     # 256/8 = 32 planes at level 0 ... 2 planes at 16^3, then agglomerate at 8^3
-    assert [l.distributed for l in p.levels] == [True, True, True, True, True, False, False]
-    assert p.levels[0].x0 == 96 and p.levels[0].x1 == 128
-    assert p.levels[3].x0 == 12 and p.levels[3].x1 == 16
-    assert p.agglomeration_level == 5
-    # weak-scaling shape of BASELINE config 5 on 8 GPUs
-    p5 = SlabPlan((512, 512, 512), 8, 0)
-    assert p5.levels[0].nx_local == 64 and p5.agglomeration_level == 6
+    assert L.nlev_dist == 5 and L.nxl(0) == 32 and L.nxl(3) == 4
+    # weak-scaling shape of BASELINE config 5 on 8 GPUs: 64 planes per rank at level 0
+    L5 = SlabLayout.make((512, 512, 512), 8)
+    assert L5.nxl(0) == 64 and L5.chain[L5.nlev_dist] == (64, 64, 64)
     with pytest.raises(ValueError):
-        SlabPlan((6, 6, 6), 4, 0)
+        SlabLayout.make((6, 6, 6), 4)
 
 
-def test_owned_part_single_rank():
-    plan = SlabPlan((8, 4, 4), 1, 0)
+def test_in_process_exchange_single_slab():
     full = torch.arange(8 * 16, dtype=torch.float64).reshape(8, 4, 4)
-    assert torch.equal(owned_part(full, plan), full)
-    pad = halo_exchange(with_ghosts(full), plan)
+    pad = _ghosted(full)
+    LocalComm(1).halo([pad])
     assert torch.equal(pad[0], full[-1]) and torch.equal(pad[-1], full[0])
+    assert torch.equal(LocalComm(1).gather([pad]), full)
