@@ -1,5 +1,8 @@
 """Run N design iterations of c3 through DesignRun (for ncu launch lists of the
-steady state: skip the first iterations' launches with --launch-skip)."""
+steady state: skip the first iterations' launches with --launch-skip).
+
+    python tools/profile_run.py ITERS [CONFIG] [graph]
+"""
 import os
 import sys
 
@@ -17,8 +20,11 @@ dims = bench.CONFIGS[cfg_name]["dims"]
 seed = otm.init_density(dims, otm.InitPattern("iwp", bench.CONFIGS[cfg_name]["vf"], seed=0)).rho
 cfg = bench.make_config(otm, cfg_name, iters, 0.0, init_field=seed)
 run = DesignRun(cfg)
-while not run.finished:
-    run.step()
+if len(sys.argv) > 3 and sys.argv[3] == "graph":
+    run.run()                                   # device-resident iteration graph
+else:
+    while not run.finished:
+        run.step()
 torch.cuda.synchronize()
 lib = run.hier.ctx.lib
 print("launches", lib.otm_launch_count(run.hier.ctx.h), "iterations", len(run.log),
