@@ -342,6 +342,14 @@ def run_gpu(args):
                     "pcg_iterations_per_oc_iteration": st[2] / max(st[0], 1),
                     "vcycles_per_oc_iteration": sum(r.vcycles for r in run.log) / max(len(run.log), 1),
                     "oc_passes_per_update": st[4] / max(st[3], 1), "frozen_retries": st[5]}
+    ph = (C.c_double * 4)()
+    lib.otm_loop_phases(ctx.h, ph)
+    n_it = max(sum(iters_done), 1)
+    if ph[0] > 0:
+        solver_stats["iteration_phases_us"] = {
+            "filter_build_solve": round(ph[0] * 1e3 / n_it, 1), "tensor_objective": round(ph[1] * 1e3 / n_it, 1),
+            "sens_filter_oc": round(ph[2] * 1e3 / n_it, 1), "gap": round(ph[3] * 1e3 / n_it, 1),
+            "note": "graph path, %globaltimer stamps of the loop-control kernels, mean per OC iteration"}
     # max over ranks
     t_max = total_ms
     if world > 1:

@@ -246,6 +246,12 @@ long long otm_launch_count(const otm_ctx* ctx);
 int otm_stats(const otm_ctx* ctx, long long out[6]);
 int otm_stats_reset(otm_ctx* ctx);
 
+/* Device time of the phases of the graph-path design iterations since the last
+ * otm_stats_reset (%globaltimer stamps written by the loop-control kernels), ms:
+ * [0] filter + hierarchy build + solve, [1] tensor + objective / governor,
+ * [2] sensitivities + adjoint filter + OC step, [3] gaps between iterations. */
+int otm_loop_phases(const otm_ctx* ctx, double ms[4]);
+
 #ifdef __cplusplus
 }
 #endif

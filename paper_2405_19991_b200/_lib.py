@@ -108,6 +108,7 @@ _SIGS = {
     "otm_launch_count": (C.c_longlong, [C.c_void_p]),
     "otm_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong)]),
     "otm_stats_reset": (C.c_int, [C.c_void_p]),
+    "otm_loop_phases": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "otm_vcycle": (C.c_int, [C.c_void_p, dptr, dptr]),
     # include/otm_slab.h: slab-decomposed solve pieces (multi-GPU)
     "otm_slab_create": (C.c_void_p, [C.c_longlong]),

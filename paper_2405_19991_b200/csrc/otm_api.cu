@@ -66,6 +66,7 @@ struct otm_ctx {
     SimpParams sp{};
     double* kap64 = nullptr;
     double* T64 = nullptr;
+    double* oc_q = nullptr;                   // k_oc_coop: per-element c_e of the current search
     double* rho_f = nullptr;   // last filtered density used by otm_build (for sensitivities)
     double* sensf = nullptr;   // design-loop scratch: sensitivity wrt rho_f, then wrt rho
     double* sens = nullptr;
@@ -105,6 +106,7 @@ struct otm_ctx {
     size_t bytes = 0;
     long long launches = 0;
     long long stat_inner = 0, stat_outer = 0, stat_solves = 0, stat_oc = 0, stat_oc_passes = 0, stat_oc_retry = 0;
+    double stat_phase_ms[4] = {0, 0, 0, 0};      // graph-path iteration phases (otm_loop_phases)
     // inner-iteration graphs (plain, profiled)
     cudaGraphExec_t gexec = nullptr;
     cudaGraphExec_t gexec_prof = nullptr;
@@ -698,6 +700,7 @@ int otm_create(otm_ctx** out, int nx, int ny, int nz, const otm_params* pin) {
     CK(dalloc(ctx, &ctx->gj, 2 * (size_t)ctx->nc * ctx->nc + ctx->nc + 2));
     const size_t mb = max_blocks(ctx);
     CK(dalloc(ctx, &ctx->red.partials, mb * 32 * 2 + mb));     // k_oc_coop: 2 x partials + flags
+    CK(dalloc(ctx, &ctx->oc_q, (size_t)ctx->g0.n));
     CK(dalloc(ctx, &ctx->red.counter, 8));
     CK(cudaMemset(ctx->red.counter, 0, 8 * sizeof(unsigned)));
     CK(dalloc(ctx, &ctx->sc, 1));
@@ -706,6 +709,9 @@ int otm_create(otm_ctx** out, int nx, int ny, int nz, const otm_params* pin) {
     CK(cudaMemset(ctx->scal, 0, 128 * sizeof(double)));
     CK(dalloc(ctx, &ctx->changed, 4));
     CK(dalloc(ctx, &ctx->ocl, 1));
+    // host staging: [0, 64) scalars, 64.. PcgScalars, 160.. PcgScalars read-back, 256.. / 384.. OcCtl
+    static_assert(sizeof(PcgScalars) <= 96 * sizeof(double) && sizeof(OcCtl) <= 128 * sizeof(double),
+                  "host staging slots too small");
     CK(cudaMallocHost((void**)&ctx->h, 1024 * sizeof(double)));
     CK(dalloc(ctx, &ctx->hist, 3 * kHistCap));
     CK(cudaMallocHost((void**)&ctx->h_hist, 3 * kHistCap * sizeof(double)));
@@ -747,7 +753,7 @@ int otm_destroy(otm_ctx* ctx) {
     if (ctx->lstate) cudaFree(ctx->lstate);
     for (auto& s : ctx->slots) { cudaEventDestroy(s.a); cudaEventDestroy(s.b); }
     auto F = [](void* p) { if (p) cudaFree(p); };
-    F(ctx->kap64); F(ctx->T64); F(ctx->rho_f); F(ctx->sensf); F(ctx->sens); F(ctx->r); F(ctx->p); F(ctx->q); F(ctx->d);
+    F(ctx->kap64); F(ctx->T64); F(ctx->oc_q); F(ctx->rho_f); F(ctx->sensf); F(ctx->sens); F(ctx->r); F(ctx->p); F(ctx->q); F(ctx->d);
     for (size_t l = 0; l < ctx->L.size(); ++l) {
         F(ctx->L[l].kap); F(ctx->L[l].dinv); F(ctx->L[l].z); F(ctx->L[l].res);
         if (l > 0) F(ctx->L[l].f);
@@ -1173,6 +1179,13 @@ int otm_stats_reset(otm_ctx* ctx) {
     if (!ctx) return OTM_EINVAL;
     ctx->stat_solves = ctx->stat_outer = ctx->stat_inner = 0;
     ctx->stat_oc = ctx->stat_oc_passes = ctx->stat_oc_retry = 0;
+    for (double& v : ctx->stat_phase_ms) v = 0.0;
+    return OTM_OK;
+}
+
+int otm_loop_phases(const otm_ctx* ctx, double ms[4]) {
+    if (!ctx || !ms) return OTM_EINVAL;
+    for (int k = 0; k < 4; ++k) ms[k] = ctx->stat_phase_ms[k];
     return OTM_OK;
 }
 
@@ -1292,7 +1305,7 @@ static int oc_search_coop(otm_ctx* ctx, const double* rho, const double* sens, d
     CK(cudaMemcpyAsync(ctx->ocl, ctx->h + 256, sizeof init, cudaMemcpyHostToDevice, s));
     {
         ProfScope ps(ctx, kProfOC, 0.0);
-        if (launch_oc_coop(s, ctx->g0.n, rho, sens, a, rho_out, ctx->ocl, ctx->red.partials)) {
+        if (launch_oc_coop(s, ctx->g0.n, rho, sens, a, rho_out, ctx->ocl, ctx->red.partials, ctx->oc_q)) {
             cudaGetLastError();
             return OTM_ECUDA;
         }
@@ -1734,14 +1747,20 @@ static int capture_iteration(otm_ctx* ctx, const LoopCfg& C, double* rho) {
     launch_solve_fin(s1, S, n, ctx->T64);
     launch_tensor(s1, ctx->g0, ctx->T64, ctx->kap64, ctx->red, ctx->scal + 32);
     launch_design_eval(s1, S, C, ctx->scal + 32, ctx->scal + 56, n, ctx->ocl, (unsigned long long)h_upd);
+    static const bool stamps = getenv("OTM_STAMPS") != nullptr;
+    if (stamps) launch_stamp(s1, S, 0);
     launch_sens(s1, ctx->g0, ctx->T64, ctx->rho_f, ctx->sp, Dg{}, ctx->sensf, &S->dG);
+    if (stamps) launch_stamp(s1, S, 1);
     launch_filter(s1, ctx->g0, ctx->fs, 1, ctx->sensf, ctx->sens, ctx->red);
+    if (stamps) launch_stamp(s1, S, 2);
     if (C.symmetry == 1) launch_symmetrize(s1, ctx->g0, ctx->sens);
     // IF(not finished) { governor-bounded OC search + update }
     CKC(cond_node(s1, h_upd, cudaGraphCondTypeIf, &body_upd), "IF update");
     CKC(cudaStreamBeginCaptureToGraph(s2, body_upd, nullptr, nullptr, 0, mode), "capture update");
-    if (launch_oc_coop(s2, n, rho, ctx->sens, a, rho, ctx->ocl, ctx->red.partials))
+    if (stamps) launch_stamp(s2, S, 3);
+    if (launch_oc_coop(s2, n, rho, ctx->sens, a, rho, ctx->ocl, ctx->red.partials, ctx->oc_q))
         return fail_capture("cooperative OC launch", cudaGetLastError());
+    if (stamps) launch_stamp(s2, S, 4);
     if (C.symmetry == 1) launch_symmetrize(s2, ctx->g0, rho);
     launch_oc_account(s2, S, ctx->ocl);
     CKC(cudaStreamEndCapture(s2, &g_tmp), "end update");
@@ -1861,6 +1880,12 @@ int otm_run_batch(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, do
     ctx->stat_oc += H->n_oc;
     ctx->stat_oc_passes += H->n_oc_passes;
     ctx->stat_oc_retry += H->n_oc_retries;
+    for (int k = 0; k < 4; ++k) ctx->stat_phase_ms[k] += H->ph_ms[k];
+    if (getenv("OTM_STAMPS"))
+        fprintf(stderr, "[otm] stamps (ms over %d iterations): sens %.3f  adjoint filter %.3f  ->IF %.3f  oc %.3f"
+                        " (%.3f passes per update)\n",
+                done, H->mark_ms[1], H->mark_ms[2], H->mark_ms[3], H->mark_ms[4],
+                H->n_oc ? (double)H->n_oc_passes / H->n_oc : 0.0);
     // graph nodes launched: per iteration ~14 fixed + the build, per refinement step 5,
     // per PCG iteration the inner body
     ctx->launches += (long long)(done + (status ? 1 : 0)) * (14 + ctx->build_launches) + 5 * (H->n_solves + H->n_outer) +

@@ -65,6 +65,7 @@ struct PcgScalars {
     double red[16];
     double rz[3], beta[3], pq[3], alpha[3], rr[3], target2[3], active[3];
     double sumT[3];
+    double rr_min[3];    // smallest r.r of the current inner loop per case (0: none yet)
     double flags[8];     // active[3], rr[3]: copied to the host after the inner loop
     int first;
     int it;              // device-side inner loop control (conditional graph node)
@@ -145,7 +146,8 @@ void launch_sens(cudaStream_t s, const Geo& g, const double* T, const double* rf
 void launch_oc_eval(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a, int nlam,
                     const LamSet& lam_pow, Red& red, double* out);
 int launch_oc_coop(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a,
-                   double* rho_out, OcCtl* ctl, double* partials);
+                   double* rho_out, OcCtl* ctl, double* partials,
+                   double* qbuf);
 void launch_oc_apply(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a,
                      double lam, double* rho_out, int* changed);
 

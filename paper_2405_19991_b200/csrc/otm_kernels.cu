@@ -3,6 +3,7 @@
 // (paths relative to /root/reference/pkg/src/opentm/).
 #include "otm_common.cuh"
 #include "otm_internal.h"
+#include "otm_res64p.cuh"
 #include "otm_res64w.cuh"
 #include "otm_stencil10.cuh"
 
@@ -94,8 +95,20 @@ __global__ void __launch_bounds__(128) k_filter(Geo g, int xb, FilterTaps taps, 
 }
 
 // High-parallelism filter (reach 1): one thread per z pair, 27 window loads up front,
-// taps in the reference's order (bit-exact, see k_filter).  nz even.
-template <int MODE>
+// taps in the reference's order (bit-exact, see k_filter).  nz even.  MASK = the
+// nonzero taps (bit slot) when known at compile time (radius 1.5: no corners; radius
+// >= sqrt 3: all 27), so zero taps cost neither a compare nor their window loads;
+// MASK = 0 tests every weight at run time.
+constexpr unsigned kTapsAll = (1u << 27) - 1;
+constexpr unsigned taps_no_corners() {
+    unsigned m = 0;
+    for (int s = 0; s < 27; ++s)
+        if (s / 9 == 1 || (s / 3) % 3 == 1 || s % 3 == 1) m |= 1u << s;
+    return m;
+}
+constexpr unsigned kTapsNoCorners = taps_no_corners();
+
+template <int MODE, unsigned MASK = 0>
 __global__ void __launch_bounds__(256) k_filter_b(Geo g, FilterTaps taps, const double* __restrict__ in,
                                                   double* __restrict__ out, double* __restrict__ kappa64,
                                                   float* __restrict__ kappa32, SimpParams sp, double* partials,
@@ -131,7 +144,7 @@ __global__ void __launch_bounds__(256) k_filter_b(Geo g, FilterTaps taps, const 
 #pragma unroll
             for (int slot = 0; slot < 27; ++slot) {
                 const double wt = taps.w27[slot];
-                if (wt != 0.0) {
+                if (MASK ? ((MASK >> slot) & 1u) != 0u : wt != 0.0) {
                     const int src = MODE == 1 ? 26 - slot : slot;
                     const int p = src / 9, j = (src / 3) % 3, m = src % 3;
                     s = __dadd_rn(s, __dmul_rn(wt, t[p][j][h + m]));
@@ -659,26 +672,45 @@ __global__ void __launch_bounds__(128) k_apply64(Geo g, int xb, LevelTemplate lt
 
 // Means of the three macro loads (solver.py:386-387 projects them out; they are
 // round-off, but for a uniform medium round-off is all the load there is).
-__global__ void k_load_means(Geo g, LevelTemplate lt, const double* __restrict__ kap, double* partials,
-                             unsigned* counter, double* out) {
+// One (y, z) column per thread marching x: the element factors of plane x - 1
+// carry over (4 loads per vertex instead of 8, no per-vertex index division); each
+// vertex's load is the fixed-order sum of its 8 element terms.
+__global__ void __launch_bounds__(256) k_load_means_x(Geo g, int chunks, LevelTemplate lt,
+                                                      const double* __restrict__ kap, double* partials,
+                                                      unsigned* counter, double* out) {
     double v3[3] = {0.0, 0.0, 0.0};
-    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < g.n;
-         v += (long long)gridDim.x * blockDim.x) {
-        const int x = (int)(v / g.pl), rem = (int)(v - (long long)x * g.pl);
-        const int y = rem / g.nz, z = rem - y * g.nz;
-        const int xs[2] = {wrap_m(x, g.nx), x}, ys[2] = {wrap_m(y, g.ny), y}, zs[2] = {wrap_m(z, g.nz), z};
-        double k[8];
+    const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned cols = (unsigned)g.pl;
+    if (t < cols * (unsigned)chunks) {
+        const unsigned c = t / cols, r = t - c * cols;
+        const unsigned y = r / (unsigned)g.nz, z = r - y * (unsigned)g.nz;
+        const unsigned ym = y == 0 ? (unsigned)g.ny - 1 : y - 1, zm = z == 0 ? (unsigned)g.nz - 1 : z - 1;
+        // slot (dy, dz) = element (y - dy, z - dz)
+        const unsigned o[4] = {y * g.nz + z, y * g.nz + zm, ym * g.nz + z, ym * g.nz + zm};
+        const int per = (g.nx + chunks - 1) / chunks;
+        const int x0 = (int)c * per, x1 = min(g.nx, x0 + per);
+        if (x0 < x1) {
+            double P[4], Q[4];
+            const unsigned pm = (unsigned)(x0 == 0 ? g.nx - 1 : x0 - 1) * cols;
 #pragma unroll
-        for (int a = 0; a < 8; ++a) {   // element v - c_a
-            const int q = 1 - (a & 1), jj = 1 - ((a >> 1) & 1), kk = 1 - ((a >> 2) & 1);
-            k[a] = kap[((long long)xs[q] * g.ny + ys[jj]) * g.nz + zs[kk]];
-        }
+            for (int k = 0; k < 4; ++k) P[k] = __ldg(kap + pm + o[k]);
+            for (int x = x0; x < x1; ++x) {
+                const unsigned po = (unsigned)x * cols;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            double f = 0.0;
+                for (int k = 0; k < 4; ++k) Q[k] = __ldg(kap + po + o[k]);
 #pragma unroll
-            for (int a = 0; a < 8; ++a) f = __dadd_rn(f, __dmul_rn(lt.f0[a * 3 + c], k[a]));
-            v3[c] += f;
+                for (int cc = 0; cc < 3; ++cc) {
+                    double f = 0.0;
+#pragma unroll
+                    for (int a = 0; a < 8; ++a) {   // element v - c_a
+                        const int slot = ((a >> 1) & 1) * 2 + ((a >> 2) & 1);
+                        f = __dadd_rn(f, __dmul_rn(lt.f0[a * 3 + cc], (a & 1) ? P[slot] : Q[slot]));
+                    }
+                    v3[cc] += f;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) P[k] = Q[k];
+            }
         }
     }
     if (reduce_finalize<3>(v3, partials, counter, out)) {
@@ -926,6 +958,12 @@ __global__ void __launch_bounds__(256) k_upd(long long n, float* __restrict__ r,
             was[c] = sc->active[c] != 0.0;
             sc->rr[c] = sc->red[6 + c];
             if (was[c] && sc->rr[c] <= sc->target2[c]) sc->active[c] = 0.0;
+            // fp32 breakdown guard: a recursive residual 10x above its minimum in this
+            // loop means the fp32 recurrences have lost the preconditioned operator's
+            // positivity (seen on thin, high-contrast 2-D designs at tol 1e-8); the case
+            // stops and the outer fp64 step restarts it from the true residual
+            else if (was[c] && sc->rr_min[c] > 0.0 && sc->rr[c] > 100.0 * sc->rr_min[c]) sc->active[c] = 0.0;
+            if (was[c]) sc->rr_min[c] = sc->rr_min[c] > 0.0 ? fmin(sc->rr_min[c], sc->rr[c]) : sc->rr[c];
             sc->flags[c] = sc->active[c];
         }
         sc->flags[3] = sc->rr[0];
@@ -1647,7 +1685,8 @@ __device__ void oc_walk(OcCtl* C) {
 
 __global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* __restrict__ rho,
                                                     const double* __restrict__ sens, const OcArgs a,
-                                                    double* rho_out, OcCtl* C, double* partials) {
+                                                    double* rho_out, OcCtl* C, double* partials,
+                                                    double* __restrict__ qbuf) {
     // Every block keeps its own copy of the search state in shared memory and replays
     // the same walk on the same fixed-order sums, so all blocks agree on the next
     // multipliers with ONE grid barrier per pass.  Partial sums are double-buffered by
@@ -1682,6 +1721,7 @@ __global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* _
     __syncthreads();
     set_pows();
     int parity = 0;
+    int epass = 0;                                 // evaluation passes done in this launch
     while (true) {
         __syncthreads();
         if (threadIdx.x < kOcLam) s_lp[threadIdx.x] = sC.lam_pow[threadIdx.x];
@@ -1699,6 +1739,7 @@ __global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* _
             // exact candidate of the chosen multiplier (reference expression)
             const double lam = sC.lam;
             int ch = 0;
+#pragma unroll 4
             for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
                  i += (long long)gridDim.x * blockDim.x) {
                 const double r = rho[i];
@@ -1746,40 +1787,70 @@ __global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* _
         // The clamp decisions are exact (fp64 products are monotone in lam^-damp).
         const int nlam = sC.nlam;
         const double lpk = lane < nlam ? s_lp[lane] : 0.0;
+        const bool free0 = s_lp[0] == 0.0;
         const double lpmin = s_lpr[0], lpmax = s_lpr[1];
         double acc[kOcLam];
 #pragma unroll
         for (int k = 0; k < kOcLam; ++k) acc[k] = 0.0;
         double acck = 0.0, sCn = 0.0, sL = 0.0, sF = 0.0;
         const long long wstride = (long long)gridDim.x * nw * 32;
-        for (long long base = ((long long)blockIdx.x * nw + wid) * 32; base < n; base += wstride) {
+        // the next element's (rho, sens) are loaded before this one is processed: the
+        // loop is otherwise one L2 round trip per element (long-scoreboard bound)
+        // The pass-invariant c_e = rho * desc^damp (a square root per element) is formed
+        // in the first pass and kept in qbuf with the sign of desc encoded
+        // (q >= 0: c_e, desc > 0;  -1: desc < 0;  -2: desc == 0); later passes read q
+        // instead of the sensitivity.  Each thread revisits its own elements only.
+        const bool first = epass == 0 || !qbuf;
+        const double* src = first ? sens : qbuf;
+        long long base = ((long long)blockIdx.x * nw + wid) * 32;
+        double r_nx = 0.0, s_nx = 0.0;
+        if (base + lane < n) {
+            r_nx = __ldg(rho + base + lane);
+            s_nx = src[base + lane];
+        }
+        for (; base < n; base += wstride) {
             const long long i = base + lane;
+            const double r_cur = r_nx, s_cur = s_nx;
+            if (i + wstride < n) {
+                r_nx = __ldg(rho + i + wstride);
+                s_nx = src[i + wstride];
+            }
             bool mixed = false;
             double ce = 0.0, lof = 0.0, hi = 0.0, freev = 0.0;
             if (i < n) {
-                const double r = __ldg(rho + i);
-                const double desc = M * (-__ldg(sens + i));
+                const double r = r_cur;
+                double q;
+                if (first) {
+                    const double desc = M * (-s_cur);
+                    q = desc > 0.0 ? r * (a.sqrt_damp ? sqrt(desc) : pow(desc, a.damp)) : (desc < 0.0 ? -1.0 : -2.0);
+                    if (qbuf) qbuf[i] = q;
+                } else {
+                    q = s_cur;
+                }
                 const double lo = fmax(r - a.step, a.rmin);
                 hi = fmin(r + a.step, 1.0);
                 lof = fmax(lo, r * a.floor_ratio);
-                ce = desc > 0.0 ? r * (a.sqrt_damp ? sqrt(desc) : pow(desc, a.damp)) : 0.0;
-                freev = desc > 0.0 ? hi : (desc < 0.0 ? lo : r);
+                ce = fmax(q, 0.0);
+                freev = q >= 0.0 ? hi : (q == -1.0 ? lo : r);
                 const double tlo = ce * lpmin, thi = ce * lpmax;
-                if (thi <= lof) { sCn += lof; sF += freev; }
-                else if (tlo >= hi) { sCn += hi; sF += freev; }
-                else if (tlo >= lof && thi <= hi) { sL += ce; sF += freev; }
-                else mixed = true;
+                // branch-free classification: all multipliers of the pass clamp to lof,
+                // all to hi, all stay inside (linear), or mixed
+                const bool c_lo = thi <= lof, c_hi = !c_lo && tlo >= hi;
+                const bool c_lin = !c_lo && !c_hi && tlo >= lof && thi <= hi;
+                mixed = !(c_lo || c_hi || c_lin);
+                sCn += c_lo ? lof : (c_hi ? hi : 0.0);
+                sL += c_lin ? ce : 0.0;
+                sF += mixed ? 0.0 : freev;
             }
             unsigned m = __ballot_sync(0xffffffffu, mixed);
             if (!m) continue;
             if (__popc(m) > 10) {
                 if (mixed) {
+                    // only slot 0 can be the free step (lam = 0); slots >= nlam (lam^-damp 0)
+                    // accumulate values nobody reads
+                    acc[0] += free0 ? freev : fmin(fmax(ce * s_lp[0], lof), hi);
 #pragma unroll
-                    for (int k = 0; k < kOcLam; ++k) {
-                        const double lp = s_lp[k];
-                        const double cand = lp == 0.0 ? freev : fmin(fmax(ce * lp, lof), hi);
-                        acc[k] += k < nlam ? cand : 0.0;
-                    }
+                    for (int k = 1; k < kOcLam; ++k) acc[k] += fmin(fmax(ce * s_lp[k], lof), hi);
                 }
             } else {
                 while (m) {
@@ -1813,15 +1884,23 @@ __global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* _
         grid.sync();
         // every block: the same fixed-order sum of all blocks' partials
         {
+            // 16 loads in flight per thread (the sum is a chain of L2 round trips otherwise)
             double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
-            unsigned b = wid;
-            for (; b + 3 * nw < nb; b += 4 * nw) {
-                t0 += __ldcg(part + (size_t)b * 32 + lane);
-                t1 += __ldcg(part + (size_t)(b + nw) * 32 + lane);
-                t2 += __ldcg(part + (size_t)(b + 2 * nw) * 32 + lane);
-                t3 += __ldcg(part + (size_t)(b + 3 * nw) * 32 + lane);
+            for (unsigned b = wid; b < nb; b += 16 * nw) {
+                double v[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const unsigned bb = b + j * nw;
+                    v[j] = bb < nb ? __ldcg(part + (size_t)bb * 32 + lane) : 0.0;
+                }
+#pragma unroll
+                for (int j = 0; j < 16; j += 4) {
+                    t0 += v[j];
+                    t1 += v[j + 1];
+                    t2 += v[j + 2];
+                    t3 += v[j + 3];
+                }
             }
-            for (; b < nb; b += nw) t0 += __ldcg(part + (size_t)b * 32 + lane);
             sm[wid][lane] = (t0 + t1) + (t2 + t3);
         }
         __syncthreads();
@@ -1831,6 +1910,7 @@ __global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* _
             sC.means[threadIdx.x] = u / M;
         }
         parity ^= 1;
+        ++epass;
         __syncthreads();
         if (threadIdx.x == 0) oc_walk(&sC);
         __syncthreads();
@@ -2032,17 +2112,32 @@ static inline dim3 stencil_grid(const Geo& g, int* xb) {
     return dim3((unsigned)((g.pl + 127) / 128), (unsigned)ch, 1);
 }
 
+// k_filter_b for the tap pattern of fs (compile-time mask when it is a common one)
+template <int MODE>
+static void launch_filter_b(cudaStream_t s, const Geo& g, const FilterSetup& fs, const double* in, double* out,
+                            double* k64, float* k32, const SimpParams& sp, double* partials, unsigned* counter,
+                            double* out3) {
+    FilterTaps taps;
+    unsigned mask = 0;
+    for (int i = 0; i < 27; ++i) {
+        taps.w27[i] = fs.w27[i];
+        if (fs.w27[i] != 0.0) mask |= 1u << i;
+    }
+    const unsigned blocks = nblk(g.n >> 1, 256);
+    if (mask == kTapsNoCorners)
+        k_filter_b<MODE, kTapsNoCorners><<<blocks, 256, 0, s>>>(g, taps, in, out, k64, k32, sp, partials, counter, out3);
+    else if (mask == kTapsAll)
+        k_filter_b<MODE, kTapsAll><<<blocks, 256, 0, s>>>(g, taps, in, out, k64, k32, sp, partials, counter, out3);
+    else
+        k_filter_b<MODE, 0><<<blocks, 256, 0, s>>>(g, taps, in, out, k64, k32, sp, partials, counter, out3);
+}
+
 void launch_filter(cudaStream_t s, const Geo& g, const FilterSetup& fs, int adjoint, const double* in,
                    double* out, Red& red) {
     if (fs.window && g.nz % 2 == 0) {
-        FilterTaps taps;
-        for (int i = 0; i < 27; ++i) taps.w27[i] = fs.w27[i];
         SimpParams sp{};
-        const long long th = g.n >> 1;
-        if (adjoint)
-            k_filter_b<1><<<nblk(th, 256), 256, 0, s>>>(g, taps, in, out, nullptr, nullptr, sp, nullptr, nullptr, nullptr);
-        else
-            k_filter_b<0><<<nblk(th, 256), 256, 0, s>>>(g, taps, in, out, nullptr, nullptr, sp, nullptr, nullptr, nullptr);
+        if (adjoint) launch_filter_b<1>(s, g, fs, in, out, nullptr, nullptr, sp, nullptr, nullptr, nullptr);
+        else launch_filter_b<0>(s, g, fs, in, out, nullptr, nullptr, sp, nullptr, nullptr, nullptr);
         return;
     }
     if (fs.window) {
@@ -2063,10 +2158,7 @@ void launch_filter(cudaStream_t s, const Geo& g, const FilterSetup& fs, int adjo
 void launch_filter_simp(cudaStream_t s, const Geo& g, const FilterSetup& fs, const SimpParams& sp,
                         const double* rho, double* rho_f, double* k64, float* k32, Red& red, double* out3) {
     if (fs.window && g.nz % 2 == 0) {
-        FilterTaps taps;
-        for (int i = 0; i < 27; ++i) taps.w27[i] = fs.w27[i];
-        const long long th = g.n >> 1;
-        k_filter_b<2><<<nblk(th, 256), 256, 0, s>>>(g, taps, rho, rho_f, k64, k32, sp, red.partials, red.counter, out3);
+        launch_filter_b<2>(s, g, fs, rho, rho_f, k64, k32, sp, red.partials, red.counter, out3);
         return;
     }
     if (fs.window) {
@@ -2141,8 +2233,74 @@ void launch_coarse_solve(cudaStream_t s, int n, const float* G, const float* f, 
     const int blocks = rows <= 32 ? 1 : (rows + 31) / 32 > 148 ? 148 : (rows + 31) / 32;
     launch_pdl(k_coarse_solve, blocks, 1024, 0, s, n, G, f, z);
 }
+// 4-D (z, case, y, x) fp64 map of the three stacked cases (k_res64p), box rows x 3 cases x nz
+static bool encode_map64c(CUtensorMap* m, const double* base, const Geo& g, int box_rows) {
+    PFN_encodeTiled_t fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[4] = {(cuuint64_t)g.nz, 3, (cuuint64_t)g.ny, (cuuint64_t)g.nx};
+    const cuuint64_t strides[3] = {(cuuint64_t)g.n * 8, (cuuint64_t)g.nz * 8, (cuuint64_t)g.pl * 8};
+    const cuuint32_t box[4] = {(cuuint32_t)g.nz, 3, (cuuint32_t)box_rows, 1};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)base, dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int NZ>
+static void l_res64p(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const R64PMaps& M0, const double* fmean,
+                     float* r32, Red& red, double* out9, const int* skip) {
+    using P = R64P<NZ>;
+    smem_attr(k_res64p<NZ>, P::SMEM);
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_res64p<NZ>, P::THREADS, P::SMEM);
+    if (per_sm < 1) per_sm = 1;
+    const long long nty = g.ny / P::TY, units = nty * g.nx, slots = (long long)per_sm * sms;
+    R64PMaps M = M0;
+    M.lock = 0;
+    long long blocks = std::min(slots, units);
+    // lockstep row-tile order where the three fp64 cases (24 B per vertex) exceed half the L2
+    static const bool lock_on = !(getenv("OTM_K10_LOCK") && atoi(getenv("OTM_K10_LOCK")) == 0);
+    if (lock_on && g.n * 24 > (64LL << 20)) {
+        const long long k = std::max<long long>(1, std::min<long long>(slots / nty, g.nx / 8));
+        M.lock = (int)k;
+        blocks = nty * k;
+    }
+    k_res64p<NZ><<<(unsigned)blocks, dim3(NZ, P::TY), P::SMEM, s>>>(g, lt, M, fmean, r32, red.partials, red.counter,
+                                                                    out9, skip);
+}
+
 void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
                   const double* fext, const double* fmean, float* r32, Red& red, double* out9, const int* skip) {
+    // all three cases in one push march (k_res64p; OTM_RES64P=0: the per-case k_res64w)
+    static const bool use_p = !(getenv("OTM_RES64P") && atoi(getenv("OTM_RES64P")) == 0);
+    if (use_p && !fext && lt.equal && (g.nz == 64 || g.nz == 128 || g.nz == 256) && g.nx >= 2) {
+        const int ty = g.nz >= 256 ? 1 : 256 / g.nz;
+        if (g.ny % ty == 0 && g.ny >= 2 * ty) {
+            static R64PMaps M;
+            static const double *lastT = nullptr, *lastK = nullptr;
+            static int lastdims[3] = {0, 0, 0};
+            static bool lastok = false;
+            if (T != lastT || kap != lastK || g.nx != lastdims[0] || g.ny != lastdims[1] || g.nz != lastdims[2]) {
+                lastok = encode_map64c(&M.t_full, T, g, ty + 2) && encode_map64c(&M.t_main, T, g, ty) &&
+                         encode_map64c(&M.t_halo, T, g, 1) && encode_map64(&M.k_full, kap, g.nz, g.ny, g.nx, ty + 1) &&
+                         encode_map64(&M.k_main, kap, g.nz, g.ny, g.nx, ty) &&
+                         encode_map64(&M.k_halo, kap, g.nz, g.ny, g.nx, 1);
+                lastT = T;
+                lastK = kap;
+                lastdims[0] = g.nx;
+                lastdims[1] = g.ny;
+                lastdims[2] = g.nz;
+            }
+            if (lastok) {
+                if (g.nz == 64) l_res64p<64>(s, g, lt, M, fmean, r32, red, out9, skip);
+                else if (g.nz == 128) l_res64p<128>(s, g, lt, M, fmean, r32, red, out9, skip);
+                else l_res64p<256>(s, g, lt, M, fmean, r32, red, out9, skip);
+                return;
+            }
+        }
+    }
     static const bool r512 = !(getenv("OTM_RES64_512") && atoi(getenv("OTM_RES64_512")) == 0);
     const bool w512 = r512 && lt.equal && g.nz == 512 && g.nx >= 2;
     if (!fext && (tma_tiling(g, lt) || w512)) {
@@ -2217,11 +2375,22 @@ void launch_apply64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const
     const dim3 grid = stencil_grid(g, &xb);
     k_apply64<<<grid, 128, 0, s>>>(g, xb, lt, kap, T, out, load_case);
 }
+template <class K>
+static int march_chunks(K kernel, const Geo& g) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
+    const long long want = 2LL * sms * std::max(per_sm, 1) * 256;
+    long long c = (want + g.pl - 1) / g.pl;
+    c = std::min<long long>(c, std::max(1, g.nx / 4));
+    return (int)std::max<long long>(1, c);
+}
 void launch_load_means(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, Red& red,
                        double* out3) {
-    long long want = (g.n + 255) / 256;
-    unsigned blocks = (unsigned)(want < 1184 ? want : 1184);
-    k_load_means<<<blocks, 256, 0, s>>>(g, lt, kap, red.partials, red.counter, out3);
+    static int ch = 0, for_pl = -1, for_nx = -1;
+    if (for_pl != g.pl || for_nx != g.nx) { ch = march_chunks(k_load_means_x, g); for_pl = g.pl; for_nx = g.nx; }
+    k_load_means_x<<<nblk((long long)g.pl * ch, 256), 256, 0, s>>>(g, ch, lt, kap, red.partials, red.counter, out3);
 }
 void launch_sum3(cudaStream_t s, long long n, const double* f, Red& red, double* out3) {
     k_sum3<<<592, 256, 0, s>>>(n, f, red.partials, red.counter, out3);
@@ -2522,17 +2691,6 @@ void launch_submean(cudaStream_t s, long long n, double* T, const double* sumT) 
 }
 // x chunks per (y, z) column: about 2 waves of the kernel's resident threads,
 // >= 4 planes each (a chunk reloads its first plane)
-template <class K>
-static int march_chunks(K kernel, const Geo& g) {
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
-    const long long want = 2LL * sms * std::max(per_sm, 1) * 256;
-    long long c = (want + g.pl - 1) / g.pl;
-    c = std::min<long long>(c, std::max(1, g.nx / 4));
-    return (int)std::max<long long>(1, c);
-}
 void launch_tensor(cudaStream_t s, const Geo& g, const double* T, const double* kap, Red& red, double* out6) {
     static int ch = 0, for_pl = -1, for_nx = -1;
     if (for_pl != g.pl || for_nx != g.nx) { ch = march_chunks(k_tensor_x, g); for_pl = g.pl; for_nx = g.nx; }
@@ -2556,7 +2714,7 @@ void launch_oc_eval(cudaStream_t s, long long n, const double* rho, const double
     k_oc_eval<<<blocks, 256, 0, s>>>(n, rho, sens, a, nlam, lam_pow, red.partials, red.counter, out);
 }
 int launch_oc_coop(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a,
-                   double* rho_out, OcCtl* ctl, double* partials) {
+                   double* rho_out, OcCtl* ctl, double* partials, double* qbuf) {
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2566,7 +2724,8 @@ int launch_oc_coop(cudaStream_t s, long long n, const double* rho, const double*
     long long blocks = (long long)per_sm * sms;
     if (blocks > want) blocks = want;
     if (blocks < 1) blocks = 1;
-    void* args[] = {(void*)&n, (void*)&rho, (void*)&sens, (void*)&a, (void*)&rho_out, (void*)&ctl, (void*)&partials};
+    void* args[] = {(void*)&n,       (void*)&rho, (void*)&sens,     (void*)&a,
+                    (void*)&rho_out, (void*)&ctl, (void*)&partials, (void*)&qbuf};
     return cudaLaunchCooperativeKernel((void*)k_oc_coop, dim3((unsigned)blocks), dim3(256), args, 0, s) == cudaSuccess
                ? 0 : 1;
 }

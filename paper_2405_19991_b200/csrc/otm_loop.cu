@@ -28,6 +28,7 @@ __global__ void k_iter_begin(LoopState* S, cudaGraphConditionalHandle h) {
     const bool run = !S->finished;
     if (run) {
         S->t0 = global_ns();
+        if (S->t_oc) S->ph_ms[3] += (double)(S->t0 - S->t_oc) * 1e-6;
         S->outer = 0;
         S->cycles = 0;
         for (int c = 0; c < 3; ++c) S->ccyc[c] = 0;
@@ -72,6 +73,7 @@ __global__ void k_solve_ctl(LoopState* S, LoopCfg C, const double* __restrict__ 
     S->outer += 1;
     for (int c = 0; c < 3; ++c) S->done[c] = done[c];
     if (all || over) {
+        S->t_solve = global_ns();
         if (!all) S->status = 2;               // ConvergenceError (solver.py:404-406)
         sc->skip = 1;
         cudaGraphSetConditional(h_out, 0u);
@@ -81,7 +83,7 @@ __global__ void k_solve_ctl(LoopState* S, LoopCfg C, const double* __restrict__ 
     for (int k = 0; k < 16; ++k) sc->red[k] = 0.0;
     for (int c = 0; c < 3; ++c) {
         const double tgt = fmax(C.inner_reduction * S->rnorm[c], C.tolf * C.solver_tol * S->fnorm[c]);
-        sc->rz[c] = sc->beta[c] = sc->pq[c] = sc->alpha[c] = sc->rr[c] = sc->sumT[c] = 0.0;
+        sc->rz[c] = sc->beta[c] = sc->pq[c] = sc->alpha[c] = sc->rr[c] = sc->sumT[c] = sc->rr_min[c] = 0.0;
         sc->target2[c] = tgt * tgt;
         sc->active[c] = done[c] ? 0.0 : 1.0;
         sc->ccyc[c] = S->ccyc[c];
@@ -114,6 +116,10 @@ __global__ void k_design_eval(LoopState* S, LoopCfg C, const double* __restrict_
                               cudaGraphConditionalHandle h_upd) {
     const int it = S->iter + 1;
     LoopRecord* rec = &S->rec[(it - 1) % kLoopRing];
+    S->t_eval = global_ns();
+    S->ph_ms[0] += (double)(S->t_solve - S->t0) * 1e-6;
+    S->ph_ms[1] += (double)(S->t_eval - S->t_solve) * 1e-6;
+    S->t_oc = 0;
     const double mean_rho = sums3[0] / (double)n, mean_rho_p = sums3[1] / (double)n, mean_rf = sums3[2] / (double)n;
     rec->iter = it;
     rec->vcycles = S->cycles;
@@ -160,7 +166,16 @@ __global__ void k_design_eval(LoopState* S, LoopCfg C, const double* __restrict_
     cudaGraphSetConditional(h_upd, finished ? 0u : 1u);
 }
 
+// diagnostic time stamps inside the iteration graph (OTM_STAMPS=1): idx 0 restarts
+__global__ void k_stamp(LoopState* S, int idx) {
+    const unsigned long long t = global_ns();
+    if (idx > 0 && S->t_mark) S->mark_ms[idx] += (double)(t - S->t_mark) * 1e-6;
+    S->t_mark = t;
+}
+
 __global__ void k_oc_account(LoopState* S, const OcCtl* ocl) {
+    S->t_oc = global_ns();
+    S->ph_ms[2] += (double)(S->t_oc - S->t_eval) * 1e-6;
     S->n_oc += 1;
     S->n_oc_passes += ocl->passes;
     S->n_oc_retries += ocl->retried;
@@ -182,6 +197,7 @@ void launch_solve_ctl(cudaStream_t s, LoopState* S, const LoopCfg& C, const doub
 void launch_solve_fin(cudaStream_t s, LoopState* S, long long n, double* T) {
     k_solve_fin<<<592, 256, 0, s>>>(S, n, T);
 }
+void launch_stamp(cudaStream_t s, LoopState* S, int idx) { k_stamp<<<1, 1, 0, s>>>(S, idx); }
 void launch_design_eval(cudaStream_t s, LoopState* S, const LoopCfg& C, const double* kap6, const double* sums3,
                         long long n, OcCtl* ocl, unsigned long long h_upd) {
     k_design_eval<<<1, 1, 0, s>>>(S, C, kap6, sums3, n, ocl, (cudaGraphConditionalHandle)h_upd);

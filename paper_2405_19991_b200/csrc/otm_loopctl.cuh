@@ -139,6 +139,10 @@ struct LoopState {
     int done[3], zero_load[3], ccyc[3];
     int cycles, outer;
     unsigned long long t0;        // %globaltimer at the start of the iteration
+    unsigned long long t_solve, t_eval, t_oc;   // ... at the end of the solve, of the evaluation, of the OC step
+    double ph_ms[4];              // accumulated: filter+build+solve, tensor+objective, sens+OC, gap to next
+    unsigned long long t_mark;    // OTM_STAMPS: last k_stamp
+    double mark_ms[8];            // OTM_STAMPS: device time before each k_stamp since the previous one
     long long n_solves, n_outer, n_inner, n_oc, n_oc_passes, n_oc_retries;   // otm_stats counters
     Dg dG;
     LoopRecord rec[kLoopRing];
@@ -171,5 +175,6 @@ void launch_solve_fin(cudaStream_t s, LoopState* S, long long n, double* T);
 void launch_design_eval(cudaStream_t s, LoopState* S, const LoopCfg& C, const double* kap6, const double* sums3,
                         long long n, OcCtl* ocl, unsigned long long h_upd);
 void launch_oc_account(cudaStream_t s, LoopState* S, const OcCtl* ocl);
+void launch_stamp(cudaStream_t s, LoopState* S, int idx);
 
 }  // namespace otm
