@@ -17,6 +17,9 @@ fixed 500 iterations") on the 128^3 IWP seed (vf 0.5), target
          then warm-started), warm iteration x500
   c1_to_convergence / c3_to_convergence  whole runs to the reference's own
          convergence rule (no extrapolation): C1 on both arms, C3 on the GPU
+  multi_structure  throughput with 3 structures designed at once on the GPU
+         (threads + streams, the gallery's --per-gpu 3); `value` stays the
+         one-structure latency
 
 ``--impl reference`` times that CPU port alone (rank 0) on the same metric: one
 oracle run, W warm-up iterations (the first is the cold solve from the seed),
@@ -154,6 +157,56 @@ def cpu_iteration_times(name, n_iter):
     stamps = [time.perf_counter()]
     O.optimize(cfg, callback=lambda *a: stamps.append(time.perf_counter()))
     return [b - a for a, b in zip(stamps, stamps[1:])]
+
+
+def multi_structure(otm, torch, name, iters, seed, k=3):
+    """Throughput with k independent structures designed at once on this GPU (the
+    gallery's `--per-gpu k`): one host thread, hierarchy, CUDA stream and captured
+    iteration graph each; device time from the first launch to the last completion
+    (events on the default stream bracketing the k runs), against the same k runs
+    one after another."""
+    import threading
+    from paper_2405_19991_b200.optimize import DesignRun
+    from paper_2405_19991_b200.solver import GridHierarchy
+    cfg = make_config(otm, name, iters, 0.0, init_field=seed)
+    hiers = [GridHierarchy(cfg.dims, material=cfg.material, filter_radius=cfg.filter.radius) for _ in range(k)]
+    streams = [torch.cuda.Stream() for _ in range(k)]
+    logs = [None] * k
+
+    def one(i):
+        with torch.cuda.stream(streams[i]):
+            run = DesignRun(cfg, hier=hiers[i])
+            run.run()
+            logs[i] = run.log
+
+    def timed(concurrent):
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()
+        if concurrent:
+            th = [threading.Thread(target=one, args=(i,)) for i in range(k)]
+            for t in th:
+                t.start()
+            for t in th:
+                t.join()
+        else:
+            for i in range(k):
+                one(i)
+        cur = torch.cuda.current_stream()
+        for st in streams:
+            cur.wait_stream(st)
+        ev[1].record()
+        ev[1].synchronize()
+        return ev[0].elapsed_time(ev[1]) / 1e3
+
+    timed(False)                                   # capture every hierarchy's graphs
+    seq = timed(False)
+    conc = timed(True)
+    same = all(len(lg) == len(logs[0]) and all(a.g == b.g for a, b in zip(lg, logs[0])) for lg in logs)
+    del hiers
+    return {"value": conc / k, "unit": "s/structure", "one_at_a_time_s": seq / k, "speedup": seq / conc,
+            "identical_results": bool(same),
+            "note": f"{k} {name} structures at once on one GPU (threads + streams), device time / {k}"}
 
 
 def cpu_to_convergence(name):
@@ -421,6 +474,9 @@ def run_gpu(args):
                            "workload": config_block(cname, 500)["workload"]
                            + " (stops at the reference's convergence rule)",
                            "path": "run_optimization (numpy seed in, numpy field out), host wall clock"}
+    multi = multi_structure(otm, torch, name, args.iters, seed_dev) if (world == 1 and args.multi > 1) else None
+    if multi:
+        multi["structures_per_gpu"] = args.multi
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -456,6 +512,8 @@ def run_gpu(args):
     }
     for cname, rec in conv.items():
         line[f"{cname}_to_convergence"] = rec
+    if multi:
+        line["multi_structure"] = multi
     if args.beyond_l2 and world == 1 and name != "c4":
         line["roofline_beyond_l2"] = beyond_l2(otm, _lib, lib, torch, peak, peak_kind)
     if not args.no_cpu and world == 1:
@@ -578,6 +636,8 @@ def main():
     ap.add_argument("--iters", type=int, default=500, help="OC iterations per structure")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-c1", action="store_true", help="skip the C1 to-convergence legs")
+    ap.add_argument("--multi", type=int, default=3,
+                    help="structures designed at once for the multi_structure key (<= 1: skip)")
     ap.add_argument("--no-single", action="store_true", help="--mode slab: skip the single-GPU reference time")
     ap.add_argument("--host-loop", action="store_true",
                     help="drive the design loop from the host (otm_run_step/update) instead of the iteration graph")

@@ -2278,10 +2278,12 @@ void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const d
     if (use_p && !fext && lt.equal && (g.nz == 64 || g.nz == 128 || g.nz == 256) && g.nx >= 2) {
         const int ty = g.nz >= 256 ? 1 : 256 / g.nz;
         if (g.ny % ty == 0 && g.ny >= 2 * ty) {
-            static R64PMaps M;
-            static const double *lastT = nullptr, *lastK = nullptr;
-            static int lastdims[3] = {0, 0, 0};
-            static bool lastok = false;
+            // per host thread: structures designed concurrently from several threads
+            // (one stream each) must not share the tensor-map cache
+            static thread_local R64PMaps M;
+            static thread_local const double *lastT = nullptr, *lastK = nullptr;
+            static thread_local int lastdims[3] = {0, 0, 0};
+            static thread_local bool lastok = false;
             if (T != lastT || kap != lastK || g.nx != lastdims[0] || g.ny != lastdims[1] || g.nz != lastdims[2]) {
                 lastok = encode_map64c(&M.t_full, T, g, ty + 2) && encode_map64c(&M.t_main, T, g, ty) &&
                          encode_map64c(&M.t_halo, T, g, 1) && encode_map64(&M.k_full, kap, g.nz, g.ny, g.nx, ty + 1) &&
@@ -2307,10 +2309,10 @@ void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const d
         const int tyd = g.nz >= 256 ? 1 : 256 / g.nz;
         // tensor maps of the last (T, kappa, grid) are reused: encoding costs a few us of
         // host time per map, on the critical path between two host waits
-        static R64Maps M;
-        static const double *lastT = nullptr, *lastK = nullptr;
-        static int lastdims[3] = {0, 0, 0};
-        static bool lastok = false;
+        static thread_local R64Maps M;
+        static thread_local const double *lastT = nullptr, *lastK = nullptr;
+        static thread_local int lastdims[3] = {0, 0, 0};
+        static thread_local bool lastok = false;
         if (T != lastT || kap != lastK || g.nx != lastdims[0] || g.ny != lastdims[1] || g.nz != lastdims[2]) {
             lastok = encode_map64(&M.Tm, T, g.nz, g.ny, 3LL * g.nx, tyd) &&
                      encode_map64(&M.Th, T, g.nz, g.ny, 3LL * g.nx, 1) &&
@@ -2388,7 +2390,7 @@ static int march_chunks(K kernel, const Geo& g) {
 }
 void launch_load_means(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, Red& red,
                        double* out3) {
-    static int ch = 0, for_pl = -1, for_nx = -1;
+    static thread_local int ch = 0, for_pl = -1, for_nx = -1;
     if (for_pl != g.pl || for_nx != g.nx) { ch = march_chunks(k_load_means_x, g); for_pl = g.pl; for_nx = g.nx; }
     k_load_means_x<<<nblk((long long)g.pl * ch, 256), 256, 0, s>>>(g, ch, lt, kap, red.partials, red.counter, out3);
 }
@@ -2464,14 +2466,14 @@ static bool k10_maps(K10Maps& M, const Geo& g, const float* op3, const float* d,
         M.f_main = M.f_full = M.f_halo = M.op_main;
     return ok;
 }
-static int g_k10_nxr = 0;            // output plane count of the launch being issued (0: all nx)
+static thread_local int g_k10_nxr = 0;            // output plane count of the launch being issued (0: all nx)
 // Lockstep tile order: CTA b takes row tile b % nty and x chunk b / nty, so the CTAs
 // resident together cover contiguous bands of row tiles marching the same x planes
 // and a tile's y-halo rows -- its neighbours' main rows -- are read from L2, not HBM
 // (ncu at 256^3 / 512^3 with contiguous x ranges: 1.38x / 1.40x the algorithmic DRAM
 // bytes).  One CTA per (tile, chunk); chunks of >= 8 planes.  OTM_K10_LOCK=0: the
 // contiguous per-CTA ranges of round 1.
-static int g_k10_lock = 0;
+static thread_local int g_k10_lock = 0;
 template <class K>
 static dim3 k10_grid(K kernel, size_t smem, const Geo& g, int TY) {
     int dev = 0, sms = 148, per_sm = 1;
@@ -2692,7 +2694,7 @@ void launch_submean(cudaStream_t s, long long n, double* T, const double* sumT) 
 // x chunks per (y, z) column: about 2 waves of the kernel's resident threads,
 // >= 4 planes each (a chunk reloads its first plane)
 void launch_tensor(cudaStream_t s, const Geo& g, const double* T, const double* kap, Red& red, double* out6) {
-    static int ch = 0, for_pl = -1, for_nx = -1;
+    static thread_local int ch = 0, for_pl = -1, for_nx = -1;
     if (for_pl != g.pl || for_nx != g.nx) { ch = march_chunks(k_tensor_x, g); for_pl = g.pl; for_nx = g.nx; }
     const long long th = (long long)g.pl * ch;
     k_tensor_x<<<nblk(th, 256), 256, 0, s>>>(g, ch, T, kap, red.partials, red.counter, out6);
@@ -2702,7 +2704,7 @@ void launch_pair_energy(cudaStream_t s, const Geo& g, const double* T, double* E
 }
 void launch_sens(cudaStream_t s, const Geo& g, const double* T, const double* rf, const SimpParams& sp,
                  const Dg& dG, double* sens, const Dg* dG_dev) {
-    static int ch = 0, for_pl = -1, for_nx = -1;
+    static thread_local int ch = 0, for_pl = -1, for_nx = -1;
     if (for_pl != g.pl || for_nx != g.nx) { ch = march_chunks(k_sens_x, g); for_pl = g.pl; for_nx = g.nx; }
     const long long th = (long long)g.pl * ch;
     k_sens_x<<<nblk(th, 256), 256, 0, s>>>(g, ch, T, rf, sp, dG, dG_dev, sens);

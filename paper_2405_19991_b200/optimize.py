@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import threading
 import warnings
 from dataclasses import dataclass, field as dc_field
 from enum import Enum
@@ -332,7 +333,19 @@ class DesignRun:
         return self.hier.ctx.lib.otm_last_error(self.hier.ctx.h).decode()
 
 
-_HIER_CACHE: dict = {}
+_HIER_CACHE: dict = {}          # the main thread's; every other host thread has its own
+_TLS = threading.local()
+
+
+def _hier_cache() -> dict:
+    """Per host thread: runs issued from several threads at once (structures designed
+    concurrently on one GPU, each on its own hierarchy and stream) never share one."""
+    if threading.current_thread() is threading.main_thread():
+        return _HIER_CACHE
+    cache = getattr(_TLS, "cache", None)
+    if cache is None:
+        cache = _TLS.cache = {}
+    return cache
 
 
 def _cached_hierarchy(config: RunConfig):
@@ -344,11 +357,12 @@ def _cached_hierarchy(config: RunConfig):
     mp = config.material
     key = (tuple(int(d) for d in config.dims), float(mp.kappa0), float(mp.kappa_min), float(mp.penalty),
            float(config.filter.radius), _dev.torch().cuda.current_device())
-    h = _HIER_CACHE.get(key)
+    cache = _hier_cache()
+    h = cache.get(key)
     if h is None:
-        _HIER_CACHE.clear()            # one grid at a time: 512^3 needs ~20 GB
+        cache.clear()                  # one grid at a time per thread: 512^3 needs ~20 GB
         h = GridHierarchy(config.dims, material=mp, filter_radius=config.filter.radius)
-        _HIER_CACHE[key] = h
+        cache[key] = h
     return h
 
 

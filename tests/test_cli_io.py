@@ -158,6 +158,17 @@ class TestCliGpu:
         assert len(lines) == 62 and all(l.endswith(",ok") for l in lines[1:])
         assert (tmp_path / "case_060" / "manifest.json").exists()
 
+    def test_gallery_cases_at_once_match_one_at_a_time(self, tmp_path):
+        """--per-gpu K: K cases designed concurrently from K host threads (own
+        hierarchy and stream each) give the same results as one at a time."""
+        from paper_2405_19991_b200.cli import run_gallery
+        one = run_gallery([0.3, 0.2, 0.1], 0.1, tmp_path / "one", reso=(16, 16, 16), max_iter=6)
+        four = run_gallery([0.3, 0.2, 0.1], 0.1, tmp_path / "four", reso=(16, 16, 16), max_iter=6, per_gpu=4)
+        assert len(one) == len(four) > 4
+        for a, b in zip(one, four):
+            assert a[0] == b[0] and a[5] == b[5] == "ok"
+            assert a[2] == b[2] and a[3] == b[3]          # g and volume, bit for bit
+
 
 class TestReferenceBytes:
     """Every output file byte-identical to what the reference's own writers produce
