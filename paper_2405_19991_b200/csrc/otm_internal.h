@@ -80,6 +80,15 @@ struct PcgScalars {
                          // the T update and the trailing fp64 defect pass become no-ops
 };
 
+// Output x-plane range of a level kernel and the divisor of its sums: the whole
+// periodic grid ([0, nx), n), or a slab's interior planes [1, nxl + 1) of a ghosted
+// array of nxl + 2 planes (the slab path, otm_slab.cu), whose neighbour planes are
+// the ghosts -- no index wraps -- and whose sums are partials of the global ones.
+struct XRange {
+    int xa, xb;
+    double norm;
+};
+
 // Deterministic two-stage reduction workspace.
 struct Red {
     double* partials;    // >= max blocks * 32 doubles
@@ -101,6 +110,10 @@ void launch_filter(cudaStream_t s, const Geo& g, const FilterSetup& fs, int adjo
                    double* out, Red& red);
 void launch_filter_simp(cudaStream_t s, const Geo& g, const FilterSetup& fs, const SimpParams& sp,
                         const double* rho, double* rho_f, double* k64, float* k32, Red& red, double* out4);
+// the z-pair filter kernel on the planes [xr.xa, xr.xb) (mode 2: + SIMP into k64 and the
+// sums of rho, rho^p, rho_f into out3; mode 1: adjoint); false if the shape has no pair kernel
+bool launch_filter_range(cudaStream_t s, const Geo& g, const FilterSetup& fs, int mode, const SimpParams& sp,
+                         const double* in, double* out, double* k64, Red& red, double* out3, const XRange& xr);
 void launch_simp(cudaStream_t s, long long n, const double* rf, double* k64, float* k32, const SimpParams& sp);
 void launch_set_kappa(cudaStream_t s, long long n, const double* kin, double* k64, float* k32);
 void launch_means(cudaStream_t s, long long n, const double* rho, double p, Red& red, double* out2);
@@ -113,10 +126,13 @@ void launch_coarse_solve(cudaStream_t s, int n, const float* G, const float* f, 
 void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
                   const double* fext, const double* fmean, float* r32, Red& red, double* out9,
                   const int* skip = nullptr);   // *skip != 0: no-op (device-side solve control)
+// k_res64p on the output planes [xr.xa, xr.xb); false if the shape has no k_res64p
+bool launch_res64_range(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
+                        const double* fmean, float* r32, Red& red, double* out9, const XRange& xr);
 void launch_apply64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
                     double* out, int load_case);
 void launch_load_means(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, Red& red,
-                       double* out3);
+                       double* out3, const XRange* xr = nullptr);
 void launch_sum3(cudaStream_t s, long long n, const double* f, Red& red, double* out3);
 void launch_smooth_res(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const float* kap, const float* f,
                        const float* dinv, float omega, float* z, float* res);
@@ -139,10 +155,12 @@ void launch_prolong(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3],
 void launch_Tupd(cudaStream_t s, long long n, double* T, const float* d, const float* p, const PcgScalars* sc);
 void launch_submean_means(cudaStream_t s, long long n, double* T, const double* means);
 void launch_submean(cudaStream_t s, long long n, double* T, const double* sumT);
-void launch_tensor(cudaStream_t s, const Geo& g, const double* T, const double* kap, Red& red, double* out6);
+void launch_tensor(cudaStream_t s, const Geo& g, const double* T, const double* kap, Red& red, double* out6,
+                   const XRange* xr = nullptr);
 void launch_pair_energy(cudaStream_t s, const Geo& g, const double* T, double* E);
 void launch_sens(cudaStream_t s, const Geo& g, const double* T, const double* rf, const SimpParams& sp,
-                 const Dg& dG, double* sens, const Dg* dG_dev = nullptr);   // dG_dev != NULL overrides dG
+                 const Dg& dG, double* sens, const Dg* dG_dev = nullptr,   // dG_dev != NULL overrides dG
+                 const XRange* xr = nullptr);
 void launch_oc_eval(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a, int nlam,
                     const LamSet& lam_pow, Red& red, double* out);
 int launch_oc_coop(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a,

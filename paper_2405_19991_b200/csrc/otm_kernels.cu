@@ -109,14 +109,15 @@ constexpr unsigned taps_no_corners() {
 constexpr unsigned kTapsNoCorners = taps_no_corners();
 
 template <int MODE, unsigned MASK = 0>
-__global__ void __launch_bounds__(256) k_filter_b(Geo g, FilterTaps taps, const double* __restrict__ in,
-                                                  double* __restrict__ out, double* __restrict__ kappa64,
-                                                  float* __restrict__ kappa32, SimpParams sp, double* partials,
-                                                  unsigned* counter, double* red_out) {
-    const long long npair = g.n >> 1;
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) k_filter_b(Geo g, long long p0, long long p1, FilterTaps taps,
+                                                  const double* __restrict__ in, double* __restrict__ out,
+                                                  double* __restrict__ kappa64, float* __restrict__ kappa32,
+                                                  SimpParams sp, double* partials, unsigned* counter,
+                                                  double* red_out) {
+    // z pairs [p0, p1): the whole grid, or a slab's interior planes (XRange)
+    const long long i = p0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
     double acc3[3] = {0.0, 0.0, 0.0};
-    if (i < npair) {
+    if (i < p1) {
         const long long vp = i * 2;
         // 32-bit index arithmetic (fields < 2^31 vertices; see element_energies)
         const unsigned uv = (unsigned)vp, upl = (unsigned)g.pl;
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(256) k_filter_b(Geo g, FilterTaps taps, const 
             double k0 = sp.kmin + simp_pow(res[0], sp.p) * (sp.k0 - sp.kmin);
             double k1 = sp.kmin + simp_pow(res[1], sp.p) * (sp.k0 - sp.kmin);
             *reinterpret_cast<double2*>(kappa64 + vp) = make_double2(k0, k1);
-            *reinterpret_cast<float2*>(kappa32 + vp) = make_float2((float)k0, (float)k1);
+            if (kappa32) *reinterpret_cast<float2*>(kappa32 + vp) = make_float2((float)k0, (float)k1);
             const double r0 = t[1][1][1], r1 = t[1][1][2];
             acc3[0] = r0 + r1;
             acc3[1] = simp_pow(r0, sp.p) + simp_pow(r1, sp.p);
@@ -675,7 +676,7 @@ __global__ void __launch_bounds__(128) k_apply64(Geo g, int xb, LevelTemplate lt
 // One (y, z) column per thread marching x: the element factors of plane x - 1
 // carry over (4 loads per vertex instead of 8, no per-vertex index division); each
 // vertex's load is the fixed-order sum of its 8 element terms.
-__global__ void __launch_bounds__(256) k_load_means_x(Geo g, int chunks, LevelTemplate lt,
+__global__ void __launch_bounds__(256) k_load_means_x(Geo g, int chunks, XRange xr, LevelTemplate lt,
                                                       const double* __restrict__ kap, double* partials,
                                                       unsigned* counter, double* out) {
     double v3[3] = {0.0, 0.0, 0.0};
@@ -687,8 +688,8 @@ __global__ void __launch_bounds__(256) k_load_means_x(Geo g, int chunks, LevelTe
         const unsigned ym = y == 0 ? (unsigned)g.ny - 1 : y - 1, zm = z == 0 ? (unsigned)g.nz - 1 : z - 1;
         // slot (dy, dz) = element (y - dy, z - dz)
         const unsigned o[4] = {y * g.nz + z, y * g.nz + zm, ym * g.nz + z, ym * g.nz + zm};
-        const int per = (g.nx + chunks - 1) / chunks;
-        const int x0 = (int)c * per, x1 = min(g.nx, x0 + per);
+        const int per = (xr.xb - xr.xa + chunks - 1) / chunks;
+        const int x0 = xr.xa + (int)c * per, x1 = min(xr.xb, x0 + per);
         if (x0 < x1) {
             double P[4], Q[4];
             const unsigned pm = (unsigned)(x0 == 0 ? g.nx - 1 : x0 - 1) * cols;
@@ -714,7 +715,7 @@ __global__ void __launch_bounds__(256) k_load_means_x(Geo g, int chunks, LevelTe
         }
     }
     if (reduce_finalize<3>(v3, partials, counter, out)) {
-        for (int c = 0; c < 3; ++c) out[c] /= (double)g.n;
+        for (int c = 0; c < 3; ++c) out[c] /= xr.norm;
     }
 }
 
@@ -1470,7 +1471,8 @@ __device__ __forceinline__ void energies_wht(const double (&A)[3][4], const doub
 }
 
 // one (y, z) column and a chunk [x0, x1) of planes per thread
-__device__ __forceinline__ bool march_setup(const Geo& g, int chunks, MarchCol& q, int& x0, int& x1) {
+__device__ __forceinline__ bool march_setup(const Geo& g, int chunks, int xa, int xb, MarchCol& q, int& x0,
+                                            int& x1) {
     const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
     const unsigned cols = (unsigned)g.pl;
     if (t >= cols * (unsigned)chunks) return false;
@@ -1481,19 +1483,19 @@ __device__ __forceinline__ bool march_setup(const Geo& g, int chunks, MarchCol& 
     q.o01 = y * g.nz + zp;
     q.o10 = yp * g.nz + z;
     q.o11 = yp * g.nz + zp;
-    const int per = (g.nx + chunks - 1) / chunks;
-    x0 = (int)c * per;
-    x1 = min(g.nx, x0 + per);
+    const int per = (xb - xa + chunks - 1) / chunks;
+    x0 = xa + (int)c * per;
+    x1 = min(xb, x0 + per);
     return x0 < x1;
 }
 
-__global__ void __launch_bounds__(256) k_tensor_x(Geo g, int chunks, const double* __restrict__ T,
+__global__ void __launch_bounds__(256) k_tensor_x(Geo g, int chunks, XRange xr, const double* __restrict__ T,
                                                   const double* __restrict__ kap, double* partials, unsigned* counter,
                                                   double* out) {
     double acc[6] = {0, 0, 0, 0, 0, 0};
     MarchCol q;
     int x0, x1;
-    if (march_setup(g, chunks, q, x0, x1)) {
+    if (march_setup(g, chunks, xr.xa, xr.xb, q, x0, x1)) {
         // planes x and x + 1 in registers, plane x + 2 prefetched while x is consumed
         double A[3][4], B[3][4], Cn[3][4];
         load_plane(T, g.n, (unsigned)x0 * (unsigned)g.pl, q, A);
@@ -1518,21 +1520,21 @@ __global__ void __launch_bounds__(256) k_tensor_x(Geo g, int chunks, const doubl
         }
     }
     if (reduce_finalize<6>(acc, partials, counter, out)) {
-        for (int c = 0; c < 6; ++c) out[c] /= (double)g.n;
+        for (int c = 0; c < 6; ++c) out[c] /= xr.norm;
     }
 }
 
-__global__ void __launch_bounds__(256) k_sens_x(Geo g, int chunks, const double* __restrict__ T,
+__global__ void __launch_bounds__(256) k_sens_x(Geo g, int chunks, XRange xr, const double* __restrict__ T,
                                                 const double* __restrict__ rf, SimpParams sp, Dg dG,
                                                 const Dg* __restrict__ dG_dev, double* __restrict__ sens) {
     MarchCol q;
     int x0, x1;
-    if (!march_setup(g, chunks, q, x0, x1)) return;
+    if (!march_setup(g, chunks, xr.xa, xr.xb, q, x0, x1)) return;
     if (dG_dev) dG = *dG_dev;               // objective weights computed on the device (otm_loop.cu)
     double A[3][4], B[3][4], Cn[3][4];
     load_plane(T, g.n, (unsigned)x0 * (unsigned)g.pl, q, A);
     load_plane(T, g.n, (unsigned)(x0 + 1 == g.nx ? 0 : x0 + 1) * (unsigned)g.pl, q, B);
-    const double scale = (sp.k0 - sp.kmin) * sp.p / (double)g.n;
+    const double scale = (sp.k0 - sp.kmin) * sp.p / xr.norm;
     for (int x = x0; x < x1; ++x) {
         if (x + 1 < x1) {
             const int xn = x + 2 >= g.nx ? x + 2 - g.nx : x + 2;
@@ -2116,20 +2118,31 @@ static inline dim3 stencil_grid(const Geo& g, int* xb) {
 template <int MODE>
 static void launch_filter_b(cudaStream_t s, const Geo& g, const FilterSetup& fs, const double* in, double* out,
                             double* k64, float* k32, const SimpParams& sp, double* partials, unsigned* counter,
-                            double* out3) {
+                            double* out3, const XRange* xr = nullptr) {
     FilterTaps taps;
     unsigned mask = 0;
     for (int i = 0; i < 27; ++i) {
         taps.w27[i] = fs.w27[i];
         if (fs.w27[i] != 0.0) mask |= 1u << i;
     }
-    const unsigned blocks = nblk(g.n >> 1, 256);
+    const long long p0 = xr ? (long long)xr->xa * g.pl / 2 : 0, p1 = xr ? (long long)xr->xb * g.pl / 2 : g.n >> 1;
+    const unsigned blocks = nblk(p1 - p0, 256);
     if (mask == kTapsNoCorners)
-        k_filter_b<MODE, kTapsNoCorners><<<blocks, 256, 0, s>>>(g, taps, in, out, k64, k32, sp, partials, counter, out3);
+        k_filter_b<MODE, kTapsNoCorners><<<blocks, 256, 0, s>>>(g, p0, p1, taps, in, out, k64, k32, sp, partials,
+                                                                counter, out3);
     else if (mask == kTapsAll)
-        k_filter_b<MODE, kTapsAll><<<blocks, 256, 0, s>>>(g, taps, in, out, k64, k32, sp, partials, counter, out3);
+        k_filter_b<MODE, kTapsAll><<<blocks, 256, 0, s>>>(g, p0, p1, taps, in, out, k64, k32, sp, partials, counter,
+                                                          out3);
     else
-        k_filter_b<MODE, 0><<<blocks, 256, 0, s>>>(g, taps, in, out, k64, k32, sp, partials, counter, out3);
+        k_filter_b<MODE, 0><<<blocks, 256, 0, s>>>(g, p0, p1, taps, in, out, k64, k32, sp, partials, counter, out3);
+}
+
+bool launch_filter_range(cudaStream_t s, const Geo& g, const FilterSetup& fs, int mode, const SimpParams& sp,
+                         const double* in, double* out, double* k64, Red& red, double* out3, const XRange& xr) {
+    if (!fs.window || g.nz % 2 != 0) return false;
+    if (mode == 2) launch_filter_b<2>(s, g, fs, in, out, k64, nullptr, sp, red.partials, red.counter, out3, &xr);
+    else launch_filter_b<1>(s, g, fs, in, out, nullptr, nullptr, sp, nullptr, nullptr, nullptr, &xr);
+    return true;
 }
 
 void launch_filter(cudaStream_t s, const Geo& g, const FilterSetup& fs, int adjoint, const double* in,
@@ -2256,19 +2269,39 @@ static void l_res64p(cudaStream_t s, const Geo& g, const LevelTemplate& lt, cons
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_res64p<NZ>, P::THREADS, P::SMEM);
     if (per_sm < 1) per_sm = 1;
-    const long long nty = g.ny / P::TY, units = nty * g.nx, slots = (long long)per_sm * sms;
+    const int nxr = M0.xb - M0.xa;
+    const long long nty = g.ny / P::TY, units = nty * nxr, slots = (long long)per_sm * sms;
     R64PMaps M = M0;
     M.lock = 0;
     long long blocks = std::min(slots, units);
     // lockstep row-tile order where the three fp64 cases (24 B per vertex) exceed half the L2
     static const bool lock_on = !(getenv("OTM_K10_LOCK") && atoi(getenv("OTM_K10_LOCK")) == 0);
-    if (lock_on && g.n * 24 > (64LL << 20)) {
-        const long long k = std::max<long long>(1, std::min<long long>(slots / nty, g.nx / 8));
+    if (lock_on && (long long)nxr * g.pl * 24 > (64LL << 20)) {
+        const long long k = std::max<long long>(1, std::min<long long>(slots / nty, nxr / 8));
         M.lock = (int)k;
         blocks = nty * k;
     }
     k_res64p<NZ><<<(unsigned)blocks, dim3(NZ, P::TY), P::SMEM, s>>>(g, lt, M, fmean, r32, red.partials, red.counter,
                                                                     out9, skip);
+}
+
+bool launch_res64_range(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
+                        const double* fmean, float* r32, Red& red, double* out9, const XRange& xr) {
+    if (!lt.equal || !(g.nz == 64 || g.nz == 128 || g.nz == 256) || xr.xa < 1 || xr.xb > g.nx - 1 || xr.xb <= xr.xa)
+        return false;
+    const int ty = g.nz >= 256 ? 1 : 256 / g.nz;
+    if (g.ny % ty != 0 || g.ny < 2 * ty) return false;
+    R64PMaps M;
+    if (!(encode_map64c(&M.t_full, T, g, ty + 2) && encode_map64c(&M.t_main, T, g, ty) &&
+          encode_map64c(&M.t_halo, T, g, 1) && encode_map64(&M.k_full, kap, g.nz, g.ny, g.nx, ty + 1) &&
+          encode_map64(&M.k_main, kap, g.nz, g.ny, g.nx, ty) && encode_map64(&M.k_halo, kap, g.nz, g.ny, g.nx, 1)))
+        return false;
+    M.xa = xr.xa;
+    M.xb = xr.xb;
+    if (g.nz == 64) l_res64p<64>(s, g, lt, M, fmean, r32, red, out9, nullptr);
+    else if (g.nz == 128) l_res64p<128>(s, g, lt, M, fmean, r32, red, out9, nullptr);
+    else l_res64p<256>(s, g, lt, M, fmean, r32, red, out9, nullptr);
+    return true;
 }
 
 void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
@@ -2296,6 +2329,8 @@ void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const d
                 lastdims[2] = g.nz;
             }
             if (lastok) {
+                M.xa = 0;
+                M.xb = g.nx;
                 if (g.nz == 64) l_res64p<64>(s, g, lt, M, fmean, r32, red, out9, skip);
                 else if (g.nz == 128) l_res64p<128>(s, g, lt, M, fmean, r32, red, out9, skip);
                 else l_res64p<256>(s, g, lt, M, fmean, r32, red, out9, skip);
@@ -2378,21 +2413,34 @@ void launch_apply64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const
     k_apply64<<<grid, 128, 0, s>>>(g, xb, lt, kap, T, out, load_case);
 }
 template <class K>
-static int march_chunks(K kernel, const Geo& g) {
+static int march_chunks(K kernel, const Geo& g, int planes) {
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
     const long long want = 2LL * sms * std::max(per_sm, 1) * 256;
     long long c = (want + g.pl - 1) / g.pl;
-    c = std::min<long long>(c, std::max(1, g.nx / 4));
+    c = std::min<long long>(c, std::max(1, planes / 4));
     return (int)std::max<long long>(1, c);
 }
+static XRange whole(const Geo& g, const XRange* xr) { return xr ? *xr : XRange{0, g.nx, (double)g.n}; }
+// x chunks per (y, z) column of a marching kernel, cached per (plane size, plane count)
+template <class K>
+static int chunks_for(K kernel, const Geo& g, int planes, int& ch, int& for_pl, int& for_np) {
+    if (for_pl != g.pl || for_np != planes) {
+        ch = march_chunks(kernel, g, planes);
+        for_pl = g.pl;
+        for_np = planes;
+    }
+    return ch;
+}
 void launch_load_means(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, Red& red,
-                       double* out3) {
-    static thread_local int ch = 0, for_pl = -1, for_nx = -1;
-    if (for_pl != g.pl || for_nx != g.nx) { ch = march_chunks(k_load_means_x, g); for_pl = g.pl; for_nx = g.nx; }
-    k_load_means_x<<<nblk((long long)g.pl * ch, 256), 256, 0, s>>>(g, ch, lt, kap, red.partials, red.counter, out3);
+                       double* out3, const XRange* xr) {
+    static thread_local int ch = 0, for_pl = -1, for_np = -1;
+    const XRange r = whole(g, xr);
+    chunks_for(k_load_means_x, g, r.xb - r.xa, ch, for_pl, for_np);
+    k_load_means_x<<<nblk((long long)g.pl * ch, 256), 256, 0, s>>>(g, ch, r, lt, kap, red.partials, red.counter,
+                                                                   out3);
 }
 void launch_sum3(cudaStream_t s, long long n, const double* f, Red& red, double* out3) {
     k_sum3<<<592, 256, 0, s>>>(n, f, red.partials, red.counter, out3);
@@ -2693,21 +2741,24 @@ void launch_submean(cudaStream_t s, long long n, double* T, const double* sumT) 
 }
 // x chunks per (y, z) column: about 2 waves of the kernel's resident threads,
 // >= 4 planes each (a chunk reloads its first plane)
-void launch_tensor(cudaStream_t s, const Geo& g, const double* T, const double* kap, Red& red, double* out6) {
-    static thread_local int ch = 0, for_pl = -1, for_nx = -1;
-    if (for_pl != g.pl || for_nx != g.nx) { ch = march_chunks(k_tensor_x, g); for_pl = g.pl; for_nx = g.nx; }
+void launch_tensor(cudaStream_t s, const Geo& g, const double* T, const double* kap, Red& red, double* out6,
+                   const XRange* xr) {
+    static thread_local int ch = 0, for_pl = -1, for_np = -1;
+    const XRange r = whole(g, xr);
+    chunks_for(k_tensor_x, g, r.xb - r.xa, ch, for_pl, for_np);
     const long long th = (long long)g.pl * ch;
-    k_tensor_x<<<nblk(th, 256), 256, 0, s>>>(g, ch, T, kap, red.partials, red.counter, out6);
+    k_tensor_x<<<nblk(th, 256), 256, 0, s>>>(g, ch, r, T, kap, red.partials, red.counter, out6);
 }
 void launch_pair_energy(cudaStream_t s, const Geo& g, const double* T, double* E) {
     k_pair_energy<<<nblk(g.n, 256), 256, 0, s>>>(g, T, E);
 }
 void launch_sens(cudaStream_t s, const Geo& g, const double* T, const double* rf, const SimpParams& sp,
-                 const Dg& dG, double* sens, const Dg* dG_dev) {
-    static thread_local int ch = 0, for_pl = -1, for_nx = -1;
-    if (for_pl != g.pl || for_nx != g.nx) { ch = march_chunks(k_sens_x, g); for_pl = g.pl; for_nx = g.nx; }
+                 const Dg& dG, double* sens, const Dg* dG_dev, const XRange* xr) {
+    static thread_local int ch = 0, for_pl = -1, for_np = -1;
+    const XRange r = whole(g, xr);
+    chunks_for(k_sens_x, g, r.xb - r.xa, ch, for_pl, for_np);
     const long long th = (long long)g.pl * ch;
-    k_sens_x<<<nblk(th, 256), 256, 0, s>>>(g, ch, T, rf, sp, dG, dG_dev, sens);
+    k_sens_x<<<nblk(th, 256), 256, 0, s>>>(g, ch, r, T, rf, sp, dG, dG_dev, sens);
 }
 void launch_oc_eval(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a, int nlam,
                     const LamSet& lam_pow, Red& red, double* out) {

@@ -40,6 +40,7 @@ struct R64PMaps {
     CUtensorMap t_full, t_main, t_halo;      // 4-D (z, case, y, x) fp64: TY + 2 / TY / 1 rows
     CUtensorMap k_full, k_main, k_halo;      // 3-D (z, y, x) fp64: TY + 1 / TY / 1 rows
     int lock;                                // as K10Maps::lock (lockstep row-tile order beyond L2)
+    int xa, xb;                              // output x planes [xa, xb) (as K10Maps)
 };
 
 // element factors of one element plane around the vertex: corners c[jj][kk] =
@@ -80,12 +81,13 @@ __global__ void __launch_bounds__(R64P<NZ>::THREADS, R64P<NZ>::CPS)
     const double fm[3] = {fmean[0], fmean[1], fmean[2]};
     const unsigned n = (unsigned)g.n, pl = (unsigned)g.pl;
     const int nty = g.ny / TY;
-    const long long W = (long long)nty * g.nx;
+    const int nxr = maps.xb - maps.xa;
+    const long long W = (long long)nty * nxr;
     long long u, u1;
     if (maps.lock > 0) {
         const int yt = (int)(blockIdx.x % (unsigned)nty), c = (int)(blockIdx.x / (unsigned)nty);
-        u = (long long)yt * g.nx + (long long)g.nx * c / maps.lock;
-        u1 = (long long)yt * g.nx + (long long)g.nx * (c + 1) / maps.lock;
+        u = (long long)yt * nxr + (long long)nxr * c / maps.lock;
+        u1 = (long long)yt * nxr + (long long)nxr * (c + 1) / maps.lock;
     } else {
         u = W * blockIdx.x / gridDim.x;
         u1 = W * (blockIdx.x + 1) / gridDim.x;
@@ -130,9 +132,9 @@ __global__ void __launch_bounds__(R64P<NZ>::THREADS, R64P<NZ>::CPS)
         return a + b;
     };
     while (u < u1) {
-        const int yt = (int)(u / g.nx);
-        const int x0 = (int)(u - (long long)yt * g.nx);
-        const int x1 = (int)min((long long)g.nx, x0 + (u1 - u));
+        const int yt = (int)(u / nxr);
+        const int x0 = maps.xa + (int)(u - (long long)yt * nxr);
+        const int x1 = (int)min((long long)maps.xb, x0 + (u1 - u));
         const int y0 = yt * TY;
         const bool seam = (y0 == 0) || (y0 + TY == g.ny);
         const int ym = y0 == 0 ? g.ny - 1 : y0 - 1;

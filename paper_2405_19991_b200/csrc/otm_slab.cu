@@ -510,46 +510,58 @@ __global__ void __launch_bounds__(256) ks_sens(SGeo g, const double* __restrict_
     sens[idx] = dk * con / M;
 }
 
-// OC candidate sums for up to 32 multipliers (optimize.py:114-160, the reference's
-// candidate expression); lam == 0 is the free step.  APPLY: write the candidate of
-// lams[0] and count changed vertices.
-template <bool APPLY>
-__global__ void __launch_bounds__(256) ks_oc(SGeo g, const double* __restrict__ rho,
-                                             const double* __restrict__ sens, OcArgs a, double M, LamSet lams,
-                                             int nlam, double* __restrict__ rho_out, double* partials,
-                                             unsigned* counter, double* out32) {
+// OC candidate sums for up to 32 multipliers (optimize.py:114-160) over the slab's
+// interior (contiguous: planes 1 .. nxl).  The candidate clip(rho * max(desc/lam,
+// 1e-10)^damp, lo, hi) is evaluated as clip(max(c_e lam^-damp, rho 1e-10^damp), lo,
+// hi) with c_e = rho desc^damp formed once per element (the single-GPU search's form,
+// k_oc_coop); lam_pow[k] = lam^-damp, 0 for the free step (lam = 0).
+__global__ void __launch_bounds__(256) ks_oc_sums(SGeo g, const double* __restrict__ rho,
+                                                  const double* __restrict__ sens, OcArgs a, double M, LamSet lam_pow,
+                                                  double* partials, unsigned* counter, double* out32) {
     double acc[32];
 #pragma unroll
     for (int k = 0; k < 32; ++k) acc[k] = 0.0;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < g.ni; i += (long long)gridDim.x * blockDim.x) {
-        int x, y, z;
-        s_decode(g, i, x, y, z);
-        const long long idx = (long long)x * g.pl + y * g.nz + z;
+        const long long idx = g.pl + i;
+        const double r = __ldg(rho + idx);
+        const double desc = M * (-__ldg(sens + idx));
+        const double lo = fmax(r - a.step, a.rmin), hi = fmin(r + a.step, 1.0);
+        const double lof = fmax(lo, r * a.floor_ratio);
+        const double ce = desc > 0.0 ? r * (a.sqrt_damp ? sqrt(desc) : pow(desc, a.damp)) : 0.0;
+        const double freev = desc > 0.0 ? hi : (desc < 0.0 ? lo : r);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            const double lp = lam_pow.v[k];
+            acc[k] += lp == 0.0 ? freev : fmin(fmax(ce * lp, lof), hi);
+        }
+    }
+    reduce_finalize32(acc, partials, counter, out32);
+}
+
+// the update with the chosen multiplier, the reference's exact expression
+// (optimize.py:131-138, bit-identical to k_oc_apply); out[0] = changed elements
+__global__ void __launch_bounds__(256) ks_oc_apply(SGeo g, const double* rho,          // may alias rho_out
+                                                   const double* __restrict__ sens, OcArgs a, double M, double lam,
+                                                   double* rho_out, double* partials, unsigned* counter,
+                                                   double* out) {
+    double acc[1] = {0.0};
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < g.ni; i += (long long)gridDim.x * blockDim.x) {
+        const long long idx = g.pl + i;
         const double r = rho[idx];
         const double desc = M * (-sens[idx]);
         const double lo = fmax(r - a.step, a.rmin), hi = fmin(r + a.step, 1.0);
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-            if (k < nlam) {
-                const double lam = lams.v[k];
-                double out;
-                if (lam == 0.0) {
-                    out = desc > 0.0 ? hi : (desc < 0.0 ? lo : r);
-                } else {
-                    const double qv = fmax(desc / lam, 1e-10);
-                    const double ratio = a.sqrt_damp ? sqrt(qv) : pow(qv, a.damp);
-                    out = fmin(fmax(r * ratio, lo), hi);
-                }
-                if (APPLY) {
-                    rho_out[idx] = out;
-                    acc[0] += out != r ? 1.0 : 0.0;
-                    break;
-                }
-                acc[k] += out;
-            }
+        double o;
+        if (lam == 0.0) {
+            o = desc > 0.0 ? hi : (desc < 0.0 ? lo : r);
+        } else {
+            const double q = fmax(desc / lam, 1e-10);
+            const double ratio = a.sqrt_damp ? sqrt(q) : pow(q, a.damp);
+            o = fmin(fmax(r * ratio, lo), hi);
         }
+        rho_out[idx] = o;
+        acc[0] += o != r ? 1.0 : 0.0;
     }
-    if (reduce_finalize32(acc, partials, counter, out32)) {}
+    reduce_finalize<1>(acc, partials, counter, out);
 }
 
 inline unsigned nb(long long n, int bs) { return (unsigned)((n + bs - 1) / bs); }
@@ -627,6 +639,12 @@ static int sfetch(otm_slab_ws* w, int nq, double* out) {
     SCK(cudaStreamSynchronize(w->stream));
     std::memcpy(out, w->h, nq * sizeof(double));
     return OTM_OK;
+}
+// OTM_SLAB_GENERIC=1: the slab's own per-element kernels instead of the single-GPU
+// marching / TMA kernels restricted to the interior planes (A/B and fallback)
+static bool fast_off() {
+    static const bool v = getenv("OTM_SLAB_GENERIC") && atoi(getenv("OTM_SLAB_GENERIC")) != 0;
+    return v;
 }
 static LevelTemplate tmpl(const double scale[3]) {
     LevelTemplate lt;
@@ -790,8 +808,14 @@ int otm_slab_load_sums(otm_slab_ws* w, int nxl, int ny, int nz, const double sca
     const SGeo g = make_sgeo(nxl, ny, nz);
     if (!blocks_ok(w, g.ni, 128)) return OTM_EINVAL;
     const LevelTemplate lt = tmpl(scale);
-    ks_res64<0><<<nbr(g.ni, 128), 128, 0, w->stream>>>(g, lt, kap64, nullptr, nullptr, nullptr, w->partials,
-                                                       w->counter, w->out);
+    if (!fast_off()) {
+        Red red{w->partials, w->counter};
+        const XRange xr{1, nxl + 1, 1.0};
+        launch_load_means(w->stream, make_geo(nxl + 2, ny, nz), lt, kap64, red, w->out, &xr);
+    } else {
+        ks_res64<0><<<nbr(g.ni, 128), 128, 0, w->stream>>>(g, lt, kap64, nullptr, nullptr, nullptr, w->partials,
+                                                           w->counter, w->out);
+    }
     int rc = scheck(w);
     if (rc) return rc;
     double o[9];
@@ -808,6 +832,15 @@ int otm_slab_res64(otm_slab_ws* w, int nxl, int ny, int nz, const double scale[3
     if (!blocks_ok(w, g.ni, 128)) return OTM_EINVAL;
     const LevelTemplate lt = tmpl(scale);
     SCK(cudaMemcpyAsync(w->out + 9, fmean3, 3 * sizeof(double), cudaMemcpyHostToDevice, w->stream));
+    // the single-GPU push march (k_res64p) on the interior planes of the ghosted slab
+    Red red{w->partials, w->counter};
+    const XRange xr{1, nxl + 1, 1.0};
+    if (!fast_off() && launch_res64_range(w->stream, make_geo(nxl + 2, ny, nz), lt, kap64, T, w->out + 9, r32, red,
+                                          w->out, xr)) {
+        int rc = scheck(w);
+        if (rc) return rc;
+        return sfetch(w, 9, sums9);
+    }
     ks_res64<1><<<nbr(g.ni, 128), 128, 0, w->stream>>>(g, lt, kap64, T, w->out + 9, r32, w->partials, w->counter,
                                                        w->out);
     int rc = scheck(w);
@@ -828,8 +861,15 @@ int otm_slab_tensor_sums(otm_slab_ws* w, int nxl, int ny, int nz, const double s
     const SGeo g = make_sgeo(nxl, ny, nz);
     if (!blocks_ok(w, g.ni, 256)) return OTM_EINVAL;
     const LevelTemplate lt = tmpl(scale);
-    SCK(cudaMemcpyAsync(w->out + 8, lt.kt, 8 * sizeof(double), cudaMemcpyHostToDevice, w->stream));
-    ks_tensor<<<nbr(g.ni, 256), 256, 0, w->stream>>>(g, T, kap64, w->out + 8, w->partials, w->counter, w->out);
+    if (!fast_off() && scale[0] == 1.0 && scale[1] == 1.0 && scale[2] == 1.0) {
+        // k_tensor_x (energies in the Walsh-Hadamard basis of the unit element) on the interior
+        Red red{w->partials, w->counter};
+        const XRange xr{1, nxl + 1, 1.0};
+        launch_tensor(w->stream, make_geo(nxl + 2, ny, nz), T, kap64, red, w->out, &xr);
+    } else {
+        SCK(cudaMemcpyAsync(w->out + 8, lt.kt, 8 * sizeof(double), cudaMemcpyHostToDevice, w->stream));
+        ks_tensor<<<nbr(g.ni, 256), 256, 0, w->stream>>>(g, T, kap64, w->out + 8, w->partials, w->counter, w->out);
+    }
     int rc = scheck(w);
     if (rc) return rc;
     return sfetch(w, 6, sums6);
@@ -856,6 +896,17 @@ int otm_slab_filter(otm_slab_ws* w, int mode, int nxl, int ny, int nz, double ra
     sp.k0 = kappa0;
     sp.kmin = kappa_min;
     sp.p = penalty;
+    FilterSetup fs{};
+    fs.window = 1;
+    for (int i = 0; i < 27; ++i) fs.w27[i] = taps.w[i];
+    Red red{w->partials, w->counter};
+    const XRange xr{1, nxl + 1, 1.0};
+    if (!fast_off() &&
+        launch_filter_range(w->stream, make_geo(nxl + 2, ny, nz), fs, mode, sp, in, out, kap64, red, w->out, xr)) {
+        int rc = scheck(w);
+        if (rc || mode == 1) return rc;
+        return sfetch(w, 3, sums3);
+    }
     if (mode == 2)
         ks_filter<2><<<nbr(g.ni, 256), 256, 0, w->stream>>>(g, taps, in, out, kap64, sp, w->partials, w->counter,
                                                             w->out);
@@ -880,6 +931,11 @@ int otm_slab_sensitivity(otm_slab_ws* w, int nxl, int ny, int nz, double n_total
     sp.p = penalty;
     Dg dg;
     for (int q = 0; q < 6; ++q) dg.v[q] = dG6[q];
+    if (!fast_off()) {
+        const XRange xr{1, nxl + 1, n_total};
+        launch_sens(w->stream, make_geo(nxl + 2, ny, nz), T, rho_f, sp, dg, sens_f, nullptr, &xr);
+        return scheck(w);
+    }
     ks_sens<<<nb(g.ni, 256), 256, 0, w->stream>>>(g, T, rho_f, w->out + 8, sp, dg, n_total, sens_f);
     return scheck(w);
 }
@@ -896,9 +952,12 @@ int otm_slab_oc_sums(otm_slab_ws* w, int nxl, int ny, int nz, double n_total, co
     a.floor_ratio = std::pow(1e-10, pp->damp);
     a.sqrt_damp = pp->damp == 0.5;
     LamSet ls;
-    for (int k = 0; k < 32; ++k) ls.v[k] = k < nlam ? lams[k] : 0.0;
-    ks_oc<false><<<nbr(g.ni, 256), 256, 0, w->stream>>>(g, rho, sens, a, n_total, ls, nlam, nullptr, w->partials,
-                                                        w->counter, w->out32);
+    for (int k = 0; k < 32; ++k) {
+        const double lam = k < nlam ? lams[k] : 0.0;
+        ls.v[k] = lam == 0.0 ? 0.0 : (a.sqrt_damp ? 1.0 / std::sqrt(lam) : std::pow(lam, -a.damp));
+    }
+    ks_oc_sums<<<nbr(g.ni, 256), 256, 0, w->stream>>>(g, rho, sens, a, n_total, ls, w->partials, w->counter,
+                                                      w->out32);
     int rc = scheck(w);
     if (rc) return rc;
     SCK(cudaMemcpyAsync(w->h32, w->out32, 32 * sizeof(double), cudaMemcpyDeviceToHost, w->stream));
@@ -918,10 +977,7 @@ int otm_slab_oc_apply(otm_slab_ws* w, int nxl, int ny, int nz, double n_total, c
     a.damp = pp->damp;
     a.floor_ratio = std::pow(1e-10, pp->damp);
     a.sqrt_damp = pp->damp == 0.5;
-    LamSet ls;
-    for (int k = 0; k < 32; ++k) ls.v[k] = 0.0;
-    ls.v[0] = lam;
-    ks_oc<true><<<nbr(g.ni, 256), 256, 0, w->stream>>>(g, rho, sens, a, n_total, ls, 1, rho_out, w->partials,
+    ks_oc_apply<<<nbr(g.ni, 256), 256, 0, w->stream>>>(g, rho, sens, a, n_total, lam, rho_out, w->partials,
                                                        w->counter, w->out32);
     int rc = scheck(w);
     if (rc) return rc;

@@ -541,10 +541,13 @@ class SlabSolver:
     def solve(self, tol=1e-6, max_vcycles=200, check_every=4):
         """The batched MG-PCG with the PCG scalars on the device: dots are all-reduced in
         device memory and the recurrences run in a one-thread kernel
-        (otm_slab_pcg_step), so an inner iteration has no host round trip; the host
-        reads the active flags every `check_every` iterations (iterations after a case
-        converged apply alpha = 0 to it: no effect).  Every load case has its own budget
-        of `max_vcycles` preconditioner applications (homogenize.py:85-90)."""
+        (otm_slab_pcg_step), so an inner iteration has no host round trip.  The host
+        reads the active flags every `check_every` iterations, and after every
+        iteration from two before the previous solve's count on (iterations after a
+        case converged apply alpha = 0 to it: no effect on the result, but a whole
+        iteration of work -- at 256^3 one iteration costs ~1 ms, a flag read ~30 us).
+        Every load case has its own budget of `max_vcycles` preconditioner
+        applications (homogenize.py:85-90)."""
         B, L = self.B, self.L
         d0 = self.slabs[0].levels[0].dims
         sc0 = L.scales[0]
@@ -584,7 +587,9 @@ class SlabSolver:
             B.put(S, 15, rr)
             B.pcg_step(2, S)
 
+        first_loop = True
         while not done.all():
+            pred = self._inner_pred if first_loop else 1
             if ((~done) & (ccyc >= max_vcycles)).any():
                 from ._dev import ConvergenceError
                 raise ConvergenceError(f"slab solve did not converge in {max_vcycles} V-cycles per case",
@@ -606,11 +611,14 @@ class SlabSolver:
                     one_iteration()
                     if self._graph_ok and it == 0:
                         self._capture(one_iteration)
-                if (it + 1) % check_every == 0 or it + 1 == self.max_inner:
+                if (it + 1) % check_every == 0 or it + 1 >= pred - 2 or it + 1 == self.max_inner:
                     h = B.to_host(S)
                     active = h[21:24] != 0
                     if not active.any() or (active & (h[25:28] >= max_vcycles)).any():
                         break
+            if first_loop:
+                self._inner_pred = it + 1
+                first_loop = False
             h = B.to_host(S)
             ccyc = h[25:28].copy()
             for s in self.slabs:
@@ -630,6 +638,7 @@ class SlabSolver:
     # the GPU time at 256^3); in-process slabs only, unless OTM_SLAB_GRAPH=1 (NCCL
     # collectives inside a captured graph are untested on this single-GPU project)
     _pcg_graph = None
+    _inner_pred = 1          # inner iterations of the previous solve's first loop
 
     @property
     def _graph_ok(self):
