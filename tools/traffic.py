@@ -17,7 +17,7 @@ import sys
 
 rep, cfg, nx = sys.argv[1], sys.argv[2], int(sys.argv[3])
 n = nx ** 3
-ALG = {"k10_smooth_res": 44, "k10_jacobi": 44, "k10_spmv": 28, "k_res64w": 44,
+ALG = {"k10_smooth_res": 44, "k10_jacobi": 44, "k10_spmv": 28, "k_res64w": 44, "k_res64p": 44, "k_load_means_x": 8,
        "k_tensor_x": 32, "k_sens_x": 40, "k_filter_b<2>": 28, "k_filter_b<1>": 16}
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--print-units", "base"], capture_output=True,
                      text=True).stdout
@@ -26,7 +26,7 @@ h = rows[0]
 per, times = {}, {}
 for row in rows[2:]:
     name = row[h.index("Kernel Name")]
-    m = re.search(r"(k10_smooth_res|k10_jacobi|k10_spmv|k_res64w)<([^>]*)>", name)
+    m = re.search(r"(k10_smooth_res|k10_jacobi|k10_spmv|k_res64w|k_res64p)<([^>]*)>", name)
     if m:
         args = [a.strip() for a in m.group(2).split(",")]
         nums = [int(a) for a in args if a.lstrip("-").isdigit()]
@@ -34,7 +34,7 @@ for row in rows[2:]:
         if nz != nx:
             continue
     else:
-        m = re.search(r"(k_tensor_x|k_sens_x|k_filter_b<[12]>)", name)
+        m = re.search(r"(k_tensor_x|k_sens_x|k_load_means_x|k_filter_b<[12]>)", name)
         if not m:
             continue
     num = lambda c: float(row[h.index(c)].replace(",", ""))          # base units (bytes, ns)
