@@ -313,6 +313,11 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false, bool vonly = fa
         if (ok) { vb = l; break; }
     }
     const int top = vb > 0 ? vb : nl - 1;     // levels [0, top) are launched per level
+    // OTM_STAMPS=2: %globaltimer stamps between the legs of the captured PCG iteration
+    static const bool st = getenv("OTM_STAMPS") && atoi(getenv("OTM_STAMPS")) == 2;
+    const bool stamp = st && in_loop && ctx->lstate;
+    auto mark = [&](int i) { if (stamp) launch_stamp(s, ctx->lstate, i); };
+    mark(0);
     for (int l = 0; l < top; ++l) {
         LevelBuf& A = ctx->L[l];
         LevelBuf& B = ctx->L[l + 1];
@@ -320,7 +325,9 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false, bool vonly = fa
         if (prof && l == 0) prof_record(ctx, kProfL0Stencil, bsm, true, sl);
         launch_smooth_res(s, A.g, A.lt, A.kap, A.f, A.dinv, oml(l), A.z, A.res);
         if (prof && l == 0) prof_record(ctx, kProfL0Stencil, 0, false, sl);
+        if (l == 0) mark(8);
         launch_restrict(s, A.g, B.g, B.cf, A.res, B.f);
+        if (l == 0) mark(9);
         vbytes += bsm + 12.0 * A.g.n + 12.0 * B.g.n;
         launches += 2;
     }
@@ -348,7 +355,9 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false, bool vonly = fa
         LevelBuf& A = ctx->L[l];
         LevelBuf& B = ctx->L[l + 1];
         const double bj = 44.0 * (double)A.g.n;
+        if (l == 0) mark(10);
         launch_prolong(s, A.g, B.g, B.cf, B.res, A.z);
+        if (l == 0) mark(11);
         if (prof && l == 0) prof_record(ctx, kProfL0Stencil, bj, true, sl);
         launch_jacobi(s, A.g, A.lt, A.kap, A.z, A.f, A.dinv, oml(l), A.res, l == 0 && !vonly, ctx->red, ctx->sc);
         if (prof && l == 0) prof_record(ctx, kProfL0Stencil, 0, false, sl);
@@ -366,12 +375,16 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false, bool vonly = fa
         ctx->slots[sl_v].bytes = vbytes;
     }
     if (vonly) return OTM_OK;                  // V-cycle only: z in L[0].res
+    mark(12);
     float* z0 = nl == 1 ? ctx->L[0].z : ctx->L[0].res;
     launch_pupd(s, ctx->g0.n, z0, ctx->p, ctx->d, ctx->sc);
+    mark(13);
     if (prof) prof_record(ctx, kProfL0Stencil, 28.0 * n0, true, sl);
     launch_spmv(s, ctx->g0, ctx->L[0].lt, ctx->L[0].kap, ctx->p, ctx->q, ctx->red, ctx->sc);
     if (prof) prof_record(ctx, kProfL0Stencil, 0, false, sl);
+    mark(14);
     launch_upd(s, ctx->g0.n, ctx->r, ctx->q, ctx->red, ctx->sc, in_loop ? ctx->loop_handle : 0ULL);
+    mark(15);
     launches += 3;
     if (!in_loop) cudaMemcpyAsync(ctx->h, ctx->sc->flags, 8 * sizeof(double), cudaMemcpyDeviceToHost, s);
     ctx->launches_per_inner = launches;
@@ -1886,6 +1899,13 @@ int otm_run_batch(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, do
                         " (%.3f passes per update)\n",
                 done, H->mark_ms[1], H->mark_ms[2], H->mark_ms[3], H->mark_ms[4],
                 H->n_oc ? (double)H->n_oc_passes / H->n_oc : 0.0);
+    if (getenv("OTM_STAMPS") && atoi(getenv("OTM_STAMPS")) == 2 && H->n_inner > 0)
+        fprintf(stderr, "[otm] PCG iteration legs (us, mean over %lld): L0 smooth_res %.1f  L0 restrict %.1f  "
+                        "coarse %.1f  L0 prolong %.1f  L0 jacobi %.1f  pupd %.1f  spmv %.1f  upd %.1f\n",
+                H->n_inner, H->mark_ms[8] * 1e3 / H->n_inner, H->mark_ms[9] * 1e3 / H->n_inner,
+                H->mark_ms[10] * 1e3 / H->n_inner, H->mark_ms[11] * 1e3 / H->n_inner,
+                H->mark_ms[12] * 1e3 / H->n_inner, H->mark_ms[13] * 1e3 / H->n_inner,
+                H->mark_ms[14] * 1e3 / H->n_inner, H->mark_ms[15] * 1e3 / H->n_inner);
     // graph nodes launched: per iteration ~14 fixed + the build, per refinement step 5,
     // per PCG iteration the inner body
     ctx->launches += (long long)(done + (status ? 1 : 0)) * (14 + ctx->build_launches) + 5 * (H->n_solves + H->n_outer) +

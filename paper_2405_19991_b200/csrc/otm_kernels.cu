@@ -2508,10 +2508,9 @@ static bool k10_maps(K10Maps& M, const Geo& g, const float* op3, const float* d,
     else
         M.d_full = M.d_main = M.d_halo = M.k_main;
     if (f3)
-        ok = ok && encode_map4(&M.f_main, f3, g, TY) && encode_map4(&M.f_full, f3, g, TY + 2) &&
-             encode_map4(&M.f_halo, f3, g, 1);
+        ok = ok && encode_map4(&M.f_main, f3, g, TY);
     else
-        M.f_main = M.f_full = M.f_halo = M.op_main;
+        M.f_main = M.op_main;
     return ok;
 }
 static thread_local int g_k10_nxr = 0;            // output plane count of the launch being issued (0: all nx)

@@ -142,7 +142,7 @@ struct LoopState {
     unsigned long long t_solve, t_eval, t_oc;   // ... at the end of the solve, of the evaluation, of the OC step
     double ph_ms[4];              // accumulated: filter+build+solve, tensor+objective, sens+OC, gap to next
     unsigned long long t_mark;    // OTM_STAMPS: last k_stamp
-    double mark_ms[8];            // OTM_STAMPS: device time before each k_stamp since the previous one
+    double mark_ms[20];           // OTM_STAMPS: device time before each k_stamp since the previous one
     long long n_solves, n_outer, n_inner, n_oc, n_oc_passes, n_oc_retries;   // otm_stats counters
     Dg dG;
     LoopRecord rec[kLoopRing];

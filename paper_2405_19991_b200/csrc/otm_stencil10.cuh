@@ -32,7 +32,7 @@ namespace otm {
 struct K10Maps {
     CUtensorMap op_full, op_main, op_halo;   // 4-D (z, case, y, x): TY+2 / TY / 1 rows
     CUtensorMap d_full, d_main, d_halo;      // 3-D (z, y, x) D^-1: TY+2 / TY / 1 rows
-    CUtensorMap f_full, f_main, f_halo;      // 4-D right-hand side: TY+2 / TY / 1 rows
+    CUtensorMap f_main;                      // 4-D right-hand side, centre rows (jacobi)
     CUtensorMap k_full, k_main, k_halo;      // 3-D factors: TY+1 / TY / 1 rows
     int lock;                                // > 0: CTA b owns row tile b % nty, x chunk b / nty of `lock`
                                              // chunks (row-tile neighbours march the same planes at the
@@ -41,21 +41,17 @@ struct K10Maps {
                                              // interior [1, nxl + 1) between its ghost planes
 };
 
-// K10_JACOBI_P: post-smoothing whose operand z = w D^-1 f + P e is rebuilt on the fly
-// from f, D^-1 and the prolonged correction (so the pre-smoothing never stores z0
-// and the prolongation writes P e instead of read-modify-writing z0 + P e)
-enum { K10_SMOOTH = 0, K10_JACOBI = 1, K10_SPMV = 2, K10_JACOBI_P = 3 };
+enum { K10_SMOOTH = 0, K10_JACOBI = 1, K10_SPMV = 2 };
 
 template <int MODE, int NZ, int TY, int CPS = 2>
 struct K10Geo {
-    static constexpr bool HAS_D = MODE == K10_SMOOTH || MODE == K10_JACOBI_P;
+    static constexpr bool HAS_D = MODE == K10_SMOOTH;
     static constexpr bool HAS_C = MODE == K10_JACOBI;
-    static constexpr bool HAS_FH = MODE == K10_JACOBI_P;               // f with y halo
     static constexpr int OP = 0;
     static constexpr int D = OP + (TY + 2) * 3 * NZ;
     static constexpr int K = D + (HAS_D ? (TY + 2) * NZ : 0);
     static constexpr int F = K + (TY + 1) * NZ;
-    static constexpr int DC = F + (HAS_C ? TY * 3 * NZ : (HAS_FH ? (TY + 2) * 3 * NZ : 0));
+    static constexpr int DC = F + (HAS_C ? TY * 3 * NZ : 0);
     static constexpr int SLOT = DC + (HAS_C ? TY * NZ : 0);          // floats
     static constexpr int SLOT_BYTES = SLOT * 4;
     static constexpr int BUDGET = (224 * 1024) / CPS - 2048;          // CPS CTAs per SM
@@ -179,7 +175,7 @@ struct K10Op {
     K10Row dw[3];         // smooth_res: omega D^-1 around the pair, rows y-1, y, y+1 (per plane)
 
     __device__ __forceinline__ void plane(const float* S, int ty, const K10Cols& q) {
-        if (MODE == K10_SMOOTH || MODE == K10_JACOBI_P) {
+        if (MODE == K10_SMOOTH) {
             const float2 om = f2(omega, omega);
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
@@ -199,11 +195,6 @@ struct K10Op {
                 R[j].L = fmul2(R[j].L, dw[j].L);
                 R[j].C = fmul2(R[j].C, dw[j].C);
                 R[j].R = fmul2(R[j].R, dw[j].R);
-            } else if (MODE == K10_JACOBI_P) {            // operand = omega D^-1 f + P e
-                const K10Row fr = k10_row<NZ>(S + G::F + ((ty + j) * 3 + c) * NZ, q);
-                R[j].L = ffma2(fr.L, dw[j].L, R[j].L);
-                R[j].C = ffma2(fr.C, dw[j].C, R[j].C);
-                R[j].R = ffma2(fr.R, dw[j].R, R[j].R);
             }
         }
     }
@@ -221,13 +212,6 @@ struct K10Op {
             const float2 f = pair(Sp + G::OP + ((ty + 1) * 3 + c) * NZ, tx);
             if (WZ) put(out0 + c * n + v, ctr);
             put(out1 + c * n + v, f2(f.x - kt.x, f.y - kt.y));
-        } else if (MODE == K10_JACOBI_P) {
-            const float2 f = pair(Sp + G::F + ((ty + 1) * 3 + c) * NZ, tx);
-            const float2 d = pair(Sp + G::D + (ty + 1) * NZ, tx);
-            const float z0 = ctr.x + omega * d.x * (f.x - kt.x);
-            const float z1 = ctr.y + omega * d.y * (f.y - kt.y);
-            put(out0 + c * n + v, f2(z0, z1));
-            if (DOT) acc[c] += (double)f.x * (double)z0 + (double)f.y * (double)z1;
         } else {
             const float2 f = pair(Sp + G::F + (ty * 3 + c) * NZ, tx);
             const float2 d = pair(Sp + G::DC + ty * NZ, tx);
@@ -303,15 +287,6 @@ __device__ __forceinline__ void march10(const Geo& g, float s12f, const K10Maps&
             x = x < 0 ? x + g.nx : (x >= g.nx ? x - g.nx : x);
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             mbar_expect_tx(bars + k, (unsigned)G::SLOT_BYTES);
-            if (G::HAS_FH) {
-                if (!seam) {
-                    k10_ld_c3<NZ>(S + G::F, &maps.f_full, y0 - 1, x, bars + k);
-                } else {
-                    k10_ld_c3<NZ>(S + G::F, &maps.f_halo, ym, x, bars + k);
-                    k10_ld_c3<NZ>(S + G::F + 3 * NZ, &maps.f_main, y0, x, bars + k);
-                    k10_ld_c3<NZ>(S + G::F + (TY + 1) * 3 * NZ, &maps.f_halo, yp, x, bars + k);
-                }
-            }
             if (!seam) {
                 k10_ld_c3<NZ>(S + G::OP, &maps.op_full, y0 - 1, x, bars + k);
                 if (G::HAS_D) k10_ld_1<NZ>(S + G::D, &maps.d_full, y0 - 1, x, bars + k);
