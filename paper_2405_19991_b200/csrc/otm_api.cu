@@ -982,8 +982,7 @@ int otm_solve(otm_ctx* ctx, const double* fext, double tol, int max_cycles, int*
         init.hcount = 0;
         std::memcpy(ctx->h + 64, &init, sizeof init);
         CK(cudaMemcpyAsync(ctx->sc, ctx->h + 64, sizeof init, cudaMemcpyHostToDevice, s));
-        CK(cudaMemsetAsync(ctx->d, 0, 3 * n * sizeof(float), s));
-        CK(cudaMemsetAsync(ctx->p, 0, 3 * n * sizeof(float), s));
+        // d and p start from zero: k_pupd's first iteration writes them (no memsets)
         if (ctx->gexec_loop && !ctx->prof) {
             CK(cudaGraphLaunch(ctx->gexec_loop, s));
         } else {
@@ -1741,8 +1740,6 @@ static int capture_iteration(otm_ctx* ctx, const LoopCfg& C, double* rho) {
     CKC(cudaStreamBeginCaptureToGraph(s2, body_out, nullptr, nullptr, 0, mode), "capture outer");
     CKC(cond_handle(s2, 0, &h_in), "handle inner");
     launch_solve_ctl(s2, S, C, ctx->scal, ctx->sc, (unsigned long long)h_out, (unsigned long long)h_in);
-    CKC(cudaMemsetAsync(ctx->d, 0, 3 * n * sizeof(float), s2), "memset d");
-    CKC(cudaMemsetAsync(ctx->p, 0, 3 * n * sizeof(float), s2), "memset p");
     CKC(cond_node(s2, h_in, cudaGraphCondTypeWhile, &body_in), "WHILE inner");
     CKC(cudaStreamBeginCaptureToGraph(s3, body_in, nullptr, nullptr, 0, mode), "capture inner");
     ctx->stream = s3;

@@ -903,6 +903,24 @@ __global__ void k_pupd(long long n, const float* __restrict__ z, float* __restri
     const long long n4 = n >> 2;
     const float b[3] = {(float)sc->beta[0], (float)sc->beta[1], (float)sc->beta[2]};
     const float al[3] = {(float)sc->alpha[0], (float)sc->alpha[1], (float)sc->alpha[2]};
+    if (sc->it == 0) {
+        // first iteration of an inner solve: d = 0, p = z (the buffers hold the previous
+        // solve's vectors, or nothing yet; this replaces two memsets per outer step)
+        if (i < n4) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                reinterpret_cast<float4*>(p + c * n)[i] = __ldg(reinterpret_cast<const float4*>(z + c * n) + i);
+                reinterpret_cast<float4*>(d + c * n)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        const long long t = (n4 << 2) + i;
+        if (i < (n & 3))
+            for (int c = 0; c < 3; ++c) {
+                p[c * n + t] = z[c * n + t];
+                d[c * n + t] = 0.f;
+            }
+        return;
+    }
     if (i < n4) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
