@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -391,7 +392,19 @@ int enqueue_inner(otm_ctx* ctx, bool prof, bool in_loop = false, bool vonly = fa
     return OTM_OK;
 }
 
+// Contexts may be driven from several host threads at once (structures designed
+// concurrently on one GPU, each with its own stream).  A stream capture in one thread
+// and a device-wide synchronisation (context creation) or cudaFree (destruction) in
+// another do not mix -- "operation not permitted when stream is capturing" -- so
+// captures, creation and destruction are serialised process-wide.
+static std::recursive_mutex& capture_mutex() {
+    static std::recursive_mutex mu;
+    return mu;
+}
+using CaptureLock = std::lock_guard<std::recursive_mutex>;
+
 int capture_inner(otm_ctx* ctx, bool prof) {
+    CaptureLock lock(capture_mutex());
     cudaGraph_t graph;
     CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     enqueue_inner(ctx, prof);
@@ -407,6 +420,7 @@ int capture_inner(otm_ctx* ctx, bool prof) {
 // one iteration followed by k_loop_ctl, which decides on the device whether to
 // run again (no host round trip per iteration).
 int capture_loop(otm_ctx* ctx) {
+    CaptureLock lock(capture_mutex());
     cudaGraph_t g;
     CK(cudaGraphCreate(&g, 0));
     cudaGraphConditionalHandle h;
@@ -497,25 +511,29 @@ struct ProfScope {
 int enqueue_build(otm_ctx* ctx) {
     cudaStream_t s = ctx->stream;
     const int nl = (int)ctx->L.size();
-    for (int l = 1; l < nl; ++l) {
-        launch_coarsen(s, ctx->L[l - 1].g, ctx->L[l].g, ctx->L[l].cf, ctx->L[l - 1].kap, ctx->L[l].kap);
-        ctx->launches++;
-    }
-    for (int l = 0; l < nl; ++l) {
-        // diagonal template weight: on a flat axis (n = 1) the couplings to the corner
-        // across that axis wrap onto the vertex itself (_fold, solver.py:56-63), so the
-        // diagonal is sum of kt[d] over every corner offset d inside the flat axes
+    // diagonal template weight: on a flat axis (n = 1) the couplings to the corner
+    // across that axis wrap onto the vertex itself (_fold, solver.py:56-63), so the
+    // diagonal is sum of kt[d] over every corner offset d inside the flat axes
+    auto kdiag = [&](int l) {
         const Geo& g = ctx->L[l].g;
         const int flat = (g.nx == 1 ? 1 : 0) | (g.ny == 1 ? 2 : 0) | (g.nz == 1 ? 4 : 0);
-        double kdiag = 0.0;
+        double kd = 0.0;
         for (int d = 0; d < 8; ++d)
-            if ((d & ~flat) == 0) kdiag += ctx->L[l].lt.kt[d];
-        launch_dinv(s, g, ctx->L[l].kap, (float)kdiag, ctx->L[l].dinv);
+            if ((d & ~flat) == 0) kd += ctx->L[l].lt.kt[d];
+        return (float)kd;
+    };
+    // the chain child means of level l + D^-1 of level l-1, one launch per level, then
+    // the coarse pseudo-inverse (it needs only the coarsest factors) and the coarsest D^-1
+    for (int l = 1; l < nl; ++l) {
+        launch_coarsen_dinv(s, ctx->L[l - 1].g, ctx->L[l].g, ctx->L[l].cf, ctx->L[l - 1].kap, ctx->L[l].kap,
+                            kdiag(l - 1), ctx->L[l - 1].dinv);
         ctx->launches++;
     }
     CoarseTemplate ct;
     for (int i = 0; i < 8; ++i) ct.kt[i] = ctx->L[nl - 1].lt.kt[i];
     ctx->launches += launch_coarse_setup(s, ctx->L[nl - 1].g, ctx->L[nl - 1].kap, ct, ctx->gj, ctx->G);
+    launch_dinv(s, ctx->L[nl - 1].g, ctx->L[nl - 1].kap, kdiag(nl - 1), ctx->L[nl - 1].dinv);
+    ctx->launches++;
     return OTM_OK;
 }
 
@@ -550,6 +568,7 @@ int build_levels(otm_ctx* ctx, bool async = false) {
         if (rc) return rc;
     } else {
         if (!ctx->gexec_build) {
+            CaptureLock lock(capture_mutex());
             cudaGraph_t g;
             CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
             const long long l0 = ctx->launches;
@@ -624,6 +643,7 @@ void otm_default_run_config(otm_run_config* c) {
 
 int otm_create(otm_ctx** out, int nx, int ny, int nz, const otm_params* pin) {
     if (!out) return OTM_EINVAL;
+    CaptureLock lock(capture_mutex());
     *out = nullptr;
     otm_ctx* ctx = new otm_ctx();
     if (pin) ctx->P = *pin; else otm_default_params(&ctx->P);
@@ -742,6 +762,7 @@ int otm_create(otm_ctx** out, int nx, int ny, int nz, const otm_params* pin) {
 static void oc_settle(otm_ctx* ctx);
 
 int otm_destroy(otm_ctx* ctx) {
+    CaptureLock lock(capture_mutex());
     if (!ctx) return OTM_OK;
     if (ctx->oc_pending) {
         cudaStreamSynchronize(ctx->stream);
@@ -1664,6 +1685,7 @@ static cudaError_t cond_node(cudaStream_t s, cudaGraphConditionalHandle h, cudaG
 
 // One design iteration as a graph (see otm_loop.cu for the structure).
 static int capture_iteration(otm_ctx* ctx, const LoopCfg& C, double* rho) {
+    CaptureLock lock(capture_mutex());
     const long long n = ctx->g0.n;
     for (auto& cs : ctx->cap)
         if (!cs) CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));

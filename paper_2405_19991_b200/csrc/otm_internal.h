@@ -120,6 +120,8 @@ void launch_means(cudaStream_t s, long long n, const double* rho, double p, Red&
 void launch_symmetrize(cudaStream_t s, const Geo& g, double* a);
 void launch_coarsen(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* kf, float* kc);
 void launch_dinv(cudaStream_t s, const Geo& g, const float* k, float kdiag, float* dinv);
+void launch_coarsen_dinv(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* kf, float* kc,
+                         float kdiag_f, float* dinv_f);
 int launch_coarse_setup(cudaStream_t s, const Geo& g, const float* k, const CoarseTemplate& ct, double* work,
                          float* G);
 void launch_coarse_solve(cudaStream_t s, int n, const float* G, const float* f, float* z);

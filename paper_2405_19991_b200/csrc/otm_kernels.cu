@@ -266,6 +266,37 @@ __global__ void k_dinv(Geo g, const float* __restrict__ k, float kdiag, float* _
     dinv[v] = 1.0f / (kdiag * s);
 }
 
+// One step of the hierarchy build chain: child means of level l (from level l-1)
+// and D^-1 of level l-1 (whose factors the previous step produced) in one launch.
+__global__ void k_coarsen_dinv(Geo f, Geo c, int cx, int cy, int cz, const float* __restrict__ kf,
+                               float* __restrict__ kc, float kdiag_f, float* __restrict__ dinv_f) {
+    const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < c.n) {
+        const int X = (int)(v / c.pl), rem = (int)(v - (long long)X * c.pl);
+        const int Y = rem / c.nz, Z = rem - Y * c.nz;
+        float s = 0.f;
+        int cnt = 0;
+        for (int a = 0; a <= cx; ++a)
+            for (int b = 0; b <= cy; ++b)
+                for (int d = 0; d <= cz; ++d) {
+                    const int x = (cx ? 2 * X : X) + a, y = (cy ? 2 * Y : Y) + b, z = (cz ? 2 * Z : Z) + d;
+                    s += kf[((long long)x * f.ny + y) * f.nz + z];
+                    ++cnt;
+                }
+        kc[v] = s / (float)cnt;
+    }
+    if (v < f.n) {
+        const int x = (int)(v / f.pl), rem = (int)(v - (long long)x * f.pl);
+        const int y = rem / f.nz, z = rem - y * f.nz;
+        const int xs[2] = {wrap_m(x, f.nx), x}, ys[2] = {wrap_m(y, f.ny), y}, zs[2] = {wrap_m(z, f.nz), z};
+        float s = 0.f;
+        for (int a = 0; a < 2; ++a)
+            for (int b = 0; b < 2; ++b)
+                for (int d = 0; d < 2; ++d) s += kf[((long long)xs[a] * f.ny + ys[b]) * f.nz + zs[d]];
+        dinv_f[v] = 1.0f / (kdiag_f * s);
+    }
+}
+
 // Coarsest level: assemble the dense periodic matrix (solver.py:278-296), invert
 // the vertex-0-pinned block (solver.py:298-305), and fold the mean projections of
 // coarse_solve (solver.py:307-324) into one symmetric matrix G = P Z P so the
@@ -2221,6 +2252,10 @@ void launch_symmetrize(cudaStream_t s, const Geo& g, double* a) {
 }
 void launch_coarsen(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* kf, float* kc) {
     k_coarsen<<<nblk(c.n, 256), 256, 0, s>>>(f, c, cf[0], cf[1], cf[2], kf, kc);
+}
+void launch_coarsen_dinv(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* kf, float* kc,
+                         float kdiag_f, float* dinv_f) {
+    k_coarsen_dinv<<<nblk(std::max(f.n, c.n), 256), 256, 0, s>>>(f, c, cf[0], cf[1], cf[2], kf, kc, kdiag_f, dinv_f);
 }
 void launch_dinv(cudaStream_t s, const Geo& g, const float* k, float kdiag, float* dinv) {
     k_dinv<<<nblk(g.n, 256), 256, 0, s>>>(g, k, kdiag, dinv);
