@@ -104,6 +104,15 @@ int otm_slab_set_scalar_mode(otm_slab_ws* w, int device);
  * stage 2: cycles += active; active &= r.r > target^2 */
 int otm_slab_pcg_step(otm_slab_ws* w, int stage, double* S_dev);
 
+/* Ghost planes of a slab field from its neighbours' interiors, in one launch on
+ * `stream`: for every case c < ncases, dst plane 0 <- left plane nxl_left and dst
+ * plane nxl + 1 <- right plane 1 (planes of pl elements of elem_size 4 or 8 bytes;
+ * a field holds ncases blocks of (its nxl + 2) planes).  In-process slabs
+ * (LocalComm) and the single-rank case of DistComm; left == right == dst for one
+ * slab.  Replaces 2 strided copies per case and side. */
+int otm_slab_halo_local(void* stream, int elem_size, int ncases, long long pl, void* dst, int nxl,
+                        const void* left, int nxl_left, const void* right, int nxl_right);
+
 #ifdef __cplusplus
 }
 #endif

@@ -119,6 +119,8 @@ _SIGS = {
                                    dptr, dptr, dptr, C.c_double, dptr, dptr, C.POINTER(C.c_double)]),
     "otm_slab_set_scalar_mode": (C.c_int, [C.c_void_p, C.c_int]),
     "otm_slab_pcg_step": (C.c_int, [C.c_void_p, C.c_int, dptr]),
+    "otm_slab_halo_local": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_longlong, C.c_void_p, C.c_int, C.c_void_p,
+                                      C.c_int, C.c_void_p, C.c_int]),
     "otm_slab_restrict": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, dptr, dptr]),
     "otm_slab_prolong": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, dptr, dptr]),
     "otm_slab_coarsen": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, dptr, dptr]),

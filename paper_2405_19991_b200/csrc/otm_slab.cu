@@ -564,6 +564,23 @@ __global__ void __launch_bounds__(256) ks_oc_apply(SGeo g, const double* rho,   
     reduce_finalize<1>(acc, partials, counter, out);
 }
 
+// ghost planes from the neighbours (otm_slab_halo_local); T = float or double, one thread
+// per (case, side, element of the plane)
+template <class T>
+__global__ void ks_halo_local(int ncases, long long pl, T* __restrict__ dst, int nxl, const T* __restrict__ left,
+                              int nxl_left, const T* __restrict__ right, int nxl_right) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long per = 2 * pl;
+    if (i >= ncases * per) return;
+    const int c = (int)(i / per);
+    const long long r = i - (long long)c * per;
+    const int side = (int)(r / pl);
+    const long long e = r - (long long)side * pl;
+    const long long nd = (long long)(nxl + 2) * pl;
+    if (side == 0) dst[c * nd + e] = left[c * (long long)(nxl_left + 2) * pl + (long long)nxl_left * pl + e];
+    else dst[c * nd + (long long)(nxl + 1) * pl + e] = right[c * (long long)(nxl_right + 2) * pl + pl + e];
+}
+
 inline unsigned nb(long long n, int bs) { return (unsigned)((n + bs - 1) / bs); }
 // reducing kernels are grid-stride with a bounded grid: one partial per block and one
 // ticket atomic per block (an unbounded one-item-per-thread grid serialised ~10^5
@@ -991,6 +1008,22 @@ int otm_slab_set_scalar_mode(otm_slab_ws* w, int device) {
     if (!w) return OTM_EINVAL;
     w->dev = device != 0;
     return OTM_OK;
+}
+
+int otm_slab_halo_local(void* stream, int elem_size, int ncases, long long pl, void* dst, int nxl,
+                        const void* left, int nxl_left, const void* right, int nxl_right) {
+    if (!dst || !left || !right || ncases < 1 || pl < 1 || nxl < 1 || nxl_left < 1 || nxl_right < 1 ||
+        (elem_size != 4 && elem_size != 8))
+        return OTM_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    const unsigned blocks = nb(2 * pl * ncases, 256);
+    if (elem_size == 4)
+        ks_halo_local<float><<<blocks, 256, 0, s>>>(ncases, pl, (float*)dst, nxl, (const float*)left, nxl_left,
+                                                    (const float*)right, nxl_right);
+    else
+        ks_halo_local<double><<<blocks, 256, 0, s>>>(ncases, pl, (double*)dst, nxl, (const double*)left, nxl_left,
+                                                     (const double*)right, nxl_right);
+    return cudaGetLastError() == cudaSuccess ? OTM_OK : OTM_ECUDA;
 }
 
 int otm_slab_pcg_step(otm_slab_ws* w, int stage, double* S) {

@@ -103,6 +103,26 @@ class SlabLayout:
 
 
 # --------------------------------------------------------------------------- comms
+def _halo_kernel(dsts, lefts, rights) -> bool:
+    """Ghost planes of CUDA slab fields in one launch each (otm_slab_halo_local);
+    False when the fields are not contiguous CUDA tensors (the caller copies)."""
+    if not all(getattr(t, "is_cuda", False) and t.is_contiguous() for t in (*dsts, *lefts, *rights)):
+        return False
+    import torch
+    from . import _lib
+    lib = _lib.load()
+    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for t, left, right in zip(dsts, lefts, rights):
+        ncases = t.shape[0] if t.dim() == 4 else 1
+        pl = t.shape[-1] * t.shape[-2]
+        rc = lib.otm_slab_halo_local(stream, t.element_size(), ncases, pl, C.c_void_p(t.data_ptr()), t.shape[-3] - 2,
+                                     C.c_void_p(left.data_ptr()), left.shape[-3] - 2, C.c_void_p(right.data_ptr()),
+                                     right.shape[-3] - 2)
+        if rc != 0:
+            raise RuntimeError(f"otm_slab_halo_local failed ({rc})")
+    return True
+
+
 class LocalComm:
     """All slabs live in this process (list index = rank); exchanges are copies."""
 
@@ -113,6 +133,8 @@ class LocalComm:
     def halo(self, ts):
         # ghost planes are written, interior planes read: no aliasing, no staging copies
         W = len(ts)
+        if _halo_kernel(ts, [ts[(i - 1) % W] for i in range(W)], [ts[(i + 1) % W] for i in range(W)]):
+            return
         for i, t in enumerate(ts):
             left, right = ts[(i - 1) % W], ts[(i + 1) % W]
             t.select(-3, 0).copy_(left.select(-3, left.shape[-3] - 2))
@@ -152,8 +174,9 @@ class DistComm:
         dist = self.dist
         r, W = self.ranks[0], self.world
         if W == 1:
-            t.select(-3, 0).copy_(t.select(-3, t.shape[-3] - 2))
-            t.select(-3, t.shape[-3] - 1).copy_(t.select(-3, 1))
+            if not _halo_kernel([t], [t], [t]):
+                t.select(-3, 0).copy_(t.select(-3, t.shape[-3] - 2))
+                t.select(-3, t.shape[-3] - 1).copy_(t.select(-3, 1))
             return
         last = t.select(-3, t.shape[-3] - 2).contiguous()
         first = t.select(-3, 1).contiguous()
