@@ -68,6 +68,7 @@ struct otm_ctx {
     double* kap64 = nullptr;
     double* T64 = nullptr;
     double* oc_q = nullptr;                   // k_oc_coop: per-element c_e of the current search
+    double* oc_lam = nullptr;                 // k_oc_coop: the last update's multiplier (next prediction)
     double* rho_f = nullptr;   // last filtered density used by otm_build (for sensitivities)
     double* sensf = nullptr;   // design-loop scratch: sensitivity wrt rho_f, then wrt rho
     double* sens = nullptr;
@@ -734,6 +735,8 @@ int otm_create(otm_ctx** out, int nx, int ny, int nz, const otm_params* pin) {
     const size_t mb = max_blocks(ctx);
     CK(dalloc(ctx, &ctx->red.partials, mb * 32 * 2 + mb));     // k_oc_coop: 2 x partials + flags
     CK(dalloc(ctx, &ctx->oc_q, (size_t)ctx->g0.n));
+    CK(dalloc(ctx, &ctx->oc_lam, 1));
+    CK(cudaMemset(ctx->oc_lam, 0, sizeof(double)));
     CK(dalloc(ctx, &ctx->red.counter, 8));
     CK(cudaMemset(ctx->red.counter, 0, 8 * sizeof(unsigned)));
     CK(dalloc(ctx, &ctx->sc, 1));
@@ -787,7 +790,7 @@ int otm_destroy(otm_ctx* ctx) {
     if (ctx->lstate) cudaFree(ctx->lstate);
     for (auto& s : ctx->slots) { cudaEventDestroy(s.a); cudaEventDestroy(s.b); }
     auto F = [](void* p) { if (p) cudaFree(p); };
-    F(ctx->kap64); F(ctx->T64); F(ctx->oc_q); F(ctx->rho_f); F(ctx->sensf); F(ctx->sens); F(ctx->r); F(ctx->p); F(ctx->q); F(ctx->d);
+    F(ctx->kap64); F(ctx->T64); F(ctx->oc_q); F(ctx->oc_lam); F(ctx->rho_f); F(ctx->sensf); F(ctx->sens); F(ctx->r); F(ctx->p); F(ctx->q); F(ctx->d);
     for (size_t l = 0; l < ctx->L.size(); ++l) {
         F(ctx->L[l].kap); F(ctx->L[l].dinv); F(ctx->L[l].z); F(ctx->L[l].res);
         if (l > 0) F(ctx->L[l].f);
@@ -1321,7 +1324,7 @@ static void oc_settle(otm_ctx* ctx) {
 }
 static int oc_search_coop(otm_ctx* ctx, const double* rho, const double* sens, double V, double V_retry,
                           const otm_oc_params* pp, double* rho_out, double* lam_out, int* active_out,
-                          int* changed_out, int* retried_out, bool wait = true) {
+                          int* changed_out, int* retried_out, bool wait = true, bool first_update = true) {
     cudaStream_t s = ctx->stream;
     OcArgs a;
     a.step = pp->step_limit;
@@ -1334,11 +1337,13 @@ static int oc_search_coop(otm_ctx* ctx, const double* rho, const double* sens, d
     init.V = V;
     init.V_retry = V_retry;
     init.bis_tol = pp->bisection_tol;
+    init.first_update = first_update ? 1 : 0;
     std::memcpy(ctx->h + 256, &init, sizeof init);
     CK(cudaMemcpyAsync(ctx->ocl, ctx->h + 256, sizeof init, cudaMemcpyHostToDevice, s));
     {
         ProfScope ps(ctx, kProfOC, 0.0);
-        if (launch_oc_coop(s, ctx->g0.n, rho, sens, a, rho_out, ctx->ocl, ctx->red.partials, ctx->oc_q)) {
+        if (launch_oc_coop(s, ctx->g0.n, rho, sens, a, rho_out, ctx->ocl, ctx->red.partials, ctx->oc_q,
+                           ctx->oc_lam)) {
             cudaGetLastError();
             return OTM_ECUDA;
         }
@@ -1589,7 +1594,8 @@ int otm_run_update(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, d
         double vb, vretry;
         oc_bounds(otm_governor_update(&st->gov, st->g, mean_rho, st->mean_rho_p), mean_rho, cfg->oc.step_limit, &vb,
                   &vretry);
-        rc = oc_search_coop(ctx, rho, ctx->sens, vb, vretry, &cfg->oc, rho, nullptr, nullptr, nullptr, nullptr, false);
+        rc = oc_search_coop(ctx, rho, ctx->sens, vb, vretry, &cfg->oc, rho, nullptr, nullptr, nullptr, nullptr, false,
+                            st->iter <= 1);
         if (rc == OTM_OK) {
             if (cfg->symmetry == 1) {
                 launch_symmetrize(ctx->stream, ctx->g0, rho);
@@ -1790,7 +1796,7 @@ static int capture_iteration(otm_ctx* ctx, const LoopCfg& C, double* rho) {
     CKC(cond_node(s1, h_upd, cudaGraphCondTypeIf, &body_upd), "IF update");
     CKC(cudaStreamBeginCaptureToGraph(s2, body_upd, nullptr, nullptr, 0, mode), "capture update");
     if (stamps) launch_stamp(s2, S, 3);
-    if (launch_oc_coop(s2, n, rho, ctx->sens, a, rho, ctx->ocl, ctx->red.partials, ctx->oc_q))
+    if (launch_oc_coop(s2, n, rho, ctx->sens, a, rho, ctx->ocl, ctx->red.partials, ctx->oc_q, ctx->oc_lam))
         return fail_capture("cooperative OC launch", cudaGetLastError());
     if (stamps) launch_stamp(s2, S, 4);
     if (C.symmetry == 1) launch_symmetrize(s2, ctx->g0, rho);

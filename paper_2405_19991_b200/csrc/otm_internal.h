@@ -58,6 +58,11 @@ struct OcCtl {
     double lams[kOcLam];
     double lam_pow[kOcLam];
     double means[kOcLam];
+    int first_update;               // 1: no previous update of this run (no predicted multiplier)
+    int nbr;                        // bracket values in the first pass (slots 1 .. nbr)
+    int plan;                       // 1: the next bisection subtree is to be planned (oc_plan_node)
+    double lam_prev;                // the previous update's multiplier (0: none)
+    double ka, kb;                  // multipliers whose mean is known to be > V + tol (ka) / < V - tol (kb)
 };
 
 // Device-resident scalars of the batched PCG (3 load cases).
@@ -166,8 +171,7 @@ void launch_sens(cudaStream_t s, const Geo& g, const double* T, const double* rf
 void launch_oc_eval(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a, int nlam,
                     const LamSet& lam_pow, Red& red, double* out);
 int launch_oc_coop(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a,
-                   double* rho_out, OcCtl* ctl, double* partials,
-                   double* qbuf);
+                   double* rho_out, OcCtl* ctl, double* partials, double* qbuf, double* lam_mem);
 void launch_oc_apply(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a,
                      double lam, double* rho_out, int* changed);
 

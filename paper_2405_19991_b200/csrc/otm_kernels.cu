@@ -1657,41 +1657,97 @@ __device__ double oc_lam_pow(const OcArgs& a, double lam) {
     return a.sqrt_damp ? 1.0 / sqrt(lam) : pow(lam, -a.damp);
 }
 
+// First pass: the free step and bracket values 4^0, 4^1, ... (optimize.py:141-150);
+// with a predicted multiplier (the previous update's), 15 bracket values and 16
+// multipliers spaced by 3.5 % around the prediction: their means bound the
+// crossing tightly, and every bisection midpoint outside those bounds is decided
+// without being evaluated (oc_learn / oc_skip), usually saving a whole pass.
+constexpr int kOcBracket = 15;
+constexpr double kOcSpread = 1.035;
 __device__ void oc_plan_first(OcCtl* C, const OcArgs& a) {
     C->phase = 0;
     C->lams[0] = 0.0;
+    const bool pred = C->lam_prev > 0.0;
+    const int nb = pred ? kOcBracket : kOcLam - 1;
     double l2 = 1.0;
-    for (int k = 1; k < kOcLam; ++k) { C->lams[k] = l2; l2 *= 4.0; }
+    for (int k = 1; k <= nb; ++k) { C->lams[k] = l2; l2 *= 4.0; }
+    if (pred) {
+        double v = C->lam_prev;
+        for (int i = 0; i < (kOcLam - 1 - nb) / 2; ++i) v /= kOcSpread;
+        for (int k = nb + 1; k < kOcLam; ++k) { C->lams[k] = v; v *= kOcSpread; }
+    }
+    C->nbr = nb;
     C->nlam = kOcLam;
+    C->ka = 0.0;
+    C->kb = INFINITY;
+    C->plan = 0;
 }
 
-__device__ void oc_plan_tree(OcCtl* C) {
-    // BFS subtree of midpoints below (l1, l2): node i covers (lo, hi); children (lo, mid), (mid, hi)
-    const int nodes = kOcLam - 1;
-    double lo[kOcLam], hi[kOcLam];
-    lo[0] = C->l1;
-    hi[0] = C->l2;
-    for (int i = 0; i < nodes; ++i) {
-        const double mid = 0.5 * (lo[i] + hi[i]);
-        C->lams[i] = mid;
-        if (2 * i + 2 < nodes) {
-            lo[2 * i + 1] = lo[i]; hi[2 * i + 1] = mid;
-            lo[2 * i + 2] = mid;  hi[2 * i + 2] = hi[i];
-        }
+// The candidate mean is monotone non-increasing in the multiplier (every element's
+// candidate is, and the fixed-order sum of monotone terms is).  A bisection midpoint
+// at or below a multiplier whose mean exceeded V by more than the tolerance sends
+// the search right without stopping it (optimize.py:153-158), one at or above a
+// multiplier whose mean was below V by more than the tolerance sends it left: such
+// midpoints are decided without evaluating them.  The margin covers the rounding
+// difference between passes (their settled / mixed splits differ).
+constexpr double kOcMargin = 1e-12;
+__device__ void oc_learn(OcCtl* C, double lam, double mean) {
+    if (mean - C->V > C->bis_tol + kOcMargin) C->ka = fmax(C->ka, lam);
+    else if (C->V - mean > C->bis_tol + kOcMargin) C->kb = fmin(C->kb, lam);
+}
+// advance (l1, l2) through the midpoints the known bounds decide; false: the
+// bisection's own stopping rule ends the search inside (l1, l2)
+__device__ bool oc_skip(const OcCtl* C, double& l1, double& l2) {
+    while (true) {
+        if (!((l2 - l1) / (l1 + l2) > 1e-13)) return false;
+        const double m = 0.5 * (l1 + l2);
+        if (m <= C->ka) l1 = m;
+        else if (m >= C->kb) l2 = m;
+        else return true;
     }
-    C->nlam = nodes;
+}
+__device__ void oc_finish(OcCtl* C, double l1, double l2) {
+    C->lam = 0.5 * (l1 + l2);
+    C->active = 1;
+    C->phase = 3;
+}
+
+// Next pass of the bisection (optimize.py:151-158): the depth-5 subtree of undecided
+// midpoints below (l1, l2), node i's children 2i+1 (lo, mid) and 2i+2 (mid, hi), the
+// decided midpoints between them stepped over exactly as oc_walk does.  Requested by
+// thread 0 (oc_plan_tree), planned by threads 0..30 in parallel (oc_plan_node).
+__device__ void oc_plan_tree(OcCtl* C) {
+    double l1 = C->l1, l2 = C->l2;
+    if (!oc_skip(C, l1, l2)) { oc_finish(C, l1, l2); return; }   // decided without another pass
     C->phase = 2;
+    C->nlam = kOcLam - 1;
+    C->plan = 1;
+}
+__device__ void oc_plan_node(OcCtl* C, int t) {
+    const int d = 31 - __clz(t + 1);             // depth of node t; path = the low d bits of t + 1
+    double l1 = C->l1, l2 = C->l2;
+    bool live = oc_skip(C, l1, l2);
+    for (int b = d - 1; b >= 0 && live; --b) {
+        const double m = 0.5 * (l1 + l2);
+        if (((t + 1) >> b) & 1) l1 = m;
+        else l2 = m;
+        live = oc_skip(C, l1, l2);
+    }
+    C->lams[t] = live ? 0.5 * (l1 + l2) : 0.0;   // 0: no node (the walk ends above it)
 }
 
 // consume C->means of the pass just evaluated; plan the next pass or finish
 __device__ void oc_walk(OcCtl* C) {
     const double V = C->V;
     C->passes += 1;
+    if (C->phase <= 1) {
+        for (int k = C->phase == 0 ? 1 : 0; k < C->nlam; ++k) oc_learn(C, C->lams[k], C->means[k]);
+    }
     if (C->phase == 0) {
         if (C->means[0] <= V) { C->lam = 0.0; C->active = 0; C->phase = 3; return; }
         C->l2 = 1.0;
         C->bracket_it = 0;
-        for (int k = 1; k < kOcLam; ++k) {
+        for (int k = 1; k <= C->nbr; ++k) {
             if (C->means[k] <= V) { C->l1 = 1e-30; oc_plan_tree(C); return; }
             C->l2 *= 4.0;
             if (++C->bracket_it >= 200) { C->l1 = 1e-30; oc_plan_tree(C); return; }
@@ -1716,19 +1772,21 @@ __device__ void oc_walk(OcCtl* C) {
         C->nlam = k;
         return;
     }
-    // phase 2: walk the evaluated subtree
+    // phase 2: walk the evaluated subtree (decided midpoints stepped over as planned)
     int node = 0;
     const int nodes = kOcLam - 1;
     double l1 = C->l1, l2 = C->l2;
     while (true) {
-        if (!((l2 - l1) / (l1 + l2) > 1e-13)) { C->lam = 0.5 * (l1 + l2); C->active = 1; C->phase = 3; return; }
-        if (node >= nodes) break;
+        if (!oc_skip(C, l1, l2)) { oc_finish(C, l1, l2); return; }
+        if (node >= nodes) break;                // below the evaluated subtree: next pass
         const double m = 0.5 * (l1 + l2);
         const double cur = C->means[node];
         if (cur > V) { l1 = m; node = 2 * node + 2; }
         else { l2 = m; node = 2 * node + 1; }
-        if (fabs(cur - V) <= C->bis_tol) { C->lam = 0.5 * (l1 + l2); C->active = 1; C->phase = 3; return; }
+        if (fabs(cur - V) <= C->bis_tol) { oc_finish(C, l1, l2); return; }
     }
+    for (int k = 0; k < C->nlam; ++k)
+        if (C->lams[k] != 0.0) oc_learn(C, C->lams[k], C->means[k]);
     C->l1 = l1;
     C->l2 = l2;
     oc_plan_tree(C);
@@ -1737,7 +1795,7 @@ __device__ void oc_walk(OcCtl* C) {
 __global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* __restrict__ rho,
                                                     const double* __restrict__ sens, const OcArgs a,
                                                     double* rho_out, OcCtl* C, double* partials,
-                                                    double* __restrict__ qbuf) {
+                                                    double* __restrict__ qbuf, double* lam_mem) {
     // Every block keeps its own copy of the search state in shared memory and replays
     // the same walk on the same fixed-order sums, so all blocks agree on the next
     // multipliers with ONE grid barrier per pass.  Partial sums are double-buffered by
@@ -1767,6 +1825,8 @@ __global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* _
         sC.changed = 0;
         sC.active = 0;
         sC.lam = 0.0;
+        sC.first_update = C->first_update;
+        sC.lam_prev = (C->first_update || !lam_mem) ? 0.0 : *lam_mem;
         oc_plan_first(&sC, a);
     }
     __syncthreads();
@@ -1965,9 +2025,16 @@ __global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* _
         __syncthreads();
         if (threadIdx.x == 0) oc_walk(&sC);
         __syncthreads();
+        if (sC.plan) {
+            if (threadIdx.x < kOcLam - 1) oc_plan_node(&sC, threadIdx.x);
+            __syncthreads();
+            if (threadIdx.x == 0) sC.plan = 0;
+            __syncthreads();
+        }
         set_pows();
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (lam_mem) *lam_mem = sC.active ? sC.lam : 0.0;   // the next update's prediction
         C->passes = sC.passes;
         C->retried = sC.retried;
         C->changed = sC.changed;
@@ -2819,7 +2886,7 @@ void launch_oc_eval(cudaStream_t s, long long n, const double* rho, const double
     k_oc_eval<<<blocks, 256, 0, s>>>(n, rho, sens, a, nlam, lam_pow, red.partials, red.counter, out);
 }
 int launch_oc_coop(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a,
-                   double* rho_out, OcCtl* ctl, double* partials, double* qbuf) {
+                   double* rho_out, OcCtl* ctl, double* partials, double* qbuf, double* lam_mem) {
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2829,8 +2896,8 @@ int launch_oc_coop(cudaStream_t s, long long n, const double* rho, const double*
     long long blocks = (long long)per_sm * sms;
     if (blocks > want) blocks = want;
     if (blocks < 1) blocks = 1;
-    void* args[] = {(void*)&n,       (void*)&rho, (void*)&sens,     (void*)&a,
-                    (void*)&rho_out, (void*)&ctl, (void*)&partials, (void*)&qbuf};
+    void* args[] = {(void*)&n,       (void*)&rho, (void*)&sens,     (void*)&a,        (void*)&rho_out,
+                    (void*)&ctl,     (void*)&partials, (void*)&qbuf, (void*)&lam_mem};
     return cudaLaunchCooperativeKernel((void*)k_oc_coop, dim3((unsigned)blocks), dim3(256), args, 0, s) == cudaSuccess
                ? 0 : 1;
 }

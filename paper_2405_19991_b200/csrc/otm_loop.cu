@@ -161,6 +161,7 @@ __global__ void k_design_eval(LoopState* S, LoopCfg C, const double* __restrict_
         z.V = V;
         z.V_retry = V_retry;
         z.bis_tol = C.oc_bis_tol;
+        z.first_update = it == 1;                // the OC search predicts from the previous update
         *ocl = z;
     }
     cudaGraphSetConditional(h_upd, finished ? 0u : 1u);
