@@ -1711,8 +1711,8 @@ static int capture_iteration(otm_ctx* ctx, const LoopCfg& C, double* rho) {
     a.damp = C.oc_damp;
     a.floor_ratio = std::pow(1e-10, C.oc_damp);
     a.sqrt_damp = C.oc_damp == 0.5;
-    cudaGraph_t G, g_tmp, body_if, body_out, body_in, body_upd;
-    cudaGraphConditionalHandle h_body, h_out, h_in, h_upd;
+    cudaGraph_t G, g_tmp, body_loop, body_if, body_out, body_in, body_upd;
+    cudaGraphConditionalHandle h_loop, h_body, h_out, h_in, h_upd;
     int rc = OTM_OK;
     const long long launches_at_capture = ctx->launches;     // capturing launches nothing
     auto fail_capture = [&](const char* what, cudaError_t e) {
@@ -1735,12 +1735,17 @@ static int capture_iteration(otm_ctx* ctx, const LoopCfg& C, double* rho) {
         if (e_ != cudaSuccess) return fail_capture(what, e_); \
     } while (0)
     CKC(cudaGraphCreate(&G, 0), "create");
-    // top level: k_iter_begin -> IF(not finished) { body }
+    // top level: WHILE(batch) { k_iter_begin -> IF(not finished) { body } }: one graph
+    // launch runs a whole batch of iterations (a launch per iteration cost ~14 us of gap)
     CKC(cudaStreamBeginCaptureToGraph(s0, G, nullptr, nullptr, 0, mode), "capture top");
-    CKC(cond_handle(s0, 0, &h_body), "handle body");
-    launch_iter_begin(s0, S, (unsigned long long)h_body);
-    CKC(cond_node(s0, h_body, cudaGraphCondTypeIf, &body_if), "IF body");
+    CKC(cond_handle(s0, 1, &h_loop), "handle batch");
+    CKC(cond_node(s0, h_loop, cudaGraphCondTypeWhile, &body_loop), "WHILE batch");
     CKC(cudaStreamEndCapture(s0, &g_tmp), "end top");
+    CKC(cudaStreamBeginCaptureToGraph(s0, body_loop, nullptr, nullptr, 0, mode), "capture batch");
+    CKC(cond_handle(s0, 0, &h_body), "handle body");
+    launch_iter_begin(s0, S, (unsigned long long)h_body, (unsigned long long)h_loop);
+    CKC(cond_node(s0, h_body, cudaGraphCondTypeIf, &body_if), "IF body");
+    CKC(cudaStreamEndCapture(s0, &g_tmp), "end batch");
     // the iteration
     CKC(cudaStreamBeginCaptureToGraph(s1, body_if, nullptr, nullptr, 0, mode), "capture body");
     ctx->stream = s1;
@@ -1758,11 +1763,11 @@ static int capture_iteration(otm_ctx* ctx, const LoopCfg& C, double* rho) {
     ctx->stream = s1;
     double* fmean = ctx->scal + 16;
     launch_load_means(s1, ctx->g0, ctx->L[0].lt, ctx->kap64, ctx->red, fmean);
-    launch_T_cold(s1, S, 3 * n, ctx->T64);
-    launch_res64(s1, ctx->g0, ctx->L[0].lt, ctx->kap64, ctx->T64, nullptr, fmean, ctx->r, ctx->red, ctx->scal);
-    CKC(cudaStreamWaitEvent(s1, ctx->ev_cj, 0), "join wait");
     // solve: WHILE(not converged) { control ; WHILE(PCG) {...} ; T += d ; defect }
     CKC(cond_handle(s1, 1, &h_out), "handle outer");
+    launch_T_cold(s1, S, 3 * n, ctx->T64, (unsigned long long)h_out);
+    launch_res64(s1, ctx->g0, ctx->L[0].lt, ctx->kap64, ctx->T64, nullptr, fmean, ctx->r, ctx->red, ctx->scal);
+    CKC(cudaStreamWaitEvent(s1, ctx->ev_cj, 0), "join wait");
     CKC(cond_handle(s1, 0, &h_upd), "handle update");
     CKC(cond_node(s1, h_out, cudaGraphCondTypeWhile, &body_out), "WHILE outer");
     CKC(cudaStreamBeginCaptureToGraph(s2, body_out, nullptr, nullptr, 0, mode), "capture outer");
@@ -1867,7 +1872,9 @@ int otm_run_batch(otm_ctx* ctx, const otm_run_config* cfg, otm_run_state* st, do
     bool finished = false;
     while (done < max_iters && !finished) {
         const int m = std::min(std::min(std::max(batch, 1), max_iters - done), kLoopRing);
-        for (int k = 0; k < m; ++k) CK(cudaGraphLaunch(ctx->gexec_iter, s));
+        H->batch_left = m;
+        CK(cudaMemcpyAsync(&ctx->lstate->batch_left, &H->batch_left, sizeof(int), cudaMemcpyHostToDevice, s));
+        CK(cudaGraphLaunch(ctx->gexec_iter, s));
         CK(cudaMemcpyAsync(H, ctx->lstate, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
         CK(stream_wait(s));
         // records of this batch: iterations first_iter + done + 1 .. H->iter (+1 on failure)

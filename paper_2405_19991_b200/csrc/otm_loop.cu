@@ -24,9 +24,13 @@ __device__ __forceinline__ unsigned long long global_ns() {
     return t;
 }
 
-__global__ void k_iter_begin(LoopState* S, cudaGraphConditionalHandle h) {
-    const bool run = !S->finished;
+// one design iteration of the batch loop: run it unless the run finished or the
+// batch is used up; the WHILE around the batch ends with the first no-run
+__global__ void k_iter_begin(LoopState* S, cudaGraphConditionalHandle h, cudaGraphConditionalHandle h_loop) {
+    const bool run = !S->finished && S->batch_left > 0;
+    cudaGraphSetConditional(h_loop, run ? 1u : 0u);
     if (run) {
+        S->batch_left -= 1;
         S->t0 = global_ns();
         if (S->t_oc) S->ph_ms[3] += (double)(S->t0 - S->t_oc) * 1e-6;
         S->outer = 0;
@@ -37,7 +41,11 @@ __global__ void k_iter_begin(LoopState* S, cudaGraphConditionalHandle h) {
 }
 
 // cold start (solver.py:388-391 with x0 = None): T = 0 before the first solve
-__global__ void k_T_cold(const LoopState* __restrict__ S, long long n3, double* __restrict__ T) {
+// also re-arms the solve's outer WHILE: a conditional's default value is applied per
+// graph launch, and one launch now runs a whole batch of design iterations
+__global__ void k_T_cold(const LoopState* __restrict__ S, long long n3, double* __restrict__ T,
+                         cudaGraphConditionalHandle h_out) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(h_out, 1u);
     if (S->warm) return;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n3; i += (long long)gridDim.x * blockDim.x)
         T[i] = 0.0;
@@ -185,11 +193,11 @@ __global__ void k_oc_account(LoopState* S, const OcCtl* ocl) {
 }  // namespace
 
 void launch_oc_account(cudaStream_t s, LoopState* S, const OcCtl* ocl) { k_oc_account<<<1, 1, 0, s>>>(S, ocl); }
-void launch_iter_begin(cudaStream_t s, LoopState* S, unsigned long long h) {
-    k_iter_begin<<<1, 1, 0, s>>>(S, (cudaGraphConditionalHandle)h);
+void launch_iter_begin(cudaStream_t s, LoopState* S, unsigned long long h, unsigned long long h_loop) {
+    k_iter_begin<<<1, 1, 0, s>>>(S, (cudaGraphConditionalHandle)h, (cudaGraphConditionalHandle)h_loop);
 }
-void launch_T_cold(cudaStream_t s, const LoopState* S, long long n3, double* T) {
-    k_T_cold<<<592, 256, 0, s>>>(S, n3, T);
+void launch_T_cold(cudaStream_t s, const LoopState* S, long long n3, double* T, unsigned long long h_out) {
+    k_T_cold<<<592, 256, 0, s>>>(S, n3, T, (cudaGraphConditionalHandle)h_out);
 }
 void launch_solve_ctl(cudaStream_t s, LoopState* S, const LoopCfg& C, const double* res9, PcgScalars* sc,
                       unsigned long long h_out, unsigned long long h_in) {

@@ -138,6 +138,7 @@ struct LoopState {
     double fnorm[3], rnorm[3], rel[3];
     int done[3], zero_load[3], ccyc[3];
     int cycles, outer;
+    int batch_left;               // iterations the current graph launch may still run (otm_run_batch)
     unsigned long long t0;        // %globaltimer at the start of the iteration
     unsigned long long t_solve, t_eval, t_oc;   // ... at the end of the solve, of the evaluation, of the OC step
     double ph_ms[4];              // accumulated: filter+build+solve, tensor+objective, sens+OC, gap to next
@@ -167,8 +168,8 @@ __host__ __device__ inline bool convergence_step(int model, double conv_threshol
 }
 
 // launchers (otm_loop.cu)
-void launch_iter_begin(cudaStream_t s, LoopState* S, unsigned long long h);
-void launch_T_cold(cudaStream_t s, const LoopState* S, long long n3, double* T);
+void launch_iter_begin(cudaStream_t s, LoopState* S, unsigned long long h_body, unsigned long long h_loop);
+void launch_T_cold(cudaStream_t s, const LoopState* S, long long n3, double* T, unsigned long long h_out);
 void launch_solve_ctl(cudaStream_t s, LoopState* S, const LoopCfg& C, const double* res9, PcgScalars* sc,
                       unsigned long long h_out, unsigned long long h_in);
 void launch_solve_fin(cudaStream_t s, LoopState* S, long long n, double* T);
