@@ -67,7 +67,7 @@ struct otm_ctx {
     SimpParams sp{};
     double* kap64 = nullptr;
     double* T64 = nullptr;
-    double* oc_q = nullptr;                   // k_oc_coop: per-element c_e of the current search
+    double* oc_q = nullptr;                   // k_oc_coop: per-element c_e of the current search (aliases sensf)
     double* oc_lam = nullptr;                 // k_oc_coop: the last update's multiplier (next prediction)
     double* rho_f = nullptr;   // last filtered density used by otm_build (for sensitivities)
     double* sensf = nullptr;   // design-loop scratch: sensitivity wrt rho_f, then wrt rho
@@ -734,7 +734,7 @@ int otm_create(otm_ctx** out, int nx, int ny, int nz, const otm_params* pin) {
     CK(dalloc(ctx, &ctx->gj, 2 * (size_t)ctx->nc * ctx->nc + ctx->nc + 2));
     const size_t mb = max_blocks(ctx);
     CK(dalloc(ctx, &ctx->red.partials, mb * 32 * 2 + mb));     // k_oc_coop: 2 x partials + flags
-    CK(dalloc(ctx, &ctx->oc_q, (size_t)ctx->g0.n));
+    ctx->oc_q = ctx->sensf;       // dead once the adjoint filter has run: the OC search's c_e scratch
     CK(dalloc(ctx, &ctx->oc_lam, 1));
     CK(cudaMemset(ctx->oc_lam, 0, sizeof(double)));
     CK(dalloc(ctx, &ctx->red.counter, 8));
@@ -790,7 +790,7 @@ int otm_destroy(otm_ctx* ctx) {
     if (ctx->lstate) cudaFree(ctx->lstate);
     for (auto& s : ctx->slots) { cudaEventDestroy(s.a); cudaEventDestroy(s.b); }
     auto F = [](void* p) { if (p) cudaFree(p); };
-    F(ctx->kap64); F(ctx->T64); F(ctx->oc_q); F(ctx->oc_lam); F(ctx->rho_f); F(ctx->sensf); F(ctx->sens); F(ctx->r); F(ctx->p); F(ctx->q); F(ctx->d);
+    F(ctx->kap64); F(ctx->T64); F(ctx->oc_lam); F(ctx->rho_f); F(ctx->sensf); F(ctx->sens); F(ctx->r); F(ctx->p); F(ctx->q); F(ctx->d);
     for (size_t l = 0; l < ctx->L.size(); ++l) {
         F(ctx->L[l].kap); F(ctx->L[l].dinv); F(ctx->L[l].z); F(ctx->L[l].res);
         if (l > 0) F(ctx->L[l].f);
