@@ -190,6 +190,11 @@ int otm_coarse_solve(otm_ctx* ctx, const double* f_dev, double* T_dev);
 int otm_tensor(otm_ctx* ctx, double kappa_out[6]);
 /* pair_energy cache (6*n doubles, homogenize.py:116-120), for API compatibility. */
 int otm_pair_energy(otm_ctx* ctx, double* E_dev);
+
+/* HomogenizationResult.elem_diff (homogenize.py:94-100): for one load case's field T
+ * (device, level-0 layout, n doubles) the per-element corner differences
+ * w[e*8 + a] = c_a[load_case] - T[e + c_a] as float32 (n*8 floats, device). */
+int otm_elem_diff(otm_ctx* ctx, const double* T_dev, int load_case, float* w_dev);
 /* tensor_sensitivity (homogenize.py:143-160): sens_f = kappa'(rho_f) dG.E / M. */
 int otm_sensitivity(otm_ctx* ctx, const double dG[6], double* sens_f_dev);
 

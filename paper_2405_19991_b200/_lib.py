@@ -88,6 +88,7 @@ _SIGS = {
     "otm_coarse_solve": (C.c_int, [C.c_void_p, dptr, dptr]),
     "otm_tensor": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "otm_pair_energy": (C.c_int, [C.c_void_p, dptr]),
+    "otm_elem_diff": (C.c_int, [C.c_void_p, dptr, C.c_int, dptr]),
     "otm_sensitivity": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), dptr]),
     "otm_objective": (C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                 C.POINTER(C.c_double), C.POINTER(C.c_double)]),

@@ -1272,6 +1272,14 @@ int otm_pair_energy(otm_ctx* ctx, double* E) {
     return OTM_OK;
 }
 
+int otm_elem_diff(otm_ctx* ctx, const double* T, int load_case, float* w) {
+    if (!ctx || !T || !w || load_case < 0 || load_case > 2) return OTM_EINVAL;
+    launch_elem_diff(ctx->stream, ctx->g0, T, load_case, w);
+    ctx->launches++;
+    CKL();
+    return OTM_OK;
+}
+
 int otm_sensitivity(otm_ctx* ctx, const double dG[6], double* sens) {
     if (!ctx || !dG || !sens) return OTM_EINVAL;
     if (!ctx->have_T) return fail(ctx, OTM_ESTATE, "homogenization caches missing; run effective_tensor first");

@@ -165,6 +165,7 @@ void launch_submean(cudaStream_t s, long long n, double* T, const double* sumT);
 void launch_tensor(cudaStream_t s, const Geo& g, const double* T, const double* kap, Red& red, double* out6,
                    const XRange* xr = nullptr);
 void launch_pair_energy(cudaStream_t s, const Geo& g, const double* T, double* E);
+void launch_elem_diff(cudaStream_t s, const Geo& g, const double* T, int ci, float* w);
 void launch_sens(cudaStream_t s, const Geo& g, const double* T, const double* rf, const SimpParams& sp,
                  const Dg& dG, double* sens, const Dg* dG_dev = nullptr,   // dG_dev != NULL overrides dG
                  const XRange* xr = nullptr);

@@ -1417,22 +1417,6 @@ __device__ __forceinline__ void element_energies(const Geo& g, long long e, cons
     }
 }
 
-__global__ void __launch_bounds__(256, 3) k_tensor(Geo g, const double* __restrict__ T, const double* __restrict__ kap, double* partials,
-                         unsigned* counter, double* out) {
-    double acc[6] = {0, 0, 0, 0, 0, 0};
-    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < g.n;
-         e += (long long)gridDim.x * blockDim.x) {
-        double E[6];
-        element_energies(g, e, T, E);
-        const double k = kap[e];
-#pragma unroll
-        for (int c = 0; c < 6; ++c) acc[c] += k * E[c];
-    }
-    if (reduce_finalize<6>(acc, partials, counter, out)) {
-        for (int c = 0; c < 6; ++c) out[c] /= (double)g.n;
-    }
-}
-
 __global__ void k_pair_energy(Geo g, const double* __restrict__ T, double* __restrict__ Eout) {
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= g.n) return;
@@ -1441,19 +1425,6 @@ __global__ void k_pair_energy(Geo g, const double* __restrict__ T, double* __res
     for (int c = 0; c < 6; ++c) Eout[(size_t)c * g.n + e] = E[c];
 }
 
-// sens_f = kappa'(rho_f) * (dG . E) / M   (homogenize.py:143-160, element.py:97-100)
-__global__ void __launch_bounds__(256, 4) k_sens(Geo g, const double* __restrict__ T, const double* __restrict__ rf, SimpParams sp,
-                       Dg dG, double* __restrict__ sens) {
-    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= g.n) return;
-    double E[6];
-    element_energies(g, e, T, E);
-    double con = 0.0;
-#pragma unroll
-    for (int c = 0; c < 6; ++c) con += dG.v[c] * E[c];
-    const double dk = sp.p * simp_pow(rf[e], sp.p - 1.0) * (sp.k0 - sp.kmin);
-    sens[e] = dk * con / (double)g.n;
-}
 
 // ---- x-marching form (the design-loop path) ---------------------------------
 // In the Walsh-Hadamard basis of the 8 corners (chi_s(a) = (-1)^popcount(s & a))
@@ -2867,6 +2838,24 @@ void launch_tensor(cudaStream_t s, const Geo& g, const double* T, const double* 
     chunks_for(k_tensor_x, g, r.xb - r.xa, ch, for_pl, for_np);
     const long long th = (long long)g.pl * ch;
     k_tensor_x<<<nblk(th, 256), 256, 0, s>>>(g, ch, r, T, kap, red.partials, red.counter, out6);
+}
+// HomogenizationResult.elem_diff (homogenize.py:94-100): w[e, a] = c_a[i] - T_i[e + c_a]
+// as float32, element e = its lower corner, corners periodic
+__global__ void k_elem_diff(Geo g, const double* __restrict__ T, int ci, float* __restrict__ w) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= g.n) return;
+    const int x = (int)(e / g.pl), rem = (int)(e - (long long)x * g.pl);
+    const int y = rem / g.nz, z = rem - y * g.nz;
+    const int xs[2] = {x, wrap_p(x, g.nx)}, ys[2] = {y, wrap_p(y, g.ny)}, zs[2] = {z, wrap_p(z, g.nz)};
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        const int bx = a & 1, by = (a >> 1) & 1, bz = (a >> 2) & 1;
+        const double c = (double)((a >> ci) & 1);
+        w[e * 8 + a] = (float)(c - T[((long long)xs[bx] * g.ny + ys[by]) * g.nz + zs[bz]]);
+    }
+}
+void launch_elem_diff(cudaStream_t s, const Geo& g, const double* T, int ci, float* w) {
+    k_elem_diff<<<nblk(g.n, 256), 256, 0, s>>>(g, T, ci, w);
 }
 void launch_pair_energy(cudaStream_t s, const Geo& g, const double* T, double* E) {
     k_pair_energy<<<nblk(g.n, 256), 256, 0, s>>>(g, T, E);

@@ -14,7 +14,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import _dev
-from .element import CORNERS, MaterialParams
+from .element import MaterialParams
 from .solver import GridHierarchy
 
 PACKED_PAIRS = ((0, 0), (1, 1), (2, 2), (0, 1), (1, 2), (0, 2))     # homogenize.py:23
@@ -95,12 +95,13 @@ class HomogenizationResult:
         """Per case (nx, ny, nz, 8) float32: c_a[i] - T_i[e + c_a] (homogenize.py:94-100)."""
         if "w" not in self._cache:
             t = _dev.torch()
+            h = self._hier
             out = []
             for i, T in enumerate(self.T_fields):
-                Td, _ = _dev.to_device(T)
-                w = t.stack([float(CORNERS[a, i]) - t.roll(Td, shifts=tuple(-int(s) for s in CORNERS[a]),
-                                                              dims=(0, 1, 2)) for a in range(8)], dim=-1)
-                w = w.to(t.float32)
+                Td, _ = _dev.to_device(T, shape=h.dims)
+                Td = Td.contiguous()
+                w = t.empty(tuple(h.dims) + (8,), dtype=t.float32, device="cuda")
+                h.ctx.call("otm_elem_diff", _dev.ptr(Td), i, _dev.ptr(w))
                 out.append(w.cpu().numpy() if self._host() else w)
             self._cache["w"] = out
         return self._cache["w"]

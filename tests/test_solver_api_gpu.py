@@ -237,3 +237,22 @@ def test_flat_grid_solve_vs_oracle(otm, O):
     To, _ = O.solve_three(ho, rho, O.Material(), tol=1e-11)
     for i in range(2):
         assert np.abs(T[i] - To[i]).max() <= 1e-6 * np.abs(To[i]).max()
+
+
+def test_elem_diff_matches_corner_formula(otm):
+    """HomogenizationResult.elem_diff (homogenize.py:94-100) from the device kernel
+    against c_a[i] - T_i[e + c_a] evaluated with numpy rolls."""
+    from paper_2405_19991_b200.element import CORNERS
+    dims = (8, 6, 4)
+    rng = np.random.default_rng(11)
+    rho_f = rng.uniform(0.1, 1.0, dims)
+    mp = otm.MaterialParams()
+    h = otm.GridHierarchy(dims)
+    T, _ = otm.solve_cases(h, rho_f, mp, tol=1e-10)
+    res = otm.effective_tensor(h, T, rho_f, mp)
+    w = res.elem_diff
+    for i in range(3):
+        ref = np.stack([float(CORNERS[a, i]) - np.roll(T[i], tuple(-int(s) for s in CORNERS[a]), axis=(0, 1, 2))
+                        for a in range(8)], axis=-1).astype(np.float32)
+        assert w[i].shape == dims + (8,)
+        assert np.array_equal(w[i], ref)
