@@ -21,6 +21,11 @@ fixed 500 iterations") on the 128^3 IWP seed (vf 0.5), target
          (threads + streams, the gallery's --per-gpu 3); `value` stays the
          one-structure latency
 
+Under ncu (its injection environment) the same kernels run with eager launches from
+the host-driven loop, so a launch list can be taken of this command
+(profiles/r02zc_bench_launches_c3.md); numbers printed under a profiler are not
+bench values.
+
 ``--impl reference`` times that CPU port alone (rank 0) on the same metric: one
 oracle run, W warm-up iterations (the first is the cold solve from the seed),
 then K timed warm-started iterations; value = median x500; plus C1 run to
@@ -647,6 +652,15 @@ def main():
     ap.add_argument("--mode", default="replicas", choices=["replicas", "slab"],
                     help="N>1: independent structures per rank (default) or one structure on x-slabs")
     args = ap.parse_args()
+    if any(os.environ.get(k) for k in ("NV_NSIGHT_INJECTION_TRANSPORT_TYPE", "NV_TPS_LAUNCH_TOKEN",
+                                       "CUDA_INJECTION64_PATH")):
+        # under a profiler (ncu's injection environment): kernel nodes of graphs with
+        # conditional nodes cannot be profiled one by one, so run the same kernels
+        # from the host (eager launches, host-driven design loop); a number printed
+        # under a profiler is never a bench value
+        for k in ("OTM_NO_ITER_GRAPH", "OTM_NO_LOOP_GRAPH", "OTM_EAGER"):
+            os.environ.setdefault(k, "1")
+        args.host_loop = True
     if args.impl == "reference":
         run_reference(args)
     elif args.mode == "slab":
