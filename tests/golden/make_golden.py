@@ -265,6 +265,8 @@ def gen_long(ot, which):
         _run_logged(ot, "traj_c3_3.npz", (128, 128, 128), [0.3, 0.2, 0.1, 0.1, 0.05, 0.05], 0.5, 3)
     elif which == "c3x10":  # config 3, 10 iterations
         _run_logged(ot, "traj_c3_10.npz", (128, 128, 128), [0.3, 0.2, 0.1, 0.1, 0.05, 0.05], 0.5, 10)
+    elif which == "c4x2":   # config 4 (256^3, the C3 target), 2 iterations: k10 nz = 256, lockstep tiles
+        _run_logged(ot, "traj_c4_2.npz", (256, 256, 256), [0.3, 0.2, 0.1, 0.1, 0.05, 0.05], 0.5, 2)
     elif which == "flat":   # tests/test_acceptance.py:144-158 (100x100x1, r = 2, NaN targets)
         _run_logged(ot, "traj_flat100.npz", (100, 100, 1), [0.4, 0.2, np.nan, 0.05, np.nan, np.nan],
                     0.5, 500, filt=2.0)
@@ -317,7 +319,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
     ap.add_argument("--only", default=None)
-    ap.add_argument("--long", default=None, help="c1conv | c2 | c3 | c3x10 | flat")
+    ap.add_argument("--long", default=None, help="c1conv | c2 | c3 | c3x10 | c4x2 | flat")
     ap.add_argument("--tol", type=float, default=None, help="solver_tol of the --long run")
     args = ap.parse_args()
     global SOLVER_TOL

@@ -138,6 +138,19 @@ def test_c3_128_cubed_trajectory(otm, name):
     _compare(res, kap, g, n)
 
 
+def test_c4_256_cubed_two_iterations(otm):
+    """Config 4 (256^3, the C3 target): the first two design iterations against the
+    reference -- the level stencils on nz = 256 and, beyond the L2, the lockstep tile
+    order of the k10 march and of the fp64 defect kernel."""
+    try:
+        g = golden("traj_c4_2.npz")
+    except FileNotFoundError:
+        pytest.skip("traj_c4_2.npz not generated")
+    res, kap = _run(otm, g)
+    assert len(res.log) == int(g["iterations"])
+    _compare(res, kap, g, int(g["iterations"]))
+
+
 def test_c1_to_convergence(otm):
     """Config 1 (32^3 isotropic, vf 0.3) run to convergence: the reference stops at
     iteration 237 with g 9.98e-5 and V 0.2335 (tests/test_acceptance.py:171-179)."""
