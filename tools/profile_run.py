@@ -20,12 +20,16 @@ dims = bench.CONFIGS[cfg_name]["dims"]
 seed = otm.init_density(dims, otm.InitPattern("iwp", bench.CONFIGS[cfg_name]["vf"], seed=0)).rho
 cfg = bench.make_config(otm, cfg_name, iters, 0.0, init_field=seed)
 run = DesignRun(cfg)
+import time
+torch.cuda.synchronize()
+t0 = time.perf_counter()
 if len(sys.argv) > 3 and sys.argv[3] == "graph":
     run.run()                                   # device-resident iteration graph
 else:
     while not run.finished:
         run.step()
 torch.cuda.synchronize()
+print(f"wall {time.perf_counter() - t0:.4f} s")
 lib = run.hier.ctx.lib
 print("launches", lib.otm_launch_count(run.hier.ctx.h), "iterations", len(run.log),
       "vcycles", sum(r.vcycles for r in run.log))
