@@ -447,7 +447,14 @@ def run_gpu(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         cfg = make_config(otm, name, args.iters, 0.0, init_field=seed)     # numpy seed: H2D inside
-        res = otm.run_optimization(cfg)                                     # numpy field back: D2H inside
+        if s == 0 and os.environ.get("OTM_BENCH_PSTATS"):                    # where a slow first call went
+            import cProfile
+            import pstats
+            pr = cProfile.Profile()
+            res = pr.runcall(otm.run_optimization, cfg)
+            pstats.Stats(pr, stream=sys.stderr).sort_stats("tottime").print_stats(10)
+        else:
+            res = otm.run_optimization(cfg)                                 # numpy field back: D2H inside
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
         assert isinstance(res.field.rho, np.ndarray)
