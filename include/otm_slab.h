@@ -50,6 +50,13 @@ const char* otm_slab_last_error(otm_slab_ws* w);
 int otm_slab_stencil(otm_slab_ws* w, int op, int nxl, int ny, int nz, const double scale[3], const float* kap,
                      const float* a, const float* f, const float* dinv, double omega, float* o1, float* o2,
                      double* dots3);
+/* otm_slab_stencil on the output planes [x_lo, x_hi) of the ghost-padded slab only
+ * (1 <= x_lo < x_hi <= nxl + 1; dots3 sums over those planes).  Planes 2 .. nxl-1 do
+ * not read the ghost planes, so they can run while the halo exchange is in flight;
+ * planes 1 and nxl follow it (slab.py SlabSolver._overlapped). */
+int otm_slab_stencil_range(otm_slab_ws* w, int op, int nxl, int ny, int nz, const double scale[3], const float* kap,
+                           const float* a, const float* f, const float* dinv, double omega, float* o1, float* o2,
+                           int x_lo, int x_hi, double* dots3);
 /* fine slab (nxl_f even, starting at an even global plane) -> coarse slab interior */
 int otm_slab_restrict(otm_slab_ws* w, int nxl_f, int ny_f, int nz_f, const float* res_f, float* f_c);
 /* z_f (interior) += P z_c; z_c needs its right ghost plane */

@@ -118,6 +118,9 @@ _SIGS = {
     "otm_slab_last_error": (C.c_char_p, [C.c_void_p]),
     "otm_slab_stencil": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double), dptr,
                                    dptr, dptr, dptr, C.c_double, dptr, dptr, C.POINTER(C.c_double)]),
+    "otm_slab_stencil_range": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
+                                         dptr, dptr, dptr, dptr, C.c_double, dptr, dptr, C.c_int, C.c_int,
+                                         C.POINTER(C.c_double)]),
     "otm_slab_set_scalar_mode": (C.c_int, [C.c_void_p, C.c_int]),
     "otm_slab_pcg_step": (C.c_int, [C.c_void_p, C.c_int, dptr]),
     "otm_slab_halo_local": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_longlong, C.c_void_p, C.c_int, C.c_void_p,

@@ -35,8 +35,9 @@ struct W27 {
 struct SGeo {
     int nxl, ny, nz;
     int pl;             // ny * nz
-    long long ni;       // interior values per case: nxl * pl
+    long long ni;       // items per case: nxl * pl (a plane range: its planes * pl)
     long long na;       // allocated values per case: (nxl + 2) * pl
+    int x0;             // first item plane (1: the whole interior)
 };
 
 SGeo make_sgeo(int nxl, int ny, int nz) {
@@ -45,16 +46,17 @@ SGeo make_sgeo(int nxl, int ny, int nz) {
     g.pl = ny * nz;
     g.ni = (long long)nxl * g.pl;
     g.na = (long long)(nxl + 2) * g.pl;
+    g.x0 = 1;
     return g;
 }
 
-// interior item i (0 .. ni-1) -> local plane (1 .. nxl), y, z
+// item i (0 .. ni-1) -> local plane (x0 .. ; 1 .. nxl for the interior), y, z
 __device__ __forceinline__ void s_decode(const SGeo& g, long long i, int& x, int& y, int& z) {
     x = (int)(i / g.pl);
     const int rem = (int)(i - (long long)x * g.pl);
     y = rem / g.nz;
     z = rem - y * g.nz;
-    x += 1;
+    x += g.x0;
 }
 
 // 27 operand values around (x, y, z): x from the ghosted planes, y/z periodic
@@ -716,18 +718,27 @@ const char* otm_slab_last_error(otm_slab_ws* w) { return w ? w->err : "null work
 int otm_slab_stencil(otm_slab_ws* w, int op, int nxl, int ny, int nz, const double scale[3], const float* kap,
                      const float* a, const float* f, const float* dinv, double omega, float* o1, float* o2,
                      double* dots3) {
+    return otm_slab_stencil_range(w, op, nxl, ny, nz, scale, kap, a, f, dinv, omega, o1, o2, 1, nxl + 1, dots3);
+}
+
+int otm_slab_stencil_range(otm_slab_ws* w, int op, int nxl, int ny, int nz, const double scale[3], const float* kap,
+                           const float* a, const float* f, const float* dinv, double omega, float* o1, float* o2,
+                           int x_lo, int x_hi, double* dots3) {
     if (!w || nxl < 1 || ny < 1 || nz < 1 || op < 0 || op > 2) return OTM_EINVAL;
-    const SGeo g = make_sgeo(nxl, ny, nz);
+    if (x_lo < 1 || x_hi > nxl + 1 || x_hi <= x_lo) return OTM_EINVAL;
+    SGeo g = make_sgeo(nxl, ny, nz);
+    g.x0 = x_lo;
+    g.ni = (long long)(x_hi - x_lo) * g.pl;
     const LevelTemplate lt = tmpl(scale);
     const long long items = 3 * g.ni;
     if (!blocks_ok(w, items, 256)) return OTM_EINVAL;
     const int dot = dots3 != nullptr && op > 0;
     {
-        // fast path: the single-GPU k10 march on the interior planes [1, nxl] of the
+        // fast path: the single-GPU k10 march on the output planes [x_lo, x_hi) of the
         // ghost-padded slab (the x neighbours are the ghost planes; y, z periodic)
         const Geo gg = make_geo(nxl + 2, ny, nz);
         Red red{w->partials, w->counter};
-        if (launch_k10_range(w->stream, op, gg, lt, 1, nxl + 1, kap, a, f, dinv, (float)omega, o1, o2, dot != 0,
+        if (launch_k10_range(w->stream, op, gg, lt, x_lo, x_hi, kap, a, f, dinv, (float)omega, o1, o2, dot != 0,
                              red, w->sc)) {
             int rc = scheck(w);
             if (rc || !dot) return rc;

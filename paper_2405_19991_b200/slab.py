@@ -140,6 +140,13 @@ class LocalComm:
             t.select(-3, 0).copy_(left.select(-3, left.shape[-3] - 2))
             t.select(-3, t.shape[-3] - 1).copy_(right.select(-3, 1))
 
+    def halo_start(self, ts):
+        """In-process ghost planes are plain device copies: done at once."""
+        self.halo(ts)
+
+    def halo_finish(self, pending):
+        pass
+
     def allreduce(self, vals):
         out = np.zeros_like(np.asarray(vals[0], dtype=np.float64))
         for v in vals:                      # rank order: deterministic
@@ -170,6 +177,13 @@ class DistComm:
         self.ranks = [dist.get_rank(group)]
 
     def halo(self, ts):
+        self.halo_finish(self.halo_start(ts))
+
+    def halo_start(self, ts):
+        """Post the exchange of the two boundary planes with the neighbours (NCCL runs
+        it on its own stream, after the work already queued on the current one) and
+        return without waiting: the caller can queue work that does not read the ghost
+        planes before halo_finish."""
         (t,) = ts
         dist = self.dist
         r, W = self.ranks[0], self.world
@@ -177,7 +191,7 @@ class DistComm:
             if not _halo_kernel([t], [t], [t]):
                 t.select(-3, 0).copy_(t.select(-3, t.shape[-3] - 2))
                 t.select(-3, t.shape[-3] - 1).copy_(t.select(-3, 1))
-            return
+            return None
         last = t.select(-3, t.shape[-3] - 2).contiguous()
         first = t.select(-3, 1).contiguous()
         from_left = last.new_empty(last.shape)
@@ -186,7 +200,15 @@ class DistComm:
                dist.P2POp(dist.isend, first, (r - 1) % W, self.group),
                dist.P2POp(dist.irecv, from_left, (r - 1) % W, self.group),
                dist.P2POp(dist.irecv, from_right, (r + 1) % W, self.group)]
-        for q in dist.batch_isend_irecv(ops):
+        return dist.batch_isend_irecv(ops), t, from_left, from_right, (last, first)
+
+    def halo_finish(self, pending):
+        """Wait for a halo_start exchange (the current stream waits on NCCL's) and
+        write the received planes into the ghost planes."""
+        if pending is None:
+            return
+        reqs, t, from_left, from_right, _sent = pending
+        for q in reqs:
             q.wait()
         t.select(-3, 0).copy_(from_left)
         t.select(-3, t.shape[-3] - 1).copy_(from_right)
@@ -303,6 +325,21 @@ class CudaSlabBackend:
         self._rc(self._dev_call(self.lib.otm_slab_stencil, self.ws, op, *dims, self._d3(scale), self._p(kap),
                                 self._p(a), self._p(f), self._p(dinv), float(omega), self._p(o1), self._p(o2),
                                 C.cast(C.c_void_p(out.data_ptr()), C.POINTER(C.c_double))))
+        return out
+
+    def stencil_range(self, op, dims, scale, kap, a, f, dinv, omega, o1, o2, x_lo, x_hi, want_dots=False):
+        """otm_slab_stencil_range: only the output planes [x_lo, x_hi) of the ghosted
+        slab; want_dots returns the range's dot products as a (3,) device tensor."""
+        self._sync_stream()
+        if not want_dots:
+            self._rc(self.lib.otm_slab_stencil_range(self.ws, op, *dims, self._d3(scale), self._p(kap), self._p(a),
+                                                     self._p(f), self._p(dinv), float(omega), self._p(o1),
+                                                     self._p(o2), int(x_lo), int(x_hi), None))
+            return None
+        out = self.t.empty(3, dtype=self.f64, device="cuda")
+        self._rc(self._dev_call(self.lib.otm_slab_stencil_range, self.ws, op, *dims, self._d3(scale), self._p(kap),
+                                self._p(a), self._p(f), self._p(dinv), float(omega), self._p(o1), self._p(o2),
+                                int(x_lo), int(x_hi), C.cast(C.c_void_p(out.data_ptr()), C.POINTER(C.c_double))))
         return out
 
     def pupd_dev(self, dims, z, p, beta):
@@ -464,6 +501,11 @@ class SlabSolver:
         self.n_total = int(np.prod(dims))
         self.warm = False
         self.fmean = np.zeros(3)
+        # halo / stencil overlap: on where the exchange is a real transfer (NCCL between
+        # processes); OTM_SLAB_OVERLAP=1 forces it (tests: the split on any comm), =0 off
+        import os
+        ov = os.environ.get("OTM_SLAB_OVERLAP")
+        self.overlap = (ov == "1") if ov is not None else (isinstance(comm, DistComm) and comm.world > 1)
 
     # ---- helpers
     def _cidx(self, s, device):
@@ -480,6 +522,30 @@ class SlabSolver:
 
     def _halo(self, get):
         self.comm.halo([get(s) for s in self.slabs])
+
+    def _stencil_after_halo(self, get, level, full, part):
+        """The halo exchange of get(s) followed by a stencil reading it: full(s) runs
+        the stencil on the whole slab once the ghost planes are in (-> dots or None).
+        With self.overlap the stencil is split (SURVEY 8(e) overlap): part(s, lo, hi)
+        on the output planes [2, nxl) -- which read no ghost plane -- is queued while
+        the exchange is in flight, planes 1 and nxl after it; the three partial dot
+        products are added (a different summation order than full())."""
+        if not self.overlap:
+            self._halo(get)
+            return [full(s) for s in self.slabs]
+        pending = self.comm.halo_start([get(s) for s in self.slabs])
+        n = self.slabs[0].levels[level].dims[0]
+        inner = [part(s, 2, n) if n > 2 else None for s in self.slabs]
+        self.comm.halo_finish(pending)
+        out = []
+        for s, di in zip(self.slabs, inner):
+            parts = [di, part(s, 1, 2)] + ([part(s, n, n + 1)] if n > 1 else [])
+            parts = [d for d in parts if d is not None]
+            tot = None
+            for d in parts:
+                tot = d if tot is None else tot + d
+            out.append(tot)
+        return out
 
     def _sum(self, vals):
         return self.comm.allreduce(vals)
@@ -522,11 +588,17 @@ class SlabSolver:
         nd = L.nlev_dist
         dots = [None] * len(self.slabs)
         for l in range(nd):
-            self._halo(lambda s, l=l: s.levels[l].f)
             om = self.omega if l == 0 else self.omega_coarse
-            for s in self.slabs:
+
+            def sm_full(s, l=l, om=om):
                 lv = s.levels[l]
                 B.stencil(0, lv.dims, L.scales[l], lv.kap, None, lv.f, lv.dinv, om, lv.z, lv.res)
+
+            def sm_part(s, lo, hi, l=l, om=om):
+                lv = s.levels[l]
+                B.stencil_range(0, lv.dims, L.scales[l], lv.kap, None, lv.f, lv.dinv, om, lv.z, lv.res, lo, hi)
+
+            self._stencil_after_halo(lambda s, l=l: s.levels[l].f, l, sm_full, sm_part)
             self._halo(lambda s, l=l: s.levels[l].res)
             for s in self.slabs:
                 lv = s.levels[l]
@@ -544,14 +616,22 @@ class SlabSolver:
                 lv = s.levels[l]
                 src = s.levels[l + 1].res if l + 1 < nd else s.cres
                 B.prolong(lv.dims, src, lv.z)
-            self._halo(lambda s, l=l: s.levels[l].z)
             om = self.omega if l == 0 else self.omega_coarse
-            for s_i, s in enumerate(self.slabs):
+
+            def jac_full(s, l=l, om=om):
                 lv = s.levels[l]
                 if l == 0:
-                    dots[s_i] = B.stencil_dev(1, lv.dims, L.scales[l], lv.kap, lv.z, lv.f, lv.dinv, om, lv.res)
-                else:
-                    B.stencil(1, lv.dims, L.scales[l], lv.kap, lv.z, lv.f, lv.dinv, om, lv.res, None)
+                    return B.stencil_dev(1, lv.dims, L.scales[l], lv.kap, lv.z, lv.f, lv.dinv, om, lv.res)
+                B.stencil(1, lv.dims, L.scales[l], lv.kap, lv.z, lv.f, lv.dinv, om, lv.res, None)
+
+            def jac_part(s, lo, hi, l=l, om=om):
+                lv = s.levels[l]
+                return B.stencil_range(1, lv.dims, L.scales[l], lv.kap, lv.z, lv.f, lv.dinv, om, lv.res, None,
+                                       lo, hi, want_dots=(l == 0))
+
+            got = self._stencil_after_halo(lambda s, l=l: s.levels[l].z, l, jac_full, jac_part)
+            if l == 0:
+                dots = got
             if l > 0:
                 self._halo(lambda s, l=l: s.levels[l].res)
         return self._pcg_dots(dots)                       # r . z per case (device)
@@ -601,9 +681,11 @@ class SlabSolver:
             B.pcg_step(0, S)
             for s in self.slabs:
                 B.pupd_dev(d0, s.levels[0].res, s.p, S[6:9])
-            self._halo(lambda s: s.p)
-            pq = self._pcg_dots([B.stencil_dev(2, d0, sc0, s.levels[0].kap, s.p, None, None, 0.0, s.q)
-                                 for s in self.slabs])
+            pq = self._pcg_dots(self._stencil_after_halo(
+                lambda s: s.p, 0,
+                lambda s: B.stencil_dev(2, d0, sc0, s.levels[0].kap, s.p, None, None, 0.0, s.q),
+                lambda s, lo, hi: B.stencil_range(2, d0, sc0, s.levels[0].kap, s.p, None, None, 0.0, s.q, None,
+                                                  lo, hi, want_dots=True)))
             B.put(S, 9, pq)
             B.pcg_step(1, S)
             rr = self._pcg_dots([B.upd_dev(d0, s.d, s.levels[0].f, s.p, s.q, S[12:15]) for s in self.slabs])

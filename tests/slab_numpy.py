@@ -107,6 +107,22 @@ class NumpySlabBackend:
             self._w(o2, np.stack(outs2))
         return dots if want_dots else None
 
+    def stencil_range(self, op, dims, scale, kap, a, f, dinv, omega, o1, o2, x_lo, x_hi, want_dots=False):
+        """otm_slab_stencil_range: the whole-slab stencil on the arrays as they are now,
+        of which only the output planes [x_lo, x_hi) are written; dots over those planes."""
+        t1 = o1.clone()
+        t2 = o2.clone() if o2 is not None else None
+        self.stencil(op, dims, scale, kap, a, f, dinv, omega, t1, t2)
+        k = x_hi - x_lo
+        o1.narrow(-3, x_lo, k).copy_(t1.narrow(-3, x_lo, k))
+        if o2 is not None:
+            o2.narrow(-3, x_lo, k).copy_(t2.narrow(-3, x_lo, k))
+        if not want_dots:
+            return None
+        out = self._n(o1)[:, x_lo:x_hi]
+        other = self._n(f if op == 1 else a)[:, x_lo:x_hi]
+        return (other * out).sum(axis=(1, 2, 3))
+
     # device-scalar protocol of slab.py (here plain numpy arrays)
     @staticmethod
     def scalars(n):

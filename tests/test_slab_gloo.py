@@ -20,9 +20,11 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, dims, q):
+def _worker(rank, world, port, dims, q, overlap=None):
     import torch
     import torch.distributed as dist
+    if overlap is not None:
+        os.environ["OTM_SLAB_OVERLAP"] = overlap
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -42,11 +44,11 @@ def _worker(rank, world, port, dims, q):
         dist.destroy_process_group()
 
 
-def _run(world, dims):
+def _run(world, dims, overlap=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, q, overlap)) for r in range(world)]
     for p in procs:
         p.start()
     out = [q.get(timeout=300) for _ in range(world)]
@@ -56,8 +58,11 @@ def _run(world, dims):
     return sorted(out, key=lambda t: t[0])
 
 
-@pytest.mark.parametrize("world,dims", [(1, (8, 8, 8)), (2, (16, 8, 8)), (4, (16, 8, 8))])
-def test_distributed_slab_solve_matches_oracle(world, dims):
+# overlap: None = the default (the halo / interior-stencil split on for world > 1),
+# "1" forces the split at world 1, "0" turns it off at world 2
+@pytest.mark.parametrize("world,dims,overlap", [(1, (8, 8, 8), None), (1, (8, 8, 8), "1"), (2, (16, 8, 8), None),
+                                                (2, (16, 8, 8), "0"), (4, (16, 8, 8), None)])
+def test_distributed_slab_solve_matches_oracle(world, dims, overlap):
     from oracle import otm_oracle as O
     rng = np.random.default_rng(3)
     rho_f = rng.uniform(0.05, 1.0, dims)
@@ -66,7 +71,7 @@ def test_distributed_slab_solve_matches_oracle(world, dims):
     h.build(O.simp(rho_f, mat))
     To, _ = O.solve_three(h, rho_f, mat, tol=1e-11)
     ko = O.tensor_from_energies(O.pair_energies(To), rho_f, mat)
-    res = _run(world, dims)
+    res = _run(world, dims, overlap)
     for rank, cycles, k, T in res:
         assert cycles > 0
         for i in range(3):

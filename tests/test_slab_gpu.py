@@ -46,6 +46,68 @@ def test_slab_solve_matches_single_gpu(dims, world):
     assert cycles > 0
 
 
+@pytest.mark.parametrize("dims,world", [((32, 32, 32), 2), ((64, 64, 64), 4), ((16, 32, 128), 2), ((8, 16, 16), 4)])
+def test_slab_solve_halo_overlap_split(dims, world, monkeypatch):
+    """OTM_SLAB_OVERLAP=1: every stencil after a halo exchange runs as the interior
+    output planes [2, nxl) + planes 1 and nxl (otm_slab_stencil_range; k10 ranges of
+    one plane at nz 64 / 128) with the three partial dot products added -- what the
+    NCCL path does between processes.  Same answers as the whole-slab launches."""
+    import paper_2405_19991_b200 as otm
+    rng = np.random.default_rng(7 + world)
+    rho_f = rng.uniform(0.05, 1.0, dims)
+    mp = otm.MaterialParams()
+    h = otm.GridHierarchy(dims)
+    T_ref, _ = otm.solve_cases(h, rho_f, mp, tol=1e-10)
+    base, cyc0 = _solve_slabs(dims, world, rho_f, tol=1e-10)
+    monkeypatch.setenv("OTM_SLAB_OVERLAP", "1")
+    split, cyc1 = _solve_slabs(dims, world, rho_f, tol=1e-10)
+    assert split.overlap and not base.overlap
+    T0 = base.fields().cpu().numpy()
+    T1 = split.fields().cpu().numpy()
+    for i in range(3):
+        assert np.abs(T1[i] - T_ref[i]).max() <= 1e-7 * np.abs(T_ref[i]).max()
+        assert np.abs(T1[i] - T0[i]).max() <= 1e-7 * np.abs(T0[i]).max()
+    assert abs(cyc1 - cyc0) <= 3
+
+
+def test_stencil_range_writes_only_its_planes():
+    """otm_slab_stencil_range on [lo, hi) equals the whole-slab launch on those planes
+    (bit for bit: the same per-vertex arithmetic) and leaves the other planes alone;
+    the range dot products add up to the whole-slab ones."""
+    import torch
+    from paper_2405_19991_b200.slab import CudaSlabBackend
+    for dims in ((6, 16, 16), (6, 64, 64)):        # generic kernel / k10 march
+        nxl, ny, nz = dims
+        B = CudaSlabBackend(3 * (nxl + 2) * ny * nz)
+        g = torch.Generator().manual_seed(5)
+        kap = (0.05 + torch.rand((nxl + 2, ny, nz), generator=g)).cuda()
+        dinv = (0.5 + torch.rand((nxl + 2, ny, nz), generator=g)).cuda()
+        a = torch.randn((3, nxl + 2, ny, nz), generator=g).cuda()
+        f = torch.randn((3, nxl + 2, ny, nz), generator=g).cuda()
+        sc = (1.0, 1.0, 1.0)
+        for op in (0, 1, 2):
+            o1 = torch.zeros_like(a)
+            o2 = torch.zeros_like(a) if op == 0 else None
+            B.stencil(op, dims, sc, kap, a if op else None, f if op < 2 else None, dinv if op < 2 else None, 0.9,
+                      o1, o2)
+            whole = B.stencil_dev(op, dims, sc, kap, a if op else None, f if op < 2 else None,
+                                  dinv if op < 2 else None, 0.9, torch.zeros_like(a)) if op else None
+            tot = 0.0
+            r1 = torch.full_like(a, 7.0)
+            r2 = torch.full_like(a, 7.0) if op == 0 else None
+            for lo, hi in ((2, nxl), (1, 2), (nxl, nxl + 1)):
+                d = B.stencil_range(op, dims, sc, kap, a if op else None, f if op < 2 else None,
+                                    dinv if op < 2 else None, 0.9, r1, r2, lo, hi, want_dots=op > 0)
+                if op:
+                    tot = tot + d
+            assert torch.equal(r1[:, 1:nxl + 1], o1[:, 1:nxl + 1])
+            assert (r1[:, 0] == 7.0).all() and (r1[:, nxl + 1] == 7.0).all()
+            if op == 0:
+                assert torch.equal(r2[:, 1:nxl + 1], o2[:, 1:nxl + 1])
+            else:
+                assert torch.allclose(tot, whole, rtol=1e-12, atol=0)
+
+
 def test_slab_design_run_tracks_single_gpu():
     """12 OC iterations of the slab design loop (2 slabs) against run_optimization."""
     import torch
