@@ -2341,6 +2341,15 @@ void launch_coarse_solve(cudaStream_t s, int n, const float* G, const float* f, 
 static bool encode_map64c(CUtensorMap* m, const double* base, const Geo& g, int box_rows) {
     PFN_encodeTiled_t fn = encode_fn();
     if (!fn) return false;
+    if (g.nz > 256) {                     // z split into (256, nz / 256) (box dims hold <= 256 elements)
+        const cuuint64_t d5[5] = {256, (cuuint64_t)(g.nz / 256), 3, (cuuint64_t)g.ny, (cuuint64_t)g.nx};
+        const cuuint64_t s5[4] = {256 * 8, (cuuint64_t)g.n * 8, (cuuint64_t)g.nz * 8, (cuuint64_t)g.pl * 8};
+        const cuuint32_t b5[5] = {256, (cuuint32_t)(g.nz / 256), 3, (cuuint32_t)box_rows, 1};
+        const cuuint32_t e5[5] = {1, 1, 1, 1, 1};
+        return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, (void*)base, d5, s5, b5, e5, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
     const cuuint64_t dims[4] = {(cuuint64_t)g.nz, 3, (cuuint64_t)g.ny, (cuuint64_t)g.nx};
     const cuuint64_t strides[3] = {(cuuint64_t)g.n * 8, (cuuint64_t)g.nz * 8, (cuuint64_t)g.pl * 8};
     const cuuint32_t box[4] = {(cuuint32_t)g.nz, 3, (cuuint32_t)box_rows, 1};
@@ -2376,9 +2385,22 @@ static void l_res64p(cudaStream_t s, const Geo& g, const LevelTemplate& lt, cons
                                                                     out9, skip);
 }
 
+// z extents with a k_res64p instantiation (OTM_RES64P_512=0: nz = 512 on k_res64w<512>)
+static bool res64p_nz(int nz) {
+    static const bool p512 = !(getenv("OTM_RES64P_512") && atoi(getenv("OTM_RES64P_512")) == 0);
+    return nz == 64 || nz == 128 || nz == 256 || (nz == 512 && p512);
+}
+static void l_res64p_nz(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const R64PMaps& M, const double* fmean,
+                        float* r32, Red& red, double* out9, const int* skip) {
+    if (g.nz == 64) l_res64p<64>(s, g, lt, M, fmean, r32, red, out9, skip);
+    else if (g.nz == 128) l_res64p<128>(s, g, lt, M, fmean, r32, red, out9, skip);
+    else if (g.nz == 256) l_res64p<256>(s, g, lt, M, fmean, r32, red, out9, skip);
+    else l_res64p<512>(s, g, lt, M, fmean, r32, red, out9, skip);
+}
+
 bool launch_res64_range(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const double* kap, const double* T,
                         const double* fmean, float* r32, Red& red, double* out9, const XRange& xr) {
-    if (!lt.equal || !(g.nz == 64 || g.nz == 128 || g.nz == 256) || xr.xa < 1 || xr.xb > g.nx - 1 || xr.xb <= xr.xa)
+    if (!lt.equal || !res64p_nz(g.nz) || xr.xa < 1 || xr.xb > g.nx - 1 || xr.xb <= xr.xa)
         return false;
     const int ty = g.nz >= 256 ? 1 : 256 / g.nz;
     if (g.ny % ty != 0 || g.ny < 2 * ty) return false;
@@ -2389,9 +2411,7 @@ bool launch_res64_range(cudaStream_t s, const Geo& g, const LevelTemplate& lt, c
         return false;
     M.xa = xr.xa;
     M.xb = xr.xb;
-    if (g.nz == 64) l_res64p<64>(s, g, lt, M, fmean, r32, red, out9, nullptr);
-    else if (g.nz == 128) l_res64p<128>(s, g, lt, M, fmean, r32, red, out9, nullptr);
-    else l_res64p<256>(s, g, lt, M, fmean, r32, red, out9, nullptr);
+    l_res64p_nz(s, g, lt, M, fmean, r32, red, out9, nullptr);
     return true;
 }
 
@@ -2399,7 +2419,7 @@ void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const d
                   const double* fext, const double* fmean, float* r32, Red& red, double* out9, const int* skip) {
     // all three cases in one push march (k_res64p; OTM_RES64P=0: the per-case k_res64w)
     static const bool use_p = !(getenv("OTM_RES64P") && atoi(getenv("OTM_RES64P")) == 0);
-    if (use_p && !fext && lt.equal && (g.nz == 64 || g.nz == 128 || g.nz == 256) && g.nx >= 2) {
+    if (use_p && !fext && lt.equal && res64p_nz(g.nz) && g.nx >= 2) {
         const int ty = g.nz >= 256 ? 1 : 256 / g.nz;
         if (g.ny % ty == 0 && g.ny >= 2 * ty) {
             // per host thread: structures designed concurrently from several threads
@@ -2422,9 +2442,7 @@ void launch_res64(cudaStream_t s, const Geo& g, const LevelTemplate& lt, const d
             if (lastok) {
                 M.xa = 0;
                 M.xb = g.nx;
-                if (g.nz == 64) l_res64p<64>(s, g, lt, M, fmean, r32, red, out9, skip);
-                else if (g.nz == 128) l_res64p<128>(s, g, lt, M, fmean, r32, red, out9, skip);
-                else l_res64p<256>(s, g, lt, M, fmean, r32, red, out9, skip);
+                l_res64p_nz(s, g, lt, M, fmean, r32, red, out9, skip);
                 return;
             }
         }

@@ -27,7 +27,7 @@ struct R64P {
     static constexpr int K = (TY + 2) * 3 * NZ;              // (TY + 1) x NZ doubles
     static constexpr int SLOT = K + (TY + 1) * NZ;
     static constexpr int SLOT_BYTES = SLOT * 8;
-    static constexpr int CPS = 2;                            // CTAs per SM the ring is sized for
+    static constexpr int CPS = NZ > 256 ? 1 : 2;             // CTAs per SM the ring is sized for
     static constexpr int BUDGET = (224 * 1024) / CPS - 2048;
     static constexpr int ST0 = BUDGET / (SLOT_BYTES + 8);
     static constexpr int STAGES = ST0 > 8 ? 8 : ST0;
@@ -35,6 +35,20 @@ struct R64P {
     static constexpr size_t SMEM = (size_t)STAGES * SLOT_BYTES + STAGES * 8;
     static_assert(STAGES >= 3, "res64p ring too shallow");
 };
+
+// Box loads: a TMA box dimension holds at most 256 elements, so for NZ > 256 the
+// host splits z into (256, NZ / 256) map dimensions (as k10_ld_c3); the box lands as
+// [row][case][NZ] / [row][NZ], the same layout.
+template <int NZ>
+__device__ __forceinline__ void r64_ld_t(void* dst, const CUtensorMap* map, int y, int x, uint64_t* bar) {
+    if constexpr (NZ > 256) tma_load_5d(reinterpret_cast<float*>(dst), map, 0, 0, 0, y, x, bar);
+    else tma_load_4d(reinterpret_cast<float*>(dst), map, 0, 0, y, x, bar);
+}
+template <int NZ>
+__device__ __forceinline__ void r64_ld_k(void* dst, const CUtensorMap* map, int y, int x, uint64_t* bar) {
+    if constexpr (NZ > 256) tma_load_4d(reinterpret_cast<float*>(dst), map, 0, 0, y, x, bar);
+    else tma_load_3d(reinterpret_cast<float*>(dst), map, 0, y, x, bar);
+}
 
 struct R64PMaps {
     CUtensorMap t_full, t_main, t_halo;      // 4-D (z, case, y, x) fp64: TY + 2 / TY / 1 rows
@@ -148,18 +162,15 @@ __global__ void __launch_bounds__(R64P<NZ>::THREADS, R64P<NZ>::CPS)
             x = x < 0 ? x + g.nx : (x >= g.nx ? x - g.nx : x);
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             mbar_expect_tx(bars + k, (unsigned)P::SLOT_BYTES);
-            float* St = reinterpret_cast<float*>(S + P::T);
-            float* Sk = reinterpret_cast<float*>(S + P::K);
             if (!seam) {
-                tma_load_4d(St, &maps.t_full, 0, 0, y0 - 1, x, bars + k);
-                tma_load_3d(Sk, &maps.k_full, 0, y0 - 1, x, bars + k);
+                r64_ld_t<NZ>(S + P::T, &maps.t_full, y0 - 1, x, bars + k);
+                r64_ld_k<NZ>(S + P::K, &maps.k_full, y0 - 1, x, bars + k);
             } else {
-                tma_load_4d(St, &maps.t_halo, 0, 0, ym, x, bars + k);
-                tma_load_4d(reinterpret_cast<float*>(S + P::T + 3 * NZ), &maps.t_main, 0, 0, y0, x, bars + k);
-                tma_load_4d(reinterpret_cast<float*>(S + P::T + (TY + 1) * 3 * NZ), &maps.t_halo, 0, 0, yp, x,
-                            bars + k);
-                tma_load_3d(Sk, &maps.k_halo, 0, ym, x, bars + k);
-                tma_load_3d(reinterpret_cast<float*>(S + P::K + NZ), &maps.k_main, 0, y0, x, bars + k);
+                r64_ld_t<NZ>(S + P::T, &maps.t_halo, ym, x, bars + k);
+                r64_ld_t<NZ>(S + P::T + 3 * NZ, &maps.t_main, y0, x, bars + k);
+                r64_ld_t<NZ>(S + P::T + (TY + 1) * 3 * NZ, &maps.t_halo, yp, x, bars + k);
+                r64_ld_k<NZ>(S + P::K, &maps.k_halo, ym, x, bars + k);
+                r64_ld_k<NZ>(S + P::K + NZ, &maps.k_main, y0, x, bars + k);
             }
             ++sissue;
             ki = ki + 1 == STAGES ? 0 : ki + 1;
