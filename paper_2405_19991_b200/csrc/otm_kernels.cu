@@ -1763,7 +1763,10 @@ __device__ void oc_walk(OcCtl* C) {
     oc_plan_tree(C);
 }
 
-__global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* __restrict__ rho,
+// SMACC: the 32 per-lane candidate accumulators in shared memory instead of 64
+// registers (3 CTAs per SM instead of 2; chosen beyond L2, launch_oc_coop)
+template <bool SMACC>
+__global__ void __launch_bounds__(256, SMACC ? 3 : 2) k_oc_coop(long long n, const double* __restrict__ rho,
                                                     const double* __restrict__ sens, const OcArgs a,
                                                     double* rho_out, OcCtl* C, double* partials,
                                                     double* __restrict__ qbuf, double* lam_mem) {
@@ -1871,9 +1874,16 @@ __global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* _
         const double lpk = lane < nlam ? s_lp[lane] : 0.0;
         const bool free0 = s_lp[0] == 0.0;
         const double lpmin = s_lpr[0], lpmax = s_lpr[1];
-        double acc[kOcLam];
+        extern __shared__ double oc_acc_dyn[];          // SMACC: [kOcLam][256]
+        double* A = oc_acc_dyn + threadIdx.x;
+        double acc[SMACC ? 1 : kOcLam];
+        if constexpr (SMACC) {
 #pragma unroll
-        for (int k = 0; k < kOcLam; ++k) acc[k] = 0.0;
+            for (int k = 0; k < kOcLam; ++k) A[k * 256] = 0.0;
+        } else {
+#pragma unroll
+            for (int k = 0; k < kOcLam; ++k) acc[k] = 0.0;
+        }
         double acck = 0.0, sCn = 0.0, sL = 0.0, sF = 0.0;
         const long long wstride = (long long)gridDim.x * nw * 32;
         // the next element's (rho, sens) are loaded before this one is processed: the
@@ -1930,9 +1940,15 @@ __global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* _
                 if (mixed) {
                     // only slot 0 can be the free step (lam = 0); slots >= nlam (lam^-damp 0)
                     // accumulate values nobody reads
-                    acc[0] += free0 ? freev : fmin(fmax(ce * s_lp[0], lof), hi);
+                    if constexpr (SMACC) {
+                        A[0] += free0 ? freev : fmin(fmax(ce * s_lp[0], lof), hi);
 #pragma unroll
-                    for (int k = 1; k < kOcLam; ++k) acc[k] += fmin(fmax(ce * s_lp[k], lof), hi);
+                        for (int k = 1; k < kOcLam; ++k) A[k * 256] += fmin(fmax(ce * s_lp[k], lof), hi);
+                    } else {
+                        acc[0] += free0 ? freev : fmin(fmax(ce * s_lp[0], lof), hi);
+#pragma unroll
+                        for (int k = 1; k < kOcLam; ++k) acc[k] += fmin(fmax(ce * s_lp[k], lof), hi);
+                    }
                 }
             } else {
                 while (m) {
@@ -1947,7 +1963,15 @@ __global__ void __launch_bounds__(256, 2) k_oc_coop(long long n, const double* _
                 }
             }
         }
-        double mine = acck + warp_reduce_scatter32(acc);
+        double mine;
+        if constexpr (SMACC) {
+            double t[kOcLam];
+#pragma unroll
+            for (int k = 0; k < kOcLam; ++k) t[k] = A[k * 256];
+            mine = acck + warp_reduce_scatter32(t);
+        } else {
+            mine = acck + warp_reduce_scatter32(acc);
+        }
         {
             // warp_sum leaves the total in lane 0
             const double Cs = __shfl_sync(0xffffffffu, warp_sum(sCn), 0);
@@ -2897,7 +2921,16 @@ int launch_oc_coop(cudaStream_t s, long long n, const double* rho, const double*
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_oc_coop, 256, 0);
+    // beyond L2 (rho and c_e > 64 MB) the search is bound by loads in flight: the
+    // shared-memory accumulators' third CTA per SM pays (512^3: 11.2 -> 8.3 ms per
+    // single-pass update); at 128^3 the register version is faster (21.5 vs 23.8 ms
+    // per 200 updates).  OTM_OC_SMACC=0/1 forces either.
+    static const int smacc_env = getenv("OTM_OC_SMACC") ? atoi(getenv("OTM_OC_SMACC")) : -1;
+    const bool smacc = smacc_env >= 0 ? smacc_env == 1 : n * 16 > (64LL << 20);
+    const size_t dyn = smacc ? (size_t)kOcLam * 256 * sizeof(double) : 0;
+    void* kern = smacc ? (void*)k_oc_coop<true> : (void*)k_oc_coop<false>;
+    if (smacc) smem_attr(k_oc_coop<true>, dyn);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, dyn);
     if (per_sm < 1) return 1;
     long long want = (n + 255) / 256;
     long long blocks = (long long)per_sm * sms;
@@ -2905,7 +2938,7 @@ int launch_oc_coop(cudaStream_t s, long long n, const double* rho, const double*
     if (blocks < 1) blocks = 1;
     void* args[] = {(void*)&n,       (void*)&rho, (void*)&sens,     (void*)&a,        (void*)&rho_out,
                     (void*)&ctl,     (void*)&partials, (void*)&qbuf, (void*)&lam_mem};
-    return cudaLaunchCooperativeKernel((void*)k_oc_coop, dim3((unsigned)blocks), dim3(256), args, 0, s) == cudaSuccess
+    return cudaLaunchCooperativeKernel(kern, dim3((unsigned)blocks), dim3(256), args, dyn, s) == cudaSuccess
                ? 0 : 1;
 }
 void launch_oc_apply(cudaStream_t s, long long n, const double* rho, const double* sens, const OcArgs& a,
