@@ -108,16 +108,17 @@ constexpr unsigned taps_no_corners() {
 }
 constexpr unsigned kTapsNoCorners = taps_no_corners();
 
-template <int MODE, unsigned MASK = 0>
+template <int MODE, unsigned MASK = 0, bool GS = false>
 __global__ void __launch_bounds__(256) k_filter_b(Geo g, long long p0, long long p1, FilterTaps taps,
                                                   const double* __restrict__ in, double* __restrict__ out,
                                                   double* __restrict__ kappa64, float* __restrict__ kappa32,
                                                   SimpParams sp, double* partials, unsigned* counter,
                                                   double* red_out) {
-    // z pairs [p0, p1): the whole grid, or a slab's interior planes (XRange)
-    const long long i = p0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    // z pairs [p0, p1): the whole grid, or a slab's interior planes (XRange); GS: a
+    // capped grid walks them (gs_cap)
     double acc3[3] = {0.0, 0.0, 0.0};
-    if (i < p1) {
+    for (long long i = p0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < p1;
+         i += GS ? (long long)gridDim.x * blockDim.x : p1) {
         const long long vp = i * 2;
         // 32-bit index arithmetic (fields < 2^31 vertices; see element_energies)
         const unsigned uv = (unsigned)vp, upl = (unsigned)g.pl;
@@ -160,9 +161,15 @@ __global__ void __launch_bounds__(256) k_filter_b(Geo g, long long p0, long long
             *reinterpret_cast<double2*>(kappa64 + vp) = make_double2(k0, k1);
             if (kappa32) *reinterpret_cast<float2*>(kappa32 + vp) = make_float2((float)k0, (float)k1);
             const double r0 = t[1][1][1], r1 = t[1][1][2];
-            acc3[0] = r0 + r1;
-            acc3[1] = simp_pow(r0, sp.p) + simp_pow(r1, sp.p);
-            acc3[2] = res[0] + res[1];
+            if (GS) {
+                acc3[0] += r0 + r1;
+                acc3[1] += simp_pow(r0, sp.p) + simp_pow(r1, sp.p);
+                acc3[2] += res[0] + res[1];
+            } else {
+                acc3[0] = r0 + r1;
+                acc3[1] = simp_pow(r0, sp.p) + simp_pow(r1, sp.p);
+                acc3[2] = res[0] + res[1];
+            }
         }
     }
     if (MODE == 2) reduce_finalize<3>(acc3, partials, counter, red_out);
@@ -975,6 +982,9 @@ __global__ void k_pupd(long long n, const float* __restrict__ z, float* __restri
 }
 
 // r -= alpha q ; r.r partial sums -> convergence flags (d is updated by the next k_pupd)
+// GS: grid-stride over a capped grid (large fields: the per-block fence + atomic of
+// the reduction epilogue, once per 256 float4, was a third of the kernel at 512^3)
+template <bool GS>
 __global__ void __launch_bounds__(256) k_upd(long long n, float* __restrict__ r, const float* __restrict__ q,
                                              double* partials, unsigned* counter, PcgScalars* sc,
                                              unsigned long long loop) {
@@ -983,16 +993,21 @@ __global__ void __launch_bounds__(256) k_upd(long long n, float* __restrict__ r,
     const float al[3] = {(float)sc->alpha[0], (float)sc->alpha[1], (float)sc->alpha[2]};
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long n4 = n >> 2;
-    if (i < n4) {
+    auto body = [&](long long j) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const float4 qv = __ldg(reinterpret_cast<const float4*>(q + c * n) + i);
-            float4* rp = reinterpret_cast<float4*>(r + c * n) + i;
+            const float4 qv = __ldg(reinterpret_cast<const float4*>(q + c * n) + j);
+            float4* rp = reinterpret_cast<float4*>(r + c * n) + j;
             float4 rv = *rp;
             rv.x -= al[c] * qv.x; rv.y -= al[c] * qv.y; rv.z -= al[c] * qv.z; rv.w -= al[c] * qv.w;
             *rp = rv;
             acc[c] += ((double)rv.x * rv.x + (double)rv.y * rv.y) + ((double)rv.z * rv.z + (double)rv.w * rv.w);
         }
+    };
+    if constexpr (GS) {
+        for (long long j = i; j < n4; j += (long long)gridDim.x * blockDim.x) body(j);
+    } else {
+        if (i < n4) body(i);
     }
     if (i < (n & 3)) {
         const long long t = (n4 << 2) + i;
@@ -2181,6 +2196,19 @@ static bool encode_map64(CUtensorMap* m, const double* base, int nz, int ny, lon
 
 static inline unsigned nblk(long long n, int bs) { return (unsigned)((n + bs - 1) / bs); }
 
+// Grid cap for the one-item-per-thread kernels that end in a cross-block reduction
+// (k_upd, the forward filter's sums) on fields above 4M vertices: 8 blocks per SM
+// walking the field, instead of one fence + atomic per 256 items.  0: no cap (the
+// 128^3 headline keeps its one-pass grids; OTM_GS_CAP=0 turns the cap off).
+static unsigned gs_cap(long long n) {
+    static const bool on = !(getenv("OTM_GS_CAP") && atoi(getenv("OTM_GS_CAP")) == 0);
+    if (!on || n <= (1LL << 22)) return 0;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return (unsigned)(8 * sms);
+}
+
 // Inner-loop kernels go through launch_pdl: programmatic stream serialisation lets
 // the next kernel's CTAs be scheduled while the previous grid drains (each such
 // kernel starts with pdl_wait()).  OTM_PDL=0 turns it off.
@@ -2237,7 +2265,18 @@ static void launch_filter_b(cudaStream_t s, const Geo& g, const FilterSetup& fs,
         if (fs.w27[i] != 0.0) mask |= 1u << i;
     }
     const long long p0 = xr ? (long long)xr->xa * g.pl / 2 : 0, p1 = xr ? (long long)xr->xb * g.pl / 2 : g.n >> 1;
-    const unsigned blocks = nblk(p1 - p0, 256);
+    unsigned blocks = nblk(p1 - p0, 256);
+    const unsigned cap = MODE == 2 ? gs_cap(2 * (p1 - p0)) : 0;
+    if (cap && blocks > cap) {                     // the forward filter's sums over a capped grid
+        blocks = cap;
+        if (mask == kTapsNoCorners)
+            k_filter_b<MODE, kTapsNoCorners, true><<<blocks, 256, 0, s>>>(g, p0, p1, taps, in, out, k64, k32, sp,
+                                                                          partials, counter, out3);
+        else
+            k_filter_b<MODE, 0, true><<<blocks, 256, 0, s>>>(g, p0, p1, taps, in, out, k64, k32, sp, partials,
+                                                             counter, out3);
+        return;
+    }
     if (mask == kTapsNoCorners)
         k_filter_b<MODE, kTapsNoCorners><<<blocks, 256, 0, s>>>(g, p0, p1, taps, in, out, k64, k32, sp, partials,
                                                                 counter, out3);
@@ -2832,7 +2871,11 @@ void launch_pupd(cudaStream_t s, long long n, const float* z, float* p, float* d
 void launch_upd(cudaStream_t s, long long n, float* r, const float* q, Red& red, PcgScalars* sc,
                 unsigned long long loop) {
     const long long th = std::max<long long>(n >> 2, n & 3);
-    launch_pdl(k_upd, nblk(th, 256), 256, 0, s, n, r, q, red.partials, red.counter, sc, loop);
+    const unsigned cap = gs_cap(n);
+    if (cap && nblk(th, 256) > cap)
+        launch_pdl(k_upd<true>, cap, 256, 0, s, n, r, q, red.partials, red.counter, sc, loop);
+    else
+        launch_pdl(k_upd<false>, nblk(th, 256), 256, 0, s, n, r, q, red.partials, red.counter, sc, loop);
 }
 void launch_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* res, float* fc) {
     if (cf[0] && cf[1] && cf[2]) {
