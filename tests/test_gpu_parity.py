@@ -376,3 +376,33 @@ def test_cooperative_oc_matches_host_search(otm, monkeypatch):
     optimize._HIER_CACHE.clear()
     assert np.array_equal(out[0].field.rho, out[1].field.rho)
     assert [r.vstar for r in out[0].log] == [r.vstar for r in out[1].log]
+
+
+def test_cooperative_oc_shared_memory_accumulators():
+    """The beyond-L2 variant of the cooperative OC search (candidate accumulators in
+    shared memory, 3 CTAs per SM; OTM_OC_SMACC=1 forces it at any size) picks the
+    same multipliers as the register variant: bit-identical designs after 30
+    iterations.  The switch is read once per process, hence the subprocesses."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_2405_19991_b200 as otm\n"
+        "t = otm.ObjectiveSpec('mse', otm.ConductivityTensor([0.1, 0.1, 0.1, 0, 0, 0]))\n"
+        "cfg = otm.RunConfig(dims=(32, 32, 32), target=t, init=otm.InitPattern('iwp', 0.3, seed=0),"
+        " max_iter=30, conv_threshold=0.0)\n"
+        "r = otm.run_optimization(cfg)\n"
+        "np.save(sys.argv[1], r.field.rho)\n" % root)
+    import tempfile
+    out = []
+    with tempfile.TemporaryDirectory() as d:
+        for v in ("0", "1"):
+            f = os.path.join(d, f"rho_{v}.npy")
+            env = dict(os.environ, OTM_OC_SMACC=v)
+            proc = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True,
+                                  timeout=600)
+            assert proc.returncode == 0, proc.stderr[-2000:]
+            out.append(np.load(f))
+    assert np.array_equal(out[0], out[1])
