@@ -1281,6 +1281,46 @@ __global__ void __launch_bounds__(256) k_restrict3w(Geo f, Geo c, const float* _
     fc[i] = s;
 }
 
+// Restriction for coarse rows with c.nz % 64 == 0: a thread makes two
+// consecutive coarse z (one float4 of fine z per row, the 4Z-1 neighbour from the lane
+// below), grid (Y, Z pair) x (case, X): no 64-bit index division, half the load
+// instructions per output.  Same weights and summation order as k_restrict3w.
+__global__ void __launch_bounds__(256) k_restrict3v(Geo f, Geo c, const float* __restrict__ res,
+                                                    float* __restrict__ fc) {
+    pdl_wait();
+    const int hz = c.nz >> 1;                       // coarse z pairs per row
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= c.ny * hz) return;                     // hz % 32 == 0: whole warps only
+    const int lane = threadIdx.x & 31;
+    const int cc = blockIdx.y / c.nx, X = blockIdx.y - cc * c.nx;
+    const int Y = t / hz, Zp = t - Y * hz;
+    const int xs[3] = {wrap_m(2 * X, f.nx), 2 * X, wrap_p(2 * X, f.nx)};
+    const int ys[3] = {wrap_m(2 * Y, f.ny) * f.nz, 2 * Y * f.nz, wrap_p(2 * Y, f.ny) * f.nz};
+    const int z4 = 4 * Zp;
+    const int zm = z4 == 0 ? f.nz - 1 : z4 - 1;
+    const float w[3] = {0.25f, 0.5f, 0.25f};
+    const float* r = res + (size_t)cc * f.n;
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        float sb0 = 0.f, sb1 = 0.f;
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            const float* row = r + (size_t)xs[a] * f.pl + ys[b];
+            const float4 m = __ldg(reinterpret_cast<const float4*>(row + z4));
+            float left = __shfl_up_sync(0xffffffffu, m.w, 1);
+            if (lane == 0) left = __ldg(row + zm);
+            const float sz0 = w[0] * left + w[1] * m.x + w[2] * m.y;
+            const float sz1 = w[0] * m.y + w[1] * m.z + w[2] * m.w;
+            sb0 += w[b] * sz0;
+            sb1 += w[b] * sz1;
+        }
+        s0 += w[a] * sb0;
+        s1 += w[a] * sb1;
+    }
+    *reinterpret_cast<float2*>(fc + (size_t)cc * c.n + (size_t)X * c.pl + Y * c.nz + 2 * Zp) = make_float2(s0, s1);
+}
+
 // trilinear prolongation + correction, every axis coarsened: 8 coarse loads, weights 0/0.5/1
 __global__ void __launch_bounds__(256) k_prolong3(Geo f, Geo c, const float* __restrict__ zc,
                                                   float* __restrict__ zf) {
@@ -2879,7 +2919,12 @@ void launch_upd(cudaStream_t s, long long n, float* r, const float* q, Red& red,
 }
 void launch_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* res, float* fc) {
     if (cf[0] && cf[1] && cf[2]) {
-        if (c.nz % 32 == 0)
+        // two coarse z per thread where the coarse rows allow it (OTM_RESTRICT_V=0: off)
+        static const bool rv = !(getenv("OTM_RESTRICT_V") && atoi(getenv("OTM_RESTRICT_V")) == 0);
+        if (rv && c.nz % 64 == 0 && 3LL * c.nx <= 65535)
+            launch_pdl(k_restrict3v, dim3(nblk((long long)c.ny * (c.nz / 2), 256), 3 * c.nx), 256, 0, s, f, c, res,
+                       fc);
+        else if (c.nz % 32 == 0)
             launch_pdl(k_restrict3w, nblk(3 * c.n, 256), 256, 0, s, f, c, res, fc);
         else
             launch_pdl(k_restrict3, nblk(3 * c.n, 256), 256, 0, s, f, c, res, fc);
