@@ -1067,12 +1067,35 @@ __global__ void __launch_bounds__(256) k_upd(long long n, float* __restrict__ r,
 template <bool CG>
 __device__ __forceinline__ float ldf(const float* p) { return CG ? __ldcg(p) : __ldg(p); }
 
+// (case, vertex) of a flat 3-case item index: 32-bit division when 3 n fits
+__device__ __forceinline__ void split_case(long long i, long long n, int& c, int& v) {
+    if (3 * n < (1LL << 31)) {
+        const unsigned ui = (unsigned)i, un = (unsigned)n;
+        c = (int)(ui / un);
+        v = (int)(ui - (unsigned)c * un);
+    } else {
+        c = (int)(i / n);
+        v = (int)(i - (long long)c * n);
+    }
+}
+
+template <bool CG, bool ASSIGN = false>
+__device__ __forceinline__ void prolong3b_at(const Geo& f, const Geo& c, const float* __restrict__ zc,
+                                             float* __restrict__ zf, int cc, int X, int Y, int Z);
+
 template <bool CG, bool ASSIGN = false>
 __device__ __forceinline__ void prolong3b_body(const Geo& f, const Geo& c, const float* __restrict__ zc,
                                                float* __restrict__ zf, long long i) {
-    const int cc = (int)(i / c.n);
-    const int v = (int)(i - (long long)cc * c.n);
+    int cc, v;
+    split_case(i, c.n, cc, v);
     const int X = v / c.pl, rem = v - X * c.pl, Y = rem / c.nz, Z = rem - Y * c.nz;
+    prolong3b_at<CG, ASSIGN>(f, c, zc, zf, cc, X, Y, Z);
+}
+
+// the 2x2x2 fine block of coarse vertex (X, Y, Z) of case cc
+template <bool CG, bool ASSIGN>
+__device__ __forceinline__ void prolong3b_at(const Geo& f, const Geo& c, const float* __restrict__ zc,
+                                             float* __restrict__ zf, int cc, int X, int Y, int Z) {
     const int X1 = X + 1 == c.nx ? 0 : X + 1, Y1 = Y + 1 == c.ny ? 0 : Y + 1, Z1 = Z + 1 == c.nz ? 0 : Z + 1;
     const float* a = zc + (size_t)cc * c.n;
     float q[2][2][2];
@@ -1127,6 +1150,18 @@ __global__ void __launch_bounds__(256) k_prolong3b(Geo f, Geo c, const float* __
     prolong3b_body<false, ASSIGN>(f, c, zc, zf, i);
 }
 
+// the same on a (Y, Z) x (case, X) grid: 32-bit index arithmetic, no division by n
+template <bool ASSIGN>
+__global__ void __launch_bounds__(256) k_prolong3c(Geo f, Geo c, const float* __restrict__ zc,
+                                                   float* __restrict__ zf) {
+    pdl_wait();
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= c.pl) return;
+    const int cc = blockIdx.y / c.nx, X = blockIdx.y - cc * c.nx;
+    const int Y = t / c.nz, Z = t - Y * c.nz;
+    prolong3b_at<false, ASSIGN>(f, c, zc, zf, cc, X, Y, Z);
+}
+
 // ---- small levels: one thread per (case, vertex), every load issued up front ----
 // one (case, vertex) item of the small-level smoother (OP 0: smooth_res, OP 1: jacobi)
 template <int OP, bool DOT, bool CG>
@@ -1134,8 +1169,8 @@ __device__ __forceinline__ void small_item(const Geo& g, const LevelTemplate& lt
                                            const float* __restrict__ a, const float* __restrict__ f,
                                            const float* __restrict__ dinv, float omega, float* __restrict__ o1,
                                            float* __restrict__ o2, long long i, double (&dot3)[3]) {
-    const int c = (int)(i / g.n);
-    const int v = (int)(i - (long long)c * g.n);
+    int c, v;
+    split_case(i, g.n, c, v);
     const int x = v / g.pl, rem = v - x * g.pl, y = rem / g.nz, z = rem - y * g.nz;
     const int xs[3] = {wrap_m(x, g.nx), x, wrap_p(x, g.nx)};
     const int ys[3] = {wrap_m(y, g.ny) * g.nz, y * g.nz, wrap_p(y, g.ny) * g.nz};
@@ -1208,8 +1243,8 @@ __global__ void __launch_bounds__(256) k_small(Geo g, LevelTemplate lt, const fl
 template <bool CG>
 __device__ __forceinline__ void restrict3_body(const Geo& f, const Geo& c, const float* __restrict__ res,
                                                float* __restrict__ fc, long long i) {
-    const int cc = (int)(i / c.n);
-    const int v = (int)(i - (long long)cc * c.n);
+    int cc, v;
+    split_case(i, c.n, cc, v);
     const int X = v / c.pl, rem = v - X * c.pl, Y = rem / c.nz, Z = rem - Y * c.nz;
     const int xs[3] = {wrap_m(2 * X, f.nx), 2 * X, wrap_p(2 * X, f.nx)};
     const int ys[3] = {wrap_m(2 * Y, f.ny) * f.nz, 2 * Y * f.nz, wrap_p(2 * Y, f.ny) * f.nz};
@@ -1255,8 +1290,8 @@ __global__ void __launch_bounds__(256) k_restrict3w(Geo f, Geo c, const float* _
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= 3 * c.n) return;                      // c.n % 32 == 0: whole warps only
     const int lane = threadIdx.x & 31;
-    const int cc = (int)(i / c.n);
-    const int v = (int)(i - (long long)cc * c.n);
+    int cc, v;
+    split_case(i, c.n, cc, v);
     const int X = v / c.pl, rem = v - X * c.pl, Y = rem / c.nz, Z = rem - Y * c.nz;
     const int xs[3] = {wrap_m(2 * X, f.nx), 2 * X, wrap_p(2 * X, f.nx)};
     const int ys[3] = {wrap_m(2 * Y, f.ny) * f.nz, 2 * Y * f.nz, wrap_p(2 * Y, f.ny) * f.nz};
@@ -2934,7 +2969,11 @@ void launch_restrict(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3]
 }
 void launch_prolong(cudaStream_t s, const Geo& f, const Geo& c, const int cf[3], const float* zc, float* zf) {
     if (cf[0] && cf[1] && cf[2]) {
-        launch_pdl(k_prolong3b<false>, nblk(3 * c.n, 256), 256, 0, s, f, c, zc, zf);
+        static const bool pc = !(getenv("OTM_PROLONG_C") && atoi(getenv("OTM_PROLONG_C")) == 0);
+        if (pc && 3LL * c.nx <= 65535)
+            launch_pdl(k_prolong3c<false>, dim3(nblk(c.pl, 256), 3 * c.nx), 256, 0, s, f, c, zc, zf);
+        else
+            launch_pdl(k_prolong3b<false>, nblk(3 * c.n, 256), 256, 0, s, f, c, zc, zf);
         return;
     }
     k_prolong<<<nblk(f.n, 256), 256, 0, s>>>(f, c, cf[0], cf[1], cf[2], zc, zf);
