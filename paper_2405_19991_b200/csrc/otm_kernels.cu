@@ -1356,29 +1356,6 @@ __global__ void __launch_bounds__(256) k_restrict3v(Geo f, Geo c, const float* _
     *reinterpret_cast<float2*>(fc + (size_t)cc * c.n + (size_t)X * c.pl + Y * c.nz + 2 * Zp) = make_float2(s0, s1);
 }
 
-// trilinear prolongation + correction, every axis coarsened: 8 coarse loads, weights 0/0.5/1
-__global__ void __launch_bounds__(256) k_prolong3(Geo f, Geo c, const float* __restrict__ zc,
-                                                  float* __restrict__ zf) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= 3 * f.n) return;
-    const int cc = (int)(i / f.n);
-    const int v = (int)(i - (long long)cc * f.n);
-    const int x = v / f.pl, rem = v - x * f.pl, y = rem / f.nz, z = rem - y * f.nz;
-    const int X0 = x >> 1, Y0 = y >> 1, Z0 = z >> 1;
-    const int X1 = X0 + 1 == c.nx ? 0 : X0 + 1, Y1 = Y0 + 1 == c.ny ? 0 : Y0 + 1, Z1 = Z0 + 1 == c.nz ? 0 : Z0 + 1;
-    const float wx1 = (x & 1) ? 0.5f : 0.f, wy1 = (y & 1) ? 0.5f : 0.f, wz1 = (z & 1) ? 0.5f : 0.f;
-    const float wx0 = 1.f - wx1, wy0 = 1.f - wy1, wz0 = 1.f - wz1;
-    const float* a = zc + (size_t)cc * c.n;
-    const long long r00 = (long long)X0 * c.pl + Y0 * c.nz, r01 = (long long)X0 * c.pl + Y1 * c.nz;
-    const long long r10 = (long long)X1 * c.pl + Y0 * c.nz, r11 = (long long)X1 * c.pl + Y1 * c.nz;
-    const float v000 = __ldg(a + r00 + Z0), v001 = __ldg(a + r00 + Z1), v010 = __ldg(a + r01 + Z0),
-                v011 = __ldg(a + r01 + Z1), v100 = __ldg(a + r10 + Z0), v101 = __ldg(a + r10 + Z1),
-                v110 = __ldg(a + r11 + Z0), v111 = __ldg(a + r11 + Z1);
-    const float s = wx0 * (wy0 * (wz0 * v000 + wz1 * v001) + wy1 * (wz0 * v010 + wz1 * v011)) +
-                    wx1 * (wy0 * (wz0 * v100 + wz1 * v101) + wy1 * (wz0 * v110 + wz1 * v111));
-    zf[i] += s;
-}
-
 // full-weighting restriction (solver.py:167-177): coarse J <- sum_d w(d) res[2J+d]
 __global__ void k_restrict(Geo f, Geo c, int cx, int cy, int cz, const float* __restrict__ res,
                            float* __restrict__ fc) {
